@@ -1,0 +1,153 @@
+/*
+ * starplat_b200.h -- C ABI of the B200 (sm_100a) graph-kernel backend.
+ *
+ * This is the drop-in boundary behind the reference's Python entry points.
+ * The reference (trident, pure Python) has no FFI of its own; each entry
+ * point below replaces one Python function of the hot path, cited as
+ * trident/<file>:<line> (relative to /root/reference/pkg/src).  The Python
+ * host layer (paper_2305_03317_b200/) binds these with ctypes and keeps the
+ * reference's signatures, argument checks and exception types.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Vertex ids int32, edge ids / offsets
+ *     int64, weights int32, properties int32 / double.
+ *   - `mem` says where a caller buffer lives: SP_MEM_HOST (pageable or
+ *     pinned host memory; copied inside the call) or SP_MEM_DEVICE (a device
+ *     pointer on the graph's device, e.g. a torch tensor's data_ptr()).
+ *   - Return SP_OK (0) or a negative SP_ERR_*; sp_last_error() gives a
+ *     thread-local message.  No call falls back to the CPU.
+ *   - A graph handle is immutable after creation and safe for concurrent
+ *     readers; every algorithm call uses its own stream and
+ *     scratch (stream-ordered allocations).
+ */
+#ifndef STARPLAT_B200_H
+#define STARPLAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+
+enum sp_status {
+    SP_OK = 0,
+    SP_ERR_ARG = -1,          /* bad argument -> ExecError (interp.py:98-128) */
+    SP_ERR_NONCONV = -2,      /* fixedPoint cap -> NonConvergenceError (errors.py:85-92) */
+    SP_ERR_CUDA = -3,         /* CUDA runtime failure -> RuntimeError */
+    SP_ERR_OOM = -4,          /* device allocation failed */
+    SP_ERR_OVERFLOW = -5,     /* an int32 distance would leave int32 range */
+    SP_ERR_UNSUPPORTED = -6,  /* input outside the backend's domain (e.g. n >= 2^31) */
+    SP_ERR_ABORTED = -7       /* iteration callback asked to stop */
+};
+
+enum sp_mem { SP_MEM_HOST = 0, SP_MEM_DEVICE = 1 };
+
+/* Algorithm flags. */
+#define SP_FLAG_DETERMINISTIC 1u /* bit-exact left folds everywhere (PR, BC) */
+
+/* Arrays a graph handle can hand back (sp_graph_download). */
+enum sp_array {
+    SP_ARR_OFFSETS = 0,     /* int64[n+1]  CsrGraph.offsets     graph.py:30 */
+    SP_ARR_ADJ = 1,         /* int32[m]    CsrGraph.adj         graph.py:31 */
+    SP_ARR_WEIGHTS = 2,     /* int32[m]    CsrGraph.weights     graph.py:32 */
+    SP_ARR_REV_OFFSETS = 3, /* int64[n+1]  CsrGraph.rev_offsets graph.py:33 */
+    SP_ARR_REV_ADJ = 4,     /* int32[m]    CsrGraph.rev_adj     graph.py:34 */
+    SP_ARR_REV_EID = 5,     /* int64[m]    CsrGraph.rev_eid     graph.py:35 */
+    SP_ARR_WEFF = 6         /* int32[m]    weight of the first slot u->v (get_edge) */
+};
+
+enum sp_gen_kind { SP_GEN_RMAT = 0, SP_GEN_UNIFORM = 1, SP_GEN_GRID = 2 };
+
+typedef struct sp_graph sp_graph;
+
+/* Optional per-call counters (NULL to skip). */
+typedef struct sp_stats {
+    int64_t iterations;        /* fixedPoint iterations / BFS levels summed   */
+    int64_t edges_visited;     /* SSSP: relaxations R; PR: iters*m; BC: sum m_s; TC: pairs */
+    int64_t vertices_visited;  /* SSSP: frontier sum F; PR: iters*n; BC: sum n_s */
+    int64_t kernel_launches;   /* kernels this call launched                  */
+    double device_ms;          /* device time of the call (CUDA events)       */
+    double main_kernel_ms;     /* summed device time of the dominant kernel   */
+    int64_t main_kernel_launches;
+} sp_stats;
+
+/* fixedPoint iteration callback, mirrors interp.py:138,411-412
+ * (on_fixedpoint_iteration(flag, iters, executor)); return nonzero to abort. */
+typedef int (*sp_iter_cb)(int64_t iters, void *user);
+
+/* ---- runtime ---------------------------------------------------------- */
+int sp_abi_version(void);
+const char *sp_last_error(void);
+int sp_device_count(void);
+
+/* ---- graph core: replaces trident/graph.py ----------------------------- */
+
+/* from_edges (graph.py:101-116): one slot per edge plus the mirror for
+ * undirected non-loop edges, n = max(n, 1 + max id), forward CSR stably
+ * sorted by (src, dst) (graph.py:70-81), reverse CSR by (dst, src, eid)
+ * (graph.py:84-96).  Built on the device; uploaded once, never copied back. */
+int sp_graph_from_edges(const int32_t *u, const int32_t *v, const int32_t *w,
+                        int64_t nedges, int64_t n, int directed, int mem,
+                        int device, sp_graph **out);
+
+/* CsrGraph(...) (graph.py:18-36) from an existing forward CSR whose rows are
+ * already in reference order; the reverse CSR is rebuilt on the device. */
+int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj,
+                      const int32_t *weights, int64_t n, int64_t m,
+                      int directed, int mem, int device, sp_graph **out);
+
+/* Seeded synthetic graphs generated on the device, bit-identical to
+ * paper_2305_03317_b200/gen.py (pattern: pkg/tools/gen_fixtures.py:37-78).
+ *   SP_GEN_RMAT:    p0 = scale, p1 = edge factor
+ *   SP_GEN_UNIFORM: p0 = n,     p1 = candidate edges
+ *   SP_GEN_GRID:    p0 = rows,  p1 = cols (always undirected)            */
+int sp_graph_generate(int kind, int64_t p0, int64_t p1, int64_t seed,
+                      int undirected, int device, sp_graph **out);
+
+int sp_graph_info(const sp_graph *g, int64_t *n, int64_t *m, int *directed);
+int sp_graph_download(const sp_graph *g, int which, void *host_dst);
+/* min_wt / max_wt (graph.py:252-261); SP_ERR_ARG when m == 0. */
+int sp_graph_weight_range(const sp_graph *g, int32_t *wmin, int32_t *wmax);
+void sp_graph_destroy(sp_graph *g);
+
+/* ---- executor: replaces trident/interp.py:579-589 on the corpus -------- */
+
+/* corpus/programs/sssp.sp (and sssp_pull.sp: same dist).  dist[n] int32
+ * (INT_MAX = unreachable, syntax.py:114).  cap = fixedPoint cap
+ * (interp.py:36-37,143,415-416).  iters = fixedPoint iterations. */
+int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist, int mem,
+            int64_t *iters, sp_iter_cb cb, void *user, sp_stats *st);
+
+/* corpus/programs/pr.sp.  rank[n] = final ranks (== rank_nxt at exit);
+ * iter / diff = the program's scalars; iters = fixedPoint iterations. */
+int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t max_iter,
+                int64_t cap, unsigned flags, double *rank, int mem,
+                int64_t *iter, double *diff, int64_t *iters, sp_iter_cb cb,
+                void *user, sp_stats *st);
+
+/* Vertex-range PageRank step for block-partitioned multi-GPU runs
+ * (graph.py:226-249 ownership): computes rank for v in [v0, v1) from a full
+ * contrib[n] array and writes contrib_out[v-v0] = rank/outdeg; returns the
+ * local max |delta| in *diff.  All pointers are device pointers. */
+int sp_pagerank_block_step(sp_graph *g, int64_t v0, int64_t v1,
+                           double damping, const double *contrib_in,
+                           double *rank_local, double *contrib_out,
+                           double *diff, unsigned flags, sp_stats *st);
+int sp_pagerank_block_init(sp_graph *g, int64_t v0, int64_t v1,
+                           double *rank_local, double *contrib_out);
+
+/* corpus/programs/bc.sp over srcs in list order (duplicates re-run).
+ * bc[n] accumulated; sigma/delta[n] of the LAST source (may be NULL). */
+int sp_bc(sp_graph *g, const int32_t *srcs, int64_t nsrc, unsigned flags,
+          double *bc, double *sigma, double *delta, int mem, sp_stats *st);
+
+/* corpus/programs/tc.sp restricted to middle vertices v in [v0, v1)
+ * (v0 = 0, v1 = n for the whole program); exact, with multiplicity. */
+int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_stats *st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STARPLAT_B200_H */

@@ -1,0 +1,150 @@
+// sp_common.cuh -- shared runtime plumbing for the sm_100a graph backend.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/starplat_b200.h"
+
+namespace sp {
+
+constexpr int kIntMax = 2147483647;
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs (queried at runtime too)
+
+void set_error(const char *fmt, ...);
+int cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+
+#define SP_CUDA(call)                                                        \
+    do {                                                                     \
+        cudaError_t _e = (call);                                             \
+        if (_e != cudaSuccess)                                               \
+            return ::sp::cuda_fail(_e, #call, __FILE__, __LINE__);           \
+    } while (0)
+
+#define SP_CHECK(cond, code, ...)                                            \
+    do {                                                                     \
+        if (!(cond)) {                                                       \
+            ::sp::set_error(__VA_ARGS__);                                    \
+            return (code);                                                   \
+        }                                                                    \
+    } while (0)
+
+#define SP_TRY(call)                                                         \
+    do {                                                                     \
+        int _rc = (call);                                                    \
+        if (_rc != SP_OK)                                                    \
+            return _rc;                                                      \
+    } while (0)
+
+int num_sms(int device);
+
+// Stream-ordered scratch allocation (cudaMallocAsync from the device's
+// default pool, release threshold raised so repeated calls reuse memory).
+int scratch_alloc(void **p, size_t bytes, cudaStream_t s);
+void scratch_free(void *p, cudaStream_t s);
+
+// RAII holder for a per-call stream + scratch list + timing events.
+struct Call {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    void *bufs[32];
+    int nbufs = 0;
+    int64_t launches = 0;
+    int begin(int dev);
+    template <class T>
+    int alloc(T **p, size_t count) {
+        void *q = nullptr;
+        int rc = scratch_alloc(&q, count * sizeof(T) + 16, stream);
+        if (rc != SP_OK) return rc;
+        bufs[nbufs++] = q;
+        *p = static_cast<T *>(q);
+        return SP_OK;
+    }
+    int finish(sp_stats *st);  // sync + elapsed into st->device_ms
+    ~Call();
+};
+
+// Copy a caller buffer to/from the device according to `mem`.
+int to_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s);
+int from_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s);
+
+}  // namespace sp
+
+// ---- the graph handle ----------------------------------------------------
+struct sp_graph {
+    int device = 0;
+    int64_t n = 0, m = 0;
+    int directed = 1;
+    // forward CSR (graph.py:30-32)
+    int64_t *off = nullptr;
+    int32_t *adj = nullptr;
+    int32_t *w = nullptr;
+    int32_t *weff = nullptr;  // get_edge first-slot weight
+    int32_t *outdeg = nullptr;
+    // reverse CSR (graph.py:33-35); aliases of off/adj when undirected
+    int64_t *roff = nullptr;
+    int32_t *radj = nullptr;
+    int64_t *reid = nullptr;
+    int32_t *indeg = nullptr;
+    int64_t max_outdeg = 0, max_indeg = 0;
+    // vertices whose in-/out-degree exceeds the hub threshold (PR/BC hub path)
+    int32_t *hubs_in = nullptr;
+    int64_t nhubs_in = 0;
+    int32_t *wrange = nullptr;  // [min, max] weight (device), m > 0
+};
+
+// ---- device helpers --------------------------------------------------------
+namespace sp {
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Max of non-negative doubles via their IEEE bit patterns (order-preserving).
+__device__ __forceinline__ void atomic_max_nonneg(double *addr, double v) {
+    atomicMax(reinterpret_cast<unsigned long long *>(addr),
+              static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// Warp-aggregated append: lanes with `want` get consecutive slots.
+__device__ __forceinline__ int64_t warp_append(bool want, unsigned long long *counter) {
+    unsigned mask = __ballot_sync(0xffffffffu, want);
+    if (!mask) return -1;
+    int leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if ((int)lane_id() == leader) base = atomicAdd(counter, (unsigned long long)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!want) return -1;
+    return (int64_t)base + __popc(mask & ((1u << lane_id()) - 1u));
+}
+
+__device__ __forceinline__ int ld_stream_i32(const int32_t *p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+inline int grid_for(int64_t work, int block, int device, int per_sm = 8) {
+    int64_t g = (work + block - 1) / block;
+    int64_t cap = (int64_t)num_sms(device) * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+}  // namespace sp

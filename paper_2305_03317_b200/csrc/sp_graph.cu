@@ -1,0 +1,701 @@
+// sp_graph.cu -- device CSR builder, device generators, graph handle.
+//
+// Replaces trident/graph.py:68-116 (_build_csr / from_edges) and the
+// CsrGraph storage (graph.py:18-65).  The build runs entirely on the GPU:
+//   slots (graph.py:107-113: edge, then its mirror if undirected and u != v)
+//   -> 2b-bit keys (src << b | dst), values = slot index
+//   -> stable LSD radix sort (CUB)  == Python's stable sort by (src, dst)
+//   -> offsets from run boundaries, weights gathered through the permutation
+//   -> w_eff (weight of the first slot of each equal-dst run; get_edge's
+//      bisect_left, graph.py:56-62)
+//   -> reverse CSR: stable sort of forward slots by (dst << b | src), which
+//      yields graph.py:92's (dst, src, eid) order.
+// Arrays stay resident; nothing is copied back unless the host asks for a
+// view (sp_graph_download).
+#include <cub/cub.cuh>
+
+#include <mutex>
+#include <new>
+
+#include "sp_common.cuh"
+
+using namespace sp;
+
+namespace {
+
+std::mutex g_lazy_mu;  // guards lazy reverse-eid construction
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+int bits_for(int64_t n) {
+    int b = 1;
+    while (b < 62 && ((int64_t)1 << b) < n) b++;
+    return b;
+}
+
+__global__ void k_id_range(const int32_t *__restrict__ u, const int32_t *__restrict__ v,
+                           int64_t ne, int *mn, int *mx) {
+    int lo = 0x7fffffff, hi = -1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int a = u[i], b = v[i];
+        lo = min(lo, min(a, b));
+        hi = max(hi, max(a, b));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mn, lo);
+        atomicMax(mx, hi);
+    }
+}
+
+__global__ void k_nonloop(const int32_t *__restrict__ u, const int32_t *__restrict__ v,
+                          int64_t ne, int64_t *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne;
+         i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (u[i] != v[i]);
+}
+
+// Fill slot keys (src << b | dst) in graph.py:107-113 append order.
+template <class IdxT>
+__global__ void k_fill_slots(const int32_t *__restrict__ u, const int32_t *__restrict__ v,
+                             const int32_t *__restrict__ w, int64_t ne,
+                             const int64_t *__restrict__ excl, int directed, int b,
+                             uint64_t *key, IdxT *val, int32_t *sw) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = directed ? i : i + excl[i];
+        uint64_t a = (uint32_t)u[i], c = (uint32_t)v[i];
+        key[p] = (a << b) | c;
+        val[p] = (IdxT)p;
+        sw[p] = w[i];
+        if (!directed && a != c) {
+            key[p + 1] = (c << b) | a;
+            val[p + 1] = (IdxT)(p + 1);
+            sw[p + 1] = w[i];
+        }
+    }
+}
+
+template <class IdxT>
+__global__ void k_iota(IdxT *val, int64_t m) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        val[i] = (IdxT)i;
+}
+
+// Offsets from the sorted key's high part: off[x] = first e with src(e) >= x.
+__global__ void k_offsets(const uint64_t *__restrict__ key, int64_t m, int64_t n, int b,
+                          int64_t *off) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t prev = e == 0 ? -1 : (int64_t)(key[e - 1] >> b);
+        int64_t cur = e == m ? n : (int64_t)(key[e] >> b);
+        for (int64_t x = prev + 1; x <= cur; x++) off[x] = e;
+    }
+}
+
+template <class IdxT>
+__global__ void k_forward(const uint64_t *__restrict__ key, const IdxT *__restrict__ perm,
+                          const int32_t *__restrict__ sw, int64_t m, int b,
+                          int32_t *adj, int32_t *w, int64_t *runstart) {
+    uint64_t mask = (1ull << b) - 1;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = key[e];
+        adj[e] = (int32_t)(k & mask);
+        w[e] = sw[perm[e]];
+        runstart[e] = (e == 0 || key[e - 1] != k) ? e : 0;
+    }
+}
+
+struct MaxOp {
+    __device__ __forceinline__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; }
+};
+
+__global__ void k_runstart(const uint64_t *__restrict__ key, int64_t m, int64_t *runstart) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x)
+        runstart[e] = (e == 0 || key[e - 1] != key[e]) ? e : 0;
+}
+
+__global__ void k_weff(const int32_t *__restrict__ w, const int64_t *__restrict__ runstart,
+                       int64_t m, int32_t *weff) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x)
+        weff[e] = w[runstart[e]];
+}
+
+__global__ void k_deg(const int64_t *__restrict__ off, int64_t n, int32_t *deg,
+                      unsigned long long *maxdeg) {
+    unsigned long long mx = 0;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int64_t d = off[x + 1] - off[x];
+        deg[x] = (int32_t)(d > 0x7fffffff ? 0x7fffffff : d);
+        mx = max(mx, (unsigned long long)d);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxdeg, mx);
+}
+
+__global__ void k_hubs(const int32_t *__restrict__ deg, int64_t n, int thr, int32_t *list,
+                       unsigned long long *cnt) {
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        int64_t x = base + threadIdx.x;
+        bool hub = x < n && deg[x] > thr;
+        int64_t slot = warp_append(hub, cnt);
+        if (hub) list[slot] = (int32_t)x;
+    }
+}
+
+__global__ void k_wrange(const int32_t *__restrict__ w, int64_t m, int32_t *r) {
+    int lo = 0x7fffffff, hi = (int)0x80000000;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        lo = min(lo, w[e]);
+        hi = max(hi, w[e]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&r[0], lo);
+        atomicMax(&r[1], hi);
+    }
+}
+
+// Reverse keys from forward CSR: key2[e] = dst << b | src, in forward order.
+__global__ void k_rev_keys(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+                           int64_t n, int b, uint64_t *key2) {
+    // one warp per source row
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t x = warp; x < n; x += nw)
+        for (int64_t e = off[x] + lane_id(); e < off[x + 1]; e += 32)
+            key2[e] = ((uint64_t)(uint32_t)adj[e] << b) | (uint64_t)x;
+}
+
+template <class IdxT>
+__global__ void k_rev_out(const uint64_t *__restrict__ key2, const IdxT *__restrict__ perm,
+                          int64_t m, int b, int32_t *radj, int64_t *reid) {
+    uint64_t mask = (1ull << b) - 1;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (radj) radj[k] = (int32_t)(key2[k] & mask);
+        if (reid) reid[k] = (int64_t)perm[k];
+    }
+}
+
+// ---- device generators (bit-identical to paper_2305_03317_b200/gen.py) ----
+__global__ void k_gen_rmat(int64_t ne, int scale, uint64_t sk, int ta, int tb, int tc,
+                           int undirected, uint64_t *key) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t u = 0, v = 0;
+        int ngroups = (scale + 3) / 4;
+        for (int g = 0; g < ngroups; g++) {
+            uint64_t h = splitmix64(sk ^ (((uint64_t)i << 4) | (uint64_t)g));
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                int lvl = g * 4 + j;
+                if (lvl >= scale) break;
+                uint32_t r = (uint32_t)((h >> (16 * j)) & 0xFFFFu);
+                uint64_t bu = r >= (uint32_t)tb;
+                uint64_t bv = (r >= (uint32_t)ta && r < (uint32_t)tb) || r >= (uint32_t)tc;
+                u |= bu << (scale - 1 - lvl);
+                v |= bv << (scale - 1 - lvl);
+            }
+        }
+        if (undirected && u > v) { uint64_t t = u; u = v; v = t; }
+        key[i] = (u == v) ? ~0ull : ((u << 32) | v);
+    }
+}
+
+__global__ void k_gen_uniform(int64_t ne, uint64_t n, uint64_t sk, int undirected, uint64_t *key) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t h = splitmix64(sk ^ (uint64_t)i);
+        uint64_t u = ((h >> 32) * n) >> 32;
+        uint64_t v = ((h & 0xFFFFFFFFull) * n) >> 32;
+        if (undirected && u > v) { uint64_t t = u; u = v; v = t; }
+        key[i] = (u == v) ? ~0ull : ((u << 32) | v);
+    }
+}
+
+__global__ void k_keys_to_edges(const uint64_t *__restrict__ key, int64_t ne, uint64_t wsk,
+                                int32_t *u, int32_t *v, int32_t *w) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = key[i];
+        u[i] = (int32_t)(k >> 32);
+        v[i] = (int32_t)(k & 0xFFFFFFFFull);
+        w[i] = (int32_t)(1 + splitmix64(k ^ wsk) % 100ull);
+    }
+}
+
+__global__ void k_gen_grid(int64_t rows, int64_t cols, uint64_t wsk, int32_t *u, int32_t *v,
+                           int32_t *w) {
+    // cell c = r*cols + col emits right (if col+1<cols) then down (if r+1<rows);
+    // slot index = 2*c - (#missing edges before c) computed in closed form.
+    int64_t ncell = rows * cols;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = c / cols, q = c % cols;
+        // edges before cell c: full rows r*(2*cols-1) plus q*2 in this row
+        // (each earlier cell in row r has right edge; down exists if r+1<rows)
+        int64_t before = r * ((cols - 1) + cols) + q * (1 + (r + 1 < rows ? 1 : 0));
+        int64_t p = before;
+        if (q + 1 < cols) {
+            uint64_t k = ((uint64_t)c << 32) | (uint64_t)(c + 1);
+            u[p] = (int32_t)c; v[p] = (int32_t)(c + 1);
+            w[p] = (int32_t)(1 + splitmix64(k ^ wsk) % 100ull);
+            p++;
+        }
+        if (r + 1 < rows) {
+            uint64_t k = ((uint64_t)c << 32) | (uint64_t)(c + cols);
+            u[p] = (int32_t)c; v[p] = (int32_t)(c + cols);
+            w[p] = (int32_t)(1 + splitmix64(k ^ wsk) % 100ull);
+        }
+    }
+}
+
+template <class F>
+int cub_call(Call &c, F f) {
+    size_t tmp = 0;
+    SP_CUDA(f(nullptr, tmp));
+    void *d = nullptr;
+    SP_TRY(scratch_alloc(&d, tmp, c.stream));
+    cudaError_t e = f(d, tmp);
+    scratch_free(d, c.stream);
+    SP_CUDA(e);
+    return SP_OK;
+}
+
+int gridN(int64_t work, int dev) { return grid_for(work, 256, dev, 16); }
+
+void free_graph(sp_graph *g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    cudaFree(g->off);
+    cudaFree(g->adj);
+    cudaFree(g->w);
+    cudaFree(g->weff);
+    cudaFree(g->outdeg);
+    if (g->directed) {
+        cudaFree(g->roff);
+        cudaFree(g->radj);
+        cudaFree(g->indeg);
+    }
+    cudaFree(g->reid);
+    cudaFree(g->hubs_in);
+    cudaFree(g->wrange);
+    delete g;
+}
+
+template <class T>
+int dalloc(T **p, size_t count) {
+    cudaError_t e = cudaMalloc((void **)p, count * sizeof(T) + 16);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("cudaMalloc of %zu bytes failed: %s", count * sizeof(T), cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? SP_ERR_OOM : SP_ERR_CUDA;
+    }
+    return SP_OK;
+}
+
+constexpr int kHubIn = 4096;  // PR hub threshold (in-degree), see sp_pagerank.cu
+
+// Reverse CSR from the forward arrays (graph.py:84-96).
+template <class IdxT>
+int build_reverse_t(sp_graph *g, Call &c, bool want_adj, bool want_eid) {
+    int64_t n = g->n, m = g->m;
+    int b = bits_for(n);
+    uint64_t *k2, *k2s;
+    IdxT *vi, *vo;
+    SP_TRY(c.alloc(&k2, m));
+    SP_TRY(c.alloc(&k2s, m));
+    SP_TRY(c.alloc(&vi, m));
+    SP_TRY(c.alloc(&vo, m));
+    k_rev_keys<<<gridN(n * 32, c.device), 256, 0, c.stream>>>(g->off, g->adj, n, b, k2);
+    k_iota<IdxT><<<gridN(m, c.device), 256, 0, c.stream>>>(vi, m);
+    if (m)
+        SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+            return cub::DeviceRadixSort::SortPairs(t, sz, k2, k2s, vi, vo, m, 0, 2 * b, c.stream);
+        }));
+    if (want_adj) {
+        SP_TRY(dalloc(&g->roff, n + 1));
+        SP_TRY(dalloc(&g->radj, m));
+        k_offsets<<<gridN(m + 1, c.device), 256, 0, c.stream>>>(k2s, m, n, b, g->roff);
+    }
+    if (want_eid) SP_TRY(dalloc(&g->reid, m));
+    k_rev_out<IdxT><<<gridN(m, c.device), 256, 0, c.stream>>>(
+        k2s, vo, m, b, want_adj ? g->radj : nullptr, want_eid ? g->reid : nullptr);
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
+int build_reverse(sp_graph *g, Call &c, bool want_adj, bool want_eid) {
+    if (g->m < (int64_t)0xFFFFFFFFll) return build_reverse_t<uint32_t>(g, c, want_adj, want_eid);
+    return build_reverse_t<uint64_t>(g, c, want_adj, want_eid);
+}
+
+int finish_graph(sp_graph *g, Call &c) {
+    int64_t n = g->n, m = g->m;
+    unsigned long long *cnt;
+    SP_TRY(c.alloc(&cnt, 4));
+    SP_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), c.stream));
+    SP_TRY(dalloc(&g->outdeg, n));
+    k_deg<<<gridN(n, c.device), 256, 0, c.stream>>>(g->off, n, g->outdeg, cnt + 0);
+    if (g->directed) {
+        SP_TRY(build_reverse(g, c, true, false));
+        SP_TRY(dalloc(&g->indeg, n));
+        k_deg<<<gridN(n, c.device), 256, 0, c.stream>>>(g->roff, n, g->indeg, cnt + 1);
+    } else {
+        g->roff = g->off;
+        g->radj = g->adj;
+        g->indeg = g->outdeg;
+    }
+    SP_TRY(dalloc(&g->hubs_in, n));
+    k_hubs<<<gridN(n, c.device), 256, 0, c.stream>>>(g->indeg, n, kHubIn, g->hubs_in, cnt + 2);
+    SP_TRY(dalloc(&g->wrange, 2));
+    int32_t init[2] = {0x7fffffff, (int32_t)0x80000000};
+    SP_CUDA(cudaMemcpyAsync(g->wrange, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    if (m) k_wrange<<<gridN(m, c.device), 256, 0, c.stream>>>(g->w, m, g->wrange);
+    unsigned long long h[4];
+    SP_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    SP_CUDA(cudaGetLastError());
+    g->max_outdeg = (int64_t)h[0];
+    g->max_indeg = g->directed ? (int64_t)h[1] : (int64_t)h[0];
+    g->nhubs_in = (int64_t)h[2];
+    return SP_OK;
+}
+
+// Forward build from device edge arrays.
+template <class IdxT>
+int build_forward_t(sp_graph *g, Call &c, const int32_t *u, const int32_t *v,
+                    const int32_t *w, int64_t ne) {
+    int64_t n = g->n, m = g->m;
+    int b = bits_for(n);
+    int64_t *excl = nullptr;
+    if (!g->directed) {
+        SP_TRY(c.alloc(&excl, ne + 1));
+        k_nonloop<<<gridN(ne, c.device), 256, 0, c.stream>>>(u, v, ne, excl);
+        SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+            return cub::DeviceScan::ExclusiveSum(t, sz, excl, excl, ne, c.stream);
+        }));
+    }
+    uint64_t *key, *keys;
+    IdxT *vi, *perm;
+    int32_t *sw;
+    SP_TRY(c.alloc(&key, m));
+    SP_TRY(c.alloc(&keys, m));
+    SP_TRY(c.alloc(&vi, m));
+    SP_TRY(c.alloc(&perm, m));
+    SP_TRY(c.alloc(&sw, m));
+    if (ne)
+        k_fill_slots<IdxT><<<gridN(ne, c.device), 256, 0, c.stream>>>(u, v, w, ne, excl, g->directed,
+                                                                      b, key, vi, sw);
+    if (m)
+        SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+            return cub::DeviceRadixSort::SortPairs(t, sz, key, keys, vi, perm, m, 0, 2 * b, c.stream);
+        }));
+    SP_TRY(dalloc(&g->off, n + 1));
+    SP_TRY(dalloc(&g->adj, m));
+    SP_TRY(dalloc(&g->w, m));
+    SP_TRY(dalloc(&g->weff, m));
+    int64_t *runstart;
+    SP_TRY(c.alloc(&runstart, m));
+    k_offsets<<<gridN(m + 1, c.device), 256, 0, c.stream>>>(keys, m, n, b, g->off);
+    if (m) {
+        k_forward<IdxT><<<gridN(m, c.device), 256, 0, c.stream>>>(keys, perm, sw, m, b, g->adj, g->w,
+                                                                  runstart);
+        SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+            return cub::DeviceScan::InclusiveScan(t, sz, runstart, runstart, MaxOp(), m, c.stream);
+        }));
+        k_weff<<<gridN(m, c.device), 256, 0, c.stream>>>(g->w, runstart, m, g->weff);
+    }
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
+int build_from_device_edges(sp_graph *g, Call &c, const int32_t *u, const int32_t *v,
+                            const int32_t *w, int64_t ne, int64_t n_hint) {
+    // vertex count and id validation (graph.py:110,114)
+    int *mm;
+    SP_TRY(c.alloc(&mm, 2));
+    int init[2] = {0x7fffffff, -1};
+    SP_CUDA(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    if (ne) k_id_range<<<gridN(ne, c.device), 256, 0, c.stream>>>(u, v, ne, mm, mm + 1);
+    int h[2];
+    SP_CUDA(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    int64_t *nl = nullptr;
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    SP_CHECK(ne == 0 || h[0] >= 0, SP_ERR_ARG, "negative vertex id %d in edge list", h[0]);
+    int64_t n = n_hint > (int64_t)h[1] + 1 ? n_hint : (int64_t)h[1] + 1;
+    SP_CHECK(n < 0x7fffffffll, SP_ERR_UNSUPPORTED, "n = %lld exceeds int32 vertex ids", (long long)n);
+    g->n = n;
+    int64_t m = ne;
+    if (!g->directed && ne) {
+        // m = ne + #non-loop edges
+        SP_TRY(c.alloc(&nl, ne));
+        k_nonloop<<<gridN(ne, c.device), 256, 0, c.stream>>>(u, v, ne, nl);
+        int64_t *tot;
+        SP_TRY(c.alloc(&tot, 1));
+        SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+            return cub::DeviceReduce::Sum(t, sz, nl, tot, ne, c.stream);
+        }));
+        int64_t ht = 0;
+        SP_CUDA(cudaMemcpyAsync(&ht, tot, sizeof(ht), cudaMemcpyDeviceToHost, c.stream));
+        SP_CUDA(cudaStreamSynchronize(c.stream));
+        m += ht;
+    }
+    g->m = m;
+    if (m < (int64_t)0xFFFFFFFFll)
+        SP_TRY(build_forward_t<uint32_t>(g, c, u, v, w, ne));
+    else
+        SP_TRY(build_forward_t<uint64_t>(g, c, u, v, w, ne));
+    return finish_graph(g, c);
+}
+
+int new_graph(int directed, int device, sp_graph **out) {
+    sp_graph *g = new (std::nothrow) sp_graph();
+    SP_CHECK(g, SP_ERR_OOM, "host allocation failed");
+    g->directed = directed ? 1 : 0;
+    g->device = device;
+    *out = g;
+    return SP_OK;
+}
+
+// Dedupe sorted 64-bit keys in place; drop the ~0 self-loop sentinel.
+int unique_keys(Call &c, uint64_t *key, int64_t ne, uint64_t **uniq, int64_t *nu) {
+    uint64_t *keys, *outk;
+    SP_TRY(c.alloc(&keys, ne));
+    SP_TRY(c.alloc(&outk, ne));
+    SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+        return cub::DeviceRadixSort::SortKeys(t, sz, key, keys, ne, 0, 64, c.stream);
+    }));
+    int64_t *cnt;
+    SP_TRY(c.alloc(&cnt, 1));
+    SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+        return cub::DeviceSelect::Unique(t, sz, keys, outk, cnt, ne, c.stream);
+    }));
+    int64_t h = 0;
+    SP_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    if (h > 0) {
+        uint64_t last = 0;
+        SP_CUDA(cudaMemcpy(&last, outk + h - 1, sizeof(last), cudaMemcpyDeviceToHost));
+        if (last == ~0ull) h--;
+    }
+    *uniq = outk;
+    *nu = h;
+    return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sp_graph_from_edges(const int32_t *u, const int32_t *v, const int32_t *w, int64_t nedges,
+                        int64_t n, int directed, int mem, int device, sp_graph **out) {
+    SP_CHECK(out && nedges >= 0 && (nedges == 0 || (u && v && w)), SP_ERR_ARG,
+             "sp_graph_from_edges: bad arguments");
+    *out = nullptr;
+    Call c;
+    SP_TRY(c.begin(device));
+    const int32_t *du = u, *dv = v, *dw = w;
+    if (mem == SP_MEM_HOST && nedges) {
+        int32_t *a, *b2, *cc;
+        SP_TRY(c.alloc(&a, nedges));
+        SP_TRY(c.alloc(&b2, nedges));
+        SP_TRY(c.alloc(&cc, nedges));
+        SP_TRY(to_device(a, u, nedges * 4, mem, c.stream));
+        SP_TRY(to_device(b2, v, nedges * 4, mem, c.stream));
+        SP_TRY(to_device(cc, w, nedges * 4, mem, c.stream));
+        du = a; dv = b2; dw = cc;
+    }
+    sp_graph *g;
+    SP_TRY(new_graph(directed, device, &g));
+    int rc = build_from_device_edges(g, c, du, dv, dw, nedges, n);
+    if (rc == SP_OK) rc = c.finish(nullptr);
+    if (rc != SP_OK) {
+        free_graph(g);
+        return rc;
+    }
+    *out = g;
+    return SP_OK;
+}
+
+int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj, const int32_t *weights,
+                      int64_t n, int64_t m, int directed, int mem, int device, sp_graph **out) {
+    SP_CHECK(out && n >= 0 && m >= 0 && offsets, SP_ERR_ARG, "sp_graph_from_csr: bad arguments");
+    SP_CHECK(n < 0x7fffffffll, SP_ERR_UNSUPPORTED, "n exceeds int32 vertex ids");
+    *out = nullptr;
+    Call c;
+    SP_TRY(c.begin(device));
+    sp_graph *g;
+    SP_TRY(new_graph(directed, device, &g));
+    g->n = n;
+    g->m = m;
+    int rc = SP_OK;
+    do {
+        if ((rc = dalloc(&g->off, n + 1))) break;
+        if ((rc = dalloc(&g->adj, m))) break;
+        if ((rc = dalloc(&g->w, m))) break;
+        if ((rc = dalloc(&g->weff, m))) break;
+        if ((rc = to_device(g->off, offsets, (n + 1) * 8, mem, c.stream))) break;
+        if ((rc = to_device(g->adj, adj, m * 4, mem, c.stream))) break;
+        if ((rc = to_device(g->w, weights, m * 4, mem, c.stream))) break;
+        if (m) {
+            // w_eff: run starts of equal destinations within each row
+            int b = bits_for(n);
+            uint64_t *key;
+            int64_t *runstart;
+            if ((rc = c.alloc(&key, m))) break;
+            if ((rc = c.alloc(&runstart, m))) break;
+            // key = (dst << b | src): equal neighbours <=> same (src, dst) pair
+            k_rev_keys<<<gridN(n * 32, c.device), 256, 0, c.stream>>>(g->off, g->adj, n, b, key);
+            k_runstart<<<gridN(m, c.device), 256, 0, c.stream>>>(key, m, runstart);
+            if ((rc = cub_call(c, [&](void *t, size_t &sz) {
+                     return cub::DeviceScan::InclusiveScan(t, sz, runstart, runstart, MaxOp(), m,
+                                                           c.stream);
+                 })))
+                break;
+            k_weff<<<gridN(m, c.device), 256, 0, c.stream>>>(g->w, runstart, m, g->weff);
+        }
+        if ((rc = finish_graph(g, c))) break;
+        rc = c.finish(nullptr);
+    } while (0);
+    if (rc != SP_OK) {
+        free_graph(g);
+        return rc;
+    }
+    *out = g;
+    return SP_OK;
+}
+
+int sp_graph_generate(int kind, int64_t p0, int64_t p1, int64_t seed, int undirected, int device,
+                      sp_graph **out) {
+    SP_CHECK(out, SP_ERR_ARG, "sp_graph_generate: out is NULL");
+    *out = nullptr;
+    Call c;
+    SP_TRY(c.begin(device));
+    uint64_t sk = splitmix64((uint64_t)seed);
+    uint64_t wsk = splitmix64((uint64_t)seed ^ 0x5EEDull);
+    int32_t *u, *v, *w;
+    int64_t ne = 0, n = 0;
+    if (kind == SP_GEN_GRID) {
+        SP_CHECK(p0 > 0 && p1 > 0 && p0 * p1 < 0x7fffffffll, SP_ERR_ARG, "bad grid size");
+        n = p0 * p1;
+        ne = p0 * (p1 - 1) + (p0 - 1) * p1;
+        SP_TRY(c.alloc(&u, ne));
+        SP_TRY(c.alloc(&v, ne));
+        SP_TRY(c.alloc(&w, ne));
+        k_gen_grid<<<gridN(n, c.device), 256, 0, c.stream>>>(p0, p1, wsk, u, v, w);
+        undirected = 1;
+    } else {
+        int64_t cand;
+        uint64_t *key;
+        if (kind == SP_GEN_RMAT) {
+            SP_CHECK(p0 >= 1 && p0 <= 30 && p1 >= 1, SP_ERR_ARG, "bad RMAT scale/edge factor");
+            n = (int64_t)1 << p0;
+            cand = p1 << p0;
+            SP_TRY(c.alloc(&key, cand));
+            int ta = 37356, tb = 37356 + 12452, tc = 37356 + 12452 + 12452;
+            k_gen_rmat<<<gridN(cand, c.device), 256, 0, c.stream>>>(cand, (int)p0, sk, ta, tb, tc,
+                                                                   undirected, key);
+        } else if (kind == SP_GEN_UNIFORM) {
+            SP_CHECK(p0 >= 1 && p0 < 0x7fffffffll && p1 >= 0, SP_ERR_ARG, "bad uniform size");
+            n = p0;
+            cand = p1;
+            SP_TRY(c.alloc(&key, cand));
+            k_gen_uniform<<<gridN(cand, c.device), 256, 0, c.stream>>>(cand, (uint64_t)n, sk,
+                                                                      undirected, key);
+        } else {
+            SP_CHECK(false, SP_ERR_ARG, "unknown generator kind %d", kind);
+        }
+        uint64_t *uk;
+        SP_TRY(unique_keys(c, key, cand, &uk, &ne));
+        SP_TRY(c.alloc(&u, ne));
+        SP_TRY(c.alloc(&v, ne));
+        SP_TRY(c.alloc(&w, ne));
+        if (ne) k_keys_to_edges<<<gridN(ne, c.device), 256, 0, c.stream>>>(uk, ne, wsk, u, v, w);
+    }
+    SP_CUDA(cudaGetLastError());
+    sp_graph *g;
+    SP_TRY(new_graph(!undirected, device, &g));
+    int rc = build_from_device_edges(g, c, u, v, w, ne, n);
+    if (rc == SP_OK) rc = c.finish(nullptr);
+    if (rc != SP_OK) {
+        free_graph(g);
+        return rc;
+    }
+    *out = g;
+    return SP_OK;
+}
+
+int sp_graph_info(const sp_graph *g, int64_t *n, int64_t *m, int *directed) {
+    SP_CHECK(g, SP_ERR_ARG, "null graph");
+    if (n) *n = g->n;
+    if (m) *m = g->m;
+    if (directed) *directed = g->directed;
+    return SP_OK;
+}
+
+int sp_graph_download(const sp_graph *cg, int which, void *dst) {
+    SP_CHECK(cg && dst, SP_ERR_ARG, "sp_graph_download: bad arguments");
+    sp_graph *g = const_cast<sp_graph *>(cg);
+    SP_CUDA(cudaSetDevice(g->device));
+    const void *src = nullptr;
+    size_t bytes = 0;
+    switch (which) {
+        case SP_ARR_OFFSETS: src = g->off; bytes = (g->n + 1) * 8; break;
+        case SP_ARR_ADJ: src = g->adj; bytes = g->m * 4; break;
+        case SP_ARR_WEIGHTS: src = g->w; bytes = g->m * 4; break;
+        case SP_ARR_REV_OFFSETS: src = g->roff; bytes = (g->n + 1) * 8; break;
+        case SP_ARR_REV_ADJ: src = g->radj; bytes = g->m * 4; break;
+        case SP_ARR_WEFF: src = g->weff; bytes = g->m * 4; break;
+        case SP_ARR_REV_EID: {
+            std::lock_guard<std::mutex> lk(g_lazy_mu);
+            if (!g->reid && g->m) {
+                Call c;
+                SP_TRY(c.begin(g->device));
+                SP_TRY(build_reverse(g, c, false, true));
+                SP_TRY(c.finish(nullptr));
+            }
+            src = g->reid;
+            bytes = g->m * 8;
+            break;
+        }
+        default: SP_CHECK(false, SP_ERR_ARG, "unknown array id %d", which);
+    }
+    if (bytes) SP_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return SP_OK;
+}
+
+int sp_graph_weight_range(const sp_graph *g, int32_t *wmin, int32_t *wmax) {
+    SP_CHECK(g, SP_ERR_ARG, "null graph");
+    SP_CHECK(g->m > 0, SP_ERR_ARG, "weight range of a graph with no edges");
+    SP_CUDA(cudaSetDevice(g->device));
+    int32_t h[2];
+    SP_CUDA(cudaMemcpy(h, g->wrange, sizeof(h), cudaMemcpyDeviceToHost));
+    if (wmin) *wmin = h[0];
+    if (wmax) *wmax = h[1];
+    return SP_OK;
+}
+
+void sp_graph_destroy(sp_graph *g) { free_graph(g); }
+
+}  // extern "C"

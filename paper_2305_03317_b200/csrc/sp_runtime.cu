@@ -1,0 +1,134 @@
+// sp_runtime.cu -- error reporting, per-call streams, stream-ordered scratch.
+#include <stdarg.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "sp_common.cuh"
+
+namespace sp {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
+    set_error("CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+              cudaGetErrorString(e), what, file, line);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return SP_ERR_OOM;
+    }
+    return SP_ERR_CUDA;
+}
+
+int num_sms(int device) {
+    static int cached[64] = {0};
+    if (device < 0 || device >= 64) return kNumSMs;
+    if (!cached[device]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+            v = kNumSMs;
+        cached[device] = v;
+    }
+    return cached[device];
+}
+
+static std::once_flag g_pool_once[64];
+
+static void tune_pool(int device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;  // keep freed scratch for reuse
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+}
+
+int scratch_alloc(void **p, size_t bytes, cudaStream_t s) {
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("device scratch allocation of %zu bytes failed (%s)", bytes,
+                  cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? SP_ERR_OOM : SP_ERR_CUDA;
+    }
+    return SP_OK;
+}
+
+void scratch_free(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+int Call::begin(int dev) {
+    device = dev;
+    SP_CUDA(cudaSetDevice(dev));
+    if (dev >= 0 && dev < 64) std::call_once(g_pool_once[dev], tune_pool, dev);
+    SP_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    SP_CUDA(cudaEventCreate(&t0));
+    SP_CUDA(cudaEventCreate(&t1));
+    SP_CUDA(cudaEventRecord(t0, stream));
+    return SP_OK;
+}
+
+int Call::finish(sp_stats *st) {
+    SP_CUDA(cudaEventRecord(t1, stream));
+    SP_CUDA(cudaStreamSynchronize(stream));
+    SP_CUDA(cudaGetLastError());
+    if (st) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t0, t1);
+        st->device_ms = ms;
+        st->kernel_launches = launches;
+    }
+    return SP_OK;
+}
+
+Call::~Call() {
+    if (stream) {
+        for (int i = 0; i < nbufs; i++) scratch_free(bufs[i], stream);
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+    }
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+}
+
+int to_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s) {
+    if (!bytes) return SP_OK;
+    SP_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                            mem == SP_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                 : cudaMemcpyHostToDevice, s));
+    return SP_OK;
+}
+
+int from_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s) {
+    if (!bytes) return SP_OK;
+    SP_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                            mem == SP_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                 : cudaMemcpyDeviceToHost, s));
+    return SP_OK;
+}
+
+}  // namespace sp
+
+extern "C" {
+
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+
+const char *sp_last_error(void) { return sp::g_err; }
+
+int sp_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+}  // extern "C"

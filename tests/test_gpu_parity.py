@@ -1,0 +1,375 @@
+"""GPU parity: libstarplat_b200.so (through the drop-in host layer and its C
+ABI) against the golden vectors of the Python reference and against the
+CPU oracle (oracle/cpu_ref.c, itself pinned bit-exact to the reference in
+test_oracle_golden.py).
+
+Tolerances:
+  SSSP dist, TC count, CSR arrays: bit-exact.
+  PR deterministic mode: bit-exact ranks, same iter and diff.
+  PR fast mode: |d|_inf / |ref|_inf <= 1e-12 (hub rows use a tree order),
+     same iteration count.
+  BC deterministic mode: bit-exact bc/sigma/delta; fast mode <= 1e-12.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden
+from oracle import cpu_ref
+
+pytestmark = pytest.mark.gpu
+
+sp = pytest.importorskip("paper_2305_03317_b200")
+from paper_2305_03317_b200 import corpus, gen  # noqa: E402
+from paper_2305_03317_b200.errors import (ExecError,  # noqa: E402
+                                          NonConvergenceError)
+
+CASES = golden_cases()
+PR_ARGS = {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    den = max(np.abs(b).max(initial=0.0), 1e-300)
+    return float(np.abs(a - b).max(initial=0.0) / den)
+
+
+def _graph(z):
+    return sp.from_arrays(z["u"], z["v"], z["w"], directed=bool(z["directed"]),
+                          n=int(z["n"]))
+
+
+@pytest.fixture(scope="module")
+def graphs():
+    cache = {}
+
+    def get(case):
+        if case not in cache:
+            z = load_golden(case)
+            cache[case] = (z, _graph(z))
+        return cache[case]
+    return get
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_csr_build(case, graphs):
+    z, g = graphs(case)
+    assert g.n == int(z["n"]) and g.m == len(z["csr_adj"])
+    np.testing.assert_array_equal(g.offsets, z["csr_off"])
+    np.testing.assert_array_equal(g.adj, z["csr_adj"])
+    np.testing.assert_array_equal(g.weights, z["csr_w"])
+    np.testing.assert_array_equal(g.rev_offsets, z["csr_roff"])
+    np.testing.assert_array_equal(g.rev_adj, z["csr_radj"])
+    np.testing.assert_array_equal(g.rev_eid, z["csr_reid"])
+    o = cpu_ref.build_csr(z["u"], z["v"], z["w"], bool(z["directed"]), int(z["n"]))
+    np.testing.assert_array_equal(g.effective_weights, o.weff)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_sssp(case, graphs):
+    z, g = graphs(case)
+    for i, s in enumerate(z["sssp_srcs"]):
+        for prog in (corpus.SSSP, corpus.SSSP_PULL):
+            r = sp.run(prog, g, {"src": int(s)})
+            np.testing.assert_array_equal(r.env.node_props["dist"].astype(np.int64),
+                                          z["sssp_dist"][i])
+            assert r.env.scalars == {"finished": True}
+            assert not r.env.node_props["modified"].any()
+            assert r.fixedpoint_iterations["finished"] >= 1
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("det", [True, False])
+def test_pagerank(case, det, graphs):
+    z, g = graphs(case)
+    cap = int(z["pr_err_cap"])
+    if cap >= 0:
+        with pytest.raises(NonConvergenceError) as ei:
+            sp.run(corpus.PR, g, PR_ARGS, deterministic=det)
+        assert ei.value.flag == "converged" and ei.value.cap == cap
+        r = sp.run(corpus.PR, g, PR_ARGS, max_iters=10 ** 6, deterministic=det)
+    else:
+        r = sp.run(corpus.PR, g, PR_ARGS, deterministic=det)
+    rank = r.env.node_props["rank"]
+    assert r.env.scalars["iter"] == int(z["pr_iter"])
+    assert r.fixedpoint_iterations["converged"] == int(z["pr_iters"])
+    if det:
+        assert rank.tobytes() == z["pr_rank"].tobytes()
+        assert r.env.scalars["diff"] == float(z["pr_diff"])
+    else:
+        assert rel_err(rank, z["pr_rank"]) <= 1e-12
+    np.testing.assert_array_equal(r.env.node_props["rank_nxt"], rank)
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("det", [True, False])
+def test_bc(case, det, graphs):
+    z, g = graphs(case)
+    srcs = z["bc_srcs"].tolist()
+    r = sp.run(corpus.BC, g, {"sourceSet": srcs}, deterministic=det)
+    bc = r.env.node_props["bc"]
+    if det:
+        assert bc.tobytes() == z["bc"].tobytes()
+        assert r.env.node_props["sigma"].tobytes() == z["bc_sigma"].tobytes()
+        assert r.env.node_props["delta"].tobytes() == z["bc_delta"].tobytes()
+    else:
+        assert rel_err(bc, z["bc"]) <= 1e-12
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_tc(case, graphs):
+    z, g = graphs(case)
+    r = sp.run(corpus.TC, g, {})
+    assert r.env.scalars == {"triangle_count": int(z["tc"])}
+
+
+# ---------------------------------------------------------------------------
+# device generators == host generators (same edge lists -> same CSR)
+
+@pytest.mark.parametrize("kind,p0,p1,undirected", [
+    ("rmat", 10, 16, False), ("rmat", 12, 8, True), ("uniform", 5000, 40000, True),
+    ("uniform", 3000, 20000, False), ("grid", 17, 23, True)])
+def test_device_generator_matches_host(kind, p0, p1, undirected):
+    if kind == "rmat":
+        u, v, w, n = gen.rmat(p0, p1, seed=3, undirected=undirected)
+    elif kind == "uniform":
+        u, v, w, n = gen.uniform(p0, p1, seed=3, undirected=undirected)
+    else:
+        u, v, w, n = gen.grid(p0, p1, seed=3)
+    gh = sp.from_arrays(u, v, w, directed=not undirected, n=n)
+    gd = sp.generate(kind, p0, p1, seed=3, undirected=undirected)
+    assert (gd.n, gd.m, gd.directed) == (gh.n, gh.m, gh.directed)
+    np.testing.assert_array_equal(gd.offsets, gh.offsets)
+    np.testing.assert_array_equal(gd.adj, gh.adj)
+    np.testing.assert_array_equal(gd.weights, gh.weights)
+
+
+# ---------------------------------------------------------------------------
+# larger seeded graphs against the CPU oracle
+
+def _pair(kind, p0, p1, seed, undirected):
+    if kind == "rmat":
+        u, v, w, n = gen.rmat(p0, p1, seed=seed, undirected=undirected)
+    elif kind == "uniform":
+        u, v, w, n = gen.uniform(p0, p1, seed=seed, undirected=undirected)
+    else:
+        u, v, w, n = gen.grid(p0, p1, seed=seed)
+    return (sp.from_arrays(u, v, w, directed=not undirected, n=n),
+            cpu_ref.build_csr(u, v, w, not undirected, n))
+
+
+def test_sssp_cfg1_rmat16_bit_exact():
+    """BASELINE cfg1: SSSP from 0 on weighted RMAT-16 (directed)."""
+    g, o = _pair("rmat", 16, 16, 1, False)
+    r = sp.run(corpus.SSSP, g, {"src": 0})
+    dist, _, rc = cpu_ref.sssp(o, 0)
+    assert rc == 0
+    np.testing.assert_array_equal(r.env.node_props["dist"], dist)
+
+
+@pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 14, 16, False), ("grid", 64, 64, True),
+                                            ("uniform", 1 << 14, 1 << 17, True)])
+def test_sssp_seeded(kind, p0, p1, und):
+    g, o = _pair(kind, p0, p1, 11, und)
+    for s in (0, g.n // 2):
+        r = sp.run(corpus.SSSP, g, {"src": s})
+        dist, _, rc = cpu_ref.sssp(o, s)
+        np.testing.assert_array_equal(r.env.node_props["dist"], dist)
+
+
+@pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 14, 16, False), ("rmat", 13, 16, True),
+                                            ("grid", 32, 32, True), ("rmat", 16, 16, False)])
+def test_pagerank_seeded(kind, p0, p1, und):
+    g, o = _pair(kind, p0, p1, 5, und)
+    rank, it, diff, its, rc = cpu_ref.pagerank(o, 0.85, 1e-6, 100, cap=10 ** 6, nthreads=4)
+    rd = sp.run(corpus.PR, g, PR_ARGS, max_iters=10 ** 6, deterministic=True)
+    assert rd.env.node_props["rank"].tobytes() == rank.tobytes()
+    assert rd.env.scalars["iter"] == it and rd.env.scalars["diff"] == diff
+    rf = sp.run(corpus.PR, g, PR_ARGS, max_iters=10 ** 6)
+    assert rel_err(rf.env.node_props["rank"], rank) <= 1e-12
+    assert rf.env.scalars["iter"] == it
+
+
+@pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 13, 16, True), ("rmat", 12, 16, False),
+                                            ("grid", 40, 40, True)])
+def test_bc_seeded(kind, p0, p1, und):
+    g, o = _pair(kind, p0, p1, 7, und)
+    rng = np.random.default_rng(1)
+    srcs = rng.choice(g.n, size=6, replace=False).tolist() + [0]
+    bc, sg, dl = cpu_ref.bc(o, srcs, nthreads=4)
+    rd = sp.run(corpus.BC, g, {"sourceSet": srcs}, deterministic=True)
+    assert rd.env.node_props["bc"].tobytes() == bc.tobytes()
+    assert rd.env.node_props["sigma"].tobytes() == sg.tobytes()
+    assert rd.env.node_props["delta"].tobytes() == dl.tobytes()
+    rf = sp.run(corpus.BC, g, {"sourceSet": srcs})
+    assert rel_err(rf.env.node_props["bc"], bc) <= 1e-12
+
+
+@pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 13, 16, True), ("rmat", 12, 16, False),
+                                            ("uniform", 1 << 15, 1 << 19, True)])
+def test_tc_seeded(kind, p0, p1, und):
+    g, o = _pair(kind, p0, p1, 9, und)
+    r = sp.run(corpus.TC, g, {})
+    assert r.env.scalars["triangle_count"] == cpu_ref.tc(o, nthreads=8)
+
+
+def _hub_graph(directed):
+    """A 20000-leaf star plus random leaf edges: rows far above the hub
+    thresholds (PR in-degree > 4096, BC rows > 8192, SSSP/BFS > 2048)."""
+    rng = np.random.default_rng(4)
+    k = 20000
+    u = np.concatenate([np.arange(1, k + 1), rng.integers(1, k + 1, 30000)])
+    v = np.concatenate([np.zeros(k, np.int64), rng.integers(1, k + 1, 30000)])
+    w = rng.integers(1, 100, len(u))
+    if directed:  # leaves -> hub and hub -> leaves both present
+        u, v, w = np.concatenate([u, v[:k]]), np.concatenate([v, u[:k]]), np.concatenate([w, w[:k]])
+    return u, v, w, k + 1
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_hub_paths(directed):
+    u, v, w, n = _hub_graph(directed)
+    g = sp.from_arrays(u, v, w, directed=directed, n=n)
+    o = cpu_ref.build_csr(u, v, w, directed, n)
+    dist, _, _ = cpu_ref.sssp(o, 5)
+    np.testing.assert_array_equal(sp.run(corpus.SSSP, g, {"src": 5}).env.node_props["dist"], dist)
+    rank, it, diff, its, rc = cpu_ref.pagerank(o, cap=10 ** 6)
+    rd = sp.run(corpus.PR, g, PR_ARGS, max_iters=10 ** 6, deterministic=True)
+    assert rd.env.node_props["rank"].tobytes() == rank.tobytes() and rd.env.scalars["iter"] == it
+    rf = sp.run(corpus.PR, g, PR_ARGS, max_iters=10 ** 6)
+    assert rel_err(rf.env.node_props["rank"], rank) <= 1e-12 and rf.env.scalars["iter"] == it
+    srcs = [0, 7, 19999, 7]
+    bc, sg, dl = cpu_ref.bc(o, srcs)
+    rd = sp.run(corpus.BC, g, {"sourceSet": srcs}, deterministic=True)
+    assert rd.env.node_props["bc"].tobytes() == bc.tobytes()
+    assert rd.env.node_props["delta"].tobytes() == dl.tobytes()
+    rf = sp.run(corpus.BC, g, {"sourceSet": srcs})
+    assert rel_err(rf.env.node_props["bc"], bc) <= 1e-12
+    assert sp.run(corpus.TC, g, {}).env.scalars["triangle_count"] == cpu_ref.tc(o)
+
+
+# ---------------------------------------------------------------------------
+# edge cases the reference exercises
+
+def _multigraph(seed, n=300, m=3000, directed=True, neg=False):
+    rng = np.random.default_rng(seed)
+    u = rng.integers(0, n, m)
+    v = rng.integers(0, n, m)
+    # parallel edges and self-loops on purpose
+    u[: m // 10] = u[m // 10: 2 * (m // 10)]
+    v[: m // 10] = v[m // 10: 2 * (m // 10)]
+    u[-20:] = v[-20:]
+    w = rng.integers(1, 100, m)
+    if neg:  # negative weights on a DAG (u < v): no negative cycle
+        keep = u < v
+        u, v, w = u[keep], v[keep], w[keep] - 60
+    return u, v, w, n
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_multigraph_all_algorithms(directed):
+    u, v, w, n = _multigraph(3, directed=directed)
+    g = sp.from_arrays(u, v, w, directed=directed, n=n)
+    o = cpu_ref.build_csr(u, v, w, directed, n)
+    np.testing.assert_array_equal(g.adj, o.adj)
+    np.testing.assert_array_equal(g.rev_eid, o.reid)
+    dist, _, _ = cpu_ref.sssp(o, 0)
+    np.testing.assert_array_equal(sp.run(corpus.SSSP, g, {"src": 0}).env.node_props["dist"], dist)
+    rank = cpu_ref.pagerank(o, cap=10 ** 6)[0]
+    r = sp.run(corpus.PR, g, PR_ARGS, max_iters=10 ** 6, deterministic=True)
+    assert r.env.node_props["rank"].tobytes() == rank.tobytes()
+    bc = cpu_ref.bc(o, [0, 5, 7, 5])[0]
+    r = sp.run(corpus.BC, g, {"sourceSet": [0, 5, 7, 5]}, deterministic=True)
+    assert r.env.node_props["bc"].tobytes() == bc.tobytes()
+    assert sp.run(corpus.TC, g, {}).env.scalars["triangle_count"] == cpu_ref.tc(o)
+
+
+def test_sssp_negative_weights_dag():
+    u, v, w, n = _multigraph(5, neg=True)
+    g = sp.from_arrays(u, v, w, directed=True, n=n)
+    o = cpu_ref.build_csr(u, v, w, True, n)
+    dist, _, rc = cpu_ref.sssp(o, int(u[0]))
+    assert rc == 0
+    r = sp.run(corpus.SSSP, g, {"src": int(u[0])})
+    np.testing.assert_array_equal(r.env.node_props["dist"], dist)
+
+
+def test_sssp_negative_cycle_nonconvergence():
+    g = sp.from_edges([(0, 1, 1), (1, 2, -3), (2, 0, 1)])
+    with pytest.raises(NonConvergenceError) as ei:
+        sp.run(corpus.SSSP, g, {"src": 0})
+    assert ei.value.flag == "finished" and ei.value.cap == 2 * 3 + 16
+    with pytest.raises(NonConvergenceError) as ei:
+        sp.run(corpus.SSSP, g, {"src": 0}, max_iters=5)
+    assert ei.value.cap == 5
+
+
+def test_int_max_semantics():
+    """A candidate >= INT_MAX never wins (interp.py:11-14)."""
+    g = sp.from_edges([(0, 1, 2_000_000_000), (1, 2, 2_000_000_000), (0, 3, 5)])
+    d = sp.run(corpus.SSSP, g, {"src": 0}).env.node_props["dist"]
+    assert d.tolist() == [0, 2_000_000_000, 2147483647, 5]
+
+
+def test_spec_known_answers():
+    # SPEC.md:271-275
+    d = sp.run(corpus.SSSP, sp.from_edges([(0, 1, 4), (1, 2, 3)]), {"src": 0})
+    assert d.env.node_props["dist"].tolist() == [0, 4, 7]
+    iso = sp.from_edges([(1, 2, 5)], n=4)
+    assert sp.run(corpus.SSSP, iso, {"src": 0}).env.node_props["dist"].tolist() == \
+        [0, 2147483647, 2147483647, 2147483647]
+    c4 = sp.from_edges([(0, 1), (1, 2), (2, 3), (3, 0)])
+    r = sp.run(corpus.PR, c4, PR_ARGS)
+    assert np.allclose(r.env.node_props["rank"], 0.25, atol=1e-9)
+    k3 = sp.from_edges([(0, 1), (0, 2), (1, 2)], directed=False)
+    k4 = sp.from_edges([(a, b) for a in range(4) for b in range(a + 1, 4)], directed=False)
+    assert sp.run(corpus.TC, k3, {}).env.scalars["triangle_count"] == 1
+    assert sp.run(corpus.TC, k4, {}).env.scalars["triangle_count"] == 4
+    p3 = sp.from_edges([(0, 1), (1, 2)], directed=False)
+    r = sp.run(corpus.BC, p3, {"sourceSet": [0, 1, 2]}, deterministic=True)
+    assert r.env.node_props["bc"].tolist() == [0.0, 1.0, 0.0]
+
+
+def test_empty_and_degenerate():
+    g = sp.from_edges([])
+    assert g.n == 0 and g.m == 0
+    r = sp.run(corpus.PR, g, PR_ARGS)
+    assert r.env.scalars["iter"] == 1 and r.env.scalars["diff"] == 0.0
+    assert sp.run(corpus.TC, g, {}).env.scalars["triangle_count"] == 0
+    with pytest.raises(ExecError):
+        sp.run(corpus.SSSP, g, {"src": 0})
+    g1 = sp.from_edges([], n=5)
+    r = sp.run(corpus.BC, g1, {"sourceSet": []})
+    assert list(r.env.node_props) == ["bc"] and not r.env.node_props["bc"].any()
+    r = sp.run(corpus.SSSP, g1, {"src": 4})
+    assert r.env.node_props["dist"].tolist() == [2147483647] * 4 + [0]
+    with pytest.raises(ExecError, match="missing argument 'src'"):
+        sp.run(corpus.SSSP, g1, {})
+    with pytest.raises(ExecError, match="set argument 'sourceSet' id 9 out of range"):
+        sp.run(corpus.BC, g1, {"sourceSet": [1, 9]})
+
+
+def test_iteration_hook_called_each_iteration():
+    g = sp.from_edges([(i, i + 1, 1) for i in range(20)])
+    seen = []
+    r = sp.run(corpus.PR, g, PR_ARGS, on_fixedpoint_iteration=lambda f, k, ex: seen.append((f, k)))
+    assert seen == [("converged", k) for k in range(1, r.fixedpoint_iterations["converged"] + 1)]
+    seen.clear()
+    r = sp.run(corpus.SSSP, g, {"src": 0}, on_fixedpoint_iteration=lambda f, k, ex: seen.append(k))
+    assert seen == list(range(1, r.fixedpoint_iterations["finished"] + 1))
+
+    def boom(f, k, ex):
+        raise KeyboardInterrupt("stop")
+    with pytest.raises(KeyboardInterrupt):
+        sp.run(corpus.SSSP, g, {"src": 0}, on_fixedpoint_iteration=boom)
+
+
+def test_weight_range_and_io(tmp_path):
+    g = sp.from_edges([(0, 1, 3), (1, 2, 1), (2, 0, 9)])
+    assert (sp.min_wt(g), sp.max_wt(g)) == (1, 9)
+    p = tmp_path / "g.txt"
+    sp.write_edge_list(g, str(p))
+    g2 = sp.load_edge_list(str(p))
+    np.testing.assert_array_equal(g2.adj, g.adj)
+    np.testing.assert_array_equal(g2.weights, g.weights)
