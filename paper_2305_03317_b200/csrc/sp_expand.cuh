@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kExpandBlock) k_expand(
             if (push) qn[slot] = x;
         }
     }
-    scanned = warp_sum(scanned);
+    // `scanned` is warp-uniform (every lane added the same totals)
     if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);
 }
 
@@ -120,8 +120,7 @@ __global__ void __launch_bounds__(kExpandBlock) k_expand_chunks(
             if (push) qn[slot] = x;
         }
     }
-    scanned = warp_sum(scanned);
-    if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);
+    if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);  // warp-uniform
 }
 
 // Chunk buffer capacity for a graph with m slots.
