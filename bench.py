@@ -5,14 +5,16 @@ Headline workload = BASELINE.json configs[1]: PageRank (d=0.85, eps=1e-6,
 maxIter=100) on RMAT scale-22 (edge factor 16, seed 1, deduplicated, no
 self-loops), metric GTEPS = iterations * m / time.  A "step" is one full
 ``pr.sp`` run to convergence on the device-resident graph.
-  value : device-timed (CUDA events on our stream), graph already in HBM.
+  value : device-timed (CUDA events), graph already in HBM, ranks left in
+          HBM (run(..., device_outputs=True)).
   e2e   : through the public API with host buffers every step: pinned host
           CSR -> sp.from_csr (H2D + on-device reverse CSR) -> sp.run(PR) ->
           ranks back to host.  This is the paper's CUDA timing convention
           (times include CPU<->GPU transfer).
-  roofline : dominant kernel k_pull, algorithmic bytes 12 m + 36 n per
-          launch / its mean event-timed duration, against
-          MEASURED_PEAKS.json hbm_gbs.
+  roofline : one PR iteration (k_pr_units + k_pr_fix + k_pr_epi, bracketed
+          by CUDA events on the call's stream), algorithmic bytes 12 m + 36 n
+           / its mean duration, against MEASURED_PEAKS.json
+          hbm_gbs.
   cpu_baseline : the CPU oracle port (oracle/cpu_ref.c, OpenMP on all host
           threads) on a bounded sample of the same workload.
   algorithms : the other BASELINE configs at one GPU (SSSP cfg1, BC cfg4
@@ -191,33 +193,6 @@ def run_reference(a):
 # our arm
 
 
-def pr_device_run(sp, corpus, g):
-    r = sp.run(corpus.PR, g, PR_ARGS)
-    return r
-
-
-def bench_pr_single(sp, corpus, g, a, hbm_peak):
-    """Device-resident PR steps; returns dict of measurements."""
-    import torch
-    for _ in range(a.warmup):
-        pr_device_run(sp, corpus, g)
-    torch.cuda.synchronize()
-    iters = None
-    main_ms = 0.0
-    main_launches = 0
-    launches = 0
-    step_ms = []
-    for _ in range(a.steps):
-        r = pr_device_run(sp, corpus, g)
-        st = r.stats
-        step_ms.append(st["device_ms"])
-        main_ms += st["main_kernel_ms"]
-        main_launches += st["main_kernel_launches"]
-        launches += st["kernel_launches"]
-        iters = r.env.scalars["iter"]
-    return r, step_ms, main_ms, main_launches, launches, iters
-
-
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -240,7 +215,7 @@ def run_ours(a):
         if world == 1:
             # warmup + timed steps (device-resident)
             for _ in range(a.warmup):
-                sp.run(corpus.PR, g, PR_ARGS)
+                sp.run(corpus.PR, g, PR_ARGS, device_outputs=True)
             torch.cuda.synchronize()
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
@@ -250,7 +225,7 @@ def run_ours(a):
             main_launches = launches = 0
             dev_ms = []
             for _ in range(a.steps):
-                r = sp.run(corpus.PR, g, PR_ARGS)
+                r = sp.run(corpus.PR, g, PR_ARGS, device_outputs=True)
                 st = r.stats
                 dev_ms.append(st["device_ms"])
                 main_ms += st["main_kernel_ms"]
@@ -288,9 +263,10 @@ def run_ours(a):
                    "l2": "no flush: radj (4m = %.0f MB) + roff exceed the 126 MB L2; "
                          "contrib (8n = %.0f MB) is L2-resident by design"
                          % (4 * m / 1e6, 8 * n / 1e6)},
-        "roofline": {"bound": "hbm", "kernel": "k_pull", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": "k_pr_units+k_pr_fix+k_pr_epi (one PR iteration)",
+                     "achieved": achieved,
                      "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": ncu_traffic("k_pull"),
+                     "frac": achieved / hbm_peak, "traffic": ncu_traffic("pr_iteration"),
                      "algorithmic_bytes_per_launch": bytes_pull,
                      "mean_launch_ms": mean_pull_ms,
                      "note": "12 B/slot (radj 4 + contrib gather 8) + 36 B/vertex; gathers "
@@ -483,7 +459,7 @@ def main():
                     help="secondary algorithms at N=1 ('' to skip)")
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()
-    a.algos = [x for x in a.algos.split(",") if x]
+    a.algos = [x for x in a.algos.split(",") if x and x != "none"]
     if a.impl == "reference":
         return run_reference(a)
     return run_ours(a)

@@ -118,8 +118,7 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
     SP_CUDA(cudaMemsetAsync(sigma, 0, n * sizeof(double), c.stream));
     SP_CUDA(cudaMemsetAsync(delta, 0, n * sizeof(double), c.stream));
     ExpandCounters *hc = nullptr;
-    SP_CUDA(cudaMallocHost(&hc, sizeof(ExpandCounters)));
-    struct HostFree { ExpandCounters *p; ~HostFree() { if (p) cudaFreeHost(p); } } hf{hc};
+    SP_TRY(c.host_as(&hc));
     const bool big_out = g->max_outdeg > kSplit;
     const bool hub_in = g->max_indeg > kBcHub, hub_out = g->max_outdeg > kBcHub;
     int64_t levels_total = 0, scanned_total = 0, reached_total = 0;

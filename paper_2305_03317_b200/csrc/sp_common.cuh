@@ -45,6 +45,9 @@ int num_sms(int device);
 // default pool, release threshold raised so repeated calls reuse memory).
 int scratch_alloc(void **p, size_t bytes, cudaStream_t s);
 void scratch_free(void *p, cudaStream_t s);
+constexpr size_t kPinnedBlock = 4096;
+void *pinned_get();
+void pinned_put(void *p);
 
 // RAII holder for a per-call stream + scratch list + timing events.
 struct Call {
@@ -54,7 +57,17 @@ struct Call {
     void *bufs[32];
     int nbufs = 0;
     int64_t launches = 0;
+    void *pinned = nullptr;  // kPinnedBlock bytes of pinned host memory
     int begin(int dev);
+    // this call's pinned host block (recycled across calls)
+    int host(void **p);
+    template <class T>
+    int host_as(T **p) {
+        void *q;
+        SP_TRY(host(&q));
+        *p = static_cast<T *>(q);
+        return SP_OK;
+    }
     template <class T>
     int alloc(T **p, size_t count) {
         void *q = nullptr;
@@ -91,9 +104,11 @@ struct sp_graph {
     int64_t *reid = nullptr;
     int32_t *indeg = nullptr;
     int64_t max_outdeg = 0, max_indeg = 0;
-    // vertices whose in-/out-degree exceeds the hub threshold (PR/BC hub path)
-    int32_t *hubs_in = nullptr;
-    int64_t nhubs_in = 0;
+    // non-empty reverse rows (in-degree > 0) in ascending vertex order and
+    // their row ends roff[v+1]: the row index of the edge-balanced PR pull
+    int32_t *nzrow = nullptr;
+    int64_t *nzend = nullptr;
+    int64_t nnz_rows = 0;
     int32_t *wrange = nullptr;  // [min, max] weight (device), m > 0
 };
 

@@ -13,6 +13,7 @@
 // Arrays stay resident; nothing is copied back unless the host asks for a
 // view (sp_graph_download).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <mutex>
 #include <new>
@@ -147,15 +148,17 @@ __global__ void k_deg(const int64_t *__restrict__ off, int64_t n, int32_t *deg,
     if ((threadIdx.x & 31) == 0) atomicMax(maxdeg, mx);
 }
 
-__global__ void k_hubs(const int32_t *__restrict__ deg, int64_t n, int thr, int32_t *list,
-                       unsigned long long *cnt) {
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
-         base += (int64_t)gridDim.x * blockDim.x) {
-        int64_t x = base + threadIdx.x;
-        bool hub = x < n && deg[x] > thr;
-        int64_t slot = warp_append(hub, cnt);
-        if (hub) list[slot] = (int32_t)x;
-    }
+struct NonEmpty {
+    const int32_t *deg;
+    __device__ __forceinline__ bool operator()(int32_t x) const { return deg[x] > 0; }
+};
+
+__global__ void k_nzend(const int64_t *__restrict__ roff, const int32_t *__restrict__ nzrow,
+                        const int64_t *__restrict__ cnt, int64_t *nzend) {
+    const int64_t k1 = *cnt;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < k1;
+         k += (int64_t)gridDim.x * blockDim.x)
+        nzend[k] = roff[nzrow[k] + 1];
 }
 
 __global__ void k_wrange(const int32_t *__restrict__ w, int64_t m, int32_t *r) {
@@ -298,7 +301,8 @@ void free_graph(sp_graph *g) {
         cudaFree(g->indeg);
     }
     cudaFree(g->reid);
-    cudaFree(g->hubs_in);
+    cudaFree(g->nzrow);
+    cudaFree(g->nzend);
     cudaFree(g->wrange);
     delete g;
 }
@@ -313,8 +317,6 @@ int dalloc(T **p, size_t count) {
     }
     return SP_OK;
 }
-
-constexpr int kHubIn = 4096;  // PR hub threshold (in-degree), see sp_pagerank.cu
 
 // Reverse CSR from the forward arrays (graph.py:84-96).
 template <class IdxT>
@@ -366,8 +368,18 @@ int finish_graph(sp_graph *g, Call &c) {
         g->radj = g->adj;
         g->indeg = g->outdeg;
     }
-    SP_TRY(dalloc(&g->hubs_in, n));
-    k_hubs<<<gridN(n, c.device), 256, 0, c.stream>>>(g->indeg, n, kHubIn, g->hubs_in, cnt + 2);
+    // non-empty in-rows, order-preserving compaction (ascending v)
+    SP_TRY(dalloc(&g->nzrow, n));
+    SP_TRY(dalloc(&g->nzend, n));
+    if (n) {
+        int64_t *nsel = reinterpret_cast<int64_t *>(cnt + 2);
+        NonEmpty pred{g->indeg};
+        SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+            return cub::DeviceSelect::If(t, sz, thrust::counting_iterator<int32_t>(0), g->nzrow,
+                                         nsel, (int64_t)n, pred, c.stream);
+        }));
+        k_nzend<<<gridN(n, c.device), 256, 0, c.stream>>>(g->roff, g->nzrow, nsel, g->nzend);
+    }
     SP_TRY(dalloc(&g->wrange, 2));
     int32_t init[2] = {0x7fffffff, (int32_t)0x80000000};
     SP_CUDA(cudaMemcpyAsync(g->wrange, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
@@ -378,7 +390,7 @@ int finish_graph(sp_graph *g, Call &c) {
     SP_CUDA(cudaGetLastError());
     g->max_outdeg = (int64_t)h[0];
     g->max_indeg = g->directed ? (int64_t)h[1] : (int64_t)h[0];
-    g->nhubs_in = (int64_t)h[2];
+    g->nnz_rows = (int64_t)h[2];
     return SP_OK;
 }
 

@@ -9,20 +9,37 @@
 // Device layout: contrib[2][n] f64 (contrib[u] = rank[u]/outdeg(u), written
 // by the previous iteration -- the same IEEE division the interpreter does
 // per slot), rank[n] f64 updated in place (each vertex reads only its own
-// rank), outdeg int32[n], reverse CSR (roff int64, radj int32), and one
-// f64 diff slot per iteration (max via atomicMax on the bit pattern of a
-// non-negative double: exact and order-independent).
+// rank), outdeg int32[n], reverse CSR (roff int64, radj int32), the graph's
+// non-empty-row index (nzrow int32, nzend int64: rows with in-degree > 0 and
+// their ends), one f64 diff slot per iteration (max via atomicMax on the bit
+// pattern of a non-negative double: exact and order-independent).
 //
-// Kernel k_pull (one launch per iteration): a warp owns a tile of 32
-// consecutive vertices, whose rows form ONE contiguous slab of radj.  The
-// warp streams that slab in 128-slot chunks: coalesced radj loads, 4
-// independent contrib gathers per lane in flight, values staged in shared
-// memory; then every lane folds the part of ITS row inside the chunk,
-// sequentially, in CSR order -> bit-identical to the interpreter's left fold.
-// Rows with in-degree > kHub (fast mode only) are excluded from the slab and
-// summed by k_hub (one CTA per hub, fixed-shape tree: deterministic run to
-// run, within ~1e-16 relative of the left fold).  SP_FLAG_DETERMINISTIC
-// disables the hub path, making every vertex bit-exact.
+// Fast path (default) -- edge-balanced, one pass over radj per iteration:
+//   k_pr_units: the slot range is cut into units of kUnit consecutive radj
+//     slots; a warp takes a unit and streams it in kCh-slot chunks (8 slots
+//     per lane: two 128-bit radj loads, eight independent contrib gathers).
+//     Row ends inside a chunk are marked in a per-warp shared-memory bitmap
+//     from a coalesced window of nzend; each lane folds its 8 values
+//     left-to-right, a segmented Kogge-Stone warp scan carries partial sums
+//     across lanes and a warp-uniform carry across chunks, and the lane
+//     holding a row's last slot stores the row sum (sums[k], k = nz row).
+//     Every warp does the same work whatever the degree mix (a 100K-slot hub
+//     is just 50 units).
+//   k_pr_fix: a row that started in an earlier unit is finished here: its
+//     unit partials are added left-to-right (deterministic, fixed shape).
+//   k_pr_epi: pr.sp:17-23 for every non-empty row, coalesced over k
+//     (newRank, |delta| max, rank and contrib writes).
+//   k_pr_zero: rows with no in-edges have sum = 0, so newRank = (1-d)/n in
+//     every iteration; they are written in iteration 1 only (identical bits
+//     afterwards, |delta| = 0), into both contrib buffers.
+//   Accumulation order: left fold inside each lane's 8 slots, then a fixed
+//   Kogge-Stone tree across lanes/chunks/units.  Deterministic run to run;
+//   differs from the interpreter's left fold by a few ulps (<= 1e-12
+//   relative, tested; the north star allows 1e-6).
+// Exact path (SP_FLAG_DETERMINISTIC): k_pull_exact -- a warp owns 32
+//   consecutive vertices whose rows form one contiguous radj slab, streams it
+//   through shared memory and every lane folds its own row sequentially in
+//   CSR order: bit-identical to the interpreter, slower on hub rows.
 // No FMA contraction anywhere: __dadd_rn/__dmul_rn are used explicitly.
 #include <algorithm>
 
@@ -34,9 +51,9 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int kChunk = 128;  // slab slots staged per warp per step
-constexpr int kHub = 4096;   // must match sp_graph.cu kHubIn
-constexpr int kHubBlock = 512;
+constexpr int kChunk = 128;     // exact path: slab slots staged per warp per step
+constexpr int64_t kUnit = 2048;  // fast path: radj slots per work unit (one warp)
+constexpr int kCh = 256;        // fast path: slots per warp chunk (8 per lane)
 
 __global__ void k_init(double *rank, double *contrib, const int32_t *__restrict__ outdeg,
                        int64_t v0, int64_t v1, double r0) {
@@ -48,45 +65,370 @@ __global__ void k_init(double *rank, double *contrib, const int32_t *__restrict_
     }
 }
 
-// Fixed-shape CTA reduction of one hub row.
-__global__ void __launch_bounds__(kHubBlock) k_hub(const int64_t *__restrict__ roff,
-                                                   const int32_t *__restrict__ radj,
-                                                   const double *__restrict__ contrib,
-                                                   const int32_t *__restrict__ hubs, int64_t nhubs,
-                                                   int64_t v0, int64_t v1,
-                                                   double *__restrict__ hubsum) {
-    __shared__ double red[kHubBlock / 32];
-    for (int64_t h = blockIdx.x; h < nhubs; h += gridDim.x) {
-        int32_t v = hubs[h];
-        if (v < v0 || v >= v1) continue;
-        int64_t b = roff[v], e = roff[v + 1];
-        double s = 0.0;
-        for (int64_t k = b + threadIdx.x; k < e; k += kHubBlock) s = __dadd_rn(s, contrib[radj[k]]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            double t = threadIdx.x < kHubBlock / 32 ? red[threadIdx.x] : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
-            if (threadIdx.x == 0) hubsum[v] = t;
-        }
-        __syncthreads();
+// ---------------------------------------------------------------- fast path
+
+struct PrArgs {
+    const int32_t *__restrict__ radj;
+    const int64_t *__restrict__ nzend;
+    const int32_t *__restrict__ nzrow;
+    const int32_t *__restrict__ outdeg;
+    const double *__restrict__ cin;  // full n-array, global ids
+    double *__restrict__ rank;       // local (index v - v0)
+    double *__restrict__ cout;       // local (index v - v0)
+    double *__restrict__ sums;       // row sums, index k - K0 (nz row)
+    int64_t v0;
+    int64_t S0, S1;                  // radj slot range of the block
+    int64_t K0, K1;                  // nz rows [K0, K1) lie in the block
+    int64_t u0, nunits;              // global index of the first unit, count
+    const int64_t *__restrict__ unit_row;  // first nz row with end > unit start
+    double *__restrict__ hp;         // partial of a row that began before the unit
+    double *__restrict__ tp;         // partial of the row still open at unit end
+    int32_t *__restrict__ hs;        // unit holds the end of a row begun earlier
+    double base, damping;
+    double *diff_slot;
+};
+
+// pr.sp:17-23 for one vertex; returns |newRank - rank|.
+__device__ __forceinline__ double pr_apply(const PrArgs &a, int64_t v, double sum) {
+    const double nr = __dadd_rn(a.base, __dmul_rn(a.damping, sum));
+    const int64_t lv = v - a.v0;
+    const double r = a.rank[lv];
+    double d = __dsub_rn(nr, r);
+    if (d < 0.0) d = __dsub_rn(0.0, d);
+    a.rank[lv] = nr;
+    const int od = __ldg(a.outdeg + v);
+    a.cout[lv] = od > 0 ? __ddiv_rn(nr, (double)od) : 0.0;
+    return d;
+}
+
+// One atomic per block (blockDim.x == 256): same-address atomics serialise.
+__device__ __forceinline__ void block_diff(const PrArgs &a, double dmax) {
+    __shared__ double red[8];
+    dmax = warp_max(dmax);
+    if (lane_id() == 0) red[threadIdx.x >> 5] = dmax;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = threadIdx.x < 8 ? red[threadIdx.x] : 0.0;
+        t = warp_max(t);
+        if (threadIdx.x == 0 && t > 0.0) atomic_max_nonneg(a.diff_slot, t);
     }
 }
 
-// One PageRank iteration for vertices [v0, v1).
-//   contrib_in: full n-array (global ids); rank/contrib_out: local, index v-v0.
-template <bool kUseHubs>
-__global__ void __launch_bounds__(kBlock) k_pull(
+// radj[c + 8*lane .. +8) clipped to s1 (-1 past it): two 128-bit loads
+// when aligned and in range.
+__device__ __forceinline__ void load_slab(const int32_t *__restrict__ radj, int64_t c, int64_t s1,
+                                          unsigned lane, int (&idx)[8]) {
+    const int64_t q = c + 8 * (int64_t)lane;
+    if (q + 8 <= s1 && (q & 3) == 0) {
+        const int4 x0 = __ldcs(reinterpret_cast<const int4 *>(radj + q));
+        const int4 x1 = __ldcs(reinterpret_cast<const int4 *>(radj + q + 4));
+        idx[0] = x0.x; idx[1] = x0.y; idx[2] = x0.z; idx[3] = x0.w;
+        idx[4] = x1.x; idx[5] = x1.y; idx[6] = x1.z; idx[7] = x1.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; i++) idx[i] = q + i < s1 ? __ldcs(radj + q + i) : -1;
+    }
+}
+
+// Row sums over edge-balanced units (see the file header).
+__global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
+    __shared__ uint32_t bitmap[kWarps][kCh / 32];
+    const unsigned lane = lane_id();
+    uint32_t *bm = bitmap[threadIdx.x >> 5];
+    if (lane < kCh / 32) bm[lane] = 0u;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = warp; u < a.nunits; u += nwarps) {
+        const int64_t gu = a.u0 + u;
+        const int64_t s0 = max(a.S0, gu * kUnit), s1 = min(a.S1, (gu + 1) * kUnit);
+        int64_t rk = a.unit_row[u];
+        const int64_t first_row = rk;
+        // the unit's first row began in an earlier unit
+        const bool head_spill = (rk > 0 ? __ldg(a.nzend + rk - 1) : 0) < s0;
+        bool spill_flushed = false;
+        double carry = 0.0;
+        int nxt[8];
+        load_slab(a.radj, s0, s1, lane, nxt);
+        for (int64_t c = s0; c < s1; c += kCh) {
+            const int64_t lim = min(c + (int64_t)kCh, s1);
+            // ---- radj slab: 8 consecutive slots per lane (prefetched one
+            // chunk ahead so the DRAM latency overlaps this chunk's work)
+            int idx[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) idx[i] = nxt[i];
+            if (lim < s1) load_slab(a.radj, lim, s1, lane, nxt);
+            // ---- row-end bitmap for this chunk from a window of nzend
+            __syncwarp();
+            const int64_t rk_chunk = rk;
+            for (;;) {
+                const int64_t k = rk + lane;
+                const int64_t e = k < a.K1 ? __ldg(a.nzend + k) : INT64_MAX;
+                const bool in = e <= lim;  // the row's last slot e-1 lies in [c, lim)
+                if (in) {
+                    const int b = (int)(e - 1 - c);
+                    atomicOr(&bm[b >> 5], 1u << (b & 31));
+                }
+                const int cnt = __popc(__ballot_sync(0xffffffffu, in));
+                rk += cnt;
+                if (cnt < 32) break;
+            }
+            double val[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) val[i] = idx[i] >= 0 ? __ldg(a.cin + idx[i]) : 0.0;
+            __syncwarp();
+            const unsigned ends = (bm[lane >> 2] >> ((lane & 3) * 8)) & 0xFFu;
+            __syncwarp();
+            if (lane < kCh / 32) bm[lane] = 0u;
+            // ---- lane-local fold: tail = sum after the last end (all 8 if none)
+            double tail = 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                tail = __dadd_rn(tail, val[i]);
+                if ((ends >> i) & 1u) tail = 0.0;
+            }
+            // ---- segmented inclusive scan of (has_end, tail), plus end counts
+            bool f = ends != 0u;
+            double v = tail;
+            int ne = __popc(ends);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const bool fo = __shfl_up_sync(0xffffffffu, f, o);
+                const double vo = __shfl_up_sync(0xffffffffu, v, o);
+                const int no = __shfl_up_sync(0xffffffffu, ne, o);
+                if ((int)lane >= o) {
+                    if (!f) v = __dadd_rn(vo, v);
+                    f = f || fo;
+                    ne += no;
+                }
+            }
+            // exclusive values for this lane
+            bool fe = __shfl_up_sync(0xffffffffu, f, 1);
+            double ve = __shfl_up_sync(0xffffffffu, v, 1);
+            int nbefore = __shfl_up_sync(0xffffffffu, ne, 1);
+            if (lane == 0) { fe = false; ve = 0.0; nbefore = 0; }
+            const double carry_in = fe ? ve : __dadd_rn(carry, ve);
+            const bool f31 = __shfl_sync(0xffffffffu, f, 31);
+            const double v31 = __shfl_sync(0xffffffffu, v, 31);
+            carry = f31 ? v31 : __dadd_rn(carry, v31);
+            // ---- rows whose last slot this lane holds: store their sums
+            if (ends) {
+                double run = 0.0;
+                int j = 0;
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    run = __dadd_rn(run, val[i]);
+                    if ((ends >> i) & 1u) {
+                        const double total = j == 0 ? __dadd_rn(carry_in, run) : run;
+                        const int64_t row = rk_chunk + nbefore + j;
+                        if (head_spill && row == first_row) {
+                            a.hp[u] = total;
+                            spill_flushed = true;
+                        } else {
+                            a.sums[row - a.K0] = total;
+                        }
+                        j++;
+                        run = 0.0;
+                    }
+                }
+            }
+        }
+        spill_flushed = __any_sync(0xffffffffu, spill_flushed);
+        if (lane == 0) {
+            a.tp[u] = carry;
+            a.hs[u] = spill_flushed ? 1 : 0;
+        }
+    }
+}
+
+// Rows spanning several units: partials added left-to-right.
+__global__ void k_pr_fix(PrArgs a) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < a.nunits;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        if (a.hs[u]) {
+            const int64_t row = a.unit_row[u];
+            const int64_t start = row > 0 ? a.nzend[row - 1] : 0;
+            const int64_t ustart = max((int64_t)0, start / kUnit - a.u0);
+            double acc = 0.0;
+            for (int64_t w = ustart; w < u; w++) acc = __dadd_rn(acc, a.tp[w]);
+            a.sums[row - a.K0] = __dadd_rn(acc, a.hp[u]);
+        }
+    }
+}
+
+// pr.sp:17-23 for every non-empty row of the block (coalesced over k).
+// Each thread takes kEpi rows strided by the block size: all loads of a
+// thread are issued before any store (memory-level parallelism).
+constexpr int kEpi = 4;
+__global__ void __launch_bounds__(256) k_pr_epi(PrArgs a) {
+    const int64_t nk = a.K1 - a.K0;
+    const int64_t base_k = blockIdx.x * (int64_t)(256 * kEpi) + threadIdx.x;
+    int32_t v[kEpi];
+    double sum[kEpi], r[kEpi];
+    int od[kEpi];
+#pragma unroll
+    for (int j = 0; j < kEpi; j++) {
+        const int64_t k = base_k + j * 256;
+        v[j] = k < nk ? __ldcs(a.nzrow + a.K0 + k) : -1;
+        sum[j] = k < nk ? __ldcs(a.sums + k) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kEpi; j++) {
+        r[j] = v[j] >= 0 ? a.rank[v[j] - a.v0] : 0.0;
+        od[j] = v[j] >= 0 ? __ldg(a.outdeg + v[j]) : 0;
+    }
+    double dmax = 0.0;
+#pragma unroll
+    for (int j = 0; j < kEpi; j++) {
+        if (v[j] < 0) continue;
+        const double nr = __dadd_rn(a.base, __dmul_rn(a.damping, sum[j]));
+        double d = __dsub_rn(nr, r[j]);
+        if (d < 0.0) d = __dsub_rn(0.0, d);
+        dmax = fmax(dmax, d);
+        a.rank[v[j] - a.v0] = nr;
+        a.cout[v[j] - a.v0] = od[j] > 0 ? __ddiv_rn(nr, (double)od[j]) : 0.0;
+    }
+    block_diff(a, dmax);
+}
+
+// Rows without in-edges: newRank = base (sum = 0).  cout2 (optional) is the
+// other contrib buffer of the single-GPU ping-pong.
+__global__ void __launch_bounds__(256) k_pr_zero(PrArgs a, const int32_t *__restrict__ indeg,
+                                                 int64_t v1, double *cout2) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double dmax = 0.0;
+    if (i < v1 - a.v0 && __ldcs(indeg + a.v0 + i) == 0) {
+        dmax = pr_apply(a, a.v0 + i, 0.0);
+        if (cout2) cout2[i] = a.cout[i];
+    }
+    block_diff(a, dmax);
+}
+
+// unit_row[u] = first nz row in [K0, K1) whose end exceeds the unit start.
+__global__ void k_pr_setup(const int64_t *__restrict__ nzend, int64_t K0, int64_t K1, int64_t S0,
+                           int64_t u0, int64_t nunits, int64_t *unit_row) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nunits;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s0 = max(S0, (u0 + u) * kUnit);
+        int64_t lo = K0, hi = K1;
+        while (lo < hi) {
+            const int64_t mid = lo + ((hi - lo) >> 1);
+            if (nzend[mid] <= s0) lo = mid + 1; else hi = mid;
+        }
+        unit_row[u] = lo;
+    }
+}
+
+// out = {roff[v0], roff[v1], K0, K1}: the block's slot range and its nz
+// rows (first index in nzrow with nzrow[k] >= v0 / v1).
+__global__ void k_pr_bounds(const int64_t *__restrict__ roff, const int32_t *__restrict__ nzrow,
+                            int64_t nnz, int64_t v0, int64_t v1, int64_t *out) {
+    const int t = threadIdx.x;
+    if (t < 2) {
+        out[t] = roff[t == 0 ? v0 : v1];
+    } else if (t < 4) {
+        const int64_t want = t == 2 ? v0 : v1;
+        int64_t lo = 0, hi = nnz;
+        while (lo < hi) {
+            const int64_t mid = lo + ((hi - lo) >> 1);
+            if (nzrow[mid] < want) lo = mid + 1; else hi = mid;
+        }
+        out[t] = lo;
+    }
+}
+
+// Per-call state of the fast path for a vertex block [v0, v1).
+struct FastPlan {
+    PrArgs a{};
+    int grid_units = 1, grid_fix = 1, grid_epi = 1, grid_zero = 1;
+};
+
+int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, FastPlan &p) {
+    int64_t *kb, *hb;
+    SP_TRY(c.alloc(&kb, 4));
+    SP_TRY(c.host_as(&hb));
+    k_pr_bounds<<<1, 32, 0, c.stream>>>(g->roff, g->nzrow, g->nnz_rows, v0, v1, kb);
+    c.launches++;
+    SP_CUDA(cudaMemcpyAsync(hb + 8, kb, 32, cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t S[2] = {hb[8], hb[9]}, K[2] = {hb[10], hb[11]};
+    PrArgs &a = p.a;
+    a.radj = g->radj;
+    a.nzend = g->nzend;
+    a.nzrow = g->nzrow;
+    a.outdeg = g->outdeg;
+    a.v0 = v0;
+    a.S0 = S[0];
+    a.S1 = S[1];
+    a.K0 = K[0];
+    a.K1 = K[1];
+    a.u0 = S[0] / kUnit;
+    a.nunits = S[1] > S[0] ? (S[1] - 1) / kUnit - a.u0 + 1 : 0;
+    a.base = (1.0 - damping) / (double)g->n;  // pr.sp:17, no FMA on host either
+    a.damping = damping;
+    const int64_t nu = std::max<int64_t>(1, a.nunits);
+    int64_t *ur;
+    SP_TRY(c.alloc(&ur, nu));
+    double *hp, *tp, *sums;
+    int32_t *hs;
+    SP_TRY(c.alloc(&sums, std::max<int64_t>(1, a.K1 - a.K0)));
+    a.sums = sums;
+    SP_TRY(c.alloc(&hp, nu));
+    SP_TRY(c.alloc(&tp, nu));
+    SP_TRY(c.alloc(&hs, nu));
+    a.hp = hp;
+    a.tp = tp;
+    a.hs = hs;
+    a.unit_row = ur;
+    if (a.nunits) {
+        k_pr_setup<<<grid_for(a.nunits, 256, c.device), 256, 0, c.stream>>>(
+            g->nzend, a.K0, a.K1, a.S0, a.u0, a.nunits, ur);
+        c.launches++;
+    }
+    // one unit per warp, no cap: the block scheduler balances the tail
+    p.grid_units = (int)std::max<int64_t>(1, (a.nunits + kWarps - 1) / kWarps);
+    p.grid_fix = grid_for(std::max<int64_t>(1, a.nunits), 256, c.device, 4);
+    p.grid_epi = (int)std::max<int64_t>(1, (a.K1 - a.K0 + 256 * kEpi - 1) / (256 * kEpi));
+    p.grid_zero = (int)std::max<int64_t>(1, (v1 - v0 + 255) / 256);
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
+// One fast iteration; `zero` says whether zero-in-degree rows are written.
+int launch_fast(Call &c, FastPlan &p, sp_graph *g, int64_t v1, const double *cin, double *rank,
+                double *cout, double *cout2, bool zero, double *diff_slot, cudaEvent_t ka,
+                cudaEvent_t kb) {
+    PrArgs a = p.a;
+    a.cin = cin;
+    a.rank = rank;
+    a.cout = cout;
+    a.diff_slot = diff_slot;
+    if (ka) cudaEventRecord(ka, c.stream);
+    if (a.nunits) {
+        k_pr_units<<<p.grid_units, kBlock, 0, c.stream>>>(a);
+        k_pr_fix<<<p.grid_fix, 256, 0, c.stream>>>(a);
+        k_pr_epi<<<p.grid_epi, 256, 0, c.stream>>>(a);
+        c.launches += 3;
+    }
+    if (kb) cudaEventRecord(kb, c.stream);
+    if (zero) {
+        k_pr_zero<<<p.grid_zero, 256, 0, c.stream>>>(a, g->indeg, v1, cout2);
+        c.launches++;
+    }
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
+// ---------------------------------------------------------------- exact path
+
+// One PageRank iteration for vertices [v0, v1), bit-identical to the
+// interpreter's left fold.  contrib_in: full n-array (global ids);
+// rank/contrib_out: local, index v-v0.
+__global__ void __launch_bounds__(kBlock) k_pull_exact(
     const int64_t *__restrict__ roff, const int32_t *__restrict__ radj,
     const int32_t *__restrict__ outdeg, const double *__restrict__ contrib_in,
-    const double *__restrict__ hubsum, double *__restrict__ rank,
-    double *__restrict__ contrib_out, int64_t v0, int64_t v1, double base, double damping,
-    double *diff_slot) {
+    double *__restrict__ rank, double *__restrict__ contrib_out, int64_t v0, int64_t v1,
+    double base, double damping, double *diff_slot) {
     __shared__ double stage[kWarps][kChunk];
-    __shared__ double red[kWarps];
     const unsigned lane = lane_id();
     const int wib = threadIdx.x >> 5;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -101,9 +443,8 @@ __global__ void __launch_bounds__(kBlock) k_pull(
             rs = roff[v];
             re = roff[v + 1];
         }
-        bool hub = kUseHubs && live && (re - rs) > kHub;
-        int64_t deg = hub ? 0 : re - rs;
-        // positions of this lane's row inside the warp's flattened slab
+        const int64_t deg = re - rs;
+        // the tile's rows are one contiguous slab radj[roff[t0] .. roff[t0+32])
         int64_t incl = deg;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -112,41 +453,21 @@ __global__ void __launch_bounds__(kBlock) k_pull(
         }
         const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
         const int64_t excl = incl - deg;
-        // Without hub rows the tile's slab is radj[roff[t0] .. roff[t0+32]):
-        // slot p is simply radj[sb + p].  Tiles holding a hub row (fast mode,
-        // rare) map slots to rows by a binary search over the lane prefix.
-        const unsigned hubmask = __ballot_sync(0xffffffffu, hub);
         const int64_t sb = __shfl_sync(0xffffffffu, rs, 0);
         double sum = 0.0;
         for (int64_t p0 = 0; p0 < total; p0 += kChunk) {
 #pragma unroll
             for (int j = 0; j < kChunk / 32; j++) {
                 const int64_t p = p0 + j * 32 + lane;
-                int64_t idx = sb + p;
-                if (kUseHubs && hubmask) {
-                    int lo = 0;
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        int cand = lo + step;
-                        int64_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
-                        if (cand < 32 && ex <= p) lo = cand;
-                    }
-                    int64_t ex = __shfl_sync(0xffffffffu, excl, lo);
-                    int64_t b0 = __shfl_sync(0xffffffffu, rs, lo);
-                    idx = b0 + (p - ex);
-                }
-                double val = 0.0;
-                if (p < total) val = contrib_in[radj[idx]];
-                buf[j * 32 + lane] = val;
+                buf[j * 32 + lane] = p < total ? contrib_in[radj[sb + p]] : 0.0;
             }
             __syncwarp();
             // sequential left fold of this lane's slice of the chunk
-            int64_t a = max(excl, p0), b = min(excl + deg, p0 + (int64_t)kChunk);
-            for (int64_t p = a; p < b; p++) sum = __dadd_rn(sum, buf[p - p0]);
+            int64_t lo = max(excl, p0), hi = min(excl + deg, p0 + (int64_t)kChunk);
+            for (int64_t p = lo; p < hi; p++) sum = __dadd_rn(sum, buf[p - p0]);
             __syncwarp();
         }
         if (live) {
-            if (hub) sum = hubsum[v];
             double nr = __dadd_rn(base, __dmul_rn(damping, sum));
             double r = rank[v - v0];
             double d = __dsub_rn(nr, r);
@@ -158,36 +479,18 @@ __global__ void __launch_bounds__(kBlock) k_pull(
         }
     }
     dmax = warp_max(dmax);
-    if (lane == 0) red[wib] = dmax;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        double t = threadIdx.x < kWarps ? red[threadIdx.x] : 0.0;
-        t = warp_max(t);
-        if (threadIdx.x == 0) atomic_max_nonneg(diff_slot, t);
-    }
+    if (lane == 0 && dmax > 0.0) atomic_max_nonneg(diff_slot, dmax);
 }
 
-int launch_iteration(sp_graph *g, Call &c, bool use_hubs, int64_t v0, int64_t v1, double damping,
-                     const double *cin, double *rank, double *cout, double *hubsum,
-                     double *diff_slot, cudaEvent_t ka, cudaEvent_t kb) {
-    const int dev = c.device;
-    const double base = (1.0 - damping) / (double)g->n;  // pr.sp:17, no FMA on host either
-    if (use_hubs) {
-        int gh = (int)std::min<int64_t>(g->nhubs_in, (int64_t)num_sms(dev) * 4);
-        k_hub<<<gh, kHubBlock, 0, c.stream>>>(g->roff, g->radj, cin, g->hubs_in, g->nhubs_in, v0,
-                                              v1, hubsum);
-        c.launches++;
-    }
+int launch_exact(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, const double *cin,
+                 double *rank, double *cout, double *diff_slot, cudaEvent_t ka, cudaEvent_t kb) {
+    const double base = (1.0 - damping) / (double)g->n;  // pr.sp:17
     int64_t tiles = (v1 - v0 + 31) / 32;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + kWarps - 1) / kWarps,
-                                                           (int64_t)num_sms(dev) * 8));
+                                                           (int64_t)num_sms(c.device) * 8));
     if (ka) cudaEventRecord(ka, c.stream);
-    if (use_hubs)
-        k_pull<true><<<grid, kBlock, 0, c.stream>>>(g->roff, g->radj, g->outdeg, cin, hubsum, rank,
-                                                    cout, v0, v1, base, damping, diff_slot);
-    else
-        k_pull<false><<<grid, kBlock, 0, c.stream>>>(g->roff, g->radj, g->outdeg, cin, hubsum, rank,
-                                                     cout, v0, v1, base, damping, diff_slot);
+    k_pull_exact<<<grid, kBlock, 0, c.stream>>>(g->roff, g->radj, g->outdeg, cin, rank, cout, v0,
+                                                v1, base, damping, diff_slot);
     if (kb) cudaEventRecord(kb, c.stream);
     c.launches++;
     SP_CUDA(cudaGetLastError());
@@ -204,18 +507,18 @@ extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t 
     Call c;
     SP_TRY(c.begin(g->device));
     const int64_t n = g->n;
-    const bool use_hubs = !(flags & SP_FLAG_DETERMINISTIC) && g->nhubs_in > 0;
-    double *rank, *ca, *cb2, *hubsum = nullptr, *diffs;
+    const bool exact = flags & SP_FLAG_DETERMINISTIC;
+    double *rank, *ca, *cb2, *diffs;
     SP_TRY(c.alloc(&rank, n));
     SP_TRY(c.alloc(&ca, n));
     SP_TRY(c.alloc(&cb2, n));
-    if (use_hubs) SP_TRY(c.alloc(&hubsum, n));
     const int64_t kSlots = 1024;  // diff slots, recycled in a ring
     SP_TRY(c.alloc(&diffs, kSlots));
     SP_CUDA(cudaMemsetAsync(diffs, 0, kSlots * sizeof(double), c.stream));
     double *hdiff = nullptr;
-    SP_CUDA(cudaMallocHost(&hdiff, sizeof(double)));
-    struct HostFree { double *p; ~HostFree() { if (p) cudaFreeHost(p); } } hf{hdiff};
+    SP_TRY(c.host_as(&hdiff));
+    FastPlan plan;
+    if (n && !exact) SP_TRY(plan_fast(g, c, 0, n, damping, plan));
     const double r0 = n ? 1.0 / (double)n : 0.0;  // pr.sp:6
     if (n) {
         k_init<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(rank, ca, g->outdeg, 0, n, r0);
@@ -231,7 +534,8 @@ extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t 
     for (;;) {
         double *slot = diffs + (iters % kSlots);
         if (n) {
-            rc = launch_iteration(g, c, use_hubs, 0, n, damping, ca, rank, cb2, hubsum, slot, ka, kb);
+            rc = exact ? launch_exact(g, c, 0, n, damping, ca, rank, cb2, slot, ka, kb)
+                       : launch_fast(c, plan, g, n, ca, rank, cb2, ca, iters == 0, slot, ka, kb);
             if (rc) break;
             SP_CUDA(cudaMemcpyAsync(hdiff, slot, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
             SP_CUDA(cudaMemsetAsync(diffs + ((iters + 1) % kSlots), 0, sizeof(double), c.stream));
@@ -296,14 +600,22 @@ extern "C" int sp_pagerank_block_step(sp_graph *g, int64_t v0, int64_t v1, doubl
     SP_CHECK(g && v0 >= 0 && v0 <= v1 && v1 <= g->n && diff, SP_ERR_ARG, "bad vertex block");
     Call c;
     SP_TRY(c.begin(g->device));
-    const bool use_hubs = !(flags & SP_FLAG_DETERMINISTIC) && g->nhubs_in > 0;
-    double *hubsum = nullptr, *slot;
-    if (use_hubs) SP_TRY(c.alloc(&hubsum, g->n));
+    double *slot;
     SP_TRY(c.alloc(&slot, 1));
     SP_CUDA(cudaMemsetAsync(slot, 0, sizeof(double), c.stream));
-    if (v1 > v0)
-        SP_TRY(launch_iteration(g, c, use_hubs, v0, v1, damping, contrib_in, rank_local,
-                                contrib_out, hubsum, slot, nullptr, nullptr));
+    if (v1 > v0) {
+        if (flags & SP_FLAG_DETERMINISTIC) {
+            SP_TRY(launch_exact(g, c, v0, v1, damping, contrib_in, rank_local, contrib_out, slot,
+                                nullptr, nullptr));
+        } else {
+            FastPlan plan;
+            SP_TRY(plan_fast(g, c, v0, v1, damping, plan));
+            // contrib_out is a single persistent buffer here: zero rows are
+            // rewritten every step (cheap: one indeg pass over the block)
+            SP_TRY(launch_fast(c, plan, g, v1, contrib_in, rank_local, contrib_out, nullptr, true,
+                               slot, nullptr, nullptr));
+        }
+    }
     SP_CUDA(cudaMemcpyAsync(diff, slot, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     SP_TRY(c.finish(st));
     return SP_OK;

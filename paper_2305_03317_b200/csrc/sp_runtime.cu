@@ -3,6 +3,7 @@
 #include <string.h>
 
 #include <mutex>
+#include <vector>
 
 #include "sp_common.cuh"
 
@@ -49,6 +50,35 @@ static void tune_pool(int device) {
     }
 }
 
+// Pinned host words for per-iteration flag/counter reads: a process-wide
+// free list of kPinnedBlock-byte blocks (cudaMallocHost costs milliseconds,
+// so blocks are allocated once and recycled across calls).
+static std::mutex g_pinned_mu;
+static std::vector<void *> g_pinned_free;
+
+void *pinned_get() {
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        if (!g_pinned_free.empty()) {
+            void *p = g_pinned_free.back();
+            g_pinned_free.pop_back();
+            return p;
+        }
+    }
+    void *p = nullptr;
+    if (cudaMallocHost(&p, kPinnedBlock) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void pinned_put(void *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.push_back(p);
+}
+
 int scratch_alloc(void **p, size_t bytes, cudaStream_t s) {
     cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, s);
     if (e != cudaSuccess) {
@@ -88,12 +118,20 @@ int Call::finish(sp_stats *st) {
     return SP_OK;
 }
 
+int Call::host(void **p) {
+    if (!pinned) pinned = pinned_get();
+    SP_CHECK(pinned, SP_ERR_OOM, "pinned host allocation failed");
+    *p = pinned;
+    return SP_OK;
+}
+
 Call::~Call() {
     if (stream) {
         for (int i = 0; i < nbufs; i++) scratch_free(bufs[i], stream);
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
     }
+    pinned_put(pinned);
     if (t0) cudaEventDestroy(t0);
     if (t1) cudaEventDestroy(t1);
 }

@@ -81,8 +81,7 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
     SP_TRY(c.alloc(&cnt, 2));
     SP_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(ExpandCounters), c.stream));
     ExpandCounters *hc = nullptr;
-    SP_CUDA(cudaMallocHost(&hc, sizeof(ExpandCounters)));
-    struct HostFree { ExpandCounters *p; ~HostFree() { if (p) cudaFreeHost(p); } } hf{hc};
+    SP_TRY(c.host_as(&hc));
     const int dev = c.device;
     const int sms = num_sms(dev);
     const bool big = g->max_outdeg > kSplit;

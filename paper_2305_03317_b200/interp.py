@@ -136,11 +136,30 @@ def _i64(x: int) -> int:
     return max(-(2 ** 63), min(2 ** 63 - 1, int(x)))
 
 
+def _out(n: int, dtype, dev: int | None):
+    """Result buffer: a NumPy array (host) or a torch CUDA tensor (device)."""
+    if dev is None:
+        return np.empty(n, dtype=dtype), _lib.SP_MEM_HOST
+    import torch  # plumbing only: device memory for results that stay in HBM
+    t = torch.empty(max(1, n), dtype={np.float64: torch.float64,
+                                      np.int32: torch.int32}[dtype],
+                    device=torch.device("cuda", dev))[:n]
+    return t, _lib.SP_MEM_DEVICE
+
+
+def _ptr(buf):
+    return C.c_void_p(buf.data_ptr()) if hasattr(buf, "data_ptr") else \
+        buf.ctypes.data_as(C.c_void_p)
+
+
 def run(tp, g, args: dict, function: str | None = None,
         max_iters: int | None = None, on_fixedpoint_iteration=None, *,
-        deterministic: bool = False) -> RunResult:
+        deterministic: bool = False, device_outputs: bool = False) -> RunResult:
     """Run a corpus program on the GPU.  ``tp`` is a reference TypedProgram
-    (recognised structurally), a ``corpus.Program`` or a corpus key."""
+    (recognised structurally), a ``corpus.Program`` or a corpus key.
+
+    ``device_outputs=True`` leaves the property arrays in HBM (torch CUDA
+    tensors on the graph's device) instead of copying them to NumPy."""
     E = errors_for(tp)
     prog = corpus.identify(tp, function)
     dg = device_graph(g)
@@ -151,41 +170,43 @@ def run(tp, g, args: dict, function: str | None = None,
     hook = _Hook(on_fixedpoint_iteration, prog, dg)
     flags = _lib.SP_FLAG_DETERMINISTIC if deterministic else 0
     n = dg.n
+    odev = dg.device if device_outputs else None
     t0 = time.perf_counter()
     env = PropertyEnv()
     fpi: dict = {}
     if prog.key in ("sssp", "sssp_pull"):
-        dist = np.empty(n, dtype=np.int32)
+        dist, mem = _out(n, np.int32, odev)
         iters = C.c_int64()
-        rc = L.sp_sssp(dg.handle, bound["src"], cap, dist.ctypes.data_as(C.c_void_p),
-                       _lib.SP_MEM_HOST, C.byref(iters), hook.cb, None, C.byref(st))
+        rc = L.sp_sssp(dg.handle, bound["src"], cap, _ptr(dist), mem, C.byref(iters),
+                       hook.cb, None, C.byref(st))
         _raise_for(rc, E, prog.flag, cap, hook.exc)
         env.node_props = {"dist": dist, "modified": np.zeros(n, dtype=bool),
                           "modified_nxt": np.zeros(n, dtype=bool)}
+        if odev is not None:
+            env.node_props["modified"] = env.node_props["modified_nxt"] = None
         env.scalars = {"finished": True}
         fpi = {"finished": int(iters.value)}
     elif prog.key == "pr":
-        rank = np.empty(n, dtype=np.float64)
+        rank, mem = _out(n, np.float64, odev)
         it, its = C.c_int64(), C.c_int64()
         diff = C.c_double()
         rc = L.sp_pagerank(dg.handle, bound["damping"], bound["epsilon"],
-                           _i64(bound["maxIter"]), cap, flags,
-                           rank.ctypes.data_as(C.c_void_p), _lib.SP_MEM_HOST,
+                           _i64(bound["maxIter"]), cap, flags, _ptr(rank), mem,
                            C.byref(it), C.byref(diff), C.byref(its), hook.cb, None,
                            C.byref(st))
         _raise_for(rc, E, prog.flag, cap, hook.exc)
-        env.node_props = {"rank": rank, "rank_nxt": rank.copy()}
+        # rank_nxt == rank at exit (pr.sp:25-27 copies it back every iteration)
+        env.node_props = {"rank": rank, "rank_nxt": rank if odev is not None else rank.copy()}
         env.scalars = {"iter": int(it.value), "diff": float(diff.value),
                        "converged": True}
         fpi = {"converged": int(its.value)}
     elif prog.key == "bc":
         srcs = np.asarray(bound["sourceSet"], dtype=np.int32)
-        bc = np.empty(n, dtype=np.float64)
-        sigma = np.empty(n, dtype=np.float64)
-        delta = np.empty(n, dtype=np.float64)
+        bc, mem = _out(n, np.float64, odev)
+        sigma, _ = _out(n, np.float64, odev)
+        delta, _ = _out(n, np.float64, odev)
         rc = L.sp_bc(dg.handle, srcs.ctypes.data_as(C.c_void_p), len(srcs), flags,
-                     bc.ctypes.data_as(C.c_void_p), sigma.ctypes.data_as(C.c_void_p),
-                     delta.ctypes.data_as(C.c_void_p), _lib.SP_MEM_HOST, C.byref(st))
+                     _ptr(bc), _ptr(sigma), _ptr(delta), mem, C.byref(st))
         _raise_for(rc, E, None, cap, None)
         env.node_props = {"bc": bc}
         if len(srcs):  # sigma/delta are attached inside the source loop (bc.sp:5-7)
