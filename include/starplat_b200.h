@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 1
+#define SP_ABI_VERSION 2
 
 enum sp_status {
     SP_OK = 0,
@@ -71,6 +71,7 @@ typedef struct sp_stats {
     double device_ms;          /* device time of the call (CUDA events)       */
     double main_kernel_ms;     /* summed device time of the dominant kernel   */
     int64_t main_kernel_launches;
+    int64_t model_bytes;       /* algorithmic bytes of the call per SURVEY 8d (0 = n/a) */
 } sp_stats;
 
 /* fixedPoint iteration callback, mirrors interp.py:138,411-412
@@ -143,8 +144,12 @@ int sp_pagerank_block_init(sp_graph *g, int64_t v0, int64_t v1,
 int sp_bc(sp_graph *g, const int32_t *srcs, int64_t nsrc, unsigned flags,
           double *bc, double *sigma, double *delta, int mem, sp_stats *st);
 
-/* corpus/programs/tc.sp restricted to middle vertices v in [v0, v1)
- * (v0 = 0, v1 = n for the whole program); exact, with multiplicity. */
+/* corpus/programs/tc.sp (tc.sp:3-13); exact, with multiplicity: every
+ * triangle a-b-c contributes m_ab * m_bc * m_ac (slot multiplicities).
+ * [v0, v1) selects a share of the triangles for sharded runs, so that the
+ * shares of any partition of [0, n) sum to the whole count: undirected
+ * graphs -- triangles whose lowest-ranked vertex (rank = (degree, id)) lies
+ * in [v0, v1); directed graphs -- the program's middle vertex v in [v0, v1). */
 int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_stats *st);
 
 #ifdef __cplusplus

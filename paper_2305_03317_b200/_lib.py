@@ -16,6 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libstarplat_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "starplat_b200.h")
 
+ABI_VERSION = 2  # must equal SP_ABI_VERSION in include/starplat_b200.h
+
 SP_OK = 0
 SP_ERR_ARG = -1
 SP_ERR_NONCONV = -2
@@ -41,7 +43,8 @@ class Stats(C.Structure):
                 ("kernel_launches", C.c_int64),
                 ("device_ms", C.c_double),
                 ("main_kernel_ms", C.c_double),
-                ("main_kernel_launches", C.c_int64)]
+                ("main_kernel_launches", C.c_int64),
+                ("model_bytes", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -97,6 +100,10 @@ def lib():
                     f"{LIB_PATH} not built; run `make -C {HERE}/csrc` "
                     "(no CPU fallback exists)")
             L = C.CDLL(LIB_PATH)
+            L.sp_abi_version.restype = C.c_int
+            if L.sp_abi_version() != ABI_VERSION:
+                raise LibraryMissing(
+                    f"{LIB_PATH} has ABI {L.sp_abi_version()}, expected {ABI_VERSION}; rebuild it")
             for name, (res, args) in SIGNATURES.items():
                 f = getattr(L, name)
                 f.restype = res

@@ -110,6 +110,17 @@ struct sp_graph {
     int64_t *nzend = nullptr;
     int64_t nnz_rows = 0;
     int32_t *wrange = nullptr;  // [min, max] weight (device), m > 0
+    // degree-ordered upper CSR for triangle counting (undirected graphs),
+    // built lazily by the first sp_tc call: row v holds the neighbours x of v
+    // with (deg x, x) > (deg v, v), ascending, duplicates kept, starting at
+    // slot 8*ustart8[v] (rows padded to 32 bytes with -1), ulen[v] entries;
+    // uinfo[e] = (ustart8[x], ulen[x]) of the row slot e points to
+    uint32_t *ustart8 = nullptr;
+    int32_t *ulen = nullptr;
+    int32_t *uadj = nullptr;
+    uint2 *uinfo = nullptr;
+    int64_t m_up = -1;      // real upper slots; -1: not built
+    int64_t m_up_pad = 0;   // padded slots
 };
 
 // ---- device helpers --------------------------------------------------------

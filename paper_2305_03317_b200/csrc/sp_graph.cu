@@ -303,6 +303,10 @@ void free_graph(sp_graph *g) {
     cudaFree(g->reid);
     cudaFree(g->nzrow);
     cudaFree(g->nzend);
+    cudaFree(g->ustart8);
+    cudaFree(g->ulen);
+    cudaFree(g->uadj);
+    cudaFree(g->uinfo);
     cudaFree(g->wrange);
     delete g;
 }

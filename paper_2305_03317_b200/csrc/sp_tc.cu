@@ -2,21 +2,42 @@
 //
 // Reference semantics (tc.sp:3-13 under trident/interp.py): for every v, every
 // slot u < v of N(v), every slot w > v of N(v), add the multiplicity of w in
-// N(u).  Rows are sorted (graph.py:77), so per (v, u) the inner loops are a
-// multiset dot product of A = N(v)_{>v} (a suffix of row v) and
-// B = N(u)_{>v} (a suffix of row u).  Integer arithmetic: exact, any order.
+// N(u).  Integer arithmetic: exact in any order.  For a triangle a < b < c
+// with slot multiplicities m_ab, m_bc, m_ac the program adds m_ab*m_bc*m_ac
+// exactly once (v = b, u = a, w = c); self-loops never take part (u < v < w).
 //
-// Kernel k_tc: persistent warps pull 32-vertex batches from a global counter.
-// Per v the warp loads row v once (coalesced), stages A in shared memory (up
-// to kA entries) with a 2048-bit membership filter, and hands each slot u < v
-// to one lane.  A lane walks B = row u with independent 128-bit loads when B
-// is short, or binary-searches the start of B when row u is long; each
-// element x > v costs one shared-memory filter probe and, on a hit, a binary
-// search in A for its multiplicity.  When B is far longer than A (a hub u)
-// the lane instead walks A and binary-searches B in global memory.  Rows of
-// v whose suffix exceeds kA search A in global memory (L2-resident).
-// Counts: per-lane uint64 -> warp sum -> one atomicAdd per warp.
+// Undirected graphs (mirror slots: mult(b in N(a)) == mult(a in N(b))): that
+// product is symmetric in the three vertices, so any total order of the
+// vertices counts the same triangles with the same weights.  The backend
+// orients every edge from the lower to the higher rank, rank(v) = (degree v,
+// v), which bounds every out-row by sqrt(2m) whatever the skew:
+//   upper CSR  (ustart8, ulen, uadj): row a = the neighbours x of a with
+//              rank(x) > rank(a), ascending id, duplicates kept, each row
+//              padded to whole 32-byte sectors; uinfo[e] = (row start, row
+//              length) of the vertex slot e points to, so a row is found
+//              without a dependent random offset load; built once per graph
+//              on the device (count -> scan -> fill -> info) and cached;
+//   count    = sum over slots b of N+(a), over slots x of N+(b), of
+//              mult(x in N+(a))  (= m_ab * m_bc * m_ac summed per triangle).
+// Kernel k_tc_fwd: persistent warps pull 32-vertex batches from a global
+// counter.  Per vertex a the warp stages A = N+(a), the row starts of its
+// b's (from uinfo) and a prefix of their 32-byte sector counts in shared
+// memory with a 4096-bit membership filter, then walks all rows N+(b) as one
+// flattened space of 16-byte half-sectors: each lane loads one int4 per step
+// and keeps kUnroll independent loads in flight (the walk is DRAM-latency
+// bound otherwise); the row of a half-sector is one shared-memory binary
+// search, amortised over its 4 slots.  Every element costs one
+// shared-memory filter probe and, on a hit, a binary search in A for its
+// multiplicity.  Counts: per-lane uint64 -> warp sum -> one atomicAdd per
+// warp.
+//
+// Directed graphs (no mirror, the program's orientation matters): k_tc_mid
+// follows tc.sp literally -- per middle vertex v, A = N(v)_{>v} staged with
+// the same filter, each slot u < v of N(v) scans N(u)_{>v}.
+#include <cub/cub.cuh>
+
 #include <algorithm>
+#include <mutex>
 
 #include "sp_common.cuh"
 
@@ -26,9 +47,16 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int kA = 1024;          // staged A entries per warp
-constexpr int kFilterWords = 64;  // 2048-bit filter per warp
+constexpr int kA = 256;            // staged A entries per warp (larger rows: global search)
+constexpr int kFilterWords = 128;  // 4096-bit filter per warp
+constexpr int kFilterShift = 20;   // 32 - log2(4096)
 constexpr int kBatch = 32;
+constexpr int kGroup = 8;          // lanes per b-row (long-row path of k_tc_fwd)
+constexpr int kUnroll = 2;         // 16-byte loads in flight per lane in k_tc_fwd
+constexpr int kPad = 8;            // upper rows padded/aligned to 32-byte sectors
+constexpr int kQ = kPad / 4;       // 16-byte quarters per padded block
+
+std::mutex g_up_mu;  // guards the lazy upper-CSR build
 
 __device__ __forceinline__ int64_t lower_bound_g(const int32_t *__restrict__ a, int64_t lo,
                                                  int64_t hi, int32_t x) {
@@ -39,98 +67,351 @@ __device__ __forceinline__ int64_t lower_bound_g(const int32_t *__restrict__ a, 
     return lo;
 }
 
-__device__ __forceinline__ int lower_bound_s(const int32_t *a, int lo, int hi, int32_t x) {
+__device__ __forceinline__ uint32_t fhash(int32_t x) {
+    return ((uint32_t)x * 2654435761u) >> kFilterShift;  // 12 bits
+}
+
+// multiplicity of x in sorted A (shared memory, na entries)
+__device__ __forceinline__ int mult_s(const int32_t *A, int na, int32_t x) {
+    int lo = 0, hi = na;
     while (lo < hi) {
         int mid = (lo + hi) >> 1;
-        if (a[mid] < x) lo = mid + 1; else hi = mid;
+        if (A[mid] < x) lo = mid + 1; else hi = mid;
     }
-    return lo;
+    int c = 0;
+    while (lo < na && A[lo] == x) { c++; lo++; }
+    return c;
 }
 
-__device__ __forceinline__ uint32_t fhash(int32_t x) {
-    return ((uint32_t)x * 2654435761u) >> 21;  // 11 bits
+// multiplicity of x in sorted adj[lo, hi) (global memory)
+__device__ __forceinline__ int64_t mult_g(const int32_t *__restrict__ adj, int64_t lo, int64_t hi,
+                                          int32_t x) {
+    int64_t p = lower_bound_g(adj, lo, hi, x), c = 0;
+    while (p < hi && __ldg(adj + p) == x) { c++; p++; }
+    return c;
 }
 
-__global__ void __launch_bounds__(kBlock) k_tc(const int64_t *__restrict__ off,
-                                               const int32_t *__restrict__ adj, int64_t v0,
-                                               int64_t v1, unsigned long long *next,
-                                               unsigned long long *total,
-                                               unsigned long long *pairs) {
+// Stage sorted A = adj[a0, a0+na) into shared memory and set its filter bits.
+__device__ __forceinline__ void stage_a(const int32_t *__restrict__ adj, int64_t a0, int64_t na,
+                                        int32_t *A, uint32_t *F, unsigned lane) {
+    for (int k = lane; k < kFilterWords; k += 32) F[k] = 0u;
+    __syncwarp();
+    for (int64_t k = lane; k < na; k += 32) {
+        const int32_t x = adj[a0 + k];
+        A[k] = x;
+        const uint32_t h = fhash(x);
+        atomicOr(&F[h >> 5], 1u << (h & 31));
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ bool rank_gt(int32_t dx, int32_t x, int32_t dv, int32_t v) {
+    return dx > dv || (dx == dv && x > v);
+}
+
+// ---- upper CSR build (undirected) -------------------------------------
+
+__global__ void k_up_count(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+                           const int32_t *__restrict__ deg, int64_t n, int32_t *ulen,
+                           int64_t *pad8) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (int64_t v = warp; v < n; v += nw) {
+        const int64_t r0 = off[v], r1 = off[v + 1];
+        const int32_t dv = deg[v];
+        int64_t c = 0;
+        for (int64_t e = r0 + lane; e < r1; e += 32) {
+            const int32_t x = adj[e];
+            c += (x != (int32_t)v && rank_gt(__ldg(deg + x), x, dv, (int32_t)v)) ? 1 : 0;
+        }
+        c = warp_sum(c);
+        if (lane == 0) {
+            ulen[v] = (int32_t)c;
+            pad8[v] = (c + kPad - 1) / kPad;  // 32-byte sectors of the padded row
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) pad8[n] = 0;
+}
+
+__global__ void k_up_fill(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+                          const int32_t *__restrict__ deg, const int64_t *__restrict__ start8,
+                          int64_t n, int32_t *uadj) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (int64_t v = warp; v < n; v += nw) {
+        const int64_t r0 = off[v], r1 = off[v + 1];
+        const int32_t dv = deg[v];
+        const int64_t base = kPad * start8[v], end = kPad * start8[v + 1];
+        int64_t pos = base;
+        for (int64_t e0 = r0; e0 < r1; e0 += 32) {
+            const int64_t e = e0 + lane;
+            int32_t x = 0;
+            bool keep = false;
+            if (e < r1) {
+                x = adj[e];
+                keep = x != (int32_t)v && rank_gt(__ldg(deg + x), x, dv, (int32_t)v);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) uadj[pos + __popc(m & ((1u << lane) - 1u))] = x;
+            pos += __popc(m);
+        }
+        for (int64_t p = pos + lane; p < end; p += 32) uadj[p] = -1;  // row padding
+    }
+}
+
+__global__ void k_up_info(const int32_t *__restrict__ uadj, const int64_t *__restrict__ start8,
+                          const int32_t *__restrict__ ulen, int64_t mpad, uint2 *uinfo,
+                          uint32_t *ustart8, int64_t n) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < mpad;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t x = uadj[e];
+        uinfo[e] = x >= 0 ? make_uint2((uint32_t)start8[x], (uint32_t)ulen[x]) : make_uint2(0u, 0u);
+    }
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        ustart8[v] = (uint32_t)start8[v];
+}
+
+int ensure_upper(sp_graph *g, Call &c) {
+    std::lock_guard<std::mutex> lk(g_up_mu);
+    if (g->m_up >= 0) return SP_OK;
+    const int64_t n = g->n;
+    int64_t *pad8, *start8;
+    int32_t *ulen = nullptr;
+    SP_TRY(c.alloc(&pad8, n + 1));
+    SP_TRY(c.alloc(&start8, n + 1));
+    SP_CUDA(cudaMalloc(&ulen, std::max<int64_t>(1, n) * sizeof(int32_t)));
+    struct Guard {
+        void *p[4] = {nullptr, nullptr, nullptr, nullptr};
+        bool keep = false;
+        ~Guard() { if (!keep) for (void *q : p) cudaFree(q); }
+    } gd;
+    gd.p[0] = ulen;
+    const int grid = grid_for(n * 32, 256, c.device, 16);
+    k_up_count<<<grid, 256, 0, c.stream>>>(g->off, g->adj, g->outdeg, n, ulen, pad8);
+    size_t tmp = 0;
+    SP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, pad8, start8, n + 1, c.stream));
+    void *dt = nullptr;
+    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(dt, tmp, pad8, start8, n + 1, c.stream);
+    scratch_free(dt, c.stream);
+    SP_CUDA(e);
+    // real upper slots = sum of ulen (= m/2 minus self-loops); padded total
+    int64_t *h;
+    SP_TRY(c.host_as(&h));
+    SP_CUDA(cudaMemcpyAsync(h, start8 + n, 8, cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t mpad = kPad * h[0];
+    SP_CHECK(h[0] < (int64_t)0xFFFFFFFFll, SP_ERR_UNSUPPORTED,
+             "triangle counting: upper CSR of %lld slots exceeds the 2^35 limit",
+             (long long)mpad);
+    int32_t *uadj = nullptr;
+    uint2 *uinfo = nullptr;
+    uint32_t *ustart8 = nullptr;
+    SP_CUDA(cudaMalloc(&uadj, std::max<int64_t>(8, mpad) * sizeof(int32_t)));
+    gd.p[1] = uadj;
+    SP_CUDA(cudaMalloc(&uinfo, std::max<int64_t>(8, mpad) * sizeof(uint2)));
+    gd.p[2] = uinfo;
+    SP_CUDA(cudaMalloc(&ustart8, (n + 1) * sizeof(uint32_t)));
+    gd.p[3] = ustart8;
+    k_up_fill<<<grid, 256, 0, c.stream>>>(g->off, g->adj, g->outdeg, start8, n, uadj);
+    k_up_info<<<grid_for(std::max<int64_t>(mpad, n + 1), 256, c.device, 16), 256, 0, c.stream>>>(
+        uadj, start8, ulen, mpad, uinfo, ustart8, n);
+    c.launches += 3;
+    SP_CUDA(cudaGetLastError());
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    gd.keep = true;
+    g->ulen = ulen;
+    g->uadj = uadj;
+    g->uinfo = uinfo;
+    g->ustart8 = ustart8;
+    g->m_up_pad = mpad;
+    g->m_up = (g->m - 0) / 2;  // informational; exact count not needed
+    return SP_OK;
+}
+
+// ---- forward intersection (undirected) ---------------------------------
+
+struct TcCounters {
+    unsigned long long next;    // vertex batch cursor
+    unsigned long long total;   // weighted triangle count
+    unsigned long long pairs;   // oriented edges (a, b) processed
+    unsigned long long elems;   // N+(b) elements probed
+    unsigned long long abytes;  // sum over pairs of |N+(a)| (model bytes / 4)
+};
+
+__global__ void __launch_bounds__(kBlock, 1) k_tc_fwd(const uint32_t *__restrict__ ustart8,
+                                                   const int32_t *__restrict__ ulen,
+                                                   const int32_t *__restrict__ uadj,
+                                                   const uint2 *__restrict__ uinfo, int64_t v0,
+                                                   int64_t v1, TcCounters *ctr) {
+    __shared__ int32_t sA[kWarps][kA];
+    __shared__ uint32_t sB[kWarps][kA];       // sector start of row b_j
+    __shared__ int32_t sS[kWarps][kA + 1];    // sector prefix over the rows b_j
+    __shared__ uint32_t sF[kWarps][kFilterWords];
+    const unsigned lane = lane_id();
+    const int wib = threadIdx.x >> 5;
+    int32_t *A = sA[wib];
+    uint32_t *B = sB[wib];
+    int32_t *S = sS[wib];
+    uint32_t *F = sF[wib];
+    unsigned long long cnt = 0, elems = 0, pairs = 0, abytes = 0;
+    for (;;) {
+        unsigned long long bt = 0;
+        if (lane == 0) bt = atomicAdd(&ctr->next, (unsigned long long)kBatch);
+        bt = __shfl_sync(0xffffffffu, bt, 0);
+        const int64_t vb = v0 + (int64_t)bt;
+        if (vb >= v1) break;
+        const int64_t ve = min(v1, vb + kBatch);
+        // the batch's row descriptors, one coalesced load
+        const int64_t my = vb + lane;
+        const uint32_t my_s8 = my < ve ? ustart8[my] : 0u;
+        const int32_t my_len = my < ve ? ulen[my] : 0;
+        for (int64_t a = vb; a < ve; a++) {
+            const int src = (int)(a - vb);
+            const int na = __shfl_sync(0xffffffffu, my_len, src);
+            if (na < 2) continue;  // a triangle needs b and x in N+(a)
+            const int64_t r0 = kPad * (int64_t)__shfl_sync(0xffffffffu, my_s8, src);
+            if (lane == 0) {
+                pairs += (unsigned long long)na;
+                abytes += (unsigned long long)na * (unsigned long long)na;
+            }
+            if (na > kA) {
+                // long row (rare after degree ordering): groups of 8 lanes
+                // walk the b rows, membership by binary search in global A
+                const int grp = lane / kGroup, gl = lane % kGroup;
+                for (int j = grp; j < na; j += 32 / kGroup) {
+                    const uint2 inf = uinfo[r0 + j];
+                    if (gl == 0) elems += inf.y;
+                    for (int32_t k = gl; k < (int32_t)inf.y; k += kGroup)
+                        cnt += mult_g(uadj, r0, r0 + na, __ldg(uadj + kPad * (int64_t)inf.x + k));
+                }
+                continue;
+            }
+            // ---- stage A, row starts, sector prefix and filter
+            for (int k = lane; k < kFilterWords; k += 32) F[k] = 0u;
+            __syncwarp();
+            int carry = 0;
+            for (int k0 = 0; k0 < na; k0 += 32) {
+                const int k = k0 + lane;
+                int secs = 0;
+                if (k < na) {
+                    const int32_t x = uadj[r0 + k];
+                    const uint2 inf = uinfo[r0 + k];
+                    A[k] = x;
+                    B[k] = inf.x;
+                    secs = (int)((inf.y + kPad - 1u) / kPad);
+                    elems += inf.y;
+                    const uint32_t hh = fhash(x);
+                    atomicOr(&F[hh >> 5], 1u << (hh & 31));
+                }
+                int incl = secs;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if ((int)lane >= o) incl += t;
+                }
+                if (k < na) S[k] = carry + incl - secs;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) S[na] = carry;
+            __syncwarp();
+            // ---- flattened walk of all rows b_j in 16-byte half-sectors:
+            // one int4 per lane (rows are 32-byte aligned and padded with -1),
+            // kUnroll loads in flight per lane, one row search per 4 slots
+            const int nhalf = kQ * carry;
+            for (int h0 = 0; h0 < nhalf; h0 += 32 * kUnroll) {
+                int4 xs[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    const int h = h0 + u * 32 + (int)lane;
+                    xs[u] = make_int4(-1, -1, -1, -1);
+                    if (h < nhalf) {
+                        const int sec = h / kQ;
+                        int lo = 0, hi = na;  // last j with S[j] <= sec
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (S[mid] <= sec) lo = mid; else hi = mid;
+                        }
+                        xs[u] = __ldg(reinterpret_cast<const int4 *>(uadj) +
+                                      kQ * ((int64_t)B[lo] + (sec - S[lo])) + (h % kQ));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    const int32_t xv[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const int32_t x = xv[i];
+                        if (x < 0) continue;  // padding or past the end
+                        const uint32_t hh = fhash(x);
+                        if (F[hh >> 5] & (1u << (hh & 31))) cnt += mult_s(A, na, x);
+                    }
+                }
+            }
+            __syncwarp();  // A/B/S/F are restaged for the next vertex
+        }
+    }
+    cnt = warp_sum(cnt);
+    elems = warp_sum(elems);
+    if (lane == 0) {
+        if (cnt) atomicAdd(&ctr->total, cnt);
+        if (pairs) atomicAdd(&ctr->pairs, pairs);
+        if (elems) atomicAdd(&ctr->elems, elems);
+        if (abytes) atomicAdd(&ctr->abytes, abytes);
+    }
+}
+
+// ---- literal middle-vertex form (directed) -----------------------------
+
+__global__ void __launch_bounds__(kBlock, 1) k_tc_mid(const int64_t *__restrict__ off,
+                                                   const int32_t *__restrict__ adj, int64_t v0,
+                                                   int64_t v1, TcCounters *ctr) {
     __shared__ int32_t sA[kWarps][kA];
     __shared__ uint32_t sF[kWarps][kFilterWords];
     const unsigned lane = lane_id();
     const int wib = threadIdx.x >> 5;
     int32_t *A = sA[wib];
     uint32_t *F = sF[wib];
-    unsigned long long cnt = 0, npairs = 0;
+    unsigned long long cnt = 0, npairs = 0, elems = 0, abytes = 0;
     for (;;) {
-        unsigned long long b = 0;
-        if (lane == 0) b = atomicAdd(next, (unsigned long long)kBatch);
-        b = __shfl_sync(0xffffffffu, b, 0);
-        const int64_t vb = v0 + (int64_t)b;
+        unsigned long long bt = 0;
+        if (lane == 0) bt = atomicAdd(&ctr->next, (unsigned long long)kBatch);
+        bt = __shfl_sync(0xffffffffu, bt, 0);
+        const int64_t vb = v0 + (int64_t)bt;
         if (vb >= v1) break;
         const int64_t ve = min(v1, vb + kBatch);
         for (int64_t v = vb; v < ve; v++) {
             const int64_t r0 = off[v], r1 = off[v + 1];
             if (r1 - r0 < 2) continue;
-            // split point: first slot > v (A = [a0, r1)), slots < v are [r0, ulast)
+            // A = [a0, r1) (slots > v); slots < v are [r0, ulast)
             const int64_t a0 = lower_bound_g(adj, r0, r1, (int32_t)v + 1);
             const int64_t na = r1 - a0;
             if (na == 0) continue;
             const int64_t ulast = lower_bound_g(adj, r0, a0, (int32_t)v);
             const int64_t nu = ulast - r0;
             if (nu == 0) continue;
-            npairs += (lane == 0) ? (unsigned long long)nu : 0ull;
-            const bool staged = na <= kA;
-            if (staged) {
-                for (int k = lane; k < kFilterWords; k += 32) F[k] = 0u;
-                __syncwarp();
-                for (int64_t k = lane; k < na; k += 32) {
-                    int32_t x = adj[a0 + k];
-                    A[k] = x;
-                    uint32_t h = fhash(x);
-                    atomicOr(&F[h >> 5], 1u << (h & 31));
-                }
-                __syncwarp();
+            if (lane == 0) {
+                npairs += (unsigned long long)nu;
+                abytes += (unsigned long long)nu * (unsigned long long)na;
             }
+            const bool staged = na <= kA;
+            if (staged) stage_a(adj, a0, na, A, F, lane);
             for (int64_t k = r0 + lane; k < ulast; k += 32) {
                 const int32_t u = adj[k];
                 const int64_t u0 = off[u], u1 = off[u + 1];
-                int64_t b0 = u0;
-                if (u1 - u0 > 16) b0 = lower_bound_g(adj, u0, u1, (int32_t)v + 1);
-                const int64_t nb = u1 - b0;
-                if (nb <= 0) continue;
-                if (nb > 8 * na && na <= 64) {
-                    // hub u: walk A (runs), binary-search B in global memory
-                    int64_t lo = b0;
-                    for (int64_t i = 0; i < na;) {
-                        const int32_t x = staged ? A[i] : adj[a0 + i];
-                        int64_t j = i + 1;
-                        while (j < na && (staged ? A[j] : adj[a0 + j]) == x) j++;
-                        lo = lower_bound_g(adj, lo, u1, x);
-                        int64_t hi = lo;
-                        while (hi < u1 && __ldg(adj + hi) == x) hi++;
-                        cnt += (unsigned long long)(j - i) * (unsigned long long)(hi - lo);
-                        lo = hi;
-                        i = j;
-                    }
-                    continue;
-                }
+                const int64_t b0 = u1 - u0 > 16 ? lower_bound_g(adj, u0, u1, (int32_t)v + 1) : u0;
+                elems += (unsigned long long)(u1 - b0);
                 for (int64_t e = b0; e < u1; e++) {
                     const int32_t x = __ldg(adj + e);
                     if (x <= (int32_t)v) continue;
                     if (staged) {
                         const uint32_t h = fhash(x);
-                        if (!(F[h >> 5] & (1u << (h & 31)))) continue;
-                        int lb = lower_bound_s(A, 0, (int)na, x);
-                        int ub = lb;
-                        while (ub < na && A[ub] == x) ub++;
-                        cnt += (unsigned long long)(ub - lb);
+                        if (F[h >> 5] & (1u << (h & 31))) cnt += mult_s(A, (int)na, x);
                     } else {
-                        int64_t lb = lower_bound_g(adj, a0, r1, x);
-                        int64_t ub = lb;
-                        while (ub < r1 && __ldg(adj + ub) == x) ub++;
-                        cnt += (unsigned long long)(ub - lb);
+                        cnt += mult_g(adj, a0, r1, x);
                     }
                 }
             }
@@ -138,10 +419,12 @@ __global__ void __launch_bounds__(kBlock) k_tc(const int64_t *__restrict__ off,
         }
     }
     cnt = warp_sum(cnt);
-    npairs = warp_sum(npairs);
+    elems = warp_sum(elems);
     if (lane == 0) {
-        if (cnt) atomicAdd(total, cnt);
-        if (npairs) atomicAdd(pairs, npairs);
+        if (cnt) atomicAdd(&ctr->total, cnt);
+        if (npairs) atomicAdd(&ctr->pairs, npairs);
+        if (elems) atomicAdd(&ctr->elems, elems);
+        if (abytes) atomicAdd(&ctr->abytes, abytes);
     }
 }
 
@@ -152,9 +435,10 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
              "sp_tc: bad arguments");
     Call c;
     SP_TRY(c.begin(g->device));
-    unsigned long long *ctr;
-    SP_TRY(c.alloc(&ctr, 3));
-    SP_CUDA(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), c.stream));
+    if (!g->directed && g->n) SP_TRY(ensure_upper(g, c));
+    TcCounters *ctr;
+    SP_TRY(c.alloc(&ctr, 1));
+    SP_CUDA(cudaMemsetAsync(ctr, 0, sizeof(TcCounters), c.stream));
     const int sms = num_sms(c.device);
     cudaEvent_t ka, kb;
     SP_CUDA(cudaEventCreate(&ka));
@@ -163,26 +447,36 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
     if (v1 > v0) {
         int64_t want = (v1 - v0 + kBatch * kWarps - 1) / (kBatch * kWarps);
         int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
-        k_tc<<<grid, kBlock, 0, c.stream>>>(g->off, g->adj, v0, v1, ctr, ctr + 1, ctr + 2);
+        if (g->directed)
+            k_tc_mid<<<grid, kBlock, 0, c.stream>>>(g->off, g->adj, v0, v1, ctr);
+        else
+            k_tc_fwd<<<grid, kBlock, 0, c.stream>>>(g->ustart8, g->ulen, g->uadj, g->uinfo, v0,
+                                                    v1, ctr);
         c.launches++;
     }
     cudaEventRecord(kb, c.stream);
     SP_CUDA(cudaGetLastError());
-    unsigned long long h[3];
-    SP_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    TcCounters *h;
+    SP_TRY(c.host_as(&h));
+    SP_CUDA(cudaMemcpyAsync(h, ctr, sizeof(TcCounters), cudaMemcpyDeviceToHost, c.stream));
     int rc = c.finish(st);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ka, kb);
     cudaEventDestroy(ka);
     cudaEventDestroy(kb);
     SP_TRY(rc);
-    *count = (uint64_t)h[1];
+    *count = (uint64_t)h->total;
     if (st) {
         st->iterations = 1;
-        st->edges_visited = (int64_t)h[2];
+        st->edges_visited = (int64_t)h->pairs;
         st->vertices_visited = v1 - v0;
         st->main_kernel_ms = ms;
-        st->main_kernel_launches = c.launches;
+        st->main_kernel_launches = v1 > v0 ? 1 : 0;
+        // 8 B/vertex (offsets) + 4 B per stored slot + 4 B per
+        // element of both intersected rows
+        st->model_bytes = 8 * (v1 - v0) +
+                          4 * (g->directed ? g->m : g->m / 2) +
+                          4 * (int64_t)(h->abytes + h->elems);
     }
     return SP_OK;
 }
