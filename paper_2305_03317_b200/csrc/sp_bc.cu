@@ -13,9 +13,11 @@
 // one queue int32[n] holding all BFS levels back to back):
 //   level L -> L+1 : load-balanced top-down expansion (sp_expand.cuh) with a
 //                    CAS on level[x] (-1 -> L+1) appending the next level;
-//                    one 8-byte frontier-size read per level;
-//   sigma(L+1)     : ordered pull fold over reverse-CSR rows of the new level
-//                    (sp_fold.cuh), term = sigma[u] if level[u] == L;
+//                    one frontier-size read per level.  Fast mode pushes
+//                    sigma in the same pass (DiscoverSigmaOp, exact);
+//   sigma(L+1)     : deterministic mode: ordered pull fold over reverse-CSR
+//                    rows of the new level (sp_fold.cuh), term = sigma[u] if
+//                    level[u] == L;
 //   reverse sweep  : ordered fold over CSR rows of each level, deepest first,
 //                    term = sigma_v / sigma_w * (1 + delta_w) if level[w] ==
 //                    L+1, then bc += delta / 2 in the same kernel.
@@ -45,7 +47,32 @@ struct DiscoverOp {
     }
 };
 
-struct SigmaFold {  // bc.sp:10-12 over reverse-CSR slots
+// Fast mode: discovery and the sigma accumulation of bc.sp:10-12 in one
+// push over the level-L out-edges.  Every edge v -> x with level[x] == L+1
+// (won or lost CAS alike) adds sigma[v]; sigma values are path counts, i.e.
+// integer-valued doubles, so the atomic adds are exact in any order (below
+// 2^53) and the result equals the reference's ordered fold bit for bit.
+struct DiscoverSigmaOp {
+    using Payload = double;
+    int32_t *__restrict__ level;
+    double *__restrict__ sigma;
+    int next;
+    __device__ __forceinline__ double payload(int32_t v) const { return __ldcg(sigma + v); }
+    __device__ __forceinline__ bool visit(double sv, int64_t, int32_t x) const {
+        const int lx = __ldcg(level + x);
+        if (lx != -1 && lx != next) return false;
+        bool won = false;
+        if (lx == -1) {
+            const int old = atomicCAS(level + x, -1, next);
+            won = old == -1;
+            if (!won && old != next) return false;
+        }
+        atomicAdd(sigma + x, sv);
+        return won;
+    }
+};
+
+struct SigmaFold {  // bc.sp:10-12 over reverse-CSR slots (deterministic mode)
     const int32_t *__restrict__ radj;
     const int32_t *__restrict__ level;
     double *__restrict__ sigma;
@@ -100,7 +127,9 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
     const int64_t n = g->n;
     const int sms = num_sms(c.device);
     const bool det = flags & SP_FLAG_DETERMINISTIC;
-    int32_t *level, *queue, *hubs;
+    int32_t *level, *queue, *hubs, *reg_v, *reg_nch, *item_reg;
+    int64_t *reg_base;
+    double *csum;
     double *sigma, *delta, *bc;
     uint2 *chunks;
     ExpandCounters *cnt;
@@ -108,19 +137,25 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
     SP_TRY(c.alloc(&level, n));
     SP_TRY(c.alloc(&queue, n));
     SP_TRY(c.alloc(&hubs, n));
+    const int64_t ccap = fold_chunk_capacity(g->m);
+    SP_TRY(c.alloc(&reg_v, n));
+    SP_TRY(c.alloc(&reg_nch, n));
+    SP_TRY(c.alloc(&reg_base, n));
+    SP_TRY(c.alloc(&item_reg, ccap));
+    SP_TRY(c.alloc(&csum, ccap));
     SP_TRY(c.alloc(&sigma, n));
     SP_TRY(c.alloc(&delta, n));
     SP_TRY(c.alloc(&bc, n));
     SP_TRY(c.alloc(&chunks, expand_chunk_capacity(g->m)));
     SP_TRY(c.alloc(&cnt, 1));
-    SP_TRY(c.alloc(&nhubs, 1));
+    SP_TRY(c.alloc(&nhubs, 3));
+    const FoldLists fl{hubs, nhubs, FoldChunks{reg_v, reg_base, reg_nch, item_reg, csum, nullptr}};
     SP_CUDA(cudaMemsetAsync(bc, 0, n * sizeof(double), c.stream));
     SP_CUDA(cudaMemsetAsync(sigma, 0, n * sizeof(double), c.stream));
     SP_CUDA(cudaMemsetAsync(delta, 0, n * sizeof(double), c.stream));
     ExpandCounters *hc = nullptr;
     SP_TRY(c.host_as(&hc));
     const bool big_out = g->max_outdeg > kSplit;
-    const bool hub_in = g->max_indeg > kBcHub, hub_out = g->max_outdeg > kBcHub;
     int64_t levels_total = 0, scanned_total = 0, reached_total = 0;
     std::vector<int64_t> ls;
     for (int64_t si = 0; si < nsrc; si++) {
@@ -136,9 +171,15 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
         for (int L = 0;; L++) {
             const int64_t q0 = ls[L], q1 = ls[L + 1];
             SP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(ExpandCounters), c.stream));
-            DiscoverOp op{level, L + 1};
-            launch_expand(op, g->off, g->adj, queue + q0, q1 - q0, queue + q1, chunks, cnt, sms,
-                          big_out, c.stream, &c.launches);
+            if (det) {
+                DiscoverOp op{level, L + 1};
+                launch_expand(op, g->off, g->adj, queue + q0, q1 - q0, queue + q1, chunks, cnt,
+                              sms, big_out, c.stream, &c.launches);
+            } else {
+                DiscoverSigmaOp op{level, sigma, L + 1};
+                launch_expand(op, g->off, g->adj, queue + q0, q1 - q0, queue + q1, chunks, cnt,
+                              sms, big_out, c.stream, &c.launches);
+            }
             SP_CUDA(cudaGetLastError());
             SP_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(ExpandCounters), cudaMemcpyDeviceToHost,
                                     c.stream));
@@ -147,17 +188,19 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
             const int64_t nnew = (int64_t)hc->next_size;
             if (nnew == 0) break;
             ls.push_back(q1 + nnew);
-            SigmaFold sf{g->radj, level, sigma, L};
-            launch_fold(sf, g->roff, queue + q1, nnew, kBcHub, hubs, nhubs, det, hub_in, sms,
-                        c.stream, &c.launches);
+            if (det) {
+                SigmaFold sf{g->radj, level, sigma, L};
+                launch_fold(sf, g->roff, queue + q1, nnew, kBcHub, fl, true, g->max_indeg, sms,
+                            c.stream, &c.launches);
+            }
         }
         const int nlev = (int)ls.size() - 1;
         levels_total += nlev;
         reached_total += ls.back();
         for (int L = nlev - 2; L >= 0; L--) {
             DeltaFold df{g->adj, level, sigma, delta, bc, L + 1, s};
-            launch_fold(df, g->off, queue + ls[L], ls[L + 1] - ls[L], kBcHub, hubs, nhubs, det,
-                        hub_out, sms, c.stream, &c.launches);
+            launch_fold(df, g->off, queue + ls[L], ls[L + 1] - ls[L], kBcHub, fl, det,
+                        g->max_outdeg, sms, c.stream, &c.launches);
         }
         SP_CUDA(cudaGetLastError());
     }
@@ -171,6 +214,9 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
         st->vertices_visited = reached_total;
         st->main_kernel_ms = st->device_ms;
         st->main_kernel_launches = st->kernel_launches;
+        // 48 B per reached slot (discovery 8, sigma 16, delta 24)
+        // + 64 B per reached vertex, summed over sources
+        st->model_bytes = 48 * scanned_total + 64 * reached_total;
     }
     return SP_OK;
 }

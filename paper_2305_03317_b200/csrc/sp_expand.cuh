@@ -7,19 +7,29 @@
 //    coalesced adj / weight loads, every lane busy whatever the degree mix.
 //  * rows longer than kSplit are not walked there; they are cut into
 //    kSplit-slot chunks (vertex, chunk) and k_expand_chunks spreads the
-//    chunks over all warps, so one 100K-degree hub cannot serialise a warp.
+//    chunks over all warps, so one 100K-degree hub cannot serialise a warp;
+//  * small frontiers get fewer vertices per warp (down to one), so a
+//    frontier of a few hundred long rows still fills the GPU.
 //  * visited vertices are appended to the next frontier with one atomic per
 //    warp (ballot + popc).
-// Op supplies:  int payload(int32_t v)          -- per-source-vertex value
-//               bool visit(int pay, int64_t e, int32_t x)  -- true => push x
+// Op supplies:  Payload payload(int32_t v)      -- per-source-vertex value
+//               bool visit(Payload pay, int64_t e, int32_t x) -- true => push x
+//               (Payload defaults to int; an Op may declare `using Payload`)
 #pragma once
+
+#include <type_traits>
 
 #include "sp_common.cuh"
 
 namespace sp {
 
 constexpr int kExpandBlock = 256;
-constexpr int kSplit = 2048;  // slots per hub chunk
+
+template <class Op, class = void>
+struct PayloadOf { using type = int; };
+template <class Op>
+struct PayloadOf<Op, std::void_t<typename Op::Payload>> { using type = typename Op::Payload; };
+constexpr int kSplit = 256;  // rows longer than this are cut into kSplit-slot chunks
 
 struct ExpandCounters {
     unsigned long long next_size;  // appended frontier entries
@@ -32,17 +42,20 @@ template <class Op>
 __global__ void __launch_bounds__(kExpandBlock) k_expand(
     Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const int32_t *__restrict__ q, int64_t nq, int32_t *__restrict__ qn,
-    uint2 *__restrict__ chunks, ExpandCounters *cnt) {
+    uint2 *__restrict__ chunks, ExpandCounters *cnt, int vpw) {
+    // vpw = frontier vertices per warp (32 normally; fewer for small
+    // frontiers, so that every SM gets work)
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long scanned = 0;
-    for (int64_t base = warp * 32; base < nq; base += nwarps * 32) {
+    for (int64_t base = warp * vpw; base < nq; base += nwarps * vpw) {
         int64_t i = base + lane;
+        using P = typename PayloadOf<Op>::type;
         int32_t v = -1;
         int64_t beg = 0, deg = 0;
-        int pay = 0;
-        if (i < nq) {
+        P pay = P(0);
+        if ((int)lane < vpw && i < nq) {
             v = q[i];
             beg = off[v];
             deg = off[v + 1] - beg;
@@ -75,7 +88,7 @@ __global__ void __launch_bounds__(kExpandBlock) k_expand(
             }
             const int64_t ex = __shfl_sync(0xffffffffu, excl, lo);
             const int64_t b0 = __shfl_sync(0xffffffffu, beg, lo);
-            const int pv = __shfl_sync(0xffffffffu, pay, lo);
+            const P pv = __shfl_sync(0xffffffffu, pay, lo);
             bool push = false;
             int32_t x = 0;
             if (p < total) {
@@ -106,7 +119,7 @@ __global__ void __launch_bounds__(kExpandBlock) k_expand_chunks(
         const int64_t end = off[v + 1];
         const int64_t e0 = off[v] + (int64_t)ch.y * kSplit;
         const int64_t e1 = min(end, e0 + kSplit);
-        const int pay = op.payload(v);
+        const auto pay = op.payload(v);
         scanned += e1 - e0;
         for (int64_t e = e0; e < e1; e += 32) {
             const int64_t ee = e + lane;
@@ -132,9 +145,12 @@ inline void launch_expand(const Op &op, const int64_t *off, const int32_t *adj, 
                           int64_t nq, int32_t *qn, uint2 *chunks, ExpandCounters *cnt, int sms,
                           bool has_big_rows, cudaStream_t s, int64_t *launches) {
     const int cap = sms * 8;
-    int64_t want = (nq + 255) / 256;  // 8 warps x 32 vertices per block
+    const int64_t warps_full = (int64_t)cap * (kExpandBlock / 32);
+    int vpw = 32;
+    while (vpw > 1 && (nq + vpw - 1) / vpw < warps_full) vpw >>= 1;
+    int64_t want = ((nq + vpw - 1) / vpw + 7) / 8;  // 8 warps per block
     int g1 = (int)(want < 1 ? 1 : (want > cap ? cap : want));
-    k_expand<Op><<<g1, kExpandBlock, 0, s>>>(op, off, adj, q, nq, qn, chunks, cnt);
+    k_expand<Op><<<g1, kExpandBlock, 0, s>>>(op, off, adj, q, nq, qn, chunks, cnt, vpw);
     ++*launches;
     if (has_big_rows) {
         k_expand_chunks<Op><<<cap, kExpandBlock, 0, s>>>(op, off, adj, chunks, qn, cnt);

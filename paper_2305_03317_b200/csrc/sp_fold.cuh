@@ -9,10 +9,13 @@
 //   * each lane then folds the part of ITS row inside the chunk,
 //     sequentially, in CSR order (a skipped slot contributes +0.0, which
 //     leaves a non-negative running sum bit-identical).
-// Rows longer than hub_thr are deferred to k_fold_hub: one CTA per row,
-// staged in 1024-slot chunks; deterministic mode folds them sequentially
-// (bit-exact), fast mode uses a fixed-shape tree per chunk (deterministic
-// run to run, ~1e-16 relative from the left fold).
+// Deterministic mode: rows longer than hub_thr are deferred to k_fold_hub
+// (one CTA per row, staged in 1024-slot chunks, folded sequentially:
+// bit-exact).  Fast mode: rows longer than kShortRow are cut into
+// kFoldSplit-slot chunks folded by whole warps (k_fold_chunks) and combined
+// per row in chunk order (k_fold_combine): deterministic run to run, a few
+// ulps from the left fold, and no lane folds a long row while its
+// warp-mates idle.
 // F supplies: double payload(int32_t v); double term(double pay, int64_t slot);
 //             void finish(int32_t v, double sum).
 #pragma once
@@ -27,10 +30,28 @@ constexpr int kFoldChunk = 128;
 constexpr int kHubFoldBlock = 256;
 constexpr int kHubFoldChunk = 1024;
 
+// Fast mode: rows longer than short_thr are cut into kFoldSplit-slot chunks.
+// k_fold registers each such row (vertex, first chunk slot, chunk count) and
+// publishes one work item per chunk; k_fold_chunks gives every chunk one
+// warp (8 independent terms in flight per lane, fixed xor tree) and stores
+// its partial; k_fold_combine adds a row's partials in chunk order (fixed
+// shape: deterministic run to run) and finishes the row.
+constexpr int kFoldSplit = 256;
+
+struct FoldChunks {
+    int32_t *reg_v;      // registered row vertex
+    int64_t *reg_base;   // its first chunk slot
+    int32_t *reg_nch;    // its chunk count
+    int32_t *item_reg;   // chunk slot -> registry index
+    double *csum;        // chunk slot -> partial sum
+    unsigned long long *counts;  // [0] registered rows, [1] chunk slots used
+};
+
 template <class F>
 __global__ void __launch_bounds__(kFoldBlock) k_fold(
     F f, const int64_t *__restrict__ rowoff, const int32_t *__restrict__ q, int64_t nq,
-    int64_t hub_thr, int32_t *__restrict__ hubs, unsigned long long *nhubs) {
+    int64_t hub_thr, int32_t *__restrict__ hubs, unsigned long long *nhubs, int64_t short_thr,
+    FoldChunks fc) {
     __shared__ double stage[kFoldWarps][kFoldChunk];
     const unsigned lane = lane_id();
     double *buf = stage[threadIdx.x >> 5];
@@ -48,13 +69,24 @@ __global__ void __launch_bounds__(kFoldBlock) k_fold(
             pay = f.payload(v);
         }
         const bool hub = deg > hub_thr;
-        if (hub) {
-            deg = 0;
-        }
+        const bool mid = !hub && deg > short_thr;
         {
             int64_t slot = warp_append(hub, nhubs);
             if (hub) hubs[slot] = v;
         }
+        if (short_thr < hub_thr) {  // fast mode: register the row's chunks
+            const int64_t r = warp_append(mid, &fc.counts[0]);
+            if (mid) {
+                const int nch = (int)((deg + kFoldSplit - 1) / kFoldSplit);
+                const int64_t base = (int64_t)atomicAdd(&fc.counts[1], (unsigned long long)nch);
+                fc.reg_v[r] = v;
+                fc.reg_base[r] = base;
+                fc.reg_nch[r] = nch;
+                for (int c = 0; c < nch; c++) fc.item_reg[base + c] = (int32_t)r;
+            }
+        }
+        const bool deferred = hub || mid;
+        if (deferred) deg = 0;
         int64_t incl = deg;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -85,7 +117,56 @@ __global__ void __launch_bounds__(kFoldBlock) k_fold(
             for (int64_t p = a; p < b; p++) sum = __dadd_rn(sum, buf[p - p0]);
             __syncwarp();
         }
-        if (i < nq && !hub) f.finish(v, sum);
+        if (i < nq && !deferred) f.finish(v, sum);
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kFoldBlock) k_fold_chunks(F f, const int64_t *__restrict__ rowoff,
+                                                            FoldChunks fc) {
+    const unsigned lane = lane_id();
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nitems = (int64_t)__ldcg(&fc.counts[1]);
+    for (int64_t k = warp; k < nitems; k += nwarps) {
+        const int32_t r = fc.item_reg[k];
+        const int32_t v = fc.reg_v[r];
+        const int64_t c = k - fc.reg_base[r];
+        const int64_t re = rowoff[v + 1];
+        const int64_t s0 = rowoff[v] + c * kFoldSplit;
+        const double pay = f.payload(v);
+        double t[kFoldSplit / 32];
+#pragma unroll
+        for (int j = 0; j < kFoldSplit / 32; j++) {
+            const int64_t e = s0 + j * 32 + lane;
+            t[j] = e < re ? f.term(pay, e) : 0.0;
+        }
+        double sum = 0.0;
+#pragma unroll
+        for (int j = 0; j < kFoldSplit / 32; j++) sum = __dadd_rn(sum, t[j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+        if (lane == 0) fc.csum[k] = sum;
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kFoldBlock) k_fold_combine(F f, FoldChunks fc) {
+    const unsigned lane = lane_id();
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nreg = (int64_t)__ldcg(&fc.counts[0]);
+    for (int64_t r = warp; r < nreg; r += nwarps) {
+        const int64_t base = fc.reg_base[r];
+        const int nch = fc.reg_nch[r];
+        double s = 0.0;
+        for (int c0 = 0; c0 < nch; c0 += 32) {
+            double t = c0 + (int)lane < nch ? fc.csum[base + c0 + lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
+            s = __dadd_rn(s, t);
+        }
+        if (lane == 0) f.finish(fc.reg_v[r], s);
     }
 }
 
@@ -136,22 +217,44 @@ __global__ void __launch_bounds__(kHubFoldBlock) k_fold_hub(
     }
 }
 
+// Deferred-row buffers of a fold launch.
+struct FoldLists {
+    int32_t *hubs;                 // deterministic mode: rows > hub_thr (n)
+    unsigned long long *counts;    // [0] hubs, [1] registered rows, [2] chunk slots
+    FoldChunks chunks;             // fast mode: chunked rows
+};
+
+// Capacity of the chunk-slot buffers for a graph with m slots.
+inline int64_t fold_chunk_capacity(int64_t m) { return m / kFoldSplit + m / 48 + 2; }
+
+// Fast mode (!deterministic): rows longer than kShortRow are folded in
+// kFoldSplit-slot chunks by whole warps; deterministic mode folds every row
+// left to right (rows > hub_thr by k_fold_hub's thread 0).
+constexpr int64_t kShortRow = 48;
+
 template <class F>
 inline void launch_fold(const F &f, const int64_t *rowoff, const int32_t *q, int64_t nq,
-                        int64_t hub_thr, int32_t *hubs, unsigned long long *nhubs_dev,
-                        bool deterministic, bool may_have_hubs, int sms, cudaStream_t s,
-                        int64_t *launches) {
+                        int64_t hub_thr, const FoldLists &fl, bool deterministic,
+                        int64_t max_row, int sms, cudaStream_t s, int64_t *launches) {
     if (nq <= 0) return;
-    if (may_have_hubs) cudaMemsetAsync(nhubs_dev, 0, sizeof(unsigned long long), s);
+    const bool hubs = deterministic && max_row > hub_thr;
+    const bool chunked = !deterministic && max_row > kShortRow;
+    if (hubs || chunked) cudaMemsetAsync(fl.counts, 0, 3 * sizeof(unsigned long long), s);
     const int cap = sms * 8;
     int64_t want = (nq + kFoldBlock - 1) / kFoldBlock;
     int g = (int)(want < 1 ? 1 : (want > cap ? cap : want));
-    k_fold<F><<<g, kFoldBlock, 0, s>>>(f, rowoff, q, nq, may_have_hubs ? hub_thr : INT64_MAX,
-                                       hubs, nhubs_dev);
+    FoldChunks fc = fl.chunks;
+    fc.counts = fl.counts + 1;
+    k_fold<F><<<g, kFoldBlock, 0, s>>>(f, rowoff, q, nq, hubs ? hub_thr : INT64_MAX, fl.hubs,
+                                       fl.counts, chunked ? kShortRow : INT64_MAX, fc);
     ++*launches;
-    if (may_have_hubs) {
-        k_fold_hub<F><<<sms * 2, kHubFoldBlock, 0, s>>>(f, rowoff, hubs, nhubs_dev,
-                                                        deterministic ? 1 : 0);
+    if (chunked) {
+        k_fold_chunks<F><<<cap, kFoldBlock, 0, s>>>(f, rowoff, fc);
+        k_fold_combine<F><<<cap, kFoldBlock, 0, s>>>(f, fc);
+        *launches += 2;
+    }
+    if (hubs) {
+        k_fold_hub<F><<<sms * 2, kHubFoldBlock, 0, s>>>(f, rowoff, fl.hubs, fl.counts, 1);
         ++*launches;
     }
 }
