@@ -38,11 +38,14 @@ namespace {
 constexpr int64_t kBcHub = 8192;  // rows longer than this take the CTA fold
 
 struct DiscoverOp {
+    using Payload = int;
+    using Probe = int;  // level[x]
     int32_t *__restrict__ level;
     int next;
     __device__ __forceinline__ int payload(int32_t) const { return 0; }
-    __device__ __forceinline__ bool visit(int, int64_t, int32_t x) const {
-        if (__ldcg(level + x) != -1) return false;
+    __device__ __forceinline__ int probe(int64_t, int32_t x) const { return __ldcg(level + x); }
+    __device__ __forceinline__ bool apply(int, int64_t, int32_t x, int lx) const {
+        if (lx != -1) return false;
         return atomicCAS(level + x, -1, next) == -1;
     }
 };
@@ -54,12 +57,13 @@ struct DiscoverOp {
 // 2^53) and the result equals the reference's ordered fold bit for bit.
 struct DiscoverSigmaOp {
     using Payload = double;
+    using Probe = int;  // level[x]
     int32_t *__restrict__ level;
     double *__restrict__ sigma;
     int next;
     __device__ __forceinline__ double payload(int32_t v) const { return __ldcg(sigma + v); }
-    __device__ __forceinline__ bool visit(double sv, int64_t, int32_t x) const {
-        const int lx = __ldcg(level + x);
+    __device__ __forceinline__ int probe(int64_t, int32_t x) const { return __ldcg(level + x); }
+    __device__ __forceinline__ bool apply(double sv, int64_t, int32_t x, int lx) const {
         if (lx != -1 && lx != next) return false;
         bool won = false;
         if (lx == -1) {

@@ -159,6 +159,30 @@ __device__ __forceinline__ int64_t warp_append(bool want, unsigned long long *co
     return (int64_t)base + __popc(mask & ((1u << lane_id()) - 1u));
 }
 
+// Warp-aggregated append of K rounds at once: round u's lanes with
+// push[u] get consecutive slots, one global atomic for the whole batch.
+template <int K>
+__device__ __forceinline__ void warp_append_multi(const bool (&push)[K], const int32_t (&val)[K],
+                                                  unsigned long long *counter, int32_t *out) {
+    unsigned m[K];
+    unsigned total = 0;
+#pragma unroll
+    for (int u = 0; u < K; u++) {
+        m[u] = __ballot_sync(0xffffffffu, push[u]);
+        total += __popc(m[u]);
+    }
+    if (!total) return;
+    unsigned long long base = 0;
+    if (lane_id() == 0) base = atomicAdd(counter, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const unsigned lt = (1u << lane_id()) - 1u;
+#pragma unroll
+    for (int u = 0; u < K; u++) {
+        if (push[u]) out[base + __popc(m[u] & lt)] = val[u];
+        base += __popc(m[u]);
+    }
+}
+
 __device__ __forceinline__ int ld_stream_i32(const int32_t *p) {
     int v;
     asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));

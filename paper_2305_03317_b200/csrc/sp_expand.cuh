@@ -2,34 +2,36 @@
 // g.neighbors(v)` of a filtered outer forall, interp.py:373-399), shared by
 // SSSP relaxation and BFS discovery.
 //
-//  * k_expand: a warp takes 32 frontier vertices, prefix-sums their degrees
-//    in registers and walks the flattened edge list 32 slots at a time:
-//    coalesced adj / weight loads, every lane busy whatever the degree mix.
+//  * k_expand: a warp takes up to 32 frontier vertices, prefix-sums their
+//    degrees in registers and walks the flattened edge list kRounds x 32
+//    slots at a time: coalesced adj loads, every lane busy whatever the
+//    degree mix;
 //  * rows longer than kSplit are not walked there; they are cut into
-//    kSplit-slot chunks (vertex, chunk) and k_expand_chunks spreads the
-//    chunks over all warps, so one 100K-degree hub cannot serialise a warp;
+//    kSplit-slot chunks (vertex, chunk) and k_expand_chunks gives each chunk
+//    one warp (kSplit/32 slots per lane), so one 100K-degree hub cannot
+//    serialise a warp;
 //  * small frontiers get fewer vertices per warp (down to one), so a
-//    frontier of a few hundred long rows still fills the GPU.
+//    frontier of a few hundred long rows still fills the GPU;
+//  * every slot's work is split into a load-only probe and an apply step
+//    (the atomics); all probes of a lane are issued before any apply, so
+//    several random L2 round trips are in flight per lane instead of one
+//    dependent chain per slot;
 //  * visited vertices are appended to the next frontier with one atomic per
-//    warp (ballot + popc).
-// Op supplies:  Payload payload(int32_t v)      -- per-source-vertex value
-//               bool visit(Payload pay, int64_t e, int32_t x) -- true => push x
-//               (Payload defaults to int; an Op may declare `using Payload`)
+//    warp per kRounds x 32 (or kSplit) slots (ballots + popc): a single
+//    global counter shared by every warp must not see one atomic per round.
+// Op supplies:  Payload payload(int32_t v)             -- per-source-vertex value
+//               Probe probe(int64_t e, int32_t x)      -- loads only
+//               bool apply(Payload, int64_t e, int32_t x, Probe) -- true => push x
+//               (`using Payload` / `using Probe` declare the types)
 #pragma once
-
-#include <type_traits>
 
 #include "sp_common.cuh"
 
 namespace sp {
 
 constexpr int kExpandBlock = 256;
-
-template <class Op, class = void>
-struct PayloadOf { using type = int; };
-template <class Op>
-struct PayloadOf<Op, std::void_t<typename Op::Payload>> { using type = typename Op::Payload; };
 constexpr int kSplit = 256;  // rows longer than this are cut into kSplit-slot chunks
+constexpr int kRounds = 4;   // 32-slot rounds in flight per warp in k_expand
 
 struct ExpandCounters {
     unsigned long long next_size;  // appended frontier entries
@@ -39,19 +41,20 @@ struct ExpandCounters {
 };
 
 template <class Op>
-__global__ void __launch_bounds__(kExpandBlock) k_expand(
+__global__ void __launch_bounds__(kExpandBlock, 4) k_expand(
     Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const int32_t *__restrict__ q, int64_t nq, int32_t *__restrict__ qn,
     uint2 *__restrict__ chunks, ExpandCounters *cnt, int vpw) {
     // vpw = frontier vertices per warp (32 normally; fewer for small
     // frontiers, so that every SM gets work)
+    using P = typename Op::Payload;
+    using Pr = typename Op::Probe;
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long scanned = 0;
     for (int64_t base = warp * vpw; base < nq; base += nwarps * vpw) {
         int64_t i = base + lane;
-        using P = typename PayloadOf<Op>::type;
         int32_t v = -1;
         int64_t beg = 0, deg = 0;
         P pay = P(0);
@@ -76,28 +79,36 @@ __global__ void __launch_bounds__(kExpandBlock) k_expand(
         const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
         const int64_t excl = incl - deg;
         scanned += total;
-        for (int64_t p0 = 0; p0 < total; p0 += 32) {
-            const int64_t p = p0 + lane;
-            // owner = largest lane with excl <= p (always a lane with deg > 0)
-            int lo = 0;
+        for (int64_t p0 = 0; p0 < total; p0 += 32 * kRounds) {
+            int64_t e[kRounds];
+            int32_t x[kRounds];
+            P pv[kRounds];
+            Pr pr[kRounds];
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                int cand = lo + step;
-                int64_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
-                if (cand < 32 && ex <= p) lo = cand;
+            for (int u = 0; u < kRounds; u++) {
+                const int64_t p = p0 + u * 32 + lane;
+                // owner = largest lane with excl <= p (always a lane with deg > 0)
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    int cand = lo + step;
+                    int64_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+                    if (cand < 32 && ex <= p) lo = cand;
+                }
+                const int64_t ex = __shfl_sync(0xffffffffu, excl, lo);
+                const int64_t b0 = __shfl_sync(0xffffffffu, beg, lo);
+                pv[u] = __shfl_sync(0xffffffffu, pay, lo);
+                e[u] = p < total ? b0 + (p - ex) : -1;
+                x[u] = e[u] >= 0 ? adj[e[u]] : -1;
             }
-            const int64_t ex = __shfl_sync(0xffffffffu, excl, lo);
-            const int64_t b0 = __shfl_sync(0xffffffffu, beg, lo);
-            const P pv = __shfl_sync(0xffffffffu, pay, lo);
-            bool push = false;
-            int32_t x = 0;
-            if (p < total) {
-                const int64_t e = b0 + (p - ex);
-                x = adj[e];
-                push = op.visit(pv, e, x);
-            }
-            int64_t slot = warp_append(push, &cnt->next_size);
-            if (push) qn[slot] = x;
+#pragma unroll
+            for (int u = 0; u < kRounds; u++)
+                if (e[u] >= 0) pr[u] = op.probe(e[u], x[u]);
+            bool push[kRounds];
+#pragma unroll
+            for (int u = 0; u < kRounds; u++)
+                push[u] = e[u] >= 0 && op.apply(pv[u], e[u], x[u], pr[u]);
+            warp_append_multi<kRounds>(push, x, &cnt->next_size, qn);
         }
     }
     // `scanned` is warp-uniform (every lane added the same totals)
@@ -105,9 +116,11 @@ __global__ void __launch_bounds__(kExpandBlock) k_expand(
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kExpandBlock) k_expand_chunks(
+__global__ void __launch_bounds__(kExpandBlock, 4) k_expand_chunks(
     Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const uint2 *__restrict__ chunks, int32_t *__restrict__ qn, ExpandCounters *cnt) {
+    using Pr = typename Op::Probe;
+    constexpr int kPer = kSplit / 32;
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -121,17 +134,21 @@ __global__ void __launch_bounds__(kExpandBlock) k_expand_chunks(
         const int64_t e1 = min(end, e0 + kSplit);
         const auto pay = op.payload(v);
         scanned += e1 - e0;
-        for (int64_t e = e0; e < e1; e += 32) {
-            const int64_t ee = e + lane;
-            bool push = false;
-            int32_t x = 0;
-            if (ee < e1) {
-                x = adj[ee];
-                push = op.visit(pay, ee, x);
-            }
-            int64_t slot = warp_append(push, &cnt->next_size);
-            if (push) qn[slot] = x;
+        int32_t x[kPer];
+        Pr pr[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; j++) {
+            const int64_t ee = e0 + j * 32 + lane;
+            x[j] = ee < e1 ? adj[ee] : -1;
         }
+#pragma unroll
+        for (int j = 0; j < kPer; j++)
+            if (x[j] >= 0) pr[j] = op.probe(e0 + j * 32 + lane, x[j]);
+        bool push[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; j++)
+            push[j] = x[j] >= 0 && op.apply(pay, e0 + j * 32 + lane, x[j], pr[j]);
+        warp_append_multi<kPer>(push, x, &cnt->next_size, qn);
     }
     if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);  // warp-uniform
 }

@@ -32,21 +32,29 @@ constexpr int kBlock = 256;
 
 // Relaxation of sssp.sp:11-12 for one slot; payload = dist[v] at expansion.
 struct RelaxOp {
+    using Payload = int;
+    struct Probe {
+        int w;   // w_eff[e]
+        int dx;  // dist[x] (may be stale: dist only decreases, so conservative)
+    };
     int32_t *__restrict__ dist;
     int32_t *__restrict__ enq;
     const int32_t *__restrict__ weff;
     unsigned long long *overflow;
     int it;
     __device__ __forceinline__ int payload(int32_t v) const { return __ldcg(dist + v); }
-    __device__ __forceinline__ bool visit(int dv, int64_t e, int32_t x) const {
-        const int64_t cand = (int64_t)dv + (int64_t)weff[e];
+    __device__ __forceinline__ Probe probe(int64_t e, int32_t x) const {
+        return Probe{__ldg(weff + e), __ldcg(dist + x)};
+    }
+    __device__ __forceinline__ bool apply(int dv, int64_t, int32_t x, Probe p) const {
+        const int64_t cand = (int64_t)dv + (int64_t)p.w;
         if (cand >= (int64_t)kIntMax) return false;  // never beats INT_MAX (F12)
         if (cand < (int64_t)(-2147483647 - 1)) {
             atomicAdd(overflow, 1ull);
             return false;
         }
         const int c = (int)cand;
-        if (c >= __ldcg(dist + x)) return false;  // conservative pre-filter
+        if (c >= p.dx) return false;  // conservative pre-filter
         const int old = atomicMin(dist + x, c);
         return c < old && atomicExch(enq + x, it) != it;
     }
