@@ -126,6 +126,9 @@ struct sp_graph {
 // ---- device helpers --------------------------------------------------------
 namespace sp {
 
+// Build the graph's w_eff array if it was deferred (thread-safe).
+int ensure_weff(sp_graph *g, Call &c);
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 template <class T>

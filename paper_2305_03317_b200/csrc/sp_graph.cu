@@ -122,12 +122,6 @@ struct MaxOp {
     __device__ __forceinline__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; }
 };
 
-__global__ void k_runstart(const uint64_t *__restrict__ key, int64_t m, int64_t *runstart) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
-         e += (int64_t)gridDim.x * blockDim.x)
-        runstart[e] = (e == 0 || key[e - 1] != key[e]) ? e : 0;
-}
-
 __global__ void k_weff(const int32_t *__restrict__ w, const int64_t *__restrict__ runstart,
                        int64_t m, int32_t *weff) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
@@ -175,6 +169,45 @@ __global__ void k_wrange(const int32_t *__restrict__ w, int64_t m, int32_t *r) {
     if ((threadIdx.x & 31) == 0) {
         atomicMin(&r[0], lo);
         atomicMax(&r[1], hi);
+    }
+}
+
+// w_eff of a forward CSR: weight of the first slot of each run of equal
+// destinations within a row (get_edge's bisect_left, graph.py:56-62).
+__global__ void k_weff_csr(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+                           const int32_t *__restrict__ w, int64_t n, int32_t *weff) {
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t x = warp; x < n; x += nw) {
+        const int64_t r0 = off[x], r1 = off[x + 1];
+        for (int64_t e = r0 + lane_id(); e < r1; e += 32) {
+            const int32_t d = adj[e];
+            int64_t s = e;
+            while (s > r0 && adj[s - 1] == d) s--;  // duplicates are rare and short
+            weff[e] = w[s];
+        }
+    }
+}
+
+// Destination keys and source values of every forward slot, in slot order.
+__global__ void k_rev_pairs(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+                            int64_t n, uint32_t *dkey, uint32_t *sval) {
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t x = warp; x < n; x += nw)
+        for (int64_t e = off[x] + lane_id(); e < off[x + 1]; e += 32) {
+            dkey[e] = (uint32_t)adj[e];
+            sval[e] = (uint32_t)x;
+        }
+}
+
+// off[x] = first e with key[e] >= x (sorted 32-bit keys).
+__global__ void k_offsets32(const uint32_t *__restrict__ key, int64_t m, int64_t n, int64_t *off) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t prev = e == 0 ? -1 : (int64_t)key[e - 1];
+        int64_t cur = e == m ? n : (int64_t)key[e];
+        for (int64_t x = prev + 1; x <= cur; x++) off[x] = e;
     }
 }
 
@@ -351,7 +384,33 @@ int build_reverse_t(sp_graph *g, Call &c, bool want_adj, bool want_eid) {
     return SP_OK;
 }
 
+// Reverse adjacency only (the algorithm path): a stable LSD radix sort of
+// the b-bit destination keys carrying the source ids.  The input is in
+// forward slot order, i.e. (src, eid) order, so the stable sort yields
+// graph.py:92's (dst, src, eid) order with b/8 passes over 32-bit keys.
+int build_reverse_adj(sp_graph *g, Call &c) {
+    const int64_t n = g->n, m = g->m;
+    const int b = bits_for(n);
+    uint32_t *dk, *dks, *sv;
+    SP_TRY(c.alloc(&dk, m));
+    SP_TRY(c.alloc(&dks, m));
+    SP_TRY(c.alloc(&sv, m));
+    SP_TRY(dalloc(&g->roff, n + 1));
+    SP_TRY(dalloc(&g->radj, m));
+    k_rev_pairs<<<gridN(n * 32, c.device), 256, 0, c.stream>>>(g->off, g->adj, n, dk, sv);
+    if (m)
+        SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+            return cub::DeviceRadixSort::SortPairs(t, sz, dk, dks, sv,
+                                                   reinterpret_cast<uint32_t *>(g->radj), m, 0,
+                                                   b, c.stream);
+        }));
+    k_offsets32<<<gridN(m + 1, c.device), 256, 0, c.stream>>>(dks, m, n, g->roff);
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
 int build_reverse(sp_graph *g, Call &c, bool want_adj, bool want_eid) {
+    if (want_adj && !want_eid) return build_reverse_adj(g, c);
     if (g->m < (int64_t)0xFFFFFFFFll) return build_reverse_t<uint32_t>(g, c, want_adj, want_eid);
     return build_reverse_t<uint64_t>(g, c, want_adj, want_eid);
 }
@@ -522,6 +581,27 @@ int unique_keys(Call &c, uint64_t *key, int64_t ne, uint64_t **uniq, int64_t *nu
 
 }  // namespace
 
+namespace sp {
+
+// w_eff on first use (graphs adopted from a CSR defer it; see from_csr).
+int ensure_weff(sp_graph *g, Call &c) {
+    std::lock_guard<std::mutex> lk(g_lazy_mu);
+    if (g->weff || g->m == 0) return SP_OK;
+    int32_t *weff = nullptr;
+    SP_TRY(dalloc(&weff, g->m));
+    k_weff_csr<<<gridN(g->n * 32, c.device), 256, 0, c.stream>>>(g->off, g->adj, g->w, g->n, weff);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+    if (e != cudaSuccess) {
+        cudaFree(weff);
+        SP_CUDA(e);
+    }
+    g->weff = weff;
+    return SP_OK;
+}
+
+}  // namespace sp
+
 extern "C" {
 
 int sp_graph_from_edges(const int32_t *u, const int32_t *v, const int32_t *w, int64_t nedges,
@@ -570,27 +650,10 @@ int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj, const int32_t 
         if ((rc = dalloc(&g->off, n + 1))) break;
         if ((rc = dalloc(&g->adj, m))) break;
         if ((rc = dalloc(&g->w, m))) break;
-        if ((rc = dalloc(&g->weff, m))) break;
         if ((rc = to_device(g->off, offsets, (n + 1) * 8, mem, c.stream))) break;
         if ((rc = to_device(g->adj, adj, m * 4, mem, c.stream))) break;
         if ((rc = to_device(g->w, weights, m * 4, mem, c.stream))) break;
-        if (m) {
-            // w_eff: run starts of equal destinations within each row
-            int b = bits_for(n);
-            uint64_t *key;
-            int64_t *runstart;
-            if ((rc = c.alloc(&key, m))) break;
-            if ((rc = c.alloc(&runstart, m))) break;
-            // key = (dst << b | src): equal neighbours <=> same (src, dst) pair
-            k_rev_keys<<<gridN(n * 32, c.device), 256, 0, c.stream>>>(g->off, g->adj, n, b, key);
-            k_runstart<<<gridN(m, c.device), 256, 0, c.stream>>>(key, m, runstart);
-            if ((rc = cub_call(c, [&](void *t, size_t &sz) {
-                     return cub::DeviceScan::InclusiveScan(t, sz, runstart, runstart, MaxOp(), m,
-                                                           c.stream);
-                 })))
-                break;
-            k_weff<<<gridN(m, c.device), 256, 0, c.stream>>>(g->w, runstart, m, g->weff);
-        }
+        // w_eff is built on first use (ensure_weff): PR/BC/TC never read it
         if ((rc = finish_graph(g, c))) break;
         rc = c.finish(nullptr);
     } while (0);
@@ -682,7 +745,15 @@ int sp_graph_download(const sp_graph *cg, int which, void *dst) {
         case SP_ARR_WEIGHTS: src = g->w; bytes = g->m * 4; break;
         case SP_ARR_REV_OFFSETS: src = g->roff; bytes = (g->n + 1) * 8; break;
         case SP_ARR_REV_ADJ: src = g->radj; bytes = g->m * 4; break;
-        case SP_ARR_WEFF: src = g->weff; bytes = g->m * 4; break;
+        case SP_ARR_WEFF: {
+            Call c;
+            SP_TRY(c.begin(g->device));
+            SP_TRY(ensure_weff(g, c));
+            SP_TRY(c.finish(nullptr));
+            src = g->weff;
+            bytes = g->m * 4;
+            break;
+        }
         case SP_ARR_REV_EID: {
             std::lock_guard<std::mutex> lk(g_lazy_mu);
             if (!g->reid && g->m) {

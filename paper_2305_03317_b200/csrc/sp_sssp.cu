@@ -77,6 +77,7 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
     SP_CHECK(src >= 0 && src < g->n, SP_ERR_ARG, "node argument 'src'=%d out of range", src);
     Call c;
     SP_TRY(c.begin(g->device));
+    SP_TRY(ensure_weff(g, c));
     const int64_t n = g->n;
     int32_t *dist, *enq, *qa, *qb;
     uint2 *chunks;

@@ -190,6 +190,8 @@ def _new_handle(fn, *args, what: str) -> C.c_void_p:
 
 def _as_i32(a, what: str) -> np.ndarray:
     a = np.asarray(a)
+    if a.dtype == np.int32:  # already in range: no O(m) host scan
+        return np.ascontiguousarray(a)
     if a.size and a.dtype.kind in "iu":
         lo, hi = int(a.min()), int(a.max())
         if lo < _I32_MIN or hi > _I32_MAX:
