@@ -350,6 +350,7 @@ def pr_distributed(sp, _lib, g, a, world, rank, local):
     eps, max_iter = PR_ARGS["epsilon"], PR_ARGS["maxIter"]
 
     def one_run():
+        torch.cuda.current_stream().synchronize()
         L.sp_pagerank_block_init(g.handle, v0, v1, C.c_void_p(rank_local.data_ptr()),
                                  C.c_void_p(contrib_local.data_ptr()))
         dist.all_gather_into_tensor(contrib_full, contrib_local)
@@ -358,6 +359,7 @@ def pr_distributed(sp, _lib, g, a, world, rank, local):
         kms = 0.0
         while True:
             st = _lib.Stats()
+            torch.cuda.current_stream().synchronize()  # collectives done before the native step
             rc = L.sp_pagerank_block_step(g.handle, v0, v1, PR_ARGS["damping"],
                                           C.c_void_p(contrib_full.data_ptr()),
                                           C.c_void_p(rank_local.data_ptr()),

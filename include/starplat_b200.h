@@ -121,6 +121,18 @@ void sp_graph_destroy(sp_graph *g);
 int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist, int mem,
             int64_t *iters, sp_iter_cb cb, void *user, sp_stats *st);
 
+/* Block-partitioned SSSP supersteps (multi-GPU; graph.py:226-249 ownership,
+ * the exchange is the caller's all-reduce(min) of dist between steps; this
+ * replaces the BSP model of bsp.py:393-417 with convergence evaluated after
+ * the exchange).  dist[n] and last[n] are device arrays,
+ * replicated on every rank.  A step takes F = {v in [v0, v1): dist[v] <
+ * last[v]}, sets last[v] = dist[v] on F and relaxes F's rows into dist
+ * (atomicMin, any destination); *frontier = |F|, *relaxed = slots scanned.
+ * The run has converged when a step's summed |F| over all ranks is 0. */
+int sp_sssp_block_init(sp_graph *g, int32_t src, int32_t *dist, int32_t *last);
+int sp_sssp_block_step(sp_graph *g, int64_t v0, int64_t v1, int32_t *dist,
+                       int32_t *last, int64_t *frontier, int64_t *relaxed);
+
 /* corpus/programs/pr.sp.  rank[n] = final ranks (== rank_nxt at exit);
  * iter / diff = the program's scalars; iters = fixedPoint iterations. */
 int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t max_iter,

@@ -152,3 +152,115 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
     }
     return rc;
 }
+
+// ---- block-partitioned supersteps (multi-GPU, graph.py:226-249 ownership)
+namespace {
+
+// Relaxation without a next-frontier queue: ownership decides the frontier
+// after the exchange (k_block_frontier), not the relaxing rank.
+struct RelaxNoPushOp {
+    using Payload = int;
+    using Probe = RelaxOp::Probe;
+    int32_t *__restrict__ dist;
+    const int32_t *__restrict__ weff;
+    unsigned long long *overflow;
+    __device__ __forceinline__ int payload(int32_t v) const { return __ldcg(dist + v); }
+    __device__ __forceinline__ Probe probe(int64_t e, int32_t x) const {
+        return Probe{__ldg(weff + e), __ldcg(dist + x)};
+    }
+    __device__ __forceinline__ bool apply(int dv, int64_t, int32_t x, Probe p) const {
+        const int64_t cand = (int64_t)dv + (int64_t)p.w;
+        if (cand >= (int64_t)kIntMax) return false;
+        if (cand < (int64_t)(-2147483647 - 1)) {
+            atomicAdd(overflow, 1ull);
+            return false;
+        }
+        if ((int)cand < p.dx) atomicMin(dist + x, (int)cand);
+        return false;
+    }
+};
+
+// F = {v in [v0, v1): dist[v] < last[v]}; last[v] = dist[v] for v in F.
+__global__ void k_block_frontier(const int32_t *__restrict__ dist, int32_t *__restrict__ last,
+                                 int64_t v0, int64_t v1, int32_t *q, unsigned long long *cnt) {
+    for (int64_t b = v0 + blockIdx.x * (int64_t)blockDim.x; b < v1;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = b + threadIdx.x;
+        int32_t d = 0;
+        bool in = false;
+        if (v < v1) {
+            d = dist[v];
+            in = d < last[v];
+        }
+        const int64_t slot = warp_append(in, cnt);
+        if (in) {
+            q[slot] = (int32_t)v;
+            last[v] = d;
+        }
+    }
+}
+
+__global__ void k_block_init(int32_t *dist, int32_t *last, int64_t n, int32_t src) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        dist[x] = x == src ? 0 : kIntMax;
+        last[x] = kIntMax;
+    }
+}
+
+}  // namespace
+
+extern "C" int sp_sssp_block_init(sp_graph *g, int32_t src, int32_t *dist, int32_t *last) {
+    SP_CHECK(g && dist && last, SP_ERR_ARG, "sp_sssp_block_init: bad arguments");
+    SP_CHECK(src >= 0 && src < g->n, SP_ERR_ARG, "node argument 'src'=%d out of range", src);
+    Call c;
+    SP_TRY(c.begin(g->device));
+    SP_TRY(ensure_weff(g, c));
+    k_block_init<<<grid_for(g->n, kBlock, c.device), kBlock, 0, c.stream>>>(dist, last, g->n, src);
+    c.launches++;
+    SP_CUDA(cudaGetLastError());
+    return c.finish(nullptr);
+}
+
+extern "C" int sp_sssp_block_step(sp_graph *g, int64_t v0, int64_t v1, int32_t *dist,
+                                  int32_t *last, int64_t *frontier, int64_t *relaxed) {
+    SP_CHECK(g && dist && last && v0 >= 0 && v0 <= v1 && v1 <= g->n, SP_ERR_ARG,
+             "sp_sssp_block_step: bad arguments");
+    Call c;
+    SP_TRY(c.begin(g->device));
+    SP_TRY(ensure_weff(g, c));
+    const int64_t nb = std::max<int64_t>(1, v1 - v0);
+    int32_t *q, *qn;
+    uint2 *chunks;
+    ExpandCounters *cnt;
+    SP_TRY(c.alloc(&q, nb));
+    SP_TRY(c.alloc(&qn, 1));
+    SP_TRY(c.alloc(&chunks, expand_chunk_capacity(g->m)));
+    SP_TRY(c.alloc(&cnt, 2));
+    SP_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(ExpandCounters), c.stream));
+    ExpandCounters *h;
+    SP_TRY(c.host_as(&h));
+    if (v1 > v0) {
+        k_block_frontier<<<grid_for(v1 - v0, kBlock, c.device), kBlock, 0, c.stream>>>(
+            dist, last, v0, v1, q, &cnt[1].next_size);
+        c.launches++;
+    }
+    SP_CUDA(cudaMemcpyAsync(h, &cnt[1], sizeof(ExpandCounters), cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t nq = (int64_t)h->next_size;
+    if (nq) {
+        RelaxNoPushOp op{dist, g->weff, &cnt->flag};
+        launch_expand(op, g->off, g->adj, q, nq, qn, chunks, cnt, num_sms(c.device),
+                      g->max_outdeg > kSplit, c.stream, &c.launches);
+        SP_CUDA(cudaGetLastError());
+        SP_CUDA(cudaMemcpyAsync(h, cnt, sizeof(ExpandCounters), cudaMemcpyDeviceToHost, c.stream));
+    } else {
+        h->scanned = 0;
+        h->flag = 0;
+    }
+    SP_TRY(c.finish(nullptr));
+    SP_CHECK(!h->flag, SP_ERR_OVERFLOW, "SSSP distance left the int32 range (negative weights)");
+    if (frontier) *frontier = nq;
+    if (relaxed) *relaxed = (int64_t)h->scanned;
+    return SP_OK;
+}

@@ -1,0 +1,302 @@
+"""Multi-GPU runs of the corpus programs: one process per GPU over
+``torch.distributed`` (NCCL on the GPUs; any backend for the host logic).
+
+``run_sharded(tp, g, args, ...)`` returns the same ``RunResult`` as
+``interp.run`` on every rank.  Each program shards the way SURVEY.md 8e lays
+out (the reference models multi-rank execution in-process in
+trident/bsp.py; its ownership rule is graph.py:226-249):
+
+* BC  -- sources round-robin over ranks in list order, graph replicated;
+         one ``all_reduce(sum)`` of the bc array at the end; sigma/delta of
+         the last source come from the rank that ran it (broadcast).  No
+         data-path collective.
+* TC  -- vertex ranges balanced by a sum-of-squared-degree work proxy, graph
+         replicated; one integer ``all_reduce(sum)`` (exact).
+* PR  -- block partition; per iteration a local pull over the owned block,
+         ``all_gather`` of the owned contrib slices (the reference's
+         remote-read snapshot, bsp.py:182-185/287-288) and ``all_reduce(max)``
+         of diff (the scalar merge, bsp.py:322-330).
+* SSSP -- block partition with replicated distance arrays; per superstep the
+         owned frontier (owned vertices whose distance dropped since their
+         last expansion) is relaxed into the local copy, then
+         ``all_reduce(min)`` merges all ranks' candidates (the aggregated
+         min-messages of bsp.py:45-72, dense form) and ``all_reduce(sum)`` of
+         the frontier sizes decides convergence -- evaluated AFTER the
+         exchange, which is exactly what bsp.py:393-417 gets wrong.
+
+The per-rank compute is a backend object; ``NativeBackend`` drives
+libstarplat_b200.so on this rank's GPU.  The tests substitute a CPU backend
+(tests/oracle_backend.py) to run this module's host logic on gloo.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+
+from . import _lib, corpus
+from .errors import errors_for
+from .graph import block_partition, device_graph
+from .interp import PropertyEnv, RunResult, check_args, default_iteration_cap
+
+
+class NativeBackend:
+    """Per-rank compute on a CUDA device through the C ABI (no fallback)."""
+
+    def __init__(self, device: int):
+        import torch
+        self.torch = torch
+        self.device = torch.device("cuda", device)
+        self.index = device
+        _lib.require_device(device)
+        self.L = _lib.lib()
+
+    def _fence(self):
+        # the native calls run on their own streams (and sync them before
+        # returning); torch's copies and collectives run on torch's current
+        # stream, so that work must be complete before a native call reads it
+        self.torch.cuda.current_stream(self.device).synchronize()
+
+    def _chk(self, rc, what):
+        if rc != _lib.SP_OK:
+            raise RuntimeError(f"{what} failed ({rc}): {_lib.last_error()}")
+
+    def graph(self, g):
+        return device_graph(g, self.index)
+
+    def offsets(self, g) -> np.ndarray:
+        return np.asarray(g.offsets)
+
+    # -- BC
+    def bc(self, g, srcs, deterministic):
+        t = self.torch
+        n = g.n
+        bc = t.zeros(max(1, n), dtype=t.float64, device=self.device)[:n]
+        sg = t.zeros(max(1, n), dtype=t.float64, device=self.device)[:n]
+        dl = t.zeros(max(1, n), dtype=t.float64, device=self.device)[:n]
+        self._fence()
+        if len(srcs):
+            s = np.asarray(srcs, dtype=np.int32)
+            flags = _lib.SP_FLAG_DETERMINISTIC if deterministic else 0
+            rc = self.L.sp_bc(g.handle, s.ctypes.data_as(C.c_void_p), len(s), flags,
+                              C.c_void_p(bc.data_ptr()), C.c_void_p(sg.data_ptr()),
+                              C.c_void_p(dl.data_ptr()), _lib.SP_MEM_DEVICE, None)
+            self._chk(rc, "sp_bc")
+        return bc, sg, dl
+
+    # -- TC
+    def tc(self, g, v0, v1) -> int:
+        self._fence()
+        cnt = C.c_uint64()
+        self._chk(self.L.sp_tc(g.handle, int(v0), int(v1), C.byref(cnt), None), "sp_tc")
+        return int(cnt.value)
+
+    # -- PR
+    def pr_init(self, g, v0, v1):
+        t = self.torch
+        nb = max(1, v1 - v0)
+        rank = t.empty(nb, dtype=t.float64, device=self.device)
+        contrib = t.empty(nb, dtype=t.float64, device=self.device)
+        self._fence()
+        self._chk(self.L.sp_pagerank_block_init(g.handle, int(v0), int(v1),
+                                                C.c_void_p(rank.data_ptr()),
+                                                C.c_void_p(contrib.data_ptr())),
+                  "sp_pagerank_block_init")
+        return rank, contrib
+
+    def pr_step(self, g, v0, v1, damping, contrib_full, rank, contrib, deterministic) -> float:
+        self._fence()
+        diff = C.c_double()
+        flags = _lib.SP_FLAG_DETERMINISTIC if deterministic else 0
+        self._chk(self.L.sp_pagerank_block_step(
+            g.handle, int(v0), int(v1), float(damping), C.c_void_p(contrib_full.data_ptr()),
+            C.c_void_p(rank.data_ptr()), C.c_void_p(contrib.data_ptr()), C.byref(diff), flags,
+            None), "sp_pagerank_block_step")
+        return float(diff.value)
+
+    # -- SSSP
+    def sssp_init(self, g, src):
+        t = self.torch
+        n = g.n
+        dist = t.empty(max(1, n), dtype=t.int32, device=self.device)
+        last = t.empty(max(1, n), dtype=t.int32, device=self.device)
+        self._fence()
+        rc = self.L.sp_sssp_block_init(g.handle, int(src), C.c_void_p(dist.data_ptr()),
+                                       C.c_void_p(last.data_ptr()))
+        self._chk(rc, "sp_sssp_block_init")
+        return dist, last
+
+    def sssp_step(self, g, v0, v1, dist, last):
+        self._fence()
+        f, r = C.c_int64(), C.c_int64()
+        rc = self.L.sp_sssp_block_step(g.handle, int(v0), int(v1), C.c_void_p(dist.data_ptr()),
+                                       C.c_void_p(last.data_ptr()), C.byref(f), C.byref(r))
+        if rc == _lib.SP_ERR_OVERFLOW:
+            raise OverflowError(_lib.last_error())
+        self._chk(rc, "sp_sssp_block_step")
+        return int(f.value), int(r.value)
+
+    def to_host(self, x):
+        return x.cpu().numpy()
+
+
+def _dist():
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        raise RuntimeError("run_sharded needs an initialised torch.distributed process group")
+    return dist
+
+
+def _all_gather_flat(full, part, group):
+    dist = _dist()
+    if dist.get_backend(group) == "gloo":  # no all_gather_into_tensor on gloo
+        chunks = list(full.chunk(dist.get_world_size(group)))
+        dist.all_gather(chunks, part, group=group)
+    else:
+        dist.all_gather_into_tensor(full, part, group=group)
+
+
+def tc_ranges(offsets: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """Contiguous vertex ranges with about equal sum of squared degrees (the
+    per-vertex intersection work grows with deg^2); covers [0, n) exactly."""
+    deg = np.diff(np.asarray(offsets, dtype=np.int64)).astype(np.float64)
+    n = len(deg)
+    w = np.cumsum(deg * deg + 1.0)
+    tot = w[-1] if n else 0.0
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(np.searchsorted(w, tot * r / world, side="left")) if n else 0)
+    cuts.append(n)
+    for i in range(1, len(cuts)):  # monotone even for degenerate inputs
+        cuts[i] = max(cuts[i], cuts[i - 1])
+    return [(cuts[i], cuts[i + 1]) for i in range(world)]
+
+
+def run_sharded(tp, g, args: dict, function: str | None = None,
+                max_iters: int | None = None, *, backend=None, group=None,
+                deterministic: bool = False) -> RunResult:
+    """Run a corpus program over all ranks of ``group`` (default: the world).
+    Every rank must call it with the same graph and arguments."""
+    dist = _dist()
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    if backend is None:
+        import torch
+        backend = NativeBackend(torch.cuda.current_device())
+    E = errors_for(tp)
+    prog = corpus.identify(tp, function)
+    dg = backend.graph(g)
+    bound = check_args(prog, dg, args, E)
+    cap = max_iters if max_iters is not None else default_iteration_cap(dg.n)
+    t0 = time.perf_counter()
+    fn = {"sssp": _sssp, "sssp_pull": _sssp, "pr": _pr, "bc": _bc, "tc": _tc}[prog.key]
+    env, fpi, stats = fn(backend, dg, bound, cap, world, me, group, deterministic, E, prog)
+    return RunResult(env=env, fixedpoint_iterations=fpi,
+                     wall_seconds=time.perf_counter() - t0, stats=stats)
+
+
+def _bc(be, g, bound, cap, world, me, group, det, E, prog):
+    dist = _dist()
+    srcs = bound["sourceSet"]
+    mine = srcs[me::world]
+    bc, sg, dl = be.bc(g, mine, det)
+    dist.all_reduce(bc, op=dist.ReduceOp.SUM, group=group)
+    env = PropertyEnv()
+    env.node_props = {"bc": be.to_host(bc)}
+    if srcs:
+        owner = (len(srcs) - 1) % world  # ran the last source of the list
+        glob = dist.get_global_rank(group, owner) if group is not None else owner
+        dist.broadcast(sg, src=glob, group=group)
+        dist.broadcast(dl, src=glob, group=group)
+        env.node_props.update(sigma=be.to_host(sg), delta=be.to_host(dl))
+    return env, {}, {"sources_local": len(mine)}
+
+
+def _tc(be, g, bound, cap, world, me, group, det, E, prog):
+    dist = _dist()
+    v0, v1 = tc_ranges(be.offsets(g), world)[me]
+    part = be.tc(g, v0, v1)
+    t = be.torch.tensor([part], dtype=be.torch.int64, device=be.device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    env = PropertyEnv(scalars={"triangle_count": int(t.item())})
+    return env, {}, {"range": (v0, v1), "local_count": part}
+
+
+def _pr(be, g, bound, cap, world, me, group, det, E, prog):
+    dist = _dist()
+    torch = be.torch
+    parts = block_partition(g, world)
+    per = parts[0].size
+    rr = parts[me].real_range()
+    v0, v1 = rr.start, rr.stop
+    rank_l, contrib_l = be.pr_init(g, v0, v1)
+    slice_l = torch.zeros(per, dtype=torch.float64, device=be.device)
+    full = torch.zeros(per * world, dtype=torch.float64, device=be.device)
+
+    def gather():
+        slice_l.zero_()
+        if v1 > v0:
+            slice_l[: v1 - v0] = contrib_l[: v1 - v0]
+        _all_gather_flat(full, slice_l, group)
+
+    gather()
+    it = 0
+    iters = 0
+    diff = 0.0
+    while True:
+        d = be.pr_step(g, v0, v1, bound["damping"], full, rank_l, contrib_l, det)
+        dt = torch.tensor([d], dtype=torch.float64, device=be.device)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX, group=group)
+        diff = float(dt.item())
+        gather()
+        it += 1
+        iters += 1
+        if diff < bound["epsilon"] or it >= bound["maxIter"]:  # pr.sp:10
+            break
+        if iters >= cap:
+            raise E.NonConvergenceError(prog.flag, cap)
+    # ranks back to every rank (owned slices, padded to per)
+    rl = torch.zeros(per, dtype=torch.float64, device=be.device)
+    if v1 > v0:
+        rl[: v1 - v0] = rank_l[: v1 - v0]
+    rfull = torch.zeros(per * world, dtype=torch.float64, device=be.device)
+    _all_gather_flat(rfull, rl, group)
+    rank = be.to_host(rfull)[: g.n].copy()
+    env = PropertyEnv(node_props={"rank": rank, "rank_nxt": rank.copy()},
+                      scalars={"iter": it, "diff": diff, "converged": True})
+    return env, {"converged": iters}, {"block": (v0, v1)}
+
+
+def _sssp(be, g, bound, cap, world, me, group, det, E, prog):
+    dist = _dist()
+    torch = be.torch
+    parts = block_partition(g, world)
+    rr = parts[me].real_range()
+    v0, v1 = rr.start, rr.stop
+    dvec, last = be.sssp_init(g, bound["src"])
+    steps = relaxed = 0
+    while True:
+        try:
+            f, r = be.sssp_step(g, v0, v1, dvec, last)
+            bad = 0
+        except OverflowError:
+            f, r, bad = 0, 0, 1
+        relaxed += r
+        dist.all_reduce(dvec, op=dist.ReduceOp.MIN, group=group)
+        fz = torch.tensor([f, bad], dtype=torch.int64, device=be.device)
+        dist.all_reduce(fz, op=dist.ReduceOp.SUM, group=group)
+        if int(fz[1].item()):
+            raise E.ExecError("SSSP distance left the int32 range (negative weights)")
+        if int(fz[0].item()) == 0:  # nobody had a frontier: the exchange changed nothing
+            break
+        steps += 1
+        if steps >= cap:
+            raise E.NonConvergenceError(prog.flag, cap)
+    n = g.n
+    d = be.to_host(dvec)[:n].copy()
+    env = PropertyEnv(node_props={"dist": d, "modified": np.zeros(n, dtype=bool),
+                                  "modified_nxt": np.zeros(n, dtype=bool)},
+                      scalars={"finished": True})
+    return env, {"finished": steps}, {"relaxed": relaxed, "block": (v0, v1)}

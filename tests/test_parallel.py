@@ -1,0 +1,107 @@
+"""Multi-rank host logic of paper_2305_03317_b200.parallel on gloo
+(world_size 2 and 3, CPU): sharding, exchange and convergence are checked
+against the single-process oracle -- never against trident.bsp.simulate,
+whose SSSP supersteps are wrong at nranks > 1."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import REPO  # noqa: F401  (sys.path set up)
+from oracle import cpu_ref
+from paper_2305_03317_b200 import corpus, gen, parallel
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _graph(kind, directed):
+    if kind == "rmat":
+        u, v, w, n = gen.rmat(7, 8, seed=3, undirected=not directed)
+    elif kind == "grid":
+        u, v, w, n = gen.grid(6, 7, seed=5)
+        directed = False
+    else:  # multigraph with parallel edges and self-loops
+        rng = np.random.default_rng(11)
+        n = 60
+        u = rng.integers(0, n, 500)
+        v = rng.integers(0, n, 500)
+        w = rng.integers(1, 20, 500)
+    return cpu_ref.build_csr(u, v, w, directed, n)
+
+
+def _worker(rank, world, port, kind, directed, q):
+    import torch.distributed as dist
+    from oracle_backend import OracleBackend
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = _graph(kind, directed)
+        be = OracleBackend()
+        out = {}
+        r = parallel.run_sharded(corpus.SSSP, g, {"src": 0}, backend=be)
+        out["dist"] = r.env.node_props["dist"]
+        args = {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
+        r = parallel.run_sharded(corpus.PR, g, args, backend=be)
+        out["rank"] = r.env.node_props["rank"]
+        out["iter"] = r.env.scalars["iter"]
+        srcs = [0, 5, 3, 5, 17, 1, 2]
+        r = parallel.run_sharded(corpus.BC, g, {"sourceSet": srcs}, backend=be)
+        out["bc"] = r.env.node_props["bc"]
+        out["sigma"] = r.env.node_props["sigma"]
+        out["delta"] = r.env.node_props["delta"]
+        r = parallel.run_sharded(corpus.TC, g, {}, backend=be)
+        out["tc"] = r.env.scalars["triangle_count"]
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kind,directed", [("rmat", True), ("rmat", False), ("grid", False),
+                                           ("multi", True), ("multi", False)])
+def test_sharded_matches_single_process_oracle(world, kind, directed):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, directed, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = _graph(kind, directed)
+    d_ref = cpu_ref.sssp(g, 0)[0]
+    rank_ref, it_ref, *_ = cpu_ref.pagerank(g)
+    srcs = [0, 5, 3, 5, 17, 1, 2]
+    bc_ref, sg_ref, dl_ref = cpu_ref.bc(g, srcs)
+    tc_ref = cpu_ref.tc(g)
+    for r in range(world):
+        o = res[r]
+        assert np.array_equal(o["dist"], d_ref)          # bit-exact
+        assert o["rank"].tobytes() == rank_ref.tobytes()  # same left folds per vertex
+        assert o["iter"] == it_ref
+        scale = max(1.0, float(np.abs(bc_ref).max()))
+        assert float(np.abs(o["bc"] - bc_ref).max()) <= 1e-12 * scale  # source order changes
+        assert np.array_equal(o["sigma"], sg_ref) and np.array_equal(o["delta"], dl_ref)
+        assert o["tc"] == tc_ref
+
+
+def test_tc_ranges_partition():
+    off = np.array([0, 5, 5, 9, 40, 41, 41, 60])
+    for world in (1, 2, 3, 8):
+        rs = parallel.tc_ranges(off, world)
+        assert rs[0][0] == 0 and rs[-1][1] == len(off) - 1
+        for (a, b), (c, d) in zip(rs, rs[1:]):
+            assert b == c and a <= b
