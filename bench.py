@@ -71,30 +71,49 @@ def ncu_traffic(kernel: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in
+    process through NVML (no nvidia-smi fork of the CUDA process); falls
+    back to nvidia-smi when NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+               "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period_s: float = 0.05):
         self.device = device
-        self.samples = []
+        self.period = period_s
+        self.samples = []  # (sm_mhz, max_mhz, reasons_mask, util)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            ut = nv.nvmlDeviceGetUtilizationRates(self._h).gpu
+            return float(sm), float(mx), int(rs), int(ut)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5).stdout.strip().split(",")
+        return float(out[0]), float(out[1]), int(out[2].strip(), 16), int(out[3])
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                    timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -108,17 +127,13 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        busy = [float(s[0]) for s in self.samples
-                if s[0].replace(".", "").isdigit() and s[6].isdigit() and int(s[6]) > 0]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if s[2 + i].lower() == "active"})
-        use = busy or sm
-        return {"sm_mhz": statistics.median(use) if use else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        busy = [s[0] for s in self.samples if s[3] > 0] or [s[0] for s in self.samples]
+        reasons = sorted({k for s in self.samples for k, bit in self.REASONS.items()
+                          if s[2] & bit})
+        return {"sm_mhz": statistics.median(busy),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def dist_env():
@@ -193,64 +208,79 @@ def run_reference(a):
 # our arm
 
 
+def timed(fn, steps, warmup, world, device):
+    """W untimed + K timed calls of fn, bracketed by a barrier and a device
+    sync on both sides; CUDA events on the current stream (every native call
+    syncs its own stream before returning, so the span holds all device
+    work); the max over ranks is returned.  Only the previous step's result
+    is alive during a step (as in a serving loop), so its outputs' memory is
+    recycled.  -> (total_ms, [per-step stats], last result)"""
+    import torch
+    import torch.distributed as dist
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    stats = []
+    r = None
+    for _ in range(steps):
+        r = fn()
+        stats.append(getattr(r, "stats", None))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    return ms, stats, r
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
 
     import paper_2305_03317_b200 as sp
-    from paper_2305_03317_b200 import _lib, corpus
+    from paper_2305_03317_b200 import corpus, parallel
 
     world, rank, local = dist_env()
+    # SP_BENCH_SHARE_GPU=1: every rank on cuda:0 over gloo -- exercises the
+    # N > 1 code path on a one-GPU box (not a measurement configuration)
+    share = os.environ.get("SP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     hbm_peak, peak_kind = peaks()
 
     g = sp.generate("rmat", SCALE, EF, seed=SEED, undirected=False, device=local)
     n, m = g.n, g.m
     bytes_pull = 12 * m + 36 * n
+    be = parallel.NativeBackend(local)
 
-    result = {}
+    if world == 1:
+        def step():
+            return sp.run(corpus.PR, g, PR_ARGS, device_outputs=True)
+    else:
+        def step():
+            return parallel.run_sharded(corpus.PR, g, PR_ARGS, backend=be)
+
     with ClockSampler(local) as clk:
-        if world == 1:
-            # warmup + timed steps (device-resident)
-            for _ in range(a.warmup):
-                sp.run(corpus.PR, g, PR_ARGS, device_outputs=True)
-            torch.cuda.synchronize()
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            t_wall0 = time.perf_counter()
-            main_ms = 0.0
-            main_launches = launches = 0
-            dev_ms = []
-            for _ in range(a.steps):
-                r = sp.run(corpus.PR, g, PR_ARGS, device_outputs=True)
-                st = r.stats
-                dev_ms.append(st["device_ms"])
-                main_ms += st["main_kernel_ms"]
-                main_launches += st["main_kernel_launches"]
-                launches += st["kernel_launches"]
-            ev1.record()
-            torch.cuda.synchronize()
-            t_wall = time.perf_counter() - t_wall0
-            iters = r.env.scalars["iter"]
-            # K steps bracketed by CUDA events after a device sync on both sides;
-            # each call runs on its own stream and syncs before returning, so
-            # this span holds all device work plus the per-iteration host reads
-            total_ms = ev0.elapsed_time(ev1)
-            result.update(iters=iters, total_ms=total_ms, wall_s=t_wall, main_ms=main_ms,
-                          main_launches=main_launches, launches=launches,
-                          call_device_ms=sum(dev_ms))
-        else:
-            total_ms, iters, launches, main_ms, main_launches = pr_distributed(
-                sp, _lib, g, a, world, rank, local)
-            result.update(iters=iters, total_ms=total_ms, main_ms=main_ms,
-                          main_launches=main_launches, launches=launches)
-    ms_per_step = result["total_ms"] / a.steps
-    value = result["iters"] * m / (ms_per_step / 1e3) / 1e9
-    mean_pull_ms = result["main_ms"] / max(1, result["main_launches"])
-    achieved = bytes_pull / (mean_pull_ms / 1e3) / 1e9
+        total_ms, st, r = timed(step, a.steps, a.warmup, world, dev)
+    iters = r.env.scalars["iter"]
+    ms_per_step = total_ms / a.steps
+    value = iters * m / (ms_per_step / 1e3) / 1e9
     line = {
         "metric": BASELINE_METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
@@ -258,29 +288,36 @@ def run_ours(a):
         "data": f"synthetic RMAT-{SCALE} (ef {EF}, seed {SEED}, dedup, no self-loops), "
                 "generated on device",
         "config": {"workload": "pagerank_rmat22", "graph": f"rmat{SCALE}", "n": n, "m": m,
-                   **PR_ARGS, "iterations": result["iters"],
-                   "parallelism": f"block{world}" if world > 1 else "single",
+                   **PR_ARGS, "iterations": iters,
+                   "parallelism": f"block{world}+nccl" if world > 1 else "single",
                    "l2": "no flush: radj (4m = %.0f MB) + roff exceed the 126 MB L2; "
                          "contrib (8n = %.0f MB) is L2-resident by design"
                          % (4 * m / 1e6, 8 * n / 1e6)},
-        "roofline": {"bound": "hbm", "kernel": "k_pr_units+k_pr_fix+k_pr_epi (one PR iteration)",
-                     "achieved": achieved,
-                     "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": ncu_traffic("pr_iteration"),
-                     "algorithmic_bytes_per_launch": bytes_pull,
-                     "mean_launch_ms": mean_pull_ms,
-                     "note": "12 B/slot (radj 4 + contrib gather 8) + 36 B/vertex; gathers "
-                             "hit L2, so frac > 1 is possible"},
-        "gpu_launches": result["launches"],
-        "call_device_ms_per_step": result.get("call_device_ms", result["total_ms"]) / a.steps,
         "clocks": clk.summary(),
     }
     if world == 1:
-        line["e2e"] = e2e_pr(sp, corpus, g, a)
-        if not a.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(g)
-        if a.algos:
-            line["algorithms"] = other_algorithms(sp, corpus, a, hbm_peak)
+        main_ms = sum(s["main_kernel_ms"] for s in st)
+        main_launches = sum(s["main_kernel_launches"] for s in st)
+        mean_ms = main_ms / max(1, main_launches)
+        achieved = bytes_pull / (mean_ms / 1e3) / 1e9
+        line["roofline"] = {
+            "bound": "hbm", "kernel": "k_pr_units+k_pr_fix+k_pr_epi (one PR iteration)",
+            "achieved": achieved, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": ncu_traffic("pr_iteration"),
+            "algorithmic_bytes_per_launch": bytes_pull, "mean_launch_ms": mean_ms,
+            "note": "12 B/slot (radj 4 + contrib gather 8) + 36 B/vertex (SURVEY 8d); the "
+                    "contrib gathers hit L2, so frac > 1 is possible"}
+        line["gpu_launches"] = sum(s["kernel_launches"] for s in st)
+        line["call_device_ms_per_step"] = sum(s["device_ms"] for s in st) / a.steps
+    else:
+        line["gpu_launches"] = None  # counted per rank by the native calls; not aggregated
+    line["e2e"] = e2e_pr(sp, corpus, parallel, g, a, world, dev, be)
+    if world == 1 and not a.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(g)
+    g.close()
+    if a.algos:
+        line["algorithms"] = other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world,
+                                              dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -289,33 +326,32 @@ def run_ours(a):
     return 0
 
 
-def e2e_pr(sp, corpus, g, a):
-    """Public-API PR with host buffers each step (pinned CSR in, ranks out)."""
+def e2e_pr(sp, corpus, parallel, g, a, world, dev, be):
+    """Public-API PR with host buffers every step: pinned host CSR ->
+    sp.from_csr (H2D + on-device reverse CSR) -> run -> ranks on the host."""
     import torch
-    off = torch.from_numpy(np.asarray(g.offsets)).pin_memory().numpy()
-    adj = torch.from_numpy(np.asarray(g.adj)).pin_memory().numpy()
-    w = torch.from_numpy(np.asarray(g.weights)).pin_memory().numpy()
+    off = torch.from_numpy(np.array(g.offsets)).pin_memory().numpy()
+    adj = torch.from_numpy(np.array(g.adj)).pin_memory().numpy()
+    w = torch.from_numpy(np.array(g.weights)).pin_memory().numpy()
     h2d = off.nbytes + adj.nbytes + w.nbytes
     d2h = 8 * g.n
 
     def step():
-        gg = sp.from_csr(off, adj, w, directed=True, device=g.device)
-        r = sp.run(corpus.PR, gg, PR_ARGS)
-        rank = r.env.node_props["rank"]
+        gg = sp.from_csr(off, adj, w, directed=True, device=dev.index)
+        if world == 1:
+            r = sp.run(corpus.PR, gg, PR_ARGS)
+        else:
+            r = parallel.run_sharded(corpus.PR, gg, PR_ARGS, backend=be)
+        assert isinstance(r.env.node_props["rank"], np.ndarray)
         gg.close()
-        return r, rank
+        return r
 
-    for _ in range(max(1, min(a.warmup, 2))):
-        step()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
     k = max(1, min(a.steps, 3))
-    for _ in range(k):
-        r, _ = step()
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / k
+    ms, _, r = timed(step, k, max(1, min(a.warmup, 2)), world, dev)
+    dt = ms / k / 1e3
     return {"value": r.env.scalars["iter"] * g.m / dt / 1e9, "unit": "GTEPS",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
+            "steps": k,
             "includes": "H2D CSR (pinned) + device reverse-CSR build + PR + D2H ranks"}
 
 
@@ -331,122 +367,68 @@ def cpu_baseline(g):
                 "sample": f"failed: {e}"}
 
 
-def pr_distributed(sp, _lib, g, a, world, rank, local):
-    """Block-partitioned PR over NCCL: local pull on the owned block, then
-    all_gather of contrib slices + all_reduce(max) of diff per iteration."""
-    import ctypes as C
-
-    import torch
-    import torch.distributed as dist
-    parts = sp.block_partition(g, world)
-    per = parts[0].size
-    v0, v1 = parts[rank].real_range().start, parts[rank].real_range().stop
-    L = _lib.lib()
-    dev = torch.device("cuda", local)
-    contrib_full = torch.zeros(per * world, dtype=torch.float64, device=dev)
-    rank_local = torch.zeros(max(1, per), dtype=torch.float64, device=dev)
-    contrib_local = torch.zeros(max(1, per), dtype=torch.float64, device=dev)
-    diff = C.c_double()
-    eps, max_iter = PR_ARGS["epsilon"], PR_ARGS["maxIter"]
-
-    def one_run():
-        torch.cuda.current_stream().synchronize()
-        L.sp_pagerank_block_init(g.handle, v0, v1, C.c_void_p(rank_local.data_ptr()),
-                                 C.c_void_p(contrib_local.data_ptr()))
-        dist.all_gather_into_tensor(contrib_full, contrib_local)
-        it = 0
-        launches = 0
-        kms = 0.0
-        while True:
-            st = _lib.Stats()
-            torch.cuda.current_stream().synchronize()  # collectives done before the native step
-            rc = L.sp_pagerank_block_step(g.handle, v0, v1, PR_ARGS["damping"],
-                                          C.c_void_p(contrib_full.data_ptr()),
-                                          C.c_void_p(rank_local.data_ptr()),
-                                          C.c_void_p(contrib_local.data_ptr()),
-                                          C.byref(diff), 0, C.byref(st))
-            assert rc == 0, _lib.last_error()
-            launches += st.kernel_launches
-            kms += st.device_ms
-            dt = torch.tensor([diff.value], dtype=torch.float64, device=dev)
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-            dist.all_gather_into_tensor(contrib_full, contrib_local)
-            it += 1
-            if float(dt.item()) < eps or it >= max_iter:
-                return it, launches, kms
-
-    for _ in range(a.warmup):
-        one_run()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    launches = 0
-    kms = 0.0
-    for _ in range(a.steps):
-        it, l, k = one_run()
-        launches += l
-        kms += k
-    e1.record()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    return float(ms.item()), it, launches, kms, it * a.steps
+def _line(name, graph, g, ms, edges, model_bytes, hbm_peak, **extra):
+    t = ms / 1e3
+    d = {"graph": graph, "n": g.n, "m": g.m, "ms": ms, "gteps": edges / t / 1e9}
+    if model_bytes:
+        d["roofline"] = {"achieved": model_bytes / t / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": model_bytes / t / 1e9 / hbm_peak,
+                         "model_bytes": model_bytes}
+    d.update(extra)
+    return d
 
 
-def other_algorithms(sp, corpus, a, hbm_peak):
-    """SSSP cfg1, BC cfg4 (256 sources), TC cfg3 at one GPU."""
+def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
+    """SSSP cfg1, BC cfg4 (256 sources), TC cfg3; sharded over the ranks
+    when N > 1 (BC sources, TC ranges, SSSP block supersteps)."""
     out = {}
     reps = 3
+
+    def go(prog, g, args):
+        if world == 1:
+            return sp.run(prog, g, args, device_outputs=True)
+        return parallel.run_sharded(prog, g, args, backend=be)
+
     if "sssp" in a.algos:
-        g = sp.generate("rmat", 16, 16, seed=SEED)
-        for _ in range(2):
-            sp.run(corpus.SSSP, g, {"src": 0})
-        ms, R, F, km = [], 0, 0, 0.0
-        for _ in range(reps):
-            r = sp.run(corpus.SSSP, g, {"src": 0})
-            ms.append(r.stats["device_ms"])
-            R, F, km = r.stats["edges_visited"], r.stats["vertices_visited"], r.stats["main_kernel_ms"]
-        t = statistics.median(ms) / 1e3
+        g = sp.generate("rmat", 16, 16, seed=SEED, device=dev.index)
+        ms, _, r = timed(lambda: go(corpus.SSSP, g, {"src": 0}), reps, 2, world, dev)
         offs = np.asarray(g.offsets)
-        d = r.env.node_props["dist"]
-        reached = d < 2147483647
-        m_reached = int((offs[1:] - offs[:-1])[reached].sum())
-        b = 12 * R + 20 * F
-        out["sssp_cfg1"] = {"graph": "rmat16 directed", "n": g.n, "m": g.m,
-                            "gteps": m_reached / t / 1e9, "relax_per_s": R / t / 1e9,
-                            "ms": t * 1e3, "iterations": r.fixedpoint_iterations["finished"],
-                            "roofline_frac": b / (km / 1e3) / 1e9 / hbm_peak,
-                            "note": "launch/latency-bound (m ~ 1M)"}
+        d = np.asarray(r.env.node_props["dist"].cpu() if world == 1 else
+                       r.env.node_props["dist"])
+        m_reached = int((offs[1:] - offs[:-1])[d < 2147483647].sum())
+        mb = None
+        if world == 1:
+            R, F = r.stats["edges_visited"], r.stats["vertices_visited"]
+            mb = 12 * R + 20 * F
+        out["sssp_cfg1"] = _line("sssp", "rmat16 directed", g, ms / reps, m_reached, mb,
+                                 hbm_peak, iterations=r.fixedpoint_iterations["finished"],
+                                 note="Graph500 GTEPS = edges of reached vertices / time; "
+                                      "m ~ 1M: launch/latency-bound")
         g.close()
     if "bc" in a.algos:
-        g = sp.generate("rmat", 20, 16, seed=SEED, undirected=True)
+        g = sp.generate("rmat", 20, 16, seed=SEED, undirected=True, device=dev.index)
         deg = np.diff(np.asarray(g.offsets))
-        cand = np.flatnonzero(deg > 0)
-        srcs = np.random.default_rng(SEED).choice(cand, size=256, replace=False).tolist()
-        sp.run(corpus.BC, g, {"sourceSet": srcs[:8]})
-        r = sp.run(corpus.BC, g, {"sourceSet": srcs})
-        st = r.stats
-        t = st["device_ms"] / 1e3
-        b = 48 * st["edges_visited"] + 64 * st["vertices_visited"]
-        out["bc_cfg4"] = {"graph": "rmat20 symmetrized", "n": g.n, "m": g.m, "sources": 256,
-                          "gteps": st["edges_visited"] / t / 1e9, "ms": t * 1e3,
-                          "roofline_frac": b / t / 1e9 / hbm_peak}
+        srcs = np.random.default_rng(SEED).choice(np.flatnonzero(deg > 0), size=256,
+                                                  replace=False).tolist()
+        ms, _, r = timed(lambda: go(corpus.BC, g, {"sourceSet": srcs}), 1, 1, world, dev)
+        st = r.stats  # summed over ranks when sharded
+        out["bc_cfg4"] = _line("bc", "rmat20 symmetrized", g, ms, st["edges_visited"],
+                               st["model_bytes"], hbm_peak, sources=256,
+                               sharding=f"sources/{world}",
+                               note="GTEPS = slots of the reached vertices summed over "
+                                    "sources / time; roofline per SURVEY 8d (48 B/slot + "
+                                    "64 B/vertex per source), aggregate over all GPUs")
         g.close()
     if "tc" in a.algos:
-        g = sp.generate("uniform", 1 << 24, 1 << 28, seed=SEED, undirected=True)
-        sp.run(corpus.TC, g, {})
-        ms = []
-        for _ in range(reps):
-            r = sp.run(corpus.TC, g, {})
-            ms.append(r.stats["main_kernel_ms"])
-        t = statistics.median(ms) / 1e3
-        pairs = r.stats["edges_visited"]
-        out["tc_cfg3"] = {"graph": "uniform 2^24 / 2^28 undirected", "n": g.n, "m": g.m,
-                          "triangles": r.env.scalars["triangle_count"],
-                          "gteps": (g.m // 2) / t / 1e9, "ms": t * 1e3, "pairs": pairs}
+        g = sp.generate("uniform", 1 << 24, 1 << 28, seed=SEED, undirected=True,
+                        device=dev.index)
+        go(corpus.TC, g, {})  # builds the cached upper CSR (graph preprocessing)
+        ms, _, r = timed(lambda: go(corpus.TC, g, {}), reps, 1, world, dev)
+        mb = r.stats.get("model_bytes")
+        out["tc_cfg3"] = _line("tc", "uniform 2^24 / 2^28 undirected", g, ms / reps,
+                               g.m // 2, mb, hbm_peak,
+                               triangles=r.env.scalars["triangle_count"],
+                               sharding=f"ranges/{world}")
         g.close()
     return out
 
@@ -454,8 +436,8 @@ def other_algorithms(sp, corpus, a, hbm_peak):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--algos", default="sssp,bc,tc",
                     help="secondary algorithms at N=1 ('' to skip)")

@@ -45,6 +45,8 @@ int num_sms(int device);
 // default pool, release threshold raised so repeated calls reuse memory).
 int scratch_alloc(void **p, size_t bytes, cudaStream_t s);
 void scratch_free(void *p, cudaStream_t s);
+int resident_alloc(void **p, size_t bytes);  // graph arrays (pool, any stream)
+void resident_free(void *p);
 constexpr size_t kPinnedBlock = 4096;
 void *pinned_get();
 void pinned_put(void *p);
@@ -58,6 +60,7 @@ struct Call {
     int nbufs = 0;
     int64_t launches = 0;
     void *pinned = nullptr;  // kPinnedBlock bytes of pinned host memory
+    bool owned = true;       // stream/events belong to this call (else thread-cached)
     int begin(int dev);
     // this call's pinned host block (recycled across calls)
     int host(void **p);

@@ -323,35 +323,32 @@ int gridN(int64_t work, int dev) { return grid_for(work, 256, dev, 16); }
 void free_graph(sp_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
-    cudaFree(g->off);
-    cudaFree(g->adj);
-    cudaFree(g->w);
-    cudaFree(g->weff);
-    cudaFree(g->outdeg);
+    resident_free(g->off);
+    resident_free(g->adj);
+    resident_free(g->w);
+    resident_free(g->weff);
+    resident_free(g->outdeg);
     if (g->directed) {
-        cudaFree(g->roff);
-        cudaFree(g->radj);
-        cudaFree(g->indeg);
+        resident_free(g->roff);
+        resident_free(g->radj);
+        resident_free(g->indeg);
     }
-    cudaFree(g->reid);
-    cudaFree(g->nzrow);
-    cudaFree(g->nzend);
-    cudaFree(g->ustart8);
-    cudaFree(g->ulen);
-    cudaFree(g->uadj);
-    cudaFree(g->uinfo);
-    cudaFree(g->wrange);
+    resident_free(g->reid);
+    resident_free(g->nzrow);
+    resident_free(g->nzend);
+    resident_free(g->ustart8);
+    resident_free(g->ulen);
+    resident_free(g->uadj);
+    resident_free(g->uinfo);
+    resident_free(g->wrange);
     delete g;
 }
 
 template <class T>
 int dalloc(T **p, size_t count) {
-    cudaError_t e = cudaMalloc((void **)p, count * sizeof(T) + 16);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        set_error("cudaMalloc of %zu bytes failed: %s", count * sizeof(T), cudaGetErrorString(e));
-        return e == cudaErrorMemoryAllocation ? SP_ERR_OOM : SP_ERR_CUDA;
-    }
+    void *q = nullptr;
+    SP_TRY(resident_alloc(&q, count * sizeof(T) + 16));
+    *p = static_cast<T *>(q);
     return SP_OK;
 }
 
@@ -593,7 +590,7 @@ int ensure_weff(sp_graph *g, Call &c) {
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
     if (e != cudaSuccess) {
-        cudaFree(weff);
+        resident_free(weff);
         SP_CUDA(e);
     }
     g->weff = weff;

@@ -90,17 +90,63 @@ int scratch_alloc(void **p, size_t bytes, cudaStream_t s) {
     return SP_OK;
 }
 
+// Graph-resident arrays come from the same stream-ordered pool (so graph
+// creation/destruction does not pay cudaMalloc/cudaFree, which synchronise
+// the device); allocated on the legacy stream and made visible to every
+// stream by one synchronisation.
+int resident_alloc(void **p, size_t bytes) {
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        set_error("device allocation of %zu bytes failed (%s)", bytes, cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? SP_ERR_OOM : SP_ERR_CUDA;
+    }
+    return SP_OK;
+}
+
+void resident_free(void *p) {
+    if (p) cudaFreeAsync(p, 0);
+}
+
 void scratch_free(void *p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
+
+// Per host thread and device: one non-blocking stream and two timing
+// events, created on first use and reused by every later call of that
+// thread (stream/event creation costs tens of microseconds per call
+// otherwise).  Calls from different host threads never share a stream.
+struct ThreadRes {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+static thread_local ThreadRes g_tres[64];
 
 int Call::begin(int dev) {
     device = dev;
     SP_CUDA(cudaSetDevice(dev));
     if (dev >= 0 && dev < 64) std::call_once(g_pool_once[dev], tune_pool, dev);
-    SP_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    SP_CUDA(cudaEventCreate(&t0));
-    SP_CUDA(cudaEventCreate(&t1));
+    ThreadRes *r = (dev >= 0 && dev < 64) ? &g_tres[dev] : nullptr;
+    if (r && r->stream) {
+        stream = r->stream;
+        t0 = r->t0;
+        t1 = r->t1;
+        owned = false;
+    } else {
+        SP_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        SP_CUDA(cudaEventCreate(&t0));
+        SP_CUDA(cudaEventCreate(&t1));
+        if (r) {
+            r->stream = stream;
+            r->t0 = t0;
+            r->t1 = t1;
+            owned = false;
+        } else {
+            owned = true;
+        }
+    }
     SP_CUDA(cudaEventRecord(t0, stream));
     return SP_OK;
 }
@@ -129,11 +175,13 @@ Call::~Call() {
     if (stream) {
         for (int i = 0; i < nbufs; i++) scratch_free(bufs[i], stream);
         cudaStreamSynchronize(stream);
-        cudaStreamDestroy(stream);
+        if (owned) cudaStreamDestroy(stream);
     }
     pinned_put(pinned);
-    if (t0) cudaEventDestroy(t0);
-    if (t1) cudaEventDestroy(t1);
+    if (owned) {
+        if (t0) cudaEventDestroy(t0);
+        if (t1) cudaEventDestroy(t1);
+    }
 }
 
 int to_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s) {

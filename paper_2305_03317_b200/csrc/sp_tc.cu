@@ -182,11 +182,11 @@ int ensure_upper(sp_graph *g, Call &c) {
     int32_t *ulen = nullptr;
     SP_TRY(c.alloc(&pad8, n + 1));
     SP_TRY(c.alloc(&start8, n + 1));
-    SP_CUDA(cudaMalloc(&ulen, std::max<int64_t>(1, n) * sizeof(int32_t)));
+    SP_TRY(resident_alloc((void **)&ulen, std::max<int64_t>(1, n) * sizeof(int32_t)));
     struct Guard {
         void *p[4] = {nullptr, nullptr, nullptr, nullptr};
         bool keep = false;
-        ~Guard() { if (!keep) for (void *q : p) cudaFree(q); }
+        ~Guard() { if (!keep) for (void *q : p) resident_free(q); }
     } gd;
     gd.p[0] = ulen;
     const int grid = grid_for(n * 32, 256, c.device, 16);
@@ -210,11 +210,11 @@ int ensure_upper(sp_graph *g, Call &c) {
     int32_t *uadj = nullptr;
     uint2 *uinfo = nullptr;
     uint32_t *ustart8 = nullptr;
-    SP_CUDA(cudaMalloc(&uadj, std::max<int64_t>(8, mpad) * sizeof(int32_t)));
+    SP_TRY(resident_alloc((void **)&uadj, std::max<int64_t>(8, mpad) * sizeof(int32_t)));
     gd.p[1] = uadj;
-    SP_CUDA(cudaMalloc(&uinfo, std::max<int64_t>(8, mpad) * sizeof(uint2)));
+    SP_TRY(resident_alloc((void **)&uinfo, std::max<int64_t>(8, mpad) * sizeof(uint2)));
     gd.p[2] = uinfo;
-    SP_CUDA(cudaMalloc(&ustart8, (n + 1) * sizeof(uint32_t)));
+    SP_TRY(resident_alloc((void **)&ustart8, (n + 1) * sizeof(uint32_t)));
     gd.p[3] = ustart8;
     k_up_fill<<<grid, 256, 0, c.stream>>>(g->off, g->adj, g->outdeg, start8, n, uadj);
     k_up_info<<<grid_for(std::max<int64_t>(mpad, n + 1), 256, c.device, 16), 256, 0, c.stream>>>(

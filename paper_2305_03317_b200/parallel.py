@@ -52,6 +52,7 @@ class NativeBackend:
         self.index = device
         _lib.require_device(device)
         self.L = _lib.lib()
+        self.last_stats = {}  # counters of the last native call (sp_stats)
 
     def _fence(self):
         # the native calls run on their own streams (and sync them before
@@ -80,17 +81,23 @@ class NativeBackend:
         if len(srcs):
             s = np.asarray(srcs, dtype=np.int32)
             flags = _lib.SP_FLAG_DETERMINISTIC if deterministic else 0
+            st = _lib.Stats()
             rc = self.L.sp_bc(g.handle, s.ctypes.data_as(C.c_void_p), len(s), flags,
                               C.c_void_p(bc.data_ptr()), C.c_void_p(sg.data_ptr()),
-                              C.c_void_p(dl.data_ptr()), _lib.SP_MEM_DEVICE, None)
+                              C.c_void_p(dl.data_ptr()), _lib.SP_MEM_DEVICE, C.byref(st))
             self._chk(rc, "sp_bc")
+            self.last_stats = st.as_dict()
+        else:
+            self.last_stats = {}
         return bc, sg, dl
 
     # -- TC
     def tc(self, g, v0, v1) -> int:
         self._fence()
         cnt = C.c_uint64()
-        self._chk(self.L.sp_tc(g.handle, int(v0), int(v1), C.byref(cnt), None), "sp_tc")
+        st = _lib.Stats()
+        self._chk(self.L.sp_tc(g.handle, int(v0), int(v1), C.byref(cnt), C.byref(st)), "sp_tc")
+        self.last_stats = st.as_dict()
         return int(cnt.value)
 
     # -- PR
@@ -197,6 +204,16 @@ def run_sharded(tp, g, args: dict, function: str | None = None,
                      wall_seconds=time.perf_counter() - t0, stats=stats)
 
 
+def _sum_stats(be, keys, group):
+    """Counters of this rank's last native call, summed over the ranks."""
+    dist = _dist()
+    st = getattr(be, "last_stats", {}) or {}
+    t = be.torch.tensor([float(st.get(k, 0)) for k in keys], dtype=be.torch.float64,
+                        device=be.device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return {k: int(v) for k, v in zip(keys, t.tolist())}
+
+
 def _bc(be, g, bound, cap, world, me, group, det, E, prog):
     dist = _dist()
     srcs = bound["sourceSet"]
@@ -211,7 +228,9 @@ def _bc(be, g, bound, cap, world, me, group, det, E, prog):
         dist.broadcast(sg, src=glob, group=group)
         dist.broadcast(dl, src=glob, group=group)
         env.node_props.update(sigma=be.to_host(sg), delta=be.to_host(dl))
-    return env, {}, {"sources_local": len(mine)}
+    stats = _sum_stats(be, ("edges_visited", "vertices_visited", "model_bytes"), group)
+    stats["sources_local"] = len(mine)
+    return env, {}, stats
 
 
 def _tc(be, g, bound, cap, world, me, group, det, E, prog):
@@ -221,7 +240,9 @@ def _tc(be, g, bound, cap, world, me, group, det, E, prog):
     t = be.torch.tensor([part], dtype=be.torch.int64, device=be.device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     env = PropertyEnv(scalars={"triangle_count": int(t.item())})
-    return env, {}, {"range": (v0, v1), "local_count": part}
+    stats = _sum_stats(be, ("edges_visited", "model_bytes"), group)
+    stats.update(range=(v0, v1), local_count=part)
+    return env, {}, stats
 
 
 def _pr(be, g, bound, cap, world, me, group, det, E, prog):

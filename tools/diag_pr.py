@@ -29,3 +29,17 @@ for i in range(3):
     t1 = time.perf_counter()
     print(f"native wall {(t1-t0)*1e3:.2f} ms  device {st.device_ms:.2f}  kernels "
           f"{st.main_kernel_ms:.2f}  rc {rc}", flush=True)
+
+# per-step host overhead distribution of the bench's device-resident leg
+import statistics  # noqa: E402
+walls, devs = [], []
+r = None
+for i in range(60):
+    t0 = time.perf_counter()
+    r = sp.run(corpus.PR, g, args, device_outputs=True)
+    walls.append((time.perf_counter() - t0) * 1e3)
+    devs.append(r.stats["device_ms"])
+gap = [w - d for w, d in zip(walls, devs)]
+print("gap ms: median %.3f p90 %.3f max %.3f  device median %.3f" % (
+    statistics.median(gap), sorted(gap)[54], max(gap), statistics.median(devs)))
+print("gaps:", " ".join(f"{x:.2f}" for x in gap))
