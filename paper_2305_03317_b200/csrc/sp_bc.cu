@@ -26,6 +26,7 @@
 // both are skipped without changing a bit.  Sigma values are path counts:
 // integer-valued doubles, exact in any summation order below 2^53.
 #include <algorithm>
+#include <thread>
 #include <vector>
 
 #include "sp_expand.cuh"
@@ -36,6 +37,7 @@ using namespace sp;
 namespace {
 
 constexpr int64_t kBcHub = 8192;  // rows longer than this take the CTA fold
+constexpr int kBcWorkers = 4;     // concurrent sources (host threads/streams), fast mode
 
 struct DiscoverOp {
     using Payload = int;
@@ -115,22 +117,23 @@ __global__ void k_root(int32_t *level, double *sigma, int32_t *queue, int32_t s)
     queue[0] = s;
 }
 
-}  // namespace
 
-extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned flags,
-                     double *bc_out, double *sigma_out, double *delta_out, int mem,
-                     sp_stats *st) {
-    SP_CHECK(g && bc_out && nsrc >= 0 && (nsrc == 0 || srcs_in), SP_ERR_ARG,
-             "sp_bc: bad arguments");
-    std::vector<int32_t> srcs(srcs_in, srcs_in + nsrc);  // host list (SetN argument)
-    for (int64_t i = 0; i < nsrc; i++)
-        SP_CHECK(srcs[i] >= 0 && srcs[i] < g->n, SP_ERR_ARG,
-                 "set argument 'sourceSet' id %d out of range", srcs[i]);
+// One worker: a stream (its thread's), its own scratch and bc partial, and
+// the sources srcs[first], srcs[first + stride], ... in list order.
+struct BcWorker {
+    int64_t levels = 0, scanned = 0, reached = 0, launches = 0;
+    int rc = SP_OK;
+    char err[512] = "";
+};
+
+int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first, int64_t stride,
+                   bool det, double *bc_dst, int bc_mem, bool bc_accumulate_only,
+                   double *sigma_out, double *delta_out, int mem, BcWorker &wk) {
     Call c;
     SP_TRY(c.begin(g->device));
     const int64_t n = g->n;
+    const int64_t nsrc = (int64_t)srcs.size();
     const int sms = num_sms(c.device);
-    const bool det = flags & SP_FLAG_DETERMINISTIC;
     int32_t *level, *queue, *hubs, *reg_v, *reg_nch, *item_reg;
     int64_t *reg_base;
     double *csum;
@@ -154,18 +157,19 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
     SP_TRY(c.alloc(&cnt, 1));
     SP_TRY(c.alloc(&nhubs, 3));
     const FoldLists fl{hubs, nhubs, FoldChunks{reg_v, reg_base, reg_nch, item_reg, csum, nullptr}};
+    c.persist(level, n * sizeof(int32_t));  // BFS probes hit level[] at random
     SP_CUDA(cudaMemsetAsync(bc, 0, n * sizeof(double), c.stream));
     SP_CUDA(cudaMemsetAsync(sigma, 0, n * sizeof(double), c.stream));
     SP_CUDA(cudaMemsetAsync(delta, 0, n * sizeof(double), c.stream));
     ExpandCounters *hc = nullptr;
     SP_TRY(c.host_as(&hc));
     const bool big_out = g->max_outdeg > kSplit;
-    int64_t levels_total = 0, scanned_total = 0, reached_total = 0;
     std::vector<int64_t> ls;
-    for (int64_t si = 0; si < nsrc; si++) {
+    int64_t last_done = -1;
+    for (int64_t si = first; si < nsrc; si += stride) {
         const int32_t s = srcs[si];
         SP_CUDA(cudaMemsetAsync(level, 0xFF, n * sizeof(int32_t), c.stream));
-        if (si > 0) {
+        if (last_done >= 0) {
             SP_CUDA(cudaMemsetAsync(sigma, 0, n * sizeof(double), c.stream));
             SP_CUDA(cudaMemsetAsync(delta, 0, n * sizeof(double), c.stream));
         }
@@ -188,7 +192,7 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
             SP_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(ExpandCounters), cudaMemcpyDeviceToHost,
                                     c.stream));
             SP_CUDA(cudaStreamSynchronize(c.stream));
-            scanned_total += (int64_t)hc->scanned;
+            wk.scanned += (int64_t)hc->scanned;
             const int64_t nnew = (int64_t)hc->next_size;
             if (nnew == 0) break;
             ls.push_back(q1 + nnew);
@@ -199,28 +203,110 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
             }
         }
         const int nlev = (int)ls.size() - 1;
-        levels_total += nlev;
-        reached_total += ls.back();
+        wk.levels += nlev;
+        wk.reached += ls.back();
         for (int L = nlev - 2; L >= 0; L--) {
             DeltaFold df{g->adj, level, sigma, delta, bc, L + 1, s};
             launch_fold(df, g->off, queue + ls[L], ls[L + 1] - ls[L], kBcHub, fl, det,
                         g->max_outdeg, sms, c.stream, &c.launches);
         }
         SP_CUDA(cudaGetLastError());
+        last_done = si;
     }
-    SP_TRY(from_device(bc_out, bc, n * 8, mem, c.stream));
-    if (sigma_out) SP_TRY(from_device(sigma_out, sigma, n * 8, mem, c.stream));
-    if (delta_out) SP_TRY(from_device(delta_out, delta, n * 8, mem, c.stream));
+    // bc partial out (a device buffer of the caller, or the final output)
+    if (bc_accumulate_only) {
+        SP_CUDA(cudaMemcpyAsync(bc_dst, bc, n * 8, cudaMemcpyDeviceToDevice, c.stream));
+    } else {
+        SP_TRY(from_device(bc_dst, bc, n * 8, bc_mem, c.stream));
+    }
+    if (last_done == nsrc - 1) {  // this worker ran the list's last source
+        if (sigma_out) SP_TRY(from_device(sigma_out, sigma, n * 8, mem, c.stream));
+        if (delta_out) SP_TRY(from_device(delta_out, delta, n * 8, mem, c.stream));
+    }
+    SP_TRY(c.finish(nullptr));
+    wk.launches = c.launches;
+    return SP_OK;
+}
+
+// bc = sum of the workers' partials in worker order (fixed: deterministic)
+__global__ void k_sum_partials(const double *__restrict__ parts, int k, int64_t n, double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = parts[i];
+        for (int j = 1; j < k; j++) s = __dadd_rn(s, parts[(int64_t)j * n + i]);
+        out[i] = s;
+    }
+}
+
+}  // namespace
+
+extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned flags,
+                     double *bc_out, double *sigma_out, double *delta_out, int mem,
+                     sp_stats *st) {
+    SP_CHECK(g && bc_out && nsrc >= 0 && (nsrc == 0 || srcs_in), SP_ERR_ARG,
+             "sp_bc: bad arguments");
+    std::vector<int32_t> srcs(srcs_in, srcs_in + nsrc);  // host list (SetN argument)
+    for (int64_t i = 0; i < nsrc; i++)
+        SP_CHECK(srcs[i] >= 0 && srcs[i] < g->n, SP_ERR_ARG,
+                 "set argument 'sourceSet' id %d out of range", srcs[i]);
+    const int64_t n = g->n;
+    const bool det = flags & SP_FLAG_DETERMINISTIC;
+    // Fast mode runs kBcWorkers sources concurrently (one host thread and
+    // stream each): small BFS levels of one source overlap the large levels
+    // of another, and the per-level host reads overlap too.  Deterministic
+    // mode keeps the reference's sequential source order (bit-exact bc).
+    const int K = det ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(kBcWorkers, nsrc));
+    Call c;
+    SP_TRY(c.begin(g->device));
+    std::vector<BcWorker> wk(K);
+    if (nsrc == 0) {
+        double *z;
+        SP_TRY(c.alloc(&z, n));
+        SP_CUDA(cudaMemsetAsync(z, 0, n * 8, c.stream));
+        SP_TRY(from_device(bc_out, z, n * 8, mem, c.stream));
+    } else if (K == 1) {
+        SP_TRY(c.finish(nullptr));  // order after the caller's work
+        SP_TRY(bc_run_sources(g, srcs, 0, 1, det, bc_out, mem, false, sigma_out, delta_out, mem,
+                              wk[0]));
+    } else {
+        double *parts;
+        SP_TRY(c.alloc(&parts, (int64_t)K * n));
+        SP_TRY(c.finish(nullptr));  // parts allocated before the workers use it
+        std::vector<std::thread> th;
+        for (int k = 0; k < K; k++)
+            th.emplace_back([&, k]() {
+                wk[k].rc = bc_run_sources(g, srcs, k, K, det, parts + (int64_t)k * n,
+                                          SP_MEM_DEVICE, true, sigma_out, delta_out, mem, wk[k]);
+                if (wk[k].rc != SP_OK) snprintf(wk[k].err, sizeof(wk[k].err), "%s", sp_last_error());
+            });
+        for (auto &t : th) t.join();
+        for (int k = 0; k < K; k++)
+            SP_CHECK(wk[k].rc == SP_OK, wk[k].rc, "%s", wk[k].err);
+        double *sum;
+        SP_TRY(c.alloc(&sum, n));
+        k_sum_partials<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(parts, K, n, sum);
+        c.launches++;
+        SP_CUDA(cudaGetLastError());
+        SP_TRY(from_device(bc_out, sum, n * 8, mem, c.stream));
+    }
     SP_TRY(c.finish(st));
     if (st) {
-        st->iterations = levels_total;
-        st->edges_visited = scanned_total;
-        st->vertices_visited = reached_total;
+        int64_t lv = 0, sc = 0, rc = 0, la = 0;
+        for (auto &w : wk) {
+            lv += w.levels;
+            sc += w.scanned;
+            rc += w.reached;
+            la += w.launches;
+        }
+        st->iterations = lv;
+        st->edges_visited = sc;
+        st->vertices_visited = rc;
+        st->kernel_launches += la;
         st->main_kernel_ms = st->device_ms;
         st->main_kernel_launches = st->kernel_launches;
         // 48 B per reached slot (discovery 8, sigma 16, delta 24)
         // + 64 B per reached vertex, summed over sources
-        st->model_bytes = 48 * scanned_total + 64 * reached_total;
+        st->model_bytes = 48 * sc + 64 * rc;
     }
     return SP_OK;
 }

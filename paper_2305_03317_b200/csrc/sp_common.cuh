@@ -61,6 +61,10 @@ struct Call {
     int64_t launches = 0;
     void *pinned = nullptr;  // kPinnedBlock bytes of pinned host memory
     bool owned = true;       // stream/events belong to this call (else thread-cached)
+    bool persisting = false; // an L2 access-policy window is set on the stream
+    // Keep [base, base+bytes) in the persisting L2 set-aside for this call's
+    // kernels (random-access property arrays); best effort.
+    void persist(const void *base, size_t bytes);
     int begin(int dev);
     // this call's pinned host block (recycled across calls)
     int host(void **p);

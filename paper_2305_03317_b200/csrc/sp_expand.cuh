@@ -41,8 +41,8 @@ struct ExpandCounters {
 };
 
 template <class Op>
-__global__ void __launch_bounds__(kExpandBlock, 4) k_expand(
-    Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+__device__ __forceinline__ void expand_body(
+    const Op &op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const int32_t *__restrict__ q, int64_t nq, int32_t *__restrict__ qn,
     uint2 *__restrict__ chunks, ExpandCounters *cnt, int vpw) {
     // vpw = frontier vertices per warp (32 normally; fewer for small
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kExpandBlock, 4) k_expand(
                 const int64_t b0 = __shfl_sync(0xffffffffu, beg, lo);
                 pv[u] = __shfl_sync(0xffffffffu, pay, lo);
                 e[u] = p < total ? b0 + (p - ex) : -1;
-                x[u] = e[u] >= 0 ? adj[e[u]] : -1;
+                x[u] = e[u] >= 0 ? __ldcs(adj + e[u]) : -1;  // streamed: evict first
             }
 #pragma unroll
             for (int u = 0; u < kRounds; u++)
@@ -116,8 +116,24 @@ __global__ void __launch_bounds__(kExpandBlock, 4) k_expand(
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kExpandBlock, 4) k_expand_chunks(
+__global__ void __launch_bounds__(kExpandBlock, 4) k_expand(
     Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+    const int32_t *__restrict__ q, int64_t nq, int32_t *__restrict__ qn,
+    uint2 *__restrict__ chunks, ExpandCounters *cnt, int vpw) {
+    expand_body(op, off, adj, q, nq, qn, chunks, cnt, vpw);
+}
+
+// Largest power of two <= 32 that still gives every one of `warps` warps a
+// share of an nq-vertex frontier (host and device use the same rule).
+__host__ __device__ __forceinline__ int expand_vpw(int64_t nq, int64_t warps) {
+    int vpw = 32;
+    while (vpw > 1 && (nq + vpw - 1) / vpw < warps) vpw >>= 1;
+    return vpw;
+}
+
+template <class Op>
+__device__ __forceinline__ void expand_chunks_body(
+    const Op &op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const uint2 *__restrict__ chunks, int32_t *__restrict__ qn, ExpandCounters *cnt) {
     using Pr = typename Op::Probe;
     constexpr int kPer = kSplit / 32;
@@ -139,7 +155,7 @@ __global__ void __launch_bounds__(kExpandBlock, 4) k_expand_chunks(
 #pragma unroll
         for (int j = 0; j < kPer; j++) {
             const int64_t ee = e0 + j * 32 + lane;
-            x[j] = ee < e1 ? adj[ee] : -1;
+            x[j] = ee < e1 ? __ldcs(adj + ee) : -1;  // streamed: evict first
         }
 #pragma unroll
         for (int j = 0; j < kPer; j++)
@@ -153,6 +169,13 @@ __global__ void __launch_bounds__(kExpandBlock, 4) k_expand_chunks(
     if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);  // warp-uniform
 }
 
+template <class Op>
+__global__ void __launch_bounds__(kExpandBlock, 4) k_expand_chunks(
+    Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+    const uint2 *__restrict__ chunks, int32_t *__restrict__ qn, ExpandCounters *cnt) {
+    expand_chunks_body(op, off, adj, chunks, qn, cnt);
+}
+
 // Chunk buffer capacity for a graph with m slots.
 inline int64_t expand_chunk_capacity(int64_t m) { return 2 * (m / kSplit) + 2; }
 
@@ -163,8 +186,7 @@ inline void launch_expand(const Op &op, const int64_t *off, const int32_t *adj, 
                           bool has_big_rows, cudaStream_t s, int64_t *launches) {
     const int cap = sms * 8;
     const int64_t warps_full = (int64_t)cap * (kExpandBlock / 32);
-    int vpw = 32;
-    while (vpw > 1 && (nq + vpw - 1) / vpw < warps_full) vpw >>= 1;
+    const int vpw = expand_vpw(nq, warps_full);
     int64_t want = ((nq + vpw - 1) / vpw + 7) / 8;  // 8 warps per block
     int g1 = (int)(want < 1 ? 1 : (want > cap ? cap : want));
     k_expand<Op><<<g1, kExpandBlock, 0, s>>>(op, off, adj, q, nq, qn, chunks, cnt, vpw);

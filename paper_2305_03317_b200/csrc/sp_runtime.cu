@@ -42,12 +42,24 @@ int num_sms(int device) {
 
 static std::once_flag g_pool_once[64];
 
+static size_t g_persist_max[64];
+static size_t g_window_max[64];
+
 static void tune_pool(int device) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;  // keep freed scratch for reuse
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    // L2 set-aside for persisting accesses (the random-access property
+    // arrays of the graph kernels; see Call::persist)
+    int pmax = 0, wmax = 0;
+    cudaDeviceGetAttribute(&pmax, cudaDevAttrMaxPersistingL2CacheSize, device);
+    cudaDeviceGetAttribute(&wmax, cudaDevAttrMaxAccessPolicyWindowSize, device);
+    if (pmax > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)pmax) == cudaSuccess)
+        g_persist_max[device] = (size_t)pmax;
+    g_window_max[device] = wmax > 0 ? (size_t)wmax : 0;
+    cudaGetLastError();
 }
 
 // Pinned host words for per-iteration flag/counter reads: a process-wide
@@ -121,6 +133,11 @@ void scratch_free(void *p, cudaStream_t s) {
 struct ThreadRes {
     cudaStream_t stream = nullptr;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
+    ~ThreadRes() {  // thread exit (e.g. sp_bc's workers): release the stream
+        if (stream) cudaStreamDestroy(stream);
+        if (t0) cudaEventDestroy(t0);
+        if (t1) cudaEventDestroy(t1);
+    }
 };
 static thread_local ThreadRes g_tres[64];
 
@@ -164,6 +181,22 @@ int Call::finish(sp_stats *st) {
     return SP_OK;
 }
 
+void Call::persist(const void *base, size_t bytes) {
+    if (device < 0 || device >= 64 || !g_persist_max[device] || !g_window_max[device] || !bytes)
+        return;
+    const size_t win = bytes < g_window_max[device] ? bytes : g_window_max[device];
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
+    v.accessPolicyWindow.num_bytes = win;
+    const double ratio = (double)g_persist_max[device] / (double)win;
+    v.accessPolicyWindow.hitRatio = (float)(ratio < 1.0 ? ratio : 1.0);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess)
+        persisting = true;
+    cudaGetLastError();
+}
+
 int Call::host(void **p) {
     if (!pinned) pinned = pinned_get();
     SP_CHECK(pinned, SP_ERR_OOM, "pinned host allocation failed");
@@ -175,6 +208,13 @@ Call::~Call() {
     if (stream) {
         for (int i = 0; i < nbufs; i++) scratch_free(bufs[i], stream);
         cudaStreamSynchronize(stream);
+        if (persisting) {  // the stream is reused by later calls: drop the window
+            cudaStreamAttrValue v = {};
+            v.accessPolicyWindow.num_bytes = 0;
+            cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v);
+            cudaCtxResetPersistingL2Cache();
+            cudaGetLastError();
+        }
         if (owned) cudaStreamDestroy(stream);
     }
     pinned_put(pinned);

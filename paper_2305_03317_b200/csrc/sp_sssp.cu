@@ -44,7 +44,7 @@ struct RelaxOp {
     int it;
     __device__ __forceinline__ int payload(int32_t v) const { return __ldcg(dist + v); }
     __device__ __forceinline__ Probe probe(int64_t e, int32_t x) const {
-        return Probe{__ldg(weff + e), __ldcg(dist + x)};
+        return Probe{__ldcs(weff + e), __ldcg(dist + x)};
     }
     __device__ __forceinline__ bool apply(int dv, int64_t, int32_t x, Probe p) const {
         const int64_t cand = (int64_t)dv + (int64_t)p.w;
@@ -67,6 +67,127 @@ __global__ void k_init(int32_t *dist, int32_t *enq, int64_t n, int32_t src, int3
         enq[x] = x == src ? 0 : -1;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) q[0] = src;
+}
+
+// ---- device-side fixedPoint loop (CUDA graph with a conditional WHILE node)
+// The loop state lives on the device; the body is the expansion (+ hub
+// chunks) followed by a one-thread advance kernel that folds the counters
+// into the totals, swaps the queues, resets the next counters and sets the
+// loop condition (frontier non-empty, no overflow, below the cap).  No host
+// round trip per iteration: used whenever no per-iteration callback is set.
+struct SsspLoop {
+    int32_t *q[2];
+    ExpandCounters cnt[2];
+    int cur;       // q[cur] is the frontier being expanded
+    int it;        // enqueue stamp of this iteration (iters + 1)
+    int64_t nq;    // |q[cur]|
+    int64_t iters, relaxed, frontier_sum, cap;
+    int status;    // 0 ok / converged, 1 overflow, 2 cap reached
+};
+
+__global__ void __launch_bounds__(kExpandBlock, 4) k_relax_loop(
+    int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, uint2 *chunks,
+    SsspLoop *L, int64_t warps) {
+    const int cur = L->cur;
+    const int64_t nq = L->nq;
+    RelaxOp op{dist, enq, weff, &L->cnt[cur].flag, L->it};
+    expand_body(op, off, adj, L->q[cur], nq, L->q[cur ^ 1], chunks, &L->cnt[cur],
+                expand_vpw(nq, warps));
+}
+
+__global__ void __launch_bounds__(kExpandBlock, 4) k_relax_loop_chunks(
+    int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const uint2 *chunks,
+    SsspLoop *L) {
+    const int cur = L->cur;
+    RelaxOp op{dist, enq, weff, &L->cnt[cur].flag, L->it};
+    expand_chunks_body(op, off, adj, chunks, L->q[cur ^ 1], &L->cnt[cur]);
+}
+
+__global__ void k_loop_advance(SsspLoop *L, cudaGraphConditionalHandle h) {
+    const int cur = L->cur;
+    const ExpandCounters c = L->cnt[cur];
+    L->iters++;
+    L->frontier_sum += L->nq;
+    L->relaxed += (int64_t)c.scanned;
+    int go = 1;
+    if (c.flag) {
+        L->status = 1;
+        go = 0;
+    } else if (c.next_size == 0) {
+        go = 0;  // finished = !modified
+    } else if (L->iters >= L->cap) {
+        L->status = 2;
+        go = 0;
+    }
+    L->cnt[cur ^ 1] = ExpandCounters{0, 0, 0, 0};
+    L->cur = cur ^ 1;
+    L->nq = (int64_t)c.next_size;
+    L->it = (int)(L->iters + 1);
+    cudaGraphSetConditional(h, go);
+}
+
+int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
+                     uint2 *chunks, int64_t cap, SsspLoop *hL, float *kernel_ms) {
+    SsspLoop *L;
+    SP_TRY(c.alloc(&L, 1));
+    SsspLoop init{};
+    init.q[0] = qa;
+    init.q[1] = qb;
+    init.nq = 1;
+    init.it = 1;
+    init.cap = cap;
+    SP_CUDA(cudaMemcpyAsync(L, &init, sizeof(SsspLoop), cudaMemcpyHostToDevice, c.stream));
+    const int sms = num_sms(c.device);
+    const int grid = sms * 8;
+    const int64_t warps = (int64_t)grid * (kExpandBlock / 32);
+    const bool big = g->max_outdeg > kSplit;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    struct GraphFree {
+        cudaGraph_t *g;
+        cudaGraphExec_t *e;
+        ~GraphFree() {
+            if (*e) cudaGraphExecDestroy(*e);
+            if (*g) cudaGraphDestroy(*g);
+        }
+    } gf{&graph, &exec};
+    SP_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    SP_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    SP_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+    k_relax_loop<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off, g->adj, chunks,
+                                                      L, warps);
+    if (big)
+        k_relax_loop_chunks<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off,
+                                                                 g->adj, chunks, L);
+    k_loop_advance<<<1, 1, 0, c.stream>>>(L, h);
+    cudaError_t ce = cudaStreamEndCapture(c.stream, &body);
+    SP_CUDA(ce);
+    SP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaEvent_t ka, kb;
+    SP_CUDA(cudaEventCreate(&ka));
+    SP_CUDA(cudaEventCreate(&kb));
+    cudaEventRecord(ka, c.stream);
+    SP_CUDA(cudaGraphLaunch(exec, c.stream));
+    cudaEventRecord(kb, c.stream);
+    SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(SsspLoop), cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    cudaEventElapsedTime(kernel_ms, ka, kb);
+    cudaEventDestroy(ka);
+    cudaEventDestroy(kb);
+    c.launches += hL->iters * (big ? 3 : 2);
+    return SP_OK;
 }
 
 }  // namespace
@@ -94,6 +215,7 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
     const int dev = c.device;
     const int sms = num_sms(dev);
     const bool big = g->max_outdeg > kSplit;
+    c.persist(dist, n * sizeof(int32_t));  // the relaxations' random probes
     k_init<<<grid_for(n, kBlock, dev), kBlock, 0, c.stream>>>(dist, enq, n, src, qa);
     c.launches++;
     int64_t nq = 1, iters = 0, relaxed = 0, frontier_sum = 0;
@@ -102,6 +224,27 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
     SP_CUDA(cudaEventCreate(&ka));
     SP_CUDA(cudaEventCreate(&kb));
     float kernel_ms = 0.f;
+    if (!cb) {
+        SsspLoop hL{};
+        int lrc = sssp_device_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
+        if (lrc == SP_OK) {
+            iters = hL.iters;
+            relaxed = hL.relaxed;
+            frontier_sum = hL.frontier_sum;
+            if (hL.status == 1) {
+                set_error("SSSP distance left the int32 range (negative weights)");
+                rc = SP_ERR_OVERFLOW;
+            } else if (hL.status == 2) {
+                set_error("fixedPoint 'finished' did not converge within %lld iterations",
+                          (long long)cap);
+                rc = SP_ERR_NONCONV;
+            }
+            cudaEventDestroy(ka);
+            cudaEventDestroy(kb);
+            goto done;
+        }
+        return lrc;
+    }
     for (;;) {
         ExpandCounters *cur = cnt + (iters & 1);
         RelaxOp op{dist, enq, g->weff, &cur->flag, (int)(iters + 1)};
@@ -140,6 +283,7 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
     }
     cudaEventDestroy(ka);
     cudaEventDestroy(kb);
+done:
     if (rc == SP_OK || rc == SP_ERR_NONCONV) SP_TRY(from_device(dist_out, dist, n * 4, mem, c.stream));
     SP_TRY(c.finish(st));
     if (iters_out) *iters_out = iters;
@@ -149,6 +293,9 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
         st->vertices_visited = frontier_sum;
         st->main_kernel_ms = kernel_ms;
         st->main_kernel_launches = iters;
+        // 12 B per relaxation (adj 4, w_eff 4, dist[x] 4) + 20 B
+        // per frontier vertex (two offsets 16, dist[v] 4)
+        st->model_bytes = 12 * relaxed + 20 * frontier_sum;
     }
     return rc;
 }

@@ -15,6 +15,9 @@ nsrc = int(sys.argv[3]) if len(sys.argv) > 3 else 16
 if algo == "sssp":
     g = sp.generate("rmat", 16, 16, seed=1)
     prog, args = corpus.SSSP, {"src": 0}
+elif algo.startswith("sssp_rmat"):
+    g = sp.generate("rmat", int(algo[9:]), 16, seed=1)
+    prog, args = corpus.SSSP, {"src": 0}
 elif algo == "sssp_grid":
     g = sp.generate("grid", 4096, 4096, seed=1)
     prog, args = corpus.SSSP, {"src": 0}
@@ -34,4 +37,6 @@ for i in range(reps):
     r = sp.run(prog, g, args, device_outputs=True)
     print(f"{algo} rep {i}: wall {(time.perf_counter() - t0) * 1e3:.2f} ms, device "
           f"{r.stats['device_ms']:.2f} ms, launches {r.stats['kernel_launches']}, "
-          f"edges {r.stats['edges_visited']}, model bytes {r.stats['model_bytes']}", flush=True)
+          f"edges {r.stats['edges_visited']}, vertices {r.stats['vertices_visited']}, "
+          f"iters {r.stats['iterations']}, model bytes {r.stats['model_bytes']}, "
+          f"m {g.m}", flush=True)
