@@ -128,6 +128,8 @@ struct sp_graph {
     uint2 *uinfo = nullptr;
     int64_t m_up = -1;      // real upper slots; -1: not built
     int64_t m_up_pad = 0;   // padded slots
+    int32_t *ubig = nullptr;  // vertices whose upper row exceeds the warp path
+    int64_t nbig = 0, max_ulen = 0;
 };
 
 // ---- device helpers --------------------------------------------------------

@@ -340,6 +340,7 @@ void free_graph(sp_graph *g) {
     resident_free(g->ulen);
     resident_free(g->uadj);
     resident_free(g->uinfo);
+    resident_free(g->ubig);
     resident_free(g->wrange);
     delete g;
 }

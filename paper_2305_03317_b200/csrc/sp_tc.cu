@@ -31,6 +31,9 @@
 // multiplicity.  Counts: per-lane uint64 -> warp sum -> one atomicAdd per
 // warp.
 //
+// Vertices whose upper row is longer than kA are counted by k_tc_big, one
+// CTA per vertex with A staged in dynamic shared memory.
+//
 // Directed graphs (no mirror, the program's orientation matters): k_tc_mid
 // follows tc.sp literally -- per middle vertex v, A = N(v)_{>v} staged with
 // the same filter, each slot u < v of N(v) scans N(u)_{>v}.
@@ -51,7 +54,6 @@ constexpr int kA = 256;            // staged A entries per warp (larger rows: gl
 constexpr int kFilterWords = 128;  // 4096-bit filter per warp
 constexpr int kFilterShift = 20;   // 32 - log2(4096)
 constexpr int kBatch = 32;
-constexpr int kGroup = 8;          // lanes per b-row (long-row path of k_tc_fwd)
 constexpr int kUnroll = 2;         // 16-byte loads in flight per lane in k_tc_fwd
 constexpr int kPad = 8;            // upper rows padded/aligned to 32-byte sectors
 constexpr int kQ = kPad / 4;       // 16-byte quarters per padded block
@@ -174,6 +176,21 @@ __global__ void k_up_info(const int32_t *__restrict__ uadj, const int64_t *__res
         ustart8[v] = (uint32_t)start8[v];
 }
 
+__global__ void k_big_list(const int32_t *__restrict__ ulen, int64_t n, int thr, int32_t *list,
+                           unsigned long long *cnt) {
+    unsigned long long mx = 0;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = b + threadIdx.x;
+        const int32_t l = v < n ? ulen[v] : 0;
+        mx = max(mx, (unsigned long long)l);
+        const bool big = l > thr;
+        const int64_t slot = warp_append(big, &cnt[0]);
+        if (big) list[slot] = (int32_t)v;
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&cnt[1], mx);
+}
+
 int ensure_upper(sp_graph *g, Call &c) {
     std::lock_guard<std::mutex> lk(g_up_mu);
     if (g->m_up >= 0) return SP_OK;
@@ -219,10 +236,20 @@ int ensure_upper(sp_graph *g, Call &c) {
     k_up_fill<<<grid, 256, 0, c.stream>>>(g->off, g->adj, g->outdeg, start8, n, uadj);
     k_up_info<<<grid_for(std::max<int64_t>(mpad, n + 1), 256, c.device, 16), 256, 0, c.stream>>>(
         uadj, start8, ulen, mpad, uinfo, ustart8, n);
-    c.launches += 3;
+    int32_t *big = nullptr;
+    SP_TRY(resident_alloc((void **)&big, std::max<int64_t>(1, n) * sizeof(int32_t)));
+    unsigned long long *bc;
+    SP_TRY(c.alloc(&bc, 2));
+    SP_CUDA(cudaMemsetAsync(bc, 0, 2 * sizeof(unsigned long long), c.stream));
+    k_big_list<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(ulen, n, kA, big, bc);
+    c.launches += 4;
     SP_CUDA(cudaGetLastError());
+    SP_CUDA(cudaMemcpyAsync(h + 1, bc, 16, cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
     gd.keep = true;
+    g->ubig = big;
+    g->nbig = (int64_t)h[1];
+    g->max_ulen = (int64_t)h[2];
     g->ulen = ulen;
     g->uadj = uadj;
     g->uinfo = uinfo;
@@ -274,21 +301,10 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd(const uint32_t *__restrict
             const int na = __shfl_sync(0xffffffffu, my_len, src);
             if (na < 2) continue;  // a triangle needs b and x in N+(a)
             const int64_t r0 = kPad * (int64_t)__shfl_sync(0xffffffffu, my_s8, src);
+            if (na > kA) continue;  // k_tc_big (one CTA per vertex) counts it
             if (lane == 0) {
                 pairs += (unsigned long long)na;
                 abytes += (unsigned long long)na * (unsigned long long)na;
-            }
-            if (na > kA) {
-                // long row (rare after degree ordering): groups of 8 lanes
-                // walk the b rows, membership by binary search in global A
-                const int grp = lane / kGroup, gl = lane % kGroup;
-                for (int j = grp; j < na; j += 32 / kGroup) {
-                    const uint2 inf = uinfo[r0 + j];
-                    if (gl == 0) elems += inf.y;
-                    for (int32_t k = gl; k < (int32_t)inf.y; k += kGroup)
-                        cnt += mult_g(uadj, r0, r0 + na, __ldg(uadj + kPad * (int64_t)inf.x + k));
-                }
-                continue;
             }
             // ---- stage A, row starts, sector prefix and filter
             for (int k = lane; k < kFilterWords; k += 32) F[k] = 0u;
@@ -352,6 +368,105 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd(const uint32_t *__restrict
                 }
             }
             __syncwarp();  // A/B/S/F are restaged for the next vertex
+        }
+    }
+    cnt = warp_sum(cnt);
+    elems = warp_sum(elems);
+    if (lane == 0) {
+        if (cnt) atomicAdd(&ctr->total, cnt);
+        if (pairs) atomicAdd(&ctr->pairs, pairs);
+        if (elems) atomicAdd(&ctr->elems, elems);
+        if (abytes) atomicAdd(&ctr->abytes, abytes);
+    }
+}
+
+// One CTA per vertex whose upper row exceeds the warp path (kA): the block
+// stages A = N+(a) (up to kBigMax entries) and a kBigFilterBits filter in
+// dynamic shared memory; each warp takes 32 of A's b's at a time, loads
+// their row descriptors with one coalesced read, and walks the flattened
+// 16-byte half-sectors of their rows (owner by a 5-step shuffle search),
+// one filter probe per element and a shared-memory binary search on a hit.
+constexpr int kBigFilterBits = 1 << 17;  // 16 KB
+constexpr int kBigFilterShift = 32 - 17;
+constexpr int kBigMax = 48 * 1024;      // staged A entries (192 KB) -- beyond: global search
+
+__global__ void __launch_bounds__(kBlock, 1) k_tc_big(const uint32_t *__restrict__ ustart8,
+                                                      const int32_t *__restrict__ ulen,
+                                                      const int32_t *__restrict__ uadj,
+                                                      const uint2 *__restrict__ uinfo,
+                                                      const int32_t *__restrict__ big,
+                                                      int64_t nbig, int64_t v0, int64_t v1,
+                                                      TcCounters *ctr) {
+    extern __shared__ uint32_t smem[];
+    uint32_t *F = smem;                                        // kBigFilterBits / 32 words
+    int32_t *A = reinterpret_cast<int32_t *>(smem + kBigFilterBits / 32);
+    const unsigned lane = lane_id();
+    const int wid = threadIdx.x >> 5;
+    unsigned long long cnt = 0, elems = 0, pairs = 0, abytes = 0;
+    for (int64_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+        const int32_t a = big[bi];
+        if (a < v0 || a >= v1) continue;  // block-uniform
+        const int na = ulen[a];
+        const int64_t r0 = kPad * (int64_t)ustart8[a];
+        const bool staged = na <= kBigMax;
+        __syncthreads();  // previous vertex done with A/F
+        if (staged) {
+            for (int k = threadIdx.x; k < kBigFilterBits / 32; k += blockDim.x) F[k] = 0u;
+            __syncthreads();
+            for (int k = threadIdx.x; k < na; k += blockDim.x) {
+                const int32_t x = uadj[r0 + k];
+                A[k] = x;
+                const uint32_t hh = ((uint32_t)x * 2654435761u) >> kBigFilterShift;
+                atomicOr(&F[hh >> 5], 1u << (hh & 31));
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            pairs += (unsigned long long)na;
+            abytes += (unsigned long long)na * (unsigned long long)na;
+        }
+        for (int j0 = wid * 32; j0 < na; j0 += (kBlock / 32) * 32) {
+            const int j = j0 + (int)lane;
+            uint2 inf = make_uint2(0u, 0u);
+            if (j < na) inf = uinfo[r0 + j];
+            elems += inf.y;
+            const int secs = (int)((inf.y + kPad - 1u) / kPad);
+            int incl = secs;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane >= o) incl += t;
+            }
+            const int excl = incl - secs;
+            const int nhalf = kQ * __shfl_sync(0xffffffffu, incl, 31);
+            for (int h0 = 0; h0 < nhalf; h0 += 32) {
+                const int h = h0 + (int)lane;
+                const int sec = h / kQ;
+                int lo = 0;  // owner lane: largest with excl <= sec
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = lo + step;
+                    const int ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+                    if (cand < 32 && ex <= sec) lo = cand;
+                }
+                const int ex = __shfl_sync(0xffffffffu, excl, lo);
+                const uint32_t s8 = __shfl_sync(0xffffffffu, inf.x, lo);
+                if (h >= nhalf) continue;
+                const int4 xs = __ldg(reinterpret_cast<const int4 *>(uadj) +
+                                      kQ * ((int64_t)s8 + (sec - ex)) + (h % kQ));
+                const int32_t xv[4] = {xs.x, xs.y, xs.z, xs.w};
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int32_t x = xv[i];
+                    if (x < 0) continue;
+                    if (staged) {
+                        const uint32_t hh = ((uint32_t)x * 2654435761u) >> kBigFilterShift;
+                        if (F[hh >> 5] & (1u << (hh & 31))) cnt += mult_s(A, na, x);
+                    } else {
+                        cnt += mult_g(uadj, r0, r0 + na, x);
+                    }
+                }
+            }
         }
     }
     cnt = warp_sum(cnt);
@@ -447,12 +562,27 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
     if (v1 > v0) {
         int64_t want = (v1 - v0 + kBatch * kWarps - 1) / (kBatch * kWarps);
         int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
-        if (g->directed)
+        if (g->directed) {
             k_tc_mid<<<grid, kBlock, 0, c.stream>>>(g->off, g->adj, v0, v1, ctr);
-        else
+            c.launches++;
+        } else {
             k_tc_fwd<<<grid, kBlock, 0, c.stream>>>(g->ustart8, g->ulen, g->uadj, g->uinfo, v0,
                                                     v1, ctr);
-        c.launches++;
+            c.launches++;
+            if (g->nbig) {
+                const size_t smem = kBigFilterBits / 8 +
+                                    4 * (size_t)std::min<int64_t>(g->max_ulen, kBigMax);
+                SP_CUDA(cudaFuncSetAttribute(k_tc_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+                int per_sm = 1;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_big, kBlock, smem);
+                const int gb = (int)std::min<int64_t>(g->nbig,
+                                                      (int64_t)sms * std::max(1, per_sm));
+                k_tc_big<<<gb, kBlock, smem, c.stream>>>(g->ustart8, g->ulen, g->uadj, g->uinfo,
+                                                         g->ubig, g->nbig, v0, v1, ctr);
+                c.launches++;
+            }
+        }
     }
     cudaEventRecord(kb, c.stream);
     SP_CUDA(cudaGetLastError());

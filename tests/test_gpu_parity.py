@@ -373,3 +373,21 @@ def test_weight_range_and_io(tmp_path):
     g2 = sp.load_edge_list(str(p))
     np.testing.assert_array_equal(g2.adj, g.adj)
     np.testing.assert_array_equal(g2.weights, g.weights)
+
+
+@pytest.mark.parametrize("n,p,seed", [(600, 0.8, 1), (900, 0.45, 2)])
+def test_tc_dense_rows_cta_path(n, p, seed):
+    """Upper rows longer than the warp path (> 256 after degree ordering)
+    go through the CTA kernel; dense random graphs exercise it, with
+    parallel edges sprinkled in (multiplicity products)."""
+    rng = np.random.default_rng(seed)
+    iu, ju = np.triu_indices(n, 1)
+    keep = rng.random(len(iu)) < p
+    u, v = iu[keep], ju[keep]
+    dup = rng.random(len(u)) < 0.01
+    u = np.concatenate([u, u[dup]])
+    v = np.concatenate([v, v[dup]])
+    w = np.ones(len(u), dtype=np.int64)
+    g = sp.from_arrays(u, v, w, directed=False, n=n)
+    o = cpu_ref.build_csr(u, v, w, False, n)
+    assert sp.run(corpus.TC, g, {}).env.scalars["triangle_count"] == cpu_ref.tc(o, nthreads=8)

@@ -21,6 +21,12 @@ elif algo.startswith("sssp_rmat"):
 elif algo == "sssp_grid":
     g = sp.generate("grid", 4096, 4096, seed=1)
     prog, args = corpus.SSSP, {"src": 0}
+elif algo.startswith("pr_rmat"):
+    g = sp.generate("rmat", int(algo[7:]), 16, seed=1)
+    prog, args = corpus.PR, {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
+elif algo.startswith("tc_rmat"):
+    g = sp.generate("rmat", int(algo[7:]), 16, seed=1, undirected=True)
+    prog, args = corpus.TC, {}
 elif algo == "pr":
     g = sp.generate("rmat", 22, 16, seed=1)
     prog, args = corpus.PR, {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
