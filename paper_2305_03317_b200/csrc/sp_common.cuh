@@ -175,7 +175,8 @@ __device__ __forceinline__ int64_t warp_append(bool want, unsigned long long *co
 // push[u] get consecutive slots, one global atomic for the whole batch.
 template <int K>
 __device__ __forceinline__ void warp_append_multi(const bool (&push)[K], const int32_t (&val)[K],
-                                                  unsigned long long *counter, int32_t *out) {
+                                                  unsigned long long *counter, int32_t *out,
+                                                  unsigned long long cap = ~0ull) {
     unsigned m[K];
     unsigned total = 0;
 #pragma unroll
@@ -190,7 +191,8 @@ __device__ __forceinline__ void warp_append_multi(const bool (&push)[K], const i
     const unsigned lt = (1u << lane_id()) - 1u;
 #pragma unroll
     for (int u = 0; u < K; u++) {
-        if (push[u]) out[base + __popc(m[u] & lt)] = val[u];
+        const unsigned long long at = base + __popc(m[u] & lt);
+        if (push[u] && at < cap) out[at] = val[u];  // the counter still counts overflow
         base += __popc(m[u]);
     }
 }

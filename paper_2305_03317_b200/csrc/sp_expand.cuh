@@ -25,6 +25,9 @@
 //               (`using Payload` / `using Probe` declare the types)
 #pragma once
 
+#include <type_traits>
+#include <utility>
+
 #include "sp_common.cuh"
 
 namespace sp {
@@ -39,6 +42,36 @@ struct ExpandCounters {
     unsigned long long chunks;     // hub chunk work items published
     unsigned long long flag;       // op-specific error flag
 };
+
+// Optional Op extensions (detected at compile time):
+//   bool keep(int32_t v, Payload pay)  -- false: skip v's row (stale entry)
+//   apply() returning 2 = push x to the far queue (Op::kFar == true; the
+//   far queue and its counter come from op.far_q / op.far_n)
+template <class Op, class = void>
+struct HasFar : std::false_type {};
+template <class Op>
+struct HasFar<Op, std::void_t<decltype(Op::kFar)>> : std::integral_constant<bool, Op::kFar> {};
+template <class Op, class = void>
+struct HasKeep : std::false_type {};
+template <class Op>
+struct HasKeep<Op, std::void_t<decltype(std::declval<const Op &>().keep(0, typename Op::Payload()))>>
+    : std::true_type {};
+
+template <class Op, int K>
+__device__ __forceinline__ void append_results(const Op &op, const int (&res)[K],
+                                               const int32_t (&x)[K], ExpandCounters *cnt,
+                                               int32_t *qn) {
+    bool near[K];
+#pragma unroll
+    for (int u = 0; u < K; u++) near[u] = res[u] == 1;
+    warp_append_multi<K>(near, x, &cnt->next_size, qn);
+    if constexpr (HasFar<Op>::value) {
+        bool far[K];
+#pragma unroll
+        for (int u = 0; u < K; u++) far[u] = res[u] == 2;
+        warp_append_multi<K>(far, x, op.far_n, op.far_q, op.far_cap);
+    }
+}
 
 template <class Op>
 __device__ __forceinline__ void expand_body(
@@ -63,6 +96,9 @@ __device__ __forceinline__ void expand_body(
             beg = off[v];
             deg = off[v + 1] - beg;
             pay = op.payload(v);
+            if constexpr (HasKeep<Op>::value) {
+                if (!op.keep(v, pay)) deg = 0;
+            }
         }
         if (deg > kSplit) {  // hub row -> chunk work items
             int64_t nch = (deg + kSplit - 1) / kSplit;
@@ -104,11 +140,11 @@ __device__ __forceinline__ void expand_body(
 #pragma unroll
             for (int u = 0; u < kRounds; u++)
                 if (e[u] >= 0) pr[u] = op.probe(e[u], x[u]);
-            bool push[kRounds];
+            int res[kRounds];
 #pragma unroll
             for (int u = 0; u < kRounds; u++)
-                push[u] = e[u] >= 0 && op.apply(pv[u], e[u], x[u], pr[u]);
-            warp_append_multi<kRounds>(push, x, &cnt->next_size, qn);
+                res[u] = e[u] >= 0 ? (int)op.apply(pv[u], e[u], x[u], pr[u]) : 0;
+            append_results<Op, kRounds>(op, res, x, cnt, qn);
         }
     }
     // `scanned` is warp-uniform (every lane added the same totals)
@@ -160,11 +196,11 @@ __device__ __forceinline__ void expand_chunks_body(
 #pragma unroll
         for (int j = 0; j < kPer; j++)
             if (x[j] >= 0) pr[j] = op.probe(e0 + j * 32 + lane, x[j]);
-        bool push[kPer];
+        int res[kPer];
 #pragma unroll
         for (int j = 0; j < kPer; j++)
-            push[j] = x[j] >= 0 && op.apply(pay, e0 + j * 32 + lane, x[j], pr[j]);
-        warp_append_multi<kPer>(push, x, &cnt->next_size, qn);
+            res[j] = x[j] >= 0 ? (int)op.apply(pay, e0 + j * 32 + lane, x[j], pr[j]) : 0;
+        append_results<Op, kPer>(op, res, x, cnt, qn);
     }
     if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);  // warp-uniform
 }

@@ -20,6 +20,8 @@
 //   * the frontier size is the convergence flag (finished = size == 0):
 //     one 8-byte device->host read per iteration (K5/K6 in SURVEY 2.2).
 // Candidates >= INT_MAX never win (interp.py:11-14).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "sp_expand.cuh"
@@ -29,6 +31,8 @@ using namespace sp;
 namespace {
 
 constexpr int kBlock = 256;
+constexpr int64_t kDeltaMul = 16;        // near-far step = kDeltaMul x mean weight
+constexpr int64_t kNearFarMaxAvgDeg = 8;  // near-far only when m <= 8 n
 
 // Relaxation of sssp.sp:11-12 for one slot; payload = dist[v] at expansion.
 struct RelaxOp {
@@ -126,6 +130,270 @@ __global__ void k_loop_advance(SsspLoop *L, cudaGraphConditionalHandle h) {
     L->nq = (int64_t)c.next_size;
     L->it = (int)(L->iters + 1);
     cudaGraphSetConditional(h, go);
+}
+
+// ---- near-far ordering (large-diameter graphs, non-negative weights) -----
+// Improvements below the threshold T go to the near queue (processed next
+// iteration), the others to a far pile.  When the near queue runs dry, T
+// grows by delta and k_nf_split moves the far entries below T back (stale
+// and already-expanded entries are dropped).  `last[v]` is the distance v
+// was last expanded with: a queue entry is expanded only if dist[v] < last.
+// Same fixpoint as Bellman-Ford, far fewer repeated relaxations on graphs
+// whose shortest paths are many hops long (road-like grids).
+struct NfLoop {
+    int32_t *q[2];
+    int32_t *far[2];
+    ExpandCounters cnt[2];
+    unsigned long long far_n[2];
+    unsigned long long split_n;  // near entries appended by k_nf_split
+    int cur, fcur;
+    int it;
+    int64_t nq;
+    int64_t T, delta;
+    int64_t iters, relaxed, frontier_sum, cap;
+    unsigned long long fcap;  // far pile capacity
+    int status;               // 0 ok, 1 overflow, 2 cap, 3 far pile overflow
+};
+
+struct NearFarOp {
+    using Payload = int;
+    using Probe = RelaxOp::Probe;
+    static constexpr bool kFar = true;
+    int32_t *__restrict__ dist;
+    int32_t *__restrict__ enq;
+    int32_t *__restrict__ last;
+    const int32_t *__restrict__ weff;
+    unsigned long long *overflow;
+    int32_t *far_q;
+    unsigned long long *far_n;
+    unsigned long long far_cap;
+    int64_t T;
+    int it;
+    __device__ __forceinline__ int payload(int32_t v) const { return __ldcg(dist + v); }
+    __device__ __forceinline__ bool keep(int32_t v, int dv) const {
+        if (dv >= __ldcg(last + v)) return false;  // expanded at this distance already
+        last[v] = dv;
+        return true;
+    }
+    __device__ __forceinline__ Probe probe(int64_t e, int32_t x) const {
+        return Probe{__ldcs(weff + e), __ldcg(dist + x)};
+    }
+    __device__ __forceinline__ int apply(int dv, int64_t, int32_t x, Probe p) const {
+        const int64_t cand = (int64_t)dv + (int64_t)p.w;
+        if (cand >= (int64_t)kIntMax) return 0;
+        if (cand < (int64_t)(-2147483647 - 1)) {
+            atomicAdd(overflow, 1ull);
+            return 0;
+        }
+        const int c = (int)cand;
+        if (c >= p.dx) return 0;
+        const int old = atomicMin(dist + x, c);
+        if (c >= old) return 0;
+        if (cand < T) return atomicExch(enq + x, it) != it ? 1 : 0;
+        return 2;
+    }
+};
+
+__global__ void __launch_bounds__(kExpandBlock, 4) k_nf_expand(
+    int32_t *dist, int32_t *enq, int32_t *last, const int32_t *__restrict__ weff,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, uint2 *chunks, NfLoop *L,
+    int64_t warps) {
+    const int cur = L->cur;
+    const int64_t nq = L->nq;
+    if (nq == 0) return;
+    NearFarOp op{dist, enq, last, weff, &L->cnt[cur].flag, L->far[L->fcur], &L->far_n[L->fcur],
+                 L->fcap, L->T, L->it};
+    expand_body(op, off, adj, L->q[cur], nq, L->q[cur ^ 1], chunks, &L->cnt[cur],
+                expand_vpw(nq, warps));
+}
+
+__global__ void __launch_bounds__(kExpandBlock, 4) k_nf_chunks(
+    int32_t *dist, int32_t *enq, int32_t *last, const int32_t *__restrict__ weff,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const uint2 *chunks,
+    NfLoop *L) {
+    const int cur = L->cur;
+    if (L->nq == 0) return;
+    NearFarOp op{dist, enq, last, weff, &L->cnt[cur].flag, L->far[L->fcur], &L->far_n[L->fcur],
+                 L->fcap, L->T, L->it};
+    expand_chunks_body(op, off, adj, chunks, L->q[cur ^ 1], &L->cnt[cur]);
+}
+
+// The far pile is split when the expansion produced no near entries (every
+// block of k_nf_split and k_nf_advance derive the same decision from the
+// finished expansion counters; T for the split is T + delta).
+__device__ __forceinline__ bool nf_split_now(const NfLoop *L) {
+    const ExpandCounters &c = L->cnt[L->cur];
+    return c.next_size == 0 && !c.flag && L->far_n[L->fcur] <= L->fcap;
+}
+
+// Far entries below T -> near queue (if not stale / not expanded at this
+// distance); the rest -> the other far pile.
+__global__ void k_nf_split(const int32_t *__restrict__ dist, int32_t *enq,
+                           const int32_t *__restrict__ last, NfLoop *L) {
+    if (!nf_split_now(L)) return;
+    const int cur = L->cur, fc = L->fcur;
+    const int64_t nf = (int64_t)min(L->far_n[fc], L->fcap);
+    const int32_t *src = L->far[fc];
+    const int64_t T = L->T + L->delta;
+    const int it = L->it;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < nf; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = b + threadIdx.x;
+        bool to_near = false, to_far = false;
+        int32_t v = 0;
+        if (i < nf) {
+            v = src[i];
+            const int d = __ldcg(dist + v);
+            if ((int64_t)d < T) {
+                to_near = d < __ldcg(last + v) && atomicExch(enq + v, it) != it;
+            } else {
+                to_far = true;
+            }
+        }
+        const bool nb[1] = {to_near}, fb[1] = {to_far};
+        const int32_t xv[1] = {v};
+        warp_append_multi<1>(nb, xv, &L->split_n, L->q[cur ^ 1]);
+        warp_append_multi<1>(fb, xv, &L->far_n[fc ^ 1], L->far[fc ^ 1], L->fcap);
+    }
+}
+
+__global__ void k_nf_advance2(NfLoop *L, cudaGraphConditionalHandle h) {
+    const int cur = L->cur;
+    const ExpandCounters c = L->cnt[cur];
+    const bool split = nf_split_now(L);  // same decision k_nf_split took
+    L->frontier_sum += L->nq;
+    L->relaxed += (int64_t)c.scanned;
+    L->iters++;
+    int64_t next = (int64_t)c.next_size;
+    if (split) {
+        L->T += L->delta;
+        L->far_n[L->fcur] = 0;
+        L->fcur ^= 1;
+        next = (int64_t)L->split_n;
+        L->split_n = 0;
+    }
+    int go = 1;
+    const bool far_left = L->far_n[L->fcur] > 0;
+    if (L->far_n[0] > L->fcap || L->far_n[1] > L->fcap) {
+        L->status = 3;  // the caller falls back to plain Bellman-Ford
+        go = 0;
+    } else if (c.flag) {
+        L->status = 1;
+        go = 0;
+    } else if (next == 0 && !far_left) {
+        go = 0;  // nothing near, nothing far: finished
+    } else if (L->iters >= L->cap) {
+        L->status = 2;
+        go = 0;
+    }
+    L->cnt[cur ^ 1] = ExpandCounters{0, 0, 0, 0};
+    L->cur = cur ^ 1;
+    L->nq = next;
+    L->it = (int)(L->iters + 1);
+    cudaGraphSetConditional(h, go);
+}
+
+__global__ void k_fill_i32(int32_t *p, int64_t n, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+int sssp_near_far(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
+                  uint2 *chunks, int64_t cap, int64_t delta, SsspLoop *out, float *kernel_ms) {
+    const int64_t n = g->n, m = g->m;
+    int32_t *last, *fa, *fb;
+    NfLoop *L;
+    SP_TRY(c.alloc(&last, n));
+    // far piles: every entry is an improvement above T; bounded by the
+    // relaxations of one iteration plus the surviving pile (<= 2m + n)
+    const int64_t fcap = 2 * m + n + 16;
+    SP_TRY(c.alloc(&fa, fcap));
+    SP_TRY(c.alloc(&fb, fcap));
+    SP_TRY(c.alloc(&L, 1));
+    k_fill_i32<<<grid_for(n, kBlock, c.device), kBlock, 0, c.stream>>>(last, n, kIntMax);
+    c.launches++;
+    NfLoop init{};
+    init.q[0] = qa;
+    init.q[1] = qb;
+    init.far[0] = fa;
+    init.far[1] = fb;
+    init.nq = 1;
+    init.it = 1;
+    init.T = delta;
+    init.delta = delta;
+    init.cap = cap;
+    init.fcap = (unsigned long long)fcap;
+    SP_CUDA(cudaMemcpyAsync(L, &init, sizeof(NfLoop), cudaMemcpyHostToDevice, c.stream));
+    const int sms = num_sms(c.device);
+    // near-far frontiers are small (a band of the graph): a smaller grid
+    // keeps the fixed per-iteration launch cost down
+    const int grid = sms * 2;
+    const int64_t warps = (int64_t)grid * (kExpandBlock / 32);
+    const bool big = g->max_outdeg > kSplit;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    struct GraphFree {
+        cudaGraph_t *g;
+        cudaGraphExec_t *e;
+        ~GraphFree() {
+            if (*e) cudaGraphExecDestroy(*e);
+            if (*g) cudaGraphDestroy(*g);
+        }
+    } gf{&graph, &exec};
+    SP_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    SP_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    SP_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+    k_nf_expand<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, last, g->weff, g->off, g->adj,
+                                                     chunks, L, warps);
+    if (big)
+        k_nf_chunks<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, last, g->weff, g->off, g->adj,
+                                                         chunks, L);
+    k_nf_split<<<grid, kBlock, 0, c.stream>>>(dist, enq, last, L);
+    k_nf_advance2<<<1, 1, 0, c.stream>>>(L, h);
+    SP_CUDA(cudaStreamEndCapture(c.stream, &body));
+    SP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaEvent_t ka, kb;
+    SP_CUDA(cudaEventCreate(&ka));
+    SP_CUDA(cudaEventCreate(&kb));
+    cudaEventRecord(ka, c.stream);
+    SP_CUDA(cudaGraphLaunch(exec, c.stream));
+    cudaEventRecord(kb, c.stream);
+    NfLoop *hL;
+    SP_TRY(c.host_as(&hL));
+    SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(NfLoop), cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    cudaEventElapsedTime(kernel_ms, ka, kb);
+    cudaEventDestroy(ka);
+    cudaEventDestroy(kb);
+    out->iters = hL->iters;
+    out->relaxed = hL->relaxed;
+    out->frontier_sum = hL->frontier_sum;
+    out->status = hL->status;
+    c.launches += hL->iters * (big ? 4 : 3);
+    return SP_OK;
+}
+
+// Near-far threshold step; 0 selects plain Bellman-Ford (negative weights,
+// or SP_SSSP_DELTA=0).  Default: kDeltaMul x the mean of the weight range.
+int64_t near_far_delta(const sp_graph *g, int32_t wmin, int32_t wmax) {
+    if (g->m == 0 || wmin < 0) return 0;
+    const char *env = getenv("SP_SSSP_DELTA");
+    if (env) return atoll(env);
+    // road-like (low average degree, long shortest paths) graphs only; on
+    // low-diameter graphs (RMAT) plain Bellman-Ford needs fewer iterations
+    if (g->m > kNearFarMaxAvgDeg * g->n) return 0;
+    const int64_t mean = ((int64_t)wmin + (int64_t)wmax + 1) / 2;
+    return std::max<int64_t>(1, kDeltaMul * mean);
 }
 
 int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
@@ -226,7 +494,18 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
     float kernel_ms = 0.f;
     if (!cb) {
         SsspLoop hL{};
-        int lrc = sssp_device_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
+        int lrc;
+        int32_t wr[2] = {0, 0};
+        if (g->m) SP_CUDA(cudaMemcpy(wr, g->wrange, sizeof(wr), cudaMemcpyDeviceToHost));
+        const int64_t delta = near_far_delta(g, wr[0], wr[1]);
+        if (delta > 0)
+            lrc = sssp_near_far(g, c, dist, enq, qa, qb, chunks, cap, delta, &hL, &kernel_ms);
+        if (delta <= 0 || (lrc == SP_OK && hL.status == 3)) {  // plain Bellman-Ford
+            k_init<<<grid_for(n, kBlock, dev), kBlock, 0, c.stream>>>(dist, enq, n, src, qa);
+            c.launches++;
+            hL = SsspLoop{};
+            lrc = sssp_device_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
+        }
         if (lrc == SP_OK) {
             iters = hL.iters;
             relaxed = hL.relaxed;
