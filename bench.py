@@ -405,6 +405,22 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
                                  note="Graph500 GTEPS = edges of reached vertices / time; "
                                       "m ~ 1M: launch/latency-bound")
         g.close()
+    if "grid" in a.algos:  # cfg5a: 4096 x 4096 road-like grid, SSSP from 0 + PR
+        g = sp.generate("grid", 4096, 4096, seed=SEED, device=dev.index)
+        ms, _, r = timed(lambda: go(corpus.SSSP, g, {"src": 0}), 2, 1, world, dev)
+        mb = None
+        if world == 1:
+            mb = 12 * r.stats["edges_visited"] + 20 * r.stats["vertices_visited"]
+        out["sssp_cfg5_grid"] = _line("sssp", "grid 4096x4096 undirected, w U[1,100]", g, ms / 2,
+                                      g.m, mb, hbm_peak,
+                                      iterations=r.fixedpoint_iterations["finished"],
+                                      note="GTEPS = m / time (every vertex reached); near-far "
+                                           "ordering, device-side loop")
+        ms, _, r = timed(lambda: go(corpus.PR, g, PR_ARGS), 2, 1, world, dev)
+        it = r.env.scalars["iter"]
+        out["pr_cfg5_grid"] = _line("pr", "grid 4096x4096 undirected", g, ms / 2, it * g.m,
+                                    it * (12 * g.m + 36 * g.n), hbm_peak, iterations=it)
+        g.close()
     if "bc" in a.algos:
         g = sp.generate("rmat", 20, 16, seed=SEED, undirected=True, device=dev.index)
         deg = np.diff(np.asarray(g.offsets))
@@ -439,7 +455,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--algos", default="sssp,bc,tc",
+    ap.add_argument("--algos", default="sssp,grid,bc,tc",
                     help="secondary algorithms at N=1 ('' to skip)")
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()

@@ -576,6 +576,9 @@ extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t 
         st->vertices_visited = iters * n;
         st->main_kernel_ms = kernel_ms;
         st->main_kernel_launches = iters;
+        // per iteration 12 B per slot (radj 4 + contrib gather 8)
+        // + 36 B per vertex (roff 8, rank r/w 16, contrib write 8, outdeg 4)
+        st->model_bytes = iters * (12 * g->m + 36 * n);
     }
     return rc;
 }

@@ -51,16 +51,19 @@ static void tune_pool(int device) {
         uint64_t thr = UINT64_MAX;  // keep freed scratch for reuse
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    // L2 set-aside for persisting accesses (the random-access property
-    // arrays of the graph kernels; see Call::persist)
+    // L2 set-aside limits for persisting accesses (see Call::persist); the
+    // set-aside itself is reserved only while a call holds a window, since
+    // it shrinks the L2 every other kernel sees
     int pmax = 0, wmax = 0;
     cudaDeviceGetAttribute(&pmax, cudaDevAttrMaxPersistingL2CacheSize, device);
     cudaDeviceGetAttribute(&wmax, cudaDevAttrMaxAccessPolicyWindowSize, device);
-    if (pmax > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)pmax) == cudaSuccess)
-        g_persist_max[device] = (size_t)pmax;
+    g_persist_max[device] = pmax > 0 ? (size_t)pmax : 0;
     g_window_max[device] = wmax > 0 ? (size_t)wmax : 0;
     cudaGetLastError();
 }
+
+static std::mutex g_persist_mu;
+static int g_persist_users[64];  // calls currently holding a persisting window
 
 // Pinned host words for per-iteration flag/counter reads: a process-wide
 // free list of kPinnedBlock-byte blocks (cudaMallocHost costs milliseconds,
@@ -184,6 +187,11 @@ int Call::finish(sp_stats *st) {
 void Call::persist(const void *base, size_t bytes) {
     if (device < 0 || device >= 64 || !g_persist_max[device] || !g_window_max[device] || !bytes)
         return;
+    {
+        std::lock_guard<std::mutex> lk(g_persist_mu);
+        if (g_persist_users[device]++ == 0)
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_persist_max[device]);
+    }
     const size_t win = bytes < g_window_max[device] ? bytes : g_window_max[device];
     cudaStreamAttrValue v = {};
     v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
@@ -192,8 +200,8 @@ void Call::persist(const void *base, size_t bytes) {
     v.accessPolicyWindow.hitRatio = (float)(ratio < 1.0 ? ratio : 1.0);
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    if (cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess)
-        persisting = true;
+    cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    persisting = true;  // released in ~Call (also when the window was refused)
     cudaGetLastError();
 }
 
@@ -212,7 +220,11 @@ Call::~Call() {
             cudaStreamAttrValue v = {};
             v.accessPolicyWindow.num_bytes = 0;
             cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v);
-            cudaCtxResetPersistingL2Cache();
+            std::lock_guard<std::mutex> lk(g_persist_mu);
+            if (--g_persist_users[device] == 0) {  // last holder: give the L2 back
+                cudaCtxResetPersistingL2Cache();
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+            }
             cudaGetLastError();
         }
         if (owned) cudaStreamDestroy(stream);

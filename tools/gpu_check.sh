@@ -12,6 +12,6 @@ timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; ech
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-   --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --algos "" > $OUT/ncu_launch_bench.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pull -s 6 -c 2 \
-   -o $OUT/prof_pull python bench.py --steps 1 --warmup 1 --no-cpu --algos "" > $OUT/ncu_full.log 2>&1
+   --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --algos none > $OUT/ncu_launch_bench.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pr_units|k_pr_fix|k_pr_epi" -s 9 -c 3 \
+   -o $OUT/prof_pr python bench.py --steps 1 --warmup 1 --no-cpu --algos none > $OUT/ncu_full.log 2>&1

@@ -111,6 +111,19 @@ def full(rep: str, out: str, json_path: str | None = None, key: str | None = Non
                         d.get("occupancy_pct", 0), d.get("threads_per_inst", 0),
                         d.get("regs", 0), d.get("grid", 0)))
     print(open(out).read())
+    if json_path and key == "pr_iteration" and res:
+        # one PR iteration = one launch each of k_pr_units, k_pr_fix, k_pr_epi
+        try:
+            cur = json.load(open(json_path))
+        except Exception:
+            cur = {}
+        tot = sum(d.get("dram_read", 0) + d.get("dram_write", 0) for d in res)
+        names = sorted({d["kernel"] for d in res})
+        cur[key] = {"dram_bytes_per_launch": tot * len(names) / len(res),
+                    "kernels": names, "source": os.path.basename(rep),
+                    "note": "sum of the iteration's kernels' dram__bytes_read+write"}
+        json.dump(cur, open(json_path, "w"), indent=1)
+        return
     if json_path and key and res:
         try:
             cur = json.load(open(json_path))
