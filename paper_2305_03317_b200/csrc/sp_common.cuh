@@ -197,6 +197,53 @@ __device__ __forceinline__ void warp_append_multi(const bool (&push)[K], const i
     }
 }
 
+// Per-warp staging of queue appends in shared memory: entries collect in a
+// warp-private buffer and go to the global queue in batches of up to kCap,
+// one global atomic per batch (a single global counter shared by every warp
+// serialises at one L2 slice otherwise).  `n` is warp-uniform.
+template <int kCap>
+struct WarpStage {
+    int32_t *buf;  // kCap entries of shared memory, private to the warp
+    int n = 0;
+
+    __device__ __forceinline__ void flush(unsigned long long *counter, int32_t *out,
+                                          unsigned long long cap = ~0ull) {
+        if (n == 0) return;
+        __syncwarp();
+        unsigned long long base = 0;
+        if (lane_id() == 0) base = atomicAdd(counter, (unsigned long long)n);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int i = lane_id(); i < n; i += 32)
+            if (base + i < cap) out[base + i] = buf[i];  // the counter still counts overflow
+        __syncwarp();
+        n = 0;
+    }
+
+    template <int K>
+    __device__ __forceinline__ void push(const bool (&p)[K], const int32_t (&val)[K],
+                                         unsigned long long *counter, int32_t *out,
+                                         unsigned long long cap = ~0ull) {
+        static_assert(K * 32 <= kCap, "one push must fit an empty stage");
+        unsigned m[K];
+        int total = 0;
+#pragma unroll
+        for (int u = 0; u < K; u++) {
+            m[u] = __ballot_sync(0xffffffffu, p[u]);
+            total += __popc(m[u]);
+        }
+        if (total == 0) return;
+        if (n + total > kCap) flush(counter, out, cap);
+        const unsigned lt = (1u << lane_id()) - 1u;
+        int at = n;
+#pragma unroll
+        for (int u = 0; u < K; u++) {
+            if (p[u]) buf[at + __popc(m[u] & lt)] = val[u];
+            at += __popc(m[u]);
+        }
+        n = at;
+    }
+};
+
 __device__ __forceinline__ int ld_stream_i32(const int32_t *p) {
     int v;
     asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));

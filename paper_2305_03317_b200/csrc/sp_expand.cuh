@@ -16,9 +16,10 @@
 //    (the atomics); all probes of a lane are issued before any apply, so
 //    several random L2 round trips are in flight per lane instead of one
 //    dependent chain per slot;
-//  * visited vertices are appended to the next frontier with one atomic per
-//    warp per kRounds x 32 (or kSplit) slots (ballots + popc): a single
-//    global counter shared by every warp must not see one atomic per round.
+//  * visited vertices are staged in a per-warp shared-memory buffer and
+//    appended to the next frontier kStage at a time, one global atomic per
+//    batch: a single global counter shared by every warp serialises at one
+//    L2 slice, and waiting for its return was the top stall.
 // Op supplies:  Payload payload(int32_t v)             -- per-source-vertex value
 //               Probe probe(int64_t e, int32_t x)      -- loads only
 //               bool apply(Payload, int64_t e, int32_t x, Probe) -- true => push x
@@ -57,20 +58,43 @@ template <class Op>
 struct HasKeep<Op, std::void_t<decltype(std::declval<const Op &>().keep(0, typename Op::Payload()))>>
     : std::true_type {};
 
+constexpr int kStage = 256;  // staged queue entries per warp (shared memory)
+
+// The warp's staging buffers for the next frontier (and the far pile).
+struct ExpandStage {
+    WarpStage<kStage> near, far;
+};
+
+__device__ __forceinline__ ExpandStage make_stage() {
+    __shared__ int32_t s_near[kExpandBlock / 32][kStage];
+    __shared__ int32_t s_far[kExpandBlock / 32][kStage];
+    ExpandStage st;
+    st.near.buf = s_near[threadIdx.x >> 5];
+    st.far.buf = s_far[threadIdx.x >> 5];
+    return st;
+}
+
 template <class Op, int K>
 __device__ __forceinline__ void append_results(const Op &op, const int (&res)[K],
                                                const int32_t (&x)[K], ExpandCounters *cnt,
-                                               int32_t *qn) {
+                                               int32_t *qn, ExpandStage &st) {
     bool near[K];
 #pragma unroll
     for (int u = 0; u < K; u++) near[u] = res[u] == 1;
-    warp_append_multi<K>(near, x, &cnt->next_size, qn);
+    st.near.push<K>(near, x, &cnt->next_size, qn);
     if constexpr (HasFar<Op>::value) {
         bool far[K];
 #pragma unroll
         for (int u = 0; u < K; u++) far[u] = res[u] == 2;
-        warp_append_multi<K>(far, x, op.far_n, op.far_q, op.far_cap);
+        st.far.push<K>(far, x, op.far_n, op.far_q, op.far_cap);
     }
+}
+
+template <class Op>
+__device__ __forceinline__ void flush_stage(const Op &op, ExpandCounters *cnt, int32_t *qn,
+                                            ExpandStage &st) {
+    st.near.flush(&cnt->next_size, qn);
+    if constexpr (HasFar<Op>::value) st.far.flush(op.far_n, op.far_q, op.far_cap);
 }
 
 template <class Op>
@@ -86,6 +110,7 @@ __device__ __forceinline__ void expand_body(
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long scanned = 0;
+    ExpandStage st = make_stage();
     for (int64_t base = warp * vpw; base < nq; base += nwarps * vpw) {
         int64_t i = base + lane;
         int32_t v = -1;
@@ -144,9 +169,10 @@ __device__ __forceinline__ void expand_body(
 #pragma unroll
             for (int u = 0; u < kRounds; u++)
                 res[u] = e[u] >= 0 ? (int)op.apply(pv[u], e[u], x[u], pr[u]) : 0;
-            append_results<Op, kRounds>(op, res, x, cnt, qn);
+            append_results<Op, kRounds>(op, res, x, cnt, qn, st);
         }
     }
+    flush_stage(op, cnt, qn, st);
     // `scanned` is warp-uniform (every lane added the same totals)
     if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);
 }
@@ -178,6 +204,7 @@ __device__ __forceinline__ void expand_chunks_body(
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nch = (int64_t)__ldcg(&cnt->chunks);
     unsigned long long scanned = 0;
+    ExpandStage st = make_stage();
     for (int64_t w = warp; w < nch; w += nwarps) {
         const uint2 ch = chunks[w];
         const int32_t v = (int32_t)ch.x;
@@ -200,8 +227,9 @@ __device__ __forceinline__ void expand_chunks_body(
 #pragma unroll
         for (int j = 0; j < kPer; j++)
             res[j] = x[j] >= 0 ? (int)op.apply(pay, e0 + j * 32 + lane, x[j], pr[j]) : 0;
-        append_results<Op, kPer>(op, res, x, cnt, qn);
+        append_results<Op, kPer>(op, res, x, cnt, qn, st);
     }
+    flush_stage(op, cnt, qn, st);
     if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);  // warp-uniform
 }
 
