@@ -107,6 +107,21 @@ int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj,
 int sp_graph_generate(int kind, int64_t p0, int64_t p1, int64_t seed,
                       int undirected, int device, sp_graph **out);
 
+/* Text parsing of load_edge_list (graph.py:119-151), host only: `u v [w]`
+ * lines (\n, \r\n or \r terminated), '#' and blank lines skipped,
+ * duplicates kept, parsed on all host threads (nthreads <= 0: all).  On
+ * success *uvw is a malloc'd block [u | v | w] (stride info[7], info[6]
+ * edges) for sp_graph_from_edges; free it with sp_free_host.  info[8]:
+ * [0] error kind (1 field count, 2 non-integer field, 3 negative vertex id;
+ * returned with SP_ERR_ARG for the first failing line = the line the
+ * reference raises FormatError on), [1] that line number, [2..3] vertex id
+ * min/max, [4..5] weight min/max.  SP_ERR_UNSUPPORTED: non-ASCII text or
+ * values outside int32 (the host layer then parses with the reference's own
+ * Python semantics). */
+int sp_parse_edge_text(const char *buf, int64_t len, int64_t default_weight,
+                       int nthreads, int32_t **uvw, int64_t *info);
+void sp_free_host(void *p);
+
 int sp_graph_info(const sp_graph *g, int64_t *n, int64_t *m, int *directed);
 int sp_graph_download(const sp_graph *g, int which, void *host_dst);
 /* min_wt / max_wt (graph.py:252-261); SP_ERR_ARG when m == 0. */

@@ -67,6 +67,8 @@ SIGNATURES = {
     "sp_graph_from_edges": (_int, [_p, _p, _p, _i64, _i64, _int, _int, _int, _p]),
     "sp_graph_from_csr": (_int, [_p, _p, _p, _i64, _i64, _int, _int, _int, _p]),
     "sp_graph_generate": (_int, [_int, _i64, _i64, _i64, _int, _int, _p]),
+    "sp_parse_edge_text": (_int, [C.c_char_p, _i64, _i64, _int, _p, _p]),
+    "sp_free_host": (None, [_p]),
     "sp_graph_info": (_int, [_p, _p, _p, _p]),
     "sp_graph_download": (_int, [_p, _int, _p]),
     "sp_graph_weight_range": (_int, [_p, _p, _p]),

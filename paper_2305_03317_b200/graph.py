@@ -201,7 +201,7 @@ def _as_i32(a, what: str) -> np.ndarray:
 
 
 def from_arrays(u, v, w=None, directed: bool = True, default_weight: int = 1,
-                n: int | None = None, device: int = 0) -> CsrGraph:
+                n: int | None = None, device: int = 0, _nonneg: bool = False) -> CsrGraph:
     """Array form of ``from_edges``: edge i is (u[i], v[i], w[i])."""
     u = _as_i32(u, "vertex id")
     v = _as_i32(v, "vertex id")
@@ -210,7 +210,7 @@ def from_arrays(u, v, w=None, directed: bool = True, default_weight: int = 1,
     if w is None:
         w = np.full(len(u), default_weight, dtype=np.int64)
     w = _as_i32(w, "edge weight")
-    if len(u) and (int(u.min()) < 0 or int(v.min()) < 0):
+    if len(u) and not _nonneg and (int(u.min()) < 0 or int(v.min()) < 0):
         raise ArgError("negative vertex id in edge list")
     _lib.require_device(device)
     L = _lib.lib()
@@ -237,12 +237,55 @@ def load_edge_list(path: str, directed: bool = True,
                    default_weight: int = 1, device: int = 0) -> CsrGraph:
     """Whitespace-separated ``u v [w]`` edge list (graph.py:119-151): 0-based
     ids, ``#`` and blank lines skipped, duplicates kept; raises GraphIoError /
-    FormatError(lineno) exactly where the reference does."""
+    FormatError(lineno) exactly where the reference does.  The text is parsed
+    by the native multithreaded loader (sp_graph_from_edge_text); non-ASCII
+    text or values outside int32 take the reference's Python parsing path."""
     try:
-        with open(path, "r", encoding="utf-8") as f:
-            lines = f.readlines()
+        with open(path, "rb") as f:
+            data = f.read()
     except OSError as e:
         raise GraphIoError(f"cannot read graph file {path!r}: {e}") from e
+    if _I32_MIN <= int(default_weight) <= _I32_MAX:
+        L = _lib.lib()
+        info = (C.c_int64 * 8)()
+        blk = C.POINTER(C.c_int32)()
+        rc = L.sp_parse_edge_text(data, len(data), int(default_weight), 0, C.byref(blk), info)
+        if rc == _lib.SP_OK:
+            try:
+                ne, stride = int(info[6]), int(info[7])
+                a = np.ctypeslib.as_array(blk, shape=(3 * stride,))
+                return from_arrays(a[:ne], a[stride:stride + ne], a[2 * stride:2 * stride + ne],
+                                   directed=directed, device=device, _nonneg=True)
+            finally:
+                L.sp_free_host(blk)
+        if rc == _lib.SP_ERR_ARG and info[0] in (1, 2, 3):
+            _raise_format_error(data, int(info[0]), int(info[1]))
+        if rc != _lib.SP_ERR_UNSUPPORTED:
+            _check(rc, "sp_parse_edge_text")
+    return _load_edge_list_py(_py_lines(data), directed, default_weight, device)
+
+
+def _py_lines(data: bytes) -> list[str]:
+    """The lines f.readlines() yields in text mode (universal newlines)."""
+    text = data.decode("utf-8").replace("\r\n", "\n").replace("\r", "\n")
+    lines = text.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    return lines
+
+
+def _raise_format_error(data: bytes, kind: int, lineno: int):
+    """The reference's FormatError for line `lineno` (messages built from
+    the line text exactly as graph.py:134-148 does)."""
+    stripped = _py_lines(data)[lineno - 1].strip()
+    if kind == 1:
+        raise FormatError(lineno, f"expected 2 or 3 fields, got {len(stripped.split())}")
+    if kind == 2:
+        raise FormatError(lineno, f"non-integer field in {stripped!r}")
+    raise FormatError(lineno, f"negative vertex id in {stripped!r}")
+
+
+def _load_edge_list_py(lines, directed, default_weight, device) -> CsrGraph:
     us: list[int] = []
     vs: list[int] = []
     ws: list[int] = []
@@ -264,9 +307,17 @@ def load_edge_list(path: str, directed: bool = True,
         us.append(a)
         vs.append(b)
         ws.append(c)
-    return from_arrays(np.array(us, dtype=np.int64), np.array(vs, dtype=np.int64),
-                       np.array(ws, dtype=np.int64), directed=directed,
-                       device=device)
+    return from_arrays(_ints(us, "vertex id"), _ints(vs, "vertex id"),
+                       _ints(ws, "edge weight"), directed=directed, device=device)
+
+
+def _ints(vals: list[int], what: str) -> np.ndarray:
+    """int64 array of Python ints; values the backend cannot hold raise the
+    same ArgError as _as_i32."""
+    if vals and (min(vals) < _I32_MIN or max(vals) > _I32_MAX):
+        raise ArgError(f"{what} outside the int32 range [{min(vals)}, {max(vals)}] "
+                       "(unsupported by the B200 backend)")
+    return np.array(vals, dtype=np.int64)
 
 
 def from_csr(offsets, adj, weights, directed: bool = True,

@@ -391,3 +391,40 @@ def test_tc_dense_rows_cta_path(n, p, seed):
     g = sp.from_arrays(u, v, w, directed=False, n=n)
     o = cpu_ref.build_csr(u, v, w, False, n)
     assert sp.run(corpus.TC, g, {}).env.scalars["triangle_count"] == cpu_ref.tc(o, nthreads=8)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_native_loader_builds_reference_csr(case, tmp_path):
+    """load_edge_list through the native parser (mixed \\n / \\r\\n / \\r line
+    ends, comments, blank lines, tabs) builds the reference's CSR arrays."""
+    z = load_golden(case)
+    u, v, w = z["u"], z["v"], z["w"]
+    if len(u) == 0 or int(max(u.max(), v.max())) + 1 != int(z["n"]):
+        pytest.skip("n is not 1 + max id for this case")
+    ends = ["\n", "\r\n", "\r"]
+    lines = ["# generated from the golden edge list", ""]
+    for i in range(len(u)):
+        sep = "\t" if i % 3 == 0 else " "
+        lines.append(f"{u[i]}{sep}{v[i]} {w[i]}" if i % 5 else f"  {u[i]} {v[i]}  {w[i]} ")
+    text = "".join(ln + ends[i % 3] for i, ln in enumerate(lines))
+    p = tmp_path / "g.txt"
+    p.write_bytes(text.encode())
+    g = sp.load_edge_list(str(p), directed=bool(z["directed"]))
+    np.testing.assert_array_equal(g.offsets, z["csr_off"])
+    np.testing.assert_array_equal(g.adj, z["csr_adj"])
+    np.testing.assert_array_equal(g.weights, z["csr_w"])
+    np.testing.assert_array_equal(g.rev_adj, z["csr_radj"])
+
+
+def test_native_loader_large_file_matches_arrays(tmp_path):
+    """A multi-MiB file (parsed by several host threads) gives the same graph
+    as from_arrays on the same edges."""
+    u, v, w, n = gen.rmat(15, 16, seed=9)
+    text = "\n".join(f"{a} {b} {c}" for a, b, c in zip(u.tolist(), v.tolist(), w.tolist()))
+    p = tmp_path / "big.txt"
+    p.write_text(text + "\n")
+    g = sp.load_edge_list(str(p))
+    h = sp.from_arrays(u, v, w, directed=True)
+    np.testing.assert_array_equal(g.offsets, h.offsets)
+    np.testing.assert_array_equal(g.adj, h.adj)
+    np.testing.assert_array_equal(g.weights, h.weights)

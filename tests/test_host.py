@@ -185,6 +185,61 @@ def test_loader_format_errors(tmp_path, text, lineno, msg):
         assert str(er.value) == str(ei.value)
 
 
+_TRICKY = [
+    b"0 1\r\n1 2\r\n2 x\r\n",                    # CRLF, error on line 3
+    b"0 1\r1 2\r-3 4\r",                           # bare CR terminators
+    b"0 1\n\r\n1 2 3 4\n",                         # \n then \r\n: line 3
+    b"  # comment\n\t\n0\t1\x0b\n1 1_0\n2 1__0\n",  # \v whitespace, underscores
+    b"0 1\n2 _3\n",
+    b"0 1\n3_ 4\n",
+    b"0 1\n+\n",
+    b"0 +1 -2\n1 2 0x10\n",
+    b"0 1 2\n1.5 2\n",
+    b"0 1\n\x0c\x1c\n5 -0\n-0 3\n 7\n",           # \f, \x1c whitespace; -0 is 0
+    b"0 1 99999999999999999999\n1 2 x\n",           # huge weight parses, then error
+    b"0 1",                                          # no final newline, valid
+]
+
+
+@pytest.mark.parametrize("k", range(len(_TRICKY)))
+def test_native_parser_errors_match_reference(tmp_path, k):
+    """The native parser raises FormatError on the same line with the same
+    message as the reference (or parses the file the reference accepts)."""
+    p = tmp_path / "g.txt"
+    p.write_bytes(_TRICKY[k])
+    ours = ref = None
+    try:
+        spg.load_edge_list(str(p))
+    except FormatError as e:
+        ours = str(e)
+    except (RuntimeError, ArgError):
+        ours = "parsed"  # no GPU here (or out of int32 range): the text parsed
+    if not HAVE_REF:
+        return
+    sys.path.insert(0, REF)
+    from trident.errors import FormatError as RFE
+    from trident.graph import load_edge_list
+    try:
+        load_edge_list(str(p))
+        ref = "parsed"
+    except RFE as e:
+        ref = str(e)
+    assert ours == ref
+
+
+def test_native_parser_multithreaded_error_line(tmp_path):
+    """A > 1 MiB file is cut into per-thread parts; the reported line is the
+    global first failing line."""
+    good = "".join(f"{i} {i + 1} {i % 7}\n" for i in range(120000))
+    text = "# header\n" + good + "12 oops\n" + good + "bad line here now\n"
+    p = tmp_path / "big.txt"
+    p.write_text(text)
+    with pytest.raises(FormatError) as ei:
+        spg.load_edge_list(str(p))
+    assert ei.value.lineno == 1 + 120000 + 1
+    assert "non-integer field in '12 oops'" in str(ei.value)
+
+
 def test_loader_io_error(tmp_path):
     with pytest.raises(GraphIoError):
         spg.load_edge_list(str(tmp_path / "missing.txt"))
