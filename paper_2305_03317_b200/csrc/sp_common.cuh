@@ -88,6 +88,11 @@ struct Call {
     ~Call();
 };
 
+// Launch `graph` through this thread's executable cache for (key, kind)
+// (see sp_runtime.cu); the caller keeps ownership of `graph`.
+enum { kLoopSsspBf = 1, kLoopSsspNf = 2, kLoopPr = 3 };
+int launch_cached_graph(cudaGraph_t graph, const void *key, int kind, cudaStream_t stream);
+
 // Copy a caller buffer to/from the device according to `mem`.
 int to_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s);
 int from_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s);

@@ -25,10 +25,13 @@
 //     holding a row's last slot stores the row sum (sums[k], k = nz row).
 //     Every warp does the same work whatever the degree mix (a 100K-slot hub
 //     is just 50 units).
-//   k_pr_fix: a row that started in an earlier unit is finished here: its
-//     unit partials are added left-to-right (deterministic, fixed shape).
 //   k_pr_epi: pr.sp:17-23 for every non-empty row, coalesced over k
-//     (newRank, |delta| max, rank and contrib writes).
+//     (newRank, |delta| max, rank and contrib writes); a row that started
+//     in an earlier unit is finished here first, its unit partials added
+//     left to right (deterministic, fixed shape).
+//   The iterations run as a device-side loop (CUDA graph with a conditional
+//   WHILE node; k_pr_advance evaluates `diff < eps || iter >= maxIter` and
+//   swaps the contrib buffers) unless a per-iteration callback is set.
 //   k_pr_zero: rows with no in-edges have sum = 0, so newRank = (1-d)/n in
 //     every iteration; they are written in iteration 1 only (identical bits
 //     afterwards, |delta| = 0), into both contrib buffers.
@@ -83,10 +86,30 @@ struct PrArgs {
     const int64_t *__restrict__ unit_row;  // first nz row with end > unit start
     double *__restrict__ hp;         // partial of a row that began before the unit
     double *__restrict__ tp;         // partial of the row still open at unit end
-    int32_t *__restrict__ hs;        // unit holds the end of a row begun earlier
     double base, damping;
     double *diff_slot;
+    struct PrLoop *loop;  // device loop state (cin/cout/slot come from it) or null
 };
+
+// Device-side fixedPoint loop state (pr.sp:10): contrib ping-pong and diff
+// slots are picked by `cur`, so the captured kernels never change.
+struct PrLoop {
+    double *c[2];
+    double *slot[2];
+    int cur;
+    int64_t iter, iters, max_iter, cap;
+    double eps, diff;
+    int status;  // 0 running/converged, 2 cap reached
+};
+
+__device__ __forceinline__ void pr_bind(PrArgs &a) {
+    if (a.loop) {
+        const int cur = a.loop->cur;
+        a.cin = a.loop->c[cur];
+        a.cout = a.loop->c[cur ^ 1];
+        a.diff_slot = a.loop->slot[cur];
+    }
+}
 
 // pr.sp:17-23 for one vertex; returns |newRank - rank|.
 __device__ __forceinline__ double pr_apply(const PrArgs &a, int64_t v, double sum) {
@@ -132,6 +155,7 @@ __device__ __forceinline__ void load_slab(const int32_t *__restrict__ radj, int6
 
 // Row sums over edge-balanced units (see the file header).
 __global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
+    pr_bind(a);
     __shared__ uint32_t bitmap[kWarps][kCh / 32];
     const unsigned lane = lane_id();
     uint32_t *bm = bitmap[threadIdx.x >> 5];
@@ -145,7 +169,6 @@ __global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
         const int64_t first_row = rk;
         // the unit's first row began in an earlier unit
         const bool head_spill = (rk > 0 ? __ldg(a.nzend + rk - 1) : 0) < s0;
-        bool spill_flushed = false;
         double carry = 0.0;
         int nxt[8];
         load_slab(a.radj, s0, s1, lane, nxt);
@@ -221,8 +244,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
                         const double total = j == 0 ? __dadd_rn(carry_in, run) : run;
                         const int64_t row = rk_chunk + nbefore + j;
                         if (head_spill && row == first_row) {
-                            a.hp[u] = total;
-                            spill_flushed = true;
+                            a.hp[u] = total;  // finished by k_pr_epi
                         } else {
                             a.sums[row - a.K0] = total;
                         }
@@ -232,34 +254,19 @@ __global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
                 }
             }
         }
-        spill_flushed = __any_sync(0xffffffffu, spill_flushed);
-        if (lane == 0) {
-            a.tp[u] = carry;
-            a.hs[u] = spill_flushed ? 1 : 0;
-        }
-    }
-}
-
-// Rows spanning several units: partials added left-to-right.
-__global__ void k_pr_fix(PrArgs a) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < a.nunits;
-         u += (int64_t)gridDim.x * blockDim.x) {
-        if (a.hs[u]) {
-            const int64_t row = a.unit_row[u];
-            const int64_t start = row > 0 ? a.nzend[row - 1] : 0;
-            const int64_t ustart = max((int64_t)0, start / kUnit - a.u0);
-            double acc = 0.0;
-            for (int64_t w = ustart; w < u; w++) acc = __dadd_rn(acc, a.tp[w]);
-            a.sums[row - a.K0] = __dadd_rn(acc, a.hp[u]);
-        }
+        if (lane == 0) a.tp[u] = carry;
     }
 }
 
 // pr.sp:17-23 for every non-empty row of the block (coalesced over k).
 // Each thread takes kEpi rows strided by the block size: all loads of a
 // thread are issued before any store (memory-level parallelism).
+// A row whose first and last slots lie in different units (a "spill" row)
+// was not summed by k_pr_units: its partials are added here left to right,
+// tp of every unit it crosses, then hp of the unit holding its end.
 constexpr int kEpi = 4;
 __global__ void __launch_bounds__(256) k_pr_epi(PrArgs a) {
+    pr_bind(a);
     const int64_t nk = a.K1 - a.K0;
     const int64_t base_k = blockIdx.x * (int64_t)(256 * kEpi) + threadIdx.x;
     int32_t v[kEpi];
@@ -269,7 +276,20 @@ __global__ void __launch_bounds__(256) k_pr_epi(PrArgs a) {
     for (int j = 0; j < kEpi; j++) {
         const int64_t k = base_k + j * 256;
         v[j] = k < nk ? __ldcs(a.nzrow + a.K0 + k) : -1;
-        sum[j] = k < nk ? __ldcs(a.sums + k) : 0.0;
+        sum[j] = 0.0;
+        if (k < nk) {
+            const int64_t kk = a.K0 + k;
+            const int64_t end = __ldg(a.nzend + kk);
+            const int64_t start = kk > 0 ? __ldg(a.nzend + kk - 1) : 0;
+            const int64_t us = start / kUnit, ue = (end - 1) / kUnit;
+            if (us == ue) {
+                sum[j] = __ldcs(a.sums + k);
+            } else {
+                double acc = 0.0;
+                for (int64_t w = us; w < ue; w++) acc = __dadd_rn(acc, a.tp[w - a.u0]);
+                sum[j] = __dadd_rn(acc, a.hp[ue - a.u0]);
+            }
+        }
     }
 #pragma unroll
     for (int j = 0; j < kEpi; j++) {
@@ -294,6 +314,7 @@ __global__ void __launch_bounds__(256) k_pr_epi(PrArgs a) {
 // other contrib buffer of the single-GPU ping-pong.
 __global__ void __launch_bounds__(256) k_pr_zero(PrArgs a, const int32_t *__restrict__ indeg,
                                                  int64_t v1, double *cout2) {
+    pr_bind(a);
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double dmax = 0.0;
     if (i < v1 - a.v0 && __ldcs(indeg + a.v0 + i) == 0) {
@@ -339,7 +360,7 @@ __global__ void k_pr_bounds(const int64_t *__restrict__ roff, const int32_t *__r
 // Per-call state of the fast path for a vertex block [v0, v1).
 struct FastPlan {
     PrArgs a{};
-    int grid_units = 1, grid_fix = 1, grid_epi = 1, grid_zero = 1;
+    int grid_units = 1, grid_epi = 1, grid_zero = 1;
 };
 
 int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, FastPlan &p) {
@@ -369,15 +390,12 @@ int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, Fast
     int64_t *ur;
     SP_TRY(c.alloc(&ur, nu));
     double *hp, *tp, *sums;
-    int32_t *hs;
     SP_TRY(c.alloc(&sums, std::max<int64_t>(1, a.K1 - a.K0)));
     a.sums = sums;
     SP_TRY(c.alloc(&hp, nu));
     SP_TRY(c.alloc(&tp, nu));
-    SP_TRY(c.alloc(&hs, nu));
     a.hp = hp;
     a.tp = tp;
-    a.hs = hs;
     a.unit_row = ur;
     if (a.nunits) {
         k_pr_setup<<<grid_for(a.nunits, 256, c.device), 256, 0, c.stream>>>(
@@ -386,7 +404,6 @@ int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, Fast
     }
     // one unit per warp, no cap: the block scheduler balances the tail
     p.grid_units = (int)std::max<int64_t>(1, (a.nunits + kWarps - 1) / kWarps);
-    p.grid_fix = grid_for(std::max<int64_t>(1, a.nunits), 256, c.device, 4);
     p.grid_epi = (int)std::max<int64_t>(1, (a.K1 - a.K0 + 256 * kEpi - 1) / (256 * kEpi));
     p.grid_zero = (int)std::max<int64_t>(1, (v1 - v0 + 255) / 256);
     SP_CUDA(cudaGetLastError());
@@ -405,9 +422,8 @@ int launch_fast(Call &c, FastPlan &p, sp_graph *g, int64_t v1, const double *cin
     if (ka) cudaEventRecord(ka, c.stream);
     if (a.nunits) {
         k_pr_units<<<p.grid_units, kBlock, 0, c.stream>>>(a);
-        k_pr_fix<<<p.grid_fix, 256, 0, c.stream>>>(a);
         k_pr_epi<<<p.grid_epi, 256, 0, c.stream>>>(a);
-        c.launches += 3;
+        c.launches += 2;
     }
     if (kb) cudaEventRecord(kb, c.stream);
     if (zero) {
@@ -415,6 +431,88 @@ int launch_fast(Call &c, FastPlan &p, sp_graph *g, int64_t v1, const double *cin
         c.launches++;
     }
     SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
+__global__ void k_pr_advance(PrLoop *L, cudaGraphConditionalHandle h) {
+    const int cur = L->cur;
+    const double diff = *L->slot[cur];
+    L->diff = diff;
+    L->iter++;
+    L->iters++;
+    int go = !(diff < L->eps || L->iter >= L->max_iter);  // pr.sp:10
+    if (go && L->iters >= L->cap) {
+        L->status = 2;
+        go = 0;
+    }
+    *L->slot[cur ^ 1] = 0.0;
+    L->cur = cur ^ 1;
+    cudaGraphSetConditional(h, go);
+}
+
+// Iterations 2.. of the fast path as one graph launch (no host round trip
+// per iteration).  `hL` receives the final loop state.
+int pr_device_loop(Call &c, FastPlan &p, double *rank, double *c0, double *c1, double *s0,
+                   double *s1, int64_t iter0, int64_t iters0, int64_t max_iter, int64_t cap,
+                   double eps, PrLoop *hL, float *kernel_ms) {
+    PrLoop *L;
+    SP_TRY(c.alloc(&L, 1));
+    PrLoop init{};
+    init.c[0] = c0;
+    init.c[1] = c1;
+    init.slot[0] = s0;
+    init.slot[1] = s1;
+    init.iter = iter0;
+    init.iters = iters0;
+    init.max_iter = max_iter;
+    init.cap = cap;
+    init.eps = eps;
+    SP_CUDA(cudaMemcpyAsync(L, &init, sizeof(PrLoop), cudaMemcpyHostToDevice, c.stream));
+    SP_CUDA(cudaMemsetAsync(s0, 0, sizeof(double), c.stream));
+    PrArgs a = p.a;
+    a.rank = rank;
+    a.loop = L;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    struct GraphFree {
+        cudaGraph_t *g;
+        cudaGraphExec_t *e;
+        ~GraphFree() {
+            if (*e) cudaGraphExecDestroy(*e);
+            if (*g) cudaGraphDestroy(*g);
+        }
+    } gf{&graph, &exec};
+    SP_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    SP_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    SP_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+    if (a.nunits) {
+        k_pr_units<<<p.grid_units, kBlock, 0, c.stream>>>(a);
+        k_pr_epi<<<p.grid_epi, 256, 0, c.stream>>>(a);
+    }
+    k_pr_advance<<<1, 1, 0, c.stream>>>(L, h);
+    SP_CUDA(cudaStreamEndCapture(c.stream, &body));
+    cudaEvent_t ka, kb;
+    SP_CUDA(cudaEventCreate(&ka));
+    SP_CUDA(cudaEventCreate(&kb));
+    cudaEventRecord(ka, c.stream);
+    SP_TRY(launch_cached_graph(graph, p.a.radj, kLoopPr, c.stream));
+    cudaEventRecord(kb, c.stream);
+    SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(PrLoop), cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    cudaEventElapsedTime(kernel_ms, ka, kb);
+    cudaEventDestroy(ka);
+    cudaEventDestroy(kb);
+    c.launches += (hL->iters - iters0) * 3;
     return SP_OK;
 }
 
@@ -560,6 +658,24 @@ extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t 
             set_error("fixedPoint 'converged' did not converge within %lld iterations",
                       (long long)cap);
             rc = SP_ERR_NONCONV;
+            break;
+        }
+        if (!cb && !exact && n) {
+            // the remaining iterations on the device: contrib to read is ca
+            PrLoop *hL;
+            SP_TRY(c.host_as(&hL));
+            float ms = 0.f;
+            SP_TRY(pr_device_loop(c, plan, rank, ca, cb2, diffs, diffs + 1, iter, iters,
+                                  max_iter, cap, epsilon, hL, &ms));
+            kernel_ms += ms;
+            iter = hL->iter;
+            iters = hL->iters;
+            diff = hL->diff;
+            if (hL->status == 2) {
+                set_error("fixedPoint 'converged' did not converge within %lld iterations",
+                          (long long)cap);
+                rc = SP_ERR_NONCONV;
+            }
             break;
         }
     }

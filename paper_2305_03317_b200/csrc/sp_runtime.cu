@@ -236,6 +236,50 @@ Call::~Call() {
     }
 }
 
+// Executable graphs of the device-side loops, per host thread, keyed by
+// (graph handle, loop kind): a later call captures its body again and
+// refreshes the executable with cudaGraphExecUpdate (kernel parameters
+// change from call to call, the topology does not), which is far cheaper
+// than cudaGraphInstantiate; a topology change falls back to instantiate.
+struct ExecEntry {
+    const void *key;
+    int kind;
+    cudaGraphExec_t exec;
+};
+struct ExecCache {
+    std::vector<ExecEntry> v;
+    ~ExecCache() {
+        for (auto &e : v) cudaGraphExecDestroy(e.exec);
+    }
+};
+static thread_local ExecCache g_exec_cache;
+
+int launch_cached_graph(cudaGraph_t graph, const void *key, int kind, cudaStream_t stream) {
+    for (auto &e : g_exec_cache.v) {
+        if (e.key != key || e.kind != kind) continue;
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(e.exec, graph, &info) == cudaSuccess) {
+            SP_CUDA(cudaGraphLaunch(e.exec, stream));
+            return SP_OK;
+        }
+        cudaGetLastError();
+        cudaGraphExecDestroy(e.exec);
+        e.exec = nullptr;
+        SP_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
+        SP_CUDA(cudaGraphLaunch(e.exec, stream));
+        return SP_OK;
+    }
+    cudaGraphExec_t exec = nullptr;
+    SP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    if (g_exec_cache.v.size() >= 16) {  // bounded: drop the oldest
+        cudaGraphExecDestroy(g_exec_cache.v.front().exec);
+        g_exec_cache.v.erase(g_exec_cache.v.begin());
+    }
+    g_exec_cache.v.push_back(ExecEntry{key, kind, exec});
+    SP_CUDA(cudaGraphLaunch(exec, stream));
+    return SP_OK;
+}
+
 int to_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s) {
     if (!bytes) return SP_OK;
     SP_CUDA(cudaMemcpyAsync(dst, src, bytes,

@@ -361,12 +361,11 @@ int sssp_near_far(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa
     k_nf_split<<<grid, kBlock, 0, c.stream>>>(dist, enq, last, L);
     k_nf_advance2<<<1, 1, 0, c.stream>>>(L, h);
     SP_CUDA(cudaStreamEndCapture(c.stream, &body));
-    SP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     cudaEvent_t ka, kb;
     SP_CUDA(cudaEventCreate(&ka));
     SP_CUDA(cudaEventCreate(&kb));
     cudaEventRecord(ka, c.stream);
-    SP_CUDA(cudaGraphLaunch(exec, c.stream));
+    SP_TRY(launch_cached_graph(graph, g, kLoopSsspNf, c.stream));
     cudaEventRecord(kb, c.stream);
     NfLoop *hL;
     SP_TRY(c.host_as(&hL));
@@ -442,12 +441,11 @@ int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t 
     k_loop_advance<<<1, 1, 0, c.stream>>>(L, h);
     cudaError_t ce = cudaStreamEndCapture(c.stream, &body);
     SP_CUDA(ce);
-    SP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     cudaEvent_t ka, kb;
     SP_CUDA(cudaEventCreate(&ka));
     SP_CUDA(cudaEventCreate(&kb));
     cudaEventRecord(ka, c.stream);
-    SP_CUDA(cudaGraphLaunch(exec, c.stream));
+    SP_TRY(launch_cached_graph(graph, g, kLoopSsspBf, c.stream));
     cudaEventRecord(kb, c.stream);
     SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(SsspLoop), cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
