@@ -1,0 +1,107 @@
+"""Parity at the BASELINE configs' full sizes.
+
+The CPU oracle (oracle/cpu_ref.c, pinned bit-exact to the reference) runs
+the full-size PR / SSSP / BC (sampled sources) / TC configs here, fed with
+the device graph's CSR arrays (the CSR builder itself is pinned against the
+reference on the golden cases and by the device-vs-host generator tests).
+Where the oracle would take too long (SSSP on the 4096x4096 grid, ~10^4
+sequential sweeps) the result is certified by a size-independent property:
+the Bellman optimality conditions, which determine shortest-path distances
+uniquely for positive weights."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import REPO  # noqa: F401
+from oracle import cpu_ref
+
+import paper_2305_03317_b200 as sp  # noqa: E402
+from paper_2305_03317_b200 import corpus  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+NT = os.cpu_count() or 1
+PR_ARGS = {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
+
+
+def _oracle_csr(g):
+    return cpu_ref.Csr(g.n, g.m, g.directed, np.asarray(g.offsets), np.asarray(g.adj),
+                       np.asarray(g.weights), np.asarray(g.rev_offsets),
+                       np.asarray(g.rev_adj), None, np.asarray(g.effective_weights))
+
+
+@pytest.fixture(scope="module")
+def rmat22():
+    g = sp.generate("rmat", 22, 16, seed=1)
+    yield g, _oracle_csr(g)
+    g.close()
+
+
+def test_pr_cfg2_full(rmat22):
+    """BASELINE cfg2: PR on RMAT-22 -- fast mode within 1e-12 relative and the
+    same iteration count; deterministic mode bit-exact."""
+    g, o = rmat22
+    rank, it, diff, its, rc = cpu_ref.pagerank(o, nthreads=NT)
+    assert rc == 0
+    r = sp.run(corpus.PR, g, PR_ARGS)
+    assert r.env.scalars["iter"] == it
+    rel = np.abs(r.env.node_props["rank"] - rank).max() / np.abs(rank).max()
+    assert rel <= 1e-12
+    rd = sp.run(corpus.PR, g, PR_ARGS, deterministic=True)
+    assert rd.env.node_props["rank"].tobytes() == rank.tobytes()
+    assert rd.env.scalars["iter"] == it and rd.env.scalars["diff"] == diff
+
+
+def test_sssp_rmat22_full(rmat22):
+    g, o = rmat22
+    dist, _, rc = cpu_ref.sssp(o, 0)
+    assert rc == 0
+    np.testing.assert_array_equal(sp.run(corpus.SSSP, g, {"src": 0}).env.node_props["dist"],
+                                  dist)
+
+
+def test_bc_cfg4_full_sampled_sources():
+    """BASELINE cfg4 graph (symmetrized RMAT-20) with 6 of the 256 sources."""
+    g = sp.generate("rmat", 20, 16, seed=1, undirected=True)
+    o = _oracle_csr(g)
+    deg = np.diff(o.off)
+    srcs = np.random.default_rng(1).choice(np.flatnonzero(deg > 0), size=256,
+                                           replace=False)[:6].tolist()
+    bc, sg, dl = cpu_ref.bc(o, srcs, nthreads=NT)
+    r = sp.run(corpus.BC, g, {"sourceSet": srcs})
+    rel = np.abs(r.env.node_props["bc"] - bc).max() / np.abs(bc).max()
+    assert rel <= 1e-12
+    np.testing.assert_array_equal(r.env.node_props["sigma"], sg)  # exact path counts
+    rd = sp.run(corpus.BC, g, {"sourceSet": srcs}, deterministic=True)
+    assert rd.env.node_props["bc"].tobytes() == bc.tobytes()
+    assert rd.env.node_props["delta"].tobytes() == dl.tobytes()
+    g.close()
+
+
+def test_tc_cfg3_full():
+    """BASELINE cfg3: uniform 2^24 vertices / 2^28 edges, exact count."""
+    g = sp.generate("uniform", 1 << 24, 1 << 28, seed=1, undirected=True)
+    o = cpu_ref.Csr(g.n, g.m, False, np.asarray(g.offsets), np.asarray(g.adj), None, None,
+                    None, None, None)
+    t = sp.run(corpus.TC, g, {}).env.scalars["triangle_count"]
+    assert t == cpu_ref.tc(o, nthreads=NT)
+    g.close()
+
+
+def test_sssp_grid_cfg5_bellman_certificate():
+    """BASELINE cfg5a: 4096x4096 grid, SSSP from 0.  dist[0] = 0 and, for
+    every other vertex, dist = min over in-edges of dist[u] + w_eff (all
+    vertices are reached on a connected grid): the Bellman equations, whose
+    solution is unique for positive weights."""
+    g = sp.generate("grid", 4096, 4096, seed=1)
+    dist = sp.run(corpus.SSSP, g, {"src": 0}).env.node_props["dist"].astype(np.int64)
+    off, adj = np.asarray(g.offsets), np.asarray(g.adj)
+    w = np.asarray(g.effective_weights).astype(np.int64)
+    assert w.min() > 0 and dist[0] == 0 and dist.max() < 2147483647
+    src = np.repeat(np.arange(g.n), np.diff(off))
+    best = np.full(g.n, np.iinfo(np.int64).max)
+    np.minimum.at(best, adj, dist[src] + w)
+    best[0] = 0
+    np.testing.assert_array_equal(dist, best)
+    g.close()
