@@ -39,16 +39,27 @@ namespace {
 constexpr int64_t kBcHub = 8192;  // rows longer than this take the CTA fold
 constexpr int kBcWorkers = 4;     // concurrent sources (host threads/streams), fast mode
 
+// Per-vertex record, 16 bytes: level (int32) and, in fast mode, the child
+// coefficient coef[w] = (1 + delta[w]) / sigma[w] (written when delta[w] is
+// final).  A delta-fold term then needs ONE random 16-byte read (level and
+// coef share a sector) instead of level, sigma[w] and delta[w].  `level`
+// below points at the record array viewed as int32, stride kVs.
+constexpr int64_t kVs = 4;
+__device__ __forceinline__ int32_t *lvl(int32_t *vs, int32_t x) { return vs + kVs * (int64_t)x; }
+__device__ __forceinline__ const int32_t *lvl(const int32_t *vs, int32_t x) {
+    return vs + kVs * (int64_t)x;
+}
+
 struct DiscoverOp {
     using Payload = int;
     using Probe = int;  // level[x]
     int32_t *__restrict__ level;
     int next;
     __device__ __forceinline__ int payload(int32_t) const { return 0; }
-    __device__ __forceinline__ int probe(int64_t, int32_t x) const { return __ldcg(level + x); }
+    __device__ __forceinline__ int probe(int64_t, int32_t x) const { return __ldcg(lvl(level, x)); }
     __device__ __forceinline__ bool apply(int, int64_t, int32_t x, int lx) const {
         if (lx != -1) return false;
-        return atomicCAS(level + x, -1, next) == -1;
+        return atomicCAS(lvl(level, x), -1, next) == -1;
     }
 };
 
@@ -64,12 +75,12 @@ struct DiscoverSigmaOp {
     double *__restrict__ sigma;
     int next;
     __device__ __forceinline__ double payload(int32_t v) const { return __ldcg(sigma + v); }
-    __device__ __forceinline__ int probe(int64_t, int32_t x) const { return __ldcg(level + x); }
+    __device__ __forceinline__ int probe(int64_t, int32_t x) const { return __ldcg(lvl(level, x)); }
     __device__ __forceinline__ bool apply(double sv, int64_t, int32_t x, int lx) const {
         if (lx != -1 && lx != next) return false;
         bool won = false;
         if (lx == -1) {
-            const int old = atomicCAS(level + x, -1, next);
+            const int old = atomicCAS(lvl(level, x), -1, next);
             won = old == -1;
             if (!won && old != next) return false;
         }
@@ -86,12 +97,12 @@ struct SigmaFold {  // bc.sp:10-12 over reverse-CSR slots (deterministic mode)
     __device__ __forceinline__ double payload(int32_t) const { return 0.0; }
     __device__ __forceinline__ double term(double, int64_t k) const {
         const int32_t u = radj[k];
-        return __ldg(level + u) == parent_level ? sigma[u] : 0.0;
+        return __ldg(lvl(level, u)) == parent_level ? sigma[u] : 0.0;
     }
     __device__ __forceinline__ void finish(int32_t v, double s) const { sigma[v] = s; }
 };
 
-struct DeltaFold {  // bc.sp:14-19 over CSR slots
+struct DeltaFold {  // bc.sp:14-19 over CSR slots (deterministic mode: exact formula)
     const int32_t *__restrict__ adj;
     const int32_t *__restrict__ level;
     const double *__restrict__ sigma;
@@ -102,7 +113,7 @@ struct DeltaFold {  // bc.sp:14-19 over CSR slots
     __device__ __forceinline__ double payload(int32_t v) const { return sigma[v]; }
     __device__ __forceinline__ double term(double sv, int64_t e) const {
         const int32_t w = adj[e];
-        if (__ldg(level + w) != child_level) return 0.0;
+        if (__ldg(lvl(level, w)) != child_level) return 0.0;
         return __dmul_rn(__ddiv_rn(sv, sigma[w]), __dadd_rn(1.0, delta[w]));
     }
     __device__ __forceinline__ void finish(int32_t v, double s) const {
@@ -111,8 +122,43 @@ struct DeltaFold {  // bc.sp:14-19 over CSR slots
     }
 };
 
+// Fast mode: term = sigma_v * coef_w from one 16-byte record read
+// (sigma_v / sigma_w * (1 + delta_w) regrouped: a few ulps apart).
+struct DeltaFoldFast {
+    const int32_t *__restrict__ adj;
+    int32_t *__restrict__ vs;  // records (level, coef)
+    const double *__restrict__ sigma;
+    double *__restrict__ delta;
+    double *__restrict__ bc;
+    int child_level;
+    int32_t src;
+    __device__ __forceinline__ double payload(int32_t v) const { return sigma[v]; }
+    __device__ __forceinline__ double term(double sv, int64_t e) const {
+        const int32_t w = __ldcs(adj + e);
+        const int4 r = __ldg(reinterpret_cast<const int4 *>(vs) + w);
+        if (r.x != child_level) return 0.0;
+        return __dmul_rn(sv, __hiloint2double(r.w, r.z));
+    }
+    __device__ __forceinline__ void finish(int32_t v, double s) const {
+        delta[v] = s;
+        reinterpret_cast<double *>(vs)[2 * (int64_t)v + 1] =
+            __ddiv_rn(__dadd_rn(1.0, s), sigma[v]);
+        if (v != src) bc[v] = __dadd_rn(bc[v], __ddiv_rn(s, 2.0));
+    }
+};
+
+// coef of the deepest level's vertices (no children: delta = 0)
+__global__ void k_leaf_coef(const int32_t *__restrict__ q, int64_t nq, int32_t *vs,
+                            const double *__restrict__ sigma) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = q[i];
+        reinterpret_cast<double *>(vs)[2 * (int64_t)v + 1] = __ddiv_rn(1.0, sigma[v]);
+    }
+}
+
 __global__ void k_root(int32_t *level, double *sigma, int32_t *queue, int32_t s) {
-    level[s] = 0;
+    level[kVs * (int64_t)s] = 0;
     sigma[s] = 1.0;
     queue[0] = s;
 }
@@ -141,7 +187,7 @@ int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
     uint2 *chunks;
     ExpandCounters *cnt;
     unsigned long long *nhubs;
-    SP_TRY(c.alloc(&level, n));
+    SP_TRY(c.alloc(&level, kVs * n));  // 16-byte (level, coef) records
     SP_TRY(c.alloc(&queue, n));
     SP_TRY(c.alloc(&hubs, n));
     const int64_t ccap = fold_chunk_capacity(g->m);
@@ -157,7 +203,7 @@ int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
     SP_TRY(c.alloc(&cnt, 1));
     SP_TRY(c.alloc(&nhubs, 3));
     const FoldLists fl{hubs, nhubs, FoldChunks{reg_v, reg_base, reg_nch, item_reg, csum, nullptr}};
-    c.persist(level, n * sizeof(int32_t));  // BFS probes hit level[] at random
+    c.persist(level, kVs * n * sizeof(int32_t));  // BFS/fold probes hit the records at random
     SP_CUDA(cudaMemsetAsync(bc, 0, n * sizeof(double), c.stream));
     SP_CUDA(cudaMemsetAsync(sigma, 0, n * sizeof(double), c.stream));
     SP_CUDA(cudaMemsetAsync(delta, 0, n * sizeof(double), c.stream));
@@ -168,7 +214,7 @@ int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
     int64_t last_done = -1;
     for (int64_t si = first; si < nsrc; si += stride) {
         const int32_t s = srcs[si];
-        SP_CUDA(cudaMemsetAsync(level, 0xFF, n * sizeof(int32_t), c.stream));
+        SP_CUDA(cudaMemsetAsync(level, 0xFF, kVs * n * sizeof(int32_t), c.stream));
         if (last_done >= 0) {
             SP_CUDA(cudaMemsetAsync(sigma, 0, n * sizeof(double), c.stream));
             SP_CUDA(cudaMemsetAsync(delta, 0, n * sizeof(double), c.stream));
@@ -205,10 +251,23 @@ int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
         const int nlev = (int)ls.size() - 1;
         wk.levels += nlev;
         wk.reached += ls.back();
+        if (!det && nlev >= 2) {
+            const int64_t d0 = ls[nlev - 1], d1 = ls[nlev];
+            k_leaf_coef<<<grid_for(d1 - d0, 256, c.device), 256, 0, c.stream>>>(queue + d0,
+                                                                               d1 - d0, level,
+                                                                               sigma);
+            c.launches++;
+        }
         for (int L = nlev - 2; L >= 0; L--) {
-            DeltaFold df{g->adj, level, sigma, delta, bc, L + 1, s};
-            launch_fold(df, g->off, queue + ls[L], ls[L + 1] - ls[L], kBcHub, fl, det,
-                        g->max_outdeg, sms, c.stream, &c.launches);
+            if (det) {
+                DeltaFold df{g->adj, level, sigma, delta, bc, L + 1, s};
+                launch_fold(df, g->off, queue + ls[L], ls[L + 1] - ls[L], kBcHub, fl, det,
+                            g->max_outdeg, sms, c.stream, &c.launches);
+            } else {
+                DeltaFoldFast df{g->adj, level, sigma, delta, bc, L + 1, s};
+                launch_fold(df, g->off, queue + ls[L], ls[L + 1] - ls[L], kBcHub, fl, det,
+                            g->max_outdeg, sms, c.stream, &c.launches);
+            }
         }
         SP_CUDA(cudaGetLastError());
         last_done = si;
