@@ -20,6 +20,7 @@
 //   * the frontier size is the convergence flag (finished = size == 0):
 //     one 8-byte device->host read per iteration (K5/K6 in SURVEY 2.2).
 // Candidates >= INT_MAX never win (interp.py:11-14).
+#include <cooperative_groups.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -33,6 +34,7 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int64_t kDeltaMul = 16;        // near-far step = kDeltaMul x mean weight
 constexpr int64_t kNearFarMaxAvgDeg = 8;  // near-far only when m <= 8 n
+constexpr int kPersistBlocksPerSm = 1;    // persistent near-far grid: blocks per SM
 
 // Relaxation of sssp.sp:11-12 for one slot; payload = dist[v] at expansion.
 struct RelaxOp {
@@ -153,6 +155,7 @@ struct NfLoop {
     int64_t iters, relaxed, frontier_sum, cap;
     unsigned long long fcap;  // far pile capacity
     int status;               // 0 ok, 1 overflow, 2 cap, 3 far pile overflow
+    int go;                   // persistent kernel: continue
 };
 
 struct NearFarOp {
@@ -298,6 +301,94 @@ __global__ void k_fill_i32(int32_t *p, int64_t n, int32_t v) {
         p[i] = v;
 }
 
+// Persistent near-far loop for thin graphs (every row <= kSplit slots): one
+// cooperative launch runs all iterations, grid-wide barriers between the
+// expansion, the far split and the advance (a few microseconds per
+// iteration instead of one graph node launch per kernel).
+__global__ void __launch_bounds__(kExpandBlock) k_nf_persistent(
+    int32_t *dist, int32_t *enq, int32_t *last, const int32_t *__restrict__ weff,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, NfLoop *L) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (;;) {
+        {   // near expansion
+            const int cur = L->cur;
+            const int64_t nq = L->nq;
+            if (nq > 0) {
+                NearFarOp op{dist, enq, last, weff, &L->cnt[cur].flag, L->far[L->fcur],
+                             &L->far_n[L->fcur], L->fcap, L->T, L->it};
+                expand_body(op, off, adj, L->q[cur], nq, L->q[cur ^ 1], nullptr, &L->cnt[cur],
+                            expand_vpw(nq, warps));
+            }
+        }
+        grid.sync();
+        if (nf_split_now(L)) {  // same decision in every block
+            const int cur = L->cur, fc = L->fcur;
+            const int64_t nf = (int64_t)min(L->far_n[fc], L->fcap);
+            const int32_t *src = L->far[fc];
+            const int64_t T = L->T + L->delta;
+            const int it = L->it;
+            for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < nf;
+                 b += (int64_t)gridDim.x * blockDim.x) {
+                const int64_t i = b + threadIdx.x;
+                bool to_near = false, to_far = false;
+                int32_t v = 0;
+                if (i < nf) {
+                    v = src[i];
+                    const int d = __ldcg(dist + v);
+                    if ((int64_t)d < T)
+                        to_near = d < __ldcg(last + v) && atomicExch(enq + v, it) != it;
+                    else
+                        to_far = true;
+                }
+                const bool nb[1] = {to_near}, fb[1] = {to_far};
+                const int32_t xv[1] = {v};
+                warp_append_multi<1>(nb, xv, &L->split_n, L->q[cur ^ 1]);
+                warp_append_multi<1>(fb, xv, &L->far_n[fc ^ 1], L->far[fc ^ 1], L->fcap);
+            }
+        }
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // advance (k_nf_advance2)
+            const int cur = L->cur;
+            const ExpandCounters c = L->cnt[cur];
+            const bool split = nf_split_now(L);
+            L->frontier_sum += L->nq;
+            L->relaxed += (int64_t)c.scanned;
+            L->iters++;
+            int64_t next = (int64_t)c.next_size;
+            if (split) {
+                L->T += L->delta;
+                L->far_n[L->fcur] = 0;
+                L->fcur ^= 1;
+                next = (int64_t)L->split_n;
+                L->split_n = 0;
+            }
+            int go = 1;
+            const bool far_left = L->far_n[L->fcur] > 0;
+            if (L->far_n[0] > L->fcap || L->far_n[1] > L->fcap) {
+                L->status = 3;
+                go = 0;
+            } else if (c.flag) {
+                L->status = 1;
+                go = 0;
+            } else if (next == 0 && !far_left) {
+                go = 0;
+            } else if (L->iters >= L->cap) {
+                L->status = 2;
+                go = 0;
+            }
+            L->cnt[cur ^ 1] = ExpandCounters{0, 0, 0, 0};
+            L->cur = cur ^ 1;
+            L->nq = next;
+            L->it = (int)(L->iters + 1);
+            L->go = go;
+        }
+        grid.sync();
+        if (!L->go) break;
+    }
+}
+
 int sssp_near_far(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
                   uint2 *chunks, int64_t cap, int64_t delta, SsspLoop *out, float *kernel_ms) {
     const int64_t n = g->n, m = g->m;
@@ -325,6 +416,33 @@ int sssp_near_far(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa
     init.fcap = (unsigned long long)fcap;
     SP_CUDA(cudaMemcpyAsync(L, &init, sizeof(NfLoop), cudaMemcpyHostToDevice, c.stream));
     const int sms = num_sms(c.device);
+    if (g->max_outdeg <= kSplit) {  // thin graph: one persistent cooperative launch
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nf_persistent, kExpandBlock, 0);
+        const int pgrid = sms * std::max(1, std::min(per_sm, kPersistBlocksPerSm));
+        void *kargs[] = {&dist, &enq, &last, (void *)&g->weff, (void *)&g->off,
+                         (void *)&g->adj, &L};
+        cudaEvent_t ka, kb;
+        SP_CUDA(cudaEventCreate(&ka));
+        SP_CUDA(cudaEventCreate(&kb));
+        cudaEventRecord(ka, c.stream);
+        SP_CUDA(cudaLaunchCooperativeKernel((const void *)k_nf_persistent, pgrid, kExpandBlock,
+                                            kargs, 0, c.stream));
+        cudaEventRecord(kb, c.stream);
+        NfLoop *hL;
+        SP_TRY(c.host_as(&hL));
+        SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(NfLoop), cudaMemcpyDeviceToHost, c.stream));
+        SP_CUDA(cudaStreamSynchronize(c.stream));
+        cudaEventElapsedTime(kernel_ms, ka, kb);
+        cudaEventDestroy(ka);
+        cudaEventDestroy(kb);
+        out->iters = hL->iters;
+        out->relaxed = hL->relaxed;
+        out->frontier_sum = hL->frontier_sum;
+        out->status = hL->status;
+        c.launches += 1;
+        return SP_OK;
+    }
     // near-far frontiers are small (a band of the graph): a smaller grid
     // keeps the fixed per-iteration launch cost down
     const int grid = sms * 2;
