@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import ctypes as C
 import time
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -165,6 +166,88 @@ def _all_gather_flat(full, part, group):
         dist.all_gather_into_tensor(full, part, group=group)
 
 
+# ---------------------------------------------------------------------------
+# superstep trace (the reference's bsp.Superstep / SimResult / TSV, bsp.py:75-103)
+
+
+@dataclass
+class Superstep:
+    """One superstep of a sharded run, per rank (global rank -> count).
+
+    local_updates: owned vertices whose property changed in the step (SSSP
+    dist drops, PR ranks written, BC/TC: vertices processed); msgs_out: the
+    values this rank contributed to the exchange after aggregation -- SSSP:
+    remote vertices whose distance it lowered (one aggregated Min message
+    per vertex, bsp.py:45-72), PR: its contrib slice (all-gather), BC: its
+    bc partial (all-reduce), TC: its count."""
+    index: int
+    label: str
+    local_updates: dict = field(default_factory=dict)
+    msgs_out: dict = field(default_factory=dict)
+    exchanged: int = 0
+    finished: bool = False
+
+
+@dataclass
+class SimResult:
+    result: RunResult
+    supersteps: list
+
+
+def format_trace_tsv(sim) -> str:
+    """bsp.format_trace_tsv's layout (bsp.py:96-103)."""
+    lines = ["superstep\trank\tlocal_updates\tmsgs_out\tfinished"]
+    for step in sim.supersteps:
+        for rank in sorted(step.local_updates):
+            lines.append(f"{step.index}\t{rank}\t{step.local_updates[rank]}"
+                         f"\t{step.msgs_out[rank]}"
+                         f"\t{'true' if step.finished else 'false'}")
+    return "\n".join(lines) + "\n"
+
+
+class _Tracer:
+    def __init__(self, enabled, be, group):
+        self.on = enabled
+        self.be = be
+        self.group = group
+        self.steps: list[Superstep] = []
+
+    def record(self, label, local_updates, msgs_out, finished=False):
+        if not self.on:
+            return
+        dist = _dist()
+        t = self.be.torch.tensor([int(local_updates), int(msgs_out)],
+                                 dtype=self.be.torch.int64, device=self.be.device)
+        parts = [self.be.torch.zeros_like(t) for _ in range(dist.get_world_size(self.group))]
+        dist.all_gather(parts, t, group=self.group)
+        ranks = [dist.get_global_rank(self.group, r) if self.group is not None else r
+                 for r in range(len(parts))]
+        lu = {rk: int(p[0].item()) for rk, p in zip(ranks, parts)}
+        mo = {rk: int(p[1].item()) for rk, p in zip(ranks, parts)}
+        self.steps.append(Superstep(len(self.steps), label, lu, mo, sum(mo.values()),
+                                    bool(finished)))
+
+    def finish_last(self):
+        if self.on and self.steps:
+            self.steps[-1].finished = True
+
+
+def simulate(tp, g, nranks: int, args: dict, function: str | None = None,
+             max_iters: int | None = None, *, backend=None, group=None,
+             deterministic: bool = False) -> SimResult:
+    """bsp.simulate's surface (bsp.py:452-465) over real ranks: nranks must
+    equal the process group's size (one rank per GPU); returns the run's
+    result and its superstep trace (convergence evaluated after the
+    exchange, unlike bsp.py:393-417 -- SURVEY F4)."""
+    dist = _dist()
+    if nranks != dist.get_world_size(group):
+        raise ValueError(f"simulate: nranks={nranks} but the process group has "
+                         f"{dist.get_world_size(group)} ranks (one rank per GPU)")
+    r = run_sharded(tp, g, args, function, max_iters, backend=backend, group=group,
+                    deterministic=deterministic, trace=True)
+    return SimResult(result=r, supersteps=r.supersteps)
+
+
 def tc_ranges(offsets: np.ndarray, world: int) -> list[tuple[int, int]]:
     """Contiguous vertex ranges with about equal sum of squared degrees (the
     per-vertex intersection work grows with deg^2); covers [0, n) exactly."""
@@ -183,9 +266,11 @@ def tc_ranges(offsets: np.ndarray, world: int) -> list[tuple[int, int]]:
 
 def run_sharded(tp, g, args: dict, function: str | None = None,
                 max_iters: int | None = None, *, backend=None, group=None,
-                deterministic: bool = False) -> RunResult:
+                deterministic: bool = False, trace: bool = False) -> RunResult:
     """Run a corpus program over all ranks of ``group`` (default: the world).
-    Every rank must call it with the same graph and arguments."""
+    Every rank must call it with the same graph and arguments.  trace=True
+    records the superstep trace in ``result.supersteps`` (one extra small
+    all-gather per superstep)."""
     dist = _dist()
     world = dist.get_world_size(group)
     me = dist.get_rank(group)
@@ -199,9 +284,12 @@ def run_sharded(tp, g, args: dict, function: str | None = None,
     cap = max_iters if max_iters is not None else default_iteration_cap(dg.n)
     t0 = time.perf_counter()
     fn = {"sssp": _sssp, "sssp_pull": _sssp, "pr": _pr, "bc": _bc, "tc": _tc}[prog.key]
-    env, fpi, stats = fn(backend, dg, bound, cap, world, me, group, deterministic, E, prog)
-    return RunResult(env=env, fixedpoint_iterations=fpi,
-                     wall_seconds=time.perf_counter() - t0, stats=stats)
+    tr = _Tracer(trace, backend, group)
+    env, fpi, stats = fn(backend, dg, bound, cap, world, me, group, deterministic, E, prog, tr)
+    r = RunResult(env=env, fixedpoint_iterations=fpi,
+                  wall_seconds=time.perf_counter() - t0, stats=stats)
+    r.supersteps = tr.steps if trace else None
+    return r
 
 
 def _sum_stats(be, keys, group):
@@ -214,11 +302,12 @@ def _sum_stats(be, keys, group):
     return {k: int(v) for k, v in zip(keys, t.tolist())}
 
 
-def _bc(be, g, bound, cap, world, me, group, det, E, prog):
+def _bc(be, g, bound, cap, world, me, group, det, E, prog, tr):
     dist = _dist()
     srcs = bound["sourceSet"]
     mine = srcs[me::world]
     bc, sg, dl = be.bc(g, mine, det)
+    tr.record("bc sources", len(mine), g.n if mine else 0, finished=True)
     dist.all_reduce(bc, op=dist.ReduceOp.SUM, group=group)
     env = PropertyEnv()
     env.node_props = {"bc": be.to_host(bc)}
@@ -233,10 +322,11 @@ def _bc(be, g, bound, cap, world, me, group, det, E, prog):
     return env, {}, stats
 
 
-def _tc(be, g, bound, cap, world, me, group, det, E, prog):
+def _tc(be, g, bound, cap, world, me, group, det, E, prog, tr):
     dist = _dist()
     v0, v1 = tc_ranges(be.offsets(g), world)[me]
     part = be.tc(g, v0, v1)
+    tr.record("tc range", v1 - v0, 1, finished=True)
     t = be.torch.tensor([part], dtype=be.torch.int64, device=be.device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     env = PropertyEnv(scalars={"triangle_count": int(t.item())})
@@ -245,7 +335,7 @@ def _tc(be, g, bound, cap, world, me, group, det, E, prog):
     return env, {}, stats
 
 
-def _pr(be, g, bound, cap, world, me, group, det, E, prog):
+def _pr(be, g, bound, cap, world, me, group, det, E, prog, tr):
     dist = _dist()
     torch = be.torch
     parts = block_partition(g, world)
@@ -274,7 +364,9 @@ def _pr(be, g, bound, cap, world, me, group, det, E, prog):
         gather()
         it += 1
         iters += 1
-        if diff < bound["epsilon"] or it >= bound["maxIter"]:  # pr.sp:10
+        done = diff < bound["epsilon"] or it >= bound["maxIter"]  # pr.sp:10
+        tr.record("fixedPoint converged", v1 - v0, v1 - v0, finished=done)
+        if done:
             break
         if iters >= cap:
             raise E.NonConvergenceError(prog.flag, cap)
@@ -290,7 +382,7 @@ def _pr(be, g, bound, cap, world, me, group, det, E, prog):
     return env, {"converged": iters}, {"block": (v0, v1)}
 
 
-def _sssp(be, g, bound, cap, world, me, group, det, E, prog):
+def _sssp(be, g, bound, cap, world, me, group, det, E, prog, tr):
     dist = _dist()
     torch = be.torch
     parts = block_partition(g, world)
@@ -299,18 +391,24 @@ def _sssp(be, g, bound, cap, world, me, group, det, E, prog):
     dvec, last = be.sssp_init(g, bound["src"])
     steps = relaxed = 0
     while True:
+        before = dvec.clone() if tr.on else None
         try:
             f, r = be.sssp_step(g, v0, v1, dvec, last)
             bad = 0
         except OverflowError:
             f, r, bad = 0, 0, 1
         relaxed += r
+        if tr.on:  # owned drops vs remote candidates (aggregated: one per vertex)
+            dropped = (dvec < before)[: g.n]
+            own = int(dropped[v0:v1].sum().item())
+            tr.record("fixedPoint finished", own, int(dropped.sum().item()) - own)
         dist.all_reduce(dvec, op=dist.ReduceOp.MIN, group=group)
         fz = torch.tensor([f, bad], dtype=torch.int64, device=be.device)
         dist.all_reduce(fz, op=dist.ReduceOp.SUM, group=group)
         if int(fz[1].item()):
             raise E.ExecError("SSSP distance left the int32 range (negative weights)")
         if int(fz[0].item()) == 0:  # nobody had a frontier: the exchange changed nothing
+            tr.finish_last()
             break
         steps += 1
         if steps >= cap:

@@ -105,3 +105,50 @@ def test_tc_ranges_partition():
         assert rs[0][0] == 0 and rs[-1][1] == len(off) - 1
         for (a, b), (c, d) in zip(rs, rs[1:]):
             assert b == c and a <= b
+
+
+def _trace_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from oracle_backend import OracleBackend
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # path10 with unit weights: the reference's bsp.simulate loses
+        # dist[6..9] at nranks=2; run_sharded must not
+        u = list(range(9))
+        v = list(range(1, 10))
+        g = cpu_ref.build_csr(u, v, [1] * 9, True, 10)
+        sim = parallel.simulate(corpus.SSSP, g, world, {"src": 0}, backend=OracleBackend())
+        q.put((rank, sim.result.env.node_props["dist"], parallel.format_trace_tsv(sim),
+               [(s.index, s.finished, dict(s.local_updates), dict(s.msgs_out))
+                for s in sim.supersteps]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_simulate_trace_and_f4_fix():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_trace_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, rest) for r, *rest in (q.get(timeout=120) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        d, tsv, steps = res[r]
+        assert d.tolist() == list(range(10))  # every vertex reached (F4 fixed)
+        lines = tsv.strip().split("\n")
+        assert lines[0] == "superstep\trank\tlocal_updates\tmsgs_out\tfinished"
+        assert len(lines) == 1 + 2 * len(steps)
+        assert [s[1] for s in steps] == [False] * (len(steps) - 1) + [True]
+        # the path crosses from rank 0's block into rank 1's exactly once:
+        # one aggregated Min message, sent by rank 0
+        assert sum(s[3][0] for s in steps) == 1 and sum(s[3][1] for s in steps) == 0
+        # every vertex but the source is lowered once, by its owner or via
+        # that message
+        assert sum(s[2][0] + s[2][1] for s in steps) + 1 == 9
+    assert res[0][1] == res[1][1]
