@@ -135,6 +135,12 @@ struct sp_graph {
     int64_t m_up_pad = 0;   // padded slots
     int32_t *ubig = nullptr;  // vertices whose upper row exceeds the warp path
     int64_t nbig = 0, max_ulen = 0;
+    // PageRank hot sources (built by the first fast PR call): the pr_H
+    // vertices of largest out-degree, and radj re-encoded so that a slot
+    // whose source is hot carries (1 << 30) | hot index
+    int32_t *pr_hot_ids = nullptr;
+    int32_t *pr_radj_hot = nullptr;
+    int pr_H = -1;  // -1: not built, 0: disabled
 };
 
 // ---- device helpers --------------------------------------------------------

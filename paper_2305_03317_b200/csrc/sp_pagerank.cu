@@ -44,7 +44,11 @@
 //   through shared memory and every lane folds its own row sequentially in
 //   CSR order: bit-identical to the interpreter, slower on hub rows.
 // No FMA contraction anywhere: __dadd_rn/__dmul_rn are used explicitly.
+#include <cub/cub.cuh>
+#include <stdlib.h>
+
 #include <algorithm>
+#include <mutex>
 
 #include "sp_common.cuh"
 
@@ -57,6 +61,9 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kChunk = 128;     // exact path: slab slots staged per warp per step
 constexpr int64_t kUnit = 2048;  // fast path: radj slots per work unit (one warp)
 constexpr int kCh = 256;        // fast path: slots per warp chunk (8 per lane)
+constexpr int kHotBlock = 1024;   // persistent hot-source variant: threads per block
+constexpr int kHotMax = 24 * 1024;  // hot contrib values kept in shared memory (192 KB)
+constexpr int kHotBit = 1 << 30;    // encoded radj: source is hot, low bits = hot index
 
 __global__ void k_init(double *rank, double *contrib, const int32_t *__restrict__ outdeg,
                        int64_t v0, int64_t v1, double r0) {
@@ -154,11 +161,9 @@ __device__ __forceinline__ void load_slab(const int32_t *__restrict__ radj, int6
 }
 
 // Row sums over edge-balanced units (see the file header).
-__global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
-    pr_bind(a);
-    __shared__ uint32_t bitmap[kWarps][kCh / 32];
+template <bool kHot>
+__device__ __forceinline__ void pr_units_body(const PrArgs &a, uint32_t *bm, const double *hot) {
     const unsigned lane = lane_id();
-    uint32_t *bm = bitmap[threadIdx.x >> 5];
     if (lane < kCh / 32) bm[lane] = 0u;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -197,7 +202,15 @@ __global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
             }
             double val[8];
 #pragma unroll
-            for (int i = 0; i < 8; i++) val[i] = idx[i] >= 0 ? __ldg(a.cin + idx[i]) : 0.0;
+            for (int i = 0; i < 8; i++) {
+                if constexpr (kHot) {  // hot sources: shared-memory copy
+                    const int x = idx[i];
+                    val[i] = x < 0 ? 0.0 : (x & kHotBit) ? hot[x & (kHotBit - 1)]
+                                                         : __ldg(a.cin + x);
+                } else {
+                    val[i] = idx[i] >= 0 ? __ldg(a.cin + idx[i]) : 0.0;
+                }
+            }
             __syncwarp();
             const unsigned ends = (bm[lane >> 2] >> ((lane & 3) * 8)) & 0xFFu;
             __syncwarp();
@@ -256,6 +269,36 @@ __global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
         }
         if (lane == 0) a.tp[u] = carry;
     }
+}
+
+__global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
+    pr_bind(a);
+    __shared__ uint32_t bitmap[kWarps][kCh / 32];
+    pr_units_body<false>(a, bitmap[threadIdx.x >> 5], nullptr);
+}
+
+// hotc[h] = contrib of the h-th hot source (one gather per iteration)
+__global__ void k_pr_hot_gather(PrArgs a, const int32_t *__restrict__ hot_ids, int H,
+                                double *__restrict__ hotc) {
+    pr_bind(a);
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x)
+        hotc[h] = __ldg(a.cin + hot_ids[h]);
+}
+
+// Persistent variant (one 1024-thread block per SM): the block copies the H
+// hot contrib values into shared memory once per iteration, then its warps
+// walk their units; a gather whose (encoded) source carries kHotBit reads
+// the shared copy -- the same value, so the sums are bit-identical.
+__global__ void __launch_bounds__(kHotBlock, 1) k_pr_units_hot(PrArgs a, const double *hotc,
+                                                             int H) {
+    pr_bind(a);
+    extern __shared__ double hot_smem[];
+    uint32_t *bitmaps = reinterpret_cast<uint32_t *>(hot_smem + H);
+    const int4 *src = reinterpret_cast<const int4 *>(hotc);
+    int4 *dst = reinterpret_cast<int4 *>(hot_smem);
+    for (int i = threadIdx.x; i < (H + 1) / 2; i += blockDim.x) dst[i] = __ldcg(src + i);
+    __syncthreads();
+    pr_units_body<true>(a, bitmaps + (threadIdx.x >> 5) * (kCh / 32), hot_smem);
 }
 
 // pr.sp:17-23 for every non-empty row of the block (coalesced over k).
@@ -357,10 +400,111 @@ __global__ void k_pr_bounds(const int64_t *__restrict__ roff, const int32_t *__r
     }
 }
 
+// ---- hot-source set (per graph, built once) ---------------------------
+
+std::mutex g_hot_mu;
+constexpr int64_t kHotMinSlots = 1 << 20;  // smaller graphs keep the plain kernel
+constexpr double kHotMinCover = 0.4;       // hot sources must cover >= 40% of the slots
+
+__global__ void k_hot_keys(const int32_t *__restrict__ outdeg, int64_t n, uint32_t *key,
+                           int32_t *id, int32_t *hot_idx) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        key[v] = (uint32_t)outdeg[v];
+        id[v] = (int32_t)v;
+        hot_idx[v] = -1;
+    }
+}
+
+__global__ void k_hot_scatter(const int32_t *__restrict__ ids, int H, int32_t *hot_idx) {
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x)
+        hot_idx[ids[h]] = h;
+}
+
+__global__ void k_hot_encode(const int32_t *__restrict__ radj, int64_t m,
+                             const int32_t *__restrict__ hot_idx, int32_t *out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = radj[k];
+        const int32_t h = hot_idx[u];
+        out[k] = h >= 0 ? (kHotBit | h) : u;
+    }
+}
+
+int ensure_pr_hot(sp_graph *g, Call &c) {
+    std::lock_guard<std::mutex> lk(g_hot_mu);
+    if (g->pr_H >= 0) return SP_OK;
+    const int64_t n = g->n, m = g->m;
+    if (m < kHotMinSlots || n >= kHotBit) {
+        g->pr_H = 0;
+        return SP_OK;
+    }
+    const int H = (int)std::min<int64_t>(kHotMax, n);
+    uint32_t *key, *key_s;
+    int32_t *id, *id_s, *hot_idx;
+    SP_TRY(c.alloc(&key, n));
+    SP_TRY(c.alloc(&key_s, n));
+    SP_TRY(c.alloc(&id, n));
+    SP_TRY(c.alloc(&id_s, n));
+    SP_TRY(c.alloc(&hot_idx, n));
+    k_hot_keys<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(g->outdeg, n, key, id,
+                                                                     hot_idx);
+    size_t tmp = 0;
+    SP_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, key, key_s, id, id_s, n, 0,
+                                                      32, c.stream));
+    void *dt = nullptr;
+    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(dt, tmp, key, key_s, id, id_s, n,
+                                                              0, 32, c.stream);
+    scratch_free(dt, c.stream);
+    SP_CUDA(e);
+    // coverage: share of the slots whose source is hot (sum of the top H
+    // out-degrees); below kHotMinCover the per-iteration refill of the shared
+    // copies costs more than the gathers it saves
+    unsigned long long *cov;
+    SP_TRY(c.alloc(&cov, 1));
+    tmp = 0;
+    SP_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, key_s, cov, H, c.stream));
+    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
+    e = cub::DeviceReduce::Sum(dt, tmp, key_s, cov, H, c.stream);
+    scratch_free(dt, c.stream);
+    SP_CUDA(e);
+    unsigned long long *hcov;
+    SP_TRY(c.host_as(&hcov));
+    SP_CUDA(cudaMemcpyAsync(hcov, cov, 8, cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    if ((double)hcov[0] < kHotMinCover * (double)m) {
+        g->pr_H = 0;
+        return SP_OK;
+    }
+    int32_t *ids = nullptr, *enc = nullptr;
+    SP_TRY(resident_alloc((void **)&ids, (size_t)H * sizeof(int32_t)));
+    if (resident_alloc((void **)&enc, (size_t)m * sizeof(int32_t)) != SP_OK) {
+        resident_free(ids);
+        return SP_ERR_OOM;
+    }
+    SP_CUDA(cudaMemcpyAsync(ids, id_s, (size_t)H * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                            c.stream));
+    k_hot_scatter<<<grid_for(H, 256, c.device), 256, 0, c.stream>>>(ids, H, hot_idx);
+    k_hot_encode<<<grid_for(m, 256, c.device, 16), 256, 0, c.stream>>>(g->radj, m, hot_idx, enc);
+    c.launches += 4;
+    SP_CUDA(cudaGetLastError());
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    g->pr_hot_ids = ids;
+    g->pr_radj_hot = enc;
+    g->pr_H = H;
+    return SP_OK;
+}
+
 // Per-call state of the fast path for a vertex block [v0, v1).
 struct FastPlan {
     PrArgs a{};
     int grid_units = 1, grid_epi = 1, grid_zero = 1;
+    // hot-source variant
+    int H = 0, grid_hot = 0;
+    size_t hot_smem = 0;
+    const int32_t *hot_ids = nullptr;
+    double *hotc = nullptr;
 };
 
 int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, FastPlan &p) {
@@ -404,10 +548,36 @@ int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, Fast
     }
     // one unit per warp, no cap: the block scheduler balances the tail
     p.grid_units = (int)std::max<int64_t>(1, (a.nunits + kWarps - 1) / kWarps);
+    SP_TRY(ensure_pr_hot(g, c));
+    if (g->pr_H > 0) {
+        p.H = g->pr_H;
+        p.hot_ids = g->pr_hot_ids;
+        a.radj = g->pr_radj_hot;  // encoded slots
+        double *hotc;
+        SP_TRY(c.alloc(&hotc, p.H + 1));
+        p.hotc = hotc;
+        p.hot_smem = (size_t)p.H * sizeof(double) + (kHotBlock / 32) * (kCh / 32) * 4;
+        SP_CUDA(cudaFuncSetAttribute(k_pr_units_hot, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)p.hot_smem));
+        p.grid_hot = num_sms(c.device);
+    }
     p.grid_epi = (int)std::max<int64_t>(1, (a.K1 - a.K0 + 256 * kEpi - 1) / (256 * kEpi));
     p.grid_zero = (int)std::max<int64_t>(1, (v1 - v0 + 255) / 256);
     SP_CUDA(cudaGetLastError());
     return SP_OK;
+}
+
+// The row-sum kernel of one iteration (hot-source variant when built).
+void launch_units(Call &c, const FastPlan &p, const PrArgs &a) {
+    if (p.H > 0) {
+        k_pr_hot_gather<<<grid_for(p.H, 256, c.device), 256, 0, c.stream>>>(a, p.hot_ids, p.H,
+                                                                            p.hotc);
+        k_pr_units_hot<<<p.grid_hot, kHotBlock, p.hot_smem, c.stream>>>(a, p.hotc, p.H);
+        c.launches += 2;
+    } else {
+        k_pr_units<<<p.grid_units, kBlock, 0, c.stream>>>(a);
+        c.launches++;
+    }
 }
 
 // One fast iteration; `zero` says whether zero-in-degree rows are written.
@@ -421,9 +591,9 @@ int launch_fast(Call &c, FastPlan &p, sp_graph *g, int64_t v1, const double *cin
     a.diff_slot = diff_slot;
     if (ka) cudaEventRecord(ka, c.stream);
     if (a.nunits) {
-        k_pr_units<<<p.grid_units, kBlock, 0, c.stream>>>(a);
+        launch_units(c, p, a);
         k_pr_epi<<<p.grid_epi, 256, 0, c.stream>>>(a);
-        c.launches += 2;
+        c.launches += 1;
     }
     if (kb) cudaEventRecord(kb, c.stream);
     if (zero) {
@@ -496,7 +666,7 @@ int pr_device_loop(Call &c, FastPlan &p, double *rank, double *c0, double *c1, d
     SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
                                           cudaStreamCaptureModeThreadLocal));
     if (a.nunits) {
-        k_pr_units<<<p.grid_units, kBlock, 0, c.stream>>>(a);
+        launch_units(c, p, a);
         k_pr_epi<<<p.grid_epi, 256, 0, c.stream>>>(a);
     }
     k_pr_advance<<<1, 1, 0, c.stream>>>(L, h);
@@ -660,7 +830,8 @@ extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t 
             rc = SP_ERR_NONCONV;
             break;
         }
-        if (!cb && !exact && n) {
+        const char *hostloop = getenv("SP_HOSTLOOP");  // ncu cannot profile conditional graphs
+        if (!cb && !exact && n && !(hostloop && hostloop[0] == '1')) {
             // the remaining iterations on the device: contrib to read is ca
             PrLoop *hL;
             SP_TRY(c.host_as(&hL));

@@ -608,9 +608,9 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
     SP_CUDA(cudaEventCreate(&ka));
     SP_CUDA(cudaEventCreate(&kb));
     float kernel_ms = 0.f;
-    // SP_SSSP_HOSTLOOP=1 keeps the host-driven loop (ncu cannot profile the
+    // SP_HOSTLOOP=1 keeps the host-driven loop (ncu cannot profile the
     // kernel nodes of a graph with conditional nodes)
-    const char *hostloop = getenv("SP_SSSP_HOSTLOOP");
+    const char *hostloop = getenv("SP_HOSTLOOP");
     if (!cb && !(hostloop && hostloop[0] == '1')) {
         SsspLoop hL{};
         int lrc;
