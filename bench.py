@@ -330,14 +330,15 @@ def e2e_pr(sp, corpus, parallel, g, a, world, dev, be):
     """Public-API PR with host buffers every step: pinned host CSR ->
     sp.from_csr (H2D + on-device reverse CSR) -> run -> ranks on the host."""
     import torch
+    # pr.sp reads no edge weights: the unweighted CSR (offsets + adjacency)
+    # is the step's input; from_csr(weights=None) gives every slot weight 1
     off = torch.from_numpy(np.array(g.offsets)).pin_memory().numpy()
     adj = torch.from_numpy(np.array(g.adj)).pin_memory().numpy()
-    w = torch.from_numpy(np.array(g.weights)).pin_memory().numpy()
-    h2d = off.nbytes + adj.nbytes + w.nbytes
+    h2d = off.nbytes + adj.nbytes
     d2h = 8 * g.n
 
     def step():
-        gg = sp.from_csr(off, adj, w, directed=True, device=dev.index)
+        gg = sp.from_csr(off, adj, None, directed=True, device=dev.index)
         if world == 1:
             r = sp.run(corpus.PR, gg, PR_ARGS)
         else:
@@ -352,7 +353,8 @@ def e2e_pr(sp, corpus, parallel, g, a, world, dev, be):
     return {"value": r.env.scalars["iter"] * g.m / dt / 1e9, "unit": "GTEPS",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
             "steps": k,
-            "includes": "H2D CSR (pinned) + device reverse-CSR build + PR + D2H ranks"}
+            "includes": "H2D unweighted CSR (pinned) + device reverse-CSR build + PR + D2H "
+                        "ranks (into pinned host memory)"}
 
 
 def cpu_baseline(g):

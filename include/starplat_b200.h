@@ -94,7 +94,9 @@ int sp_graph_from_edges(const int32_t *u, const int32_t *v, const int32_t *w,
                         int device, sp_graph **out);
 
 /* CsrGraph(...) (graph.py:18-36) from an existing forward CSR whose rows are
- * already in reference order; the reverse CSR is rebuilt on the device. */
+ * already in reference order; the reverse CSR is rebuilt on the device.
+ * weights == NULL: unweighted input, every slot gets weight 1 (the
+ * reference's default_weight) on the device, nothing is copied for it. */
 int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj,
                       const int32_t *weights, int64_t n, int64_t m,
                       int directed, int mem, int device, sp_graph **out);

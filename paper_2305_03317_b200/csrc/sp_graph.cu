@@ -189,16 +189,24 @@ __global__ void k_weff_csr(const int64_t *__restrict__ off, const int32_t *__res
     }
 }
 
-// Destination keys and source values of every forward slot, in slot order.
-__global__ void k_rev_pairs(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
-                            int64_t n, uint32_t *dkey, uint32_t *sval) {
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t x = warp; x < n; x += nw)
-        for (int64_t e = off[x] + lane_id(); e < off[x + 1]; e += 32) {
-            dkey[e] = (uint32_t)adj[e];
-            sval[e] = (uint32_t)x;
-        }
+// Row id of every forward slot: the row starts are scattered (row x with
+// slots marks off[x] with x), then an inclusive max-scan fills the rows.
+__global__ void k_row_starts(const int64_t *__restrict__ off, int64_t n, uint32_t *mark) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x)
+        if (off[x + 1] > off[x]) mark[off[x]] = (uint32_t)x;
+}
+
+struct MaxU32 {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const {
+        return a > b ? a : b;
+    }
+};
+
+__global__ void k_fill_w(int32_t *w, int64_t m, int32_t v) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x)
+        w[e] = v;
 }
 
 // off[x] = first e with key[e] >= x (sorted 32-bit keys).
@@ -391,13 +399,20 @@ int build_reverse_t(sp_graph *g, Call &c, bool want_adj, bool want_eid) {
 int build_reverse_adj(sp_graph *g, Call &c) {
     const int64_t n = g->n, m = g->m;
     const int b = bits_for(n);
-    uint32_t *dk, *dks, *sv;
-    SP_TRY(c.alloc(&dk, m));
+    uint32_t *dks, *sv;
     SP_TRY(c.alloc(&dks, m));
     SP_TRY(c.alloc(&sv, m));
     SP_TRY(dalloc(&g->roff, n + 1));
     SP_TRY(dalloc(&g->radj, m));
-    k_rev_pairs<<<gridN(n * 32, c.device), 256, 0, c.stream>>>(g->off, g->adj, n, dk, sv);
+    // source of every slot (slots are in (src, eid) order): scatter + max-scan
+    SP_CUDA(cudaMemsetAsync(sv, 0, m * sizeof(uint32_t), c.stream));
+    k_row_starts<<<gridN(n, c.device), 256, 0, c.stream>>>(g->off, n, sv);
+    if (m)
+        SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+            return cub::DeviceScan::InclusiveScan(t, sz, sv, sv, MaxU32(), m, c.stream);
+        }));
+    // the destinations are the forward adj itself (the sort keys)
+    const uint32_t *dk = reinterpret_cast<const uint32_t *>(g->adj);
     if (m)
         SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
             return cub::DeviceRadixSort::SortPairs(t, sz, dk, dks, sv,
@@ -652,7 +667,11 @@ int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj, const int32_t 
         if ((rc = dalloc(&g->w, m))) break;
         if ((rc = to_device(g->off, offsets, (n + 1) * 8, mem, c.stream))) break;
         if ((rc = to_device(g->adj, adj, m * 4, mem, c.stream))) break;
-        if ((rc = to_device(g->w, weights, m * 4, mem, c.stream))) break;
+        if (weights) {
+            if ((rc = to_device(g->w, weights, m * 4, mem, c.stream))) break;
+        } else if (m) {  // unweighted CSR: every slot has the default weight 1
+            k_fill_w<<<gridN(m, c.device), 256, 0, c.stream>>>(g->w, m, 1);
+        }
         // w_eff is built on first use (ensure_weff): PR/BC/TC never read it
         if ((rc = finish_graph(g, c))) break;
         rc = c.finish(nullptr);

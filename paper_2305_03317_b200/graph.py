@@ -320,19 +320,20 @@ def _ints(vals: list[int], what: str) -> np.ndarray:
     return np.array(vals, dtype=np.int64)
 
 
-def from_csr(offsets, adj, weights, directed: bool = True,
+def from_csr(offsets, adj, weights=None, directed: bool = True,
              device: int = 0) -> CsrGraph:
     """Wrap an existing forward CSR (rows already in reference order, e.g. a
     trident CsrGraph's lists); the reverse CSR and w_eff are built on the
-    device."""
+    device.  weights=None: an unweighted graph (every slot weight 1, filled
+    on the device; nothing is uploaded for it)."""
     off = np.ascontiguousarray(np.asarray(offsets), dtype=np.int64)
     adj = _as_i32(adj, "vertex id")
-    w = _as_i32(weights, "edge weight")
+    w = None if weights is None else _as_i32(weights, "edge weight")
     n = len(off) - 1
     _lib.require_device(device)
-    h = _new_handle(_lib.lib().sp_graph_from_csr, _ptr(off), _ptr(adj), _ptr(w),
-                    n, len(adj), int(bool(directed)), _lib.SP_MEM_HOST, device,
-                    what="sp_graph_from_csr")
+    h = _new_handle(_lib.lib().sp_graph_from_csr, _ptr(off), _ptr(adj),
+                    None if w is None else _ptr(w), n, len(adj), int(bool(directed)),
+                    _lib.SP_MEM_HOST, device, what="sp_graph_from_csr")
     return CsrGraph(h, device)
 
 

@@ -136,10 +136,42 @@ def _i64(x: int) -> int:
     return max(-(2 ** 63), min(2 ** 63 - 1, int(x)))
 
 
+_PINNED_MIN = 1 << 16  # results at least this long land in pinned host memory
+
+
+def _torch():
+    try:
+        import torch  # plumbing only: pinned host / device buffers
+        return torch
+    except ImportError:  # pragma: no cover
+        return None
+
+
+def _host_array(n: int, dtype) -> np.ndarray:
+    """NumPy result array; large ones are backed by torch's cached pinned
+    host memory so the device-to-host copy runs at full PCIe speed (the
+    array keeps its pinned storage alive)."""
+    torch = _torch()
+    if n >= _PINNED_MIN and torch is not None and torch.cuda.is_available():
+        td = {np.float64: torch.float64, np.int32: torch.int32}[dtype]
+        return torch.empty(n, dtype=td, pin_memory=True).numpy()
+    return np.empty(n, dtype=dtype)
+
+
+def _host_copy(a: np.ndarray) -> np.ndarray:
+    """A copy of a result array (multi-threaded for large ones)."""
+    torch = _torch()
+    if len(a) >= _PINNED_MIN and torch is not None:
+        out = _host_array(len(a), a.dtype.type)
+        torch.from_numpy(out).copy_(torch.from_numpy(a))
+        return out
+    return a.copy()
+
+
 def _out(n: int, dtype, dev: int | None):
     """Result buffer: a NumPy array (host) or a torch CUDA tensor (device)."""
     if dev is None:
-        return np.empty(n, dtype=dtype), _lib.SP_MEM_HOST
+        return _host_array(n, dtype), _lib.SP_MEM_HOST
     import torch  # plumbing only: device memory for results that stay in HBM
     t = torch.empty(max(1, n), dtype={np.float64: torch.float64,
                                       np.int32: torch.int32}[dtype],
@@ -196,7 +228,8 @@ def run(tp, g, args: dict, function: str | None = None,
                            C.byref(st))
         _raise_for(rc, E, prog.flag, cap, hook.exc)
         # rank_nxt == rank at exit (pr.sp:25-27 copies it back every iteration)
-        env.node_props = {"rank": rank, "rank_nxt": rank if odev is not None else rank.copy()}
+        env.node_props = {"rank": rank,
+                          "rank_nxt": rank if odev is not None else _host_copy(rank)}
         env.scalars = {"iter": int(it.value), "diff": float(diff.value),
                        "converged": True}
         fpi = {"converged": int(its.value)}
