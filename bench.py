@@ -217,8 +217,9 @@ def timed(fn, steps, warmup, world, device):
     recycled.  -> (total_ms, [per-step stats], last result)"""
     import torch
     import torch.distributed as dist
-    for _ in range(warmup):
-        fn()
+    r = None
+    for _ in range(warmup):  # same liveness pattern as the timed loop
+        r = fn()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -347,8 +348,8 @@ def e2e_pr(sp, corpus, parallel, g, a, world, dev, be):
         gg.close()
         return r
 
-    k = max(1, min(a.steps, 3))
-    ms, _, r = timed(step, k, max(1, min(a.warmup, 2)), world, dev)
+    k = max(1, min(a.steps, 5))
+    ms, _, r = timed(step, k, max(2, min(a.warmup, 3)), world, dev)
     dt = ms / k / 1e3
     return {"value": r.env.scalars["iter"] * g.m / dt / 1e9, "unit": "GTEPS",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
