@@ -320,10 +320,12 @@ __global__ void __launch_bounds__(256) k_pr_epi(PrArgs a) {
         const int64_t k = base_k + j * 256;
         v[j] = k < nk ? __ldcs(a.nzrow + a.K0 + k) : -1;
         sum[j] = 0.0;
+        const int64_t kk = a.K0 + k;
+        // row k starts where row k-1 ends: the previous lane's end (lane 0 loads it)
+        const int64_t end = k < nk ? __ldg(a.nzend + kk) : 0;
+        int64_t start = __shfl_up_sync(0xffffffffu, end, 1);
+        if ((threadIdx.x & 31) == 0) start = (k < nk && kk > 0) ? __ldg(a.nzend + kk - 1) : 0;
         if (k < nk) {
-            const int64_t kk = a.K0 + k;
-            const int64_t end = __ldg(a.nzend + kk);
-            const int64_t start = kk > 0 ? __ldg(a.nzend + kk - 1) : 0;
             const int64_t us = start / kUnit, ue = (end - 1) / kUnit;
             if (us == ue) {
                 sum[j] = __ldcs(a.sums + k);
