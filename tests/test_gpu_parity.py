@@ -428,3 +428,46 @@ def test_native_loader_large_file_matches_arrays(tmp_path):
     np.testing.assert_array_equal(g.offsets, h.offsets)
     np.testing.assert_array_equal(g.adj, h.adj)
     np.testing.assert_array_equal(g.weights, h.weights)
+
+
+def test_concurrent_calls_on_one_graph():
+    """A graph handle is immutable and safe for concurrent readers
+    (SPEC.md:239): four host threads run all four programs on the same
+    graph at once and get the single-threaded results."""
+    import threading
+    u, v, w, n = gen.rmat(12, 16, seed=21, undirected=True)
+    g = sp.from_arrays(u, v, w, directed=False, n=n)
+    want = {
+        "sssp": sp.run(corpus.SSSP, g, {"src": 1}).env.node_props["dist"],
+        "pr": sp.run(corpus.PR, g, {"damping": 0.85, "epsilon": 1e-6,
+                                    "maxIter": 100}).env.node_props["rank"],
+        "bc": sp.run(corpus.BC, g, {"sourceSet": [1, 2, 3]}).env.node_props["bc"],
+        "tc": sp.run(corpus.TC, g, {}).env.scalars["triangle_count"],
+    }
+    got, errs = {}, []
+
+    def work(key):
+        try:
+            for _ in range(3):
+                if key == "sssp":
+                    got[key] = sp.run(corpus.SSSP, g, {"src": 1}).env.node_props["dist"]
+                elif key == "pr":
+                    got[key] = sp.run(corpus.PR, g, {"damping": 0.85, "epsilon": 1e-6,
+                                                     "maxIter": 100}).env.node_props["rank"]
+                elif key == "bc":
+                    got[key] = sp.run(corpus.BC, g, {"sourceSet": [1, 2, 3]}).env.node_props["bc"]
+                else:
+                    got[key] = sp.run(corpus.TC, g, {}).env.scalars["triangle_count"]
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in want]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    assert np.array_equal(got["sssp"], want["sssp"])
+    assert got["pr"].tobytes() == want["pr"].tobytes()  # deterministic run to run
+    assert got["bc"].tobytes() == want["bc"].tobytes()
+    assert got["tc"] == want["tc"]
