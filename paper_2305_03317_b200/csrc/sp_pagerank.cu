@@ -134,6 +134,7 @@ __device__ __forceinline__ double pr_apply(const PrArgs &a, int64_t v, double su
 // One atomic per block (blockDim.x == 256): same-address atomics serialise.
 __device__ __forceinline__ void block_diff(const PrArgs &a, double dmax) {
     __shared__ double red[8];
+    __syncwarp();  // reconverge after divergent per-row work: the block barrier is .aligned
     dmax = warp_max(dmax);
     if (lane_id() == 0) red[threadIdx.x >> 5] = dmax;
     __syncthreads();

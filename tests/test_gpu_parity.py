@@ -471,3 +471,20 @@ def test_concurrent_calls_on_one_graph():
     assert got["pr"].tobytes() == want["pr"].tobytes()  # deterministic run to run
     assert got["bc"].tobytes() == want["bc"].tobytes()
     assert got["tc"] == want["tc"]
+
+
+@pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 14, 16, False), ("rmat", 18, 16, False),
+                                            ("grid", 64, 64, True)])
+def test_device_loop_equals_host_loop(kind, p0, p1, und, monkeypatch):
+    """The conditional-graph fixedPoint loops (PR, SSSP) give bit-identical
+    results to the host-driven loop over the same kernels (SP_HOSTLOOP=1)."""
+    g, _ = _pair(kind, p0, p1, 5, und)
+    args = {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
+    dev_pr = sp.run(corpus.PR, g, args)
+    dev_ss = sp.run(corpus.SSSP, g, {"src": 0})
+    monkeypatch.setenv("SP_HOSTLOOP", "1")
+    host_pr = sp.run(corpus.PR, g, args)
+    host_ss = sp.run(corpus.SSSP, g, {"src": 0})
+    assert dev_pr.env.node_props["rank"].tobytes() == host_pr.env.node_props["rank"].tobytes()
+    assert dev_pr.env.scalars == host_pr.env.scalars
+    assert np.array_equal(dev_ss.env.node_props["dist"], host_ss.env.node_props["dist"])
