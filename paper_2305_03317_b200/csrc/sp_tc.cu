@@ -50,7 +50,9 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int kA = 256;            // staged A entries per warp (larger rows: global search)
+constexpr int kA = 256;            // warp path: upper rows up to kA (longer: k_tc_big)
+constexpr int kT = 512;            // warp path: hash table entries (>= 2 kA)
+constexpr int kFwdWarpWords = 2 * kT + 2 * kA + 1 + 128;  // per-warp shared words
 constexpr int kFilterWords = 128;  // 4096-bit filter per warp
 constexpr int kFilterShift = 20;   // 32 - log2(4096)
 constexpr int kBatch = 32;
@@ -269,7 +271,9 @@ struct TcCounters {
     unsigned long long abytes;  // sum over pairs of |N+(a)| (model bytes / 4)
 };
 
-__global__ void __launch_bounds__(kBlock, 1) k_tc_fwd(const uint32_t *__restrict__ ustart8,
+// Warp path, plain form: A sorted in shared memory, filter probe, binary
+// search on a filter hit (cheapest when hits are rare, e.g. uniform graphs).
+__global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__restrict__ ustart8,
                                                    const int32_t *__restrict__ ulen,
                                                    const int32_t *__restrict__ uadj,
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
@@ -380,15 +384,160 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd(const uint32_t *__restrict
     }
 }
 
+// Warp path, hashed form: on a filter hit the multiplicity comes from a
+// per-warp hash table of A (skewed graphs, where most probes are hits).
+__global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__restrict__ ustart8,
+                                                   const int32_t *__restrict__ ulen,
+                                                   const int32_t *__restrict__ uadj,
+                                                   const uint2 *__restrict__ uinfo, int64_t v0,
+                                                   int64_t v1, TcCounters *ctr) {
+    // per warp, dynamic shared memory: hash keys[kT] + counts[kT] of A,
+    // sector starts B[kA], sector prefix S[kA+1], filter F[kFilterWords]
+    extern __shared__ uint32_t fwd_smem[];
+    const unsigned lane = lane_id();
+    const int wib = threadIdx.x >> 5;
+    uint32_t *base = fwd_smem + (size_t)wib * kFwdWarpWords;
+    int32_t *HK = reinterpret_cast<int32_t *>(base);
+    uint32_t *HC = base + kT;
+    uint32_t *B = base + 2 * kT;
+    int32_t *S = reinterpret_cast<int32_t *>(base + 2 * kT + kA);
+    uint32_t *F = base + 2 * kT + 2 * kA + 1;
+    unsigned long long cnt = 0, elems = 0, pairs = 0, abytes = 0;
+    for (;;) {
+        unsigned long long bt = 0;
+        if (lane == 0) bt = atomicAdd(&ctr->next, (unsigned long long)kBatch);
+        bt = __shfl_sync(0xffffffffu, bt, 0);
+        const int64_t vb = v0 + (int64_t)bt;
+        if (vb >= v1) break;
+        const int64_t ve = min(v1, vb + kBatch);
+        // the batch's row descriptors, one coalesced load
+        const int64_t my = vb + lane;
+        const uint32_t my_s8 = my < ve ? ustart8[my] : 0u;
+        const int32_t my_len = my < ve ? ulen[my] : 0;
+        for (int64_t a = vb; a < ve; a++) {
+            const int src = (int)(a - vb);
+            const int na = __shfl_sync(0xffffffffu, my_len, src);
+            if (na < 2) continue;  // a triangle needs b and x in N+(a)
+            const int64_t r0 = kPad * (int64_t)__shfl_sync(0xffffffffu, my_s8, src);
+            if (na > kA) continue;  // k_tc_big (one CTA per vertex) counts it
+            if (lane == 0) {
+                pairs += (unsigned long long)na;
+                abytes += (unsigned long long)na * (unsigned long long)na;
+            }
+            // ---- hash table of A (with multiplicities), row starts, sector
+            // prefix and filter
+            int tbits = 5;
+            while ((1 << tbits) < 2 * na) tbits++;
+            const int T = 1 << tbits;
+            for (int k = lane; k < kFilterWords; k += 32) F[k] = 0u;
+            for (int k = lane; k < T; k += 32) {
+                HK[k] = -1;
+                HC[k] = 0u;
+            }
+            __syncwarp();
+            int carry = 0;
+            for (int k0 = 0; k0 < na; k0 += 32) {
+                const int k = k0 + lane;
+                int secs = 0;
+                if (k < na) {
+                    const int32_t x = uadj[r0 + k];
+                    const uint2 inf = uinfo[r0 + k];
+                    uint32_t h = ((uint32_t)x * 2654435761u) >> (32 - tbits);
+                    for (;;) {
+                        const int32_t old = atomicCAS(&HK[h], -1, x);
+                        if (old == -1 || old == x) {
+                            atomicAdd(&HC[h], 1u);
+                            break;
+                        }
+                        h = (h + 1) & (T - 1);
+                    }
+                    B[k] = inf.x;
+                    secs = (int)((inf.y + kPad - 1u) / kPad);
+                    elems += inf.y;
+                    const uint32_t hh = fhash(x);
+                    atomicOr(&F[hh >> 5], 1u << (hh & 31));
+                }
+                int incl = secs;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if ((int)lane >= o) incl += t;
+                }
+                if (k < na) S[k] = carry + incl - secs;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) S[na] = carry;
+            __syncwarp();
+            // ---- flattened walk of all rows b_j in 16-byte half-sectors:
+            // one int4 per lane (rows are 32-byte aligned and padded with -1),
+            // kUnroll loads in flight per lane, one row search per 4 slots
+            const int nhalf = kQ * carry;
+            for (int h0 = 0; h0 < nhalf; h0 += 32 * kUnroll) {
+                int4 xs[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    const int h = h0 + u * 32 + (int)lane;
+                    xs[u] = make_int4(-1, -1, -1, -1);
+                    if (h < nhalf) {
+                        const int sec = h / kQ;
+                        int lo = 0, hi = na;  // last j with S[j] <= sec
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (S[mid] <= sec) lo = mid; else hi = mid;
+                        }
+                        xs[u] = __ldg(reinterpret_cast<const int4 *>(uadj) +
+                                      kQ * ((int64_t)B[lo] + (sec - S[lo])) + (h % kQ));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    const int32_t xv[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const int32_t x = xv[i];
+                        if (x < 0) continue;  // padding or past the end
+                        const uint32_t hh = fhash(x);
+                        if (F[hh >> 5] & (1u << (hh & 31))) {  // filter hit: hash probe
+                            uint32_t h = ((uint32_t)x * 2654435761u) >> (32 - tbits);
+                            for (;;) {
+                                const int32_t key = HK[h];
+                                if (key == x) {
+                                    cnt += HC[h];
+                                    break;
+                                }
+                                if (key == -1) break;
+                                h = (h + 1) & (T - 1);
+                            }
+                        }
+                    }
+                }
+            }
+            __syncwarp();  // A/B/S/F are restaged for the next vertex
+        }
+    }
+    cnt = warp_sum(cnt);
+    elems = warp_sum(elems);
+    if (lane == 0) {
+        if (cnt) atomicAdd(&ctr->total, cnt);
+        if (pairs) atomicAdd(&ctr->pairs, pairs);
+        if (elems) atomicAdd(&ctr->elems, elems);
+        if (abytes) atomicAdd(&ctr->abytes, abytes);
+    }
+}
+
 // One CTA per vertex whose upper row exceeds the warp path (kA): the block
-// stages A = N+(a) (up to kBigMax entries) and a kBigFilterBits filter in
-// dynamic shared memory; each warp takes 32 of A's b's at a time, loads
+// builds an open-addressing hash table of A = N+(a) with multiplicities in
+// dynamic shared memory (rows up to kHashMax; a membership hit -- on skewed
+// graphs most probes are hits -- costs one probe instead of a binary
+// search), or for longer rows stages A (up to kBigMax) with a
+// kBigFilterBits filter; each warp takes 32 of A's b's at a time, loads
 // their row descriptors with one coalesced read, and walks the flattened
 // 16-byte half-sectors of their rows (owner by a 5-step shuffle search),
 // one filter probe per element and a shared-memory binary search on a hit.
 constexpr int kBigFilterBits = 1 << 17;  // 16 KB
 constexpr int kBigFilterShift = 32 - 17;
 constexpr int kBigMax = 48 * 1024;      // staged A entries (192 KB) -- beyond: global search
+constexpr int kHashMax = 8 * 1024;      // rows up to this are hashed: 2^14 x (key, count) = 128 KB
 
 __global__ void __launch_bounds__(kBlock, 1) k_tc_big(const uint32_t *__restrict__ ustart8,
                                                       const int32_t *__restrict__ ulen,
@@ -400,6 +549,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_big(const uint32_t *__restrict
     extern __shared__ uint32_t smem[];
     uint32_t *F = smem;                                        // kBigFilterBits / 32 words
     int32_t *A = reinterpret_cast<int32_t *>(smem + kBigFilterBits / 32);
+    // hashed form (na <= kHashMax): keys[T] then counts[T] from smem[0]
+    int32_t *HK = reinterpret_cast<int32_t *>(smem);
     const unsigned lane = lane_id();
     const int wid = threadIdx.x >> 5;
     unsigned long long cnt = 0, elems = 0, pairs = 0, abytes = 0;
@@ -409,8 +560,32 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_big(const uint32_t *__restrict
         const int na = ulen[a];
         const int64_t r0 = kPad * (int64_t)ustart8[a];
         const bool staged = na <= kBigMax;
-        __syncthreads();  // previous vertex done with A/F
-        if (staged) {
+        const bool hashed = na <= kHashMax;
+        int tbits = 6;  // table of 2^tbits >= 2 na entries
+        while ((1 << tbits) < 2 * na) tbits++;
+        const int T = 1 << tbits;
+        uint32_t *HC = reinterpret_cast<uint32_t *>(HK + T);
+        __syncthreads();  // previous vertex done with the shared structures
+        if (hashed) {
+            for (int k = threadIdx.x; k < T; k += blockDim.x) {
+                HK[k] = -1;
+                HC[k] = 0u;
+            }
+            __syncthreads();
+            for (int k = threadIdx.x; k < na; k += blockDim.x) {
+                const int32_t x = uadj[r0 + k];
+                uint32_t h = ((uint32_t)x * 2654435761u) >> (32 - tbits);
+                for (;;) {
+                    const int32_t old = atomicCAS(&HK[h], -1, x);
+                    if (old == -1 || old == x) {
+                        atomicAdd(&HC[h], 1u);
+                        break;
+                    }
+                    h = (h + 1) & (T - 1);
+                }
+            }
+            __syncthreads();
+        } else if (staged) {
             for (int k = threadIdx.x; k < kBigFilterBits / 32; k += blockDim.x) F[k] = 0u;
             __syncthreads();
             for (int k = threadIdx.x; k < na; k += blockDim.x) {
@@ -459,7 +634,18 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_big(const uint32_t *__restrict
                 for (int i = 0; i < 4; i++) {
                     const int32_t x = xv[i];
                     if (x < 0) continue;
-                    if (staged) {
+                    if (hashed) {  // multiplicity of x in A: one probe on average
+                        uint32_t h = ((uint32_t)x * 2654435761u) >> (32 - tbits);
+                        for (;;) {
+                            const int32_t k = HK[h];
+                            if (k == x) {
+                                cnt += HC[h];
+                                break;
+                            }
+                            if (k == -1) break;
+                            h = (h + 1) & (T - 1);
+                        }
+                    } else if (staged) {
                         const uint32_t hh = ((uint32_t)x * 2654435761u) >> kBigFilterShift;
                         if (F[hh >> 5] & (1u << (hh & 31))) cnt += mult_s(A, na, x);
                     } else {
@@ -566,12 +752,23 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
             k_tc_mid<<<grid, kBlock, 0, c.stream>>>(g->off, g->adj, v0, v1, ctr);
             c.launches++;
         } else {
-            k_tc_fwd<<<grid, kBlock, 0, c.stream>>>(g->ustart8, g->ulen, g->uadj, g->uinfo, v0,
-                                                    v1, ctr);
+            if (g->nbig > 0) {  // skewed: long upper rows exist, hits are frequent
+                const size_t fsm = (size_t)kWarps * kFwdWarpWords * 4;
+                SP_CUDA(cudaFuncSetAttribute(k_tc_fwd_hash,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+                k_tc_fwd_hash<<<grid, kBlock, fsm, c.stream>>>(g->ustart8, g->ulen, g->uadj,
+                                                               g->uinfo, v0, v1, ctr);
+            } else {
+                k_tc_fwd_plain<<<grid, kBlock, 0, c.stream>>>(g->ustart8, g->ulen, g->uadj,
+                                                              g->uinfo, v0, v1, ctr);
+            }
             c.launches++;
             if (g->nbig) {
-                const size_t smem = kBigFilterBits / 8 +
-                                    4 * (size_t)std::min<int64_t>(g->max_ulen, kBigMax);
+                int tb = 6;
+                while ((1 << tb) < 2 * std::min<int64_t>(g->max_ulen, kHashMax)) tb++;
+                const size_t smem = std::max<size_t>(
+                    (size_t)8 << tb,  // hash keys + counts
+                    kBigFilterBits / 8 + 4 * (size_t)std::min<int64_t>(g->max_ulen, kBigMax));
                 SP_CUDA(cudaFuncSetAttribute(k_tc_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
                 int per_sm = 1;
