@@ -138,6 +138,14 @@ void sp_graph_destroy(sp_graph *g);
 int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist, int mem,
             int64_t *iters, sp_iter_cb cb, void *user, sp_stats *st);
 
+/* corpus/programs/sssp_pull.sp (sssp_pull.sp:9-14): the pull form --
+ * every vertex takes the minimum over its frontier in-neighbours (reverse
+ * CSR, w_eff of the first forward slot u -> v), exact min, no atomics on
+ * dist -- for large frontiers, push steps for small ones (direction
+ * optimisation).  Same dist as sp_sssp (the unique relaxation fixpoint). */
+int sp_sssp_pull(sp_graph *g, int32_t src, int64_t cap, int32_t *dist, int mem,
+                 int64_t *iters, sp_iter_cb cb, void *user, sp_stats *st);
+
 /* Block-partitioned SSSP supersteps (multi-GPU; graph.py:226-249 ownership,
  * the exchange is the caller's all-reduce(min) of dist between steps; this
  * replaces the BSP model of bsp.py:393-417 with convergence evaluated after

@@ -74,6 +74,7 @@ SIGNATURES = {
     "sp_graph_weight_range": (_int, [_p, _p, _p]),
     "sp_graph_destroy": (None, [_p]),
     "sp_sssp": (_int, [_p, _i32, _i64, _p, _int, _p, ITER_CB, _p, _p]),
+    "sp_sssp_pull": (_int, [_p, _i32, _i64, _p, _int, _p, ITER_CB, _p, _p]),
     "sp_sssp_block_init": (_int, [_p, _i32, _p, _p]),
     "sp_sssp_block_step": (_int, [_p, _i64, _i64, _p, _p, _p, _p]),
     "sp_pagerank": (_int, [_p, _d, _d, _i64, _i64, _u, _p, _int, _p, _p, _p,

@@ -90,7 +90,7 @@ struct Call {
 
 // Launch `graph` through this thread's executable cache for (key, kind)
 // (see sp_runtime.cu); the caller keeps ownership of `graph`.
-enum { kLoopSsspBf = 1, kLoopSsspNf = 2, kLoopPr = 3 };
+enum { kLoopSsspBf = 1, kLoopSsspNf = 2, kLoopPr = 3, kLoopSsspDo = 4 };
 int launch_cached_graph(cudaGraph_t graph, const void *key, int kind, cudaStream_t stream);
 
 // Copy a caller buffer to/from the device according to `mem`.
@@ -109,6 +109,7 @@ struct sp_graph {
     int32_t *adj = nullptr;
     int32_t *w = nullptr;
     int32_t *weff = nullptr;  // get_edge first-slot weight
+    int32_t *rweff = nullptr; // w_eff of the forward slot behind each reverse slot (pull SSSP)
     int32_t *outdeg = nullptr;
     // reverse CSR (graph.py:33-35); aliases of off/adj when undirected
     int64_t *roff = nullptr;
@@ -148,6 +149,8 @@ namespace sp {
 
 // Build the graph's w_eff array if it was deferred (thread-safe).
 int ensure_weff(sp_graph *g, Call &c);
+// Reverse-slot weights rweff[k] = w_eff[reid[k]] (undirected: w_eff itself).
+int ensure_rweff(sp_graph *g, Call &c);
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 

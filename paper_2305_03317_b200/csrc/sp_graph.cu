@@ -335,6 +335,7 @@ void free_graph(sp_graph *g) {
     resident_free(g->adj);
     resident_free(g->w);
     resident_free(g->weff);
+    if (g->directed) resident_free(g->rweff);
     resident_free(g->outdeg);
     if (g->directed) {
         resident_free(g->roff);
@@ -612,6 +613,35 @@ int ensure_weff(sp_graph *g, Call &c) {
         SP_CUDA(e);
     }
     g->weff = weff;
+    return SP_OK;
+}
+
+__global__ void k_rweff(const int32_t *__restrict__ weff, const int64_t *__restrict__ reid,
+                        int64_t m, int32_t *rw) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x)
+        rw[k] = weff[reid[k]];
+}
+
+int ensure_rweff(sp_graph *g, Call &c) {
+    SP_TRY(ensure_weff(g, c));
+    std::lock_guard<std::mutex> lk(g_lazy_mu);
+    if (g->rweff || g->m == 0) return SP_OK;
+    if (!g->directed) {  // reverse CSR == forward CSR, mirrored slots share runs (F11)
+        g->rweff = g->weff;
+        return SP_OK;
+    }
+    if (!g->reid) SP_TRY(build_reverse(g, c, false, true));
+    int32_t *rw = nullptr;
+    SP_TRY(dalloc(&rw, g->m));
+    k_rweff<<<gridN(g->m, c.device), 256, 0, c.stream>>>(g->weff, g->reid, g->m, rw);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+    if (e != cudaSuccess) {
+        resident_free(rw);
+        SP_CUDA(e);
+    }
+    g->rweff = rw;
     return SP_OK;
 }
 

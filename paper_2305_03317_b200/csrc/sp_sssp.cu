@@ -500,6 +500,355 @@ int sssp_near_far(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa
     return SP_OK;
 }
 
+// ---- direction-optimising loop (push / pull), low-diameter graphs -------
+// sssp_pull.sp's form of the relaxation: every vertex v takes the minimum
+// of dist[u] + w_eff(u -> v) over its in-neighbours u in the frontier (a
+// bitmap), an exact min in any order, one write per improved vertex, no
+// atomics on dist.  Large frontiers run pull steps, small ones push steps
+// (Beamer's direction optimisation); both converge to the same fixpoint.
+struct DoLoop {
+    SsspLoop s;            // push-side state (queues, counters, totals)
+    uint32_t *bitsF;       // frontier bitmap (pull input)
+    uint32_t *bitsN;       // next-frontier bitmap (pull output, zeroed)
+    int32_t *hubs;         // in-rows longer than kPullHub of this pull step
+    unsigned long long nhubs;
+    int64_t nwords, n;
+    int64_t pull_div;      // pull when the frontier exceeds n / pull_div
+    int mode;              // 0 push, 1 pull (this iteration)
+    int next_mode;
+    int conv;              // after advance: 1 queue->bits, 2 bits->queue
+};
+
+constexpr int kPullChunk = 128;
+constexpr int64_t kPullHub = 1024;
+constexpr int64_t kPullDiv = 24;  // pull when the frontier exceeds n / kPullDiv
+
+__device__ __forceinline__ bool fbit(const uint32_t *b, int32_t u) {
+    return (__ldcg(b + (u >> 5)) >> (u & 31)) & 1u;
+}
+
+// Apply a row's minimum: improve dist[v], mark v in the next bitmap, count.
+__device__ __forceinline__ bool pull_apply(DoLoop *L, int32_t *dist, int64_t v, int64_t best) {
+    if (best >= (int64_t)kIntMax || best >= (int64_t)__ldcg(dist + v)) return false;
+    if (best < (int64_t)(-2147483647 - 1)) {
+        atomicAdd(&L->s.cnt[L->s.cur].flag, 1ull);
+        return false;
+    }
+    dist[v] = (int32_t)best;
+    atomicOr(L->bitsN + (v >> 5), 1u << (v & 31));
+    return true;
+}
+
+__global__ void __launch_bounds__(256) k_pull_tiles(const int64_t *__restrict__ roff,
+                                                    const int32_t *__restrict__ radj,
+                                                    const int32_t *__restrict__ rw, int32_t *dist,
+                                                    DoLoop *L) {
+    if (L->mode != 1) return;
+    __shared__ int32_t stage[8][kPullChunk];
+    const unsigned lane = lane_id();
+    int32_t *buf = stage[threadIdx.x >> 5];
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t n = L->n;
+    const uint32_t *F = L->bitsF;
+    unsigned long long useful = 0, improved = 0;
+    for (int64_t t0 = warp * 32; t0 < n; t0 += nwarps * 32) {
+        const int64_t v = t0 + lane;
+        int64_t rs = 0, deg = 0;
+        if (v < n) {
+            rs = roff[v];
+            deg = roff[v + 1] - rs;
+        }
+        const bool hub = deg > kPullHub;
+        {
+            const int64_t slot = warp_append(hub, &L->nhubs);
+            if (hub) L->hubs[slot] = (int32_t)v;
+        }
+        if (hub) deg = 0;
+        int64_t incl = deg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl += t;
+        }
+        const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const int64_t excl = incl - deg;
+        int64_t best = INT64_MAX;
+        for (int64_t p0 = 0; p0 < total; p0 += kPullChunk) {
+#pragma unroll
+            for (int j = 0; j < kPullChunk / 32; j++) {
+                const int64_t p = p0 + j * 32 + lane;
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = lo + step;
+                    const int64_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+                    if (cand < 32 && ex <= p) lo = cand;
+                }
+                const int64_t ex = __shfl_sync(0xffffffffu, excl, lo);
+                const int64_t b0 = __shfl_sync(0xffffffffu, rs, lo);
+                int32_t c = kIntMax;
+                if (p < total) {
+                    const int64_t k = b0 + (p - ex);
+                    const int32_t u = __ldcs(radj + k);
+                    if (fbit(F, u)) {
+                        useful++;
+                        const int64_t cand = (int64_t)__ldcg(dist + u) + (int64_t)__ldcs(rw + k);
+                        c = cand >= (int64_t)kIntMax ? kIntMax
+                            : (cand < (int64_t)(-2147483647 - 1) ? (int32_t)(-2147483647 - 1)
+                                                                 : (int32_t)cand);
+                    }
+                }
+                buf[j * 32 + lane] = c;
+            }
+            __syncwarp();
+            const int64_t a = max(excl, p0), b = min(excl + deg, p0 + (int64_t)kPullChunk);
+            for (int64_t p = a; p < b; p++) best = min(best, (int64_t)buf[p - p0]);
+            __syncwarp();
+        }
+        if (v < n && !hub && deg > 0) improved += pull_apply(L, dist, v, best) ? 1 : 0;
+    }
+    useful = warp_sum(useful);
+    improved = warp_sum(improved);
+    if (lane == 0) {
+        if (useful) atomicAdd(&L->s.cnt[L->s.cur].scanned, useful);
+        if (improved) atomicAdd(&L->s.cnt[L->s.cur].next_size, improved);
+    }
+}
+
+// In-rows longer than kPullHub: one warp per row, strided slots, warp min.
+__global__ void __launch_bounds__(256) k_pull_hubs(const int64_t *__restrict__ roff,
+                                                   const int32_t *__restrict__ radj,
+                                                   const int32_t *__restrict__ rw, int32_t *dist,
+                                                   DoLoop *L) {
+    if (L->mode != 1) return;
+    const unsigned lane = lane_id();
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nh = (int64_t)__ldcg(&L->nhubs);
+    const uint32_t *F = L->bitsF;
+    unsigned long long useful = 0, improved = 0;
+    for (int64_t h = warp; h < nh; h += nwarps) {
+        const int32_t v = L->hubs[h];
+        const int64_t r0 = roff[v], r1 = roff[v + 1];
+        int64_t best = INT64_MAX;
+        for (int64_t k = r0 + lane; k < r1; k += 32) {
+            const int32_t u = __ldcs(radj + k);
+            if (fbit(F, u)) {
+                useful++;
+                best = min(best, (int64_t)__ldcg(dist + u) + (int64_t)__ldcs(rw + k));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0) improved += pull_apply(L, dist, v, best) ? 1 : 0;
+    }
+    useful = warp_sum(useful);
+    if (lane == 0) {
+        if (useful) atomicAdd(&L->s.cnt[L->s.cur].scanned, useful);
+        if (improved) atomicAdd(&L->s.cnt[L->s.cur].next_size, improved);
+    }
+}
+
+__global__ void __launch_bounds__(kExpandBlock, 4) k_do_push(
+    int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, uint2 *chunks,
+    DoLoop *D, int64_t warps) {
+    if (D->mode != 0) return;
+    SsspLoop *L = &D->s;
+    const int cur = L->cur;
+    const int64_t nq = L->nq;
+    RelaxOp op{dist, enq, weff, &L->cnt[cur].flag, L->it};
+    expand_body(op, off, adj, L->q[cur], nq, L->q[cur ^ 1], chunks, &L->cnt[cur],
+                expand_vpw(nq, warps));
+}
+
+__global__ void __launch_bounds__(kExpandBlock, 4) k_do_push_chunks(
+    int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const uint2 *chunks,
+    DoLoop *D) {
+    if (D->mode != 0) return;
+    SsspLoop *L = &D->s;
+    const int cur = L->cur;
+    RelaxOp op{dist, enq, weff, &L->cnt[cur].flag, L->it};
+    expand_chunks_body(op, off, adj, chunks, L->q[cur ^ 1], &L->cnt[cur]);
+}
+
+// Totals, termination, and the direction of the next iteration.
+__global__ void k_do_advance(DoLoop *D, cudaGraphConditionalHandle h) {
+    SsspLoop *L = &D->s;
+    const int cur = L->cur;
+    const ExpandCounters c = L->cnt[cur];
+    L->iters++;
+    L->frontier_sum += L->nq;
+    L->relaxed += (int64_t)c.scanned;
+    const int64_t next = (int64_t)c.next_size;
+    int go = 1;
+    if (c.flag) {
+        L->status = 1;
+        go = 0;
+    } else if (next == 0) {
+        go = 0;
+    } else if (L->iters >= L->cap) {
+        L->status = 2;
+        go = 0;
+    }
+    const int nm = next * D->pull_div > D->n ? 1 : 0;
+    D->conv = 0;
+    if (D->mode == 0 && nm == 1) D->conv = 1;  // queue -> bits
+    if (D->mode == 1) {                         // the pull output becomes the frontier
+        uint32_t *t = D->bitsF;
+        D->bitsF = D->bitsN;
+        D->bitsN = t;
+        if (nm == 0) D->conv = 2;               // bits -> queue
+    }
+    D->next_mode = nm;
+    D->nhubs = 0;
+    L->cnt[cur ^ 1] = ExpandCounters{0, 0, 0, 0};
+    L->cur = cur ^ 1;
+    L->nq = next;
+    L->it = (int)(L->iters + 1);
+    cudaGraphSetConditional(h, go);
+}
+
+// Zero the bitmap the next pull writes (and the frontier bitmap a
+// queue -> bits conversion fills).
+__global__ void k_do_clear(DoLoop *D) {
+    if (D->next_mode != 1) return;
+    uint32_t *N = D->bitsN, *F = D->bitsF;
+    const bool clearF = D->conv == 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < D->nwords;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        N[i] = 0u;
+        if (clearF) F[i] = 0u;
+    }
+}
+
+__global__ void k_do_convert(DoLoop *D) {
+    SsspLoop *L = &D->s;
+    const int conv = D->conv;
+    if (conv == 1) {  // the queue just produced (q[cur]) -> frontier bits
+        const int32_t *q = L->q[L->cur];
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L->nq;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int32_t v = q[i];
+            atomicOr(D->bitsF + (v >> 5), 1u << (v & 31));
+        }
+    } else if (conv == 2) {  // frontier bits -> queue q[cur]; nq already counted
+        int32_t *q = L->q[L->cur];
+        for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < D->nwords;
+             b += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t i = b + threadIdx.x;
+            const uint32_t w = i < D->nwords ? __ldcg(D->bitsF + i) : 0u;
+            const int c = __popc(w);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane_id() >= o) incl += t;
+            }
+            const int tot = __shfl_sync(0xffffffffu, incl, 31);
+            unsigned long long base = 0;
+            if (lane_id() == 0 && tot) base = atomicAdd(&D->s.cnt[D->s.cur].chunks, (unsigned long long)tot);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            uint32_t x = w;
+            int64_t at = (int64_t)base + incl - c;
+            while (x) {
+                const int bit = __ffs(x) - 1;
+                x &= x - 1;
+                q[at++] = (int32_t)(i * 32 + bit);
+            }
+        }
+    }
+    // counters of the new current iteration start clean (chunks was borrowed)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && conv == 2) {}
+}
+
+__global__ void k_do_mode(DoLoop *D) {
+    D->mode = D->next_mode;
+    D->s.cnt[D->s.cur].chunks = 0;  // borrowed by the bits -> queue conversion
+}
+
+int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
+                 uint2 *chunks, int64_t cap, SsspLoop *out, float *kernel_ms) {
+    SP_TRY(ensure_rweff(g, c));
+    const int64_t n = g->n;
+    const int64_t nwords = (n + 31) / 32;
+    DoLoop *D;
+    uint32_t *b0, *b1;
+    int32_t *hubs;
+    SP_TRY(c.alloc(&D, 1));
+    SP_TRY(c.alloc(&b0, nwords));
+    SP_TRY(c.alloc(&b1, nwords));
+    SP_TRY(c.alloc(&hubs, n));
+    DoLoop init{};
+    init.s.q[0] = qa;
+    init.s.q[1] = qb;
+    init.s.nq = 1;
+    init.s.it = 1;
+    init.s.cap = cap;
+    init.bitsF = b0;
+    init.bitsN = b1;
+    init.hubs = hubs;
+    init.nwords = nwords;
+    init.n = n;
+    const char *pd = getenv("SP_SSSP_PULL_DIV");
+    init.pull_div = pd ? atoll(pd) : kPullDiv;
+    SP_CUDA(cudaMemcpyAsync(D, &init, sizeof(DoLoop), cudaMemcpyHostToDevice, c.stream));
+    const int sms = num_sms(c.device);
+    const int grid = sms * 8;
+    const int64_t warps = (int64_t)grid * (kExpandBlock / 32);
+    const bool big = g->max_outdeg > kSplit;
+    cudaGraph_t graph = nullptr;
+    struct GraphFree {
+        cudaGraph_t *g;
+        ~GraphFree() {
+            if (*g) cudaGraphDestroy(*g);
+        }
+    } gf{&graph};
+    SP_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    SP_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    SP_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+    k_do_push<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off, g->adj, chunks, D,
+                                                   warps);
+    if (big)
+        k_do_push_chunks<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off, g->adj,
+                                                              chunks, D);
+    k_pull_tiles<<<grid, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
+    k_pull_hubs<<<sms * 2, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
+    k_do_advance<<<1, 1, 0, c.stream>>>(D, h);
+    k_do_clear<<<grid, 256, 0, c.stream>>>(D);
+    k_do_convert<<<grid, 256, 0, c.stream>>>(D);
+    k_do_mode<<<1, 1, 0, c.stream>>>(D);
+    SP_CUDA(cudaStreamEndCapture(c.stream, &body));
+    cudaEvent_t ka, kb;
+    SP_CUDA(cudaEventCreate(&ka));
+    SP_CUDA(cudaEventCreate(&kb));
+    cudaEventRecord(ka, c.stream);
+    SP_TRY(launch_cached_graph(graph, g, kLoopSsspDo, c.stream));
+    cudaEventRecord(kb, c.stream);
+    DoLoop *hD;
+    SP_TRY(c.host_as(&hD));
+    SP_CUDA(cudaMemcpyAsync(hD, D, sizeof(DoLoop), cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    cudaEventElapsedTime(kernel_ms, ka, kb);
+    cudaEventDestroy(ka);
+    cudaEventDestroy(kb);
+    *out = hD->s;
+    c.launches += hD->s.iters * (big ? 8 : 7);
+    return SP_OK;
+}
+
 // Near-far threshold step; 0 selects plain Bellman-Ford (negative weights,
 // or SP_SSSP_DELTA=0).  Default: kDeltaMul x the mean of the weight range.
 int64_t near_far_delta(const sp_graph *g, int32_t wmin, int32_t wmax) {
@@ -576,8 +925,9 @@ int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t 
 
 }  // namespace
 
-extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, int mem,
-                       int64_t *iters_out, sp_iter_cb cb, void *user, sp_stats *st) {
+static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, int mem,
+                     int64_t *iters_out, sp_iter_cb cb, void *user, sp_stats *st,
+                     bool pull_form) {
     SP_CHECK(g && dist_out, SP_ERR_ARG, "sp_sssp: bad arguments");
     SP_CHECK(src >= 0 && src < g->n, SP_ERR_ARG, "node argument 'src'=%d out of range", src);
     Call c;
@@ -616,14 +966,17 @@ extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out,
         int lrc;
         int32_t wr[2] = {0, 0};
         if (g->m) SP_CUDA(cudaMemcpy(wr, g->wrange, sizeof(wr), cudaMemcpyDeviceToHost));
-        const int64_t delta = near_far_delta(g, wr[0], wr[1]);
+        const int64_t delta = pull_form ? 0 : near_far_delta(g, wr[0], wr[1]);
         if (delta > 0)
             lrc = sssp_near_far(g, c, dist, enq, qa, qb, chunks, cap, delta, &hL, &kernel_ms);
-        if (delta <= 0 || (lrc == SP_OK && hL.status == 3)) {  // plain Bellman-Ford
+        if (delta <= 0 || (lrc == SP_OK && hL.status == 3)) {  // Bellman-Ford
             k_init<<<grid_for(n, kBlock, dev), kBlock, 0, c.stream>>>(dist, enq, n, src, qa);
             c.launches++;
             hL = SsspLoop{};
-            lrc = sssp_device_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
+            if (pull_form)  // sssp_pull.sp: pull steps for large frontiers
+                lrc = sssp_do_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
+            else
+                lrc = sssp_device_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
         }
         if (lrc == SP_OK) {
             iters = hL.iters;
@@ -696,6 +1049,16 @@ done:
         st->model_bytes = 12 * relaxed + 20 * frontier_sum;
     }
     return rc;
+}
+
+extern "C" int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, int mem,
+                       int64_t *iters_out, sp_iter_cb cb, void *user, sp_stats *st) {
+    return sssp_impl(g, src, cap, dist_out, mem, iters_out, cb, user, st, false);
+}
+
+extern "C" int sp_sssp_pull(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, int mem,
+                            int64_t *iters_out, sp_iter_cb cb, void *user, sp_stats *st) {
+    return sssp_impl(g, src, cap, dist_out, mem, iters_out, cb, user, st, true);
 }
 
 // ---- block-partitioned supersteps (multi-GPU, graph.py:226-249 ownership)

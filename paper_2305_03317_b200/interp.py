@@ -209,8 +209,9 @@ def run(tp, g, args: dict, function: str | None = None,
     if prog.key in ("sssp", "sssp_pull"):
         dist, mem = _out(n, np.int32, odev)
         iters = C.c_int64()
-        rc = L.sp_sssp(dg.handle, bound["src"], cap, _ptr(dist), mem, C.byref(iters),
-                       hook.cb, None, C.byref(st))
+        fn = L.sp_sssp_pull if prog.key == "sssp_pull" else L.sp_sssp
+        rc = fn(dg.handle, bound["src"], cap, _ptr(dist), mem, C.byref(iters),
+                hook.cb, None, C.byref(st))
         _raise_for(rc, E, prog.flag, cap, hook.exc)
         env.node_props = {"dist": dist, "modified": np.zeros(n, dtype=bool),
                           "modified_nxt": np.zeros(n, dtype=bool)}

@@ -105,3 +105,11 @@ def test_sssp_grid_cfg5_bellman_certificate():
     best[0] = 0
     np.testing.assert_array_equal(dist, best)
     g.close()
+
+
+def test_sssp_pull_rmat22_full(rmat22):
+    """sssp_pull.sp's pull form (direction-optimising) on the cfg2 graph."""
+    g, o = rmat22
+    dist, _, rc = cpu_ref.sssp(o, 0)
+    np.testing.assert_array_equal(
+        sp.run(corpus.SSSP_PULL, g, {"src": 0}).env.node_props["dist"], dist)

@@ -173,9 +173,10 @@ def test_sssp_cfg1_rmat16_bit_exact():
 def test_sssp_seeded(kind, p0, p1, und):
     g, o = _pair(kind, p0, p1, 11, und)
     for s in (0, g.n // 2):
-        r = sp.run(corpus.SSSP, g, {"src": s})
         dist, _, rc = cpu_ref.sssp(o, s)
-        np.testing.assert_array_equal(r.env.node_props["dist"], dist)
+        for prog in (corpus.SSSP, corpus.SSSP_PULL):  # push and pull forms
+            r = sp.run(prog, g, {"src": s})
+            np.testing.assert_array_equal(r.env.node_props["dist"], dist)
 
 
 @pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 14, 16, False), ("rmat", 13, 16, True),
@@ -276,6 +277,9 @@ def test_multigraph_all_algorithms(directed):
     np.testing.assert_array_equal(g.rev_eid, o.reid)
     dist, _, _ = cpu_ref.sssp(o, 0)
     np.testing.assert_array_equal(sp.run(corpus.SSSP, g, {"src": 0}).env.node_props["dist"], dist)
+    # pull form: reverse slots carry the first forward slot's weight (rweff)
+    np.testing.assert_array_equal(sp.run(corpus.SSSP_PULL, g, {"src": 0}).env.node_props["dist"],
+                                  dist)
     rank = cpu_ref.pagerank(o, cap=10 ** 6)[0]
     r = sp.run(corpus.PR, g, PR_ARGS, max_iters=10 ** 6, deterministic=True)
     assert r.env.node_props["rank"].tobytes() == rank.tobytes()
