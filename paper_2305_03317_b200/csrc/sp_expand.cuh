@@ -97,79 +97,110 @@ __device__ __forceinline__ void flush_stage(const Op &op, ExpandCounters *cnt, i
     if constexpr (HasFar<Op>::value) st.far.flush(op.far_n, op.far_q, op.far_cap);
 }
 
+// One batch: lane-held frontier vertex v (-1: none) expanded by the warp.
 template <class Op>
+__device__ __forceinline__ void expand_batch(const Op &op, const int64_t *__restrict__ off,
+                                             const int32_t *__restrict__ adj, int32_t v,
+                                             int32_t *__restrict__ qn, uint2 *__restrict__ chunks,
+                                             ExpandCounters *cnt, ExpandStage &st,
+                                             unsigned long long &scanned) {
+    using P = typename Op::Payload;
+    using Pr = typename Op::Probe;
+    const unsigned lane = lane_id();
+    int64_t beg = 0, deg = 0;
+    P pay = P(0);
+    if (v >= 0) {
+        beg = off[v];
+        deg = off[v + 1] - beg;
+        pay = op.payload(v);
+        if constexpr (HasKeep<Op>::value) {
+            if (!op.keep(v, pay)) deg = 0;
+        }
+    }
+    if (deg > kSplit) {  // hub row -> chunk work items
+        int64_t nch = (deg + kSplit - 1) / kSplit;
+        unsigned long long s = atomicAdd(&cnt->chunks, (unsigned long long)nch);
+        for (int64_t c = 0; c < nch; c++) chunks[s + c] = make_uint2((unsigned)v, (unsigned)c);
+        deg = 0;
+    }
+    int64_t incl = deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl += t;
+    }
+    const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const int64_t excl = incl - deg;
+    scanned += total;
+    for (int64_t p0 = 0; p0 < total; p0 += 32 * kRounds) {
+        int64_t e[kRounds];
+        int32_t x[kRounds];
+        P pv[kRounds];
+        Pr pr[kRounds];
+#pragma unroll
+        for (int u = 0; u < kRounds; u++) {
+            const int64_t p = p0 + u * 32 + lane;
+            // owner = largest lane with excl <= p (always a lane with deg > 0)
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                int cand = lo + step;
+                int64_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+                if (cand < 32 && ex <= p) lo = cand;
+            }
+            const int64_t ex = __shfl_sync(0xffffffffu, excl, lo);
+            const int64_t b0 = __shfl_sync(0xffffffffu, beg, lo);
+            pv[u] = __shfl_sync(0xffffffffu, pay, lo);
+            e[u] = p < total ? b0 + (p - ex) : -1;
+            x[u] = e[u] >= 0 ? __ldcs(adj + e[u]) : -1;  // streamed: evict first
+        }
+#pragma unroll
+        for (int u = 0; u < kRounds; u++)
+            if (e[u] >= 0) pr[u] = op.probe(e[u], x[u]);
+        int res[kRounds];
+#pragma unroll
+        for (int u = 0; u < kRounds; u++)
+            res[u] = e[u] >= 0 ? (int)op.apply(pv[u], e[u], x[u], pr[u]) : 0;
+        append_results<Op, kRounds>(op, res, x, cnt, qn, st);
+    }
+}
+
+// kHops > 0 (thin graphs, persistent loops): after its share of the
+// frontier, a warp keeps expanding the near entries it has just produced,
+// up to kHops hops, before the grid-wide barrier.  Those entries are still
+// flushed to the next frontier as usual; the local expansion is
+// speculative extra work that Op::keep() (distance dropped since the last
+// expansion?) makes idempotent, so correctness never depends on it.
+template <class Op, int kHops = 0>
 __device__ __forceinline__ void expand_body(
     const Op &op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const int32_t *__restrict__ q, int64_t nq, int32_t *__restrict__ qn,
     uint2 *__restrict__ chunks, ExpandCounters *cnt, int vpw) {
     // vpw = frontier vertices per warp (32 normally; fewer for small
     // frontiers, so that every SM gets work)
-    using P = typename Op::Payload;
-    using Pr = typename Op::Probe;
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long scanned = 0;
     ExpandStage st = make_stage();
     for (int64_t base = warp * vpw; base < nq; base += nwarps * vpw) {
-        int64_t i = base + lane;
-        int32_t v = -1;
-        int64_t beg = 0, deg = 0;
-        P pay = P(0);
-        if ((int)lane < vpw && i < nq) {
-            v = q[i];
-            beg = off[v];
-            deg = off[v + 1] - beg;
-            pay = op.payload(v);
-            if constexpr (HasKeep<Op>::value) {
-                if (!op.keep(v, pay)) deg = 0;
+        const int64_t i = base + lane;
+        const int32_t v = ((int)lane < vpw && i < nq) ? q[i] : -1;
+        expand_batch(op, off, adj, v, qn, chunks, cnt, st, scanned);
+    }
+    if constexpr (kHops > 0) {
+        __shared__ int32_t s_local[kExpandBlock / 32][kStage];
+        int32_t *lq = s_local[threadIdx.x >> 5];
+        for (int hop = 0; hop < kHops && st.near.n > 0; hop++) {
+            const int nl = st.near.n;
+            for (int k = lane; k < nl; k += 32) lq[k] = st.near.buf[k];
+            __syncwarp();
+            st.near.flush(&cnt->next_size, qn);  // the global frontier gets them too
+            for (int b = 0; b < nl; b += 32) {
+                const int32_t v = b + (int)lane < nl ? lq[b + lane] : -1;
+                expand_batch(op, off, adj, v, qn, chunks, cnt, st, scanned);
             }
-        }
-        if (deg > kSplit) {  // hub row -> chunk work items
-            int64_t nch = (deg + kSplit - 1) / kSplit;
-            unsigned long long s = atomicAdd(&cnt->chunks, (unsigned long long)nch);
-            for (int64_t c = 0; c < nch; c++) chunks[s + c] = make_uint2((unsigned)v, (unsigned)c);
-            deg = 0;
-        }
-        int64_t incl = deg;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((int)lane >= o) incl += t;
-        }
-        const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
-        const int64_t excl = incl - deg;
-        scanned += total;
-        for (int64_t p0 = 0; p0 < total; p0 += 32 * kRounds) {
-            int64_t e[kRounds];
-            int32_t x[kRounds];
-            P pv[kRounds];
-            Pr pr[kRounds];
-#pragma unroll
-            for (int u = 0; u < kRounds; u++) {
-                const int64_t p = p0 + u * 32 + lane;
-                // owner = largest lane with excl <= p (always a lane with deg > 0)
-                int lo = 0;
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1) {
-                    int cand = lo + step;
-                    int64_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
-                    if (cand < 32 && ex <= p) lo = cand;
-                }
-                const int64_t ex = __shfl_sync(0xffffffffu, excl, lo);
-                const int64_t b0 = __shfl_sync(0xffffffffu, beg, lo);
-                pv[u] = __shfl_sync(0xffffffffu, pay, lo);
-                e[u] = p < total ? b0 + (p - ex) : -1;
-                x[u] = e[u] >= 0 ? __ldcs(adj + e[u]) : -1;  // streamed: evict first
-            }
-#pragma unroll
-            for (int u = 0; u < kRounds; u++)
-                if (e[u] >= 0) pr[u] = op.probe(e[u], x[u]);
-            int res[kRounds];
-#pragma unroll
-            for (int u = 0; u < kRounds; u++)
-                res[u] = e[u] >= 0 ? (int)op.apply(pv[u], e[u], x[u], pr[u]) : 0;
-            append_results<Op, kRounds>(op, res, x, cnt, qn, st);
+            __syncwarp();
         }
     }
     flush_stage(op, cnt, qn, st);

@@ -35,6 +35,7 @@ constexpr int kBlock = 256;
 constexpr int64_t kDeltaMul = 16;        // near-far step = kDeltaMul x mean weight
 constexpr int64_t kNearFarMaxAvgDeg = 8;  // near-far only when m <= 8 n
 constexpr int kPersistBlocksPerSm = 1;    // persistent near-far grid: blocks per SM
+constexpr int kNfHops = 8;                // warp-local continuation hops (persistent near-far)
 
 // Relaxation of sssp.sp:11-12 for one slot; payload = dist[v] at expansion.
 struct RelaxOp {
@@ -318,8 +319,8 @@ __global__ void __launch_bounds__(kExpandBlock) k_nf_persistent(
             if (nq > 0) {
                 NearFarOp op{dist, enq, last, weff, &L->cnt[cur].flag, L->far[L->fcur],
                              &L->far_n[L->fcur], L->fcap, L->T, L->it};
-                expand_body(op, off, adj, L->q[cur], nq, L->q[cur ^ 1], nullptr, &L->cnt[cur],
-                            expand_vpw(nq, warps));
+                expand_body<NearFarOp, kNfHops>(op, off, adj, L->q[cur], nq, L->q[cur ^ 1],
+                                                 nullptr, &L->cnt[cur], expand_vpw(nq, warps));
             }
         }
         grid.sync();
