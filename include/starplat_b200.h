@@ -189,6 +189,14 @@ int sp_bc(sp_graph *g, const int32_t *srcs, int64_t nsrc, unsigned flags,
  * in [v0, v1); directed graphs -- the program's middle vertex v in [v0, v1). */
 int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_stats *st);
 
+/* Generic forall/reduction (corpus/programs/reduction.sp:5-10 and programs
+ * of its shape): for every v, sum an int64 node property over N(v)
+ * (reverse = 0, g.neighbors) or over nodesTo(v) (reverse = 1); exact.
+ * prop == NULL: every property is 1 (attachNodeProperty(prop = 1)).
+ * per_vertex[n] (may be NULL) gets the row sums, *total their sum. */
+int sp_neighbor_sum(sp_graph *g, const int64_t *prop, int mem, int reverse,
+                    int64_t *per_vertex, int64_t *total, sp_stats *st);
+
 #ifdef __cplusplus
 }
 #endif

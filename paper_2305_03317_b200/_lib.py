@@ -83,6 +83,7 @@ SIGNATURES = {
     "sp_pagerank_block_init": (_int, [_p, _i64, _i64, _p, _p]),
     "sp_bc": (_int, [_p, _p, _i64, _u, _p, _p, _p, _int, _p]),
     "sp_tc": (_int, [_p, _i64, _i64, _p, _p]),
+    "sp_neighbor_sum": (_int, [_p, _p, _int, _int, _p, _p, _p]),
 }
 
 _lib = None

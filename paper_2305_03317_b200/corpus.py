@@ -27,6 +27,7 @@ FINGERPRINTS = {
     "pr": "a33949c2ad8e09dc92baa40f5c8346ea342991540c9fd4e92d36dce2c2b48cdc",
     "bc": "fe91f9b5fbe40d6a1d2a0b614d162bfa9b09470fea4e1c9ce877ccfe999e7172",
     "tc": "28f098b022be174a0cb41954159d8d5a3d04b6bb473db20181a9ab7c7dca9aaa",
+    "reduction": "08246c459994266f33ec2ab393b539a180995d24fc199b3e6e981ad69cd5325f",
 }
 
 
@@ -54,8 +55,10 @@ PR = Program("pr", "Compute_PR", (("g", "Graph"), ("damping", "double"),
                                   ("epsilon", "double"), ("maxIter", "int")), "converged")
 BC = Program("bc", "Compute_BC", (("g", "Graph"), ("sourceSet", "SetN")), None)
 TC = Program("tc", "Compute_TC", (("g", "Graph"),), None)
+# reduction.sp: the generic forall / neighbour-reduction shape (sp_forall.cu)
+REDUCTION = Program("reduction", "Sum_Neighbor_Props", (("g", "Graph"),), None)
 
-BY_KEY = {p.key: p for p in (SSSP, SSSP_PULL, PR, BC, TC)}
+BY_KEY = {p.key: p for p in (SSSP, SSSP_PULL, PR, BC, TC, REDUCTION)}
 _BY_PRINT = {v: BY_KEY[k] for k, v in FINGERPRINTS.items()}
 
 
@@ -84,6 +87,6 @@ def identify(tp, function: str | None = None) -> Program:
     if prog is None:
         raise UnsupportedProgramError(
             f"function '{getattr(fn, 'name', '?')}' is not one of the corpus programs "
-            "(sssp, sssp_pull, pr, bc, tc) that the B200 backend executes; "
+            "(sssp, sssp_pull, pr, bc, tc, reduction) that the B200 backend executes; "
             "there is no CPU fallback")
     return prog

@@ -245,6 +245,15 @@ def run(tp, g, args: dict, function: str | None = None,
         env.node_props = {"bc": bc}
         if len(srcs):  # sigma/delta are attached inside the source loop (bc.sp:5-7)
             env.node_props.update(sigma=sigma, delta=delta)
+    elif prog.key == "reduction":
+        # reduction.sp:2-10: prop = 1 everywhere; accum += nbr.prop over every
+        # (v, nbr) slot (the inner `count` is local, not in the result)
+        tot = C.c_int64()
+        rc = L.sp_neighbor_sum(dg.handle, None, _lib.SP_MEM_HOST, 0, None, C.byref(tot),
+                               C.byref(st))
+        _raise_for(rc, E, None, cap, None)
+        env.node_props = {"prop": np.ones(n, dtype=np.int64)}
+        env.scalars = {"accum": int(tot.value)}
     elif prog.key == "tc":
         cnt = C.c_uint64()
         rc = L.sp_tc(dg.handle, 0, n, C.byref(cnt), C.byref(st))

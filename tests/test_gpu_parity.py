@@ -523,3 +523,38 @@ def test_run_adopts_reference_graph_objects(case):
                    deterministic=True)
         assert r.env.node_props["rank"].tobytes() == z["pr_rank"].tobytes()
     assert sp.run(corpus.TC, tg, {}).env.scalars["triangle_count"] == int(z["tc"])
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_reduction_program(case, graphs):
+    """reduction.sp (the generic forall / neighbour-reduction shape):
+    prop = 1 everywhere, accum = number of CSR slots (the reference's
+    result, checked against the golden CSR)."""
+    z, g = graphs(case)
+    r = sp.run(corpus.REDUCTION, g, {})
+    assert r.env.scalars == {"accum": len(z["csr_adj"])}
+    assert r.env.node_props["prop"].tolist() == [1] * int(z["n"])
+
+
+@pytest.mark.parametrize("directed", [True, False])
+@pytest.mark.parametrize("reverse", [0, 1])
+def test_neighbor_sum_generic(directed, reverse):
+    """The generic neighbour reduction on an arbitrary int64 property,
+    over g.neighbors (reverse=0) or g.nodesTo (reverse=1), vs numpy."""
+    import ctypes as C
+    from paper_2305_03317_b200 import _lib
+    u, v, w, n = gen.rmat(12, 16, seed=31, undirected=not directed)
+    g = sp.from_arrays(u, v, w, directed=directed, n=n)
+    prop = np.random.default_rng(3).integers(-10 ** 12, 10 ** 12, n).astype(np.int64)
+    per = np.empty(n, dtype=np.int64)
+    tot = C.c_int64()
+    rc = _lib.lib().sp_neighbor_sum(g.handle, prop.ctypes.data_as(C.c_void_p), _lib.SP_MEM_HOST,
+                                    reverse, per.ctypes.data_as(C.c_void_p), C.byref(tot), None)
+    assert rc == 0
+    off = np.asarray(g.rev_offsets if reverse else g.offsets)
+    col = np.asarray(g.rev_adj if reverse else g.adj)
+    rows = np.repeat(np.arange(n), np.diff(off))
+    want = np.zeros(n, dtype=np.int64)
+    np.add.at(want, rows, prop[col])
+    np.testing.assert_array_equal(per, want)
+    assert tot.value == int(want.sum())

@@ -82,8 +82,9 @@ def test_oracle_not_imported_by_product():
 def test_identify_descriptors():
     assert corpus.identify(corpus.SSSP) is corpus.SSSP
     assert corpus.identify("pr") is corpus.PR
+    assert corpus.identify("reduction") is corpus.REDUCTION
     with pytest.raises(UnsupportedProgramError):
-        corpus.identify("reduction")
+        corpus.identify("bfs")
 
 
 @pytest.mark.skipif(not HAVE_REF, reason="reference not importable here")
@@ -92,7 +93,7 @@ def test_fingerprints_rederive_from_reference():
     from trident.parser import parse_source
     from trident.sema import analyze
     progs = os.path.join(REF, "trident", "corpus", "programs")
-    for key in ("sssp", "sssp_pull", "pr", "bc", "tc"):
+    for key in ("sssp", "sssp_pull", "pr", "bc", "tc", "reduction"):
         tp = analyze(parse_source(open(os.path.join(progs, key + ".sp")).read()))
         assert corpus.identify(tp) is corpus.BY_KEY[key]
         assert corpus.fingerprint(tp.function()) == corpus.FINGERPRINTS[key]
@@ -103,7 +104,8 @@ def test_fingerprints_rederive_from_reference():
     tp = analyze(parse_source(src.replace("triangle_count += 1", "triangle_count += 2")))
     with pytest.raises(UnsupportedProgramError):
         corpus.identify(tp)
-    tp = analyze(parse_source(open(os.path.join(progs, "reduction.sp")).read()))
+    red = open(os.path.join(progs, "reduction.sp")).read()
+    tp = analyze(parse_source(red.replace("accum += nbr.prop", "accum += 2 * nbr.prop")))
     with pytest.raises(UnsupportedProgramError):
         corpus.identify(tp)
     with pytest.raises(KeyError):

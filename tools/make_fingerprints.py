@@ -24,7 +24,7 @@ def fingerprint(fn):
     return hashlib.sha256(s.encode()).hexdigest()
 
 
-for name in ("sssp", "sssp_pull", "pr", "bc", "tc"):
+for name in ("sssp", "sssp_pull", "pr", "bc", "tc", "reduction"):
     p = os.path.join(REF, "trident", "corpus", "programs", name + ".sp")
     tp = analyze(parse_source(open(p).read()))
     print(f'    "{name}": "{fingerprint(tp.function())}",')
