@@ -37,7 +37,8 @@ using namespace sp;
 namespace {
 
 constexpr int64_t kBcHub = 8192;  // rows longer than this take the CTA fold
-constexpr int kBcWorkers = 4;     // concurrent sources (host threads/streams), fast mode
+constexpr int kBcWorkers = 4;     // concurrent sources (host threads/streams), per-source fast path
+constexpr int kBbWorkers = 2;     // concurrent source batches, batched fast path
 
 // Per-vertex record, 16 bytes: level (int32) and, in fast mode, the child
 // coefficient coef[w] = (1 + delta[w]) / sigma[w] (written when delta[w] is
@@ -95,8 +96,8 @@ struct SigmaFold {  // bc.sp:10-12 over reverse-CSR slots (deterministic mode)
     double *__restrict__ sigma;
     int parent_level;
     __device__ __forceinline__ double payload(int32_t) const { return 0.0; }
-    __device__ __forceinline__ double term(double, int64_t k) const {
-        const int32_t u = radj[k];
+    __device__ __forceinline__ int32_t key(int64_t k) const { return radj[k]; }
+    __device__ __forceinline__ double term(double, int32_t u) const {
         return __ldg(lvl(level, u)) == parent_level ? sigma[u] : 0.0;
     }
     __device__ __forceinline__ void finish(int32_t v, double s) const { sigma[v] = s; }
@@ -111,8 +112,8 @@ struct DeltaFold {  // bc.sp:14-19 over CSR slots (deterministic mode: exact for
     int child_level;
     int32_t src;
     __device__ __forceinline__ double payload(int32_t v) const { return sigma[v]; }
-    __device__ __forceinline__ double term(double sv, int64_t e) const {
-        const int32_t w = adj[e];
+    __device__ __forceinline__ int32_t key(int64_t e) const { return adj[e]; }
+    __device__ __forceinline__ double term(double sv, int32_t w) const {
         if (__ldg(lvl(level, w)) != child_level) return 0.0;
         return __dmul_rn(__ddiv_rn(sv, sigma[w]), __dadd_rn(1.0, delta[w]));
     }
@@ -133,8 +134,8 @@ struct DeltaFoldFast {
     int child_level;
     int32_t src;
     __device__ __forceinline__ double payload(int32_t v) const { return sigma[v]; }
-    __device__ __forceinline__ double term(double sv, int64_t e) const {
-        const int32_t w = __ldcs(adj + e);
+    __device__ __forceinline__ int32_t key(int64_t e) const { return __ldcs(adj + e); }
+    __device__ __forceinline__ double term(double sv, int32_t w) const {
         const int4 r = __ldg(reinterpret_cast<const int4 *>(vs) + w);
         if (r.x != child_level) return 0.0;
         return __dmul_rn(sv, __hiloint2double(r.w, r.z));
@@ -167,7 +168,7 @@ __global__ void k_root(int32_t *level, double *sigma, int32_t *queue, int32_t s)
 // One worker: a stream (its thread's), its own scratch and bc partial, and
 // the sources srcs[first], srcs[first + stride], ... in list order.
 struct BcWorker {
-    int64_t levels = 0, scanned = 0, reached = 0, launches = 0;
+    int64_t levels = 0, scanned = 0, reached = 0, launches = 0, pull_steps = 0;
     int rc = SP_OK;
     char err[512] = "";
 };
@@ -180,11 +181,12 @@ int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
     const int64_t n = g->n;
     const int64_t nsrc = (int64_t)srcs.size();
     const int sms = num_sms(c.device);
-    int32_t *level, *queue, *hubs, *reg_v, *reg_nch, *item_reg;
+    int32_t *level, *queue, *hubs, *reg_v, *reg_nch;
+    uint4 *items;
     int64_t *reg_base;
     double *csum;
     double *sigma, *delta, *bc;
-    uint2 *chunks;
+    ChunkItem *chunks;
     ExpandCounters *cnt;
     unsigned long long *nhubs;
     SP_TRY(c.alloc(&level, kVs * n));  // 16-byte (level, coef) records
@@ -194,7 +196,7 @@ int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
     SP_TRY(c.alloc(&reg_v, n));
     SP_TRY(c.alloc(&reg_nch, n));
     SP_TRY(c.alloc(&reg_base, n));
-    SP_TRY(c.alloc(&item_reg, ccap));
+    SP_TRY(c.alloc(&items, ccap));
     SP_TRY(c.alloc(&csum, ccap));
     SP_TRY(c.alloc(&sigma, n));
     SP_TRY(c.alloc(&delta, n));
@@ -202,7 +204,7 @@ int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
     SP_TRY(c.alloc(&chunks, expand_chunk_capacity(g->m)));
     SP_TRY(c.alloc(&cnt, 1));
     SP_TRY(c.alloc(&nhubs, 3));
-    const FoldLists fl{hubs, nhubs, FoldChunks{reg_v, reg_base, reg_nch, item_reg, csum, nullptr}};
+    const FoldLists fl{hubs, nhubs, FoldChunks{reg_v, reg_base, reg_nch, items, csum, nullptr}};
     c.persist(level, kVs * n * sizeof(int32_t));  // BFS/fold probes hit the records at random
     SP_CUDA(cudaMemsetAsync(bc, 0, n * sizeof(double), c.stream));
     SP_CUDA(cudaMemsetAsync(sigma, 0, n * sizeof(double), c.stream));
@@ -287,6 +289,639 @@ int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
     return SP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Batched sources (fast mode).  kLanes sources run one BFS together: vertex
+// state is lane-major per vertex -- level int32[kLanes] (one 32-byte sector),
+// sigma and coef f64[kLanes] -- so one random level read answers "which
+// sources see this neighbour at the next level" for all of them, and the
+// delta fold reads a neighbour's coef only for the lanes that match.  The
+// per-source arithmetic is unchanged: sigma by exact integer atomics during
+// discovery, delta_v = sigma_v * sum(coef_w) over children, coef_v =
+// (1 + delta_v) / sigma_v, bc_v += delta_v / 2 for v != src.  A vertex is
+// queued once per distinct depth it has across the lanes (stamp[v] = last
+// depth queued), so level d's queue holds every vertex with some lane at d.
+constexpr int kLanes = 8;
+constexpr int kBbShort = 32;     // rows up to this length: one thread, sequential
+constexpr int kBbSplit = 256;    // longer rows: 256-slot chunks, one warp each
+constexpr double kBbPullRatio = 4.0;  // direction choice, see bc_run_batches
+
+struct BatchSrc {
+    int32_t s[kLanes];  // -1: unused lane
+};
+
+// A vertex's kLanes levels (one 32-byte sector) / 4 of its f64 lanes, each
+// read with ONE 256-bit load (LDG.256): a random 32-byte read costs one L1
+// wavefront instead of two (int4 x 2) or eight (scalar lanes).
+struct Lev8 {
+    int x[kLanes];
+};
+__device__ __forceinline__ Lev8 load_lev(const int32_t *lev, int32_t v) {  // L2 (.cg)
+    Lev8 l;
+    asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(l.x[0]), "=r"(l.x[1]), "=r"(l.x[2]), "=r"(l.x[3]), "=r"(l.x[4]),
+                   "=r"(l.x[5]), "=r"(l.x[6]), "=r"(l.x[7])
+                 : "l"(lev + kLanes * (int64_t)v));
+    return l;
+}
+__device__ __forceinline__ Lev8 load_lev_ro(const int32_t *lev, int32_t v) {  // read-only path
+    Lev8 l;
+    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(l.x[0]), "=r"(l.x[1]), "=r"(l.x[2]), "=r"(l.x[3]), "=r"(l.x[4]), "=r"(l.x[5]),
+          "=r"(l.x[6]), "=r"(l.x[7])
+        : "l"(lev + kLanes * (int64_t)v));
+    return l;
+}
+__device__ __forceinline__ void load_f64x4_ro(const double *p, double (&o)[4]) {
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+        : "l"(p));
+}
+__device__ __forceinline__ unsigned lanes_eq(const Lev8 &l, int d) {
+    unsigned m = 0;
+#pragma unroll
+    for (int s = 0; s < kLanes; s++) m |= (unsigned)(l.x[s] == d) << s;
+    return m;
+}
+// acc[s] += coef_w[s] for the lanes in m (m != 0): two 256-bit loads
+__device__ __forceinline__ void add_lanes(const double *cw, unsigned m, double (&acc)[kLanes]) {
+    double c[kLanes];
+    if (m & 0x0Fu) load_f64x4_ro(cw, *reinterpret_cast<double(*)[4]>(c));
+    if (m & 0xF0u) load_f64x4_ro(cw + 4, *reinterpret_cast<double(*)[4]>(c + 4));
+#pragma unroll
+    for (int s = 0; s < kLanes; s++)
+        if (m >> s & 1u) acc[s] = __dadd_rn(acc[s], c[s]);
+}
+
+// Discovery + sigma push for all lanes of level `cur` in one pass.
+struct BatchDiscoverOp {
+    using Payload = unsigned long long;  // v | lanes at `cur` << 32
+    using Probe = unsigned;              // lanes unvisited | lanes at `next` << 8
+    int32_t *__restrict__ lev;
+    double *__restrict__ sig;
+    int32_t *__restrict__ stamp;
+    int cur, next;
+    __device__ __forceinline__ Payload payload(int32_t v) const {
+        return (unsigned)v | (Payload)lanes_eq(load_lev_ro(lev, v), cur) << 32;
+    }
+    __device__ __forceinline__ unsigned probe(int64_t, int32_t x) const {
+        const Lev8 l = load_lev(lev, x);
+        return lanes_eq(l, -1) | lanes_eq(l, next) << 8;
+    }
+    __device__ __forceinline__ bool apply(Payload pay, int64_t, int32_t x, unsigned pr) const {
+        unsigned act = (unsigned)(pay >> 32) & (pr | pr >> 8) & 0xFFu;
+        if (!act) return false;
+        const int64_t v8 = kLanes * (int64_t)(unsigned)pay, x8 = kLanes * (int64_t)x;
+        bool won = false;
+        do {
+            const int s = __ffs(act) - 1;
+            act &= act - 1;
+            if (pr >> s & 1u) {
+                const int old = atomicCAS(lev + x8 + s, -1, next);
+                if (old == -1) won = true;
+                else if (old != next) continue;
+            }
+            atomicAdd(sig + x8 + s, __ldg(sig + v8 + s));
+        } while (act);
+        return won && atomicMax(stamp + x, next) < next;
+    }
+};
+
+__global__ void k_bb_root(int32_t *lev, double *sig, int32_t *stamp, int32_t *queue, BatchSrc b) {
+    int k = 0;
+    for (int s = 0; s < kLanes; s++) {
+        const int32_t v = b.s[s];
+        if (v < 0) continue;
+        lev[kLanes * (int64_t)v + s] = 0;
+        sig[kLanes * (int64_t)v + s] = 1.0;
+        if (stamp[v] != 0) {
+            stamp[v] = 0;
+            queue[k++] = v;
+        }
+    }
+}
+
+struct BatchFold {
+    const int64_t *__restrict__ off;
+    const int32_t *__restrict__ adj;
+    const int32_t *__restrict__ lev;
+    const double *__restrict__ sig;
+    double *__restrict__ coef;
+    double *__restrict__ bc;
+    double *__restrict__ dlast;  // delta of lane `last` (or null)
+    int last;
+    BatchSrc src;
+    int d;
+    // delta/coef/bc of v's lanes `act` (at depth d) from their child sums
+    __device__ __forceinline__ void finish(int32_t v, unsigned act, const double (&acc)[kLanes]) const {
+        const int64_t v8 = kLanes * (int64_t)v;
+        double add = 0.0;
+        bool any = false;
+#pragma unroll
+        for (int s = 0; s < kLanes; s++) {
+            if (!(act >> s & 1u)) continue;
+            const double sv = sig[v8 + s];
+            const double dv = __dmul_rn(sv, acc[s]);
+            coef[v8 + s] = __ddiv_rn(__dadd_rn(1.0, dv), sv);
+            if (s == last && dlast) dlast[v] = dv;
+            if (v != src.s[s]) {
+                add = __dadd_rn(add, __ddiv_rn(dv, 2.0));
+                any = true;
+            }
+        }
+        if (any) bc[v] = __dadd_rn(bc[v], add);
+    }
+    // add the coef of w's lanes at d+1 among `act` to acc
+    __device__ __forceinline__ void term(int32_t w, unsigned act, double (&acc)[kLanes]) const {
+        const unsigned m = lanes_eq(load_lev_ro(lev, w), d + 1) & act;
+        if (m) add_lanes(coef + kLanes * (int64_t)w, m, acc);
+    }
+};
+
+// Long rows: registered (vertex, first chunk, chunk count), one work item
+// per 256-slot chunk; a chunk's per-lane sums go to csum[item] and the
+// row's finish adds them in chunk order (fixed shape: the batched path is
+// deterministic run to run, like the per-source one).
+struct BbChunks {
+    int32_t *reg_v;              // long rows of this level
+    int64_t *reg_base;           // first chunk item
+    int32_t *reg_nch;            // chunk count
+    uint4 *items;                // {reg index, first slot lo, hi, count}
+    double *csum;                // [item][kLanes] chunk sums
+    unsigned long long *counts;  // [0] long rows, [1] chunks
+};
+
+__device__ __forceinline__ void bb_register(const BbChunks &ck, int64_t r, int32_t v, int64_t r0,
+                                            int64_t deg) {
+    ck.reg_v[r] = v;
+    const int nch = (int)((deg + kBbSplit - 1) / kBbSplit);
+    const int64_t b0 = (int64_t)atomicAdd(&ck.counts[1], (unsigned long long)nch);
+    ck.reg_base[r] = b0;
+    ck.reg_nch[r] = nch;
+    for (int c = 0; c < nch; c++) {
+        const int64_t s0 = r0 + (int64_t)c * kBbSplit;
+        const int64_t len = min((int64_t)kBbSplit, r0 + deg - s0);
+        ck.items[b0 + c] = make_uint4((unsigned)r, (unsigned)(uint64_t)s0,
+                                      (unsigned)((uint64_t)s0 >> 32), (unsigned)len);
+    }
+}
+
+// warp sums of acc per lane in `act`, stored as the chunk's partials
+__device__ __forceinline__ void bb_store_chunk(const BbChunks &ck, int64_t k, unsigned act,
+                                               const double (&acc)[kLanes]) {
+    double mine = 0.0;
+#pragma unroll
+    for (int s = 0; s < kLanes; s++) {
+        double x = 0.0;
+        if (act >> s & 1u) {  // warp-uniform
+            x = acc[s];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+        }
+        if ((int)lane_id() == s) mine = x;
+    }
+    if (lane_id() < kLanes) ck.csum[kLanes * k + lane_id()] = mine;
+}
+
+// row r's lane sums: its chunks' partials in chunk order
+__device__ __forceinline__ void bb_row_sums(const BbChunks &ck, int64_t r, double (&acc)[kLanes]) {
+    const int64_t b0 = ck.reg_base[r];
+    const int nch = ck.reg_nch[r];
+#pragma unroll
+    for (int s = 0; s < kLanes; s++) acc[s] = 0.0;
+    for (int c = 0; c < nch; c++) {
+        double p[kLanes];
+        load_f64x4_ro(ck.csum + kLanes * (b0 + c), *reinterpret_cast<double(*)[4]>(p));
+        load_f64x4_ro(ck.csum + kLanes * (b0 + c) + 4, *reinterpret_cast<double(*)[4]>(p + 4));
+#pragma unroll
+        for (int s = 0; s < kLanes; s++) acc[s] = __dadd_rn(acc[s], p[s]);
+    }
+}
+
+// Level d's rows: short rows folded by one thread; long rows registered and
+// cut into chunks.  Deepest level (leaf = true): no children, coef = 1/sigma.
+__global__ void __launch_bounds__(256) k_bb_rows(BatchFold f, const int32_t *__restrict__ q,
+                                                 int64_t nq, bool leaf, BbChunks ck) {
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nq;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        int32_t v = -1;
+        unsigned act = 0;
+        int64_t r0 = 0, deg = 0;
+        if (i < nq) {
+            v = q[i];
+            act = lanes_eq(load_lev_ro(f.lev, v), f.d);
+            r0 = f.off[v];
+            deg = leaf ? 0 : f.off[v + 1] - r0;
+        }
+        const bool longrow = deg > kBbShort;
+        const int64_t r = warp_append(longrow, &ck.counts[0]);
+        if (longrow) {
+            bb_register(ck, r, v, r0, deg);
+        } else if (v >= 0) {
+            double acc[kLanes];
+#pragma unroll
+            for (int s = 0; s < kLanes; s++) acc[s] = 0.0;
+            for (int64_t e = r0; e < r0 + deg; e += 4) {
+                int32_t w[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) w[u] = e + u < r0 + deg ? __ldg(f.adj + e + u) : -1;
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (w[u] >= 0) f.term(w[u], act, acc);
+            }
+            f.finish(v, act, acc);
+        }
+    }
+}
+
+// One warp per chunk: lanes take slots j*32 + lane, then a fixed-shape warp
+// reduction per source lane into the chunk's partials.
+__global__ void __launch_bounds__(256) k_bb_chunks(BatchFold f, BbChunks ck) {
+    const unsigned lane = lane_id();
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nitems = (int64_t)__ldcg(&ck.counts[1]);
+    for (int64_t k = warp; k < nitems; k += nwarps) {
+        const uint4 it = ck.items[k];
+        const int32_t v = ck.reg_v[it.x];
+        const unsigned act = lanes_eq(load_lev_ro(f.lev, v), f.d);
+        const int64_t s0 = (int64_t)(((uint64_t)it.z << 32) | it.y);
+        int32_t w[kBbSplit / 32];
+#pragma unroll
+        for (int j = 0; j < kBbSplit / 32; j++) {
+            const unsigned p = j * 32 + lane;
+            w[j] = p < it.w ? __ldcs(f.adj + s0 + p) : -1;
+        }
+        double acc[kLanes];
+#pragma unroll
+        for (int s = 0; s < kLanes; s++) acc[s] = 0.0;
+        unsigned m[kBbSplit / 32];
+#pragma unroll
+        for (int j = 0; j < kBbSplit / 32; j++)
+            m[j] = w[j] >= 0 ? lanes_eq(load_lev_ro(f.lev, w[j]), f.d + 1) & act : 0u;
+#pragma unroll
+        for (int j = 0; j < kBbSplit / 32; j++)
+            if (m[j]) add_lanes(f.coef + kLanes * (int64_t)w[j], m[j], acc);
+        bb_store_chunk(ck, k, act, acc);
+    }
+}
+
+__global__ void k_bb_finish(BatchFold f, BbChunks ck) {
+    const int64_t nreg = (int64_t)__ldcg(&ck.counts[0]);
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nreg;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = ck.reg_v[r];
+        const unsigned act = lanes_eq(load_lev_ro(f.lev, v), f.d);
+        double acc[kLanes];
+        bb_row_sums(ck, r, acc);
+        f.finish(v, act, acc);
+    }
+}
+
+// Bottom-up (pull) form of one discovery step, for the large middle levels
+// (direction optimisation): every vertex w with a lane still unvisited sums
+// sigma over its in-neighbours at level d for those lanes, and the lanes
+// with a non-zero sum join level d+1 -- written by w's owner alone, so no
+// CAS and no sigma atomics.  Sums of path counts are exact in any order, so
+// sigma is identical to the push form's.  Concurrent readers of lev[w] see
+// -1 or d+1, never d, so the in-place update is race-free.
+struct BatchPull {
+    const int64_t *__restrict__ roff;
+    const int32_t *__restrict__ radj;
+    int32_t *__restrict__ lev;
+    double *__restrict__ sig;
+    int32_t *__restrict__ stamp;
+    int32_t *__restrict__ qn;   // next level's queue
+    ExpandCounters *cnt;        // next_size
+    int d;
+    __device__ __forceinline__ void term(int32_t v, unsigned pm, double (&acc)[kLanes]) const {
+        const unsigned m = lanes_eq(load_lev_ro(lev, v), d) & pm;
+        if (m) add_lanes(sig + kLanes * (int64_t)v, m, acc);
+    }
+    // lanes of w with a parent join level d+1; true => w is queued
+    __device__ __forceinline__ bool finish(int32_t w, unsigned pm,
+                                           const double (&acc)[kLanes]) const {
+        const int64_t w8 = kLanes * (int64_t)w;
+        bool any = false;
+#pragma unroll
+        for (int s = 0; s < kLanes; s++)
+            if ((pm >> s & 1u) && acc[s] != 0.0) {
+                lev[w8 + s] = d + 1;
+                sig[w8 + s] = acc[s];
+                any = true;
+            }
+        if (any) stamp[w] = d + 1;
+        return any;
+    }
+};
+
+__global__ void __launch_bounds__(256) k_bb_pull_rows(BatchPull f, int64_t n, BbChunks ck) {
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        unsigned pm = 0;
+        int64_t r0 = 0, deg = 0;
+        if (i < n) {
+            pm = lanes_eq(load_lev_ro(f.lev, (int32_t)i), -1);
+            if (pm) {
+                r0 = f.roff[i];
+                deg = f.roff[i + 1] - r0;
+            }
+        }
+        const bool longrow = deg > kBbShort;
+        const int64_t r = warp_append(longrow, &ck.counts[0]);
+        bool push = false;
+        if (longrow) {
+            bb_register(ck, r, (int32_t)i, r0, deg);
+        } else if (deg > 0) {
+            double acc[kLanes];
+#pragma unroll
+            for (int s = 0; s < kLanes; s++) acc[s] = 0.0;
+            for (int64_t e = r0; e < r0 + deg; e += 4) {
+                int32_t v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) v[u] = e + u < r0 + deg ? __ldg(f.radj + e + u) : -1;
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (v[u] >= 0) f.term(v[u], pm, acc);
+            }
+            push = f.finish((int32_t)i, pm, acc);
+        }
+        const int64_t slot = warp_append(push, &f.cnt->next_size);
+        if (push) f.qn[slot] = (int32_t)i;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bb_pull_chunks(BatchPull f, BbChunks ck) {
+    const unsigned lane = lane_id();
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nitems = (int64_t)__ldcg(&ck.counts[1]);
+    for (int64_t k = warp; k < nitems; k += nwarps) {
+        const uint4 it = ck.items[k];
+        const int32_t w = ck.reg_v[it.x];
+        const unsigned pm = lanes_eq(load_lev_ro(f.lev, w), -1);
+        const int64_t s0 = (int64_t)(((uint64_t)it.z << 32) | it.y);
+        int32_t v[kBbSplit / 32];
+#pragma unroll
+        for (int j = 0; j < kBbSplit / 32; j++) {
+            const unsigned p = j * 32 + lane;
+            v[j] = p < it.w ? __ldcs(f.radj + s0 + p) : -1;
+        }
+        unsigned m[kBbSplit / 32];
+#pragma unroll
+        for (int j = 0; j < kBbSplit / 32; j++)
+            m[j] = v[j] >= 0 ? lanes_eq(load_lev_ro(f.lev, v[j]), f.d) & pm : 0u;
+        double acc[kLanes];
+#pragma unroll
+        for (int s = 0; s < kLanes; s++) acc[s] = 0.0;
+#pragma unroll
+        for (int j = 0; j < kBbSplit / 32; j++)
+            if (m[j]) add_lanes(f.sig + kLanes * (int64_t)v[j], m[j], acc);
+        bb_store_chunk(ck, k, pm, acc);
+    }
+}
+
+__global__ void k_bb_pull_finish(BatchPull f, BbChunks ck) {
+    const int64_t nreg = (int64_t)__ldcg(&ck.counts[0]);
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nreg;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = base + threadIdx.x;
+        bool push = false;
+        int32_t w = -1;
+        if (r < nreg) {
+            w = ck.reg_v[r];
+            const unsigned pm = lanes_eq(load_lev(f.lev, w), -1);
+            double acc[kLanes];
+            bb_row_sums(ck, r, acc);
+            push = f.finish(w, pm, acc);
+        }
+        const int64_t slot = warp_append(push, &f.cnt->next_size);
+        if (push) f.qn[slot] = w;
+    }
+}
+
+// Direction choice for the next step: out[0] = out-slots of the new
+// frontier (push cost), out[1] = in-slots of vertices with an unvisited
+// lane (pull cost).
+__global__ void k_bb_plan(const int32_t *__restrict__ lev, const int64_t *__restrict__ off,
+                          const int64_t *__restrict__ roff, const int32_t *__restrict__ qn,
+                          const ExpandCounters *cnt, int64_t n, unsigned long long *out) {
+    const int64_t nq = (int64_t)cnt->next_size;
+    unsigned long long fe = 0, pe = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < nq) {
+            const int32_t v = qn[i];
+            fe += off[v + 1] - off[v];
+        }
+        if (lanes_eq(load_lev_ro(lev, (int32_t)i), -1)) pe += roff[i + 1] - roff[i];
+    }
+    fe = warp_sum(fe);
+    pe = warp_sum(pe);
+    if (lane_id() == 0) {
+        if (fe) atomicAdd(out, fe);
+        if (pe) atomicAdd(out + 1, pe);
+    }
+}
+
+// per batch: reached (vertex, source) pairs, their out-slots, levels per lane
+__global__ void k_bb_stats(const int32_t *__restrict__ lev, const int64_t *__restrict__ off,
+                           int64_t n, unsigned long long *out) {
+    unsigned long long reached = 0, slots = 0;
+    unsigned lmax[kLanes];
+#pragma unroll
+    for (int s = 0; s < kLanes; s++) lmax[s] = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t *l = lev + kLanes * v;
+        const int64_t deg = off[v + 1] - off[v];
+#pragma unroll
+        for (int s = 0; s < kLanes; s++)
+            if (l[s] >= 0) {
+                reached++;
+                slots += deg;
+                lmax[s] = max(lmax[s], (unsigned)l[s] + 1);
+            }
+    }
+    reached = warp_sum(reached);
+    slots = warp_sum(slots);
+    if (lane_id() == 0) {
+        if (reached) atomicAdd(out, reached);
+        if (slots) atomicAdd(out + 1, slots);
+    }
+#pragma unroll
+    for (int s = 0; s < kLanes; s++) {
+        unsigned x = lmax[s];
+        for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+        if (lane_id() == 0 && x) atomicMax(reinterpret_cast<unsigned *>(out + 2) + s, x);
+    }
+}
+
+__global__ void k_bb_lane_out(const double *__restrict__ sig, int lane, int64_t n, double *out) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        out[v] = sig[kLanes * v + lane];
+}
+
+// One worker over batches first, first + stride, ... of kLanes sources each
+// (sources in list order).  Same contract as bc_run_sources (fast mode).
+int bc_run_batches(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first, int64_t stride,
+                   double *bc_dst, int bc_mem, bool bc_accumulate_only, double *sigma_out,
+                   double *delta_out, int mem, BcWorker &wk) {
+    Call c;
+    SP_TRY(c.begin(g->device));
+    const int64_t n = g->n;
+    const int64_t nsrc = (int64_t)srcs.size();
+    const int64_t nb = (nsrc + kLanes - 1) / kLanes;
+    const int sms = num_sms(c.device);
+    int32_t *lev, *stamp, *queue, *reg_v, *reg_nch;
+    int64_t *reg_base;
+    double *sig, *coef, *bc, *csum, *dlast = nullptr;
+    uint4 *items;
+    ChunkItem *chunks;
+    ExpandCounters *cnt;
+    unsigned long long *counts;
+    const int64_t qcap = kLanes * n;
+    SP_TRY(c.alloc(&lev, kLanes * n));
+    SP_TRY(c.alloc(&sig, kLanes * n));
+    SP_TRY(c.alloc(&coef, kLanes * n));
+    const int64_t icap = g->m / kBbSplit + n + 1;  // chunk items per level
+    SP_TRY(c.alloc(&stamp, n));
+    SP_TRY(c.alloc(&queue, qcap));
+    SP_TRY(c.alloc(&reg_v, n));
+    SP_TRY(c.alloc(&reg_nch, n));
+    SP_TRY(c.alloc(&reg_base, n));
+    SP_TRY(c.alloc(&items, icap));
+    SP_TRY(c.alloc(&csum, kLanes * icap));
+    SP_TRY(c.alloc(&bc, n));
+    SP_TRY(c.alloc(&chunks, expand_chunk_capacity(g->m)));
+    SP_TRY(c.alloc(&cnt, 1));
+    SP_TRY(c.alloc(&counts, 2 + kLanes / 2 + 2));
+    if (delta_out) SP_TRY(c.alloc(&dlast, n));
+    const BbChunks ck{reg_v, reg_base, reg_nch, items, csum, counts};
+    c.persist(lev, kLanes * n * sizeof(int32_t));  // the per-slot probe target
+    SP_CUDA(cudaMemsetAsync(bc, 0, n * sizeof(double), c.stream));
+    ExpandCounters *hc = nullptr;
+    SP_TRY(c.host_as(&hc));
+    // the call's pinned block: counters at 0, batch stats at 64
+    unsigned long long *hs = reinterpret_cast<unsigned long long *>(hc) + 8;
+    const bool big_out = g->max_outdeg > kSplit;
+    // pull when (push cost) * ratio > (pull cost); SP_BC_PULL overrides, 0 = push only
+    const char *pe = getenv("SP_BC_PULL");
+    const double pull_ratio = pe ? atof(pe) : kBbPullRatio;
+    std::vector<int64_t> ls;
+    for (int64_t b = first; b < nb; b += stride) {
+        BatchSrc bs;
+        int used = 0;
+        for (int s = 0; s < kLanes; s++) {
+            const int64_t i = b * kLanes + s;
+            bs.s[s] = i < nsrc ? srcs[i] : -1;
+        }
+        int nq0 = 0;  // distinct sources = queue length of depth 0
+        for (int s = 0; s < kLanes; s++) {
+            if (bs.s[s] < 0) continue;
+            used++;
+            bool dup = false;
+            for (int t = 0; t < s; t++) dup |= bs.s[t] == bs.s[s];
+            nq0 += !dup;
+        }
+        SP_CUDA(cudaMemsetAsync(lev, 0xFF, kLanes * n * sizeof(int32_t), c.stream));
+        SP_CUDA(cudaMemsetAsync(stamp, 0xFF, n * sizeof(int32_t), c.stream));
+        SP_CUDA(cudaMemsetAsync(sig, 0, kLanes * n * sizeof(double), c.stream));
+        k_bb_root<<<1, 1, 0, c.stream>>>(lev, sig, stamp, queue, bs);
+        c.launches++;
+        ls.assign({0, (int64_t)nq0});
+        int64_t mf = 0, mu = g->m;  // push / pull cost of the next step
+        for (int d = 0;; d++) {
+            const int64_t q0 = ls[d], q1 = ls[d + 1];
+            SP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(ExpandCounters), c.stream));
+            const bool pull = d > 0 && pull_ratio > 0 && (double)mf * pull_ratio > (double)mu;
+            if (pull) {
+                wk.pull_steps++;
+                BatchPull f{g->roff, g->radj, lev, sig, stamp, queue + q1, cnt, d};
+                SP_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), c.stream));
+                k_bb_pull_rows<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(f, n, ck);
+                c.launches++;
+                if (g->max_indeg > kBbShort) {
+                    k_bb_pull_chunks<<<sms * 8, 256, 0, c.stream>>>(f, ck);
+                    k_bb_pull_finish<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(f, ck);
+                    c.launches += 2;
+                }
+            } else {
+                BatchDiscoverOp op{lev, sig, stamp, d, d + 1};
+                launch_expand(op, g->off, g->adj, queue + q0, q1 - q0, queue + q1, chunks, cnt,
+                              sms, big_out, c.stream, &c.launches);
+            }
+            SP_CUDA(cudaGetLastError());
+            if (pull_ratio > 0) {
+                SP_CUDA(cudaMemsetAsync(counts + 2, 0, 2 * sizeof(unsigned long long), c.stream));
+                k_bb_plan<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(
+                    lev, g->off, g->roff, queue + q1, cnt, n, counts + 2);
+                c.launches++;
+                SP_CUDA(cudaMemcpyAsync(hs, counts + 2, 16, cudaMemcpyDeviceToHost, c.stream));
+            }
+            SP_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(ExpandCounters), cudaMemcpyDeviceToHost,
+                                    c.stream));
+            SP_CUDA(cudaStreamSynchronize(c.stream));
+            const int64_t nnew = (int64_t)hc->next_size;
+            if (nnew == 0) break;
+            mf = (int64_t)hs[0];
+            mu = (int64_t)hs[1];
+            ls.push_back(q1 + nnew);
+        }
+        const int D = (int)ls.size() - 2;  // deepest depth
+        const bool is_last = b == nb - 1;
+        const int last_lane = (int)((nsrc - 1) % kLanes);
+        if (is_last && dlast) SP_CUDA(cudaMemsetAsync(dlast, 0, n * sizeof(double), c.stream));
+        for (int d = D; d >= 0; d--) {
+            const int64_t q0 = ls[d], nq = ls[d + 1] - ls[d];
+            BatchFold f{g->off, g->adj, lev, sig, coef, bc, is_last ? dlast : nullptr,
+                        last_lane, bs, d};
+            SP_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), c.stream));
+            k_bb_rows<<<grid_for(nq, 256, c.device), 256, 0, c.stream>>>(f, queue + q0, nq,
+                                                                         d == D, ck);
+            c.launches++;
+            if (d < D && g->max_outdeg > kBbShort) {
+                k_bb_chunks<<<sms * 8, 256, 0, c.stream>>>(f, ck);
+                k_bb_finish<<<grid_for(nq, 256, c.device), 256, 0, c.stream>>>(f, ck);
+                c.launches += 2;
+            }
+            SP_CUDA(cudaGetLastError());
+        }
+        SP_CUDA(cudaMemsetAsync(counts + 2, 0, (kLanes / 2 + 2) * sizeof(unsigned long long),
+                                c.stream));
+        k_bb_stats<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(lev, g->off, n, counts + 2);
+        c.launches++;
+        SP_CUDA(cudaMemcpyAsync(hs, counts + 2, 8 * (kLanes / 2 + 2), cudaMemcpyDeviceToHost,
+                                c.stream));
+        SP_CUDA(cudaStreamSynchronize(c.stream));
+        wk.reached += (int64_t)hs[0];
+        wk.scanned += (int64_t)hs[1];
+        const unsigned *lm = reinterpret_cast<const unsigned *>(hs + 2);
+        for (int s = 0; s < used; s++) wk.levels += lm[s];
+        if (is_last) {
+            if (sigma_out) {
+                double *so;
+                SP_TRY(c.alloc(&so, n));
+                k_bb_lane_out<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(sig, last_lane,
+                                                                              n, so);
+                c.launches++;
+                SP_TRY(from_device(sigma_out, so, n * 8, mem, c.stream));
+            }
+            if (delta_out) SP_TRY(from_device(delta_out, dlast, n * 8, mem, c.stream));
+        }
+    }
+    if (bc_accumulate_only) {
+        SP_CUDA(cudaMemcpyAsync(bc_dst, bc, n * 8, cudaMemcpyDeviceToDevice, c.stream));
+    } else {
+        SP_TRY(from_device(bc_dst, bc, n * 8, bc_mem, c.stream));
+    }
+    SP_TRY(c.finish(nullptr));
+    wk.launches = c.launches;
+    return SP_OK;
+}
+
 // bc = sum of the workers' partials in worker order (fixed: deterministic)
 __global__ void k_sum_partials(const double *__restrict__ parts, int k, int64_t n, double *out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -310,14 +945,36 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
                  "set argument 'sourceSet' id %d out of range", srcs[i]);
     const int64_t n = g->n;
     const bool det = flags & SP_FLAG_DETERMINISTIC;
-    // Fast mode runs kBcWorkers sources concurrently (one host thread and
-    // stream each): small BFS levels of one source overlap the large levels
-    // of another, and the per-level host reads overlap too.  Deterministic
+    // Fast mode runs batches of kLanes sources (bc_run_batches), kBbWorkers
+    // batches concurrently (one host thread and stream each): small BFS
+    // levels of one batch overlap the large levels of another, and the
+    // per-level host reads overlap too.  SP_BC_BATCH=0 selects the
+    // per-source fast path (kBcWorkers sources concurrently).  Deterministic
     // mode keeps the reference's sequential source order (bit-exact bc).
-    const int K = det ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(kBcWorkers, nsrc));
+    const char *eb = getenv("SP_BC_BATCH");
+    bool batched = !det && !(eb && eb[0] == '0');
+    const int64_t nb = (nsrc + kLanes - 1) / kLanes;
+    int K = det ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(kBcWorkers, nsrc));
+    if (batched) {
+        // per worker: lev/sig/coef/csum/queue lanes + stamp, reg, bc; items
+        const double per = (double)n * (4 + 8 + 8 + 8 + 4) * kLanes + 28.0 * n + g->m / 3.0;
+        size_t fr = 0, tot = 0;
+        SP_CUDA(cudaSetDevice(g->device));
+        SP_CUDA(cudaMemGetInfo(&fr, &tot));
+        K = (int)std::max<int64_t>(1, std::min<int64_t>(kBbWorkers, nb));
+        while (K > 1 && per * K > 0.6 * (double)fr) K--;
+        if (per > 0.6 * (double)fr) batched = false, K = 1;  // per-source state only
+    }
     Call c;
     SP_TRY(c.begin(g->device));
     std::vector<BcWorker> wk(K);
+    auto run = [&](int64_t first, int64_t stride, double *dst, int dmem, bool acc_only,
+                   BcWorker &w) {
+        return batched ? bc_run_batches(g, srcs, first, stride, dst, dmem, acc_only, sigma_out,
+                                        delta_out, mem, w)
+                       : bc_run_sources(g, srcs, first, stride, det, dst, dmem, acc_only,
+                                        sigma_out, delta_out, mem, w);
+    };
     if (nsrc == 0) {
         double *z;
         SP_TRY(c.alloc(&z, n));
@@ -325,8 +982,7 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
         SP_TRY(from_device(bc_out, z, n * 8, mem, c.stream));
     } else if (K == 1) {
         SP_TRY(c.finish(nullptr));  // order after the caller's work
-        SP_TRY(bc_run_sources(g, srcs, 0, 1, det, bc_out, mem, false, sigma_out, delta_out, mem,
-                              wk[0]));
+        SP_TRY(run(0, 1, bc_out, mem, false, wk[0]));
     } else {
         double *parts;
         SP_TRY(c.alloc(&parts, (int64_t)K * n));
@@ -334,8 +990,7 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
         std::vector<std::thread> th;
         for (int k = 0; k < K; k++)
             th.emplace_back([&, k]() {
-                wk[k].rc = bc_run_sources(g, srcs, k, K, det, parts + (int64_t)k * n,
-                                          SP_MEM_DEVICE, true, sigma_out, delta_out, mem, wk[k]);
+                wk[k].rc = run(k, K, parts + (int64_t)k * n, SP_MEM_DEVICE, true, wk[k]);
                 if (wk[k].rc != SP_OK) snprintf(wk[k].err, sizeof(wk[k].err), "%s", sp_last_error());
             });
         for (auto &t : th) t.join();

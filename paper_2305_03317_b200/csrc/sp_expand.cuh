@@ -37,6 +37,11 @@ constexpr int kExpandBlock = 256;
 constexpr int kSplit = 256;  // rows longer than this are cut into kSplit-slot chunks
 constexpr int kRounds = 4;   // 32-slot rounds in flight per warp in k_expand
 
+// A hub-chunk work item: {vertex, first slot (lo, hi), slot count}.  The
+// slot range is resolved when the chunk is published, so the chunk kernel's
+// first dependent load is the adjacency itself.
+using ChunkItem = uint4;
+
 struct ExpandCounters {
     unsigned long long next_size;  // appended frontier entries
     unsigned long long scanned;    // slots scanned
@@ -101,7 +106,7 @@ __device__ __forceinline__ void flush_stage(const Op &op, ExpandCounters *cnt, i
 template <class Op>
 __device__ __forceinline__ void expand_batch(const Op &op, const int64_t *__restrict__ off,
                                              const int32_t *__restrict__ adj, int32_t v,
-                                             int32_t *__restrict__ qn, uint2 *__restrict__ chunks,
+                                             int32_t *__restrict__ qn, ChunkItem *__restrict__ chunks,
                                              ExpandCounters *cnt, ExpandStage &st,
                                              unsigned long long &scanned) {
     using P = typename Op::Payload;
@@ -120,7 +125,12 @@ __device__ __forceinline__ void expand_batch(const Op &op, const int64_t *__rest
     if (deg > kSplit) {  // hub row -> chunk work items
         int64_t nch = (deg + kSplit - 1) / kSplit;
         unsigned long long s = atomicAdd(&cnt->chunks, (unsigned long long)nch);
-        for (int64_t c = 0; c < nch; c++) chunks[s + c] = make_uint2((unsigned)v, (unsigned)c);
+        for (int64_t c = 0; c < nch; c++) {
+            const int64_t e0 = beg + c * kSplit;
+            const int64_t len = min((int64_t)kSplit, beg + deg - e0);
+            chunks[s + c] = make_uint4((unsigned)v, (unsigned)(uint64_t)e0,
+                                       (unsigned)((uint64_t)e0 >> 32), (unsigned)len);
+        }
         deg = 0;
     }
     int64_t incl = deg;
@@ -175,7 +185,7 @@ template <class Op, int kHops = 0>
 __device__ __forceinline__ void expand_body(
     const Op &op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const int32_t *__restrict__ q, int64_t nq, int32_t *__restrict__ qn,
-    uint2 *__restrict__ chunks, ExpandCounters *cnt, int vpw) {
+    ChunkItem *__restrict__ chunks, ExpandCounters *cnt, int vpw) {
     // vpw = frontier vertices per warp (32 normally; fewer for small
     // frontiers, so that every SM gets work)
     const unsigned lane = lane_id();
@@ -212,7 +222,7 @@ template <class Op>
 __global__ void __launch_bounds__(kExpandBlock, 4) k_expand(
     Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const int32_t *__restrict__ q, int64_t nq, int32_t *__restrict__ qn,
-    uint2 *__restrict__ chunks, ExpandCounters *cnt, int vpw) {
+    ChunkItem *__restrict__ chunks, ExpandCounters *cnt, int vpw) {
     expand_body(op, off, adj, q, nq, qn, chunks, cnt, vpw);
 }
 
@@ -224,33 +234,53 @@ __host__ __device__ __forceinline__ int expand_vpw(int64_t nq, int64_t warps) {
     return vpw;
 }
 
+// Slots (adjacency, streamed) and payload of one chunk; len 0: all -1.
+template <class Op, int K>
+__device__ __forceinline__ void load_chunk(const Op &op, const int32_t *__restrict__ adj,
+                                           const ChunkItem d, unsigned lane, int32_t (&x)[K],
+                                           typename Op::Payload &pay, int64_t &e0) {
+    e0 = (int64_t)(((uint64_t)d.z << 32) | d.y);
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+        const unsigned p = j * 32 + lane;
+        x[j] = p < d.w ? __ldcs(adj + e0 + p) : -1;  // streamed: evict first
+    }
+    pay = d.w ? op.payload((int32_t)d.x) : typename Op::Payload(0);
+}
+
+// One warp per chunk, software-pipelined across the warp's chunks: the
+// descriptor two chunks ahead and the slots + payload of the next chunk are
+// in flight while the current chunk's probes and atomics run, so a chunk
+// costs about one random round trip instead of descriptor -> slots ->
+// probe in series.
 template <class Op>
 __device__ __forceinline__ void expand_chunks_body(
     const Op &op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
-    const uint2 *__restrict__ chunks, int32_t *__restrict__ qn, ExpandCounters *cnt) {
+    const ChunkItem *__restrict__ chunks, int32_t *__restrict__ qn, ExpandCounters *cnt) {
+    using P = typename Op::Payload;
     using Pr = typename Op::Probe;
     constexpr int kPer = kSplit / 32;
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nch = (int64_t)__ldcg(&cnt->chunks);
+    const ChunkItem none = make_uint4(0, 0, 0, 0);
     unsigned long long scanned = 0;
     ExpandStage st = make_stage();
+    int32_t x[kPer];
+    P pay;
+    int64_t e0;
+    const ChunkItem d0 = warp < nch ? chunks[warp] : none;
+    unsigned len = d0.w;
+    load_chunk(op, adj, d0, lane, x, pay, e0);
+    ChunkItem d1 = warp + nwarps < nch ? chunks[warp + nwarps] : none;
     for (int64_t w = warp; w < nch; w += nwarps) {
-        const uint2 ch = chunks[w];
-        const int32_t v = (int32_t)ch.x;
-        const int64_t end = off[v + 1];
-        const int64_t e0 = off[v] + (int64_t)ch.y * kSplit;
-        const int64_t e1 = min(end, e0 + kSplit);
-        const auto pay = op.payload(v);
-        scanned += e1 - e0;
-        int32_t x[kPer];
+        const ChunkItem d2 = w + 2 * nwarps < nch ? chunks[w + 2 * nwarps] : none;
+        int32_t xn[kPer];
+        P payn;
+        int64_t e0n;
+        load_chunk(op, adj, d1, lane, xn, payn, e0n);
         Pr pr[kPer];
-#pragma unroll
-        for (int j = 0; j < kPer; j++) {
-            const int64_t ee = e0 + j * 32 + lane;
-            x[j] = ee < e1 ? __ldcs(adj + ee) : -1;  // streamed: evict first
-        }
 #pragma unroll
         for (int j = 0; j < kPer; j++)
             if (x[j] >= 0) pr[j] = op.probe(e0 + j * 32 + lane, x[j]);
@@ -259,15 +289,22 @@ __device__ __forceinline__ void expand_chunks_body(
         for (int j = 0; j < kPer; j++)
             res[j] = x[j] >= 0 ? (int)op.apply(pay, e0 + j * 32 + lane, x[j], pr[j]) : 0;
         append_results<Op, kPer>(op, res, x, cnt, qn, st);
+        scanned += len;
+#pragma unroll
+        for (int j = 0; j < kPer; j++) x[j] = xn[j];
+        pay = payn;
+        e0 = e0n;
+        len = d1.w;
+        d1 = d2;
     }
     flush_stage(op, cnt, qn, st);
     if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);  // warp-uniform
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kExpandBlock, 4) k_expand_chunks(
+__global__ void __launch_bounds__(kExpandBlock, 3) k_expand_chunks(
     Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
-    const uint2 *__restrict__ chunks, int32_t *__restrict__ qn, ExpandCounters *cnt) {
+    const ChunkItem *__restrict__ chunks, int32_t *__restrict__ qn, ExpandCounters *cnt) {
     expand_chunks_body(op, off, adj, chunks, qn, cnt);
 }
 
@@ -277,7 +314,7 @@ inline int64_t expand_chunk_capacity(int64_t m) { return 2 * (m / kSplit) + 2; }
 // Launch both expansion kernels for one frontier.
 template <class Op>
 inline void launch_expand(const Op &op, const int64_t *off, const int32_t *adj, const int32_t *q,
-                          int64_t nq, int32_t *qn, uint2 *chunks, ExpandCounters *cnt, int sms,
+                          int64_t nq, int32_t *qn, ChunkItem *chunks, ExpandCounters *cnt, int sms,
                           bool has_big_rows, cudaStream_t s, int64_t *launches) {
     const int cap = sms * 8;
     const int64_t warps_full = (int64_t)cap * (kExpandBlock / 32);

@@ -16,7 +16,8 @@
 // per row in chunk order (k_fold_combine): deterministic run to run, a few
 // ulps from the left fold, and no lane folds a long row while its
 // warp-mates idle.
-// F supplies: double payload(int32_t v); double term(double pay, int64_t slot);
+// F supplies: double payload(int32_t v); int32_t key(int64_t slot) (the
+//             slot's neighbour); double term(double pay, int32_t key);
 //             void finish(int32_t v, double sum).
 #pragma once
 
@@ -42,7 +43,7 @@ struct FoldChunks {
     int32_t *reg_v;      // registered row vertex
     int64_t *reg_base;   // its first chunk slot
     int32_t *reg_nch;    // its chunk count
-    int32_t *item_reg;   // chunk slot -> registry index
+    uint4 *items;        // chunk slot -> {vertex, first slot lo, hi, slot count}
     double *csum;        // chunk slot -> partial sum
     unsigned long long *counts;  // [0] registered rows, [1] chunk slots used
 };
@@ -82,7 +83,12 @@ __global__ void __launch_bounds__(kFoldBlock) k_fold(
                 fc.reg_v[r] = v;
                 fc.reg_base[r] = base;
                 fc.reg_nch[r] = nch;
-                for (int c = 0; c < nch; c++) fc.item_reg[base + c] = (int32_t)r;
+                for (int c = 0; c < nch; c++) {
+                    const int64_t s0 = rs + (int64_t)c * kFoldSplit;
+                    const int64_t len = min((int64_t)kFoldSplit, rs + deg - s0);
+                    fc.items[base + c] = make_uint4((unsigned)v, (unsigned)(uint64_t)s0,
+                                                    (unsigned)((uint64_t)s0 >> 32), (unsigned)len);
+                }
             }
         }
         const bool deferred = hub || mid;
@@ -110,7 +116,7 @@ __global__ void __launch_bounds__(kFoldBlock) k_fold(
                 const int64_t ex = __shfl_sync(0xffffffffu, excl, lo);
                 const int64_t b0 = __shfl_sync(0xffffffffu, rs, lo);
                 const double pv = __shfl_sync(0xffffffffu, pay, lo);
-                buf[j * 32 + lane] = p < total ? f.term(pv, b0 + (p - ex)) : 0.0;
+                buf[j * 32 + lane] = p < total ? f.term(pv, f.key(b0 + (p - ex))) : 0.0;
             }
             __syncwarp();
             const int64_t a = max(excl, p0), b = min(excl + deg, p0 + (int64_t)kFoldChunk);
@@ -121,32 +127,53 @@ __global__ void __launch_bounds__(kFoldBlock) k_fold(
     }
 }
 
+// Keys (streamed slot loads) and payload of one chunk; count 0: all -1.
+template <class F, int K>
+__device__ __forceinline__ void fold_load_chunk(const F &f, const uint4 d, unsigned lane,
+                                                int32_t (&key)[K], double &pay) {
+    const int64_t s0 = (int64_t)(((uint64_t)d.z << 32) | d.y);
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+        const unsigned p = j * 32 + lane;
+        key[j] = p < d.w ? f.key(s0 + p) : -1;
+    }
+    pay = d.w ? f.payload((int32_t)d.x) : 0.0;
+}
+
+// One warp per chunk, pipelined like expand_chunks_body: the descriptor two
+// chunks ahead and the keys + payload of the next chunk load while the
+// current chunk's terms (random record reads) are summed.
 template <class F>
 __global__ void __launch_bounds__(kFoldBlock) k_fold_chunks(F f, const int64_t *__restrict__ rowoff,
                                                             FoldChunks fc) {
+    constexpr int kPer = kFoldSplit / 32;
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nitems = (int64_t)__ldcg(&fc.counts[1]);
+    const uint4 none = make_uint4(0, 0, 0, 0);
+    int32_t key[kPer];
+    double pay;
+    fold_load_chunk(f, warp < nitems ? fc.items[warp] : none, lane, key, pay);
+    uint4 d1 = warp + nwarps < nitems ? fc.items[warp + nwarps] : none;
     for (int64_t k = warp; k < nitems; k += nwarps) {
-        const int32_t r = fc.item_reg[k];
-        const int32_t v = fc.reg_v[r];
-        const int64_t c = k - fc.reg_base[r];
-        const int64_t re = rowoff[v + 1];
-        const int64_t s0 = rowoff[v] + c * kFoldSplit;
-        const double pay = f.payload(v);
-        double t[kFoldSplit / 32];
+        const uint4 d2 = k + 2 * nwarps < nitems ? fc.items[k + 2 * nwarps] : none;
+        int32_t keyn[kPer];
+        double payn;
+        fold_load_chunk(f, d1, lane, keyn, payn);
+        double t[kPer];
 #pragma unroll
-        for (int j = 0; j < kFoldSplit / 32; j++) {
-            const int64_t e = s0 + j * 32 + lane;
-            t[j] = e < re ? f.term(pay, e) : 0.0;
-        }
+        for (int j = 0; j < kPer; j++) t[j] = key[j] >= 0 ? f.term(pay, key[j]) : 0.0;
         double sum = 0.0;
 #pragma unroll
-        for (int j = 0; j < kFoldSplit / 32; j++) sum = __dadd_rn(sum, t[j]);
+        for (int j = 0; j < kPer; j++) sum = __dadd_rn(sum, t[j]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
         if (lane == 0) fc.csum[k] = sum;
+#pragma unroll
+        for (int j = 0; j < kPer; j++) key[j] = keyn[j];
+        pay = payn;
+        d1 = d2;
     }
 }
 
@@ -187,7 +214,7 @@ __global__ void __launch_bounds__(kHubFoldBlock) k_fold_hub(
 #pragma unroll
             for (int k = 0; k < kHubFoldChunk / kHubFoldBlock; k++) {
                 const int j = threadIdx.x + k * kHubFoldBlock;
-                stage[j] = j < len ? f.term(pay, c0 + j) : 0.0;
+                stage[j] = j < len ? f.term(pay, f.key(c0 + j)) : 0.0;
             }
             __syncthreads();
             if (deterministic) {

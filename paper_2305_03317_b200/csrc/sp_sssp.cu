@@ -94,7 +94,7 @@ struct SsspLoop {
 
 __global__ void __launch_bounds__(kExpandBlock, 4) k_relax_loop(
     int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, uint2 *chunks,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, ChunkItem *chunks,
     SsspLoop *L, int64_t warps) {
     const int cur = L->cur;
     const int64_t nq = L->nq;
@@ -103,9 +103,9 @@ __global__ void __launch_bounds__(kExpandBlock, 4) k_relax_loop(
                 expand_vpw(nq, warps));
 }
 
-__global__ void __launch_bounds__(kExpandBlock, 4) k_relax_loop_chunks(
+__global__ void __launch_bounds__(kExpandBlock, 3) k_relax_loop_chunks(
     int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const uint2 *chunks,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const ChunkItem *chunks,
     SsspLoop *L) {
     const int cur = L->cur;
     RelaxOp op{dist, enq, weff, &L->cnt[cur].flag, L->it};
@@ -200,7 +200,7 @@ struct NearFarOp {
 
 __global__ void __launch_bounds__(kExpandBlock, 4) k_nf_expand(
     int32_t *dist, int32_t *enq, int32_t *last, const int32_t *__restrict__ weff,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, uint2 *chunks, NfLoop *L,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, ChunkItem *chunks, NfLoop *L,
     int64_t warps) {
     const int cur = L->cur;
     const int64_t nq = L->nq;
@@ -211,9 +211,9 @@ __global__ void __launch_bounds__(kExpandBlock, 4) k_nf_expand(
                 expand_vpw(nq, warps));
 }
 
-__global__ void __launch_bounds__(kExpandBlock, 4) k_nf_chunks(
+__global__ void __launch_bounds__(kExpandBlock, 3) k_nf_chunks(
     int32_t *dist, int32_t *enq, int32_t *last, const int32_t *__restrict__ weff,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const uint2 *chunks,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const ChunkItem *chunks,
     NfLoop *L) {
     const int cur = L->cur;
     if (L->nq == 0) return;
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kExpandBlock) k_nf_persistent(
 }
 
 int sssp_near_far(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
-                  uint2 *chunks, int64_t cap, int64_t delta, SsspLoop *out, float *kernel_ms) {
+                  ChunkItem *chunks, int64_t cap, int64_t delta, SsspLoop *out, float *kernel_ms) {
     const int64_t n = g->n, m = g->m;
     int32_t *last, *fa, *fb;
     NfLoop *L;
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(256) k_pull_hubs(const int64_t *__restrict__ r
 
 __global__ void __launch_bounds__(kExpandBlock, 4) k_do_push(
     int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, uint2 *chunks,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, ChunkItem *chunks,
     DoLoop *D, int64_t warps) {
     if (D->mode != 0) return;
     SsspLoop *L = &D->s;
@@ -664,9 +664,9 @@ __global__ void __launch_bounds__(kExpandBlock, 4) k_do_push(
                 expand_vpw(nq, warps));
 }
 
-__global__ void __launch_bounds__(kExpandBlock, 4) k_do_push_chunks(
+__global__ void __launch_bounds__(kExpandBlock, 3) k_do_push_chunks(
     int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const uint2 *chunks,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const ChunkItem *chunks,
     DoLoop *D) {
     if (D->mode != 0) return;
     SsspLoop *L = &D->s;
@@ -771,7 +771,7 @@ __global__ void k_do_mode(DoLoop *D) {
 }
 
 int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
-                 uint2 *chunks, int64_t cap, SsspLoop *out, float *kernel_ms) {
+                 ChunkItem *chunks, int64_t cap, SsspLoop *out, float *kernel_ms) {
     SP_TRY(ensure_rweff(g, c));
     const int64_t n = g->n;
     const int64_t nwords = (n + 31) / 32;
@@ -864,7 +864,7 @@ int64_t near_far_delta(const sp_graph *g, int32_t wmin, int32_t wmax) {
 }
 
 int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
-                     uint2 *chunks, int64_t cap, SsspLoop *hL, float *kernel_ms) {
+                     ChunkItem *chunks, int64_t cap, SsspLoop *hL, float *kernel_ms) {
     SsspLoop *L;
     SP_TRY(c.alloc(&L, 1));
     SsspLoop init{};
@@ -936,7 +936,7 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
     SP_TRY(ensure_weff(g, c));
     const int64_t n = g->n;
     int32_t *dist, *enq, *qa, *qb;
-    uint2 *chunks;
+    ChunkItem *chunks;
     ExpandCounters *cnt;
     SP_TRY(c.alloc(&dist, n));
     SP_TRY(c.alloc(&enq, n));
@@ -1140,7 +1140,7 @@ extern "C" int sp_sssp_block_step(sp_graph *g, int64_t v0, int64_t v1, int32_t *
     SP_TRY(ensure_weff(g, c));
     const int64_t nb = std::max<int64_t>(1, v1 - v0);
     int32_t *q, *qn;
-    uint2 *chunks;
+    ChunkItem *chunks;
     ExpandCounters *cnt;
     SP_TRY(c.alloc(&q, nb));
     SP_TRY(c.alloc(&qn, 1));

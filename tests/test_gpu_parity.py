@@ -207,6 +207,59 @@ def test_bc_seeded(kind, p0, p1, und):
     assert rel_err(rf.env.node_props["bc"], bc) <= 1e-12
 
 
+def _two_components(directed):
+    """Two RMAT blocks with no edges between them plus isolated vertices:
+    lanes of one batch reach disjoint vertex sets."""
+    u1, v1, w1, n1 = gen.rmat(11, 8, seed=2, undirected=not directed)
+    u2, v2, w2, n2 = gen.rmat(10, 8, seed=3, undirected=not directed)
+    u = np.concatenate([u1, u2 + n1])
+    v = np.concatenate([v1, v2 + n1])
+    w = np.concatenate([w1, w2])
+    return u, v, w, n1 + n2 + 50
+
+
+# Fast-mode forms: batched sources with the automatic push/pull choice,
+# push-only, pull at every step after the root's, and the per-source path.
+BC_FORMS = [{}, {"SP_BC_PULL": "0"}, {"SP_BC_PULL": "1e12"}, {"SP_BC_BATCH": "0"}]
+
+
+@pytest.mark.parametrize("form", BC_FORMS, ids=["auto", "push", "pull", "per_source"])
+@pytest.mark.parametrize("graph", ["rmat_sym", "rmat_dir", "hub_dir", "hub_sym", "multi",
+                                   "two_comp_sym", "two_comp_dir"])
+def test_bc_fast_forms(graph, form, monkeypatch):
+    """Every fast-mode BC form against the oracle: 19 sources (two full
+    8-source batches and a partial one, with duplicates inside a batch),
+    bc within 1e-12, sigma of the last source bit-exact (integer path
+    counts), delta of the last source within 1e-12."""
+    for k, val in form.items():
+        monkeypatch.setenv(k, val)
+    if graph.startswith("rmat"):
+        u, v, w, n = gen.rmat(12, 16, seed=21, undirected=graph == "rmat_sym")
+        directed = graph == "rmat_dir"
+    elif graph.startswith("hub"):
+        directed = graph == "hub_dir"
+        u, v, w, n = _hub_graph(directed)
+    elif graph == "multi":
+        u, v, w, n = _multigraph(8)
+        directed = True
+    else:
+        directed = graph == "two_comp_dir"
+        u, v, w, n = _two_components(directed)
+    g = sp.from_arrays(u, v, w, directed=directed, n=n)
+    o = cpu_ref.build_csr(u, v, w, directed, n)
+    rng = np.random.default_rng(5)
+    srcs = rng.choice(n, size=16, replace=False).tolist()
+    srcs = srcs[:5] + [srcs[2]] + srcs[5:] + [0, n - 1, srcs[0]]  # 19, duplicates
+    bc, sg, dl = cpu_ref.bc(o, srcs, nthreads=4)
+    r = sp.run(corpus.BC, g, {"sourceSet": srcs})
+    assert rel_err(r.env.node_props["bc"], bc) <= 1e-12
+    assert r.env.node_props["sigma"].tobytes() == sg.tobytes()
+    assert rel_err(r.env.node_props["delta"], dl) <= 1e-12
+    for k in ("edges_visited", "vertices_visited", "iterations"):
+        assert r.stats[k] == sp.run(corpus.BC, g, {"sourceSet": srcs},
+                                    deterministic=True).stats[k]
+
+
 @pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 13, 16, True), ("rmat", 12, 16, False),
                                             ("uniform", 1 << 15, 1 << 19, True)])
 def test_tc_seeded(kind, p0, p1, und):
