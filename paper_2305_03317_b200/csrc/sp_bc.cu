@@ -38,7 +38,7 @@ namespace {
 
 constexpr int64_t kBcHub = 8192;  // rows longer than this take the CTA fold
 constexpr int kBcWorkers = 4;     // concurrent sources (host threads/streams), per-source fast path
-constexpr int kBbWorkers = 2;     // concurrent source batches, batched fast path
+constexpr int kBbWorkers = 3;     // concurrent source batches, batched fast path
 
 // Per-vertex record, 16 bytes: level (int32) and, in fast mode, the child
 // coefficient coef[w] = (1 + delta[w]) / sigma[w] (written when delta[w] is
@@ -482,19 +482,27 @@ __device__ __forceinline__ void bb_store_chunk(const BbChunks &ck, int64_t k, un
     if (lane_id() < kLanes) ck.csum[kLanes * k + lane_id()] = mine;
 }
 
-// row r's lane sums: its chunks' partials in chunk order
+// Row r's lane sums from its chunks' partials, by one warp: lane j adds
+// chunks j, j+32, ... in order, then a fixed xor tree -- the same shape
+// every run (deterministic), and a hub row's hundreds of chunks are not
+// summed by a single thread.  Every lane returns the sums.
 __device__ __forceinline__ void bb_row_sums(const BbChunks &ck, int64_t r, double (&acc)[kLanes]) {
     const int64_t b0 = ck.reg_base[r];
     const int nch = ck.reg_nch[r];
 #pragma unroll
     for (int s = 0; s < kLanes; s++) acc[s] = 0.0;
-    for (int c = 0; c < nch; c++) {
+    for (int c = lane_id(); c < nch; c += 32) {
         double p[kLanes];
         load_f64x4_ro(ck.csum + kLanes * (b0 + c), *reinterpret_cast<double(*)[4]>(p));
         load_f64x4_ro(ck.csum + kLanes * (b0 + c) + 4, *reinterpret_cast<double(*)[4]>(p + 4));
 #pragma unroll
         for (int s = 0; s < kLanes; s++) acc[s] = __dadd_rn(acc[s], p[s]);
     }
+#pragma unroll
+    for (int s = 0; s < kLanes; s++)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            acc[s] = __dadd_rn(acc[s], __shfl_xor_sync(0xffffffffu, acc[s], o));
 }
 
 // Level d's rows: short rows folded by one thread; long rows registered and
@@ -566,15 +574,18 @@ __global__ void __launch_bounds__(256) k_bb_chunks(BatchFold f, BbChunks ck) {
     }
 }
 
-__global__ void k_bb_finish(BatchFold f, BbChunks ck) {
+// one warp per long row
+__global__ void __launch_bounds__(256) k_bb_finish(BatchFold f, BbChunks ck) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nreg = (int64_t)__ldcg(&ck.counts[0]);
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nreg;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = ck.reg_v[r];
-        const unsigned act = lanes_eq(load_lev_ro(f.lev, v), f.d);
+    for (int64_t r = warp; r < nreg; r += nwarps) {
         double acc[kLanes];
         bb_row_sums(ck, r, acc);
-        f.finish(v, act, acc);
+        if (lane_id() == 0) {
+            const int32_t v = ck.reg_v[r];
+            f.finish(v, lanes_eq(load_lev_ro(f.lev, v), f.d), acc);
+        }
     }
 }
 
@@ -682,79 +693,58 @@ __global__ void __launch_bounds__(256) k_bb_pull_chunks(BatchPull f, BbChunks ck
     }
 }
 
-__global__ void k_bb_pull_finish(BatchPull f, BbChunks ck) {
+// one warp per long row
+__global__ void __launch_bounds__(256) k_bb_pull_finish(BatchPull f, BbChunks ck) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nreg = (int64_t)__ldcg(&ck.counts[0]);
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nreg;
-         base += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = base + threadIdx.x;
-        bool push = false;
-        int32_t w = -1;
-        if (r < nreg) {
-            w = ck.reg_v[r];
-            const unsigned pm = lanes_eq(load_lev(f.lev, w), -1);
-            double acc[kLanes];
-            bb_row_sums(ck, r, acc);
-            push = f.finish(w, pm, acc);
+    for (int64_t r = warp; r < nreg; r += nwarps) {
+        double acc[kLanes];
+        bb_row_sums(ck, r, acc);
+        if (lane_id() == 0) {
+            const int32_t w = ck.reg_v[r];
+            if (f.finish(w, lanes_eq(load_lev(f.lev, w), -1), acc))
+                f.qn[atomicAdd(&f.cnt->next_size, 1ull)] = w;
         }
-        const int64_t slot = warp_append(push, &f.cnt->next_size);
-        if (push) f.qn[slot] = w;
     }
 }
 
-// Direction choice for the next step: out[0] = out-slots of the new
-// frontier (push cost), out[1] = in-slots of vertices with an unvisited
-// lane (pull cost).
-__global__ void k_bb_plan(const int32_t *__restrict__ lev, const int64_t *__restrict__ off,
-                          const int64_t *__restrict__ roff, const int32_t *__restrict__ qn,
-                          const ExpandCounters *cnt, int64_t n, unsigned long long *out) {
-    const int64_t nq = (int64_t)cnt->next_size;
-    unsigned long long fe = 0, pe = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+// Over a level's queue right after it is complete: the next step's push
+// cost (out-slots of the queue), the in-slots of vertices that just lost
+// their last unvisited lane (the pull cost drops by these), and the batch
+// statistics (lanes reached at this depth, their out-slots, lane mask).
+// out: [0] push cost, [1] pull-cost decrement, [2] reached, [3] slots,
+// [4] lane mask.
+__global__ void k_bb_frontier(const int32_t *__restrict__ lev, const int64_t *__restrict__ off,
+                              const int64_t *__restrict__ roff, const int32_t *__restrict__ q,
+                              const unsigned long long *nq_dev, int64_t nq_host, int depth,
+                              unsigned long long *out) {
+    const int64_t nq = nq_dev ? (int64_t)*nq_dev : nq_host;
+    unsigned long long fe = 0, dec = 0, reached = 0, slots = 0;
+    unsigned lanes = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq;
          i += (int64_t)gridDim.x * blockDim.x) {
-        if (i < nq) {
-            const int32_t v = qn[i];
-            fe += off[v + 1] - off[v];
-        }
-        if (lanes_eq(load_lev_ro(lev, (int32_t)i), -1)) pe += roff[i + 1] - roff[i];
+        const int32_t v = q[i];
+        const Lev8 l = load_lev(lev, v);
+        const unsigned nm = lanes_eq(l, depth);
+        const int64_t od = off[v + 1] - off[v];
+        fe += od;
+        if (!lanes_eq(l, -1)) dec += roff[v + 1] - roff[v];
+        reached += __popc(nm);
+        slots += (unsigned long long)__popc(nm) * od;
+        lanes |= nm;
     }
     fe = warp_sum(fe);
-    pe = warp_sum(pe);
-    if (lane_id() == 0) {
-        if (fe) atomicAdd(out, fe);
-        if (pe) atomicAdd(out + 1, pe);
-    }
-}
-
-// per batch: reached (vertex, source) pairs, their out-slots, levels per lane
-__global__ void k_bb_stats(const int32_t *__restrict__ lev, const int64_t *__restrict__ off,
-                           int64_t n, unsigned long long *out) {
-    unsigned long long reached = 0, slots = 0;
-    unsigned lmax[kLanes];
-#pragma unroll
-    for (int s = 0; s < kLanes; s++) lmax[s] = 0;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t *l = lev + kLanes * v;
-        const int64_t deg = off[v + 1] - off[v];
-#pragma unroll
-        for (int s = 0; s < kLanes; s++)
-            if (l[s] >= 0) {
-                reached++;
-                slots += deg;
-                lmax[s] = max(lmax[s], (unsigned)l[s] + 1);
-            }
-    }
+    dec = warp_sum(dec);
     reached = warp_sum(reached);
     slots = warp_sum(slots);
+    lanes = __reduce_or_sync(0xffffffffu, lanes);
     if (lane_id() == 0) {
-        if (reached) atomicAdd(out, reached);
-        if (slots) atomicAdd(out + 1, slots);
-    }
-#pragma unroll
-    for (int s = 0; s < kLanes; s++) {
-        unsigned x = lmax[s];
-        for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
-        if (lane_id() == 0 && x) atomicMax(reinterpret_cast<unsigned *>(out + 2) + s, x);
+        if (fe) atomicAdd(out, fe);
+        if (dec) atomicAdd(out + 1, dec);
+        if (reached) atomicAdd(out + 2, reached);
+        if (slots) atomicAdd(out + 3, slots);
+        if (lanes) atomicOr(out + 4, (unsigned long long)lanes);
     }
 }
 
@@ -797,7 +787,8 @@ int bc_run_batches(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
     SP_TRY(c.alloc(&bc, n));
     SP_TRY(c.alloc(&chunks, expand_chunk_capacity(g->m)));
     SP_TRY(c.alloc(&cnt, 1));
-    SP_TRY(c.alloc(&counts, 2 + kLanes / 2 + 2));
+    SP_TRY(c.alloc(&counts, 2 + 5));
+    const int fgrid = sms * 2;  // frontier passes: small grids, grid-stride
     if (delta_out) SP_TRY(c.alloc(&dlast, n));
     const BbChunks ck{reg_v, reg_base, reg_nch, items, csum, counts};
     c.persist(lev, kLanes * n * sizeof(int32_t));  // the per-slot probe target
@@ -832,11 +823,32 @@ int bc_run_batches(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
         k_bb_root<<<1, 1, 0, c.stream>>>(lev, sig, stamp, queue, bs);
         c.launches++;
         ls.assign({0, (int64_t)nq0});
-        int64_t mf = 0, mu = g->m;  // push / pull cost of the next step
+        // per-depth frontier pass: out[5 * d .. 5 * d + 4] (see k_bb_frontier)
+        unsigned long long *fo = counts + 2;
+        SP_CUDA(cudaMemsetAsync(fo, 0, 5 * sizeof(unsigned long long), c.stream));
+        k_bb_frontier<<<fgrid, 256, 0, c.stream>>>(lev, g->off, g->roff, queue, nullptr, nq0, 0,
+                                                   fo);
+        c.launches++;
+        int64_t mu = g->m;  // pull cost: in-slots of vertices with an unvisited lane
+        int lane_last[kLanes] = {0};
         for (int d = 0;; d++) {
             const int64_t q0 = ls[d], q1 = ls[d + 1];
+            // the previous frontier pass (depth d) is in fo: read it with this step's counters
             SP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(ExpandCounters), c.stream));
-            const bool pull = d > 0 && pull_ratio > 0 && (double)mf * pull_ratio > (double)mu;
+            if (d == 0) {
+                SP_CUDA(cudaMemcpyAsync(hs, fo, 5 * 8, cudaMemcpyDeviceToHost, c.stream));
+                SP_CUDA(cudaStreamSynchronize(c.stream));
+            }
+            const int64_t mf = (int64_t)hs[0];
+            mu -= (int64_t)hs[1];
+            wk.reached += (int64_t)hs[2];
+            wk.scanned += (int64_t)hs[3];
+            for (int s = 0; s < kLanes; s++)
+                if (hs[4] >> s & 1u) lane_last[s] = d;
+            // pull when its cost (pending in-slots + a sequential pass over
+            // the level array) is below ratio x the push cost
+            const bool pull = d > 0 && pull_ratio > 0 &&
+                              (double)mf * pull_ratio > (double)mu + 0.25 * (double)n;
             if (pull) {
                 wk.pull_steps++;
                 BatchPull f{g->roff, g->radj, lev, sig, stamp, queue + q1, cnt, d};
@@ -845,7 +857,7 @@ int bc_run_batches(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
                 c.launches++;
                 if (g->max_indeg > kBbShort) {
                     k_bb_pull_chunks<<<sms * 8, 256, 0, c.stream>>>(f, ck);
-                    k_bb_pull_finish<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(f, ck);
+                    k_bb_pull_finish<<<sms * 8, 256, 0, c.stream>>>(f, ck);
                     c.launches += 2;
                 }
             } else {
@@ -854,22 +866,19 @@ int bc_run_batches(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
                               sms, big_out, c.stream, &c.launches);
             }
             SP_CUDA(cudaGetLastError());
-            if (pull_ratio > 0) {
-                SP_CUDA(cudaMemsetAsync(counts + 2, 0, 2 * sizeof(unsigned long long), c.stream));
-                k_bb_plan<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(
-                    lev, g->off, g->roff, queue + q1, cnt, n, counts + 2);
-                c.launches++;
-                SP_CUDA(cudaMemcpyAsync(hs, counts + 2, 16, cudaMemcpyDeviceToHost, c.stream));
-            }
+            SP_CUDA(cudaMemsetAsync(fo, 0, 5 * sizeof(unsigned long long), c.stream));
+            k_bb_frontier<<<fgrid, 256, 0, c.stream>>>(lev, g->off, g->roff, queue + q1,
+                                                       &cnt->next_size, 0, d + 1, fo);
+            c.launches++;
+            SP_CUDA(cudaMemcpyAsync(hs, fo, 5 * 8, cudaMemcpyDeviceToHost, c.stream));
             SP_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(ExpandCounters), cudaMemcpyDeviceToHost,
                                     c.stream));
             SP_CUDA(cudaStreamSynchronize(c.stream));
             const int64_t nnew = (int64_t)hc->next_size;
             if (nnew == 0) break;
-            mf = (int64_t)hs[0];
-            mu = (int64_t)hs[1];
             ls.push_back(q1 + nnew);
         }
+        for (int s = 0; s < used; s++) wk.levels += lane_last[s] + 1;
         const int D = (int)ls.size() - 2;  // deepest depth
         const bool is_last = b == nb - 1;
         const int last_lane = (int)((nsrc - 1) % kLanes);
@@ -884,22 +893,11 @@ int bc_run_batches(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
             c.launches++;
             if (d < D && g->max_outdeg > kBbShort) {
                 k_bb_chunks<<<sms * 8, 256, 0, c.stream>>>(f, ck);
-                k_bb_finish<<<grid_for(nq, 256, c.device), 256, 0, c.stream>>>(f, ck);
+                k_bb_finish<<<sms * 8, 256, 0, c.stream>>>(f, ck);
                 c.launches += 2;
             }
             SP_CUDA(cudaGetLastError());
         }
-        SP_CUDA(cudaMemsetAsync(counts + 2, 0, (kLanes / 2 + 2) * sizeof(unsigned long long),
-                                c.stream));
-        k_bb_stats<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(lev, g->off, n, counts + 2);
-        c.launches++;
-        SP_CUDA(cudaMemcpyAsync(hs, counts + 2, 8 * (kLanes / 2 + 2), cudaMemcpyDeviceToHost,
-                                c.stream));
-        SP_CUDA(cudaStreamSynchronize(c.stream));
-        wk.reached += (int64_t)hs[0];
-        wk.scanned += (int64_t)hs[1];
-        const unsigned *lm = reinterpret_cast<const unsigned *>(hs + 2);
-        for (int s = 0; s < used; s++) wk.levels += lm[s];
         if (is_last) {
             if (sigma_out) {
                 double *so;
@@ -961,7 +959,9 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
         size_t fr = 0, tot = 0;
         SP_CUDA(cudaSetDevice(g->device));
         SP_CUDA(cudaMemGetInfo(&fr, &tot));
-        K = (int)std::max<int64_t>(1, std::min<int64_t>(kBbWorkers, nb));
+        const char *ew = getenv("SP_BC_WORKERS");
+        const int64_t want = ew ? std::max(1, atoi(ew)) : kBbWorkers;
+        K = (int)std::max<int64_t>(1, std::min<int64_t>(want, nb));
         while (K > 1 && per * K > 0.6 * (double)fr) K--;
         if (per > 0.6 * (double)fr) batched = false, K = 1;  // per-source state only
     }
