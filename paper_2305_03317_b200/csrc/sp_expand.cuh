@@ -57,6 +57,56 @@ template <class Op, class = void>
 struct HasFar : std::false_type {};
 template <class Op>
 struct HasFar<Op, std::void_t<decltype(Op::kFar)>> : std::integral_constant<bool, Op::kFar> {};
+// Optional phased apply (Op::kPhased): the returning atomics of all of a
+// lane's slots are issued before any result is examined, so their round
+// trips overlap instead of chaining slot after slot:
+//   int a = apply(pay, e, x, probe)         -- phase 1 (predicated atomics)
+//   int b = settle(a, x, pay, probe)        -- phase 2 (predicated atomics)
+//   int r = result(a, b, x, pay, probe)     -- pure
+// x < 0 marks an empty slot (its probe is unset); the Op must ignore it.
+template <class Op, class = void>
+struct IsPhased : std::false_type {};
+template <class Op>
+struct IsPhased<Op, std::void_t<decltype(Op::kPhased)>> : std::integral_constant<bool, Op::kPhased> {};
+
+template <class Op, int K, class PayArr>
+__device__ __forceinline__ void apply_all(const Op &op, int (&res)[K], const int32_t (&x)[K],
+                                          const int64_t (&e)[K], const PayArr &pay,
+                                          const typename Op::Probe (&pr)[K]) {
+    if constexpr (IsPhased<Op>::value) {
+        int a[K], b[K];
+#pragma unroll
+        for (int u = 0; u < K; u++) a[u] = op.apply(pay[u], e[u], x[u], pr[u]);
+#pragma unroll
+        for (int u = 0; u < K; u++) b[u] = op.settle(a[u], x[u], pay[u], pr[u]);
+#pragma unroll
+        for (int u = 0; u < K; u++) res[u] = op.result(a[u], b[u], x[u], pay[u], pr[u]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < K; u++)
+            res[u] = x[u] >= 0 ? (int)op.apply(pay[u], e[u], x[u], pr[u]) : 0;
+    }
+}
+
+// Predicated returning atomics (inline PTX, no branch around them): the
+// result register is only written when p holds.
+__device__ __forceinline__ int atom_min_if(bool p, int32_t *a, int v) {
+    int old;
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %1, 0; @q atom.global.min.s32 %0, [%2], %3; }"
+                 : "=r"(old)
+                 : "r"((unsigned)p), "l"(a), "r"(v)
+                 : "memory");
+    return old;
+}
+__device__ __forceinline__ int atom_exch_if(bool p, int32_t *a, int v) {
+    int old;
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %1, 0; @q atom.global.exch.b32 %0, [%2], %3; }"
+                 : "=r"(old)
+                 : "r"((unsigned)p), "l"(a), "r"(v)
+                 : "memory");
+    return old;
+}
+
 template <class Op, class = void>
 struct HasKeep : std::false_type {};
 template <class Op>
@@ -168,9 +218,7 @@ __device__ __forceinline__ void expand_batch(const Op &op, const int64_t *__rest
         for (int u = 0; u < kRounds; u++)
             if (e[u] >= 0) pr[u] = op.probe(e[u], x[u]);
         int res[kRounds];
-#pragma unroll
-        for (int u = 0; u < kRounds; u++)
-            res[u] = e[u] >= 0 ? (int)op.apply(pv[u], e[u], x[u], pr[u]) : 0;
+        apply_all(op, res, x, e, pv, pr);
         append_results<Op, kRounds>(op, res, x, cnt, qn, st);
     }
 }
@@ -285,9 +333,14 @@ __device__ __forceinline__ void expand_chunks_body(
         for (int j = 0; j < kPer; j++)
             if (x[j] >= 0) pr[j] = op.probe(e0 + j * 32 + lane, x[j]);
         int res[kPer];
+        int64_t ej[kPer];
+        P pj[kPer];
 #pragma unroll
-        for (int j = 0; j < kPer; j++)
-            res[j] = x[j] >= 0 ? (int)op.apply(pay, e0 + j * 32 + lane, x[j], pr[j]) : 0;
+        for (int j = 0; j < kPer; j++) {
+            ej[j] = e0 + j * 32 + lane;
+            pj[j] = pay;
+        }
+        apply_all(op, res, x, ej, pj, pr);
         append_results<Op, kPer>(op, res, x, cnt, qn, st);
         scanned += len;
 #pragma unroll
