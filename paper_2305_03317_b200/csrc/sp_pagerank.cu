@@ -476,7 +476,12 @@ int ensure_pr_hot(sp_graph *g, Call &c) {
     SP_TRY(c.host_as(&hcov));
     SP_CUDA(cudaMemcpyAsync(hcov, cov, 8, cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
-    if ((double)hcov[0] < kHotMinCover * (double)m) {
+    const char *ce = getenv("SP_PR_HOT_COVER");  // tuning override of kHotMinCover
+    const double min_cover = ce ? atof(ce) : kHotMinCover;
+    if (getenv("SP_PR_HOT_VERBOSE"))
+        fprintf(stderr, "pr hot set: top %d sources cover %.3f of the slots\n", H,
+                (double)hcov[0] / (double)m);
+    if ((double)hcov[0] < min_cover * (double)m) {
         g->pr_H = 0;
         return SP_OK;
     }
