@@ -142,6 +142,7 @@ struct sp_graph {
     int32_t *pr_hot_ids = nullptr;
     int32_t *pr_radj_hot = nullptr;
     int pr_H = -1;  // -1: not built, 0: disabled
+    int pr_fast_calls = 0;  // fast PR calls so far (the hot set is built on the second)
 };
 
 // ---- device helpers --------------------------------------------------------

@@ -141,7 +141,13 @@ __device__ __forceinline__ void block_diff(const PrArgs &a, double dmax) {
     if (threadIdx.x < 32) {
         double t = threadIdx.x < 8 ? red[threadIdx.x] : 0.0;
         t = warp_max(t);
-        if (threadIdx.x == 0 && t > 0.0) atomic_max_nonneg(a.diff_slot, t);
+        // read first: same-address atomics from thousands of blocks
+        // serialise at one L2 slice (k_pr_zero: 16 K blocks, ~0.2 ms), and
+        // most blocks do not raise the maximum (order-free: exact either way)
+        if (threadIdx.x == 0 && t > 0.0 &&
+            __double_as_longlong(t) > (long long)__ldcg(
+                reinterpret_cast<const unsigned long long *>(a.diff_slot)))
+            atomic_max_nonneg(a.diff_slot, t);
     }
 }
 
@@ -437,6 +443,11 @@ __global__ void k_hot_encode(const int32_t *__restrict__ radj, int64_t m,
 int ensure_pr_hot(sp_graph *g, Call &c) {
     std::lock_guard<std::mutex> lk(g_hot_mu);
     if (g->pr_H >= 0) return SP_OK;
+    // Built on the graph's second fast PR call: the encoding (a sort of the
+    // out-degrees + one pass over radj, ~0.9 ms at cfg2) costs more than it
+    // saves in a single run (~0.4 ms), so a one-shot run on a fresh graph
+    // keeps the plain kernel (same sums either way).
+    if (g->pr_fast_calls++ == 0) return SP_OK;
     const int64_t n = g->n, m = g->m;
     if (m < kHotMinSlots || n >= kHotBit) {
         g->pr_H = 0;
