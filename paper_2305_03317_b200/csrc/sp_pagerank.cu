@@ -443,16 +443,21 @@ __global__ void k_hot_encode(const int32_t *__restrict__ radj, int64_t m,
 int ensure_pr_hot(sp_graph *g, Call &c) {
     std::lock_guard<std::mutex> lk(g_hot_mu);
     if (g->pr_H >= 0) return SP_OK;
+    const int64_t n = g->n, m = g->m;
+    const char *ce = getenv("SP_PR_HOT_COVER");  // tuning override of kHotMinCover
+    const double min_cover = ce ? atof(ce) : kHotMinCover;
+    // free upper bound on the coverage: H sources of at most max_outdeg
+    // slots each (a grid decides here, without the sort)
+    if (m < kHotMinSlots || n >= kHotBit ||
+        (double)std::min<int64_t>(kHotMax, n) * (double)g->max_outdeg < min_cover * (double)m) {
+        g->pr_H = 0;
+        return SP_OK;
+    }
     // Built on the graph's second fast PR call: the encoding (a sort of the
     // out-degrees + one pass over radj, ~0.9 ms at cfg2) costs more than it
     // saves in a single run (~0.4 ms), so a one-shot run on a fresh graph
     // keeps the plain kernel (same sums either way).
     if (g->pr_fast_calls++ == 0) return SP_OK;
-    const int64_t n = g->n, m = g->m;
-    if (m < kHotMinSlots || n >= kHotBit) {
-        g->pr_H = 0;
-        return SP_OK;
-    }
     const int H = (int)std::min<int64_t>(kHotMax, n);
     uint32_t *key, *key_s;
     int32_t *id, *id_s, *hot_idx;
@@ -487,8 +492,6 @@ int ensure_pr_hot(sp_graph *g, Call &c) {
     SP_TRY(c.host_as(&hcov));
     SP_CUDA(cudaMemcpyAsync(hcov, cov, 8, cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
-    const char *ce = getenv("SP_PR_HOT_COVER");  // tuning override of kHotMinCover
-    const double min_cover = ce ? atof(ce) : kHotMinCover;
     if (getenv("SP_PR_HOT_VERBOSE"))
         fprintf(stderr, "pr hot set: top %d sources cover %.3f of the slots\n", H,
                 (double)hcov[0] / (double)m);

@@ -193,6 +193,13 @@ __global__ void k_big_list(const int32_t *__restrict__ ulen, int64_t n, int thr,
     if ((threadIdx.x & 31) == 0) atomicMax(&cnt[1], mx);
 }
 
+__global__ void k_big_keys(const int32_t *__restrict__ big, const int32_t *__restrict__ ulen,
+                           int64_t nbig, uint32_t *key) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nbig;
+         i += (int64_t)gridDim.x * blockDim.x)
+        key[i] = (uint32_t)ulen[big[i]];
+}
+
 int ensure_upper(sp_graph *g, Call &c) {
     std::lock_guard<std::mutex> lk(g_up_mu);
     if (g->m_up >= 0) return SP_OK;
@@ -248,6 +255,28 @@ int ensure_upper(sp_graph *g, Call &c) {
     SP_CUDA(cudaGetLastError());
     SP_CUDA(cudaMemcpyAsync(h + 1, bc, 16, cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t nbig = (int64_t)h[1];
+    if (nbig > 1) {  // longest rows first (k_tc_big's dynamic schedule)
+        uint32_t *key, *key_s;
+        int32_t *big_s;
+        SP_TRY(c.alloc(&key, nbig));
+        SP_TRY(c.alloc(&key_s, nbig));
+        SP_TRY(c.alloc(&big_s, nbig));
+        k_big_keys<<<grid_for(nbig, 256, c.device), 256, 0, c.stream>>>(big, ulen, nbig, key);
+        size_t stmp = 0;
+        SP_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, stmp, key, key_s, big, big_s,
+                                                          nbig, 0, 32, c.stream));
+        void *st = nullptr;
+        SP_TRY(scratch_alloc(&st, stmp, c.stream));
+        cudaError_t se = cub::DeviceRadixSort::SortPairsDescending(st, stmp, key, key_s, big,
+                                                                   big_s, nbig, 0, 32, c.stream);
+        scratch_free(st, c.stream);
+        SP_CUDA(se);
+        SP_CUDA(cudaMemcpyAsync(big, big_s, nbig * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                c.stream));
+        c.launches += 2;
+        SP_CUDA(cudaStreamSynchronize(c.stream));
+    }
     gd.keep = true;
     g->ubig = big;
     g->nbig = (int64_t)h[1];
@@ -265,6 +294,7 @@ int ensure_upper(sp_graph *g, Call &c) {
 
 struct TcCounters {
     unsigned long long next;    // vertex batch cursor
+    unsigned long long big_next;  // k_tc_big vertex cursor
     unsigned long long total;   // weighted triangle count
     unsigned long long pairs;   // oriented edges (a, b) processed
     unsigned long long elems;   // N+(b) elements probed
@@ -556,9 +586,22 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
     // hashed form (na <= kHashMax): keys[T] then counts[T] from smem[0]
     int32_t *HK = reinterpret_cast<int32_t *>(smem);
     const unsigned lane = lane_id();
-    const int wid = threadIdx.x >> 5;
     unsigned long long cnt = 0, elems = 0, pairs = 0, abytes = 0;
-    for (int64_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+    // Dynamic schedule (big[] is sorted by row length, longest first):
+    // CTAs take vertices from a global cursor and warps take 32-row
+    // batches of the vertex from a shared cursor -- longest-first
+    // assignment keeps the hub tail short on skewed graphs.
+    __shared__ long long s_bi;
+    __shared__ int s_j;
+    for (;;) {
+        __syncthreads();  // every warp is done with the previous vertex
+        if (threadIdx.x == 0) {
+            s_bi = (long long)atomicAdd(&ctr->big_next, 1ull);
+            s_j = 0;
+        }
+        __syncthreads();
+        const int64_t bi = s_bi;
+        if (bi >= nbig) break;
         const int32_t a = big[bi];
         if (a < v0 || a >= v1) continue;  // block-uniform
         const int na = ulen[a];
@@ -612,7 +655,11 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
             pairs += (unsigned long long)na;
             abytes += (unsigned long long)na * (unsigned long long)na;
         }
-        for (int j0 = wid * 32; j0 < na; j0 += (kBigBlock / 32) * 32) {
+        for (;;) {
+            int j0 = 0;
+            if (lane == 0) j0 = atomicAdd(&s_j, 32);
+            j0 = __shfl_sync(0xffffffffu, j0, 0);
+            if (j0 >= na) break;
             const int j = j0 + (int)lane;
             uint2 inf = make_uint2(0u, 0u);
             if (j < na) inf = uinfo[r0 + j];
