@@ -21,7 +21,8 @@
 //              mult(x in N+(a))  (= m_ab * m_bc * m_ac summed per triangle).
 // Kernel k_tc_fwd: persistent warps pull 32-vertex batches from a global
 // counter.  Per vertex a the warp stages A = N+(a), the row starts of its
-// b's (from uinfo) and a prefix of their 32-byte sector counts in shared
+// b's (from uinfo) and a prefix of their element-holding 16-byte half-sector
+// counts (all-padding halves are skipped) in shared
 // memory with a 4096-bit membership filter, then walks all rows N+(b) as one
 // flattened space of 16-byte half-sectors: each lane loads one int4 per step
 // and keeps kUnroll independent loads in flight (the walk is DRAM-latency
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
                                                    int64_t v1, TcCounters *ctr) {
     __shared__ int32_t sA[kWarps][kA];
     __shared__ uint32_t sB[kWarps][kA];       // sector start of row b_j
-    __shared__ int32_t sS[kWarps][kA + 1];    // sector prefix over the rows b_j
+    __shared__ int32_t sS[kWarps][kA + 1];    // half-sector prefix over the rows b_j (element-holding halves only)
     __shared__ uint32_t sF[kWarps][kFilterWords];
     const unsigned lane = lane_id();
     const int wib = threadIdx.x >> 5;
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
                 pairs += (unsigned long long)na;
                 abytes += (unsigned long long)na * (unsigned long long)na;
             }
-            // ---- stage A, row starts, sector prefix and filter
+            // ---- stage A, row starts, half-sector prefix and filter
             for (int k = lane; k < kFilterWords; k += 32) F[k] = 0u;
             __syncwarp();
             int carry = 0;
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
                     const uint2 inf = uinfo[r0 + k];
                     A[k] = x;
                     B[k] = inf.x;
-                    secs = (int)((inf.y + kPad - 1u) / kPad);
+                    secs = (int)((inf.y + 3u) / 4u);  // half-sectors holding elements
                     elems += inf.y;
                     const uint32_t hh = fhash(x);
                     atomicOr(&F[hh >> 5], 1u << (hh & 31));
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
             // ---- flattened walk of all rows b_j in 16-byte half-sectors:
             // one int4 per lane (rows are 32-byte aligned and padded with -1),
             // kUnroll loads in flight per lane, one row search per 4 slots
-            const int nhalf = kQ * carry;
+            const int nhalf = carry;
             for (int h0 = 0; h0 < nhalf; h0 += 32 * kUnroll) {
                 int4 xs[kUnroll];
 #pragma unroll
@@ -379,14 +380,13 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
                     const int h = h0 + u * 32 + (int)lane;
                     xs[u] = make_int4(-1, -1, -1, -1);
                     if (h < nhalf) {
-                        const int sec = h / kQ;
-                        int lo = 0, hi = na;  // last j with S[j] <= sec
+                        int lo = 0, hi = na;  // last j with S[j] <= h
                         while (hi - lo > 1) {
                             const int mid = (lo + hi) >> 1;
-                            if (S[mid] <= sec) lo = mid; else hi = mid;
+                            if (S[mid] <= h) lo = mid; else hi = mid;
                         }
                         xs[u] = __ldg(reinterpret_cast<const int4 *>(uadj) +
-                                      kQ * ((int64_t)B[lo] + (sec - S[lo])) + (h % kQ));
+                                      kQ * (int64_t)B[lo] + (h - S[lo]));
                     }
                 }
 #pragma unroll
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
                                                    int64_t v1, TcCounters *ctr) {
     // per warp, dynamic shared memory: hash keys[kT] + counts[kT] of A,
-    // sector starts B[kA], sector prefix S[kA+1], filter F[kFilterWords]
+    // sector starts B[kA], half-sector prefix S[kA+1], filter F[kFilterWords]
     extern __shared__ uint32_t fwd_smem[];
     const unsigned lane = lane_id();
     const int wib = threadIdx.x >> 5;
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
                         h = (h + 1) & (T - 1);
                     }
                     B[k] = inf.x;
-                    secs = (int)((inf.y + kPad - 1u) / kPad);
+                    secs = (int)((inf.y + 3u) / 4u);  // half-sectors holding elements
                     elems += inf.y;
                     const uint32_t hh = fhash(x);
                     atomicOr(&F[hh >> 5], 1u << (hh & 31));
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
             // ---- flattened walk of all rows b_j in 16-byte half-sectors:
             // one int4 per lane (rows are 32-byte aligned and padded with -1),
             // kUnroll loads in flight per lane, one row search per 4 slots
-            const int nhalf = kQ * carry;
+            const int nhalf = carry;
             for (int h0 = 0; h0 < nhalf; h0 += 32 * kUnroll) {
                 int4 xs[kUnroll];
 #pragma unroll
@@ -509,14 +509,13 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
                     const int h = h0 + u * 32 + (int)lane;
                     xs[u] = make_int4(-1, -1, -1, -1);
                     if (h < nhalf) {
-                        const int sec = h / kQ;
-                        int lo = 0, hi = na;  // last j with S[j] <= sec
+                        int lo = 0, hi = na;  // last j with S[j] <= h
                         while (hi - lo > 1) {
                             const int mid = (lo + hi) >> 1;
-                            if (S[mid] <= sec) lo = mid; else hi = mid;
+                            if (S[mid] <= h) lo = mid; else hi = mid;
                         }
                         xs[u] = __ldg(reinterpret_cast<const int4 *>(uadj) +
-                                      kQ * ((int64_t)B[lo] + (sec - S[lo])) + (h % kQ));
+                                      kQ * (int64_t)B[lo] + (h - S[lo]));
                     }
                 }
 #pragma unroll
@@ -664,7 +663,7 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
             uint2 inf = make_uint2(0u, 0u);
             if (j < na) inf = uinfo[r0 + j];
             elems += inf.y;
-            const int secs = (int)((inf.y + kPad - 1u) / kPad);
+            const int secs = (int)((inf.y + 3u) / 4u);  // half-sectors holding elements
             int incl = secs;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -672,22 +671,21 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
                 if ((int)lane >= o) incl += t;
             }
             const int excl = incl - secs;
-            const int nhalf = kQ * __shfl_sync(0xffffffffu, incl, 31);
+            const int nhalf = __shfl_sync(0xffffffffu, incl, 31);
             for (int h0 = 0; h0 < nhalf; h0 += 32) {
                 const int h = h0 + (int)lane;
-                const int sec = h / kQ;
-                int lo = 0;  // owner lane: largest with excl <= sec
+                int lo = 0;  // owner lane: largest with excl <= h
 #pragma unroll
                 for (int step = 16; step > 0; step >>= 1) {
                     const int cand = lo + step;
                     const int ex = __shfl_sync(0xffffffffu, excl, cand & 31);
-                    if (cand < 32 && ex <= sec) lo = cand;
+                    if (cand < 32 && ex <= h) lo = cand;
                 }
                 const int ex = __shfl_sync(0xffffffffu, excl, lo);
                 const uint32_t s8 = __shfl_sync(0xffffffffu, inf.x, lo);
                 if (h >= nhalf) continue;
                 const int4 xs = __ldg(reinterpret_cast<const int4 *>(uadj) +
-                                      kQ * ((int64_t)s8 + (sec - ex)) + (h % kQ));
+                                      kQ * (int64_t)s8 + (h - ex));
                 const int32_t xv[4] = {xs.x, xs.y, xs.z, xs.w};
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
