@@ -57,7 +57,8 @@ constexpr int kFwdWarpWords = 2 * kT + 2 * kA + 1 + 128;  // per-warp shared wor
 constexpr int kFilterWords = 128;  // 4096-bit filter per warp
 constexpr int kFilterShift = 20;   // 32 - log2(4096)
 constexpr int kBatch = 32;
-constexpr int kUnroll = 2;         // 16-byte loads in flight per lane in k_tc_fwd
+constexpr int kUnroll = 2;         // 16-byte loads in flight per lane in k_tc_fwd_plain
+constexpr int kUnrollHash = 4;     // ... in k_tc_fwd_hash (skewed graphs; 2 is faster on cfg3)
 constexpr int kPad = 8;            // upper rows padded/aligned to 32-byte sectors
 constexpr int kQ = kPad / 4;       // 16-byte quarters per padded block
 
@@ -500,12 +501,12 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
             __syncwarp();
             // ---- flattened walk of all rows b_j in 16-byte half-sectors:
             // one int4 per lane (rows are 32-byte aligned and padded with -1),
-            // kUnroll loads in flight per lane, one row search per 4 slots
+            // kUnrollHash loads in flight per lane, one row search per 4 slots
             const int nhalf = carry;
-            for (int h0 = 0; h0 < nhalf; h0 += 32 * kUnroll) {
-                int4 xs[kUnroll];
+            for (int h0 = 0; h0 < nhalf; h0 += 32 * kUnrollHash) {
+                int4 xs[kUnrollHash];
 #pragma unroll
-                for (int u = 0; u < kUnroll; u++) {
+                for (int u = 0; u < kUnrollHash; u++) {
                     const int h = h0 + u * 32 + (int)lane;
                     xs[u] = make_int4(-1, -1, -1, -1);
                     if (h < nhalf) {
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < kUnroll; u++) {
+                for (int u = 0; u < kUnrollHash; u++) {
                     const int32_t xv[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
