@@ -545,32 +545,48 @@ __global__ void __launch_bounds__(256) k_bb_rows(BatchFold f, const int32_t *__r
 // One warp per chunk: lanes take slots j*32 + lane, then a fixed-shape warp
 // reduction per source lane into the chunk's partials.
 __global__ void __launch_bounds__(256) k_bb_chunks(BatchFold f, BbChunks ck) {
+    constexpr int kPer = kBbSplit / 32;
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nitems = (int64_t)__ldcg(&ck.counts[1]);
-    for (int64_t k = warp; k < nitems; k += nwarps) {
-        const uint4 it = ck.items[k];
-        const int32_t v = ck.reg_v[it.x];
-        const unsigned act = lanes_eq(load_lev_ro(f.lev, v), f.d);
+    const uint4 none = make_uint4(0, 0, 0, 0);
+    // software pipeline over the warp's chunks: the descriptor two ahead and
+    // the slots + row lanes of the next chunk load while this chunk's level
+    // and coef reads are in flight
+    auto load = [&](const uint4 it, int32_t (&w)[kPer], unsigned &act) {
         const int64_t s0 = (int64_t)(((uint64_t)it.z << 32) | it.y);
-        int32_t w[kBbSplit / 32];
 #pragma unroll
-        for (int j = 0; j < kBbSplit / 32; j++) {
+        for (int j = 0; j < kPer; j++) {
             const unsigned p = j * 32 + lane;
             w[j] = p < it.w ? __ldcs(f.adj + s0 + p) : -1;
         }
+        act = it.w ? lanes_eq(load_lev_ro(f.lev, ck.reg_v[it.x]), f.d) : 0u;
+    };
+    int32_t w[kPer];
+    unsigned act;
+    load(warp < nitems ? ck.items[warp] : none, w, act);
+    uint4 d1 = warp + nwarps < nitems ? ck.items[warp + nwarps] : none;
+    for (int64_t k = warp; k < nitems; k += nwarps) {
+        const uint4 d2 = k + 2 * nwarps < nitems ? ck.items[k + 2 * nwarps] : none;
+        int32_t wn[kPer];
+        unsigned actn;
+        load(d1, wn, actn);
+        unsigned m[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; j++)
+            m[j] = w[j] >= 0 ? lanes_eq(load_lev_ro(f.lev, w[j]), f.d + 1) & act : 0u;
         double acc[kLanes];
 #pragma unroll
         for (int s = 0; s < kLanes; s++) acc[s] = 0.0;
-        unsigned m[kBbSplit / 32];
 #pragma unroll
-        for (int j = 0; j < kBbSplit / 32; j++)
-            m[j] = w[j] >= 0 ? lanes_eq(load_lev_ro(f.lev, w[j]), f.d + 1) & act : 0u;
-#pragma unroll
-        for (int j = 0; j < kBbSplit / 32; j++)
+        for (int j = 0; j < kPer; j++)
             if (m[j]) add_lanes(f.coef + kLanes * (int64_t)w[j], m[j], acc);
         bb_store_chunk(ck, k, act, acc);
+#pragma unroll
+        for (int j = 0; j < kPer; j++) w[j] = wn[j];
+        act = actn;
+        d1 = d2;
     }
 }
 
@@ -664,32 +680,46 @@ __global__ void __launch_bounds__(256) k_bb_pull_rows(BatchPull f, int64_t n, Bb
 }
 
 __global__ void __launch_bounds__(256) k_bb_pull_chunks(BatchPull f, BbChunks ck) {
+    constexpr int kPer = kBbSplit / 32;
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nitems = (int64_t)__ldcg(&ck.counts[1]);
-    for (int64_t k = warp; k < nitems; k += nwarps) {
-        const uint4 it = ck.items[k];
-        const int32_t w = ck.reg_v[it.x];
-        const unsigned pm = lanes_eq(load_lev_ro(f.lev, w), -1);
+    const uint4 none = make_uint4(0, 0, 0, 0);
+    // pipelined like k_bb_chunks
+    auto load = [&](const uint4 it, int32_t (&v)[kPer], unsigned &pm) {
         const int64_t s0 = (int64_t)(((uint64_t)it.z << 32) | it.y);
-        int32_t v[kBbSplit / 32];
 #pragma unroll
-        for (int j = 0; j < kBbSplit / 32; j++) {
+        for (int j = 0; j < kPer; j++) {
             const unsigned p = j * 32 + lane;
             v[j] = p < it.w ? __ldcs(f.radj + s0 + p) : -1;
         }
-        unsigned m[kBbSplit / 32];
+        pm = it.w ? lanes_eq(load_lev_ro(f.lev, ck.reg_v[it.x]), -1) : 0u;
+    };
+    int32_t v[kPer];
+    unsigned pm;
+    load(warp < nitems ? ck.items[warp] : none, v, pm);
+    uint4 d1 = warp + nwarps < nitems ? ck.items[warp + nwarps] : none;
+    for (int64_t k = warp; k < nitems; k += nwarps) {
+        const uint4 d2 = k + 2 * nwarps < nitems ? ck.items[k + 2 * nwarps] : none;
+        int32_t vn[kPer];
+        unsigned pmn;
+        load(d1, vn, pmn);
+        unsigned m[kPer];
 #pragma unroll
-        for (int j = 0; j < kBbSplit / 32; j++)
+        for (int j = 0; j < kPer; j++)
             m[j] = v[j] >= 0 ? lanes_eq(load_lev_ro(f.lev, v[j]), f.d) & pm : 0u;
         double acc[kLanes];
 #pragma unroll
         for (int s = 0; s < kLanes; s++) acc[s] = 0.0;
 #pragma unroll
-        for (int j = 0; j < kBbSplit / 32; j++)
+        for (int j = 0; j < kPer; j++)
             if (m[j]) add_lanes(f.sig + kLanes * (int64_t)v[j], m[j], acc);
         bb_store_chunk(ck, k, pm, acc);
+#pragma unroll
+        for (int j = 0; j < kPer; j++) v[j] = vn[j];
+        pm = pmn;
+        d1 = d2;
     }
 }
 
