@@ -136,6 +136,7 @@ struct sp_graph {
     int64_t m_up_pad = 0;   // padded slots
     int32_t *ubig = nullptr;  // vertices whose upper row exceeds the warp path
     int64_t nbig = 0, max_ulen = 0;
+    int tc_warp_max = 256;  // upper rows longer than this are in ubig (k_tc_big)
     // PageRank hot sources (built by the first fast PR call): the pr_H
     // vertices of largest out-degree, and radj re-encoded so that a slot
     // whose source is hot carries (1 << 30) | hot index

@@ -39,6 +39,7 @@
 // follows tc.sp literally -- per middle vertex v, A = N(v)_{>v} staged with
 // the same filter, each slot u < v of N(v) scans N(u)_{>v}.
 #include <cub/cub.cuh>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
@@ -252,7 +253,10 @@ int ensure_upper(sp_graph *g, Call &c) {
     unsigned long long *bc;
     SP_TRY(c.alloc(&bc, 2));
     SP_CUDA(cudaMemsetAsync(bc, 0, 2 * sizeof(unsigned long long), c.stream));
-    k_big_list<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(ulen, n, kA, big, bc);
+    // SP_TC_WARP_MAX (tests): route shorter rows to k_tc_big too (<= kA)
+    const char *wm = getenv("SP_TC_WARP_MAX");
+    const int warp_max = wm ? std::max(1, std::min(kA, atoi(wm))) : kA;
+    k_big_list<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(ulen, n, warp_max, big, bc);
     c.launches += 4;
     SP_CUDA(cudaGetLastError());
     SP_CUDA(cudaMemcpyAsync(h + 1, bc, 16, cudaMemcpyDeviceToHost, c.stream));
@@ -280,6 +284,7 @@ int ensure_upper(sp_graph *g, Call &c) {
         SP_CUDA(cudaStreamSynchronize(c.stream));
     }
     gd.keep = true;
+    g->tc_warp_max = warp_max;
     g->ubig = big;
     g->nbig = (int64_t)h[1];
     g->max_ulen = (int64_t)h[2];
@@ -309,7 +314,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
                                                    const int32_t *__restrict__ ulen,
                                                    const int32_t *__restrict__ uadj,
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
-                                                   int64_t v1, TcCounters *ctr) {
+                                                   int64_t v1, int amax, TcCounters *ctr) {
     __shared__ int32_t sA[kWarps][kA];
     __shared__ uint32_t sB[kWarps][kA];       // sector start of row b_j
     __shared__ int32_t sS[kWarps][kA + 1];    // half-sector prefix over the rows b_j (element-holding halves only)
@@ -337,7 +342,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
             const int na = __shfl_sync(0xffffffffu, my_len, src);
             if (na < 2) continue;  // a triangle needs b and x in N+(a)
             const int64_t r0 = kPad * (int64_t)__shfl_sync(0xffffffffu, my_s8, src);
-            if (na > kA) continue;  // k_tc_big (one CTA per vertex) counts it
+            if (na > amax) continue;  // k_tc_big (one CTA per vertex) counts it
             if (lane == 0) {
                 pairs += (unsigned long long)na;
                 abytes += (unsigned long long)na * (unsigned long long)na;
@@ -421,7 +426,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
                                                    const int32_t *__restrict__ ulen,
                                                    const int32_t *__restrict__ uadj,
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
-                                                   int64_t v1, TcCounters *ctr) {
+                                                   int64_t v1, int amax, TcCounters *ctr) {
     // per warp, dynamic shared memory: hash keys[kT] + counts[kT] of A,
     // sector starts B[kA], half-sector prefix S[kA+1], filter F[kFilterWords]
     extern __shared__ uint32_t fwd_smem[];
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
             const int na = __shfl_sync(0xffffffffu, my_len, src);
             if (na < 2) continue;  // a triangle needs b and x in N+(a)
             const int64_t r0 = kPad * (int64_t)__shfl_sync(0xffffffffu, my_s8, src);
-            if (na > kA) continue;  // k_tc_big (one CTA per vertex) counts it
+            if (na > amax) continue;  // k_tc_big (one CTA per vertex) counts it
             if (lane == 0) {
                 pairs += (unsigned long long)na;
                 abytes += (unsigned long long)na * (unsigned long long)na;
@@ -579,7 +584,7 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
                                                       const uint2 *__restrict__ uinfo,
                                                       const int32_t *__restrict__ big,
                                                       int64_t nbig, int64_t v0, int64_t v1,
-                                                      TcCounters *ctr) {
+                                                      int hash_max, int big_max, TcCounters *ctr) {
     extern __shared__ uint32_t smem[];
     uint32_t *F = smem;                                        // kBigFilterBits / 32 words
     int32_t *A = reinterpret_cast<int32_t *>(smem + kBigFilterBits / 32);
@@ -606,8 +611,8 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
         if (a < v0 || a >= v1) continue;  // block-uniform
         const int na = ulen[a];
         const int64_t r0 = kPad * (int64_t)ustart8[a];
-        const bool staged = na <= kBigMax;
-        const bool hashed = na <= kHashMax;
+        const bool staged = na <= big_max;
+        const bool hashed = na <= hash_max;
         int tbits = 6;  // table of 2^tbits >= 2 na entries
         while ((1 << tbits) < 2 * na) tbits++;
         const int T = 1 << tbits;
@@ -817,18 +822,25 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
                 SP_CUDA(cudaFuncSetAttribute(k_tc_fwd_hash,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
                 k_tc_fwd_hash<<<grid, kBlock, fsm, c.stream>>>(g->ustart8, g->ulen, g->uadj,
-                                                               g->uinfo, v0, v1, ctr);
+                                                               g->uinfo, v0, v1, g->tc_warp_max,
+                                                               ctr);
             } else {
                 k_tc_fwd_plain<<<grid, kBlock, 0, c.stream>>>(g->ustart8, g->ulen, g->uadj,
-                                                              g->uinfo, v0, v1, ctr);
+                                                              g->uinfo, v0, v1, g->tc_warp_max,
+                                                              ctr);
             }
             c.launches++;
             if (g->nbig) {
+                // row-form limits (SP_TC_HASH_MAX / SP_TC_BIG_MAX: tests, to reach the
+                // staged and global-search forms on small graphs)
+                const char *hm = getenv("SP_TC_HASH_MAX"), *bm = getenv("SP_TC_BIG_MAX");
+                const int hash_max = hm ? std::max(1, std::min(kHashMax, atoi(hm))) : kHashMax;
+                const int big_max = bm ? std::max(1, std::min(kBigMax, atoi(bm))) : kBigMax;
                 int tb = 6;
-                while ((1 << tb) < 2 * std::min<int64_t>(g->max_ulen, kHashMax)) tb++;
+                while ((1 << tb) < 2 * std::min<int64_t>(g->max_ulen, hash_max)) tb++;
                 const size_t smem = std::max<size_t>(
                     ((size_t)8 << tb) + ((size_t)1 << tb),  // hash keys + counts + filter
-                    kBigFilterBits / 8 + 4 * (size_t)std::min<int64_t>(g->max_ulen, kBigMax));
+                    kBigFilterBits / 8 + 4 * (size_t)std::min<int64_t>(g->max_ulen, big_max));
                 SP_CUDA(cudaFuncSetAttribute(k_tc_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
                 int per_sm = 1;
@@ -836,7 +848,8 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
                 const int gb = (int)std::min<int64_t>(g->nbig,
                                                       (int64_t)sms * std::max(1, per_sm));
                 k_tc_big<<<gb, kBigBlock, smem, c.stream>>>(g->ustart8, g->ulen, g->uadj, g->uinfo,
-                                                         g->ubig, g->nbig, v0, v1, ctr);
+                                                         g->ubig, g->nbig, v0, v1, hash_max,
+                                                         big_max, ctr);
                 c.launches++;
             }
         }

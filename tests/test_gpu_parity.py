@@ -450,6 +450,38 @@ def test_tc_dense_rows_cta_path(n, p, seed):
     assert sp.run(corpus.TC, g, {}).env.scalars["triangle_count"] == cpu_ref.tc(o, nthreads=8)
 
 
+TC_FORMS = [{"SP_TC_WARP_MAX": "16"},
+            {"SP_TC_WARP_MAX": "16", "SP_TC_HASH_MAX": "32"},
+            {"SP_TC_WARP_MAX": "16", "SP_TC_HASH_MAX": "32", "SP_TC_BIG_MAX": "64"}]
+
+
+@pytest.mark.parametrize("form", TC_FORMS, ids=["hashed", "staged", "global"])
+@pytest.mark.parametrize("graph", ["dense_dup", "rmat_sym"])
+def test_tc_big_row_forms(graph, form, monkeypatch):
+    """k_tc_big's three row forms -- shared hash table, staged A with a
+    filter + binary search, and binary search in global memory -- are
+    normally reached only by rows longer than 256 / 8 K / 48 K; lowered
+    thresholds route small graphs through each form, against the oracle
+    (parallel edges included: multiplicity products)."""
+    for k, val in form.items():
+        monkeypatch.setenv(k, val)
+    if graph == "dense_dup":
+        rng = np.random.default_rng(9)
+        n = 500
+        iu, ju = np.triu_indices(n, 1)
+        keep = rng.random(len(iu)) < 0.3
+        u, v = iu[keep], ju[keep]
+        dup = rng.random(len(u)) < 0.02
+        u = np.concatenate([u, u[dup]])
+        v = np.concatenate([v, v[dup]])
+        w = np.ones(len(u), dtype=np.int64)
+    else:
+        u, v, w, n = gen.rmat(13, 16, seed=4, undirected=True)
+    g = sp.from_arrays(u, v, w, directed=False, n=n)
+    o = cpu_ref.build_csr(u, v, w, False, n)
+    assert sp.run(corpus.TC, g, {}).env.scalars["triangle_count"] == cpu_ref.tc(o, nthreads=8)
+
+
 @pytest.mark.parametrize("case", CASES)
 def test_native_loader_builds_reference_csr(case, tmp_path):
     """load_edge_list through the native parser (mixed \\n / \\r\\n / \\r line
