@@ -48,6 +48,11 @@ def test_pr_cfg2_full(rmat22):
     assert r.env.scalars["iter"] == it
     rel = np.abs(r.env.node_props["rank"] - rank).max() / np.abs(rank).max()
     assert rel <= 1e-12
+    # the second fast call on the graph builds and uses the hot-source
+    # shared-memory set: the same values, so the same bits
+    r2 = sp.run(corpus.PR, g, PR_ARGS)
+    assert r2.env.node_props["rank"].tobytes() == r.env.node_props["rank"].tobytes()
+    assert r2.env.scalars["iter"] == it
     rd = sp.run(corpus.PR, g, PR_ARGS, deterministic=True)
     assert rd.env.node_props["rank"].tobytes() == rank.tobytes()
     assert rd.env.scalars["iter"] == it and rd.env.scalars["diff"] == diff

@@ -192,6 +192,21 @@ def test_pagerank_seeded(kind, p0, p1, und):
     assert rf.env.scalars["iter"] == it
 
 
+@pytest.mark.parametrize("und", [False, True])
+def test_pagerank_hot_source_path(und, monkeypatch):
+    """PR's hot-source variant (the top out-degree sources' contribs in
+    shared memory, built on a graph's second fast call) gives the plain
+    kernel's bits; forced on with SP_PR_HOT_COVER=0 on RMAT-17."""
+    monkeypatch.setenv("SP_PR_HOT_COVER", "0")
+    g, o = _pair("rmat", 17, 16, 3, und)
+    rank, it, diff, its, rc = cpu_ref.pagerank(o, 0.85, 1e-6, 100, cap=10 ** 6, nthreads=4)
+    r1 = sp.run(corpus.PR, g, PR_ARGS)   # plain kernel
+    r2 = sp.run(corpus.PR, g, PR_ARGS)   # hot-source kernel
+    assert r2.env.node_props["rank"].tobytes() == r1.env.node_props["rank"].tobytes()
+    assert rel_err(r2.env.node_props["rank"], rank) <= 1e-12
+    assert r1.env.scalars["iter"] == r2.env.scalars["iter"] == it
+
+
 @pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 13, 16, True), ("rmat", 12, 16, False),
                                             ("grid", 40, 40, True)])
 def test_bc_seeded(kind, p0, p1, und):
