@@ -425,13 +425,130 @@ int build_reverse_adj(sp_graph *g, Call &c) {
     return SP_OK;
 }
 
+// ---- pipelined upload + reverse build (host CSR input, directed) -------
+// The adjacency crosses PCIe in kUpChunks pieces on a copy stream; each
+// piece is stably sorted by destination (carrying its source ids, which
+// come from the offsets alone) while the next one is in flight, and its
+// row starts start_i[x] = #(keys < x in piece i) are recorded.  Then
+// roff[x] = sum_i start_i[x], and element j of piece i with destination x
+// lands at roff[x] + sum_{i' < i} cnt_i'(x) + (j - start_i[x]) -- the
+// (dst, src) order of graph.py:92, with one scatter after the last piece
+// instead of a full sort behind the whole upload.
+constexpr int kUpChunks = 8;
+constexpr int64_t kUpMinSlots = int64_t(1) << 23;  // smaller graphs: one copy + one sort
+
+// start[x] = first j with key[j] >= x, x in [0, n] (key sorted, mc keys)
+__global__ void k_start32(const uint32_t *__restrict__ key, int64_t mc, int64_t n,
+                          uint32_t *start) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= mc;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t prev = e == 0 ? -1 : (int64_t)key[e - 1];
+        const int64_t cur = e == mc ? n : (int64_t)key[e];
+        for (int64_t x = prev + 1; x <= cur; x++) start[x] = (uint32_t)e;
+    }
+}
+
+// roff[x] and base_i[x] = roff[x] + sum_{i'<i} cnt_i'(x) - start_i[x]
+__global__ void k_up_bases(const uint32_t *__restrict__ start, int C, int64_t n, int64_t *roff,
+                           int64_t *base) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = 0;
+        for (int i = 0; i < C; i++) r += start[(int64_t)i * (n + 1) + x];
+        roff[x] = r;
+        if (x == n) continue;
+        int64_t before = 0;
+        for (int i = 0; i < C; i++) {
+            const int64_t si = start[(int64_t)i * (n + 1) + x];
+            base[(int64_t)i * n + x] = r + before - si;
+            before += (int64_t)start[(int64_t)i * (n + 1) + x + 1] - si;
+        }
+    }
+}
+
+__global__ void k_up_scatter(const uint32_t *__restrict__ dks, const uint32_t *__restrict__ svs,
+                             int64_t mc, const int64_t *__restrict__ base, int32_t *radj) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < mc;
+         j += (int64_t)gridDim.x * blockDim.x)
+        radj[base[dks[j]] + j] = (int32_t)svs[j];
+}
+
+int upload_adj_build_reverse(sp_graph *g, Call &c, const int32_t *adj_host) {
+    const int64_t n = g->n, m = g->m;
+    const int b = bits_for(n);
+    const int C = kUpChunks;
+    uint32_t *sv, *dks, *svs, *start;
+    int64_t *base;
+    SP_TRY(c.alloc(&sv, m));
+    SP_TRY(c.alloc(&dks, m));
+    SP_TRY(c.alloc(&svs, m));
+    SP_TRY(c.alloc(&start, (int64_t)C * (n + 1)));
+    SP_TRY(c.alloc(&base, (int64_t)C * n + 1));
+    SP_TRY(dalloc(&g->roff, n + 1));
+    SP_TRY(dalloc(&g->radj, m));
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[kUpChunks] = {}, ready = nullptr;
+    struct Res {
+        cudaStream_t *s;
+        cudaEvent_t *e;
+        cudaEvent_t *r;
+        ~Res() {
+            for (int i = 0; i < kUpChunks; i++)
+                if (e[i]) cudaEventDestroy(e[i]);
+            if (*r) cudaEventDestroy(*r);
+            if (*s) cudaStreamDestroy(*s);
+        }
+    } res{&cs, ev, &ready};
+    SP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    SP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    for (int i = 0; i < C; i++) SP_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    // the copies may only start once the call's stream has allocated g->adj
+    SP_CUDA(cudaEventRecord(ready, c.stream));
+    SP_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+    int64_t cut[kUpChunks + 1];
+    for (int i = 0; i <= C; i++) cut[i] = m * i / C;
+    for (int i = 0; i < C; i++) {
+        SP_CUDA(cudaMemcpyAsync(g->adj + cut[i], adj_host + cut[i],
+                                (cut[i + 1] - cut[i]) * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                cs));
+        SP_CUDA(cudaEventRecord(ev[i], cs));
+    }
+    // source of every slot, from the offsets only (overlaps the copies)
+    SP_CUDA(cudaMemsetAsync(sv, 0, m * sizeof(uint32_t), c.stream));
+    k_row_starts<<<gridN(n, c.device), 256, 0, c.stream>>>(g->off, n, sv);
+    SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+        return cub::DeviceScan::InclusiveScan(t, sz, sv, sv, MaxU32(), m, c.stream);
+    }));
+    const uint32_t *dk = reinterpret_cast<const uint32_t *>(g->adj);
+    for (int i = 0; i < C; i++) {
+        const int64_t e0 = cut[i], mc = cut[i + 1] - cut[i];
+        SP_CUDA(cudaStreamWaitEvent(c.stream, ev[i], 0));
+        if (mc)
+            SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
+                return cub::DeviceRadixSort::SortPairs(t, sz, dk + e0, dks + e0, sv + e0,
+                                                       svs + e0, mc, 0, b, c.stream);
+            }));
+        k_start32<<<gridN(mc + 1, c.device), 256, 0, c.stream>>>(dks + e0, mc, n,
+                                                                start + (int64_t)i * (n + 1));
+    }
+    k_up_bases<<<gridN(n + 1, c.device), 256, 0, c.stream>>>(start, C, n, g->roff, base);
+    for (int i = 0; i < C; i++) {
+        const int64_t e0 = cut[i], mc = cut[i + 1] - cut[i];
+        if (mc)
+            k_up_scatter<<<gridN(mc, c.device), 256, 0, c.stream>>>(
+                dks + e0, svs + e0, mc, base + (int64_t)i * n, g->radj);
+    }
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
 int build_reverse(sp_graph *g, Call &c, bool want_adj, bool want_eid) {
     if (want_adj && !want_eid) return build_reverse_adj(g, c);
     if (g->m < (int64_t)0xFFFFFFFFll) return build_reverse_t<uint32_t>(g, c, want_adj, want_eid);
     return build_reverse_t<uint64_t>(g, c, want_adj, want_eid);
 }
 
-int finish_graph(sp_graph *g, Call &c) {
+int finish_graph(sp_graph *g, Call &c, bool unit_weights = false) {
     int64_t n = g->n, m = g->m;
     unsigned long long *cnt;
     SP_TRY(c.alloc(&cnt, 4));
@@ -439,7 +556,7 @@ int finish_graph(sp_graph *g, Call &c) {
     SP_TRY(dalloc(&g->outdeg, n));
     k_deg<<<gridN(n, c.device), 256, 0, c.stream>>>(g->off, n, g->outdeg, cnt + 0);
     if (g->directed) {
-        SP_TRY(build_reverse(g, c, true, false));
+        if (!g->roff) SP_TRY(build_reverse(g, c, true, false));  // else built while uploading
         SP_TRY(dalloc(&g->indeg, n));
         k_deg<<<gridN(n, c.device), 256, 0, c.stream>>>(g->roff, n, g->indeg, cnt + 1);
     } else {
@@ -462,7 +579,12 @@ int finish_graph(sp_graph *g, Call &c) {
     SP_TRY(dalloc(&g->wrange, 2));
     int32_t init[2] = {0x7fffffff, (int32_t)0x80000000};
     SP_CUDA(cudaMemcpyAsync(g->wrange, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
-    if (m) k_wrange<<<gridN(m, c.device), 256, 0, c.stream>>>(g->w, m, g->wrange);
+    if (m && unit_weights) {  // every slot weight 1: no pass over w
+        const int32_t one[2] = {1, 1};
+        SP_CUDA(cudaMemcpyAsync(g->wrange, one, sizeof(one), cudaMemcpyHostToDevice, c.stream));
+    } else if (m) {
+        k_wrange<<<gridN(m, c.device), 256, 0, c.stream>>>(g->w, m, g->wrange);
+    }
     unsigned long long h[4];
     SP_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
@@ -696,14 +818,22 @@ int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj, const int32_t 
         if ((rc = dalloc(&g->adj, m))) break;
         if ((rc = dalloc(&g->w, m))) break;
         if ((rc = to_device(g->off, offsets, (n + 1) * 8, mem, c.stream))) break;
-        if ((rc = to_device(g->adj, adj, m * 4, mem, c.stream))) break;
+        // large directed host CSR: the reverse CSR is built while the
+        // adjacency is still crossing PCIe
+        const bool pipelined = directed && mem == SP_MEM_HOST && m >= kUpMinSlots &&
+                               m < (int64_t)0xFFFFFFFFll && !getenv("SP_UPLOAD_PLAIN");
+        if (pipelined) {
+            if ((rc = upload_adj_build_reverse(g, c, adj))) break;
+        } else if ((rc = to_device(g->adj, adj, m * 4, mem, c.stream))) {
+            break;
+        }
         if (weights) {
             if ((rc = to_device(g->w, weights, m * 4, mem, c.stream))) break;
         } else if (m) {  // unweighted CSR: every slot has the default weight 1
             k_fill_w<<<gridN(m, c.device), 256, 0, c.stream>>>(g->w, m, 1);
         }
         // w_eff is built on first use (ensure_weff): PR/BC/TC never read it
-        if ((rc = finish_graph(g, c))) break;
+        if ((rc = finish_graph(g, c, weights == nullptr))) break;
         rc = c.finish(nullptr);
     } while (0);
     if (rc != SP_OK) {
