@@ -150,6 +150,11 @@ struct sp_graph {
 namespace sp {
 
 // Build the graph's w_eff array if it was deferred (thread-safe).
+// PageRank hot-source selection (sp_pagerank.cu): for graph builders that
+// encode radj while writing it (slot = kPrHotBit | hot index when hot).
+constexpr int kPrHotBit = 1 << 30;
+int pr_hot_prepare(sp_graph *g, Call &c, const int32_t *outdeg, int64_t max_outdeg,
+                   int32_t **hot_idx, int *H);
 int ensure_weff(sp_graph *g, Call &c);
 // Reverse-slot weights rweff[k] = w_eff[reid[k]] (undirected: w_eff itself).
 int ensure_rweff(sp_graph *g, Call &c);

@@ -466,11 +466,36 @@ __global__ void k_up_bases(const uint32_t *__restrict__ start, int C, int64_t n,
     }
 }
 
+// radj (and, when the PR hot set exists, its hot-encoded copy) in one pass
 __global__ void k_up_scatter(const uint32_t *__restrict__ dks, const uint32_t *__restrict__ svs,
-                             int64_t mc, const int64_t *__restrict__ base, int32_t *radj) {
+                             int64_t mc, const int64_t *__restrict__ base, int32_t *radj,
+                             const int32_t *__restrict__ hot_idx, int32_t *enc) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < mc;
-         j += (int64_t)gridDim.x * blockDim.x)
-        radj[base[dks[j]] + j] = (int32_t)svs[j];
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pos = base[dks[j]] + j;
+        const int32_t u = (int32_t)svs[j];
+        radj[pos] = u;
+        if (enc) {
+            const int32_t h = hot_idx[u];
+            enc[pos] = h >= 0 ? (kPrHotBit | h) : u;
+        }
+    }
+}
+
+__global__ void k_outdeg(const int64_t *__restrict__ off, int64_t n, int32_t *deg,
+                         unsigned long long *mx) {
+    unsigned long long best = 0;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = off[x + 1] - off[x];
+        deg[x] = (int32_t)d;
+        best = best > (unsigned long long)d ? best : (unsigned long long)d;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+        best = best > t ? best : t;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(mx, best);
 }
 
 int upload_adj_build_reverse(sp_graph *g, Call &c, const int32_t *adj_host) {
@@ -519,6 +544,25 @@ int upload_adj_build_reverse(sp_graph *g, Call &c, const int32_t *adj_host) {
     SP_TRY(cub_call(c, [&](void *t, size_t &sz) {
         return cub::DeviceScan::InclusiveScan(t, sz, sv, sv, MaxU32(), m, c.stream);
     }));
+    // PageRank hot sources, chosen from the offsets alone while the copies
+    // run: the scatter below then writes the hot-encoded radj too, so the
+    // first PR call on the graph already has it (sp_pagerank.cu)
+    int32_t *hot_idx = nullptr, *enc = nullptr;
+    int H = 0;
+    if (!getenv("SP_UPLOAD_NO_HOT")) {
+        int32_t *deg;
+        unsigned long long *mx;
+        SP_TRY(c.alloc(&deg, n));
+        SP_TRY(c.alloc(&mx, 1));
+        SP_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), c.stream));
+        k_outdeg<<<gridN(n, c.device), 256, 0, c.stream>>>(g->off, n, deg, mx);
+        unsigned long long *hm;
+        SP_TRY(c.host_as(&hm));
+        SP_CUDA(cudaMemcpyAsync(hm, mx, 8, cudaMemcpyDeviceToHost, c.stream));
+        SP_CUDA(cudaStreamSynchronize(c.stream));  // the copies continue on their stream
+        SP_TRY(pr_hot_prepare(g, c, deg, (int64_t)hm[0], &hot_idx, &H));
+        if (H > 0) SP_TRY(dalloc(&enc, m));
+    }
     const uint32_t *dk = reinterpret_cast<const uint32_t *>(g->adj);
     for (int i = 0; i < C; i++) {
         const int64_t e0 = cut[i], mc = cut[i + 1] - cut[i];
@@ -536,9 +580,13 @@ int upload_adj_build_reverse(sp_graph *g, Call &c, const int32_t *adj_host) {
         const int64_t e0 = cut[i], mc = cut[i + 1] - cut[i];
         if (mc)
             k_up_scatter<<<gridN(mc, c.device), 256, 0, c.stream>>>(
-                dks + e0, svs + e0, mc, base + (int64_t)i * n, g->radj);
+                dks + e0, svs + e0, mc, base + (int64_t)i * n, g->radj, hot_idx, enc);
     }
     SP_CUDA(cudaGetLastError());
+    if (H > 0) {
+        g->pr_radj_hot = enc;
+        g->pr_H = H;
+    }
     return SP_OK;
 }
 

@@ -440,24 +440,22 @@ __global__ void k_hot_encode(const int32_t *__restrict__ radj, int64_t m,
     }
 }
 
-int ensure_pr_hot(sp_graph *g, Call &c) {
-    std::lock_guard<std::mutex> lk(g_hot_mu);
-    if (g->pr_H >= 0) return SP_OK;
+// Hot-set selection: the H sources of largest out-degree, if they cover at
+// least kHotMinCover of the slots.  On success g->pr_hot_ids is set (H
+// resident ids), *hot_idx (call scratch, n entries: hot index or -1) and *H_out
+// are returned; otherwise *H_out = 0.
+int pr_hot_select(sp_graph *g, Call &c, const int32_t *outdeg, int64_t max_outdeg,
+                  int32_t **hot_idx_out, int *H_out) {
+    *H_out = 0;
+    *hot_idx_out = nullptr;
     const int64_t n = g->n, m = g->m;
     const char *ce = getenv("SP_PR_HOT_COVER");  // tuning override of kHotMinCover
     const double min_cover = ce ? atof(ce) : kHotMinCover;
     // free upper bound on the coverage: H sources of at most max_outdeg
     // slots each (a grid decides here, without the sort)
     if (m < kHotMinSlots || n >= kHotBit ||
-        (double)std::min<int64_t>(kHotMax, n) * (double)g->max_outdeg < min_cover * (double)m) {
-        g->pr_H = 0;
+        (double)std::min<int64_t>(kHotMax, n) * (double)max_outdeg < min_cover * (double)m)
         return SP_OK;
-    }
-    // Built on the graph's second fast PR call: the encoding (a sort of the
-    // out-degrees + one pass over radj, ~0.9 ms at cfg2) costs more than it
-    // saves in a single run (~0.4 ms), so a one-shot run on a fresh graph
-    // keeps the plain kernel (same sums either way).
-    if (g->pr_fast_calls++ == 0) return SP_OK;
     const int H = (int)std::min<int64_t>(kHotMax, n);
     uint32_t *key, *key_s;
     int32_t *id, *id_s, *hot_idx;
@@ -466,8 +464,7 @@ int ensure_pr_hot(sp_graph *g, Call &c) {
     SP_TRY(c.alloc(&id, n));
     SP_TRY(c.alloc(&id_s, n));
     SP_TRY(c.alloc(&hot_idx, n));
-    k_hot_keys<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(g->outdeg, n, key, id,
-                                                                     hot_idx);
+    k_hot_keys<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(outdeg, n, key, id, hot_idx);
     size_t tmp = 0;
     SP_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, key, key_s, id, id_s, n, 0,
                                                       32, c.stream));
@@ -495,24 +492,51 @@ int ensure_pr_hot(sp_graph *g, Call &c) {
     if (getenv("SP_PR_HOT_VERBOSE"))
         fprintf(stderr, "pr hot set: top %d sources cover %.3f of the slots\n", H,
                 (double)hcov[0] / (double)m);
-    if ((double)hcov[0] < min_cover * (double)m) {
-        g->pr_H = 0;
-        return SP_OK;
-    }
-    int32_t *ids = nullptr, *enc = nullptr;
+    if ((double)hcov[0] < min_cover * (double)m) return SP_OK;
+    int32_t *ids = nullptr;
     SP_TRY(resident_alloc((void **)&ids, (size_t)H * sizeof(int32_t)));
-    if (resident_alloc((void **)&enc, (size_t)m * sizeof(int32_t)) != SP_OK) {
-        resident_free(ids);
-        return SP_ERR_OOM;
-    }
     SP_CUDA(cudaMemcpyAsync(ids, id_s, (size_t)H * sizeof(int32_t), cudaMemcpyDeviceToDevice,
                             c.stream));
     k_hot_scatter<<<grid_for(H, 256, c.device), 256, 0, c.stream>>>(ids, H, hot_idx);
-    k_hot_encode<<<grid_for(m, 256, c.device, 16), 256, 0, c.stream>>>(g->radj, m, hot_idx, enc);
-    c.launches += 4;
+    c.launches += 3;
+    SP_CUDA(cudaGetLastError());
+    g->pr_hot_ids = ids;
+    *hot_idx_out = hot_idx;
+    *H_out = H;
+    return SP_OK;
+}
+
+int ensure_pr_hot(sp_graph *g, Call &c) {
+    std::lock_guard<std::mutex> lk(g_hot_mu);
+    if (g->pr_H >= 0) return SP_OK;
+    // Built on the graph's second fast PR call: the encoding (a sort of the
+    // out-degrees + one pass over radj, ~0.9 ms at cfg2) costs more than it
+    // saves in a single run (~0.4 ms), so a one-shot run on a fresh graph
+    // keeps the plain kernel (same sums either way).  A large directed graph
+    // uploaded with from_csr gets it during the upload (sp_graph.cu).
+    const char *ce = getenv("SP_PR_HOT_COVER");
+    const double min_cover = ce ? atof(ce) : kHotMinCover;
+    if (g->m < kHotMinSlots || g->n >= kHotBit ||
+        (double)std::min<int64_t>(kHotMax, g->n) * (double)g->max_outdeg <
+            min_cover * (double)g->m) {
+        g->pr_H = 0;
+        return SP_OK;
+    }
+    if (g->pr_fast_calls++ == 0) return SP_OK;
+    int32_t *hot_idx = nullptr;
+    int H = 0;
+    SP_TRY(pr_hot_select(g, c, g->outdeg, g->max_outdeg, &hot_idx, &H));
+    if (H == 0) {
+        g->pr_H = 0;
+        return SP_OK;
+    }
+    int32_t *enc = nullptr;
+    SP_TRY(resident_alloc((void **)&enc, (size_t)g->m * sizeof(int32_t)));
+    k_hot_encode<<<grid_for(g->m, 256, c.device, 16), 256, 0, c.stream>>>(g->radj, g->m, hot_idx,
+                                                                          enc);
+    c.launches++;
     SP_CUDA(cudaGetLastError());
     SP_CUDA(cudaStreamSynchronize(c.stream));
-    g->pr_hot_ids = ids;
     g->pr_radj_hot = enc;
     g->pr_H = H;
     return SP_OK;
@@ -788,6 +812,14 @@ int launch_exact(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, c
 }
 
 }  // namespace
+
+namespace sp {
+int pr_hot_prepare(sp_graph *g, Call &c, const int32_t *outdeg, int64_t max_outdeg,
+                   int32_t **hot_idx, int *H) {
+    static_assert(kHotBit == kPrHotBit, "hot-slot encoding");
+    return pr_hot_select(g, c, outdeg, max_outdeg, hot_idx, H);
+}
+}  // namespace sp
 
 extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t max_iter,
                            int64_t cap, unsigned flags, double *rank_out, int mem,
