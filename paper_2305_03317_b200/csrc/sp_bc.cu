@@ -9,6 +9,10 @@
 //       delta_v += sigma_v / sigma_w * (1 + delta_w) over out-neighbours w at
 //       level+1, then bc_v += delta_v / 2 if v != src.
 //
+// Fast mode (default) runs the sources in batches of kLanes = 8 with
+// lane-major vertex state and direction-optimising discovery -- see
+// "Batched sources" below (bc_run_batches).  Deterministic mode and
+// SP_BC_BATCH=0 use the per-source plan:
 // Device plan per source (graph resident; level int32[n], sigma/delta f64[n],
 // one queue int32[n] holding all BFS levels back to back):
 //   level L -> L+1 : load-balanced top-down expansion (sp_expand.cuh) with a
