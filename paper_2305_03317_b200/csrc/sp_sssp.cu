@@ -538,7 +538,11 @@ struct DoLoop {
 
 constexpr int kPullChunk = 128;
 constexpr int64_t kPullHub = 1024;
-constexpr int64_t kPullDiv = 24;  // pull when the frontier exceeds n / kPullDiv
+constexpr int64_t kPullDiv = 8;   // pull when the frontier exceeds n / kPullDiv (4-12 measured alike)
+// Push-form SSSP uses the direction-optimising loop on graphs this large
+// (RMAT-24: 5.95 -> 5.55 ms; at RMAT-22 the two loops tie, at cfg1 the
+// extra per-iteration kernels cost more than the pull saves)
+constexpr int64_t kDoMinSlots = int64_t(1) << 27;
 
 __device__ __forceinline__ bool fbit(const uint32_t *b, int32_t u) {
     return (__ldcg(b + (u >> 5)) >> (u & 31)) & 1u;
@@ -664,6 +668,182 @@ __global__ void __launch_bounds__(256) k_pull_hubs(const int64_t *__restrict__ r
     if (lane == 0) {
         if (useful) atomicAdd(&L->s.cnt[L->s.cur].scanned, useful);
         if (improved) atomicAdd(&L->s.cnt[L->s.cur].next_size, improved);
+    }
+}
+
+// ---- edge-balanced pull step (the PageRank-units layout, min-plus) ------
+// The reverse slots are cut into kSpUnit-slot units, one warp per unit,
+// 8 consecutive slots per lane per 256-slot chunk (radj and w_eff streamed
+// with 128-bit loads, 8 independent dist gathers); row ends inside a chunk
+// come from a window of nzend marked in a shared bitmap, and a segmented
+// warp min-scan carries the open row's minimum across lanes and chunks.
+// Rows that end in their unit are applied there; a row that began in an
+// earlier unit is finished by k_spull_fix from the units' tail/head minima.
+// Every in-neighbour is relaxed (a full Bellman-Ford sweep of the rows):
+// no frontier test per slot, the same fixpoint.
+constexpr int64_t kSpUnit = 2048;
+constexpr int kSpCh = 256;
+constexpr int64_t kSpNone = INT64_MAX;
+
+struct SPull {
+    const int32_t *__restrict__ radj;
+    const int32_t *__restrict__ rw;
+    const int64_t *__restrict__ nzend;
+    const int32_t *__restrict__ nzrow;
+    const int64_t *__restrict__ unit_row;
+    int64_t *hp, *tp;
+    int64_t m, nnz, nunits;
+};
+
+__device__ __forceinline__ void sp_slab8(const int32_t *__restrict__ p, int64_t q, int64_t s1,
+                                         int (&x)[8], int fill) {
+    if (q + 8 <= s1 && (q & 3) == 0) {
+        const int4 a = __ldcs(reinterpret_cast<const int4 *>(p + q));
+        const int4 b = __ldcs(reinterpret_cast<const int4 *>(p + q + 4));
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+        x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; i++) x[i] = q + i < s1 ? __ldcs(p + q + i) : fill;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_spull_units(SPull a, int32_t *dist, DoLoop *L) {
+    if (L->mode != 1) return;
+    __shared__ uint32_t bitmap[8][kSpCh / 32];
+    uint32_t *bm = bitmap[threadIdx.x >> 5];
+    const unsigned lane = lane_id();
+    if (lane < kSpCh / 32) bm[lane] = 0u;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long improved = 0;
+    for (int64_t u = warp; u < a.nunits; u += nwarps) {
+        const int64_t s0 = u * kSpUnit, s1 = min(a.m, s0 + kSpUnit);
+        int64_t rk = a.unit_row[u];
+        const int64_t first_row = rk;
+        const bool head_spill = (rk > 0 ? __ldg(a.nzend + rk - 1) : 0) < s0;
+        int64_t carry = kSpNone;
+        for (int64_t c = s0; c < s1; c += kSpCh) {
+            const int64_t lim = min(c + (int64_t)kSpCh, s1);
+            int idx[8], w[8];
+            const int64_t q = c + 8 * (int64_t)lane;
+            sp_slab8(a.radj, q, lim, idx, -1);
+            sp_slab8(a.rw, q, lim, w, 0);
+            __syncwarp();
+            const int64_t rk_chunk = rk;
+            for (;;) {
+                const int64_t k = rk + lane;
+                const int64_t e = k < a.nnz ? __ldg(a.nzend + k) : INT64_MAX;
+                const bool in = e <= lim;
+                if (in) {
+                    const int bb = (int)(e - 1 - c);
+                    atomicOr(&bm[bb >> 5], 1u << (bb & 31));
+                }
+                const int cnt = __popc(__ballot_sync(0xffffffffu, in));
+                rk += cnt;
+                if (cnt < 32) break;
+            }
+            int64_t val[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                val[i] = kSpNone;
+                if (idx[i] >= 0) {
+                    const int du = __ldcg(dist + idx[i]);
+                    if (du != kIntMax) val[i] = (int64_t)du + (int64_t)w[i];
+                }
+            }
+            __syncwarp();
+            const unsigned ends = (bm[lane >> 2] >> ((lane & 3) * 8)) & 0xFFu;
+            __syncwarp();
+            if (lane < kSpCh / 32) bm[lane] = 0u;
+            int64_t tail = kSpNone;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                tail = min(tail, val[i]);
+                if ((ends >> i) & 1u) tail = kSpNone;
+            }
+            bool f = ends != 0u;
+            int64_t v = tail;
+            int ne = __popc(ends);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const bool fo = __shfl_up_sync(0xffffffffu, f, o);
+                const int64_t vo = __shfl_up_sync(0xffffffffu, v, o);
+                const int no = __shfl_up_sync(0xffffffffu, ne, o);
+                if ((int)lane >= o) {
+                    if (!f) v = min(vo, v);
+                    f = f || fo;
+                    ne += no;
+                }
+            }
+            bool fe = __shfl_up_sync(0xffffffffu, f, 1);
+            int64_t ve = __shfl_up_sync(0xffffffffu, v, 1);
+            int nbefore = __shfl_up_sync(0xffffffffu, ne, 1);
+            if (lane == 0) {
+                fe = false;
+                ve = kSpNone;
+                nbefore = 0;
+            }
+            const int64_t carry_in = fe ? ve : min(carry, ve);
+            const bool f31 = __shfl_sync(0xffffffffu, f, 31);
+            const int64_t v31 = __shfl_sync(0xffffffffu, v, 31);
+            carry = f31 ? v31 : min(carry, v31);
+            if (ends) {
+                int64_t run = kSpNone;
+                int j = 0;
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    run = min(run, val[i]);
+                    if ((ends >> i) & 1u) {
+                        const int64_t best = j == 0 ? min(carry_in, run) : run;
+                        const int64_t row = rk_chunk + nbefore + j;
+                        if (head_spill && row == first_row) {
+                            a.hp[u] = best;  // finished by k_spull_fix
+                        } else if (best != kSpNone) {
+                            improved += pull_apply(L, dist, __ldg(a.nzrow + row), best) ? 1 : 0;
+                        }
+                        j++;
+                        run = kSpNone;
+                    }
+                }
+            }
+        }
+        if (lane == 0) a.tp[u] = carry;
+    }
+    improved = warp_sum(improved);
+    if (lane == 0 && improved) atomicAdd(&L->s.cnt[L->s.cur].next_size, improved);
+}
+
+// rows that began in an earlier unit and end in unit u: min of the crossed
+// units' tails and u's head
+__global__ void k_spull_fix(SPull a, int32_t *dist, DoLoop *L) {
+    if (L->mode != 1) return;
+    unsigned long long improved = 0;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < a.nunits;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t rk = a.unit_row[u];
+        const int64_t s0 = u * kSpUnit, s1 = min(a.m, s0 + kSpUnit);
+        const int64_t start = rk > 0 ? a.nzend[rk - 1] : 0;
+        if (rk >= a.nnz || start >= s0 || a.nzend[rk] > s1) continue;
+        int64_t best = a.hp[u];
+        for (int64_t w = start / kSpUnit; w < u; w++) best = min(best, a.tp[w]);
+        if (best != kSpNone) improved += pull_apply(L, dist, a.nzrow[rk], best) ? 1 : 0;
+    }
+    improved = warp_sum(improved);
+    if ((threadIdx.x & 31) == 0 && improved)
+        atomicAdd(&L->s.cnt[L->s.cur].next_size, improved);
+}
+
+__global__ void k_spull_setup(SPull a) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < a.nunits;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s0 = u * kSpUnit;
+        int64_t lo = 0, hi = a.nnz;
+        while (lo < hi) {
+            const int64_t mid = lo + ((hi - lo) >> 1);
+            if (a.nzend[mid] <= s0) lo = mid + 1; else hi = mid;
+        }
+        const_cast<int64_t *>(a.unit_row)[u] = lo;
     }
 }
 
@@ -816,6 +996,27 @@ int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa,
     const int grid = sms * 8;
     const int64_t warps = (int64_t)grid * (kExpandBlock / 32);
     const bool big = g->max_outdeg > kSplit;
+    // edge-balanced pull (SP_SSSP_PULL_TILES=1: the older row-tile kernels)
+    const bool units = !getenv("SP_SSSP_PULL_TILES") && g->m > 0;
+    SPull sp{};
+    if (units) {
+        sp.radj = g->radj;
+        sp.rw = g->rweff;
+        sp.nzend = g->nzend;
+        sp.nzrow = g->nzrow;
+        sp.m = g->m;
+        sp.nnz = g->nnz_rows;
+        sp.nunits = (g->m + kSpUnit - 1) / kSpUnit;
+        int64_t *ur, *hp, *tp;
+        SP_TRY(c.alloc(&ur, sp.nunits));
+        SP_TRY(c.alloc(&hp, sp.nunits));
+        SP_TRY(c.alloc(&tp, sp.nunits));
+        sp.unit_row = ur;
+        sp.hp = hp;
+        sp.tp = tp;
+        k_spull_setup<<<grid_for(sp.nunits, 256, c.device), 256, 0, c.stream>>>(sp);
+        c.launches++;
+    }
     cudaGraph_t graph = nullptr;
     struct GraphFree {
         cudaGraph_t *g;
@@ -841,8 +1042,14 @@ int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa,
     if (big)
         k_do_push_chunks<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off, g->adj,
                                                               chunks, D);
-    k_pull_tiles<<<grid, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
-    k_pull_hubs<<<sms * 2, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
+    if (units) {
+        k_spull_units<<<(int)std::max<int64_t>(1, (sp.nunits + 7) / 8), 256, 0, c.stream>>>(
+            sp, dist, D);
+        k_spull_fix<<<grid_for(sp.nunits, 256, c.device), 256, 0, c.stream>>>(sp, dist, D);
+    } else {
+        k_pull_tiles<<<grid, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
+        k_pull_hubs<<<sms * 2, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
+    }
     k_do_advance<<<1, 1, 0, c.stream>>>(D, h);
     k_do_clear<<<grid, 256, 0, c.stream>>>(D);
     k_do_convert<<<grid, 256, 0, c.stream>>>(D);
@@ -990,7 +1197,9 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
             k_init<<<grid_for(n, kBlock, dev), kBlock, 0, c.stream>>>(dist, enq, n, src, qa);
             c.launches++;
             hL = SsspLoop{};
-            if (pull_form)  // sssp_pull.sp: pull steps for large frontiers
+            const char *de = getenv("SP_SSSP_DO");  // direction-optimising push SSSP
+            const bool use_do = de ? de[0] == '1' : g->m >= kDoMinSlots;
+            if (pull_form || use_do)  // sssp_pull.sp: pull steps for large frontiers
                 lrc = sssp_do_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
             else
                 lrc = sssp_device_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
