@@ -388,7 +388,8 @@ def _line(name, graph, g, ms, edges, model_bytes, hbm_peak, **extra):
 
 
 def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
-    """SSSP cfg1, BC cfg4 (256 sources), TC cfg3; sharded over the ranks
+    """SSSP cfg1, grid cfg5a (SSSP + PR), BC cfg4 (256 sources), TC cfg3 and the
+    RMAT-24 target row (PR, SSSP, TC); sharded over the ranks
     when N > 1 (BC sources, TC ranges, SSSP block supersteps)."""
     out = {}
     reps = 3
@@ -457,6 +458,33 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
                                triangles=r.env.scalars["triangle_count"],
                                sharding=f"ranges/{world}")
         g.close()
+    if "rmat24" in a.algos:  # SURVEY 8d target row: RMAT-24 on one GPU
+        g = sp.generate("rmat", 24, 16, seed=SEED, device=dev.index)
+        ms, _, r = timed(lambda: go(corpus.PR, g, PR_ARGS), 3, 2, world, dev)
+        it = r.env.scalars["iter"]
+        out["pr_rmat24"] = _line("pr", "rmat24 directed", g, ms / 3, it * g.m,
+                                 it * (12 * g.m + 36 * g.n), hbm_peak, iterations=it)
+        ms, _, r = timed(lambda: go(corpus.SSSP, g, {"src": 0}), 3, 2, world, dev)
+        offs = np.asarray(g.offsets)
+        d = np.asarray(r.env.node_props["dist"].cpu() if world == 1 else
+                       r.env.node_props["dist"])
+        m_reached = int((offs[1:] - offs[:-1])[d < 2147483647].sum())
+        mb = None
+        if world == 1:
+            mb = 12 * r.stats["edges_visited"] + 20 * r.stats["vertices_visited"]
+        out["sssp_rmat24"] = _line("sssp", "rmat24 directed", g, ms / 3, m_reached, mb, hbm_peak,
+                                   iterations=r.fixedpoint_iterations["finished"],
+                                   note="push model bytes; iterations whose frontier exceeds "
+                                        "n/8 are pull sweeps (not in the model)")
+        g.close()
+        g = sp.generate("rmat", 24, 16, seed=SEED, undirected=True, device=dev.index)
+        go(corpus.TC, g, {})  # builds the cached upper CSR (graph preprocessing)
+        ms, _, r = timed(lambda: go(corpus.TC, g, {}), 2, 1, world, dev)
+        out["tc_rmat24"] = _line("tc", "rmat24 symmetrized", g, ms / 2, g.m // 2,
+                                 r.stats.get("model_bytes"), hbm_peak,
+                                 triangles=r.env.scalars["triangle_count"],
+                                 sharding=f"ranges/{world}")
+        g.close()
     return out
 
 
@@ -466,7 +494,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--algos", default="sssp,grid,bc,tc",
+    ap.add_argument("--algos", default="sssp,grid,bc,tc,rmat24",
                     help="secondary algorithms at N=1 ('' to skip)")
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()
