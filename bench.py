@@ -474,8 +474,8 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
             mb = 12 * r.stats["edges_visited"] + 20 * r.stats["vertices_visited"]
         out["sssp_rmat24"] = _line("sssp", "rmat24 directed", g, ms / 3, m_reached, mb, hbm_peak,
                                    iterations=r.fixedpoint_iterations["finished"],
-                                   note="push model bytes; iterations whose frontier exceeds "
-                                        "n/8 are pull sweeps (not in the model)")
+                                   note="12 B per relaxation (push) or swept in-slot (pull sweeps, "
+                                        "frontier > n/8) + 20 B per frontier vertex")
         g.close()
         g = sp.generate("rmat", 24, 16, seed=SEED, undirected=True, device=dev.index)
         go(corpus.TC, g, {})  # builds the cached upper CSR (graph preprocessing)

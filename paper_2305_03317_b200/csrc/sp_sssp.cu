@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(256) k_spull_units(SPull a, int32_t *dist, DoL
     if (lane < kSpCh / 32) bm[lane] = 0u;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned long long improved = 0;
+    unsigned long long improved = 0, swept = 0;
     for (int64_t u = warp; u < a.nunits; u += nwarps) {
         const int64_t s0 = u * kSpUnit, s1 = min(a.m, s0 + kSpUnit);
         int64_t rk = a.unit_row[u];
@@ -808,10 +808,15 @@ __global__ void __launch_bounds__(256) k_spull_units(SPull a, int32_t *dist, DoL
                 }
             }
         }
-        if (lane == 0) a.tp[u] = carry;
+        if (lane == 0) {
+            a.tp[u] = carry;
+            swept += (unsigned long long)(s1 - s0);
+        }
     }
     improved = warp_sum(improved);
     if (lane == 0 && improved) atomicAdd(&L->s.cnt[L->s.cur].next_size, improved);
+    // every swept in-slot is a relaxation (12 B: radj, w_eff, dist gather)
+    if (lane == 0 && swept) atomicAdd(&L->s.cnt[L->s.cur].scanned, swept);
 }
 
 // rows that began in an earlier unit and end in unit u: min of the crossed

@@ -13,5 +13,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --algos none > $OUT/ncu_launch_bench.log 2>&1
-SP_HOSTLOOP=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pr_units|k_pr_hot_gather|k_pr_epi" -s 9 -c 3 \
+SP_HOSTLOOP=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pr_units|k_pr_hot_gather|k_pr_epi" -s 28 -c 3 \
    -o $OUT/prof_pr python bench.py --steps 1 --warmup 1 --no-cpu --algos none > $OUT/ncu_full.log 2>&1
