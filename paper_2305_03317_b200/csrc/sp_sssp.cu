@@ -93,6 +93,7 @@ struct SsspLoop {
     int64_t nq;    // |q[cur]|
     int64_t iters, relaxed, frontier_sum, cap;
     int status;    // 0 ok / converged, 1 overflow, 2 cap reached
+    unsigned blocks_done;  // k_relax_loop_chunks: the last block runs the advance
 };
 
 __global__ void __launch_bounds__(kExpandBlock, 4) k_relax_loop(
@@ -106,16 +107,34 @@ __global__ void __launch_bounds__(kExpandBlock, 4) k_relax_loop(
                 expand_vpw(nq, warps));
 }
 
+__device__ __forceinline__ int loop_advance(SsspLoop *L);
+
+// Hub chunks; the last block to finish also runs the loop advance (one
+// graph node per iteration fewer: ~4 us of node latency each, cfg1 runs
+// 9-10 iterations of ~40 us).
 __global__ void __launch_bounds__(kExpandBlock, 3) k_relax_loop_chunks(
     int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
     const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const ChunkItem *chunks,
-    SsspLoop *L) {
+    SsspLoop *L, cudaGraphConditionalHandle h) {
     const int cur = L->cur;
     RelaxOp op{dist, enq, weff, &L->cnt[cur].flag, L->it};
     expand_chunks_body(op, off, adj, chunks, L->q[cur ^ 1], &L->cnt[cur]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // this block's counter updates before its arrival
+        if (atomicAdd(&L->blocks_done, 1u) == gridDim.x - 1) {
+            __threadfence();
+            L->blocks_done = 0;
+            cudaGraphSetConditional(h, loop_advance(L));
+        }
+    }
 }
 
 __global__ void k_loop_advance(SsspLoop *L, cudaGraphConditionalHandle h) {
+    cudaGraphSetConditional(h, loop_advance(L));
+}
+
+__device__ __forceinline__ int loop_advance(SsspLoop *L) {
     const int cur = L->cur;
     const ExpandCounters c = L->cnt[cur];
     L->iters++;
@@ -135,7 +154,7 @@ __global__ void k_loop_advance(SsspLoop *L, cudaGraphConditionalHandle h) {
     L->cur = cur ^ 1;
     L->nq = (int64_t)c.next_size;
     L->it = (int)(L->iters + 1);
-    cudaGraphSetConditional(h, go);
+    return go;
 }
 
 // ---- near-far ordering (large-diameter graphs, non-negative weights) -----
@@ -1133,8 +1152,9 @@ int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t 
                                                       L, warps);
     if (big)
         k_relax_loop_chunks<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off,
-                                                                 g->adj, chunks, L);
-    k_loop_advance<<<1, 1, 0, c.stream>>>(L, h);
+                                                                 g->adj, chunks, L, h);
+    else
+        k_loop_advance<<<1, 1, 0, c.stream>>>(L, h);
     cudaError_t ce = cudaStreamEndCapture(c.stream, &body);
     SP_CUDA(ce);
     cudaEvent_t ka, kb;
@@ -1148,7 +1168,7 @@ int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t 
     cudaEventElapsedTime(kernel_ms, ka, kb);
     cudaEventDestroy(ka);
     cudaEventDestroy(kb);
-    c.launches += hL->iters * (big ? 3 : 2);
+    c.launches += hL->iters * 2;
     return SP_OK;
 }
 
