@@ -59,7 +59,7 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kChunk = 128;     // exact path: slab slots staged per warp per step
-constexpr int64_t kUnit = 2048;  // fast path: radj slots per work unit (one warp)
+constexpr int64_t kUnit = 768;   // fast path: radj slots per work unit (one warp); cfg2: 512/768/1024/2048/4096 -> 220/222/219/214/188 GTEPS
 constexpr int kCh = 256;        // fast path: slots per warp chunk (8 per lane)
 constexpr int kHotBlock = 1024;   // persistent hot-source variant: threads per block
 constexpr int kHotMax = 24 * 1024;  // hot contrib values kept in shared memory (192 KB)
