@@ -62,7 +62,7 @@ constexpr int kChunk = 128;     // exact path: slab slots staged per warp per st
 constexpr int64_t kUnit = 768;   // fast path: radj slots per work unit (one warp); cfg2: 512/768/1024/2048/4096 -> 220/222/219/214/188 GTEPS
 constexpr int kCh = 256;        // fast path: slots per warp chunk (8 per lane)
 constexpr int kHotBlock = 1024;   // persistent hot-source variant: threads per block
-constexpr int kHotMax = 24 * 1024;  // hot contrib values kept in shared memory (192 KB)
+constexpr int kHotMax = 20 * 1024;  // hot contrib values in shared memory (160 KB); cfg2: 16K/20K/24K/28K -> 232/233/221/154 GTEPS (more smem leaves less L1 for the cold gathers)
 constexpr int kHotBit = 1 << 30;    // encoded radj: source is hot, low bits = hot index
 
 __global__ void k_init(double *rank, double *contrib, const int32_t *__restrict__ outdeg,
