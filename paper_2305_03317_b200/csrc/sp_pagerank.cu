@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kHotBlock, 1) k_pr_units_hot(PrArgs a, const d
 // A row whose first and last slots lie in different units (a "spill" row)
 // was not summed by k_pr_units: its partials are added here left to right,
 // tp of every unit it crosses, then hp of the unit holding its end.
-constexpr int kEpi = 4;
+constexpr int kEpi = 1;  // rows per thread; cfg2: 1/2/4/8 -> 239/237/234/221 GTEPS (more blocks beat per-thread MLP)
 __global__ void __launch_bounds__(256) k_pr_epi(PrArgs a) {
     pr_bind(a);
     const int64_t nk = a.K1 - a.K0;
