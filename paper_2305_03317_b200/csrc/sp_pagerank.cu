@@ -413,7 +413,7 @@ __global__ void k_pr_bounds(const int64_t *__restrict__ roff, const int32_t *__r
 
 std::mutex g_hot_mu;
 constexpr int64_t kHotMinSlots = 1 << 20;  // smaller graphs keep the plain kernel
-constexpr double kHotMinCover = 0.4;       // hot sources must cover >= 40% of the slots
+constexpr double kHotMinCover = 0.25;  // hot sources must cover >= 25% of the slots (RMAT-24 at 0.307: 9.54 -> 8.83 ms)
 
 __global__ void k_hot_keys(const int32_t *__restrict__ outdeg, int64_t n, uint32_t *key,
                            int32_t *id, int32_t *hot_idx) {
