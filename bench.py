@@ -290,7 +290,8 @@ def run_ours(a):
                 "generated on device",
         "config": {"workload": "pagerank_rmat22", "graph": f"rmat{SCALE}", "n": n, "m": m,
                    **PR_ARGS, "iterations": iters,
-                   "parallelism": f"block{world}+nccl" if world > 1 else "single",
+                   "parallelism": (f"block{world}+{dist.get_backend()}" if world > 1
+                                   else "single"),
                    "l2": "no flush: radj (4m = %.0f MB) + roff exceed the 126 MB L2; "
                          "contrib (8n = %.0f MB) is L2-resident by design"
                          % (4 * m / 1e6, 8 * n / 1e6)},
