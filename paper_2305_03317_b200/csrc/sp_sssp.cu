@@ -1122,7 +1122,11 @@ int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t 
     init.cap = cap;
     SP_CUDA(cudaMemcpyAsync(L, &init, sizeof(SsspLoop), cudaMemcpyHostToDevice, c.stream));
     const int sms = num_sms(c.device);
-    const int grid = sms * 8;
+    // blocks per SM of the loop's kernels: small graphs pay for launching an
+    // idle grid every iteration (cfg1: 8 -> 0.36 ms, 4 -> 0.32 ms; RMAT-22
+    // wants 8); SP_SSSP_GRID_MUL overrides
+    const char *gm = getenv("SP_SSSP_GRID_MUL");
+    const int grid = sms * (gm ? std::max(1, atoi(gm)) : (g->m < (int64_t(1) << 22) ? 4 : 8));
     const int64_t warps = (int64_t)grid * (kExpandBlock / 32);
     const bool big = g->max_outdeg > kSplit;
     cudaGraph_t graph = nullptr;
