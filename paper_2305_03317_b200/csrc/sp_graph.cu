@@ -561,7 +561,14 @@ int upload_adj_build_reverse(sp_graph *g, Call &c, const int32_t *adj_host) {
         SP_CUDA(cudaMemcpyAsync(hm, mx, 8, cudaMemcpyDeviceToHost, c.stream));
         SP_CUDA(cudaStreamSynchronize(c.stream));  // the copies continue on their stream
         SP_TRY(pr_hot_prepare(g, c, deg, (int64_t)hm[0], &hot_idx, &H));
-        if (H > 0) SP_TRY(dalloc(&enc, m));
+        if (H > 0 && dalloc(&enc, m) != SP_OK) {  // optional: no memory -> no hot set
+            cudaGetLastError();
+            resident_free(g->pr_hot_ids);
+            g->pr_hot_ids = nullptr;
+            enc = nullptr;
+            hot_idx = nullptr;
+            H = 0;
+        }
     }
     const uint32_t *dk = reinterpret_cast<const uint32_t *>(g->adj);
     for (int i = 0; i < C; i++) {
