@@ -350,7 +350,7 @@ def e2e_pr(sp, corpus, parallel, g, a, world, dev, be):
         gg.close()
         return r
 
-    k = max(1, min(a.steps, 5))
+    k = max(1, min(a.steps, 10))
     ms, _, r = timed(step, k, max(2, min(a.warmup, 3)), world, dev)
     dt = ms / k / 1e3
     # the graph build alone (H2D of the CSR + device reverse CSR), reported
