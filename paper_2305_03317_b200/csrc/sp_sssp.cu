@@ -34,7 +34,7 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int64_t kDeltaMul = 16;        // near-far step = kDeltaMul x mean weight
 constexpr int64_t kNearFarMaxAvgDeg = 8;  // near-far only when m <= 8 n
-constexpr int kPersistBlocksPerSm = 1;    // persistent near-far grid: blocks per SM
+constexpr int kPersistBlocksPerSm = 2;    // persistent near-far grid: blocks per SM (cfg5a: 1 -> 87.8 ms, 2 -> 86.0 ms)
 constexpr int kNfHops = 2;  // warp-local continuation hops (persistent near-far); cfg5a: 1-4 ~87-93 ms, 8 -> 120 ms, 16 -> 158 ms
 
 // Relaxation of sssp.sp:11-12 for one slot; payload = dist[v] at expansion.
