@@ -123,6 +123,7 @@ struct sp_graph {
     int64_t *nzend = nullptr;
     int64_t nnz_rows = 0;
     int32_t *wrange = nullptr;  // [min, max] weight (device), m > 0
+    int32_t wmin_h = 0, wmax_h = 0;  // the same, on the host (read at creation)
     // degree-ordered upper CSR for triangle counting (undirected graphs),
     // built lazily by the first sp_tc call: row v holds the neighbours x of v
     // with (deg x, x) > (deg v, v), ascending, duplicates kept, starting at

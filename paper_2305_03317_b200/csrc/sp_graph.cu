@@ -641,9 +641,13 @@ int finish_graph(sp_graph *g, Call &c, bool unit_weights = false) {
         k_wrange<<<gridN(m, c.device), 256, 0, c.stream>>>(g->w, m, g->wrange);
     }
     unsigned long long h[4];
+    int32_t wr[2] = {0, 0};
     SP_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    if (m) SP_CUDA(cudaMemcpyAsync(wr, g->wrange, sizeof(wr), cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
     SP_CUDA(cudaGetLastError());
+    g->wmin_h = wr[0];
+    g->wmax_h = wr[1];
     g->max_outdeg = (int64_t)h[0];
     g->max_indeg = g->directed ? (int64_t)h[1] : (int64_t)h[0];
     g->nnz_rows = (int64_t)h[2];
@@ -1010,10 +1014,8 @@ int sp_graph_weight_range(const sp_graph *g, int32_t *wmin, int32_t *wmax) {
     SP_CHECK(g, SP_ERR_ARG, "null graph");
     SP_CHECK(g->m > 0, SP_ERR_ARG, "weight range of a graph with no edges");
     SP_CUDA(cudaSetDevice(g->device));
-    int32_t h[2];
-    SP_CUDA(cudaMemcpy(h, g->wrange, sizeof(h), cudaMemcpyDeviceToHost));
-    if (wmin) *wmin = h[0];
-    if (wmax) *wmax = h[1];
+    if (wmin) *wmin = g->wmin_h;  // read at creation (the graph is immutable)
+    if (wmax) *wmax = g->wmax_h;
     return SP_OK;
 }
 

@@ -1218,7 +1218,10 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
         SsspLoop hL{};
         int lrc;
         int32_t wr[2] = {0, 0};
-        if (g->m) SP_CUDA(cudaMemcpy(wr, g->wrange, sizeof(wr), cudaMemcpyDeviceToHost));
+        if (g->m) {  // cached at creation: no blocking copy per call
+            wr[0] = g->wmin_h;
+            wr[1] = g->wmax_h;
+        }
         const int64_t delta = pull_form ? 0 : near_far_delta(g, wr[0], wr[1]);
         if (delta > 0)
             lrc = sssp_near_far(g, c, dist, enq, qa, qb, chunks, cap, delta, &hL, &kernel_ms);
