@@ -185,7 +185,11 @@ int Call::finish(sp_stats *st) {
 }
 
 void Call::persist(const void *base, size_t bytes) {
-    if (device < 0 || device >= 64 || !g_persist_max[device] || !g_window_max[device] || !bytes)
+    // small arrays stay L2-resident anyway; reserving and resetting the
+    // persisting region costs more than it saves on short calls
+    constexpr size_t kPersistMinBytes = size_t(16) << 20;
+    if (device < 0 || device >= 64 || !g_persist_max[device] || !g_window_max[device] ||
+        bytes < kPersistMinBytes)
         return;
     {
         std::lock_guard<std::mutex> lk(g_persist_mu);
