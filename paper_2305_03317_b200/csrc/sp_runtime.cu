@@ -185,11 +185,17 @@ int Call::finish(sp_stats *st) {
 }
 
 void Call::persist(const void *base, size_t bytes) {
-    // small arrays stay L2-resident anyway; reserving and resetting the
-    // persisting region costs more than it saves on short calls
+    // Opt-in (SP_L2_PERSIST=1): measured on B200 the persisting windows
+    // slow every user down (BC cfg4 55.4 -> 59.8 ms, SSSP RMAT-24 5.27 ->
+    // 5.65 ms) -- the set-aside shrinks the L2 the other streams gather
+    // from -- and small arrays stay L2-resident anyway.
+    static const bool enabled = [] {
+        const char *e = getenv("SP_L2_PERSIST");
+        return e && e[0] == '1';
+    }();
     constexpr size_t kPersistMinBytes = size_t(16) << 20;
-    if (device < 0 || device >= 64 || !g_persist_max[device] || !g_window_max[device] ||
-        bytes < kPersistMinBytes)
+    if (!enabled || device < 0 || device >= 64 || !g_persist_max[device] ||
+        !g_window_max[device] || bytes < kPersistMinBytes)
         return;
     {
         std::lock_guard<std::mutex> lk(g_persist_mu);
