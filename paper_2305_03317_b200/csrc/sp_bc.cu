@@ -181,7 +181,8 @@ int bc_run_sources(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
                    bool det, double *bc_dst, int bc_mem, bool bc_accumulate_only,
                    double *sigma_out, double *delta_out, int mem, BcWorker &wk) {
     Call c;
-    SP_TRY(c.begin(g->device));
+    // worker k of a multi-worker call runs on the device's persistent slot-k stream
+    SP_TRY(stride > 1 ? c.begin_worker(g->device, (int)first) : c.begin(g->device));
     const int64_t n = g->n;
     const int64_t nsrc = (int64_t)srcs.size();
     const int sms = num_sms(c.device);
@@ -794,7 +795,8 @@ int bc_run_batches(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
                    double *bc_dst, int bc_mem, bool bc_accumulate_only, double *sigma_out,
                    double *delta_out, int mem, BcWorker &wk) {
     Call c;
-    SP_TRY(c.begin(g->device));
+    // worker k of a multi-worker call runs on the device's persistent slot-k stream
+    SP_TRY(stride > 1 ? c.begin_worker(g->device, (int)first) : c.begin(g->device));
     const int64_t n = g->n;
     const int64_t nsrc = (int64_t)srcs.size();
     const int64_t nb = (nsrc + kLanes - 1) / kLanes;
@@ -1021,6 +1023,7 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
         double *parts;
         SP_TRY(c.alloc(&parts, (int64_t)K * n));
         SP_TRY(c.finish(nullptr));  // parts allocated before the workers use it
+        std::lock_guard<std::mutex> slots(worker_slots_mutex(g->device));
         std::vector<std::thread> th;
         for (int k = 0; k < K; k++)
             th.emplace_back([&, k]() {

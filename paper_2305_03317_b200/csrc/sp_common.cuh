@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <mutex>
 #include <stdint.h>
 #include <stdio.h>
 
@@ -45,6 +47,9 @@ int num_sms(int device);
 // default pool, release threshold raised so repeated calls reuse memory).
 int scratch_alloc(void **p, size_t bytes, cudaStream_t s);
 void scratch_free(void *p, cudaStream_t s);
+constexpr int kWorkerSlots = 16;
+// serialises multi-worker calls on a device (they share the worker slots)
+std::mutex &worker_slots_mutex(int dev);
 int resident_alloc(void **p, size_t bytes);  // graph arrays (pool, any stream)
 void resident_free(void *p);
 constexpr size_t kPinnedBlock = 4096;
@@ -66,6 +71,11 @@ struct Call {
     // kernels (random-access property arrays); best effort.
     void persist(const void *base, size_t bytes);
     int begin(int dev);
+    // as begin(), on the persistent stream of worker slot k (k < kWorkerSlots)
+    // of the device: a multi-worker call (sp_bc) spawns its host threads per
+    // call, and per-thread streams would make every call allocate its scratch
+    // on fresh streams; slot streams keep the pool's blocks reusable
+    int begin_worker(int dev, int k);
     // this call's pinned host block (recycled across calls)
     int host(void **p);
     template <class T>

@@ -144,6 +144,34 @@ struct ThreadRes {
 };
 static thread_local ThreadRes g_tres[64];
 
+static ThreadRes g_wres[64][kWorkerSlots];
+static std::mutex g_wres_mu;
+static std::mutex g_wslot_mu[64];
+
+std::mutex &worker_slots_mutex(int dev) { return g_wslot_mu[dev & 63]; }
+
+int Call::begin_worker(int dev, int k) {
+    if (dev < 0 || dev >= 64 || k < 0 || k >= kWorkerSlots) return begin(dev);
+    device = dev;
+    SP_CUDA(cudaSetDevice(dev));
+    std::call_once(g_pool_once[dev], tune_pool, dev);
+    ThreadRes *r = &g_wres[dev][k];
+    {
+        std::lock_guard<std::mutex> lk(g_wres_mu);
+        if (!r->stream) {
+            SP_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+            SP_CUDA(cudaEventCreate(&r->t0));
+            SP_CUDA(cudaEventCreate(&r->t1));
+        }
+    }
+    stream = r->stream;
+    t0 = r->t0;
+    t1 = r->t1;
+    owned = false;
+    SP_CUDA(cudaEventRecord(t0, stream));
+    return SP_OK;
+}
+
 int Call::begin(int dev) {
     device = dev;
     SP_CUDA(cudaSetDevice(dev));
