@@ -179,6 +179,37 @@ def test_sssp_seeded(kind, p0, p1, und):
             np.testing.assert_array_equal(r.env.node_props["dist"], dist)
 
 
+@pytest.mark.parametrize("pull_div", ["8", "1000000"])
+@pytest.mark.parametrize("graph", ["rmat_dir", "rmat_sym", "hub", "multi", "neg_dag"])
+def test_sssp_direction_optimising(graph, pull_div, monkeypatch):
+    """Push-form SSSP through the direction-optimising loop (the default from
+    2^27 slots; forced here): push iterations, edge-balanced pull sweeps for
+    large frontiers (pull_div 8) or for every frontier after the root
+    (pull_div huge), spill rows across units, negative weights -- the
+    oracle's dist bit for bit."""
+    monkeypatch.setenv("SP_SSSP_DO", "1")
+    monkeypatch.setenv("SP_SSSP_PULL_DIV", pull_div)
+    if graph.startswith("rmat"):
+        u, v, w, n = gen.rmat(13, 16, seed=17, undirected=graph == "rmat_sym")
+        directed = graph == "rmat_dir"
+    elif graph == "hub":
+        u, v, w, n = _hub_graph(True)
+        directed = True
+    elif graph == "multi":
+        u, v, w, n = _multigraph(6)
+        directed = True
+    else:
+        u, v, w, n = _multigraph(5, neg=True)
+        directed = True
+    g = sp.from_arrays(u, v, w, directed=directed, n=n)
+    o = cpu_ref.build_csr(u, v, w, directed, n)
+    for s in (int(u[0]), 0):
+        dist, _, rc = cpu_ref.sssp(o, s)
+        assert rc == 0
+        r = sp.run(corpus.SSSP, g, {"src": s})
+        np.testing.assert_array_equal(r.env.node_props["dist"], dist)
+
+
 @pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 14, 16, False), ("rmat", 13, 16, True),
                                             ("grid", 32, 32, True), ("rmat", 16, 16, False)])
 def test_pagerank_seeded(kind, p0, p1, und):
