@@ -557,6 +557,10 @@ def test_from_csr_pipelined_reverse(weighted, pinned, monkeypatch):
     r1 = sp.run(corpus.PR, g, PR_ARGS)
     r2 = sp.run(corpus.PR, gd, PR_ARGS)
     assert r1.env.node_props["rank"].tobytes() == r2.env.node_props["rank"].tobytes()
+    if weighted:  # w_eff and the reverse weights come from the uploaded arrays
+        for prog in (corpus.SSSP, corpus.SSSP_PULL):
+            np.testing.assert_array_equal(sp.run(prog, g, {"src": 0}).env.node_props["dist"],
+                                          sp.run(prog, gd, {"src": 0}).env.node_props["dist"])
     for x in (g, gp, gd):
         x.close()
 
