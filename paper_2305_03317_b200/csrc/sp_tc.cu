@@ -54,7 +54,10 @@ constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kA = 256;            // warp path: upper rows up to kA (longer: k_tc_big)
 constexpr int kT = 512;            // warp path: hash table entries (>= 2 kA)
-constexpr int kFwdWarpWords = 2 * kT + 2 * kA + 1 + 128;  // per-warp shared words
+// per-warp shared words: keys[kT], 16-bit multiplicities packed two per
+// word (a count is at most kA), row starts, prefix, filter -- 5.6 KB, so
+// 5 blocks of 8 warps fit an SM (6.7 KB with 32-bit counts: 4 blocks)
+constexpr int kFwdWarpWords = kT + kT / 2 + 2 * kA + 1 + 128;
 constexpr int kFilterWords = 128;  // 4096-bit filter per warp
 constexpr int kFilterShift = 20;   // 32 - log2(4096)
 constexpr int kBatch = 32;
@@ -434,10 +437,10 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
     const int wib = threadIdx.x >> 5;
     uint32_t *base = fwd_smem + (size_t)wib * kFwdWarpWords;
     int32_t *HK = reinterpret_cast<int32_t *>(base);
-    uint32_t *HC = base + kT;
-    uint32_t *B = base + 2 * kT;
-    int32_t *S = reinterpret_cast<int32_t *>(base + 2 * kT + kA);
-    uint32_t *F = base + 2 * kT + 2 * kA + 1;
+    uint32_t *HC = base + kT;  // two 16-bit counts per word
+    uint32_t *B = base + kT + kT / 2;
+    int32_t *S = reinterpret_cast<int32_t *>(base + kT + kT / 2 + kA);
+    uint32_t *F = base + kT + kT / 2 + 2 * kA + 1;
     unsigned long long cnt = 0, elems = 0, pairs = 0, abytes = 0;
     for (;;) {
         unsigned long long bt = 0;
@@ -466,10 +469,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
             while ((1 << tbits) < 2 * na) tbits++;
             const int T = 1 << tbits;
             for (int k = lane; k < kFilterWords; k += 32) F[k] = 0u;
-            for (int k = lane; k < T; k += 32) {
-                HK[k] = -1;
-                HC[k] = 0u;
-            }
+            for (int k = lane; k < T; k += 32) HK[k] = -1;
+            for (int k = lane; k < T / 2; k += 32) HC[k] = 0u;
             __syncwarp();
             int carry = 0;
             for (int k0 = 0; k0 < na; k0 += 32) {
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
                     for (;;) {
                         const int32_t old = atomicCAS(&HK[h], -1, x);
                         if (old == -1 || old == x) {
-                            atomicAdd(&HC[h], 1u);
+                            atomicAdd(&HC[h >> 1], 1u << ((h & 1u) * 16));
                             break;
                         }
                         h = (h + 1) & (T - 1);
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
                             for (;;) {
                                 const int32_t key = HK[h];
                                 if (key == x) {
-                                    cnt += HC[h];
+                                    cnt += (HC[h >> 1] >> ((h & 1u) * 16)) & 0xFFFFu;
                                     break;
                                 }
                                 if (key == -1) break;
