@@ -30,6 +30,7 @@
 // both are skipped without changing a bit.  Sigma values are path counts:
 // integer-valued doubles, exact in any summation order below 2^53.
 #include <algorithm>
+#include <chrono>
 #include <thread>
 #include <vector>
 
@@ -796,6 +797,8 @@ int bc_run_batches(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
                    double *delta_out, int mem, BcWorker &wk) {
     Call c;
     // worker k of a multi-worker call runs on the device's persistent slot-k stream
+    const auto wt0 = std::chrono::steady_clock::now();
+    static const bool wtrace = getenv("SP_BC_TRACE") != nullptr;
     SP_TRY(stride > 1 ? c.begin_worker(g->device, (int)first) : c.begin(g->device));
     const int64_t n = g->n;
     const int64_t nsrc = (int64_t)srcs.size();
@@ -826,6 +829,12 @@ int bc_run_batches(sp_graph *g, const std::vector<int32_t> &srcs, int64_t first,
     SP_TRY(c.alloc(&counts, 2 + 5));
     const int fgrid = sms * 2;  // frontier passes: small grids, grid-stride
     if (delta_out) SP_TRY(c.alloc(&dlast, n));
+    if (wtrace) {
+        cudaStreamSynchronize(c.stream);
+        fprintf(stderr, "  worker %lld: setup+allocs %.2f ms\n", (long long)first,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wt0)
+                    .count());
+    }
     const BbChunks ck{reg_v, reg_base, reg_nch, items, csum, counts};
     c.persist(lev, kLanes * n * sizeof(int32_t));  // the per-slot probe target
     SP_CUDA(cudaMemsetAsync(bc, 0, n * sizeof(double), c.stream));
@@ -973,6 +982,13 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
                      sp_stats *st) {
     SP_CHECK(g && bc_out && nsrc >= 0 && (nsrc == 0 || srcs_in), SP_ERR_ARG,
              "sp_bc: bad arguments");
+    // SP_BC_TRACE=1: host phase times on stderr (diagnostic)
+    static const bool trace = getenv("SP_BC_TRACE") != nullptr;
+    const auto tt0 = std::chrono::steady_clock::now();
+    auto tms = [&]() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tt0)
+            .count();
+    };
     std::vector<int32_t> srcs(srcs_in, srcs_in + nsrc);  // host list (SetN argument)
     for (int64_t i = 0; i < nsrc; i++)
         SP_CHECK(srcs[i] >= 0 && srcs[i] < g->n, SP_ERR_ARG,
@@ -992,9 +1008,24 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
     if (batched) {
         // per worker: lev/sig/coef/csum/queue lanes + stamp, reg, bc; items
         const double per = (double)n * (4 + 8 + 8 + 8 + 4) * kLanes + 28.0 * n + g->m / 3.0;
-        size_t fr = 0, tot = 0;
-        SP_CUDA(cudaSetDevice(g->device));
-        SP_CUDA(cudaMemGetInfo(&fr, &tot));
+        // free device memory, re-queried at most once a second per device:
+        // cudaMemGetInfo stalled calls by up to ~20 ms under load
+        static std::mutex mi_mu;
+        static size_t mi_free[64];
+        static std::chrono::steady_clock::time_point mi_at[64];
+        size_t fr = 0;
+        {
+            std::lock_guard<std::mutex> lk(mi_mu);
+            const int d = g->device & 63;
+            const auto now = std::chrono::steady_clock::now();
+            if (!mi_free[d] || now - mi_at[d] > std::chrono::seconds(1)) {
+                size_t tot = 0;
+                SP_CUDA(cudaSetDevice(g->device));
+                SP_CUDA(cudaMemGetInfo(&mi_free[d], &tot));
+                mi_at[d] = now;
+            }
+            fr = mi_free[d];
+        }
         const char *ew = getenv("SP_BC_WORKERS");
         const int64_t want = ew ? std::max(1, atoi(ew)) : kBbWorkers;
         K = (int)std::max<int64_t>(1, std::min<int64_t>(want, nb));
@@ -1030,7 +1061,9 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
                 wk[k].rc = run(k, K, parts + (int64_t)k * n, SP_MEM_DEVICE, true, wk[k]);
                 if (wk[k].rc != SP_OK) snprintf(wk[k].err, sizeof(wk[k].err), "%s", sp_last_error());
             });
+        const double t_spawn = tms();
         for (auto &t : th) t.join();
+        if (trace) fprintf(stderr, "sp_bc: spawn %.2f ms, join %.2f ms\n", t_spawn, tms());
         for (int k = 0; k < K; k++)
             SP_CHECK(wk[k].rc == SP_OK, wk[k].rc, "%s", wk[k].err);
         double *sum;
@@ -1041,6 +1074,7 @@ extern "C" int sp_bc(sp_graph *g, const int32_t *srcs_in, int64_t nsrc, unsigned
         SP_TRY(from_device(bc_out, sum, n * 8, mem, c.stream));
     }
     SP_TRY(c.finish(st));
+    if (trace) fprintf(stderr, "sp_bc: done %.2f ms\n", tms());
     if (st) {
         int64_t lv = 0, sc = 0, rc = 0, la = 0;
         for (auto &w : wk) {
