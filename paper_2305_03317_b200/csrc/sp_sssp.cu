@@ -21,6 +21,8 @@
 //     one 8-byte device->host read per iteration (K5/K6 in SURVEY 2.2).
 // Candidates >= INT_MAX never win (interp.py:11-14).
 #include <cooperative_groups.h>
+
+#include <chrono>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -1183,6 +1185,12 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
                      bool pull_form) {
     SP_CHECK(g && dist_out, SP_ERR_ARG, "sp_sssp: bad arguments");
     SP_CHECK(src >= 0 && src < g->n, SP_ERR_ARG, "node argument 'src'=%d out of range", src);
+    static const bool trace = getenv("SP_SSSP_TRACE") != nullptr;  // host phase times
+    const auto tt0 = std::chrono::steady_clock::now();
+    auto tms = [&]() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tt0)
+            .count();
+    };
     Call c;
     SP_TRY(c.begin(g->device));
     SP_TRY(ensure_weff(g, c));
@@ -1205,6 +1213,7 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
     c.persist(dist, n * sizeof(int32_t));  // the relaxations' random probes
     k_init<<<grid_for(n, kBlock, dev), kBlock, 0, c.stream>>>(dist, enq, n, src, qa);
     c.launches++;
+    if (trace) fprintf(stderr, "sssp: begin+allocs %.2f ms\n", tms());
     int64_t nq = 1, iters = 0, relaxed = 0, frontier_sum = 0;
     int rc = SP_OK;
     cudaEvent_t ka, kb;
@@ -1225,6 +1234,7 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
         const int64_t delta = pull_form ? 0 : near_far_delta(g, wr[0], wr[1]);
         if (delta > 0)
             lrc = sssp_near_far(g, c, dist, enq, qa, qb, chunks, cap, delta, &hL, &kernel_ms);
+        if (trace) fprintf(stderr, "sssp: loop done %.2f ms (kernel %.2f ms)\n", tms(), kernel_ms);
         if (delta <= 0 || (lrc == SP_OK && hL.status == 3)) {  // Bellman-Ford
             k_init<<<grid_for(n, kBlock, dev), kBlock, 0, c.stream>>>(dist, enq, n, src, qa);
             c.launches++;
