@@ -554,14 +554,20 @@ struct FastPlan {
 };
 
 int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, FastPlan &p) {
-    int64_t *kb, *hb;
-    SP_TRY(c.alloc(&kb, 4));
-    SP_TRY(c.host_as(&hb));
-    k_pr_bounds<<<1, 32, 0, c.stream>>>(g->roff, g->nzrow, g->nnz_rows, v0, v1, kb);
-    c.launches++;
-    SP_CUDA(cudaMemcpyAsync(hb + 8, kb, 32, cudaMemcpyDeviceToHost, c.stream));
-    SP_CUDA(cudaStreamSynchronize(c.stream));
-    const int64_t S[2] = {hb[8], hb[9]}, K[2] = {hb[10], hb[11]};
+    int64_t S[2] = {0, g->m}, K[2] = {0, g->nnz_rows};  // the whole graph: known on the host
+    if (v0 != 0 || v1 != g->n) {  // a vertex block (multi-GPU): slot and row bounds
+        int64_t *kb, *hb;
+        SP_TRY(c.alloc(&kb, 4));
+        SP_TRY(c.host_as(&hb));
+        k_pr_bounds<<<1, 32, 0, c.stream>>>(g->roff, g->nzrow, g->nnz_rows, v0, v1, kb);
+        c.launches++;
+        SP_CUDA(cudaMemcpyAsync(hb + 8, kb, 32, cudaMemcpyDeviceToHost, c.stream));
+        SP_CUDA(cudaStreamSynchronize(c.stream));
+        S[0] = hb[8];
+        S[1] = hb[9];
+        K[0] = hb[10];
+        K[1] = hb[11];
+    }
     PrArgs &a = p.a;
     a.radj = g->radj;
     a.nzend = g->nzend;
