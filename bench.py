@@ -488,6 +488,20 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
                                  triangles=r.env.scalars["triangle_count"],
                                  sharding=f"ranges/{world}")
         g.close()
+    if "rmat26" in a.algos and world == 1:  # cfg5b graph, resident on one GPU
+        g = sp.generate("rmat", 26, 16, seed=SEED, device=dev.index)
+        ms, _, r = timed(lambda: go(corpus.PR, g, PR_ARGS), 2, 2, world, dev)
+        it = r.env.scalars["iter"]
+        out["pr_rmat26"] = _line("pr", "rmat26 directed (cfg5b graph)", g, ms / 2, it * g.m,
+                                 it * (12 * g.m + 36 * g.n), hbm_peak, iterations=it)
+        ms, _, r = timed(lambda: go(corpus.SSSP, g, {"src": 0}), 2, 2, world, dev)
+        offs = np.asarray(g.offsets)
+        d = np.asarray(r.env.node_props["dist"].cpu())
+        m_reached = int((offs[1:] - offs[:-1])[d < 2147483647].sum())
+        mb = 12 * r.stats["edges_visited"] + 20 * r.stats["vertices_visited"]
+        out["sssp_rmat26"] = _line("sssp", "rmat26 directed (cfg5b graph)", g, ms / 2, m_reached,
+                                   mb, hbm_peak, iterations=r.fixedpoint_iterations["finished"])
+        g.close()
     return out
 
 
@@ -497,7 +511,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--algos", default="sssp,grid,bc,tc,rmat24",
+    ap.add_argument("--algos", default="sssp,grid,bc,tc,rmat24,rmat26",
                     help="secondary algorithms at N=1 ('' to skip)")
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()

@@ -103,6 +103,26 @@ struct Call {
 enum { kLoopSsspBf = 1, kLoopSsspNf = 2, kLoopPr = 3, kLoopSsspDo = 4 };
 int launch_cached_graph(cudaGraph_t graph, const void *key, int kind, cudaStream_t stream);
 
+// Per host thread: instantiated graphs that read every per-call value from
+// a device argument block owned by the entry (allocated with it), keyed by
+// (graph uid, kind).  A later call on the same graph only copies its
+// arguments into the block and launches: no capture, no update.
+struct ArgExec {
+    uint64_t key = 0;
+    int kind = 0;
+    int device = 0;
+    cudaGraphExec_t exec = nullptr;
+    void *args = nullptr;  // device argument block
+    size_t bytes = 0;
+};
+// The entry for (key, kind) with an argument block of `bytes`; *fresh says
+// whether the caller must (re)build e->exec: instantiate it when null, else
+// refresh it with cudaGraphExecUpdate (an entry handed over from another
+// graph of the same kind and layout).
+int arg_exec_get(uint64_t key, int kind, size_t bytes, int device, ArgExec **out, bool *fresh);
+enum { kArgPr = 1, kArgPrHot = 2, kArgPrRel = 3 };
+uint64_t next_graph_uid();
+
 // Copy a caller buffer to/from the device according to `mem`.
 int to_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s);
 int from_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t s);
@@ -111,6 +131,7 @@ int from_device(void *dst, const void *src, size_t bytes, int mem, cudaStream_t 
 
 // ---- the graph handle ----------------------------------------------------
 struct sp_graph {
+    uint64_t uid = sp::next_graph_uid();  // never reused (keys per-thread executable caches)
     int device = 0;
     int64_t n = 0, m = 0;
     int directed = 1;
@@ -155,6 +176,23 @@ struct sp_graph {
     int32_t *pr_radj_hot = nullptr;
     int pr_H = -1;  // -1: not built, 0: disabled
     int pr_fast_calls = 0;  // fast PR calls so far (the hot set is built on the second)
+    // edge-balanced PR plan of the whole graph (built by the first fast call):
+    // unit_row[u] = first non-empty row whose end exceeds unit u's start
+    int64_t *pr_unit_row = nullptr;
+    int64_t pr_nunits = -1;
+    // relabelled PR layout (built by the second fast call on a skewed
+    // graph): vertices ranked by out-degree (descending, ties by id), the
+    // reverse CSR in rank order with each row's sources as ranks, ascending
+    // and laid out so that one warp load instruction reads consecutive ranks
+    // (sp_pagerank.cu); rank r's original id is rel_order[r], v's rank is
+    // rel_perm[v]
+    int pr_rel = -1;  // -1: not decided, 0: not used, 1: built
+    int pr_runs = 0;  // fast single-GPU PR runs started on this graph
+    int32_t *rel_perm = nullptr, *rel_radj = nullptr, *rel_outdeg = nullptr,
+            *rel_indeg = nullptr, *rel_nzrow = nullptr;
+    int64_t *rel_nzend = nullptr, *rel_unit_row = nullptr;
+    int64_t rel_nnz = 0, rel_nunits = 0;
+    int rel_H = 0;
 };
 
 // ---- device helpers --------------------------------------------------------

@@ -191,6 +191,26 @@ __global__ void k_weff_csr(const int64_t *__restrict__ off, const int32_t *__res
 
 // Row id of every forward slot: the row starts are scattered (row x with
 // slots marks off[x] with x), then an inclusive max-scan fills the rows.
+// from_csr input checks (graph.py:18-36 invariants the device build relies
+// on): off[0] == 0, off[n] == m, rows non-decreasing; every adj id in [0, n).
+// bad[0] |= 1 for bad offsets, bad[0] |= 2 for an id out of range.
+__global__ void k_check_off(const int64_t *__restrict__ off, int64_t n, int64_t m, int *bad) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = off[x];
+        const bool ok = (x == 0 ? o == 0 : o >= off[x - 1]) && (x < n || o == m) && o <= m;
+        if (!ok) atomicOr(bad, 1);
+    }
+}
+
+__global__ void k_check_ids(const int32_t *__restrict__ adj, int64_t m, int64_t n, int *bad) {
+    bool ok = true;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x)
+        ok &= (uint32_t)adj[e] < (uint64_t)n;
+    if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 2);
+}
+
 __global__ void k_row_starts(const int64_t *__restrict__ off, int64_t n, uint32_t *mark) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
          x += (int64_t)gridDim.x * blockDim.x)
@@ -352,6 +372,14 @@ void free_graph(sp_graph *g) {
     resident_free(g->ubig);
     resident_free(g->pr_hot_ids);
     resident_free(g->pr_radj_hot);
+    resident_free(g->pr_unit_row);
+    resident_free(g->rel_perm);
+    resident_free(g->rel_radj);
+    resident_free(g->rel_outdeg);
+    resident_free(g->rel_indeg);
+    resident_free(g->rel_nzrow);
+    resident_free(g->rel_nzend);
+    resident_free(g->rel_unit_row);
     resident_free(g->wrange);
     delete g;
 }
@@ -438,12 +466,21 @@ constexpr int kUpChunks = 8;
 constexpr int64_t kUpMinSlots = int64_t(1) << 23;  // smaller graphs: one copy + one sort
 
 // start[x] = first j with key[j] >= x, x in [0, n] (key sorted, mc keys)
+// An id outside [0, n) (caller error, reported after the build) is clamped
+// to n here and skipped by k_up_scatter: no out-of-range writes.
 __global__ void k_start32(const uint32_t *__restrict__ key, int64_t mc, int64_t n,
-                          uint32_t *start) {
+                          uint32_t *start, int *bad) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= mc;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t prev = e == 0 ? -1 : (int64_t)key[e - 1];
-        const int64_t cur = e == mc ? n : (int64_t)key[e];
+        const int64_t prev = e == 0 ? -1 : min((int64_t)key[e - 1], n);
+        int64_t cur = n;
+        if (e < mc) {
+            cur = (int64_t)key[e];
+            if (cur >= n) {
+                atomicOr(bad, 2);
+                cur = n;
+            }
+        }
         for (int64_t x = prev + 1; x <= cur; x++) start[x] = (uint32_t)e;
     }
 }
@@ -468,11 +505,14 @@ __global__ void k_up_bases(const uint32_t *__restrict__ start, int C, int64_t n,
 
 // radj (and, when the PR hot set exists, its hot-encoded copy) in one pass
 __global__ void k_up_scatter(const uint32_t *__restrict__ dks, const uint32_t *__restrict__ svs,
-                             int64_t mc, const int64_t *__restrict__ base, int32_t *radj,
+                             int64_t mc, int64_t n, int64_t m, const int64_t *__restrict__ base,
+                             int32_t *radj,
                              const int32_t *__restrict__ hot_idx, int32_t *enc) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < mc;
          j += (int64_t)gridDim.x * blockDim.x) {
+        if ((int64_t)dks[j] >= n) continue;  // bad id (k_start32 flagged it)
         const int64_t pos = base[dks[j]] + j;
+        if ((uint64_t)pos >= (uint64_t)m) continue;  // only with bad ids elsewhere
         const int32_t u = (int32_t)svs[j];
         radj[pos] = u;
         if (enc) {
@@ -498,7 +538,7 @@ __global__ void k_outdeg(const int64_t *__restrict__ off, int64_t n, int32_t *de
     if ((threadIdx.x & 31) == 0 && best) atomicMax(mx, best);
 }
 
-int upload_adj_build_reverse(sp_graph *g, Call &c, const int32_t *adj_host) {
+int upload_adj_build_reverse(sp_graph *g, Call &c, const int32_t *adj_host, int *bad) {
     const int64_t n = g->n, m = g->m;
     const int b = bits_for(n);
     const int C = kUpChunks;
@@ -579,15 +619,15 @@ int upload_adj_build_reverse(sp_graph *g, Call &c, const int32_t *adj_host) {
                 return cub::DeviceRadixSort::SortPairs(t, sz, dk + e0, dks + e0, sv + e0,
                                                        svs + e0, mc, 0, b, c.stream);
             }));
-        k_start32<<<gridN(mc + 1, c.device), 256, 0, c.stream>>>(dks + e0, mc, n,
-                                                                start + (int64_t)i * (n + 1));
+        k_start32<<<gridN(mc + 1, c.device), 256, 0, c.stream>>>(
+            dks + e0, mc, n, start + (int64_t)i * (n + 1), bad);
     }
     k_up_bases<<<gridN(n + 1, c.device), 256, 0, c.stream>>>(start, C, n, g->roff, base);
     for (int i = 0; i < C; i++) {
         const int64_t e0 = cut[i], mc = cut[i + 1] - cut[i];
         if (mc)
             k_up_scatter<<<gridN(mc, c.device), 256, 0, c.stream>>>(
-                dks + e0, svs + e0, mc, base + (int64_t)i * n, g->radj, hot_idx, enc);
+                dks + e0, svs + e0, mc, n, m, base + (int64_t)i * n, g->radj, hot_idx, enc);
     }
     SP_CUDA(cudaGetLastError());
     if (H > 0) {
@@ -860,6 +900,16 @@ int sp_graph_from_edges(const int32_t *u, const int32_t *v, const int32_t *w, in
     return SP_OK;
 }
 
+// SP_CUDA for a do { } while (0) build block: record rc and leave the block
+#define SP_CUDA_BREAK(call)                                                  \
+    {                                                                        \
+        cudaError_t _e = (call);                                             \
+        if (_e != cudaSuccess) {                                             \
+            rc = ::sp::cuda_fail(_e, #call, __FILE__, __LINE__);             \
+            break;                                                           \
+        }                                                                    \
+    }
+
 int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj, const int32_t *weights,
                       int64_t n, int64_t m, int directed, int mem, int device, sp_graph **out) {
     SP_CHECK(out && n >= 0 && m >= 0 && offsets, SP_ERR_ARG, "sp_graph_from_csr: bad arguments");
@@ -877,13 +927,34 @@ int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj, const int32_t 
         if ((rc = dalloc(&g->adj, m))) break;
         if ((rc = dalloc(&g->w, m))) break;
         if ((rc = to_device(g->off, offsets, (n + 1) * 8, mem, c.stream))) break;
+        // the offsets are trusted by every build kernel: checked first
+        int *bad, *hbad;
+        if ((rc = c.alloc(&bad, 1)) || (rc = c.host_as(&hbad))) break;
+        SP_CUDA_BREAK(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+        k_check_off<<<gridN(n + 1, c.device), 256, 0, c.stream>>>(g->off, n, m, bad);
+        SP_CUDA_BREAK(cudaMemcpyAsync(hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        SP_CUDA_BREAK(cudaStreamSynchronize(c.stream));
+        if (*hbad) {
+            set_error("sp_graph_from_csr: offsets must start at 0, be non-decreasing and end "
+                      "at m = %lld", (long long)m);
+            rc = SP_ERR_ARG;
+            break;
+        }
         // large directed host CSR: the reverse CSR is built while the
-        // adjacency is still crossing PCIe
+        // adjacency is still crossing PCIe (ids checked in flight, k_start32)
         const bool pipelined = directed && mem == SP_MEM_HOST && m >= kUpMinSlots &&
                                m < (int64_t)0xFFFFFFFFll && !getenv("SP_UPLOAD_PLAIN");
         if (pipelined) {
-            if ((rc = upload_adj_build_reverse(g, c, adj))) break;
-        } else if ((rc = to_device(g->adj, adj, m * 4, mem, c.stream))) {
+            if ((rc = upload_adj_build_reverse(g, c, adj, bad))) break;
+        } else {
+            if ((rc = to_device(g->adj, adj, m * 4, mem, c.stream))) break;
+            if (m) k_check_ids<<<gridN(m, c.device), 256, 0, c.stream>>>(g->adj, m, n, bad);
+            SP_CUDA_BREAK(cudaMemcpyAsync(hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+            SP_CUDA_BREAK(cudaStreamSynchronize(c.stream));
+        }
+        if (!pipelined && *hbad) {
+            set_error("sp_graph_from_csr: adjacency id outside [0, %lld)", (long long)n);
+            rc = SP_ERR_ARG;
             break;
         }
         if (weights) {
@@ -893,6 +964,15 @@ int sp_graph_from_csr(const int64_t *offsets, const int32_t *adj, const int32_t 
         }
         // w_eff is built on first use (ensure_weff): PR/BC/TC never read it
         if ((rc = finish_graph(g, c, weights == nullptr))) break;
+        if (pipelined) {  // finish_graph synchronised the stream
+            SP_CUDA_BREAK(cudaMemcpyAsync(hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+            SP_CUDA_BREAK(cudaStreamSynchronize(c.stream));
+            if (*hbad) {
+                set_error("sp_graph_from_csr: adjacency id outside [0, %lld)", (long long)n);
+                rc = SP_ERR_ARG;
+                break;
+            }
+        }
         rc = c.finish(nullptr);
     } while (0);
     if (rc != SP_OK) {

@@ -45,10 +45,12 @@
 //   CSR order: bit-identical to the interpreter, slower on hub rows.
 // No FMA contraction anywhere: __dadd_rn/__dmul_rn are used explicitly.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
+#include <utility>
 
 #include "sp_common.cuh"
 
@@ -98,23 +100,64 @@ struct PrArgs {
     struct PrLoop *loop;  // device loop state (cin/cout/slot come from it) or null
 };
 
-// Device-side fixedPoint loop state (pr.sp:10): contrib ping-pong and diff
-// slots are picked by `cur`, so the captured kernels never change.
+// Device-side fixedPoint loop state (pr.sp:10), one per call, in the
+// argument block of the thread's cached executable (ArgExec): every per-call
+// value lives here, so the captured kernels never change.  Contrib buffers:
+// c0 holds rank0/outdeg (iteration 1 reads it); c1/c2 ping-pong from
+// iteration 2 on (iteration i writes c1 when i is odd, c2 when even).  Rows
+// without in-edges are constant from iteration 1 on, so k_pr_init writes
+// their final rank and contrib (in c1 and c2) up front, and their
+// |delta| = |base - rank0| into iteration 1's diff slot.
 struct PrLoop {
-    double *c[2];
-    double *slot[2];
-    int cur;
+    double *c0, *c1, *c2;
+    double *rank, *sums, *hp, *tp;
+    double *rank_out;  // relabelled layout: the final ranks in vertex order
+    double base, damping, eps;
+    double slot[2];  // diff of odd / even iterations
     int64_t iter, iters, max_iter, cap;
-    double eps, diff;
+    double diff;
     int status;  // 0 running/converged, 2 cap reached
 };
 
+// pr.sp:10 after an iteration: diff, iter++, stop test; the next
+// iteration's diff slot is cleared.  In a graph, sets the WHILE condition.
+__device__ __forceinline__ void pr_advance(PrLoop *L, cudaGraphConditionalHandle h, bool in_graph) {
+    const int64_t i = L->iters + 1;  // the iteration just computed
+    const double diff = __longlong_as_double(
+        (long long)__ldcg(reinterpret_cast<const unsigned long long *>(L->slot + (i & 1))));
+    L->diff = diff;
+    L->iter++;
+    L->iters = i;
+    int go = !(diff < L->eps || L->iter >= L->max_iter);  // pr.sp:10
+    if (go && L->iters >= L->cap) {
+        L->status = 2;
+        go = 0;
+    }
+    L->slot[(i + 1) & 1] = 0.0;
+    if (in_graph) cudaGraphSetConditional(h, go);
+}
+
+// Programmatic dependent launch: the kernels of one iteration are launched
+// with programmatic stream serialisation (launch_pdl), so a kernel's blocks
+// become resident while its predecessor drains; they wait here until the
+// predecessor's writes are visible (a no-op for ordinary launches).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void pr_bind(PrArgs &a) {
+    griddep_wait();
     if (a.loop) {
-        const int cur = a.loop->cur;
-        a.cin = a.loop->c[cur];
-        a.cout = a.loop->c[cur ^ 1];
-        a.diff_slot = a.loop->slot[cur];
+        const PrLoop *L = a.loop;
+        const int64_t i = L->iters + 1;  // the iteration being computed (1-based)
+        const bool odd = i & 1;
+        a.cin = i == 1 ? L->c0 : odd ? L->c2 : L->c1;
+        a.cout = odd ? L->c1 : L->c2;
+        a.diff_slot = a.loop->slot + (odd ? 1 : 0);
+        a.rank = L->rank;
+        a.sums = L->sums;
+        a.hp = L->hp;
+        a.tp = L->tp;
+        a.base = L->base;
+        a.damping = L->damping;
     }
 }
 
@@ -168,8 +211,13 @@ __device__ __forceinline__ void load_slab(const int32_t *__restrict__ radj, int6
 }
 
 // Row sums over edge-balanced units (see the file header).
-template <bool kHot>
-__device__ __forceinline__ void pr_units_body(const PrArgs &a, uint32_t *bm, const double *hot) {
+// kMode: kPlain (every gather from cin), kEnc (radj slots carry kHotBit |
+// hot index for the hot sources), kRel (relabelled layout: sources are
+// ranked by out-degree, the hot ones are exactly the ids below relH).
+enum { kPlain = 0, kEnc = 1, kRel = 2 };
+template <int kMode>
+__device__ __forceinline__ void pr_units_body(const PrArgs &a, uint32_t *bm, const double *hot,
+                                              int relH = 0) {
     const unsigned lane = lane_id();
     if (lane < kCh / 32) bm[lane] = 0u;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -210,10 +258,13 @@ __device__ __forceinline__ void pr_units_body(const PrArgs &a, uint32_t *bm, con
             double val[8];
 #pragma unroll
             for (int i = 0; i < 8; i++) {
-                if constexpr (kHot) {  // hot sources: shared-memory copy
+                if constexpr (kMode == kEnc) {  // hot sources: shared-memory copy
                     const int x = idx[i];
                     val[i] = x < 0 ? 0.0 : (x & kHotBit) ? hot[x & (kHotBit - 1)]
                                                          : __ldg(a.cin + x);
+                } else if constexpr (kMode == kRel) {
+                    const int x = idx[i];
+                    val[i] = x < 0 ? 0.0 : x < relH ? hot[x] : __ldg(a.cin + x);
                 } else {
                     val[i] = idx[i] >= 0 ? __ldg(a.cin + idx[i]) : 0.0;
                 }
@@ -281,7 +332,7 @@ __device__ __forceinline__ void pr_units_body(const PrArgs &a, uint32_t *bm, con
 __global__ void __launch_bounds__(kBlock, 4) k_pr_units(PrArgs a) {
     pr_bind(a);
     __shared__ uint32_t bitmap[kWarps][kCh / 32];
-    pr_units_body<false>(a, bitmap[threadIdx.x >> 5], nullptr);
+    pr_units_body<kPlain>(a, bitmap[threadIdx.x >> 5], nullptr);
 }
 
 // hotc[h] = contrib of the h-th hot source (one gather per iteration)
@@ -305,7 +356,20 @@ __global__ void __launch_bounds__(kHotBlock, 1) k_pr_units_hot(PrArgs a, const d
     int4 *dst = reinterpret_cast<int4 *>(hot_smem);
     for (int i = threadIdx.x; i < (H + 1) / 2; i += blockDim.x) dst[i] = __ldcg(src + i);
     __syncthreads();
-    pr_units_body<true>(a, bitmaps + (threadIdx.x >> 5) * (kCh / 32), hot_smem);
+    pr_units_body<kEnc>(a, bitmaps + (threadIdx.x >> 5) * (kCh / 32), hot_smem);
+}
+
+// Relabelled layout: the hot contribs are cin[0, H) -- one contiguous copy
+// into shared memory per block, no gather kernel.
+__global__ void __launch_bounds__(kHotBlock, 1) k_pr_units_rel(PrArgs a, int H) {
+    pr_bind(a);
+    extern __shared__ double hot_smem[];
+    uint32_t *bitmaps = reinterpret_cast<uint32_t *>(hot_smem + H);
+    const int4 *src = reinterpret_cast<const int4 *>(a.cin);
+    int4 *dst = reinterpret_cast<int4 *>(hot_smem);
+    for (int i = threadIdx.x; i < H / 2; i += blockDim.x) dst[i] = __ldcg(src + i);
+    __syncthreads();
+    pr_units_body<kRel>(a, bitmaps + (threadIdx.x >> 5) * (kCh / 32), hot_smem, H);
 }
 
 // pr.sp:17-23 for every non-empty row of the block (coalesced over k).
@@ -542,6 +606,264 @@ int ensure_pr_hot(sp_graph *g, Call &c) {
     return SP_OK;
 }
 
+// ---- relabelled layout (per graph, built once) ---------------------------
+//
+// The pull's cost is one L1/shared-memory wavefront per distinct line or
+// bank group a warp's gather instruction touches, and random source ids put
+// every lane of an instruction on its own line.  Ranking the vertices by
+// out-degree packs the sources that are gathered most into a dense prefix
+// (the hot ones, ranks < H, are a contiguous shared-memory copy), and each
+// row's sources are stored as ascending ranks, placed within every 256-slot
+// chunk so that load instruction i of lane l (slot 8l + i) reads the row's
+// (32i + l)-th element: one instruction reads 32 consecutive ranks of the
+// row -- conflict-free shared-memory banks for the hot part, shared lines
+// for the dense warm part.  Same per-row multiset of contribs, so the same
+// fast-mode sums up to the association order (fast mode only).
+
+__global__ void k_rel_rank(const int32_t *__restrict__ order, const uint32_t *__restrict__ deg_s,
+                           int64_t n, int32_t *perm, int32_t *rel_outdeg,
+                           const int32_t *__restrict__ indeg, int32_t *rel_indeg) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = order[r];
+        perm[v] = (int32_t)r;
+        rel_outdeg[r] = (int32_t)deg_s[r];
+        rel_indeg[r] = indeg[v];
+    }
+}
+
+__global__ void k_rel_rowmark(const int64_t *__restrict__ roff, int64_t n, uint32_t *mark) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        if (roff[v + 1] > roff[v]) mark[roff[v]] = (uint32_t)v;
+}
+
+__global__ void k_rel_keys(const uint32_t *__restrict__ rowof, const int32_t *__restrict__ radj,
+                           const int32_t *__restrict__ perm, int64_t m, int b, uint64_t *key) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x)
+        key[k] = ((uint64_t)(uint32_t)perm[rowof[k]] << b) | (uint32_t)perm[radj[k]];
+}
+
+// roff[x] = first slot whose row (key >> b) is >= x, x in [0, n]
+__global__ void k_rel_offsets(const uint64_t *__restrict__ key, int64_t m, int64_t n, int b,
+                              int64_t *roff) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t prev = e == 0 ? -1 : (int64_t)(key[e - 1] >> b);
+        const int64_t cur = e == m ? n : (int64_t)(key[e] >> b);
+        for (int64_t x = prev + 1; x <= cur; x++) roff[x] = e;
+    }
+}
+
+__global__ void k_rel_nzend(const int64_t *__restrict__ roff, const int32_t *__restrict__ nzrow,
+                            const int64_t *__restrict__ cnt, int64_t *nzend) {
+    const int64_t k1 = *cnt;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < k1;
+         k += (int64_t)gridDim.x * blockDim.x)
+        nzend[k] = roff[nzrow[k] + 1];
+}
+
+// number of q in [0, x) with q % 8 == r
+__device__ __forceinline__ int64_t rel_cnt(int64_t x, int r) { return x > r ? (x - r + 7) >> 3 : 0; }
+
+// Within the part [a, b) of a row that lies in one 256-slot chunk, the
+// positions are filled in the order (q % 8, q / 8) of their chunk offset q:
+// the element of sorted rank k goes to the k-th position in that order.
+__global__ void k_rel_place(const uint64_t *__restrict__ key, int64_t m, int b,
+                            const int64_t *__restrict__ roff, int32_t *out) {
+    const uint64_t mask = (uint64_t(1) << b) - 1;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = (int64_t)(key[p] >> b);
+        const int64_t c0 = p & ~int64_t(kCh - 1);
+        const int64_t a = max(roff[row], c0), e = min(roff[row + 1], c0 + kCh);
+        const int64_t lo = a - c0, hi = e - c0, pp = p - c0;
+        const int rp = (int)(pp & 7);
+        int64_t k = rel_cnt(pp, rp) - rel_cnt(lo, rp);
+        for (int r = 0; r < rp; r++) k += rel_cnt(hi, r) - rel_cnt(lo, r);
+        out[p] = (int32_t)(key[a + k] & mask);
+    }
+}
+
+struct NonEmptyRank {
+    const int32_t *deg;
+    __device__ __forceinline__ bool operator()(int32_t x) const { return deg[x] > 0; }
+};
+
+struct MaxRow {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const {
+        return a > b ? a : b;
+    }
+};
+
+int bits_for_n(int64_t n) {
+    int b = 1;
+    while (b < 62 && ((int64_t)1 << b) < n) b++;
+    return b;
+}
+
+// Builds the relabelled layout when the hot-source criterion holds (the
+// graph is skewed enough for a shared-memory hot set); otherwise pr_rel = 0.
+int ensure_pr_rel(sp_graph *g, Call &c) {
+    std::lock_guard<std::mutex> lk(g_hot_mu);
+    if (g->pr_rel >= 0) return SP_OK;
+    const char *re = getenv("SP_PR_REL");
+    const char *ce = getenv("SP_PR_HOT_COVER");
+    const double min_cover = ce ? atof(ce) : kHotMinCover;
+    const int64_t n = g->n, m = g->m;
+    // Where it pays (measured, B200, RMAT ef16, ms per run rel / encoded):
+    // the contrib array 8n must exceed the L2 (the ranking then keeps the
+    // gathered sources' lines L2-resident: RMAT-24 7.68 / 8.26) but not by
+    // far (RMAT-26: 38.3 / 32.4 -- the final unpermute pass and the
+    // scattered rank-order rows cost more); an L2-resident contrib gains
+    // nothing (RMAT-22: 2.98 / 2.92).  SP_PR_REL=1 forces it, =0 disables.
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c.device);
+    const bool in_band = 8.0 * (double)n > (double)l2 && 8.0 * (double)n <= 2.5 * (double)l2;
+    const bool force = re && re[0] == '1';
+    if ((re && re[0] == '0') || (!force && !in_band) || m < kHotMinSlots || n >= kHotBit ||
+        2 * bits_for_n(n) > 64 ||
+        (double)std::min<int64_t>(kHotMax, n) * (double)g->max_outdeg < min_cover * (double)m) {
+        g->pr_rel = 0;
+        return SP_OK;
+    }
+    const int b = bits_for_n(n);
+    // out-degree ranking (stable: ties by id) and the hot coverage
+    uint32_t *key, *key_s;
+    int32_t *id, *id_s;
+    SP_TRY(c.alloc(&key, n));
+    SP_TRY(c.alloc(&key_s, n));
+    SP_TRY(c.alloc(&id, n));
+    SP_TRY(c.alloc(&id_s, n));
+    int32_t *hot_dummy;
+    SP_TRY(c.alloc(&hot_dummy, n));
+    k_hot_keys<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(g->outdeg, n, key, id,
+                                                                     hot_dummy);
+    size_t tmp = 0;
+    SP_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, key, key_s, id, id_s, n, 0,
+                                                      32, c.stream));
+    void *dt = nullptr;
+    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(dt, tmp, key, key_s, id, id_s, n,
+                                                              0, 32, c.stream);
+    scratch_free(dt, c.stream);
+    SP_CUDA(e);
+    const int H = (int)(std::min<int64_t>(kHotMax, n) & ~int64_t(1));
+    unsigned long long *cov;
+    SP_TRY(c.alloc(&cov, 1));
+    tmp = 0;
+    SP_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, key_s, cov, H, c.stream));
+    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
+    e = cub::DeviceReduce::Sum(dt, tmp, key_s, cov, H, c.stream);
+    scratch_free(dt, c.stream);
+    SP_CUDA(e);
+    unsigned long long *hcov;
+    SP_TRY(c.host_as(&hcov));
+    SP_CUDA(cudaMemcpyAsync(hcov, cov, 8, cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    if ((double)hcov[0] < min_cover * (double)m) {
+        g->pr_rel = 0;
+        return SP_OK;
+    }
+    int32_t *perm = nullptr, *radj = nullptr, *outd = nullptr, *ind = nullptr, *nzrow = nullptr;
+    int64_t *nzend = nullptr, *ur = nullptr;
+    struct Guard {  // frees the resident arrays unless the build completes
+        int32_t **a[5];
+        int64_t **b[2];
+        bool ok = false;
+        ~Guard() {
+            if (ok) return;
+            for (auto p : a) resident_free(*p);
+            for (auto p : b) resident_free(*p);
+        }
+    } guard{{&perm, &radj, &outd, &ind, &nzrow}, {&nzend, &ur}};
+    SP_TRY(resident_alloc((void **)&perm, (size_t)n * 4 + 16));
+    SP_TRY(resident_alloc((void **)&radj, (size_t)m * 4 + 16));
+    SP_TRY(resident_alloc((void **)&outd, (size_t)n * 4 + 16));
+    SP_TRY(resident_alloc((void **)&ind, (size_t)n * 4 + 16));
+    SP_TRY(resident_alloc((void **)&nzrow, (size_t)n * 4 + 16));
+    SP_TRY(resident_alloc((void **)&nzend, (size_t)n * 8 + 16));
+    k_rel_rank<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(id_s, key_s, n, perm, outd,
+                                                                     g->indeg, ind);
+    // the reverse CSR in rank order: sort (rank of row, rank of source)
+    uint32_t *rowof;
+    uint64_t *k0, *k1;
+    SP_TRY(c.alloc(&rowof, m));
+    SP_TRY(c.alloc(&k0, m));
+    SP_TRY(c.alloc(&k1, m));
+    SP_CUDA(cudaMemsetAsync(rowof, 0, (size_t)m * 4, c.stream));
+    k_rel_rowmark<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(g->roff, n, rowof);
+    tmp = 0;
+    SP_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tmp, rowof, rowof, MaxRow(), m,
+                                           c.stream));
+    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
+    e = cub::DeviceScan::InclusiveScan(dt, tmp, rowof, rowof, MaxRow(), m,
+                                       c.stream);
+    scratch_free(dt, c.stream);
+    SP_CUDA(e);
+    k_rel_keys<<<grid_for(m, 256, c.device, 16), 256, 0, c.stream>>>(rowof, g->radj, perm, m, b,
+                                                                     k0);
+    tmp = 0;
+    SP_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k0, k1, m, 0, 2 * b, c.stream));
+    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
+    e = cub::DeviceRadixSort::SortKeys(dt, tmp, k0, k1, m, 0, 2 * b, c.stream);
+    scratch_free(dt, c.stream);
+    SP_CUDA(e);
+    int64_t *roff2;
+    SP_TRY(c.alloc(&roff2, n + 1));
+    k_rel_offsets<<<grid_for(m + 1, 256, c.device, 16), 256, 0, c.stream>>>(k1, m, n, b, roff2);
+    k_rel_place<<<grid_for(m, 256, c.device, 16), 256, 0, c.stream>>>(k1, m, b, roff2, radj);
+    // non-empty rows in rank order and their ends
+    int64_t *nsel;
+    SP_TRY(c.alloc(&nsel, 1));
+    NonEmptyRank pred{ind};
+    tmp = 0;
+    SP_CUDA(cub::DeviceSelect::If(nullptr, tmp, thrust::counting_iterator<int32_t>(0), nzrow, nsel,
+                                  n, pred, c.stream));
+    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
+    e = cub::DeviceSelect::If(dt, tmp, thrust::counting_iterator<int32_t>(0), nzrow, nsel, n, pred,
+                              c.stream);
+    scratch_free(dt, c.stream);
+    SP_CUDA(e);
+    k_rel_nzend<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(roff2, nzrow, nsel, nzend);
+    int64_t *hn;
+    SP_TRY(c.host_as(&hn));
+    SP_CUDA(cudaMemcpyAsync(hn, nsel, 8, cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t nnz = hn[0];
+    const int64_t nunits = m ? (m - 1) / kUnit + 1 : 0;
+    SP_TRY(resident_alloc((void **)&ur, (size_t)std::max<int64_t>(1, nunits) * 8 + 16));
+    if (nunits)
+        k_pr_setup<<<grid_for(nunits, 256, c.device), 256, 0, c.stream>>>(nzend, 0, nnz, 0, 0,
+                                                                          nunits, ur);
+    c.launches += 12;
+    SP_CUDA(cudaGetLastError());
+    SP_CUDA(cudaStreamSynchronize(c.stream));  // other threads' streams read the layout
+    g->rel_perm = perm;
+    g->rel_radj = radj;
+    g->rel_outdeg = outd;
+    g->rel_indeg = ind;
+    g->rel_nzrow = nzrow;
+    g->rel_nzend = nzend;
+    g->rel_unit_row = ur;
+    g->rel_nnz = nnz;
+    g->rel_nunits = nunits;
+    g->rel_H = H;
+    g->pr_rel = 1;
+    guard.ok = true;
+    return SP_OK;
+}
+
+// rank[v] = rank'[rank of v]: the relabelled run's ranks in vertex order
+__global__ void k_pr_unperm(const PrLoop *L, const int32_t *__restrict__ perm, int64_t n) {
+    const double *rr = L->rank;
+    double *out = L->rank_out;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        out[v] = rr[__ldcs(perm + v)];
+}
+
 // Per-call state of the fast path for a vertex block [v0, v1).
 struct FastPlan {
     PrArgs a{};
@@ -551,9 +873,53 @@ struct FastPlan {
     size_t hot_smem = 0;
     const int32_t *hot_ids = nullptr;
     double *hotc = nullptr;
+    // relabelled layout (whole graph only): rows and sources are ranks
+    bool rel = false;
+    const int32_t *init_outdeg = nullptr, *init_indeg = nullptr;  // k_pr_init's view
 };
 
-int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, FastPlan &p) {
+// The whole-graph plan over the relabelled layout (ensure_pr_rel built it).
+int plan_rel(sp_graph *g, Call &c, double damping, FastPlan &p) {
+    PrArgs &a = p.a;
+    a.radj = g->rel_radj;
+    a.nzend = g->rel_nzend;
+    a.nzrow = g->rel_nzrow;
+    a.outdeg = g->rel_outdeg;
+    a.v0 = 0;
+    a.S0 = 0;
+    a.S1 = g->m;
+    a.K0 = 0;
+    a.K1 = g->rel_nnz;
+    a.u0 = 0;
+    a.nunits = g->rel_nunits;
+    a.base = (1.0 - damping) / (double)g->n;  // pr.sp:17
+    a.damping = damping;
+    a.unit_row = g->rel_unit_row;
+    const int64_t nu = std::max<int64_t>(1, a.nunits);
+    double *hp, *tp, *sums;
+    SP_TRY(c.alloc(&sums, std::max<int64_t>(1, a.K1)));
+    SP_TRY(c.alloc(&hp, nu));
+    SP_TRY(c.alloc(&tp, nu));
+    a.sums = sums;
+    a.hp = hp;
+    a.tp = tp;
+    p.rel = true;
+    p.H = g->rel_H;
+    p.hot_smem = (size_t)p.H * sizeof(double) + (kHotBlock / 32) * (kCh / 32) * 4;
+    SP_CUDA(cudaFuncSetAttribute(k_pr_units_rel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)p.hot_smem));
+    p.grid_hot = num_sms(c.device);
+    p.grid_units = (int)std::max<int64_t>(1, (a.nunits + kWarps - 1) / kWarps);
+    p.grid_epi = (int)std::max<int64_t>(1, (a.K1 + 256 * kEpi - 1) / (256 * kEpi));
+    p.init_outdeg = g->rel_outdeg;
+    p.init_indeg = g->rel_indeg;
+    return SP_OK;
+}
+
+// hotc_ext: caller-owned buffer of >= pr_H + 1 doubles for the hot copies
+// (the cached device loop keeps it in its argument block), or null.
+int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, FastPlan &p,
+              double *hotc_ext = nullptr, bool hot_settled = false) {
     int64_t S[2] = {0, g->m}, K[2] = {0, g->nnz_rows};  // the whole graph: known on the host
     if (v0 != 0 || v1 != g->n) {  // a vertex block (multi-GPU): slot and row bounds
         int64_t *kb, *hb;
@@ -583,8 +949,29 @@ int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, Fast
     a.base = (1.0 - damping) / (double)g->n;  // pr.sp:17, no FMA on host either
     a.damping = damping;
     const int64_t nu = std::max<int64_t>(1, a.nunits);
-    int64_t *ur;
-    SP_TRY(c.alloc(&ur, nu));
+    const bool whole = v0 == 0 && v1 == g->n;
+    int64_t *ur = nullptr;
+    if (whole) {  // the whole graph's unit index: built once, resident
+        std::lock_guard<std::mutex> lk(g_hot_mu);
+        if (g->pr_nunits < 0) {
+            SP_TRY(resident_alloc((void **)&g->pr_unit_row, (size_t)nu * sizeof(int64_t)));
+            if (a.nunits) {
+                k_pr_setup<<<grid_for(a.nunits, 256, c.device), 256, 0, c.stream>>>(
+                    g->nzend, a.K0, a.K1, a.S0, a.u0, a.nunits, g->pr_unit_row);
+                c.launches++;
+            }
+            SP_CUDA(cudaStreamSynchronize(c.stream));  // other threads' streams read it
+            g->pr_nunits = a.nunits;
+        }
+        ur = g->pr_unit_row;
+    } else {
+        SP_TRY(c.alloc(&ur, nu));
+        if (a.nunits) {
+            k_pr_setup<<<grid_for(a.nunits, 256, c.device), 256, 0, c.stream>>>(
+                g->nzend, a.K0, a.K1, a.S0, a.u0, a.nunits, ur);
+            c.launches++;
+        }
+    }
     double *hp, *tp, *sums;
     SP_TRY(c.alloc(&sums, std::max<int64_t>(1, a.K1 - a.K0)));
     a.sums = sums;
@@ -593,21 +980,20 @@ int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, Fast
     a.hp = hp;
     a.tp = tp;
     a.unit_row = ur;
-    if (a.nunits) {
-        k_pr_setup<<<grid_for(a.nunits, 256, c.device), 256, 0, c.stream>>>(
-            g->nzend, a.K0, a.K1, a.S0, a.u0, a.nunits, ur);
-        c.launches++;
-    }
     // one unit per warp, no cap: the block scheduler balances the tail
     p.grid_units = (int)std::max<int64_t>(1, (a.nunits + kWarps - 1) / kWarps);
-    SP_TRY(ensure_pr_hot(g, c));
+    if (!hot_settled) SP_TRY(ensure_pr_hot(g, c));
     if (g->pr_H > 0) {
         p.H = g->pr_H;
         p.hot_ids = g->pr_hot_ids;
         a.radj = g->pr_radj_hot;  // encoded slots
-        double *hotc;
-        SP_TRY(c.alloc(&hotc, p.H + 1));
-        p.hotc = hotc;
+        if (!hotc_ext) {
+            double *hotc;
+            SP_TRY(c.alloc(&hotc, p.H + 1));
+            p.hotc = hotc;
+        } else {
+            p.hotc = hotc_ext;
+        }
         p.hot_smem = (size_t)p.H * sizeof(double) + (kHotBlock / 32) * (kCh / 32) * 4;
         SP_CUDA(cudaFuncSetAttribute(k_pr_units_hot, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)p.hot_smem));
@@ -615,19 +1001,47 @@ int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, Fast
     }
     p.grid_epi = (int)std::max<int64_t>(1, (a.K1 - a.K0 + 256 * kEpi - 1) / (256 * kEpi));
     p.grid_zero = (int)std::max<int64_t>(1, (v1 - v0 + 255) / 256);
+    p.init_outdeg = g->outdeg;
+    p.init_indeg = g->indeg;
     SP_CUDA(cudaGetLastError());
     return SP_OK;
 }
 
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                Args &&...args) {
+    // opt-in (SP_PR_PDL=1): measured neutral on B200 (RMAT-22 2.921 vs
+    // 2.922 ms per run; RMAT-24 relabelled 7.89 vs 7.70 ms)
+    static const bool off = [] {
+        const char *e = getenv("SP_PR_PDL");
+        return !(e && e[0] == '1');
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // The row-sum kernel of one iteration (hot-source variant when built).
 void launch_units(Call &c, const FastPlan &p, const PrArgs &a) {
-    if (p.H > 0) {
-        k_pr_hot_gather<<<grid_for(p.H, 256, c.device), 256, 0, c.stream>>>(a, p.hot_ids, p.H,
-                                                                            p.hotc);
-        k_pr_units_hot<<<p.grid_hot, kHotBlock, p.hot_smem, c.stream>>>(a, p.hotc, p.H);
+    if (p.rel) {
+        launch_pdl(k_pr_units_rel, p.grid_hot, kHotBlock, p.hot_smem, c.stream, a, p.H);
+        c.launches++;
+    } else if (p.H > 0) {
+        launch_pdl(k_pr_hot_gather, grid_for(p.H, 256, c.device), 256, 0, c.stream, a, p.hot_ids,
+                   p.H, p.hotc);
+        launch_pdl(k_pr_units_hot, p.grid_hot, kHotBlock, p.hot_smem, c.stream, a,
+                   (const double *)p.hotc, p.H);
         c.launches += 2;
     } else {
-        k_pr_units<<<p.grid_units, kBlock, 0, c.stream>>>(a);
+        launch_pdl(k_pr_units, p.grid_units, kBlock, 0, c.stream, a);
         c.launches++;
     }
 }
@@ -656,85 +1070,123 @@ int launch_fast(Call &c, FastPlan &p, sp_graph *g, int64_t v1, const double *cin
     return SP_OK;
 }
 
-__global__ void k_pr_advance(PrLoop *L, cudaGraphConditionalHandle h) {
-    const int cur = L->cur;
-    const double diff = *L->slot[cur];
-    L->diff = diff;
-    L->iter++;
-    L->iters++;
-    int go = !(diff < L->eps || L->iter >= L->max_iter);  // pr.sp:10
-    if (go && L->iters >= L->cap) {
-        L->status = 2;
-        go = 0;
+// Loop-path init (pr.sp:5-8 plus iteration 1 of the zero-in-degree rows):
+// rank = 1/n and c0 = rank/outdeg for every vertex; rows with no in-edges
+// get their final rank = base now, c1 = c2 = base/outdeg, and contribute
+// |base - 1/n| to iteration 1's diff (exactly what iteration 1 computes for
+// them: sum = 0).
+__global__ void __launch_bounds__(256) k_pr_init(PrLoop *L, const int32_t *__restrict__ outdeg,
+                                                 const int32_t *__restrict__ indeg, int64_t n,
+                                                 double r0) {
+    const double base = L->base;
+    double *rank = L->rank, *c0 = L->c0, *c1 = L->c1, *c2 = L->c2;
+    double dmax = 0.0;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int d = __ldcs(outdeg + x);
+        c0[x] = d > 0 ? __ddiv_rn(r0, (double)d) : 0.0;
+        if (__ldcs(indeg + x) == 0) {
+            rank[x] = base;
+            const double cz = d > 0 ? __ddiv_rn(base, (double)d) : 0.0;
+            c1[x] = cz;
+            c2[x] = cz;
+            double t = __dsub_rn(base, r0);
+            if (t < 0.0) t = __dsub_rn(0.0, t);
+            dmax = fmax(dmax, t);
+        } else {
+            rank[x] = r0;
+        }
     }
-    *L->slot[cur ^ 1] = 0.0;
-    L->cur = cur ^ 1;
-    cudaGraphSetConditional(h, go);
+    dmax = warp_max(dmax);
+    // the same value from every block: read first, so at most a few atomics
+    if (lane_id() == 0 && dmax > 0.0 &&
+        __double_as_longlong(dmax) >
+            (long long)__ldcg(reinterpret_cast<const unsigned long long *>(L->slot + 1)))
+        atomic_max_nonneg(L->slot + 1, dmax);
 }
 
-// Iterations 2.. of the fast path as one graph launch (no host round trip
-// per iteration).  `hL` receives the final loop state.
-int pr_device_loop(Call &c, FastPlan &p, double *rank, double *c0, double *c1, double *s0,
-                   double *s1, int64_t iter0, int64_t iters0, int64_t max_iter, int64_t cap,
-                   double eps, PrLoop *hL, float *kernel_ms) {
-    PrLoop *L;
-    SP_TRY(c.alloc(&L, 1));
-    PrLoop init{};
-    init.c[0] = c0;
-    init.c[1] = c1;
-    init.slot[0] = s0;
-    init.slot[1] = s1;
-    init.iter = iter0;
-    init.iters = iters0;
-    init.max_iter = max_iter;
-    init.cap = cap;
-    init.eps = eps;
-    SP_CUDA(cudaMemcpyAsync(L, &init, sizeof(PrLoop), cudaMemcpyHostToDevice, c.stream));
-    SP_CUDA(cudaMemsetAsync(s0, 0, sizeof(double), c.stream));
-    PrArgs a = p.a;
-    a.rank = rank;
-    a.loop = L;
+// The loop step as its own launch (graphs without non-empty rows).
+__global__ void k_pr_advance(PrLoop *L, cudaGraphConditionalHandle h, int in_graph) {
+    griddep_wait();
+    pr_advance(L, h, in_graph != 0);
+}
+
+
+// The body of one fast iteration on the call's stream.
+// One iteration and the loop step (in a graph: sets the WHILE flag).  (A
+// last-block-done step inside k_pr_epi measured slower: thousands of
+// same-address counter atomics serialise at one L2 slice.)
+void launch_iteration(Call &c, const FastPlan &p, const PrArgs &a, bool in_graph,
+                      cudaGraphConditionalHandle cond) {
+    if (a.nunits) {
+        launch_units(c, p, a);
+        launch_pdl(k_pr_epi, p.grid_epi, 256, 0, c.stream, a);
+        c.launches++;
+    }
+    launch_pdl(k_pr_advance, 1, 1, 0, c.stream, a.loop, cond, in_graph ? 1 : 0);
+    c.launches++;
+}
+
+// Instantiate the whole fast run as one graph: k_pr_init, then a WHILE node
+// over { [hot gather,] units, epilogue, advance }.  Every per-call value is
+// read from L, so the executable is reused by every later call of this
+// thread on this graph (arg_exec_get): no capture, no update, no host round
+// trip per iteration.
+// A reused entry of another graph (same kind, same argument layout) is
+// refreshed with cudaGraphExecUpdate instead of a new instantiation: a graph
+// created per request (from_csr -> run) then costs one capture, not an
+// instantiation.
+int pr_build_exec(sp_graph *g, Call &c, const FastPlan &p, PrLoop *L, cudaGraphExec_t *exec) {
     cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
     struct GraphFree {
         cudaGraph_t *g;
-        cudaGraphExec_t *e;
         ~GraphFree() {
-            if (*e) cudaGraphExecDestroy(*e);
             if (*g) cudaGraphDestroy(*g);
         }
-    } gf{&graph, &exec};
+    } gf{&graph};
     SP_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle h;
     SP_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+    // k_pr_init as the first node (captured into the top-level graph)
+    SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, graph, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+    const double r0 = 1.0 / (double)g->n;  // pr.sp:6
+    k_pr_init<<<grid_for(g->n, 256, c.device), 256, 0, c.stream>>>(L, p.init_outdeg, p.init_indeg,
+                                                                   g->n, r0);
+    SP_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    size_t nn = 0;
+    SP_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+    SP_CHECK(nn == 1, SP_ERR_CUDA, "pr graph: unexpected init capture");
+    cudaGraphNode_t init;
+    SP_CUDA(cudaGraphGetNodes(graph, &init, &nn));
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = h;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
     cudaGraphNode_t node;
-    SP_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    SP_CUDA(cudaGraphAddNode(&node, graph, &init, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
                                           cudaStreamCaptureModeThreadLocal));
-    if (a.nunits) {
-        launch_units(c, p, a);
-        k_pr_epi<<<p.grid_epi, 256, 0, c.stream>>>(a);
-    }
-    k_pr_advance<<<1, 1, 0, c.stream>>>(L, h);
+    PrArgs a = p.a;
+    a.loop = L;
+    launch_iteration(c, p, a, true, h);
     SP_CUDA(cudaStreamEndCapture(c.stream, &body));
-    cudaEvent_t ka, kb;
-    SP_CUDA(cudaEventCreate(&ka));
-    SP_CUDA(cudaEventCreate(&kb));
-    cudaEventRecord(ka, c.stream);
-    SP_TRY(launch_cached_graph(graph, p.a.radj, kLoopPr, c.stream));
-    cudaEventRecord(kb, c.stream);
-    SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(PrLoop), cudaMemcpyDeviceToHost, c.stream));
-    SP_CUDA(cudaStreamSynchronize(c.stream));
-    cudaEventElapsedTime(kernel_ms, ka, kb);
-    cudaEventDestroy(ka);
-    cudaEventDestroy(kb);
-    c.launches += (hL->iters - iters0) * 3;
+    if (p.rel) {  // the ranks back in vertex order, after the loop
+        SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, graph, &node, nullptr, 1,
+                                              cudaStreamCaptureModeThreadLocal));
+        k_pr_unperm<<<grid_for(g->n, 256, c.device, 16), 256, 0, c.stream>>>(L, g->rel_perm, g->n);
+        SP_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    }
+    if (*exec) {
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(*exec, graph, &info) == cudaSuccess) return SP_OK;
+        cudaGetLastError();
+        cudaGraphExecDestroy(*exec);
+        *exec = nullptr;
+    }
+    SP_CUDA(cudaGraphInstantiate(exec, graph, 0));
     return SP_OK;
 }
 
@@ -827,6 +1279,141 @@ int pr_hot_prepare(sp_graph *g, Call &c, const int32_t *outdeg, int64_t max_outd
 }
 }  // namespace sp
 
+namespace {
+
+// The default (fast) path: one cached graph launch per call (see
+// pr_build_exec), or -- with a per-iteration callback or SP_HOSTLOOP=1 (ncu
+// cannot profile conditional graphs) -- the same kernels driven from the
+// host with one flag read per iteration.
+int pr_fast_run(sp_graph *g, Call &c, double damping, double epsilon, int64_t max_iter,
+                int64_t cap, sp_iter_cb cb, void *user, double *rank, PrLoop *hL,
+                float *kernel_ms) {
+    const int64_t n = g->n;
+    const char *hl = getenv("SP_HOSTLOOP");
+    const bool hostloop = cb || (hl && hl[0] == '1');
+    // the layout must be settled before the executable is chosen: the
+    // relabelled one from the graph's second fast call on (its build costs
+    // about two runs), else the hot-encoded or plain one
+    int runs;
+    {
+        std::lock_guard<std::mutex> lk(g_hot_mu);
+        runs = g->pr_runs++;
+    }
+    if (runs > 0) SP_TRY(ensure_pr_rel(g, c));
+    const bool rel = g->pr_rel == 1;
+    if (!rel) SP_TRY(ensure_pr_hot(g, c));
+    const int H = rel ? 0 : std::max(0, g->pr_H);
+    const size_t hot_off = (sizeof(PrLoop) + 255) & ~size_t(255);
+    const size_t bytes = hot_off + (size_t)(H + 1) * sizeof(double);
+    ArgExec *e = nullptr;
+    bool fresh = false;
+    PrLoop *L;
+    double *hotc = nullptr;
+    if (!hostloop) {
+        SP_TRY(arg_exec_get(g->uid, rel ? kArgPrRel : H > 0 ? kArgPrHot : kArgPr, bytes, c.device,
+                            &e, &fresh));
+        L = static_cast<PrLoop *>(e->args);
+        hotc = reinterpret_cast<double *>(static_cast<char *>(e->args) + hot_off);
+    } else {
+        char *blk;
+        SP_TRY(c.alloc(&blk, bytes));
+        L = reinterpret_cast<PrLoop *>(blk);
+        hotc = reinterpret_cast<double *>(blk + hot_off);
+    }
+    FastPlan plan;
+    if (rel) {
+        SP_TRY(plan_rel(g, c, damping, plan));
+    } else {
+        SP_TRY(plan_fast(g, c, 0, n, damping, plan, hotc, true));
+    }
+    double *c0, *c1, *c2, *rank_rel = nullptr;
+    if (rel) SP_TRY(c.alloc(&rank_rel, n));
+    SP_TRY(c.alloc(&c0, n));
+    SP_TRY(c.alloc(&c1, n));
+    SP_TRY(c.alloc(&c2, n));
+    char *pin;
+    SP_TRY(c.host_as(&pin));
+    static_assert(2048 + sizeof(PrLoop) <= kPinnedBlock, "pinned block layout");
+    PrLoop *init = reinterpret_cast<PrLoop *>(pin + 2048);  // hL is at the block's start
+    *init = PrLoop{};
+    init->c0 = c0;
+    init->c1 = c1;
+    init->c2 = c2;
+    init->rank = rel ? rank_rel : rank;
+    init->rank_out = rank;
+    init->sums = plan.a.sums;
+    init->hp = plan.a.hp;
+    init->tp = plan.a.tp;
+    init->base = plan.a.base;
+    init->damping = damping;
+    init->eps = epsilon;
+    init->max_iter = max_iter;
+    init->cap = cap;
+    SP_CUDA(cudaMemcpyAsync(L, init, sizeof(PrLoop), cudaMemcpyHostToDevice, c.stream));
+    const int per_it = (plan.a.nunits ? (H > 0 ? 3 : 2) : 0) + 1;
+    cudaEvent_t ka, kb;
+    SP_CUDA(cudaEventCreate(&ka));
+    SP_CUDA(cudaEventCreate(&kb));
+    struct EvFree {
+        cudaEvent_t a, b;
+        ~EvFree() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } ef{ka, kb};
+    if (!hostloop) {
+        if (fresh) {
+            const int64_t l0 = c.launches;
+            static const bool verbose = getenv("SP_PR_VERBOSE") != nullptr;
+            if (verbose)
+                fprintf(stderr, "pr exec: %s (graph %llu)\n",
+                        e->exec ? "capture + update" : "capture + instantiate",
+                        (unsigned long long)g->uid);
+            int rc = pr_build_exec(g, c, plan, L, &e->exec);
+            c.launches = l0;
+            if (rc != SP_OK) {
+                e->exec = nullptr;
+                return rc;
+            }
+        }
+        SP_CUDA(cudaEventRecord(ka, c.stream));
+        SP_CUDA(cudaGraphLaunch(e->exec, c.stream));
+        SP_CUDA(cudaEventRecord(kb, c.stream));
+        SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(PrLoop), cudaMemcpyDeviceToHost, c.stream));
+        SP_CUDA(cudaStreamSynchronize(c.stream));
+        c.launches += 1 + hL->iters * per_it + (rel ? 1 : 0);
+    } else {
+        PrArgs a = plan.a;
+        a.loop = L;
+        const double r0 = 1.0 / (double)n;
+        SP_CUDA(cudaEventRecord(ka, c.stream));
+        k_pr_init<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(L, plan.init_outdeg,
+                                                                    plan.init_indeg, n, r0);
+        c.launches++;
+        for (;;) {
+            launch_iteration(c, plan, a, false, cudaGraphConditionalHandle{});
+            SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(PrLoop), cudaMemcpyDeviceToHost, c.stream));
+            SP_CUDA(cudaStreamSynchronize(c.stream));
+            if (cb && cb(hL->iters, user)) {
+                set_error("aborted by the fixedPoint iteration callback");
+                return SP_ERR_ABORTED;
+            }
+            if (hL->status == 2 || hL->diff < epsilon || hL->iter >= max_iter) break;
+        }
+        if (rel) {
+            k_pr_unperm<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(L, g->rel_perm, n);
+            c.launches++;
+        }
+        SP_CUDA(cudaEventRecord(kb, c.stream));
+    }
+    SP_CUDA(cudaGetLastError());
+    SP_CUDA(cudaEventSynchronize(kb));
+    cudaEventElapsedTime(kernel_ms, ka, kb);
+    return SP_OK;
+}
+
+}  // namespace
+
 extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t max_iter,
                            int64_t cap, unsigned flags, double *rank_out, int mem,
                            int64_t *iter_out, double *diff_out, int64_t *iters_out,
@@ -836,69 +1423,22 @@ extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t 
     SP_TRY(c.begin(g->device));
     const int64_t n = g->n;
     const bool exact = flags & SP_FLAG_DETERMINISTIC;
-    double *rank, *ca, *cb2, *diffs;
-    SP_TRY(c.alloc(&rank, n));
-    SP_TRY(c.alloc(&ca, n));
-    SP_TRY(c.alloc(&cb2, n));
-    const int64_t kSlots = 1024;  // diff slots, recycled in a ring
-    SP_TRY(c.alloc(&diffs, kSlots));
-    SP_CUDA(cudaMemsetAsync(diffs, 0, kSlots * sizeof(double), c.stream));
-    double *hdiff = nullptr;
-    SP_TRY(c.host_as(&hdiff));
-    FastPlan plan;
-    if (n && !exact) SP_TRY(plan_fast(g, c, 0, n, damping, plan));
-    const double r0 = n ? 1.0 / (double)n : 0.0;  // pr.sp:6
-    if (n) {
-        k_init<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(rank, ca, g->outdeg, 0, n, r0);
-        c.launches++;
+    // results land in the caller's buffer directly when it is device memory
+    double *rank = nullptr;
+    if (mem == SP_MEM_DEVICE && n) {
+        rank = rank_out;
+    } else {
+        SP_TRY(c.alloc(&rank, n));
     }
-    cudaEvent_t ka, kb;
-    SP_CUDA(cudaEventCreate(&ka));
-    SP_CUDA(cudaEventCreate(&kb));
     float kernel_ms = 0.f;
     int64_t iter = 0, iters = 0;
     double diff = 0.0;
     int rc = SP_OK;
-    for (;;) {
-        double *slot = diffs + (iters % kSlots);
-        if (n) {
-            rc = exact ? launch_exact(g, c, 0, n, damping, ca, rank, cb2, slot, ka, kb)
-                       : launch_fast(c, plan, g, n, ca, rank, cb2, ca, iters == 0, slot, ka, kb);
-            if (rc) break;
-            SP_CUDA(cudaMemcpyAsync(hdiff, slot, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-            SP_CUDA(cudaMemsetAsync(diffs + ((iters + 1) % kSlots), 0, sizeof(double), c.stream));
-            SP_CUDA(cudaStreamSynchronize(c.stream));
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ka, kb);
-            kernel_ms += ms;
-            diff = *hdiff;
-            std::swap(ca, cb2);
-        } else {
-            diff = 0.0;
-        }
-        iter = iter + 1;
-        iters++;
-        if (cb && cb(iters, user)) {
-            set_error("aborted by the fixedPoint iteration callback");
-            rc = SP_ERR_ABORTED;
-            break;
-        }
-        if (diff < epsilon || iter >= max_iter) break;  // pr.sp:10
-        if (iters >= cap) {
-            set_error("fixedPoint 'converged' did not converge within %lld iterations",
-                      (long long)cap);
-            rc = SP_ERR_NONCONV;
-            break;
-        }
-        const char *hostloop = getenv("SP_HOSTLOOP");  // ncu cannot profile conditional graphs
-        if (!cb && !exact && n && !(hostloop && hostloop[0] == '1')) {
-            // the remaining iterations on the device: contrib to read is ca
-            PrLoop *hL;
-            SP_TRY(c.host_as(&hL));
-            float ms = 0.f;
-            SP_TRY(pr_device_loop(c, plan, rank, ca, cb2, diffs, diffs + 1, iter, iters,
-                                  max_iter, cap, epsilon, hL, &ms));
-            kernel_ms += ms;
+    if (n && !exact) {
+        PrLoop *hL;
+        SP_TRY(c.host_as(&hL));
+        rc = pr_fast_run(g, c, damping, epsilon, max_iter, cap, cb, user, rank, hL, &kernel_ms);
+        if (rc == SP_OK) {
             iter = hL->iter;
             iters = hL->iters;
             diff = hL->diff;
@@ -907,12 +1447,63 @@ extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t 
                           (long long)cap);
                 rc = SP_ERR_NONCONV;
             }
-            break;
         }
+    } else {
+        // exact path (and n == 0): host loop, one diff read per iteration
+        double *ca, *cb2, *diffs;
+        SP_TRY(c.alloc(&ca, n));
+        SP_TRY(c.alloc(&cb2, n));
+        const int64_t kSlots = 1024;  // diff slots, recycled in a ring
+        SP_TRY(c.alloc(&diffs, kSlots));
+        SP_CUDA(cudaMemsetAsync(diffs, 0, kSlots * sizeof(double), c.stream));
+        double *hdiff = nullptr;
+        SP_TRY(c.host_as(&hdiff));
+        const double r0 = n ? 1.0 / (double)n : 0.0;  // pr.sp:6
+        if (n) {
+            k_init<<<grid_for(n, 256, c.device), 256, 0, c.stream>>>(rank, ca, g->outdeg, 0, n, r0);
+            c.launches++;
+        }
+        cudaEvent_t ka, kb;
+        SP_CUDA(cudaEventCreate(&ka));
+        SP_CUDA(cudaEventCreate(&kb));
+        for (;;) {
+            double *slot = diffs + (iters % kSlots);
+            if (n) {
+                rc = launch_exact(g, c, 0, n, damping, ca, rank, cb2, slot, ka, kb);
+                if (rc) break;
+                SP_CUDA(cudaMemcpyAsync(hdiff, slot, sizeof(double), cudaMemcpyDeviceToHost,
+                                        c.stream));
+                SP_CUDA(cudaMemsetAsync(diffs + ((iters + 1) % kSlots), 0, sizeof(double),
+                                        c.stream));
+                SP_CUDA(cudaStreamSynchronize(c.stream));
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, ka, kb);
+                kernel_ms += ms;
+                diff = *hdiff;
+                std::swap(ca, cb2);
+            } else {
+                diff = 0.0;
+            }
+            iter = iter + 1;
+            iters++;
+            if (cb && cb(iters, user)) {
+                set_error("aborted by the fixedPoint iteration callback");
+                rc = SP_ERR_ABORTED;
+                break;
+            }
+            if (diff < epsilon || iter >= max_iter) break;  // pr.sp:10
+            if (iters >= cap) {
+                set_error("fixedPoint 'converged' did not converge within %lld iterations",
+                          (long long)cap);
+                rc = SP_ERR_NONCONV;
+                break;
+            }
+        }
+        cudaEventDestroy(ka);
+        cudaEventDestroy(kb);
     }
-    cudaEventDestroy(ka);
-    cudaEventDestroy(kb);
-    if (rc == SP_OK && n) SP_TRY(from_device(rank_out, rank, n * 8, mem, c.stream));
+    if (rc == SP_OK && n && rank != rank_out)
+        SP_TRY(from_device(rank_out, rank, n * 8, mem, c.stream));
     SP_TRY(c.finish(st));
     if (iter_out) *iter_out = iter;
     if (diff_out) *diff_out = diff;

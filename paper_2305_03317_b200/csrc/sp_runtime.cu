@@ -2,6 +2,7 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -323,6 +324,59 @@ int launch_cached_graph(cudaGraph_t graph, const void *key, int kind, cudaStream
     }
     g_exec_cache.v.push_back(ExecEntry{key, kind, exec});
     SP_CUDA(cudaGraphLaunch(exec, stream));
+    return SP_OK;
+}
+
+uint64_t next_graph_uid() {
+    static std::atomic<uint64_t> next{1};
+    return next++;
+}
+
+struct ArgExecCache {
+    std::vector<ArgExec> v;
+    ~ArgExecCache() {
+        for (auto &e : v) {
+            if (e.exec) cudaGraphExecDestroy(e.exec);
+            if (e.args) cudaFree(e.args);
+        }
+    }
+};
+static thread_local ArgExecCache g_arg_exec;
+
+int arg_exec_get(uint64_t key, int kind, size_t bytes, int device, ArgExec **out, bool *fresh) {
+    for (auto &e : g_arg_exec.v) {
+        if (e.key == key && e.kind == kind && e.bytes == bytes && e.exec) {
+            *out = &e;
+            *fresh = false;
+            return SP_OK;
+        }
+    }
+    // another graph's entry of the same kind and layout: handed over with
+    // its executable, which the caller refreshes (cudaGraphExecUpdate)
+    for (auto &e : g_arg_exec.v) {
+        if (e.kind == kind && e.bytes == bytes && e.exec && e.device == device) {
+            e.key = key;
+            *out = &e;
+            *fresh = true;
+            return SP_OK;
+        }
+    }
+    if (g_arg_exec.v.size() >= 16) {  // bounded: drop the oldest (calls are synchronous)
+        ArgExec &o = g_arg_exec.v.front();
+        if (o.exec) cudaGraphExecDestroy(o.exec);
+        if (o.args) cudaFree(o.args);
+        g_arg_exec.v.erase(g_arg_exec.v.begin());
+    }
+    ArgExec e;
+    e.device = device;
+    e.key = key;
+    e.kind = kind;
+    e.bytes = bytes;
+    SP_CUDA(cudaSetDevice(device));
+    SP_CUDA(cudaMalloc(&e.args, bytes));
+    g_arg_exec.v.push_back(e);
+    *out = &g_arg_exec.v.back();
+    *fresh = true;
     return SP_OK;
 }
 

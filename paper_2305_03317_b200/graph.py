@@ -189,11 +189,18 @@ def _new_handle(fn, *args, what: str) -> C.c_void_p:
 
 
 def _as_i32(a, what: str) -> np.ndarray:
+    """int32 copy/view of an integer array; values outside int32 and
+    non-integral values are rejected (never truncated or wrapped)."""
     a = np.asarray(a)
     if a.dtype == np.int32:  # already in range: no O(m) host scan
         return np.ascontiguousarray(a)
-    if a.size and a.dtype.kind in "iu":
-        lo, hi = int(a.min()), int(a.max())
+    if a.size and a.dtype.kind == "f":
+        if not np.all(np.isfinite(a)) or not np.all(a == np.floor(a)):
+            raise ArgError(f"{what} must be integers (got non-integral {a.dtype} values)")
+    elif a.size and a.dtype.kind not in "iub":
+        raise ArgError(f"{what} must be integers (got dtype {a.dtype})")
+    if a.size and a.dtype.kind in "iuf":
+        lo, hi = a.min(), a.max()
         if lo < _I32_MIN or hi > _I32_MAX:
             raise ArgError(f"{what} outside the int32 range [{lo}, {hi}] "
                            "(unsupported by the B200 backend)")
@@ -330,6 +337,15 @@ def from_csr(offsets, adj, weights=None, directed: bool = True,
     adj = _as_i32(adj, "vertex id")
     w = None if weights is None else _as_i32(weights, "edge weight")
     n = len(off) - 1
+    # O(1) shape checks here; row monotonicity and 0 <= adj < n are checked
+    # on the device before any kernel indexes by them (sp_graph_from_csr)
+    if n < 0:
+        raise ArgError("offsets must hold n + 1 >= 1 entries")
+    if int(off[0]) != 0 or int(off[-1]) != len(adj):
+        raise ArgError(f"offsets must start at 0 and end at len(adj) = {len(adj)} "
+                       f"(got {int(off[0])} .. {int(off[-1])})")
+    if w is not None and len(w) != len(adj):
+        raise ArgError(f"weights ({len(w)}) and adj ({len(adj)}) differ in length")
     _lib.require_device(device)
     h = _new_handle(_lib.lib().sp_graph_from_csr, _ptr(off), _ptr(adj),
                     None if w is None else _ptr(w), n, len(adj), int(bool(directed)),
@@ -357,13 +373,19 @@ _adopted: dict[int, tuple] = {}
 _adopt_lock = threading.Lock()
 
 
-def device_graph(g, device: int = 0) -> CsrGraph:
-    """The device-resident form of ``g``: ``g`` itself for a CsrGraph of this
-    package, else a one-time upload of a reference ``trident`` CsrGraph
-    (cached while the source object lives)."""
+def device_graph(g, device: int | None = None) -> CsrGraph:
+    """The device-resident form of ``g`` on ``device``: ``g`` itself for a
+    CsrGraph of this package on that device (a graph on another device is
+    an error: its arrays live in that GPU's memory), else a one-time upload
+    of a reference ``trident`` CsrGraph, cached per (object, device) while
+    the source object lives."""
     if isinstance(g, CsrGraph):
+        if device is not None and g.device != device:
+            raise ArgError(f"graph lives on cuda:{g.device}, not cuda:{device}")
         return g
-    key = id(g)
+    if device is None:
+        device = 0
+    key = (id(g), device)
     with _adopt_lock:
         ent = _adopted.get(key)
         if ent is not None and ent[0]() is g:
@@ -383,40 +405,46 @@ def device_graph(g, device: int = 0) -> CsrGraph:
 # utilities of trident/graph.py that are not on the device path
 
 
-def assign_random_weights(g: CsrGraph, lo: int, hi: int, seed: int) -> CsrGraph:
-    """i.i.d. uniform integer weights in [lo, hi] from Python's Mersenne
-    Twister seeded with ``seed`` (graph.py:154-190): per slot when directed;
-    per canonical (u <= v) slot when undirected, mirrored onto the matching
-    reverse copy by position.  Returns a new device graph."""
+def random_weights(offsets, adj, directed: bool, lo: int, hi: int, seed: int) -> np.ndarray:
+    """The weight array ``assign_random_weights`` gives a CSR (host only):
+    Python's Mersenne Twister seeded with ``seed``, ``randint(lo, hi)`` per
+    slot in slot order when directed (graph.py:163-167); when undirected one
+    draw per canonical (u <= v) slot in CSR order, mirrored onto the k-th
+    reverse copy of the same pair by position (graph.py:168-187)."""
     if lo > hi:
         raise RangeError(f"lo ({lo}) exceeds hi ({hi})")
     rng = random.Random(seed)
-    off = g.offsets.tolist()
-    adj = g.adj.tolist()
-    w = list(g.weights.tolist())
-    if g.directed:
-        for e in range(g.m):
-            w[e] = rng.randint(lo, hi)
-    else:
-        pending: dict[tuple[int, int], list[int]] = {}
-        for x in range(g.n):
-            for e in range(off[x], off[x + 1]):
-                y = adj[e]
-                if x <= y:
-                    val = rng.randint(lo, hi)
-                    w[e] = val
-                    if x != y:
-                        pending.setdefault((y, x), []).append(val)
-        seen: dict[tuple[int, int], int] = {}
-        for x in range(g.n):
-            for e in range(off[x], off[x + 1]):
-                y = adj[e]
-                if x > y:
-                    k = seen.get((x, y), 0)
-                    seen[(x, y)] = k + 1
-                    w[e] = pending[(x, y)][k]
-    return from_csr(g.offsets, g.adj, np.asarray(w, dtype=np.int64),
-                    directed=g.directed, device=g.device)
+    off = np.asarray(offsets).tolist()
+    adj = np.asarray(adj).tolist()
+    m = len(adj)
+    if directed:
+        return np.fromiter((rng.randint(lo, hi) for _ in range(m)), dtype=np.int64, count=m)
+    w = [0] * m
+    pending: dict[tuple[int, int], list[int]] = {}
+    for x in range(len(off) - 1):
+        for e in range(off[x], off[x + 1]):
+            y = adj[e]
+            if x <= y:
+                val = rng.randint(lo, hi)
+                w[e] = val
+                if x != y:
+                    pending.setdefault((y, x), []).append(val)
+    seen: dict[tuple[int, int], int] = {}
+    for x in range(len(off) - 1):
+        for e in range(off[x], off[x + 1]):
+            y = adj[e]
+            if x > y:
+                k = seen.get((x, y), 0)
+                seen[(x, y)] = k + 1
+                w[e] = pending[(x, y)][k]
+    return np.asarray(w, dtype=np.int64)
+
+
+def assign_random_weights(g: CsrGraph, lo: int, hi: int, seed: int) -> CsrGraph:
+    """i.i.d. uniform integer weights in [lo, hi] (graph.py:154-190; see
+    ``random_weights`` for the draw order).  Returns a new device graph."""
+    w = random_weights(g.offsets, g.adj, g.directed, lo, hi, seed)
+    return from_csr(g.offsets, g.adj, w, directed=g.directed, device=g.device)
 
 
 @dataclass(frozen=True)

@@ -8,7 +8,8 @@ follow trident/interp.py:
 The program is identified (corpus.identify), the arguments are checked and
 coerced exactly like check_args (interp.py:91-129), and the work runs on the
 GPU through libstarplat_b200.so.  Property arrays come back as NumPy arrays
-(same values as the reference's lists; ``.tolist()`` gives the lists).
+(same values as the reference's lists), or as the reference's Python lists
+with ``as_lists=True``.
 
 Differences, all documented in DESIGN.md:
   * SSSP's fixedPoint iteration count comes from the parallel frontier order,
@@ -186,12 +187,19 @@ def _ptr(buf):
 
 def run(tp, g, args: dict, function: str | None = None,
         max_iters: int | None = None, on_fixedpoint_iteration=None, *,
-        deterministic: bool = False, device_outputs: bool = False) -> RunResult:
+        deterministic: bool = False, device_outputs: bool = False,
+        as_lists: bool = False) -> RunResult:
     """Run a corpus program on the GPU.  ``tp`` is a reference TypedProgram
     (recognised structurally), a ``corpus.Program`` or a corpus key.
 
     ``device_outputs=True`` leaves the property arrays in HBM (torch CUDA
-    tensors on the graph's device) instead of copying them to NumPy."""
+    tensors on the graph's device) instead of copying them to NumPy.
+    ``as_lists=True`` returns every node property as a Python list of
+    Python ints / floats / bools, exactly the reference's ``final_env``
+    layout (interp.py:259-266), for callers that compare with ``==``,
+    mutate or JSON-serialise the lists."""
+    if as_lists and device_outputs:
+        raise ValueError("as_lists and device_outputs are mutually exclusive")
     E = errors_for(tp)
     prog = corpus.identify(tp, function)
     dg = device_graph(g)
@@ -261,6 +269,8 @@ def run(tp, g, args: dict, function: str | None = None,
         env.scalars = {"triangle_count": int(cnt.value)}
     else:  # pragma: no cover
         raise E.ExecError(f"unhandled program {prog.key}")
+    if as_lists:
+        env.node_props = {k: np.asarray(a).tolist() for k, a in env.node_props.items()}
     wall = time.perf_counter() - t0
     return RunResult(env=env, fixedpoint_iterations=fpi, wall_seconds=wall,
                      return_value=None, stats=st.as_dict())

@@ -1,7 +1,7 @@
 """Parity at the BASELINE configs' full sizes.
 
 The CPU oracle (oracle/cpu_ref.c, pinned bit-exact to the reference) runs
-the full-size PR / SSSP / BC (sampled sources) / TC configs here, fed with
+the full-size PR / SSSP / BC (all 256 sources) / TC configs here, fed with
 the device graph's CSR arrays (the CSR builder itself is pinned against the
 reference on the golden cases and by the device-vs-host generator tests).
 Where the oracle would take too long (SSSP on the 4096x4096 grid, ~10^4
@@ -53,6 +53,19 @@ def test_pr_cfg2_full(rmat22):
     r2 = sp.run(corpus.PR, g, PR_ARGS)
     assert r2.env.node_props["rank"].tobytes() == r.env.node_props["rank"].tobytes()
     assert r2.env.scalars["iter"] == it
+    # the relabelled layout (forced here; by default it is used where the
+    # contrib array outgrows the L2, e.g. RMAT-24) sums each row in another
+    # association order: within 1e-12, same iteration count
+    os.environ["SP_PR_REL"] = "1"
+    try:
+        g2 = sp.generate("rmat", 22, 16, seed=1)
+        for _ in range(3):
+            r3 = sp.run(corpus.PR, g2, PR_ARGS)
+            assert r3.env.scalars["iter"] == it
+            assert np.abs(r3.env.node_props["rank"] - rank).max() / np.abs(rank).max() <= 1e-12
+        g2.close()
+    finally:
+        del os.environ["SP_PR_REL"]
     rd = sp.run(corpus.PR, g, PR_ARGS, deterministic=True)
     assert rd.env.node_props["rank"].tobytes() == rank.tobytes()
     assert rd.env.scalars["iter"] == it and rd.env.scalars["diff"] == diff
@@ -66,20 +79,25 @@ def test_sssp_rmat22_full(rmat22):
                                   dist)
 
 
-def test_bc_cfg4_full_sampled_sources():
-    """BASELINE cfg4 graph (symmetrized RMAT-20) with 6 of the 256 sources."""
+def test_bc_cfg4_full_256_sources():
+    """BASELINE cfg4 as benchmarked: symmetrized RMAT-20 with all 256 sampled
+    sources (the bench's own sample).  Fast mode within 1e-12 relative with
+    sigma exact; deterministic mode bit-exact bc/sigma/delta."""
     g = sp.generate("rmat", 20, 16, seed=1, undirected=True)
     o = _oracle_csr(g)
     deg = np.diff(o.off)
     srcs = np.random.default_rng(1).choice(np.flatnonzero(deg > 0), size=256,
-                                           replace=False)[:6].tolist()
+                                           replace=False).tolist()
     bc, sg, dl = cpu_ref.bc(o, srcs, nthreads=NT)
     r = sp.run(corpus.BC, g, {"sourceSet": srcs})
     rel = np.abs(r.env.node_props["bc"] - bc).max() / np.abs(bc).max()
     assert rel <= 1e-12
     np.testing.assert_array_equal(r.env.node_props["sigma"], sg)  # exact path counts
+    rel = np.abs(r.env.node_props["delta"] - dl).max() / max(np.abs(dl).max(), 1e-300)
+    assert rel <= 1e-12
     rd = sp.run(corpus.BC, g, {"sourceSet": srcs}, deterministic=True)
     assert rd.env.node_props["bc"].tobytes() == bc.tobytes()
+    assert rd.env.node_props["sigma"].tobytes() == sg.tobytes()
     assert rd.env.node_props["delta"].tobytes() == dl.tobytes()
     g.close()
 
@@ -118,3 +136,95 @@ def test_sssp_pull_rmat22_full(rmat22):
     dist, _, rc = cpu_ref.sssp(o, 0)
     np.testing.assert_array_equal(
         sp.run(corpus.SSSP_PULL, g, {"src": 0}).env.node_props["dist"], dist)
+
+
+def test_pr_grid_cfg5a_full():
+    """BASELINE cfg5a PR on the 4096x4096 grid against the oracle (fast mode
+    <= 1e-12 with the same iteration count; deterministic bit-exact)."""
+    g = sp.generate("grid", 4096, 4096, seed=1)
+    o = cpu_ref.Csr(g.n, g.m, False, np.asarray(g.offsets), None, None,
+                    np.asarray(g.rev_offsets), np.asarray(g.rev_adj), None, None)
+    rank, it, diff, _, rc = cpu_ref.pagerank(o, nthreads=NT)
+    assert rc == 0
+    r = sp.run(corpus.PR, g, PR_ARGS)
+    assert r.env.scalars["iter"] == it
+    assert np.abs(r.env.node_props["rank"] - rank).max() / np.abs(rank).max() <= 1e-12
+    rd = sp.run(corpus.PR, g, PR_ARGS, deterministic=True)
+    assert rd.env.node_props["rank"].tobytes() == rank.tobytes()
+    assert rd.env.scalars["iter"] == it and rd.env.scalars["diff"] == diff
+    g.close()
+
+
+# ---- the north-star target graph: RMAT-24 on one B200 (SURVEY 8d "Target")
+
+
+@pytest.fixture(scope="module")
+def rmat24():
+    g = sp.generate("rmat", 24, 16, seed=1)
+    yield g, _oracle_csr(g)
+    g.close()
+
+
+def test_pr_rmat24_full(rmat24):
+    """PR on RMAT-24 (the bench's pr_rmat24 line): fast mode <= 1e-12 with the
+    oracle's iteration count, twice (the second call uses the hot-source
+    set); deterministic mode bit-exact."""
+    g, o = rmat24
+    rank, it, diff, _, rc = cpu_ref.pagerank(o, nthreads=NT)
+    assert rc == 0
+    for _ in range(2):
+        r = sp.run(corpus.PR, g, PR_ARGS)
+        assert r.env.scalars["iter"] == it
+        assert np.abs(r.env.node_props["rank"] - rank).max() / np.abs(rank).max() <= 1e-12
+    rd = sp.run(corpus.PR, g, PR_ARGS, deterministic=True)
+    assert rd.env.node_props["rank"].tobytes() == rank.tobytes()
+    assert rd.env.scalars["iter"] == it and rd.env.scalars["diff"] == diff
+
+
+def test_sssp_rmat24_full(rmat24):
+    """SSSP on RMAT-24 (the bench's sssp_rmat24 line), push program and the
+    pull-form program: dist bit-exact."""
+    g, o = rmat24
+    dist, _, rc = cpu_ref.sssp(o, 0)
+    assert rc == 0
+    np.testing.assert_array_equal(sp.run(corpus.SSSP, g, {"src": 0}).env.node_props["dist"],
+                                  dist)
+    np.testing.assert_array_equal(
+        sp.run(corpus.SSSP_PULL, g, {"src": 0}).env.node_props["dist"], dist)
+
+
+def test_tc_rmat24_sym_full():
+    """TC on symmetrized RMAT-24 (the bench's tc_rmat24 line): exact count."""
+    g = sp.generate("rmat", 24, 16, seed=1, undirected=True)
+    o = cpu_ref.Csr(g.n, g.m, False, np.asarray(g.offsets), np.asarray(g.adj), None, None,
+                    None, None, None)
+    t = sp.run(corpus.TC, g, {}).env.scalars["triangle_count"]
+    assert t == cpu_ref.tc(o, nthreads=NT)
+    g.close()
+
+
+# ---- cfg5b: RMAT scale-26 (67 M vertices, ~1 G slots), resident on one B200
+
+
+def test_rmat26_cfg5b_pr_sssp():
+    """BASELINE cfg5b graph at N=1: PR (fast <= 1e-12, same iteration count)
+    and SSSP from 0 (bit-exact) against the oracle.  The host copies are
+    fetched one program at a time to bound host memory (~9 GB at peak)."""
+    g = sp.generate("rmat", 26, 16, seed=1)
+    assert g.m > (1 << 29)
+    r = sp.run(corpus.PR, g, PR_ARGS)
+    o = cpu_ref.Csr(g.n, g.m, True, np.asarray(g.offsets), None, None,
+                    np.asarray(g.rev_offsets), np.asarray(g.rev_adj), None, None)
+    rank, it, _, _, rc = cpu_ref.pagerank(o, nthreads=NT)
+    assert rc == 0
+    assert r.env.scalars["iter"] == it
+    assert np.abs(r.env.node_props["rank"] - rank).max() / np.abs(rank).max() <= 1e-12
+    del o, rank, r
+    g._cache.clear()
+    d = sp.run(corpus.SSSP, g, {"src": 0}).env.node_props["dist"]
+    o = cpu_ref.Csr(g.n, g.m, True, np.asarray(g.offsets), np.asarray(g.adj), None, None,
+                    None, None, np.asarray(g.effective_weights))
+    dist, _, rc = cpu_ref.sssp(o, 0)
+    assert rc == 0
+    np.testing.assert_array_equal(d, dist)
+    g.close()

@@ -726,3 +726,85 @@ def test_neighbor_sum_generic(directed, reverse):
     np.add.at(want, rows, prop[col])
     np.testing.assert_array_equal(per, want)
     assert tot.value == int(want.sum())
+
+
+@pytest.mark.parametrize("case", ["multi300_u_7", "multi300_d_0", "rmat9_u_123"])
+def test_assign_random_weights_device_graph(case):
+    """assign_random_weights on a device graph gives the weights the
+    reference assigned (tests/golden/weights, made by the reference) and a
+    graph whose w_eff/SSSP follow them."""
+    import os
+    from conftest import REPO
+    z = np.load(os.path.join(REPO, "tests", "golden", "weights", case + ".npz"))
+    g = sp.from_csr(z["off"], z["adj"], None, directed=bool(z["directed"]))
+    g2 = sp.assign_random_weights(g, int(z["lo"]), int(z["hi"]), int(z["seed"]))
+    np.testing.assert_array_equal(g2.weights, z["w"])
+    np.testing.assert_array_equal(g2.adj, z["adj"])
+    o = cpu_ref.Csr(g2.n, g2.m, g2.directed, np.asarray(g2.offsets), np.asarray(g2.adj),
+                    np.asarray(g2.weights), None, None, None, None)
+    weff = np.zeros(g2.m, np.int32)
+    cpu_ref.lib().cr_weff(g2.n, cpu_ref._ptr(o.off), cpu_ref._ptr(o.adj),
+                          cpu_ref._ptr(np.ascontiguousarray(o.w)), cpu_ref._ptr(weff))
+    np.testing.assert_array_equal(g2.effective_weights, weff)
+
+
+@pytest.mark.parametrize("case", ["fx_rand200_a_u", "fx_k5_d", "fx_grid5x5_u"])
+def test_as_lists_matches_reference_layout(case, graphs):
+    """as_lists=True: node props are Python lists of Python scalars equal
+    (==) to the reference's final_env lists (interp.py:259-266)."""
+    z, g = graphs(case)
+    r = sp.run(corpus.SSSP, g, {"src": int(z["sssp_srcs"][0])}, as_lists=True)
+    d = r.env.node_props["dist"]
+    assert isinstance(d, list) and all(type(x) is int for x in d)
+    assert d == z["sssp_dist"][0].tolist()
+    assert r.env.node_props["modified"] == [False] * g.n
+    r = sp.run(corpus.PR, g, PR_ARGS, deterministic=True, as_lists=True)
+    assert r.env.node_props["rank"] == z["pr_rank"].tolist()
+    assert r.env.node_props["rank_nxt"] == z["pr_rank_nxt"].tolist()
+    assert all(type(x) is float for x in r.env.node_props["rank"])
+    r = sp.run(corpus.BC, g, {"sourceSet": z["bc_srcs"].tolist()}, deterministic=True,
+               as_lists=True)
+    assert r.env.node_props["bc"] == z["bc"].tolist()
+    with pytest.raises(ValueError):
+        sp.run(corpus.PR, g, PR_ARGS, as_lists=True, device_outputs=True)
+
+
+def test_from_csr_rejects_bad_input():
+    """from_csr validates its input before any kernel indexes by it."""
+    from paper_2305_03317_b200.errors import ArgError
+    off = np.array([0, 2, 3, 3], np.int64)
+    adj = np.array([1, 2, 0], np.int32)
+    g = sp.from_csr(off, adj, None, directed=True)
+    assert g.m == 3
+    with pytest.raises(ArgError):  # weights shorter than adj
+        sp.from_csr(off, adj, np.array([1, 2], np.int32))
+    with pytest.raises(ArgError):  # last offset != len(adj)
+        sp.from_csr(np.array([0, 2, 3, 4], np.int64), adj)
+    with pytest.raises(ArgError):  # rows not monotone (device check)
+        sp.from_csr(np.array([0, 3, 1, 3], np.int64), adj)
+    with pytest.raises(ArgError):  # id out of range (device check)
+        sp.from_csr(off, np.array([1, 7, 0], np.int32))
+    with pytest.raises(ArgError):
+        sp.from_csr(off, np.array([1, -1, 0], np.int32), directed=False)
+    with pytest.raises(ArgError):  # float weights are not truncated
+        sp.from_csr(off, adj, np.array([1.5, 2.0, 3.0]))
+
+
+def test_from_csr_rejects_bad_ids_pipelined():
+    """The large-graph upload path (reverse CSR built while the adjacency
+    crosses PCIe) flags an out-of-range id without writing out of bounds."""
+    from paper_2305_03317_b200.errors import ArgError
+    rng = np.random.default_rng(5)
+    n, m = 1 << 16, 1 << 23
+    adj = np.sort(rng.integers(0, n, m, dtype=np.int32).reshape(n, -1), axis=1).ravel()
+    off = np.arange(0, m + 1, m // n, dtype=np.int64)
+    g = sp.from_csr(off, adj, None, directed=True)
+    assert g.m == m
+    g.close()
+    bad = adj.copy()
+    bad[m // 2] = n + 5
+    with pytest.raises(ArgError):
+        sp.from_csr(off, bad, None, directed=True)
+    bad[m // 2] = -3
+    with pytest.raises(ArgError):
+        sp.from_csr(off, bad, None, directed=True)

@@ -307,3 +307,24 @@ def test_generators_deterministic_and_clean():
 
 def test_rmat_thresholds():
     assert gen.rmat_thresholds() == (37356, 37356 + 12452, 37356 + 2 * 12452)
+
+
+WEIGHT_CASES = sorted(f[:-4] for f in os.listdir(os.path.join(REPO, "tests", "golden", "weights"))
+                      if f.endswith(".npz"))
+
+
+@pytest.mark.parametrize("case", WEIGHT_CASES)
+def test_random_weights_match_reference_golden(case):
+    """assign_random_weights' draw order (graph.py:154-190) against weights
+    the reference itself assigned (tests/golden/make_weights_golden.py):
+    directed per slot; undirected per canonical slot, mirrored by position
+    onto parallel copies; self-loops drawn once."""
+    z = np.load(os.path.join(REPO, "tests", "golden", "weights", case + ".npz"))
+    w = spg.random_weights(z["off"], z["adj"], bool(z["directed"]), int(z["lo"]), int(z["hi"]),
+                           int(z["seed"]))
+    np.testing.assert_array_equal(w, z["w"])
+
+
+def test_random_weights_range_error():
+    with pytest.raises(spg.RangeError):
+        spg.random_weights(np.zeros(1, np.int64), np.zeros(0, np.int32), True, 5, 1, 0)
