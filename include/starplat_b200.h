@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 2
+#define SP_ABI_VERSION 3
 
 enum sp_status {
     SP_OK = 0,
@@ -146,17 +146,34 @@ int sp_sssp(sp_graph *g, int32_t src, int64_t cap, int32_t *dist, int mem,
 int sp_sssp_pull(sp_graph *g, int32_t src, int64_t cap, int32_t *dist, int mem,
                  int64_t *iters, sp_iter_cb cb, void *user, sp_stats *st);
 
-/* Block-partitioned SSSP supersteps (multi-GPU; graph.py:226-249 ownership,
- * the exchange is the caller's all-reduce(min) of dist between steps; this
- * replaces the BSP model of bsp.py:393-417 with convergence evaluated after
- * the exchange).  dist[n] and last[n] are device arrays,
- * replicated on every rank.  A step takes F = {v in [v0, v1): dist[v] <
- * last[v]}, sets last[v] = dist[v] on F and relaxes F's rows into dist
- * (atomicMin, any destination); *frontier = |F|, *relaxed = slots scanned.
- * The run has converged when a step's summed |F| over all ranks is 0. */
-int sp_sssp_block_init(sp_graph *g, int32_t src, int32_t *dist, int32_t *last);
-int sp_sssp_block_step(sp_graph *g, int64_t v0, int64_t v1, int32_t *dist,
-                       int32_t *last, int64_t *frontier, int64_t *relaxed);
+/* Owner-computes SSSP shards for multi-GPU runs (graph.py:226-249 block
+ * ownership; replaces the BSP superstep of bsp.py:290-335,393-417 for
+ * sssp.sp, with convergence evaluated after the exchange).
+ * A shard owns dist[v] for v in [v0, v1) of the caller's device array
+ * dist (>= n entries, updated in place; the other entries are this rank's
+ * candidates for remote vertices).  Per superstep:
+ *   sp_sssp_shard_relax: up to max_rounds passes over the owned frontier
+ *     (max_rounds > 1: the reference's local fixpoint, bsp.py:297-306);
+ *     owned winners form the next local frontier, remote winners are sent
+ *     as ONE message per vertex with the local minimum (aggregate_messages,
+ *     bsp.py:45-72): send[] (device, capacity n) receives packed
+ *     (vid << 32 | uint32 dist) grouped by owner rank (owner = vid / per),
+ *     counts[world] (host) the group sizes.  info[4] (host, may be NULL):
+ *     owned vertices lowered (Min wins, deduped per pass), slots relaxed,
+ *     rounds run, owned frontier left.  SP_ERR_OVERFLOW: a distance left the int32 range.
+ *   sp_sssp_shard_apply: the owner's strict min of received messages
+ *     (bsp.py:350-368) -- msgs[k] packed as above -- or, when block != NULL,
+ *     of block[v - v0] (a MIN reduce-scatter of every rank's dist array);
+ *     *frontier = the owned frontier of the next superstep.  The run has
+ *     converged when the frontiers of all ranks are empty. */
+typedef struct sp_sssp_shard sp_sssp_shard;
+int sp_sssp_shard_create(sp_graph *g, int64_t v0, int64_t v1, int32_t src, int world,
+                         int32_t *dist, sp_sssp_shard **out);
+int sp_sssp_shard_relax(sp_sssp_shard *h, int64_t max_rounds, int64_t per,
+                        int64_t *send, int64_t *counts, int64_t *info);
+int sp_sssp_shard_apply(sp_sssp_shard *h, const int64_t *msgs, int64_t k,
+                        const int32_t *block, int64_t *frontier);
+void sp_sssp_shard_destroy(sp_sssp_shard *h);
 
 /* corpus/programs/pr.sp.  rank[n] = final ranks (== rank_nxt at exit);
  * iter / diff = the program's scalars; iters = fixedPoint iterations. */

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libstarplat_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "starplat_b200.h")
 
-ABI_VERSION = 2  # must equal SP_ABI_VERSION in include/starplat_b200.h
+ABI_VERSION = 3  # must equal SP_ABI_VERSION in include/starplat_b200.h
 
 SP_OK = 0
 SP_ERR_ARG = -1
@@ -75,8 +75,10 @@ SIGNATURES = {
     "sp_graph_destroy": (None, [_p]),
     "sp_sssp": (_int, [_p, _i32, _i64, _p, _int, _p, ITER_CB, _p, _p]),
     "sp_sssp_pull": (_int, [_p, _i32, _i64, _p, _int, _p, ITER_CB, _p, _p]),
-    "sp_sssp_block_init": (_int, [_p, _i32, _p, _p]),
-    "sp_sssp_block_step": (_int, [_p, _i64, _i64, _p, _p, _p, _p]),
+    "sp_sssp_shard_create": (_int, [_p, _i64, _i64, _i32, _int, _p, _p]),
+    "sp_sssp_shard_relax": (_int, [_p, _i64, _i64, _p, _p, _p]),
+    "sp_sssp_shard_apply": (_int, [_p, _p, _i64, _p, _p]),
+    "sp_sssp_shard_destroy": (None, [_p]),
     "sp_pagerank": (_int, [_p, _d, _d, _i64, _i64, _u, _p, _int, _p, _p, _p,
                            ITER_CB, _p, _p]),
     "sp_pagerank_block_step": (_int, [_p, _i64, _i64, _d, _p, _p, _p, _p, _u, _p]),

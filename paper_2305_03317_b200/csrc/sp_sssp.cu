@@ -26,6 +26,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "sp_expand.cuh"
 
@@ -1329,114 +1330,311 @@ extern "C" int sp_sssp_pull(sp_graph *g, int32_t src, int64_t cap, int32_t *dist
     return sssp_impl(g, src, cap, dist_out, mem, iters_out, cb, user, st, true);
 }
 
-// ---- block-partitioned supersteps (multi-GPU, graph.py:226-249 ownership)
+// ---- owner-computes shards (multi-GPU, graph.py:226-249 ownership) -------
+// One shard per rank owns dist[v] for v in [v0, v1).  A superstep relaxes
+// the owned frontier (one pass, or local passes to a fixpoint: bsp.py:290-306
+// repeat_local) with atomicMin into the rank's dist array; owned winners form
+// the next local frontier, remote winners are collected once per superstep
+// (stamp-deduped) and sent as ONE aggregated (vertex, local minimum) message
+// per vertex -- the reference's aggregate_messages (bsp.py:45-72) and the
+// paper's "single message with local minimum value".  The owner applies the
+// messages it receives with a strict min (bsp.py:350-368) and appends the
+// winners to its frontier.  Messages are packed (vid << 32 | uint32 dist),
+// grouped by owner rank for an all-to-all; or, for dense supersteps, the
+// caller reduce-scatters the whole dist array with MIN and applies its block.
 namespace {
 
-// Relaxation without a next-frontier queue: ownership decides the frontier
-// after the exchange (k_block_frontier), not the relaxing rank.
-struct RelaxNoPushOp {
+// Relaxation of sssp.sp:11-12 for a shard: owned winners -> next local
+// frontier (1), remote winners -> outbox (2, once per superstep).
+struct RelaxShardOp {
     using Payload = int;
     using Probe = RelaxOp::Probe;
+    static constexpr bool kFar = true;
     int32_t *__restrict__ dist;
+    int32_t *__restrict__ enq;
     const int32_t *__restrict__ weff;
     unsigned long long *overflow;
+    int32_t *far_q;               // outbox vertex ids
+    unsigned long long *far_n;
+    unsigned long long far_cap;
+    int64_t v0, v1;
+    int it;      // round stamp (owned vertices)
+    int sstamp;  // superstep stamp (remote vertices)
     __device__ __forceinline__ int payload(int32_t v) const { return __ldcg(dist + v); }
     __device__ __forceinline__ Probe probe(int64_t e, int32_t x) const {
-        return Probe{__ldg(weff + e), __ldcg(dist + x)};
+        return Probe{__ldcs(weff + e), __ldcg(dist + x)};
     }
-    __device__ __forceinline__ bool apply(int dv, int64_t, int32_t x, Probe p) const {
+    __device__ __forceinline__ int apply(int dv, int64_t, int32_t x, Probe p) const {
         const int64_t cand = (int64_t)dv + (int64_t)p.w;
-        if (cand >= (int64_t)kIntMax) return false;
+        if (cand >= (int64_t)kIntMax) return 0;  // F12
         if (cand < (int64_t)(-2147483647 - 1)) {
             atomicAdd(overflow, 1ull);
-            return false;
+            return 0;
         }
-        if ((int)cand < p.dx) atomicMin(dist + x, (int)cand);
-        return false;
+        const int c = (int)cand;
+        if (c >= p.dx) return 0;
+        const int old = atomicMin(dist + x, c);
+        if (c >= old) return 0;
+        if (x >= v0 && x < v1) return atomicExch(enq + x, it) != it ? 1 : 0;
+        return atomicExch(enq + x, sstamp) != sstamp ? 2 : 0;
     }
 };
 
-// F = {v in [v0, v1): dist[v] < last[v]}; last[v] = dist[v] for v in F.
-__global__ void k_block_frontier(const int32_t *__restrict__ dist, int32_t *__restrict__ last,
-                                 int64_t v0, int64_t v1, int32_t *q, unsigned long long *cnt) {
-    for (int64_t b = v0 + blockIdx.x * (int64_t)blockDim.x; b < v1;
-         b += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = b + threadIdx.x;
-        int32_t d = 0;
-        bool in = false;
-        if (v < v1) {
-            d = dist[v];
-            in = d < last[v];
-        }
-        const int64_t slot = warp_append(in, cnt);
-        if (in) {
-            q[slot] = (int32_t)v;
-            last[v] = d;
-        }
-    }
-}
-
-__global__ void k_block_init(int32_t *dist, int32_t *last, int64_t n, int32_t src) {
+__global__ void k_shard_init(int32_t *dist, int32_t *enq, int64_t n, int32_t src) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
          x += (int64_t)gridDim.x * blockDim.x) {
         dist[x] = x == src ? 0 : kIntMax;
-        last[x] = kIntMax;
+        enq[x] = -1;
+    }
+}
+
+// Outbox -> per-owner counts (block partition: owner = v / per).
+__global__ void k_shard_count(const int32_t *__restrict__ ob, int64_t k, int64_t per, int world,
+                              unsigned long long *counts) {
+    extern __shared__ unsigned long long s_cnt[];
+    for (int r = threadIdx.x; r < world; r += blockDim.x) s_cnt[r] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&s_cnt[ob[i] / per], 1ull);
+    __syncthreads();
+    for (int r = threadIdx.x; r < world; r += blockDim.x)
+        if (s_cnt[r]) atomicAdd(&counts[r], s_cnt[r]);
+}
+
+// Packed messages grouped by owner: cursor[r] starts at the owner's offset.
+__global__ void k_shard_pack(const int32_t *__restrict__ ob, int64_t k, int64_t per,
+                             const int32_t *__restrict__ dist, unsigned long long *cursor,
+                             int64_t *send) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t x = ob[i];
+        const unsigned long long at = atomicAdd(&cursor[x / per], 1ull);
+        send[at] = ((int64_t)x << 32) | (int64_t)(uint32_t)__ldcg(dist + x);
+    }
+}
+
+// Owner apply of received messages (strict min, bsp.py:350-368); winners
+// join the local frontier (deduped with the apply stamp).
+__global__ void k_shard_apply(const int64_t *__restrict__ msg, int64_t k, int32_t *dist,
+                              int32_t *enq, int stamp, int32_t *q, unsigned long long *nq) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < k; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = b + threadIdx.x;
+        bool win = false;
+        int32_t x = 0;
+        if (i < k) {
+            const int64_t m = msg[i];
+            x = (int32_t)(m >> 32);
+            const int32_t c = (int32_t)(uint32_t)(m & 0xffffffffll);
+            win = c < __ldcg(dist + x) && c < atomicMin(dist + x, c) &&
+                  atomicExch(enq + x, stamp) != stamp;
+        }
+        const int64_t at = warp_append(win, nq);
+        if (win) q[at] = x;
+    }
+}
+
+// Dense form: block[v - v0] = min over the ranks' dist[v] (reduce-scatter).
+__global__ void k_shard_apply_dense(const int32_t *__restrict__ blk, int64_t v0, int64_t v1,
+                                    int32_t *dist, int32_t *enq, int stamp, int32_t *q,
+                                    unsigned long long *nq) {
+    for (int64_t b = v0 + blockIdx.x * (int64_t)blockDim.x; b < v1;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = b + threadIdx.x;
+        bool win = false;
+        if (v < v1) {
+            const int32_t c = blk[v - v0];
+            if (c < dist[v]) {
+                dist[v] = c;  // owned: only this rank writes it
+                win = atomicExch(enq + v, stamp) != stamp;
+            }
+        }
+        const int64_t at = warp_append(win, nq);
+        if (win) q[at] = (int32_t)v;
     }
 }
 
 }  // namespace
 
-extern "C" int sp_sssp_block_init(sp_graph *g, int32_t src, int32_t *dist, int32_t *last) {
-    SP_CHECK(g && dist && last, SP_ERR_ARG, "sp_sssp_block_init: bad arguments");
-    SP_CHECK(src >= 0 && src < g->n, SP_ERR_ARG, "node argument 'src'=%d out of range", src);
-    Call c;
-    SP_TRY(c.begin(g->device));
-    SP_TRY(ensure_weff(g, c));
-    k_block_init<<<grid_for(g->n, kBlock, c.device), kBlock, 0, c.stream>>>(dist, last, g->n, src);
-    c.launches++;
-    SP_CUDA(cudaGetLastError());
-    return c.finish(nullptr);
+struct sp_sssp_shard {
+    sp_graph *g = nullptr;
+    int64_t v0 = 0, v1 = 0;
+    int32_t *dist = nullptr;  // caller's device array (>= n entries)
+    int32_t *enq = nullptr, *q[2] = {nullptr, nullptr}, *ob = nullptr;
+    ChunkItem *chunks = nullptr;
+    ExpandCounters *cnt = nullptr;          // [2]
+    unsigned long long *aux = nullptr;      // [0] outbox size, [1] apply appends, [2..] per-owner counts/cursors
+    int world = 0;
+    int cur = 0;
+    int64_t nq = 0;     // |q[cur]|
+    int64_t qcap = 0;
+    int round = 0;      // round stamps 1, 2, ...
+    int step = 0;       // supersteps done
+};
+
+static void shard_free(sp_sssp_shard *h) {
+    if (!h) return;
+    void *ps[] = {h->enq, h->q[0], h->q[1], h->ob, h->chunks, h->cnt, h->aux};
+    for (void *p : ps)
+        if (p) resident_free(p);
+    delete h;
 }
 
-extern "C" int sp_sssp_block_step(sp_graph *g, int64_t v0, int64_t v1, int32_t *dist,
-                                  int32_t *last, int64_t *frontier, int64_t *relaxed) {
-    SP_CHECK(g && dist && last && v0 >= 0 && v0 <= v1 && v1 <= g->n, SP_ERR_ARG,
-             "sp_sssp_block_step: bad arguments");
+extern "C" int sp_sssp_shard_create(sp_graph *g, int64_t v0, int64_t v1, int32_t src, int world,
+                                    int32_t *dist, sp_sssp_shard **out) {
+    SP_CHECK(g && dist && out && v0 >= 0 && v0 <= v1 && v1 <= g->n && world >= 1 && world <= 4096,
+             SP_ERR_ARG, "sp_sssp_shard_create: bad arguments");
+    SP_CHECK(src >= 0 && src < g->n, SP_ERR_ARG, "node argument 'src'=%d out of range", src);
+    *out = nullptr;
     Call c;
     SP_TRY(c.begin(g->device));
     SP_TRY(ensure_weff(g, c));
-    const int64_t nb = std::max<int64_t>(1, v1 - v0);
-    int32_t *q, *qn;
-    ChunkItem *chunks;
-    ExpandCounters *cnt;
-    SP_TRY(c.alloc(&q, nb));
-    SP_TRY(c.alloc(&qn, 1));
-    SP_TRY(c.alloc(&chunks, expand_chunk_capacity(g->m)));
-    SP_TRY(c.alloc(&cnt, 2));
-    SP_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(ExpandCounters), c.stream));
-    ExpandCounters *h;
-    SP_TRY(c.host_as(&h));
-    if (v1 > v0) {
-        k_block_frontier<<<grid_for(v1 - v0, kBlock, c.device), kBlock, 0, c.stream>>>(
-            dist, last, v0, v1, q, &cnt[1].next_size);
+    sp_sssp_shard *h = new sp_sssp_shard;
+    h->g = g;
+    h->v0 = v0;
+    h->v1 = v1;
+    h->dist = dist;
+    h->world = world;
+    h->qcap = 2 * (v1 - v0) + 2;  // a frontier plus the messages applied to it
+    const int64_t n = g->n;
+    int rc = SP_OK;
+    auto al = [&](void **p, size_t b) {
+        if (rc == SP_OK) rc = resident_alloc(p, b);
+    };
+    al((void **)&h->enq, n * 4);
+    al((void **)&h->q[0], h->qcap * 4);
+    al((void **)&h->q[1], h->qcap * 4);
+    al((void **)&h->ob, std::max<int64_t>(1, n) * 4);
+    al((void **)&h->chunks, expand_chunk_capacity(g->m) * sizeof(ChunkItem));
+    al((void **)&h->cnt, 2 * sizeof(ExpandCounters));
+    al((void **)&h->aux, (2 + 2 * (size_t)world) * 8);
+    if (rc != SP_OK) {
+        shard_free(h);
+        return rc;
+    }
+    k_shard_init<<<grid_for(n, kBlock, c.device), kBlock, 0, c.stream>>>(dist, h->enq, n, src);
+    c.launches++;
+    SP_CUDA(cudaMemsetAsync(h->cnt, 0, 2 * sizeof(ExpandCounters), c.stream));
+    if (src >= v0 && src < v1) {  // the owner of src starts with it
+        SP_CUDA(cudaMemcpyAsync(h->q[0], &src, 4, cudaMemcpyHostToDevice, c.stream));
+        h->nq = 1;
+    }
+    rc = c.finish(nullptr);
+    if (rc != SP_OK) {
+        shard_free(h);
+        return rc;
+    }
+    *out = h;
+    return SP_OK;
+}
+
+extern "C" int sp_sssp_shard_relax(sp_sssp_shard *h, int64_t max_rounds, int64_t per,
+                                   int64_t *send, int64_t *counts, int64_t *info) {
+    SP_CHECK(h && send && counts && per >= 1 && max_rounds >= 1, SP_ERR_ARG,
+             "sp_sssp_shard_relax: bad arguments");
+    sp_graph *g = h->g;
+    Call c;
+    SP_TRY(c.begin(g->device));
+    ExpandCounters *hc;
+    SP_TRY(c.host_as(&hc));
+    const int sms = num_sms(c.device);
+    const bool big = g->max_outdeg > kSplit;
+    h->step++;
+    SP_CUDA(cudaMemsetAsync(h->aux, 0, (2 + 2 * (size_t)h->world) * 8, c.stream));
+    int64_t updates = 0, relaxed = 0, rounds = 0;
+    bool overflow = false;
+    while (h->nq > 0 && rounds < max_rounds) {
+        h->round++;
+        ExpandCounters *cc = h->cnt + h->cur;
+        SP_CUDA(cudaMemsetAsync(cc, 0, sizeof(ExpandCounters), c.stream));
+        RelaxShardOp op{h->dist, h->enq, g->weff, &cc->flag, h->ob, &h->aux[0],
+                        (unsigned long long)std::max<int64_t>(1, g->n), h->v0, h->v1,
+                        h->round, h->step};
+        launch_expand(op, g->off, g->adj, h->q[h->cur], h->nq, h->q[h->cur ^ 1], h->chunks, cc,
+                      sms, big, c.stream, &c.launches);
+        SP_CUDA(cudaGetLastError());
+        SP_CUDA(cudaMemcpyAsync(hc, cc, sizeof(ExpandCounters), cudaMemcpyDeviceToHost, c.stream));
+        SP_CUDA(cudaStreamSynchronize(c.stream));
+        updates += (int64_t)hc->next_size;  // owned Min wins (bsp.py:213-216)
+        relaxed += (int64_t)hc->scanned;
+        rounds++;
+        h->cur ^= 1;
+        h->nq = (int64_t)hc->next_size;
+        if (hc->flag) {
+            overflow = true;
+            break;
+        }
+    }
+    // outbox -> per-owner counts -> packed messages grouped by owner
+    unsigned long long *hk = reinterpret_cast<unsigned long long *>(hc);
+    SP_CUDA(cudaMemcpyAsync(hk, h->aux, 8, cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t k = (int64_t)hk[0];
+    unsigned long long *dcnt = h->aux + 2, *dcur = h->aux + 2 + h->world;
+    if (k > 0) {
+        k_shard_count<<<grid_for(k, kBlock, c.device), kBlock, h->world * 8, c.stream>>>(
+            h->ob, k, per, h->world, dcnt);
         c.launches++;
     }
-    SP_CUDA(cudaMemcpyAsync(h, &cnt[1], sizeof(ExpandCounters), cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaMemcpyAsync(hk, dcnt, h->world * 8, cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
-    const int64_t nq = (int64_t)h->next_size;
-    if (nq) {
-        RelaxNoPushOp op{dist, g->weff, &cnt->flag};
-        launch_expand(op, g->off, g->adj, q, nq, qn, chunks, cnt, num_sms(c.device),
-                      g->max_outdeg > kSplit, c.stream, &c.launches);
-        SP_CUDA(cudaGetLastError());
-        SP_CUDA(cudaMemcpyAsync(h, cnt, sizeof(ExpandCounters), cudaMemcpyDeviceToHost, c.stream));
-    } else {
-        h->scanned = 0;
-        h->flag = 0;
+    std::vector<unsigned long long> start(h->world);
+    unsigned long long acc = 0;
+    for (int r = 0; r < h->world; r++) {
+        counts[r] = (int64_t)hk[r];
+        start[r] = acc;
+        acc += hk[r];
+    }
+    if (k > 0) {
+        SP_CUDA(cudaMemcpyAsync(dcur, start.data(), h->world * 8, cudaMemcpyHostToDevice, c.stream));
+        k_shard_pack<<<grid_for(k, kBlock, c.device), kBlock, 0, c.stream>>>(h->ob, k, per, h->dist,
+                                                                            dcur, send);
+        c.launches++;
     }
     SP_TRY(c.finish(nullptr));
-    SP_CHECK(!h->flag, SP_ERR_OVERFLOW, "SSSP distance left the int32 range (negative weights)");
-    if (frontier) *frontier = nq;
-    if (relaxed) *relaxed = (int64_t)h->scanned;
+    if (info) {
+        info[0] = updates;
+        info[1] = relaxed;
+        info[2] = rounds;
+        info[3] = h->nq;  // owned frontier left for the next superstep
+    }
+    SP_CHECK(!overflow, SP_ERR_OVERFLOW, "SSSP distance left the int32 range (negative weights)");
     return SP_OK;
+}
+
+extern "C" int sp_sssp_shard_apply(sp_sssp_shard *h, const int64_t *msgs, int64_t k,
+                                   const int32_t *block, int64_t *frontier) {
+    SP_CHECK(h && k >= 0 && (k == 0 || msgs || block), SP_ERR_ARG,
+             "sp_sssp_shard_apply: bad arguments");
+    sp_graph *g = h->g;
+    Call c;
+    SP_TRY(c.begin(g->device));
+    unsigned long long *hk;
+    SP_TRY(c.host_as(&hk));
+    // apply stamps are negative (never a round stamp) and fresh per superstep
+    const int stamp = -2 - h->step;
+    SP_CUDA(cudaMemcpyAsync(h->aux + 1, &h->nq, 8, cudaMemcpyHostToDevice, c.stream));
+    int32_t *q = h->q[h->cur];
+    if (block && h->v1 > h->v0) {
+        k_shard_apply_dense<<<grid_for(h->v1 - h->v0, kBlock, c.device), kBlock, 0, c.stream>>>(
+            block, h->v0, h->v1, h->dist, h->enq, stamp, q, h->aux + 1);
+        c.launches++;
+    } else if (!block && k > 0) {
+        k_shard_apply<<<grid_for(k, kBlock, c.device), kBlock, 0, c.stream>>>(
+            msgs, k, h->dist, h->enq, stamp, q, h->aux + 1);
+        c.launches++;
+    }
+    SP_CUDA(cudaMemcpyAsync(hk, h->aux + 1, 8, cudaMemcpyDeviceToHost, c.stream));
+    SP_TRY(c.finish(nullptr));
+    h->nq = (int64_t)hk[0];
+    SP_CHECK(h->nq <= h->qcap, SP_ERR_CUDA, "sp_sssp_shard_apply: frontier overflow");
+    if (frontier) *frontier = h->nq;
+    return SP_OK;
+}
+
+extern "C" void sp_sssp_shard_destroy(sp_sssp_shard *h) {
+    if (!h) return;
+    cudaSetDevice(h->g->device);
+    cudaDeviceSynchronize();
+    shard_free(h);
 }

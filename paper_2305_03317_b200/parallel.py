@@ -16,13 +16,15 @@ trident/bsp.py; its ownership rule is graph.py:226-249):
          ``all_gather`` of the owned contrib slices (the reference's
          remote-read snapshot, bsp.py:182-185/287-288) and ``all_reduce(max)``
          of diff (the scalar merge, bsp.py:322-330).
-* SSSP -- block partition with replicated distance arrays; per superstep the
-         owned frontier (owned vertices whose distance dropped since their
-         last expansion) is relaxed into the local copy, then
-         ``all_reduce(min)`` merges all ranks' candidates (the aggregated
-         min-messages of bsp.py:45-72, dense form) and ``all_reduce(sum)`` of
-         the frontier sizes decides convergence -- evaluated AFTER the
-         exchange, which is exactly what bsp.py:393-417 gets wrong.
+* SSSP -- owner-computes over the block partition: per superstep each rank
+         relaxes its owned frontier (one pass, or to a local fixpoint);
+         remote improvements leave as ONE aggregated (vertex, local min)
+         message per vertex (bsp.py:45-72), grouped by owner and exchanged
+         with one ``all_to_all_single`` -- or, when the messages would
+         outweigh the distance array, a MIN ``reduce_scatter``; owners apply
+         them (bsp.py:350-368), then ``all_reduce(sum)`` of the next
+         frontier sizes decides convergence -- evaluated AFTER the exchange,
+         which is exactly what bsp.py:393-417 gets wrong.
 
 The per-rank compute is a backend object; ``NativeBackend`` drives
 libstarplat_b200.so on this rank's GPU.  The tests substitute a CPU backend
@@ -32,6 +34,7 @@ libstarplat_b200.so on this rank's GPU.  The tests substitute a CPU backend
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -124,30 +127,60 @@ class NativeBackend:
             None), "sp_pagerank_block_step")
         return float(diff.value)
 
-    # -- SSSP
-    def sssp_init(self, g, src):
-        t = self.torch
-        n = g.n
-        dist = t.empty(max(1, n), dtype=t.int32, device=self.device)
-        last = t.empty(max(1, n), dtype=t.int32, device=self.device)
-        self._fence()
-        rc = self.L.sp_sssp_block_init(g.handle, int(src), C.c_void_p(dist.data_ptr()),
-                                       C.c_void_p(last.data_ptr()))
-        self._chk(rc, "sp_sssp_block_init")
-        return dist, last
-
-    def sssp_step(self, g, v0, v1, dist, last):
-        self._fence()
-        f, r = C.c_int64(), C.c_int64()
-        rc = self.L.sp_sssp_block_step(g.handle, int(v0), int(v1), C.c_void_p(dist.data_ptr()),
-                                       C.c_void_p(last.data_ptr()), C.byref(f), C.byref(r))
-        if rc == _lib.SP_ERR_OVERFLOW:
-            raise OverflowError(_lib.last_error())
-        self._chk(rc, "sp_sssp_block_step")
-        return int(f.value), int(r.value)
+    # -- SSSP (owner-computes shard, one handle per run)
+    def sssp_shard(self, g, src, v0, v1, per, world):
+        return _NativeShard(self, g, src, v0, v1, per, world)
 
     def to_host(self, x):
         return x.cpu().numpy()
+
+
+class _NativeShard:
+    """sp_sssp_shard_* on this rank's GPU: dist (padded to per * world for a
+    reduce-scatter) and the message send buffer are torch tensors."""
+
+    def __init__(self, be, g, src, v0, v1, per, world):
+        t = be.torch
+        self.be, self.g, self.world, self.per = be, g, world, per
+        self.dist = t.full((per * world,), 2147483647, dtype=t.int32, device=be.device)
+        self.send = t.empty(max(1, g.n), dtype=t.int64, device=be.device)
+        self.h = C.c_void_p()
+        be._fence()
+        be._chk(be.L.sp_sssp_shard_create(g.handle, int(v0), int(v1), int(src), int(world),
+                                          C.c_void_p(self.dist.data_ptr()), C.byref(self.h)),
+                "sp_sssp_shard_create")
+
+    def relax(self, max_rounds):
+        """-> (per-owner message counts, info[4]: owned expanded, slots
+        relaxed, rounds, frontier left); raises OverflowError."""
+        counts = np.zeros(self.world, dtype=np.int64)
+        info = np.zeros(4, dtype=np.int64)
+        self.be._fence()
+        rc = self.be.L.sp_sssp_shard_relax(self.h, int(max_rounds), int(self.per),
+                                           C.c_void_p(self.send.data_ptr()),
+                                           counts.ctypes.data_as(C.c_void_p),
+                                           info.ctypes.data_as(C.c_void_p))
+        if rc == _lib.SP_ERR_OVERFLOW:
+            raise OverflowError(_lib.last_error())
+        self.be._chk(rc, "sp_sssp_shard_relax")
+        return counts, info
+
+    def apply(self, msgs=None, k=0, block=None) -> int:
+        self.be._fence()
+        f = C.c_int64()
+        self.be._chk(self.be.L.sp_sssp_shard_apply(
+            self.h, C.c_void_p(msgs.data_ptr()) if msgs is not None and k else None, int(k),
+            C.c_void_p(block.data_ptr()) if block is not None else None, C.byref(f)),
+            "sp_sssp_shard_apply")
+        return int(f.value)
+
+    def result(self):
+        return self.be.to_host(self.dist[: self.g.n])
+
+    def close(self):
+        if self.h:
+            self.be.L.sp_sssp_shard_destroy(self.h)
+            self.h = C.c_void_p()
 
 
 def _dist():
@@ -234,17 +267,19 @@ class _Tracer:
 
 def simulate(tp, g, nranks: int, args: dict, function: str | None = None,
              max_iters: int | None = None, *, backend=None, group=None,
-             deterministic: bool = False) -> SimResult:
+             deterministic: bool = False, local_fixpoint: bool = False) -> SimResult:
     """bsp.simulate's surface (bsp.py:452-465) over real ranks: nranks must
     equal the process group's size (one rank per GPU); returns the run's
     result and its superstep trace (convergence evaluated after the
-    exchange, unlike bsp.py:393-417 -- SURVEY F4)."""
+    exchange, unlike bsp.py:393-417 -- SURVEY F4).  local_fixpoint: SSSP
+    ranks relax their owned frontier to a local fixpoint before each
+    exchange (bsp.py:297-306)."""
     dist = _dist()
     if nranks != dist.get_world_size(group):
         raise ValueError(f"simulate: nranks={nranks} but the process group has "
                          f"{dist.get_world_size(group)} ranks (one rank per GPU)")
     r = run_sharded(tp, g, args, function, max_iters, backend=backend, group=group,
-                    deterministic=deterministic, trace=True)
+                    deterministic=deterministic, trace=True, local_fixpoint=local_fixpoint)
     return SimResult(result=r, supersteps=r.supersteps)
 
 
@@ -266,11 +301,14 @@ def tc_ranges(offsets: np.ndarray, world: int) -> list[tuple[int, int]]:
 
 def run_sharded(tp, g, args: dict, function: str | None = None,
                 max_iters: int | None = None, *, backend=None, group=None,
-                deterministic: bool = False, trace: bool = False) -> RunResult:
+                deterministic: bool = False, trace: bool = False,
+                local_fixpoint: bool = False) -> RunResult:
     """Run a corpus program over all ranks of ``group`` (default: the world).
     Every rank must call it with the same graph and arguments.  trace=True
     records the superstep trace in ``result.supersteps`` (one extra small
-    all-gather per superstep)."""
+    all-gather per superstep).  local_fixpoint (SSSP): relax the owned
+    frontier to a local fixpoint between exchanges (bsp.py:297-306) --
+    fewer supersteps, same dist."""
     dist = _dist()
     world = dist.get_world_size(group)
     me = dist.get_rank(group)
@@ -285,11 +323,24 @@ def run_sharded(tp, g, args: dict, function: str | None = None,
     t0 = time.perf_counter()
     fn = {"sssp": _sssp, "sssp_pull": _sssp, "pr": _pr, "bc": _bc, "tc": _tc}[prog.key]
     tr = _Tracer(trace, backend, group)
-    env, fpi, stats = fn(backend, dg, bound, cap, world, me, group, deterministic, E, prog, tr)
+    kw = {"local_fixpoint": local_fixpoint} if fn is _sssp else {}
+    env, fpi, stats = fn(backend, dg, bound, cap, world, me, group, deterministic, E, prog, tr,
+                         **kw)
     r = RunResult(env=env, fixedpoint_iterations=fpi,
                   wall_seconds=time.perf_counter() - t0, stats=stats)
     r.supersteps = tr.steps if trace else None
     return r
+
+
+def _reduce_scatter_min(out, full, group):
+    dist = _dist()
+    if dist.get_backend(group) == "gloo":  # no reduce_scatter on gloo
+        t = full.clone()
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        me = dist.get_rank(group)
+        out.copy_(t[me * out.numel():(me + 1) * out.numel()])
+    else:
+        dist.reduce_scatter_tensor(out, full, op=dist.ReduceOp.MIN, group=group)
 
 
 def _sum_stats(be, keys, group):
@@ -382,40 +433,77 @@ def _pr(be, g, bound, cap, world, me, group, det, E, prog, tr):
     return env, {"converged": iters}, {"block": (v0, v1)}
 
 
-def _sssp(be, g, bound, cap, world, me, group, det, E, prog, tr):
+def _sssp(be, g, bound, cap, world, me, group, det, E, prog, tr, local_fixpoint=False):
+    """Owner-computes supersteps: local relaxation (one pass, or passes to a
+    local fixpoint, bsp.py:297-306), aggregated min-messages exchanged with
+    one all-to-all (sparse supersteps) or a MIN reduce-scatter of the dist
+    arrays (dense ones), owner apply, then ONE all-reduce of the frontier
+    sizes: fixedPoint finishes when no rank has a frontier after the
+    exchange, and the cap is tested only after that
+    (bsp.py:402-415)."""
     dist = _dist()
     torch = be.torch
     parts = block_partition(g, world)
+    per = parts[0].size
     rr = parts[me].real_range()
     v0, v1 = rr.start, rr.stop
-    dvec, last = be.sssp_init(g, bound["src"])
-    steps = relaxed = 0
-    while True:
-        before = dvec.clone() if tr.on else None
-        try:
-            f, r = be.sssp_step(g, v0, v1, dvec, last)
-            bad = 0
-        except OverflowError:
-            f, r, bad = 0, 0, 1
-        relaxed += r
-        if tr.on:  # owned drops vs remote candidates (aggregated: one per vertex)
-            dropped = (dvec < before)[: g.n]
-            own = int(dropped[v0:v1].sum().item())
-            tr.record("fixedPoint finished", own, int(dropped.sum().item()) - own)
-        dist.all_reduce(dvec, op=dist.ReduceOp.MIN, group=group)
-        fz = torch.tensor([f, bad], dtype=torch.int64, device=be.device)
-        dist.all_reduce(fz, op=dist.ReduceOp.SUM, group=group)
-        if int(fz[1].item()):
-            raise E.ExecError("SSSP distance left the int32 range (negative weights)")
-        if int(fz[0].item()) == 0:  # nobody had a frontier: the exchange changed nothing
-            tr.finish_last()
-            break
-        steps += 1
-        if steps >= cap:
-            raise E.NonConvergenceError(prog.flag, cap)
     n = g.n
-    d = be.to_host(dvec)[:n].copy()
+    sh = be.sssp_shard(g, bound["src"], v0, v1, per, world)
+    try:
+        steps = relaxed = sent_total = 0
+        dense_steps = 0
+        while True:
+            try:
+                counts, info = sh.relax(cap if local_fixpoint else 1)
+                bad = 0
+            except OverflowError:
+                counts, info, bad = np.zeros(world, dtype=np.int64), np.zeros(4, np.int64), 1
+            relaxed += int(info[1])
+            # every rank's per-owner counts (+ overflow flag): the send and
+            # receive splits of the all-to-all and the global message volume
+            row = torch.tensor(list(counts) + [bad], dtype=torch.int64, device=be.device)
+            allc = [torch.zeros_like(row) for _ in range(world)]
+            dist.all_gather(allc, row, group=group)
+            M = torch.stack(allc).cpu().numpy()
+            if M[:, world].any():
+                raise E.ExecError("SSSP distance left the int32 range (negative weights)")
+            total = int(M[:, :world].sum())
+            sent_total += int(counts.sum())
+            mode = os.environ.get("SP_SSSP_EXCHANGE", "auto")  # tests force each form
+            dense = mode == "dense" or (mode == "auto" and 8 * total > 4 * per * world)
+            if dense:  # a MIN reduce-scatter of the dist arrays moves fewer bytes
+                dense_steps += 1
+                blk = torch.empty(per, dtype=torch.int32, device=be.device)
+                _reduce_scatter_min(blk, sh.dist, group)
+                f = sh.apply(block=blk[: v1 - v0] if v1 > v0 else blk)
+            elif total:
+                send_splits = [int(x) for x in M[me, :world]]
+                recv_splits = [int(x) for x in M[:, me]]
+                recv = torch.empty(max(1, sum(recv_splits)), dtype=torch.int64, device=be.device)
+                dist.all_to_all_single(recv[: sum(recv_splits)], sh.send[: sum(send_splits)],
+                                       recv_splits, send_splits, group=group)
+                f = sh.apply(recv, sum(recv_splits))
+            else:
+                f = sh.apply()
+            steps += 1
+            ft = torch.tensor([f], dtype=torch.int64, device=be.device)
+            dist.all_reduce(ft, op=dist.ReduceOp.SUM, group=group)
+            done = int(ft.item()) == 0
+            tr.record("fixedPoint finished", int(info[0]), int(counts.sum()), finished=done)
+            if done:
+                break
+            if steps >= cap:
+                raise E.NonConvergenceError(prog.flag, cap)
+        # owned blocks back to every rank
+        mine = torch.full((per,), 2147483647, dtype=torch.int32, device=be.device)
+        mine[: v1 - v0] = sh.dist[v0:v1]
+        full = torch.empty(per * world, dtype=torch.int32, device=be.device)
+        _all_gather_flat(full, mine, group)
+        d = be.to_host(full)[:n].copy()
+    finally:
+        sh.close()
     env = PropertyEnv(node_props={"dist": d, "modified": np.zeros(n, dtype=bool),
                                   "modified_nxt": np.zeros(n, dtype=bool)},
                       scalars={"finished": True})
-    return env, {"finished": steps}, {"relaxed": relaxed, "block": (v0, v1)}
+    return env, {"finished": steps}, {"relaxed": relaxed, "block": (v0, v1),
+                                      "messages": sent_total, "dense_supersteps": dense_steps}

@@ -95,27 +95,77 @@ class OracleBackend:
             contrib[v - v0] = nr / outdeg[v] if outdeg[v] > 0 else 0.0
         return d
 
-    # SSSP supersteps
-    def sssp_init(self, g, src):
-        dist = np.full(max(1, g.n), INT_MAX, dtype=np.int32)
-        dist[src] = 0
-        last = np.full(max(1, g.n), INT_MAX, dtype=np.int32)
-        return torch.from_numpy(dist), torch.from_numpy(last)
+    # SSSP owner-computes shard (sp_sssp_shard_* semantics)
+    def sssp_shard(self, g, src, v0, v1, per, world):
+        return _OracleShard(g, src, v0, v1, per, world)
 
-    def sssp_step(self, g, v0, v1, dist, last):
-        d = dist.numpy()
-        ls = last.numpy()
-        F = [v for v in range(v0, v1) if d[v] < ls[v]]
-        relaxed = 0
-        for v in F:
-            ls[v] = d[v]
-        for v in F:
-            for e in range(g.off[v], g.off[v + 1]):
-                relaxed += 1
-                x = g.adj[e]
-                cand = int(d[v]) + int(g.weff[e])
-                if cand < INT_MAX and cand < d[x]:
+
+class _OracleShard:
+    def __init__(self, g, src, v0, v1, per, world):
+        self.g, self.v0, self.v1, self.per, self.world = g, v0, v1, per, world
+        self.dist = torch.full((per * world,), INT_MAX, dtype=torch.int32)
+        self.dist[src] = 0
+        self.q = [src] if v0 <= src < v1 else []
+        self.send = torch.zeros(max(1, g.n), dtype=torch.int64)
+
+    def relax(self, max_rounds):
+        g, d = self.g, self.dist.numpy()
+        out = set()
+        upd = rel = rounds = 0
+        while self.q and rounds < max_rounds:
+            nxt = []
+            seen = set()
+            for v in self.q:
+                dv = int(d[v])
+                for e in range(g.off[v], g.off[v + 1]):
+                    rel += 1
+                    x = int(g.adj[e])
+                    cand = dv + int(g.weff[e])
+                    if cand >= INT_MAX or cand >= d[x]:
+                        continue
                     if cand < -2 ** 31:
                         raise OverflowError("int32 underflow")
                     d[x] = cand
-        return len(F), relaxed
+                    if self.v0 <= x < self.v1:
+                        if x not in seen:
+                            seen.add(x)
+                            nxt.append(x)
+                    else:
+                        out.add(x)
+            self.q = nxt
+            upd += len(nxt)
+            rounds += 1
+        ids = sorted(out, key=lambda x: x // self.per)
+        counts = np.zeros(self.world, dtype=np.int64)
+        for i, x in enumerate(ids):
+            counts[x // self.per] += 1
+            self.send[i] = (x << 32) | (int(d[x]) & 0xffffffff)
+        return counts, np.array([upd, rel, rounds, len(self.q)], dtype=np.int64)
+
+    def apply(self, msgs=None, k=0, block=None):
+        d = self.dist.numpy()
+        seen = set(self.q)
+        if block is not None:
+            b = block.numpy()
+            for v in range(self.v0, self.v1):
+                if b[v - self.v0] < d[v]:
+                    d[v] = b[v - self.v0]
+                    if v not in seen:
+                        seen.add(v)
+                        self.q.append(v)
+        else:
+            for m in (msgs[:k].tolist() if k else []):
+                x = m >> 32
+                c = ((m & 0xffffffff) ^ 0x80000000) - 0x80000000
+                if c < d[x]:
+                    d[x] = c
+                    if x not in seen:
+                        seen.add(x)
+                        self.q.append(x)
+        return len(self.q)
+
+    def result(self):
+        return self.dist.numpy()[: self.g.n]
+
+    def close(self):
+        pass

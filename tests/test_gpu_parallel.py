@@ -2,8 +2,8 @@
 
 One GPU is available, so two ranks share cuda:0 over gloo (NCCL refuses two
 ranks on one device); this drives the native block kernels
-(sp_sssp_block_step, sp_pagerank_block_step, sp_tc ranges, sp_bc source
-shares) through the real sharding/exchange logic and checks the results
+(sp_sssp_shard_*: owner-computes SSSP with aggregated messages in both
+exchange forms, sp_pagerank_block_step, sp_tc ranges, sp_bc source shares) through the real sharding/exchange logic and checks the results
 against the single-process CPU oracle."""
 
 import os
@@ -54,6 +54,18 @@ def _worker(rank, world, port, kind, q):
         out = {}
         out["dist"] = parallel.run_sharded(corpus.SSSP, g, {"src": 0},
                                            backend=be).env.node_props["dist"]
+        for ex in ("sparse", "dense"):
+            os.environ["SP_SSSP_EXCHANGE"] = ex
+            r = parallel.run_sharded(corpus.SSSP, g, {"src": 0}, backend=be)
+            out["dist_" + ex] = r.env.node_props["dist"]
+            out["k_" + ex] = r.fixedpoint_iterations["finished"]
+        os.environ["SP_SSSP_EXCHANGE"] = "auto"
+        sim = parallel.simulate(corpus.SSSP, g, 2, {"src": 0}, backend=be, local_fixpoint=True)
+        out["dist_lf"] = sim.result.env.node_props["dist"]
+        out["trace"] = parallel.format_trace_tsv(sim)
+        out["steps"] = [(s.finished, dict(s.local_updates), dict(s.msgs_out))
+                        for s in sim.supersteps]
+        out["k_lf"] = sim.result.fixedpoint_iterations["finished"]
         r = parallel.run_sharded(corpus.PR, g, {"damping": 0.85, "epsilon": 1e-6,
                                                 "maxIter": 100}, backend=be,
                                  deterministic=True)
@@ -92,6 +104,22 @@ def test_native_sharded_two_ranks(kind):
     for r in range(2):
         x = res[r]
         assert np.array_equal(x["dist"], d_ref)
+        for key in ("dist_sparse", "dist_dense", "dist_lf"):
+            assert np.array_equal(x[key], d_ref), key
+        assert x["k_sparse"] == x["k_dense"]  # same supersteps, either exchange form
+        assert x["k_lf"] <= x["k_sparse"]
+        # native simulate trace: bsp.py's TSV layout, one line per rank per
+        # superstep, finished only on the last; every vertex reached from 0
+        # is lowered once at least, by its owner or by an applied message
+        lines = x["trace"].strip().split("\n")
+        assert lines[0] == "superstep\trank\tlocal_updates\tmsgs_out\tfinished"
+        assert len(lines) == 1 + 2 * len(x["steps"])
+        assert [s[0] for s in x["steps"]] == [False] * (len(x["steps"]) - 1) + [True]
+        if len(x["steps"]) > 1:
+            assert sum(s[2][0] + s[2][1] for s in x["steps"]) > 0  # messages crossed
+        reached = int((d_ref < 2147483647).sum())
+        assert sum(s[1][0] + s[1][1] for s in x["steps"]) + \
+            sum(s[2][0] + s[2][1] for s in x["steps"]) >= reached - 1
         assert x["rank"].tobytes() == rank_ref.tobytes() and x["iter"] == it_ref
         assert np.abs(x["rank_fast"] - rank_ref).max() <= 1e-12 * np.abs(rank_ref).max()
         assert np.abs(x["bc"] - bc_ref).max() <= 1e-9 * max(1.0, np.abs(bc_ref).max())

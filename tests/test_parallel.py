@@ -38,9 +38,10 @@ def _graph(kind, directed):
     return cpu_ref.build_csr(u, v, w, directed, n)
 
 
-def _worker(rank, world, port, kind, directed, q):
+def _worker(rank, world, port, kind, directed, q, exchange="auto"):
     import torch.distributed as dist
     from oracle_backend import OracleBackend
+    os.environ["SP_SSSP_EXCHANGE"] = exchange
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -50,6 +51,8 @@ def _worker(rank, world, port, kind, directed, q):
         out = {}
         r = parallel.run_sharded(corpus.SSSP, g, {"src": 0}, backend=be)
         out["dist"] = r.env.node_props["dist"]
+        r = parallel.run_sharded(corpus.SSSP, g, {"src": 0}, backend=be, local_fixpoint=True)
+        out["dist_lf"] = r.env.node_props["dist"]
         args = {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
         r = parallel.run_sharded(corpus.PR, g, args, backend=be)
         out["rank"] = r.env.node_props["rank"]
@@ -90,6 +93,7 @@ def test_sharded_matches_single_process_oracle(world, kind, directed):
     for r in range(world):
         o = res[r]
         assert np.array_equal(o["dist"], d_ref)          # bit-exact
+        assert np.array_equal(o["dist_lf"], d_ref)       # local fixpoint: same dist
         assert o["rank"].tobytes() == rank_ref.tobytes()  # same left folds per vertex
         assert o["iter"] == it_ref
         scale = max(1.0, float(np.abs(bc_ref).max()))
@@ -152,3 +156,70 @@ def test_simulate_trace_and_f4_fix():
         # that message
         assert sum(s[2][0] + s[2][1] for s in steps) + 1 == 9
     assert res[0][1] == res[1][1]
+
+
+def _sssp_worker(rank, world, port, exchange, q):
+    import torch.distributed as dist
+    from oracle_backend import OracleBackend
+    from paper_2305_03317_b200.errors import NonConvergenceError
+    os.environ["SP_SSSP_EXCHANGE"] = exchange
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        be = OracleBackend()
+        out = {}
+        for kind, directed in (("rmat", True), ("grid", False), ("multi", True)):
+            g = _graph(kind, directed)
+            r = parallel.run_sharded(corpus.SSSP, g, {"src": 0}, backend=be)
+            k = r.fixedpoint_iterations["finished"]
+            # the cap is tested after convergence: max_iters == k converges
+            r2 = parallel.run_sharded(corpus.SSSP, g, {"src": 0}, max_iters=k, backend=be)
+            try:
+                parallel.run_sharded(corpus.SSSP, g, {"src": 0}, max_iters=k - 1, backend=be)
+                capped = None
+            except NonConvergenceError as e:
+                capped = (e.flag, e.cap)
+            lf = parallel.run_sharded(corpus.SSSP, g, {"src": 0}, backend=be,
+                                      local_fixpoint=True, trace=True)
+            out[kind] = (r.env.node_props["dist"], k, r2.env.node_props["dist"],
+                         r2.fixedpoint_iterations["finished"], capped,
+                         lf.env.node_props["dist"], lf.fixedpoint_iterations["finished"],
+                         r.stats["dense_supersteps"], r.stats["messages"])
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exchange", ["sparse", "dense"])
+def test_sharded_sssp_exchange_forms_and_cap(exchange):
+    """Both exchange forms give the oracle's dist; max_iters == k converges
+    and k - 1 raises NonConvergenceError('finished', k - 1) (the cap is
+    tested after the exchange); local fixpoints need no more
+    supersteps than single passes."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_sssp_worker, args=(r, world, port, exchange, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for kind, directed in (("rmat", True), ("grid", False), ("multi", True)):
+        d_ref = cpu_ref.sssp(_graph(kind, directed), 0)[0]
+        for r in range(world):
+            d, k, d2, k2, capped, dlf, klf, dense, msgs = res[r][kind]
+            assert np.array_equal(d, d_ref) and np.array_equal(d2, d_ref)
+            assert np.array_equal(dlf, d_ref)
+            assert k2 == k and k >= 1
+            assert capped == ("finished", k - 1)
+            assert klf <= k
+            if exchange == "dense":
+                assert dense == k
+            else:
+                assert dense == 0
+        assert len({res[r][kind][1] for r in range(world)}) == 1  # same superstep count
