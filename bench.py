@@ -59,15 +59,23 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def _ncu_summary():
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def ncu_traffic(kernel: str):
     """dram bytes per launch from the committed ncu summary, if any."""
-    path = os.path.join(REPO, "profiles", "ncu_summary.json")
-    try:
-        with open(path) as f:
-            d = json.load(f)
-        return d.get(kernel, {}).get("dram_bytes_per_launch")
-    except Exception:
-        return None
+    return _ncu_summary().get(kernel, {}).get("dram_bytes_per_launch")
+
+
+def ncu_run_traffic(line: str):
+    """DRAM bytes of one steady run of a bench line (tools/ncu_lines.sh ->
+    profiles/ncu_summary.json "run:<line>"), if captured."""
+    return _ncu_summary().get("run:" + line, {}).get("dram_bytes_per_run")
 
 
 class ClockSampler:
@@ -376,7 +384,12 @@ def cpu_baseline(g):
                 "sample": f"failed: {e}"}
 
 
-def _line(name, graph, g, ms, edges, model_bytes, hbm_peak, **extra):
+def _line(name, graph, g, ms, edges, model_bytes, hbm_peak, key=None, **extra):
+    """One algorithm line: GTEPS, the SURVEY 8d model-byte roofline and,
+    when tools/ncu_lines.sh captured it, the run's measured DRAM traffic
+    (`traffic`, bytes per run) with the fraction of peak it sustains over
+    the bench time (`dram_frac`) -- model frac >> dram_frac means the
+    gathers are served from L2, dram_frac > frac means wasted re-reads."""
     t = ms / 1e3
     d = {"graph": graph, "n": g.n, "m": g.m, "ms": ms, "gteps": edges / t / 1e9}
     if model_bytes:
@@ -384,8 +397,27 @@ def _line(name, graph, g, ms, edges, model_bytes, hbm_peak, **extra):
                          "frac": model_bytes / t / 1e9 / hbm_peak,
                          "frac_nominal_8tbs": model_bytes / t / 8e12,
                          "model_bytes": model_bytes}
+        tr = ncu_run_traffic(key) if key else None
+        d["roofline"]["traffic"] = tr
+        if tr:
+            d["roofline"]["dram_frac"] = tr / t / 1e9 / hbm_peak
     d.update(extra)
     return d
+
+
+def first_calls(fn, k, dev):
+    """Wall ms of the first k calls on a fresh graph (lazily built per-graph
+    structures: w_eff, the TC upper CSR, the PR plan / hot set / relabelled
+    layout), each synchronised."""
+    import torch
+    out = []
+    for _ in range(k):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize(dev)
+        out.append((time.perf_counter() - t0) * 1e3)
+    return out
 
 
 def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
@@ -402,6 +434,7 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
 
     if "sssp" in a.algos:
         g = sp.generate("rmat", 16, 16, seed=SEED, device=dev.index)
+        fc = first_calls(lambda: go(corpus.SSSP, g, {"src": 0}), 1, dev)
         ms, _, r = timed(lambda: go(corpus.SSSP, g, {"src": 0}), reps, 2, world, dev)
         offs = np.asarray(g.offsets)
         d = np.asarray(r.env.node_props["dist"].cpu() if world == 1 else
@@ -413,13 +446,16 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
             mb = 12 * R + 20 * F
         rel = (r.stats["edges_visited"] / (ms / reps / 1e3) / 1e9) if world == 1 else None
         out["sssp_cfg1"] = _line("sssp", "rmat16 directed", g, ms / reps, m_reached, mb,
-                                 hbm_peak, iterations=r.fixedpoint_iterations["finished"],
+                                 hbm_peak, key="sssp_cfg1",
+                                 iterations=r.fixedpoint_iterations["finished"],
+                                 first_call_ms=fc[0],
                                  relaxations_g_per_s=rel,
                                  note="Graph500 GTEPS = edges of reached vertices / time; "
                                       "m ~ 1M: launch/latency-bound")
         g.close()
     if "grid" in a.algos:  # cfg5a: 4096 x 4096 road-like grid, SSSP from 0 + PR
         g = sp.generate("grid", 4096, 4096, seed=SEED, device=dev.index)
+        fc = first_calls(lambda: go(corpus.SSSP, g, {"src": 0}), 1, dev)
         # 2 warm-ups: the result tensors of two calls must be in torch's
         # allocator cache, or the first timed call maps new device memory
         ms, _, r = timed(lambda: go(corpus.SSSP, g, {"src": 0}), 2, 2, world, dev)
@@ -427,14 +463,17 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         if world == 1:
             mb = 12 * r.stats["edges_visited"] + 20 * r.stats["vertices_visited"]
         out["sssp_cfg5_grid"] = _line("sssp", "grid 4096x4096 undirected, w U[1,100]", g, ms / 2,
-                                      g.m, mb, hbm_peak,
+                                      g.m, mb, hbm_peak, key="sssp_grid",
                                       iterations=r.fixedpoint_iterations["finished"],
-                                      note="GTEPS = m / time (every vertex reached); near-far "
-                                           "ordering, device-side loop")
+                                      first_call_ms=fc[0],
+                                      note="GTEPS = m / time (every vertex reached); "
+                                           "asynchronous near-far (per-block rings, one "
+                                           "cooperative launch); iterations = near-far phases")
         ms, _, r = timed(lambda: go(corpus.PR, g, PR_ARGS), 8, 2, world, dev)  # ~1 ms runs
         it = r.env.scalars["iter"]
         out["pr_cfg5_grid"] = _line("pr", "grid 4096x4096 undirected", g, ms / 8, it * g.m,
-                                    it * (12 * g.m + 36 * g.n), hbm_peak, iterations=it)
+                                    it * (12 * g.m + 36 * g.n), hbm_peak, key="pr_grid",
+                                    iterations=it)
         g.close()
     if "bc" in a.algos:
         g = sp.generate("rmat", 20, 16, seed=SEED, undirected=True, device=dev.index)
@@ -444,29 +483,37 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         ms, _, r = timed(lambda: go(corpus.BC, g, {"sourceSet": srcs}), 1, 2, world, dev)
         st = r.stats  # summed over ranks when sharded
         out["bc_cfg4"] = _line("bc", "rmat20 symmetrized", g, ms, st["edges_visited"],
-                               st["model_bytes"], hbm_peak, sources=256,
+                               st["model_bytes"], hbm_peak, key="bc_cfg4", sources=256,
                                sharding=f"sources/{world}",
                                note="GTEPS = slots of the reached vertices summed over "
-                                    "sources / time; roofline per SURVEY 8d (48 B/slot + "
-                                    "64 B/vertex per source), aggregate over all GPUs")
+                                    "sources / time; frac: SURVEY 8d's per-source model (48 "
+                                    "B/slot + 64 B/vertex per source) -- the 8-source batches "
+                                    "share one level read across sources, so it can exceed 1; "
+                                    "dram_frac: the batched run's measured DRAM bytes")
         g.close()
     if "tc" in a.algos:
         g = sp.generate("uniform", 1 << 24, 1 << 28, seed=SEED, undirected=True,
                         device=dev.index)
-        go(corpus.TC, g, {})  # builds the cached upper CSR (graph preprocessing)
+        # the first call builds the cached degree-ordered upper CSR
+        fc = first_calls(lambda: go(corpus.TC, g, {}), 1, dev)
         ms, _, r = timed(lambda: go(corpus.TC, g, {}), reps, 1, world, dev)
         mb = r.stats.get("model_bytes")
         out["tc_cfg3"] = _line("tc", "uniform 2^24 / 2^28 undirected", g, ms / reps,
-                               g.m // 2, mb, hbm_peak,
+                               g.m // 2, mb, hbm_peak, key="tc_cfg3",
+                               first_call_ms=fc[0], upper_csr_build_ms=fc[0] - ms / reps,
                                triangles=r.env.scalars["triangle_count"],
                                sharding=f"ranges/{world}")
         g.close()
     if "rmat24" in a.algos:  # SURVEY 8d target row: RMAT-24 on one GPU
         g = sp.generate("rmat", 24, 16, seed=SEED, device=dev.index)
+        # first calls: plan + hot set (1st), relabelled layout (2nd) -- per graph
+        fc = first_calls(lambda: go(corpus.PR, g, PR_ARGS), 2, dev)
         ms, _, r = timed(lambda: go(corpus.PR, g, PR_ARGS), 3, 2, world, dev)
         it = r.env.scalars["iter"]
         out["pr_rmat24"] = _line("pr", "rmat24 directed", g, ms / 3, it * g.m,
-                                 it * (12 * g.m + 36 * g.n), hbm_peak, iterations=it)
+                                 it * (12 * g.m + 36 * g.n), hbm_peak, key="pr_rmat24",
+                                 iterations=it, first_calls_ms=fc)
+        fc = first_calls(lambda: go(corpus.SSSP, g, {"src": 0}), 1, dev)  # + w_eff, rweff
         ms, _, r = timed(lambda: go(corpus.SSSP, g, {"src": 0}), 3, 2, world, dev)
         offs = np.asarray(g.offsets)
         d = np.asarray(r.env.node_props["dist"].cpu() if world == 1 else
@@ -476,15 +523,17 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         if world == 1:
             mb = 12 * r.stats["edges_visited"] + 20 * r.stats["vertices_visited"]
         out["sssp_rmat24"] = _line("sssp", "rmat24 directed", g, ms / 3, m_reached, mb, hbm_peak,
+                                   key="sssp_rmat24", first_call_ms=fc[0],
                                    iterations=r.fixedpoint_iterations["finished"],
                                    note="12 B per relaxation (push) or swept in-slot (pull sweeps, "
                                         "frontier > n/8) + 20 B per frontier vertex")
         g.close()
         g = sp.generate("rmat", 24, 16, seed=SEED, undirected=True, device=dev.index)
-        go(corpus.TC, g, {})  # builds the cached upper CSR (graph preprocessing)
+        fc = first_calls(lambda: go(corpus.TC, g, {}), 1, dev)  # + the upper CSR build
         ms, _, r = timed(lambda: go(corpus.TC, g, {}), 2, 1, world, dev)
         out["tc_rmat24"] = _line("tc", "rmat24 symmetrized", g, ms / 2, g.m // 2,
-                                 r.stats.get("model_bytes"), hbm_peak,
+                                 r.stats.get("model_bytes"), hbm_peak, key="tc_rmat24",
+                                 first_call_ms=fc[0], upper_csr_build_ms=fc[0] - ms / 2,
                                  triangles=r.env.scalars["triangle_count"],
                                  sharding=f"ranges/{world}")
         g.close()

@@ -38,6 +38,7 @@ constexpr int kBlock = 256;
 constexpr int64_t kDeltaMul = 16;        // near-far step = kDeltaMul x mean weight
 constexpr int64_t kNearFarMaxAvgDeg = 8;  // near-far only when m <= 8 n
 constexpr int kPersistBlocksPerSm = 2;    // persistent near-far grid: blocks per SM (cfg5a: 1 -> 87.8 ms, 2 -> 86.0 ms)
+constexpr int kAsyncBlocksPerSm = 1;  // asynchronous near-far: blocks per SM
 constexpr int kNfHops = 2;  // warp-local continuation hops (persistent near-far); cfg5a: 1-4 ~87-93 ms, 8 -> 120 ms, 16 -> 158 ms
 
 // Relaxation of sssp.sp:11-12 for one slot; payload = dist[v] at expansion.
@@ -428,6 +429,402 @@ __global__ void __launch_bounds__(kExpandBlock) k_nf_persistent(
     }
 }
 
+
+// ---- asynchronous near-far (thin graphs, non-negative weights) ----------
+// One cooperative launch; no grid-wide barrier per hop.  Improvements below
+// the threshold T go to ring queues (deduped by an in-queue flag), the rest
+// to a far pile.  Every block owns one ring -- vertex x belongs to ring
+// (x / 64) mod #blocks -- and its warps pop up to 32 entries at a time from
+// it (the head is a shared-memory counter of the block), expand them and
+// push their near improvements to the owners' rings (one tail atomic per
+// group of lanes with the same owner).  A shortest path thus advances one
+// hop per dependent round trip instead of one per grid-wide iteration
+// (k_nf_persistent: three grid barriers per iteration, 60% of its warp
+// samples stalled on them; a single global ring measured 0.37 s on cfg5a,
+// its warps queued on the head CAS).  `work` counts entries pushed and not
+// yet expanded (raised before a tail moves, lowered after the expansion's
+// own pushes): when it reaches zero the phase is drained; then (grid
+// barriers, once per phase) T grows by delta and the far pile is split.
+// Expansion order does not change the fixpoint: `dist` is bit-identical to
+// Bellman-Ford's.  In-queue protocol: a winner's atomicExch on inq[x] is
+// issued only after its atomicMin on dist[x] has returned; a popper clears
+// inq[v] with an atomicExch and its read of dist[v] depends on that
+// exchange's result -- so an improvement either re-queues v or is seen by
+// the popper (L2 operations only; a __threadfence would invalidate the SM's
+// L1 on every batch).
+struct AsyncNf {
+    int32_t *ring;                  // nring rings of (mask + 1) entries
+    unsigned long long *tails;      // ring r's tail at tails[r * kTailStride]
+    unsigned long long mask;
+    int nring;
+    alignas(128) long long work;
+    alignas(128) int32_t *far[2];
+    unsigned long long far_n[2];
+    unsigned long long fcap;
+    int fcur;
+    int go;
+    int abort;
+    int status;                     // 0 ok, 3 far-pile overflow, 4 watchdog
+    int64_t T, delta;
+    int64_t phases;
+    unsigned long long relaxed, expanded, batches;
+};
+
+constexpr int kAsyncBlock = 1024;  // launch bound; the launch uses kAsyncThreads
+constexpr int kAsyncThreads = 256;
+constexpr unsigned kAsyncBackoff = 256;
+constexpr int kTailStride = 16;    // one 128-byte line per ring tail
+constexpr int kOwnShift = 6;       // 64 consecutive vertices per ring chunk
+constexpr long long kAsyncWatchdog = 1ll << 35;  // cycles (~17 s): a hang becomes a fallback
+
+__device__ __forceinline__ int async_owner(int32_t x, int nring) {
+    return (int)((uint32_t)((uint32_t)x >> kOwnShift) % (uint32_t)nring);
+}
+
+// Push the lanes' near entries to their owners' rings, one tail atomic per
+// group of lanes with the same owner.  `work` must count an entry before its
+// tail moves: the split (counted = false) raises it here; an expansion batch
+// raised it by its slot count when the batch began (tok = that atomic's
+// result, lane 0: every tail atomic below depends on it, so it is issued only
+// after the raise was performed -- the raise itself overlapped the batch's
+// loads) and returns the surplus at the end.  Returns the entries pushed.
+__device__ __forceinline__ int async_push_near(AsyncNf *A, bool near, int32_t x, unsigned lane,
+                                               bool counted, unsigned long long tok = 0) {
+    const unsigned m = __ballot_sync(0xffffffffu, near);
+    if (!m) return 0;
+    if (!counted) {
+        if (lane == 0)
+            atomicAdd(reinterpret_cast<unsigned long long *>(&A->work),
+                      (unsigned long long)__popc(m));
+        __syncwarp();
+    }
+    tok = __shfl_sync(0xffffffffu, tok, 0);
+    if (near) {
+        const int r = async_owner(x, A->nring);
+        const unsigned grp = __match_any_sync(m, r);
+        const int leader = __ffs(grp) - 1;
+        unsigned long long pos = 0;
+        if ((int)lane == leader)
+            pos = atomicAdd(A->tails + (size_t)r * kTailStride + (tok == ~0ull ? 1 : 0),
+                            (unsigned long long)__popc(grp));
+        pos = __shfl_sync(grp, pos, leader) + __popc(grp & ((1u << lane) - 1u));
+        volatile int32_t *slot = A->ring + (size_t)r * (A->mask + 1) + (pos & A->mask);
+        bool ok = true;
+        while (*slot >= 0) {  // the previous lap's consumer has not cleared it yet
+            if (reinterpret_cast<volatile AsyncNf *>(A)->abort) {
+                ok = false;
+                break;
+            }
+        }
+        if (ok) *slot = x;
+    }
+    return __popc(m);
+}
+
+__device__ __forceinline__ void async_push_far(AsyncNf *A, int fc, bool far, int32_t x,
+                                               unsigned lane) {
+    const unsigned m = __ballot_sync(0xffffffffu, far);
+    if (!m) return;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(&A->far_n[fc], (unsigned long long)__popc(m));
+    pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
+    if (far && pos < A->fcap) A->far[fc][pos] = x;  // far_n still counts an overflow
+}
+
+__global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
+    int32_t *dist, int32_t *inq, int32_t *last, const int32_t *__restrict__ weff,
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, AsyncNf *A,
+    unsigned async_max_backoff) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned long long s_head;  // this block's ring: next entry to pop
+    if (threadIdx.x == 0) s_head = 0;
+    __syncthreads();
+    const unsigned lane = lane_id();
+    volatile AsyncNf *VA = A;
+    volatile unsigned long long *vhead = &s_head;
+    const unsigned long long mask = A->mask;
+    int32_t *myring = A->ring + (size_t)blockIdx.x * (mask + 1);
+    const volatile unsigned long long *mytail = A->tails + (size_t)blockIdx.x * kTailStride;
+    unsigned long long relaxed = 0, expanded = 0, batches = 0;
+    const long long t_start = clock64();
+    for (;;) {
+        const int64_t T = VA->T;  // fixed during a phase (written between barriers)
+        const int fc = VA->fcur;
+        // ---- drain the rings
+        unsigned backoff = 0;
+        for (;;) {
+            unsigned long long h0 = 0;
+            int k = 0;
+            long long w = 1;
+            int32_t v = -1;
+            if (lane == 0) {
+                const unsigned long long h = *vhead, t = *mytail;
+                if (h < t) {
+                    const unsigned long long want = min(t - h, 32ull);
+                    if (atomicCAS(&s_head, h, h + want) == h) {
+                        h0 = h;
+                        k = (int)want;
+                    } else {
+                        w = 1;  // lost the race: retry at once
+                    }
+                } else {
+                    w = VA->work;
+                    if (VA->abort) w = 0;
+                    else if (clock64() - t_start > kAsyncWatchdog) {
+                        A->abort = 1;
+                        A->status = 4;
+                        w = 0;
+                    }
+                }
+            }
+            k = __shfl_sync(0xffffffffu, k, 0);
+            if (k == 0) {
+                if (__shfl_sync(0xffffffffu, w, 0) == 0) break;
+                if (backoff) __nanosleep(backoff);
+                backoff = min(2u * backoff + 32u, async_max_backoff);
+                continue;
+            }
+            h0 = __shfl_sync(0xffffffffu, h0, 0);
+            backoff = 0;
+            batches++;
+            if ((int)lane < k) {
+                volatile int32_t *slot = myring + ((h0 + lane) & mask);
+                while ((v = *slot) < 0) {  // reserved by its producer, not yet written
+                    if (VA->abort) break;
+                }
+                if (v >= 0) *slot = -1;
+            }
+            int dv = 0;
+            int64_t beg = 0, deg = 0;
+            if (v >= 0) {
+                // row bounds and last[v] do not depend on the in-queue
+                // exchange: their loads overlap it
+                beg = off[v];
+                const int64_t end = off[v + 1];
+                const int lst = __ldcg(last + v);
+                // an improvement from here on re-queues v; the dist read
+                // depends on this exchange's result, so it is issued only
+                // after the exchange has been performed at L2
+                const int was = atomicExch(inq + v, 0);
+                const int32_t vd = was > 1 ? 0 : v;  // (was is 0 or 1) a real register dependency
+                dv = __ldcg(dist + vd);
+                if (dv < lst) {  // not yet expanded at this distance
+                    last[v] = dv;
+                    deg = end - beg;
+                    expanded++;
+                }
+            }
+            int64_t incl = deg;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane >= o) incl += t;
+            }
+            const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+            const int64_t excl = incl - deg;
+            // every slot may push one entry: count them all now (the atomic
+            // overlaps the slot loads), return the surplus at the end
+            unsigned long long tok = 0;
+            if (lane == 0) {
+                relaxed += total;
+                if (total)
+                    tok = atomicAdd(reinterpret_cast<unsigned long long *>(&A->work),
+                                    (unsigned long long)total);
+            }
+            long long pushed = 0;
+            for (int64_t p0 = 0; p0 < total; p0 += 32) {
+                const int64_t p = p0 + lane;
+                int lo = 0;  // owner lane: largest with excl <= p
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = lo + step;
+                    const int64_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+                    if (cand < 32 && ex <= p) lo = cand;
+                }
+                const int64_t ex = __shfl_sync(0xffffffffu, excl, lo);
+                const int64_t b0 = __shfl_sync(0xffffffffu, beg, lo);
+                const int du = __shfl_sync(0xffffffffu, dv, lo);
+                bool near = false, far = false;
+                int32_t x = -1;
+                if (p < total) {
+                    const int64_t e = b0 + (p - ex);
+                    x = __ldg(adj + e);
+                    const int64_t cand = (int64_t)du + (int64_t)__ldg(weff + e);
+                    // no pre-filter read of dist[x]: on these thin graphs the
+                    // atomic alone is one round trip less on the hop chain
+                    if (cand < (int64_t)kIntMax) {
+                        const int c = (int)cand;
+                        if (c < atomicMin(dist + x, c)) {
+                            if (cand < T)  // issued after the min returned
+                                near = atomicExch(inq + x, 1) == 0;
+                            else
+                                far = true;
+                        }
+                    }
+                }
+                pushed += async_push_near(A, near, x, lane, true, tok);
+                async_push_far(A, fc, far, x, lane);
+            }
+            __syncwarp();
+            if (lane == 0)  // expanded: the batch's k entries and the unused slot counts
+                atomicAdd(reinterpret_cast<unsigned long long *>(&A->work),
+                          (unsigned long long)(-(long long)(k + total - pushed)));
+        }
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // the phase is drained: next T
+            const int src = A->fcur;
+            const unsigned long long nf = A->far_n[src];
+            int go = 1;
+            A->phases++;
+            if (A->abort) {
+                go = 0;
+            } else if (nf > A->fcap) {
+                A->status = 3;
+                go = 0;
+            } else if (nf == 0) {
+                go = 0;
+            } else {
+                A->T += A->delta;
+                A->fcur = src ^ 1;
+                A->far_n[src ^ 1] = 0;
+            }
+            A->go = go;
+            __threadfence();
+        }
+        grid.sync();
+        if (!VA->go) break;
+        {   // split the old pile: below the new T and dropped since the last
+            // expansion -> rings (in-queue deduped); the rest -> the new pile
+            const int nfc = VA->fcur, src = nfc ^ 1;
+            const int64_t T2 = VA->T;
+            const int64_t nf = (int64_t)VA->far_n[src];
+            const int32_t *pile = A->far[src];
+            const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+            const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+            for (int64_t b = wid * 32; b < nf; b += nw * 32) {
+                const int64_t i = b + lane;
+                bool near = false, far = false;
+                int32_t x = -1;
+                if (i < nf) {
+                    x = pile[i];
+                    const int d = __ldcg(dist + x);
+                    if ((int64_t)d < T2) {
+                        near = d < __ldcg(last + x) && atomicExch(inq + x, 1) == 0;
+                    } else {
+                        far = true;
+                    }
+                }
+                async_push_near(A, near, x, lane, false);
+                async_push_far(A, nfc, far, x, lane);
+            }
+        }
+        grid.sync();
+    }
+    relaxed = warp_sum(relaxed);
+    expanded = warp_sum(expanded);
+    if (lane == 0) {
+        if (relaxed) atomicAdd(&A->relaxed, relaxed);
+        if (expanded) atomicAdd(&A->expanded, expanded);
+        if (batches) atomicAdd(&A->batches, batches);
+    }
+}
+
+__global__ void k_async_init(int32_t *inq, int32_t *ring, unsigned long long *tails, int64_t n,
+                             int64_t ring_total, int nring, int32_t src, int src_ring) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x)
+        inq[x] = x == src ? 1 : 0;
+    const int64_t per = ring_total / nring;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ring_total;
+         i += (int64_t)gridDim.x * blockDim.x)
+        ring[i] = i == (int64_t)src_ring * per ? src : -1;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nring;
+         r += (int64_t)gridDim.x * blockDim.x)
+        tails[r * kTailStride] = r == src_ring ? 1 : 0;
+}
+
+// The asynchronous near-far loop; SP_OK with out->status 3 asks the caller
+// for the Bellman-Ford fallback (far-pile overflow, or the watchdog).
+int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t *inq, int32_t src,
+                        int64_t delta, SsspLoop *out, float *kernel_ms) {
+    const int64_t n = g->n, m = g->m;
+    const int sms = num_sms(c.device);
+    const char *thr = getenv("SP_NF_ASYNC_THREADS");  // threads per block (sweeps)
+    const int threads = thr ? std::max(32, std::min(kAsyncBlock, atoi(thr) / 32 * 32))
+                            : kAsyncThreads;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nf_async, threads, 0);
+    const char *bps = getenv("SP_NF_ASYNC_BPS");  // blocks per SM (sweeps)
+    const int want = bps ? std::max(1, atoi(bps)) : kAsyncBlocksPerSm;
+    const int nring = sms * std::max(1, std::min(per_sm, want));  // one ring per block
+    const char *bo = getenv("SP_NF_ASYNC_BACKOFF");   // max idle backoff, ns (sweeps)
+    unsigned max_backoff = bo ? (unsigned)atoi(bo) : kAsyncBackoff;
+    // a ring holds each of its vertices at most once (in-queue flag) plus
+    // entries reserved but not yet cleared: twice its share is ample
+    const int64_t chunks = (n + (1 << kOwnShift) - 1) >> kOwnShift;
+    const int64_t owned = ((chunks + nring - 1) / nring) << kOwnShift;
+    unsigned long long cap = 1;
+    while (cap < (unsigned long long)(2 * owned + 4096)) cap <<= 1;
+    const int64_t fcap = 2 * m + n + 16;
+    int32_t *last, *fa, *fb, *ring;
+    unsigned long long *tails;
+    AsyncNf *A;
+    SP_TRY(c.alloc(&last, n));
+    SP_TRY(c.alloc(&fa, fcap));
+    SP_TRY(c.alloc(&fb, fcap));
+    SP_TRY(c.alloc(&ring, cap * nring));
+    SP_TRY(c.alloc(&tails, (size_t)nring * kTailStride));
+    SP_TRY(c.alloc(&A, 1));
+    k_fill_i32<<<grid_for(n, kBlock, c.device), kBlock, 0, c.stream>>>(last, n, kIntMax);
+    const int src_ring = (int)(((uint32_t)src >> kOwnShift) % (uint32_t)nring);
+    k_async_init<<<grid_for((int64_t)(cap * nring), kBlock, c.device), kBlock, 0, c.stream>>>(
+        inq, ring, tails, n, (int64_t)(cap * nring), nring, src, src_ring);
+    c.launches += 2;
+    AsyncNf init{};
+    init.ring = ring;
+    init.tails = tails;
+    init.mask = cap - 1;
+    init.nring = nring;
+    init.work = 1;  // the source
+    init.far[0] = fa;
+    init.far[1] = fb;
+    init.fcap = (unsigned long long)fcap;
+    init.T = delta;
+    init.delta = delta;
+    SP_CUDA(cudaMemcpyAsync(A, &init, sizeof(AsyncNf), cudaMemcpyHostToDevice, c.stream));
+    void *kargs[] = {&dist, &inq, &last, (void *)&g->weff, (void *)&g->off, (void *)&g->adj, &A,
+                     &max_backoff};
+    cudaEvent_t ka, kb;
+    SP_CUDA(cudaEventCreate(&ka));
+    SP_CUDA(cudaEventCreate(&kb));
+    cudaEventRecord(ka, c.stream);
+    SP_CUDA(cudaLaunchCooperativeKernel((const void *)k_nf_async, nring, threads, kargs, 0,
+                                        c.stream));
+    cudaEventRecord(kb, c.stream);
+    AsyncNf *hA;
+    SP_TRY(c.host_as(&hA));
+    SP_CUDA(cudaMemcpyAsync(hA, A, sizeof(AsyncNf), cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    cudaEventElapsedTime(kernel_ms, ka, kb);
+    cudaEventDestroy(ka);
+    cudaEventDestroy(kb);
+    if (hA->status == 4)
+        fprintf(stderr, "starplat_b200: asynchronous near-far SSSP hit its watchdog; "
+                        "falling back to Bellman-Ford\n");
+    static const bool trace = getenv("SP_SSSP_TRACE") != nullptr;
+    if (trace)
+        fprintf(stderr, "sssp async: %d blocks x %d threads, %lld phases, %llu batches, "
+                        "%llu expansions, %llu relaxations, %.2f ms\n", nring, threads,
+                (long long)hA->phases, hA->batches, hA->expanded, hA->relaxed, *kernel_ms);
+    out->iters = hA->phases;
+    out->relaxed = (int64_t)hA->relaxed;
+    out->frontier_sum = (int64_t)hA->expanded;
+    out->status = hA->status == 0 ? 0 : 3;
+    c.launches += 1;
+    return SP_OK;
+}
+
 int sssp_near_far(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
                   ChunkItem *chunks, int64_t cap, int64_t delta, SsspLoop *out, float *kernel_ms) {
     const int64_t n = g->n, m = g->m;
@@ -556,11 +953,15 @@ struct DoLoop {
     int mode;              // 0 push, 1 pull (this iteration)
     int next_mode;
     int conv;              // after advance: 1 queue->bits, 2 bits->queue
+    int go;                // the advance's loop decision (host-driven diagnostic loop)
 };
 
 constexpr int kPullChunk = 128;
 constexpr int64_t kPullHub = 1024;
-constexpr int64_t kPullDiv = 8;   // pull when the frontier exceeds n / kPullDiv (4-12 measured alike)
+constexpr int64_t kPullDiv = 8;   // pull when the frontier exceeds n / kPullDiv (4-12 measured alike);
+// a test on the frontier's out-slots (pull iteration 2 on RMAT-24, whose
+// 0.24 M hub neighbours hold ~140 M out-slots) measured slower: 5.25 -> 9.4 ms,
+// the earlier pull leaves larger frontiers and two more sweeps
 // Push-form SSSP uses the direction-optimising loop on graphs this large
 // (RMAT-24: 5.95 -> 5.55 ms; at RMAT-22 the two loops tie, at cfg1 the
 // extra per-iteration kernels cost more than the pull saves)
@@ -899,7 +1300,7 @@ __global__ void __launch_bounds__(kExpandBlock, 3) k_do_push_chunks(
 }
 
 // Totals, termination, and the direction of the next iteration.
-__global__ void k_do_advance(DoLoop *D, cudaGraphConditionalHandle h) {
+__global__ void k_do_advance(DoLoop *D, cudaGraphConditionalHandle h, int set_cond) {
     SsspLoop *L = &D->s;
     const int cur = L->cur;
     const ExpandCounters c = L->cnt[cur];
@@ -932,7 +1333,8 @@ __global__ void k_do_advance(DoLoop *D, cudaGraphConditionalHandle h) {
     L->cur = cur ^ 1;
     L->nq = next;
     L->it = (int)(L->iters + 1);
-    cudaGraphSetConditional(h, go);
+    D->go = go;
+    if (set_cond) cudaGraphSetConditional(h, go);
 }
 
 // Zero the bitmap the next pull writes (and the frontier bitmap a
@@ -1051,6 +1453,64 @@ int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa,
             if (*g) cudaGraphDestroy(*g);
         }
     } gf{&graph};
+    // body of one iteration (set_cond: inside the conditional graph)
+    auto body_launch = [&](cudaGraphConditionalHandle hh, int set_cond) {
+        k_do_push<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off, g->adj, chunks,
+                                                       D, warps);
+        if (big)
+            k_do_push_chunks<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off,
+                                                                  g->adj, chunks, D);
+        if (units) {
+            k_spull_units<<<(int)std::max<int64_t>(1, (sp.nunits + 7) / 8), 256, 0, c.stream>>>(
+                sp, dist, D);
+            k_spull_fix<<<grid_for(sp.nunits, 256, c.device), 256, 0, c.stream>>>(sp, dist, D);
+        } else {
+            k_pull_tiles<<<grid, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
+            k_pull_hubs<<<sms * 2, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
+        }
+        k_do_advance<<<1, 1, 0, c.stream>>>(D, hh, set_cond);
+        k_do_clear<<<grid, 256, 0, c.stream>>>(D);
+        k_do_convert<<<grid, 256, 0, c.stream>>>(D);
+        k_do_mode<<<1, 1, 0, c.stream>>>(D);
+    };
+    // SP_HOSTLOOP=2: host-driven iterations of this loop with per-iteration
+    // device times (SP_SSSP_TRACE prints them; ncu can profile every kernel)
+    const char *hl = getenv("SP_HOSTLOOP");
+    if (hl && hl[0] == '2') {
+        static const bool tr = getenv("SP_SSSP_TRACE") != nullptr;
+        DoLoop *hD;
+        SP_TRY(c.host_as(&hD));
+        cudaEvent_t e0, e1;
+        SP_CUDA(cudaEventCreate(&e0));
+        SP_CUDA(cudaEventCreate(&e1));
+        float tot = 0.f;
+        for (;;) {
+            SP_CUDA(cudaMemcpyAsync(hD, D, sizeof(DoLoop), cudaMemcpyDeviceToHost, c.stream));
+            SP_CUDA(cudaStreamSynchronize(c.stream));
+            const int mode = hD->mode;
+            const int64_t nq = hD->s.nq;
+            cudaEventRecord(e0, c.stream);
+            body_launch(0, 0);
+            cudaEventRecord(e1, c.stream);
+            SP_CUDA(cudaGetLastError());
+            SP_CUDA(cudaMemcpyAsync(hD, D, sizeof(DoLoop), cudaMemcpyDeviceToHost, c.stream));
+            SP_CUDA(cudaStreamSynchronize(c.stream));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            tot += ms;
+            if (tr)
+                fprintf(stderr, "sssp do it %lld: %s frontier %lld -> %lld, %.3f ms\n",
+                        (long long)hD->s.iters, mode ? "pull" : "push", (long long)nq,
+                        (long long)hD->s.nq, ms);
+            if (!hD->go) break;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *kernel_ms = tot;
+        *out = hD->s;
+        c.launches += hD->s.iters * (big ? 8 : 7);
+        return SP_OK;
+    }
     SP_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle h;
     SP_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
@@ -1064,23 +1524,7 @@ int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa,
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
                                           cudaStreamCaptureModeThreadLocal));
-    k_do_push<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off, g->adj, chunks, D,
-                                                   warps);
-    if (big)
-        k_do_push_chunks<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off, g->adj,
-                                                              chunks, D);
-    if (units) {
-        k_spull_units<<<(int)std::max<int64_t>(1, (sp.nunits + 7) / 8), 256, 0, c.stream>>>(
-            sp, dist, D);
-        k_spull_fix<<<grid_for(sp.nunits, 256, c.device), 256, 0, c.stream>>>(sp, dist, D);
-    } else {
-        k_pull_tiles<<<grid, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
-        k_pull_hubs<<<sms * 2, 256, 0, c.stream>>>(g->roff, g->radj, g->rweff, dist, D);
-    }
-    k_do_advance<<<1, 1, 0, c.stream>>>(D, h);
-    k_do_clear<<<grid, 256, 0, c.stream>>>(D);
-    k_do_convert<<<grid, 256, 0, c.stream>>>(D);
-    k_do_mode<<<1, 1, 0, c.stream>>>(D);
+    body_launch(h, 1);
     SP_CUDA(cudaStreamEndCapture(c.stream, &body));
     cudaEvent_t ka, kb;
     SP_CUDA(cudaEventCreate(&ka));
@@ -1233,7 +1677,15 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
             wr[1] = g->wmax_h;
         }
         const int64_t delta = pull_form ? 0 : near_far_delta(g, wr[0], wr[1]);
-        if (delta > 0)
+        // the asynchronous form counts phases, not iterations: it runs when
+        // no caller cap is in force (the reference default 2n+16, which no
+        // near-far run approaches) and the graph is thin (SP_NF_ASYNC=0: off)
+        const char *ae = getenv("SP_NF_ASYNC");
+        const bool async_nf = delta > 0 && g->max_outdeg <= kSplit && cap >= 2 * n + 16 &&
+                              !(ae && ae[0] == '0');
+        if (async_nf)
+            lrc = sssp_near_far_async(g, c, dist, enq, src, delta, &hL, &kernel_ms);
+        else if (delta > 0)
             lrc = sssp_near_far(g, c, dist, enq, qa, qb, chunks, cap, delta, &hL, &kernel_ms);
         if (trace) fprintf(stderr, "sssp: loop done %.2f ms (kernel %.2f ms)\n", tms(), kernel_ms);
         if (delta <= 0 || (lrc == SP_OK && hL.status == 3)) {  // Bellman-Ford

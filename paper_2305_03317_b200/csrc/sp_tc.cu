@@ -26,8 +26,9 @@
 // memory with a 4096-bit membership filter, then walks all rows N+(b) as one
 // flattened space of 16-byte half-sectors: each lane loads one int4 per step
 // and keeps kUnroll independent loads in flight (the walk is DRAM-latency
-// bound otherwise); the row of a half-sector is one shared-memory binary
-// search, amortised over its 4 slots.  Every element costs one
+// bound otherwise); the rows of a block of 32U half-sectors come from a
+// bitmap of the row starts inside it (walk_owners: U shared loads, U+1
+// warp OR/add reductions and a popcount per lane).  Every element costs one
 // shared-memory filter probe and, on a hit, a binary search in A for its
 // multiplicity.  Counts: per-lane uint64 -> warp sum -> one atomicAdd per
 // warp.
@@ -117,6 +118,64 @@ __device__ __forceinline__ void stage_a(const int32_t *__restrict__ adj, int64_t
 
 __device__ __forceinline__ bool rank_gt(int32_t dx, int32_t x, int32_t dv, int32_t v) {
     return dx > dv || (dx == dv && x > v);
+}
+
+// Append the non-empty rows of one 32-row staging chunk (lane: sector start
+// s8, `secs` element-holding half-sectors) to B/S at nr; returns the new
+// running half-sector total (nr and the total are warp-uniform).
+__device__ __forceinline__ int stage_rows(uint32_t *B, int32_t *S, int &nr, int carry,
+                                          uint32_t s8, int secs, unsigned lane) {
+    int incl = secs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl += t;
+    }
+    const unsigned keep = __ballot_sync(0xffffffffu, secs > 0);
+    if (secs > 0) {
+        const int at = nr + __popc(keep & ((1u << lane) - 1u));
+        B[at] = s8;
+        S[at] = carry + incl - secs;
+    }
+    nr += __popc(keep);
+    return carry + __shfl_sync(0xffffffffu, incl, 31);
+}
+
+// Rows owning the half-sectors h0 + 32u + lane (u < U) of a flattened walk
+// over rows whose first half-sectors S[0..nr) strictly increase (S[0] = 0,
+// S[nr] = the total; empty rows are not listed).  r = the row holding h0
+// (warp-uniform), advanced to the row holding h0 + 32U.  The at most 32U
+// rows starting inside the block are read with U independent conflict-free
+// shared loads per lane and OR-reduced into a 32U-bit start bitmap; a
+// lane's owner is then a popcount -- instead of U independent log2(nr)-step
+// binary searches (~30% of the skewed-graph walk's instructions).
+template <int U>
+__device__ __forceinline__ void walk_owners(const int32_t *S, int nr, int h0, int &r,
+                                            unsigned lane, int (&own)[U]) {
+    unsigned words[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) words[u] = 0u;
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < U; j++) {
+        const int c = r + 1 + j * 32 + (int)lane;
+        const int off = (c <= nr ? S[c] : 0x7fffffff) - h0;  // >= 1
+        cnt += off <= 32 * U ? 1 : 0;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int b = off - 32 * u;
+            words[u] |= (b >= 0 && b < 32) ? (1u << b) : 0u;
+        }
+    }
+    const unsigned le = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+    int base = r;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const unsigned w = __reduce_or_sync(0xffffffffu, words[u]);
+        own[u] = base + __popc(w & le);
+        base += __popc(w);
+    }
+    r += (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
 }
 
 // ---- upper CSR build (undirected) -------------------------------------
@@ -353,30 +412,24 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
             // ---- stage A, row starts, half-sector prefix and filter
             for (int k = lane; k < kFilterWords; k += 32) F[k] = 0u;
             __syncwarp();
-            int carry = 0;
+            int carry = 0, nr = 0;
             for (int k0 = 0; k0 < na; k0 += 32) {
                 const int k = k0 + lane;
                 int secs = 0;
+                uint32_t s8 = 0;
                 if (k < na) {
                     const int32_t x = uadj[r0 + k];
                     const uint2 inf = uinfo[r0 + k];
                     A[k] = x;
-                    B[k] = inf.x;
+                    s8 = inf.x;
                     secs = (int)((inf.y + 3u) / 4u);  // half-sectors holding elements
                     elems += inf.y;
                     const uint32_t hh = fhash(x);
                     atomicOr(&F[hh >> 5], 1u << (hh & 31));
                 }
-                int incl = secs;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if ((int)lane >= o) incl += t;
-                }
-                if (k < na) S[k] = carry + incl - secs;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
+                carry = stage_rows(B, S, nr, carry, s8, secs, lane);
             }
-            if (lane == 0) S[na] = carry;
+            if (lane == 0) S[nr] = carry;
             __syncwarp();
             // ---- flattened walk of all rows b_j in 16-byte half-sectors:
             // one int4 per lane (rows are 32-byte aligned and padded with -1),
@@ -389,7 +442,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
                     const int h = h0 + u * 32 + (int)lane;
                     xs[u] = make_int4(-1, -1, -1, -1);
                     if (h < nhalf) {
-                        int lo = 0, hi = na;  // last j with S[j] <= h
+                        // short rows (uniform graphs): a few-step binary search
+                        // beats walk_owners here (cfg3: 8.53 vs 8.75 ms)
+                        int lo = 0, hi = nr;  // last j with S[j] <= h
                         while (hi - lo > 1) {
                             const int mid = (lo + hi) >> 1;
                             if (S[mid] <= h) lo = mid; else hi = mid;
@@ -472,10 +527,11 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
             for (int k = lane; k < T; k += 32) HK[k] = -1;
             for (int k = lane; k < T / 2; k += 32) HC[k] = 0u;
             __syncwarp();
-            int carry = 0;
+            int carry = 0, nr = 0;
             for (int k0 = 0; k0 < na; k0 += 32) {
                 const int k = k0 + lane;
                 int secs = 0;
+                uint32_t s8 = 0;
                 if (k < na) {
                     const int32_t x = uadj[r0 + k];
                     const uint2 inf = uinfo[r0 + k];
@@ -488,42 +544,32 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
                         }
                         h = (h + 1) & (T - 1);
                     }
-                    B[k] = inf.x;
+                    s8 = inf.x;
                     secs = (int)((inf.y + 3u) / 4u);  // half-sectors holding elements
                     elems += inf.y;
                     const uint32_t hh = fhash(x);
                     atomicOr(&F[hh >> 5], 1u << (hh & 31));
                 }
-                int incl = secs;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if ((int)lane >= o) incl += t;
-                }
-                if (k < na) S[k] = carry + incl - secs;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
+                carry = stage_rows(B, S, nr, carry, s8, secs, lane);
             }
-            if (lane == 0) S[na] = carry;
+            if (lane == 0) S[nr] = carry;
             __syncwarp();
             // ---- flattened walk of all rows b_j in 16-byte half-sectors:
             // one int4 per lane (rows are 32-byte aligned and padded with -1),
             // kUnrollHash loads in flight per lane, one row search per 4 slots
             const int nhalf = carry;
+            int row = 0;
             for (int h0 = 0; h0 < nhalf; h0 += 32 * kUnrollHash) {
                 int4 xs[kUnrollHash];
+                int own[kUnrollHash];
+                walk_owners<kUnrollHash>(S, nr, h0, row, lane, own);
 #pragma unroll
                 for (int u = 0; u < kUnrollHash; u++) {
                     const int h = h0 + u * 32 + (int)lane;
                     xs[u] = make_int4(-1, -1, -1, -1);
-                    if (h < nhalf) {
-                        int lo = 0, hi = na;  // last j with S[j] <= h
-                        while (hi - lo > 1) {
-                            const int mid = (lo + hi) >> 1;
-                            if (S[mid] <= h) lo = mid; else hi = mid;
-                        }
+                    if (h < nhalf)
                         xs[u] = __ldg(reinterpret_cast<const int4 *>(uadj) +
-                                      kQ * (int64_t)B[lo] + (h - S[lo]));
-                    }
+                                      kQ * (int64_t)B[own[u]] + (h - S[own[u]]));
                 }
 #pragma unroll
                 for (int u = 0; u < kUnrollHash; u++) {
@@ -568,7 +614,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
 // search), or for longer rows stages A (up to kBigMax) with a
 // kBigFilterBits filter; each warp takes 32 of A's b's at a time, loads
 // their row descriptors with one coalesced read, and walks the flattened
-// 16-byte half-sectors of their rows (owner by a 5-step shuffle search),
+// 16-byte half-sectors of their rows (owner from a window bitmap of row starts),
 // one filter probe per element and a shared-memory binary search on a hit.
 constexpr int kBigFilterBits = 1 << 17;  // 16 KB
 constexpr int kBigFilterShift = 32 - 17;
@@ -599,6 +645,8 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
     // assignment keeps the hub tail short on skewed graphs.
     __shared__ long long s_bi;
     __shared__ int s_j;
+    __shared__ uint8_t s_wl[kBigBlock / 32][32];  // per warp: non-empty row rank -> lane
+    uint8_t *WL = s_wl[threadIdx.x >> 5];
     for (;;) {
         __syncthreads();  // every warp is done with the previous vertex
         if (threadIdx.x == 0) {
@@ -679,15 +727,22 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
             }
             const int excl = incl - secs;
             const int nhalf = __shfl_sync(0xffffffffu, incl, 31);
+            // owner of a half-sector: rank among the non-empty rows from a
+            // bitmap of the row starts inside its 32-half-sector window, then
+            // rank -> lane through a per-warp table (one ballot, one OR-reduce,
+            // one shared load instead of a 5-step shuffle search)
+            const bool ne = secs > 0;
+            const unsigned nem = __ballot_sync(0xffffffffu, ne);
+            if (ne) WL[__popc(nem & ((1u << lane) - 1u))] = (uint8_t)lane;
+            __syncwarp();
+            const unsigned le = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
             for (int h0 = 0; h0 < nhalf; h0 += 32) {
                 const int h = h0 + (int)lane;
-                int lo = 0;  // owner lane: largest with excl <= h
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1) {
-                    const int cand = lo + step;
-                    const int ex = __shfl_sync(0xffffffffu, excl, cand & 31);
-                    if (cand < 32 && ex <= h) lo = cand;
-                }
+                const int r0 = __popc(__ballot_sync(0xffffffffu, ne && excl <= h0)) - 1;
+                const int off = excl - h0;
+                const unsigned bits =
+                    __reduce_or_sync(0xffffffffu, (ne && off >= 1 && off <= 31) ? (1u << off) : 0u);
+                const int lo = WL[r0 + __popc(bits & le)];
                 const int ex = __shfl_sync(0xffffffffu, excl, lo);
                 const uint32_t s8 = __shfl_sync(0xffffffffu, inf.x, lo);
                 if (h >= nhalf) continue;
@@ -719,6 +774,7 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
                     }
                 }
             }
+            __syncwarp();  // WL is rewritten for the next 32 rows
         }
     }
     cnt = warp_sum(cnt);

@@ -179,6 +179,31 @@ def test_sssp_seeded(kind, p0, p1, und):
             np.testing.assert_array_equal(r.env.node_props["dist"], dist)
 
 
+@pytest.mark.parametrize("kind,p0,p1,und,delta", [
+    ("grid", 300, 280, True, None), ("grid", 512, 512, True, "40"), ("grid", 97, 1031, True, None),
+    ("uniform", 1 << 16, 1 << 18, True, None), ("uniform", 1 << 16, 1 << 18, False, "7"),
+    ("grid", 64, 64, True, "0")])
+def test_sssp_async_near_far_stress(kind, p0, p1, und, delta, monkeypatch):
+    """The asynchronous near-far loop (thin graphs, non-negative weights, no
+    caller cap): per-block rings, in-queue flags, phase splits -- racy by
+    design, so every graph runs several times, with small and large delta
+    (many / few phases; "0" = Bellman-Ford, the reference form), against
+    the oracle's dist bit for bit; the synchronous near-far kernel
+    (SP_NF_ASYNC=0) gives the same dist."""
+    if delta is not None:
+        monkeypatch.setenv("SP_SSSP_DELTA", delta)
+    g, o = _pair(kind, p0, p1, 23, und)
+    for s in (0, g.n // 3):
+        dist, _, rc = cpu_ref.sssp(o, s)
+        assert rc == 0
+        for rep in range(4):
+            r = sp.run(corpus.SSSP, g, {"src": s})
+            np.testing.assert_array_equal(r.env.node_props["dist"], dist, err_msg=f"rep {rep}")
+    monkeypatch.setenv("SP_NF_ASYNC", "0")
+    r = sp.run(corpus.SSSP, g, {"src": 0})
+    np.testing.assert_array_equal(r.env.node_props["dist"], cpu_ref.sssp(o, 0)[0])
+
+
 @pytest.mark.parametrize("pull_div", ["8", "1000000"])
 @pytest.mark.parametrize("graph", ["rmat_dir", "rmat_sym", "hub", "multi", "neg_dag"])
 def test_sssp_direction_optimising(graph, pull_div, monkeypatch):

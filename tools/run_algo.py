@@ -1,5 +1,6 @@
 """Run one corpus program on a BASELINE config graph (profiling driver).
 usage: python tools/run_algo.py {sssp,pr,bc,tc} [reps] [nsrc]"""
+import os
 import sys
 import time
 
@@ -35,12 +36,24 @@ elif algo == "bc":
     deg = np.diff(np.asarray(g.offsets))
     srcs = np.random.default_rng(1).choice(np.flatnonzero(deg > 0), size=256, replace=False)
     prog, args = corpus.BC, {"sourceSet": srcs[:nsrc].tolist()}
+elif algo == "sssp_grid_pr":
+    g = sp.generate("grid", 4096, 4096, seed=1)
+    prog, args = corpus.PR, {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
 elif algo == "tc":
     g = sp.generate("uniform", 1 << 24, 1 << 28, seed=1, undirected=True)
     prog, args = corpus.TC, {}
+nvtx = os.environ.get("SP_NVTX") == "1"  # the last rep inside an NVTX range "steady"
+if nvtx:
+    import torch
 for i in range(reps):
+    last = i == reps - 1
+    if nvtx and last:
+        torch.cuda.nvtx.range_push("steady")
     t0 = time.perf_counter()
     r = sp.run(prog, g, args, device_outputs=True)
+    if nvtx and last:
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     print(f"{algo} rep {i}: wall {(time.perf_counter() - t0) * 1e3:.2f} ms, device "
           f"{r.stats['device_ms']:.2f} ms, launches {r.stats['kernel_launches']}, "
           f"edges {r.stats['edges_visited']}, vertices {r.stats['vertices_visited']}, "
