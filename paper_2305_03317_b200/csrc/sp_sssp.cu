@@ -432,30 +432,32 @@ __global__ void __launch_bounds__(kExpandBlock) k_nf_persistent(
 
 // ---- asynchronous near-far (thin graphs, non-negative weights) ----------
 // One cooperative launch; no grid-wide barrier per hop.  Improvements below
-// the threshold T go to ring queues (deduped by an in-queue flag), the rest
-// to a far pile.  Every block owns one ring -- vertex x belongs to ring
-// (x / 64) mod #blocks -- and its warps pop up to 32 entries at a time from
-// it (the head is a shared-memory counter of the block), expand them and
-// push their near improvements to the owners' rings (one tail atomic per
-// group of lanes with the same owner).  A shortest path thus advances one
-// hop per dependent round trip instead of one per grid-wide iteration
+// the threshold T go to ring queues, the rest to a far pile.  Every block
+// owns one ring -- vertex x belongs to ring (x / 64) mod #blocks -- whose
+// head is a shared-memory counter of the block; its warps pop up to 32
+// consecutive published entries at a time, expand them and push their near
+// improvements to the owners' rings (one tail atomic per group of lanes
+// with the same owner).  A shortest path thus advances one hop per
+// dependent round trip instead of one per grid-wide iteration
 // (k_nf_persistent: three grid barriers per iteration, 60% of its warp
 // samples stalled on them; a single global ring measured 0.37 s on cfg5a,
-// its warps queued on the head CAS).  `work` counts entries pushed and not
-// yet expanded (raised before a tail moves, lowered after the expansion's
-// own pushes): when it reaches zero the phase is drained; then (grid
-// barriers, once per phase) T grows by delta and the far pile is split.
-// Expansion order does not change the fixpoint: `dist` is bit-identical to
-// Bellman-Ford's.  In-queue protocol: a winner's atomicExch on inq[x] is
-// issued only after its atomicMin on dist[x] has returned; a popper clears
-// inq[v] with an atomicExch and its read of dist[v] depends on that
-// exchange's result -- so an improvement either re-queues v or is seen by
-// the popper (L2 operations only; a __threadfence would invalidate the SM's
-// L1 on every batch).
+// its warps queued on the head CAS).
+//   dq[v] = dist << 1 | queued: one atomicMin both lowers the distance and
+//   marks the vertex queued, and its old value says whether the winner must
+//   push it (the queued bit was clear); a popper's atomicAnd clears the bit
+//   and returns the distance to expand with -- so an improvement either
+//   re-queues v or is seen by the popper, with no separate flag round trip.
+//   `work` counts entries pushed and not yet expanded (a batch raises it by
+//   its slot count before any of its pushes and returns the surplus after):
+//   zero means the phase is drained.  Then (grid barriers, once per phase)
+//   T grows by delta, every ring restarts at 0 (no lap: a phase that
+//   overflows a ring aborts to the synchronous kernel) and the far pile is
+//   split.  Expansion order does not change the fixpoint: `dist` is
+//   bit-identical to Bellman-Ford's.
 struct AsyncNf {
-    int32_t *ring;                  // nring rings of (mask + 1) entries
+    int32_t *ring;                  // nring rings of cap entries
     unsigned long long *tails;      // ring r's tail at tails[r * kTailStride]
-    unsigned long long mask;
+    unsigned long long cap;
     int nring;
     alignas(128) long long work;
     alignas(128) int32_t *far[2];
@@ -464,7 +466,7 @@ struct AsyncNf {
     int fcur;
     int go;
     int abort;
-    int status;                     // 0 ok, 3 far-pile overflow, 4 watchdog
+    int status;                     // 0 ok, 3 far-pile / ring overflow, 4 watchdog
     int64_t T, delta;
     int64_t phases;
     unsigned long long relaxed, expanded, batches;
@@ -481,13 +483,18 @@ __device__ __forceinline__ int async_owner(int32_t x, int nring) {
     return (int)((uint32_t)((uint32_t)x >> kOwnShift) % (uint32_t)nring);
 }
 
+__device__ __forceinline__ void async_fail(AsyncNf *A, int status) {
+    A->status = status;
+    A->abort = 1;
+}
+
 // Push the lanes' near entries to their owners' rings, one tail atomic per
 // group of lanes with the same owner.  `work` must count an entry before its
 // tail moves: the split (counted = false) raises it here; an expansion batch
 // raised it by its slot count when the batch began (tok = that atomic's
-// result, lane 0: every tail atomic below depends on it, so it is issued only
-// after the raise was performed -- the raise itself overlapped the batch's
-// loads) and returns the surplus at the end.  Returns the entries pushed.
+// result in lane 0: every tail atomic below depends on it, so it is issued
+// only after the raise was performed -- the raise itself overlapped the
+// batch's loads).  Returns the entries pushed.
 __device__ __forceinline__ int async_push_near(AsyncNf *A, bool near, int32_t x, unsigned lane,
                                                bool counted, unsigned long long tok = 0) {
     const unsigned m = __ballot_sync(0xffffffffu, near);
@@ -508,15 +515,10 @@ __device__ __forceinline__ int async_push_near(AsyncNf *A, bool near, int32_t x,
             pos = atomicAdd(A->tails + (size_t)r * kTailStride + (tok == ~0ull ? 1 : 0),
                             (unsigned long long)__popc(grp));
         pos = __shfl_sync(grp, pos, leader) + __popc(grp & ((1u << lane) - 1u));
-        volatile int32_t *slot = A->ring + (size_t)r * (A->mask + 1) + (pos & A->mask);
-        bool ok = true;
-        while (*slot >= 0) {  // the previous lap's consumer has not cleared it yet
-            if (reinterpret_cast<volatile AsyncNf *>(A)->abort) {
-                ok = false;
-                break;
-            }
-        }
-        if (ok) *slot = x;
+        if (pos < A->cap)
+            reinterpret_cast<volatile int32_t *>(A->ring)[(size_t)r * A->cap + pos] = x;
+        else
+            async_fail(A, 3);  // the ring overflowed within a phase
     }
     return __popc(m);
 }
@@ -532,7 +534,7 @@ __device__ __forceinline__ void async_push_far(AsyncNf *A, int fc, bool far, int
 }
 
 __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
-    int32_t *dist, int32_t *inq, int32_t *last, const int32_t *__restrict__ weff,
+    unsigned long long *dq, int32_t *last, const int32_t *__restrict__ weff,
     const int64_t *__restrict__ off, const int32_t *__restrict__ adj, AsyncNf *A,
     unsigned async_max_backoff) {
     namespace cg = cooperative_groups;
@@ -543,9 +545,8 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
     const unsigned lane = lane_id();
     volatile AsyncNf *VA = A;
     volatile unsigned long long *vhead = &s_head;
-    const unsigned long long mask = A->mask;
-    int32_t *myring = A->ring + (size_t)blockIdx.x * (mask + 1);
-    const volatile unsigned long long *mytail = A->tails + (size_t)blockIdx.x * kTailStride;
+    const unsigned long long cap = A->cap;
+    volatile int32_t *myring = A->ring + (size_t)blockIdx.x * cap;
     unsigned long long relaxed = 0, expanded = 0, batches = 0;
     const long long t_start = clock64();
     for (;;) {
@@ -554,61 +555,45 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
         // ---- drain the rings
         unsigned backoff = 0;
         for (;;) {
-            unsigned long long h0 = 0;
-            int k = 0;
-            long long w = 1;
-            int32_t v = -1;
-            if (lane == 0) {
-                const unsigned long long h = *vhead, t = *mytail;
-                if (h < t) {
-                    const unsigned long long want = min(t - h, 32ull);
-                    if (atomicCAS(&s_head, h, h + want) == h) {
-                        h0 = h;
-                        k = (int)want;
-                    } else {
-                        w = 1;  // lost the race: retry at once
-                    }
-                } else {
+            // poll the slots after the head: the published entries are the
+            // ones already written (a reserved slot still reads -1)
+            const unsigned long long h = *vhead;
+            const int32_t sv = h + lane < cap ? myring[h + lane] : -1;
+            const unsigned pub = __ballot_sync(0xffffffffu, sv >= 0);
+            const int k = __ffs(~pub) - 1 < 0 ? 32 : __ffs(~pub) - 1;  // consecutive from h
+            if (k == 0) {
+                long long w = 1;
+                if (lane == 0) {
                     w = VA->work;
-                    if (VA->abort) w = 0;
-                    else if (clock64() - t_start > kAsyncWatchdog) {
-                        A->abort = 1;
-                        A->status = 4;
+                    if (VA->abort) {
+                        w = 0;
+                    } else if (clock64() - t_start > kAsyncWatchdog) {
+                        async_fail(A, 4);
                         w = 0;
                     }
                 }
-            }
-            k = __shfl_sync(0xffffffffu, k, 0);
-            if (k == 0) {
                 if (__shfl_sync(0xffffffffu, w, 0) == 0) break;
                 if (backoff) __nanosleep(backoff);
                 backoff = min(2u * backoff + 32u, async_max_backoff);
                 continue;
             }
-            h0 = __shfl_sync(0xffffffffu, h0, 0);
+            int won = 0;
+            if (lane == 0) won = atomicCAS(&s_head, h, h + k) == h;
+            if (!__shfl_sync(0xffffffffu, won, 0)) continue;  // another warp took them
             backoff = 0;
             batches++;
-            if ((int)lane < k) {
-                volatile int32_t *slot = myring + ((h0 + lane) & mask);
-                while ((v = *slot) < 0) {  // reserved by its producer, not yet written
-                    if (VA->abort) break;
-                }
-                if (v >= 0) *slot = -1;
-            }
+            int32_t v = (int)lane < k ? sv : -1;
+            if (v >= 0) myring[h + lane] = -1;  // the slot is reused next phase
             int dv = 0;
             int64_t beg = 0, deg = 0;
             if (v >= 0) {
-                // row bounds and last[v] do not depend on the in-queue
-                // exchange: their loads overlap it
+                // row bounds and last[v] overlap the exchange
                 beg = off[v];
                 const int64_t end = off[v + 1];
                 const int lst = __ldcg(last + v);
-                // an improvement from here on re-queues v; the dist read
-                // depends on this exchange's result, so it is issued only
-                // after the exchange has been performed at L2
-                const int was = atomicExch(inq + v, 0);
-                const int32_t vd = was > 1 ? 0 : v;  // (was is 0 or 1) a real register dependency
-                dv = __ldcg(dist + vd);
+                // clear the queued bit; the distance to expand with is the
+                // value at that moment (any later improvement re-queues v)
+                dv = (int)(atomicAnd(dq + v, ~1ull) >> 1);
                 if (dv < lst) {  // not yet expanded at this distance
                     last[v] = dv;
                     deg = end - beg;
@@ -651,15 +636,15 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
                     const int64_t e = b0 + (p - ex);
                     x = __ldg(adj + e);
                     const int64_t cand = (int64_t)du + (int64_t)__ldg(weff + e);
-                    // no pre-filter read of dist[x]: on these thin graphs the
-                    // atomic alone is one round trip less on the hop chain
                     if (cand < (int64_t)kIntMax) {
-                        const int c = (int)cand;
-                        if (c < atomicMin(dist + x, c)) {
-                            if (cand < T)  // issued after the min returned
-                                near = atomicExch(inq + x, 1) == 0;
-                            else
-                                far = true;
+                        // one atomic lowers dist and marks x queued (near) --
+                        // no pre-read of dist[x]: one round trip less per hop
+                        const bool nb = cand < T;
+                        const unsigned long long old =
+                            atomicMin(dq + x, ((unsigned long long)cand << 1) | (nb ? 1ull : 0ull));
+                        if ((long long)(old >> 1) > cand) {
+                            if (nb) near = (old & 1ull) == 0;
+                            else far = true;
                         }
                     }
                 }
@@ -672,7 +657,11 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
                           (unsigned long long)(-(long long)(k + total - pushed)));
         }
         grid.sync();
-        if (blockIdx.x == 0 && threadIdx.x == 0) {  // the phase is drained: next T
+        if (threadIdx.x == 0) {  // drained: every ring restarts at slot 0
+            s_head = 0;
+            A->tails[(size_t)blockIdx.x * kTailStride] = 0;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // next T
             const int src = A->fcur;
             const unsigned long long nf = A->far_n[src];
             int go = 1;
@@ -690,12 +679,11 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
                 A->far_n[src ^ 1] = 0;
             }
             A->go = go;
-            __threadfence();
         }
         grid.sync();
         if (!VA->go) break;
         {   // split the old pile: below the new T and dropped since the last
-            // expansion -> rings (in-queue deduped); the rest -> the new pile
+            // expansion -> rings (queued bit set here); the rest -> the new pile
             const int nfc = VA->fcur, src = nfc ^ 1;
             const int64_t T2 = VA->T;
             const int64_t nf = (int64_t)VA->far_n[src];
@@ -708,9 +696,9 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
                 int32_t x = -1;
                 if (i < nf) {
                     x = pile[i];
-                    const int d = __ldcg(dist + x);
+                    const int d = (int)(__ldcg(dq + x) >> 1);
                     if ((int64_t)d < T2) {
-                        near = d < __ldcg(last + x) && atomicExch(inq + x, 1) == 0;
+                        near = d < __ldcg(last + x) && (atomicOr(dq + x, 1ull) & 1ull) == 0;
                     } else {
                         far = true;
                     }
@@ -730,24 +718,30 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
     }
 }
 
-__global__ void k_async_init(int32_t *inq, int32_t *ring, unsigned long long *tails, int64_t n,
-                             int64_t ring_total, int nring, int32_t src, int src_ring) {
+__global__ void k_async_init(unsigned long long *dq, int32_t *ring, unsigned long long *tails,
+                             int64_t n, int64_t ring_total, int nring, int32_t src, int src_ring,
+                             unsigned long long cap) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
          x += (int64_t)gridDim.x * blockDim.x)
-        inq[x] = x == src ? 1 : 0;
-    const int64_t per = ring_total / nring;
+        dq[x] = x == src ? 1ull : ((unsigned long long)kIntMax << 1);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ring_total;
          i += (int64_t)gridDim.x * blockDim.x)
-        ring[i] = i == (int64_t)src_ring * per ? src : -1;
+        ring[i] = i == (int64_t)src_ring * (int64_t)cap ? src : -1;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nring;
          r += (int64_t)gridDim.x * blockDim.x)
         tails[r * kTailStride] = r == src_ring ? 1 : 0;
 }
 
+__global__ void k_async_out(const unsigned long long *__restrict__ dq, int32_t *dist, int64_t n) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x)
+        dist[x] = (int32_t)(dq[x] >> 1);
+}
+
 // The asynchronous near-far loop; SP_OK with out->status 3 asks the caller
-// for the Bellman-Ford fallback (far-pile overflow, or the watchdog).
-int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t *inq, int32_t src,
-                        int64_t delta, SsspLoop *out, float *kernel_ms) {
+// for another form (ring or far-pile overflow, or the watchdog).
+int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t src, int64_t delta,
+                        SsspLoop *out, float *kernel_ms) {
     const int64_t n = g->n, m = g->m;
     const int sms = num_sms(c.device);
     const char *thr = getenv("SP_NF_ASYNC_THREADS");  // threads per block (sweeps)
@@ -760,16 +754,22 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t *inq, int32
     const int nring = sms * std::max(1, std::min(per_sm, want));  // one ring per block
     const char *bo = getenv("SP_NF_ASYNC_BACKOFF");   // max idle backoff, ns (sweeps)
     unsigned max_backoff = bo ? (unsigned)atoi(bo) : kAsyncBackoff;
-    // a ring holds each of its vertices at most once (in-queue flag) plus
-    // entries reserved but not yet cleared: twice its share is ample
+    // a ring restarts every phase; a phase pushes each vertex at most once
+    // per drop below T, so its owned share (x 2, + slack) bounds it in
+    // practice -- an overflow aborts to the synchronous kernel
     const int64_t chunks = (n + (1 << kOwnShift) - 1) >> kOwnShift;
     const int64_t owned = ((chunks + nring - 1) / nring) << kOwnShift;
-    unsigned long long cap = 1;
-    while (cap < (unsigned long long)(2 * owned + 4096)) cap <<= 1;
+    const char *ce = getenv("SP_NF_ASYNC_RING");  // ring capacity (tests: force overflows)
+    unsigned long long cap = ce ? (unsigned long long)atoll(ce) : 0;
+    if (!cap) {
+        cap = 1;
+        while (cap < (unsigned long long)(2 * owned + 4096)) cap <<= 1;
+    }
     const int64_t fcap = 2 * m + n + 16;
     int32_t *last, *fa, *fb, *ring;
-    unsigned long long *tails;
+    unsigned long long *tails, *dq;
     AsyncNf *A;
+    SP_TRY(c.alloc(&dq, n));
     SP_TRY(c.alloc(&last, n));
     SP_TRY(c.alloc(&fa, fcap));
     SP_TRY(c.alloc(&fb, fcap));
@@ -779,12 +779,12 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t *inq, int32
     k_fill_i32<<<grid_for(n, kBlock, c.device), kBlock, 0, c.stream>>>(last, n, kIntMax);
     const int src_ring = (int)(((uint32_t)src >> kOwnShift) % (uint32_t)nring);
     k_async_init<<<grid_for((int64_t)(cap * nring), kBlock, c.device), kBlock, 0, c.stream>>>(
-        inq, ring, tails, n, (int64_t)(cap * nring), nring, src, src_ring);
+        dq, ring, tails, n, (int64_t)(cap * nring), nring, src, src_ring, cap);
     c.launches += 2;
     AsyncNf init{};
     init.ring = ring;
     init.tails = tails;
-    init.mask = cap - 1;
+    init.cap = cap;
     init.nring = nring;
     init.work = 1;  // the source
     init.far[0] = fa;
@@ -793,7 +793,7 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t *inq, int32
     init.T = delta;
     init.delta = delta;
     SP_CUDA(cudaMemcpyAsync(A, &init, sizeof(AsyncNf), cudaMemcpyHostToDevice, c.stream));
-    void *kargs[] = {&dist, &inq, &last, (void *)&g->weff, (void *)&g->off, (void *)&g->adj, &A,
+    void *kargs[] = {&dq, &last, (void *)&g->weff, (void *)&g->off, (void *)&g->adj, &A,
                      &max_backoff};
     cudaEvent_t ka, kb;
     SP_CUDA(cudaEventCreate(&ka));
@@ -801,7 +801,9 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t *inq, int32
     cudaEventRecord(ka, c.stream);
     SP_CUDA(cudaLaunchCooperativeKernel((const void *)k_nf_async, nring, threads, kargs, 0,
                                         c.stream));
+    k_async_out<<<grid_for(n, kBlock, c.device), kBlock, 0, c.stream>>>(dq, dist, n);
     cudaEventRecord(kb, c.stream);
+    c.launches += 2;
     AsyncNf *hA;
     SP_TRY(c.host_as(&hA));
     SP_CUDA(cudaMemcpyAsync(hA, A, sizeof(AsyncNf), cudaMemcpyDeviceToHost, c.stream));
@@ -811,17 +813,17 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t *inq, int32
     cudaEventDestroy(kb);
     if (hA->status == 4)
         fprintf(stderr, "starplat_b200: asynchronous near-far SSSP hit its watchdog; "
-                        "falling back to Bellman-Ford\n");
+                        "falling back to the synchronous form\n");
     static const bool trace = getenv("SP_SSSP_TRACE") != nullptr;
     if (trace)
-        fprintf(stderr, "sssp async: %d blocks x %d threads, %lld phases, %llu batches, "
-                        "%llu expansions, %llu relaxations, %.2f ms\n", nring, threads,
-                (long long)hA->phases, hA->batches, hA->expanded, hA->relaxed, *kernel_ms);
+        fprintf(stderr, "sssp async: %d blocks x %d threads, ring %llu, %lld phases, %llu "
+                        "batches, %llu expansions, %llu relaxations, status %d, %.2f ms\n",
+                nring, threads, cap, (long long)hA->phases, hA->batches, hA->expanded,
+                hA->relaxed, hA->status, *kernel_ms);
     out->iters = hA->phases;
     out->relaxed = (int64_t)hA->relaxed;
     out->frontier_sum = (int64_t)hA->expanded;
     out->status = hA->status == 0 ? 0 : 3;
-    c.launches += 1;
     return SP_OK;
 }
 
@@ -1683,10 +1685,17 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
         const char *ae = getenv("SP_NF_ASYNC");
         const bool async_nf = delta > 0 && g->max_outdeg <= kSplit && cap >= 2 * n + 16 &&
                               !(ae && ae[0] == '0');
-        if (async_nf)
-            lrc = sssp_near_far_async(g, c, dist, enq, src, delta, &hL, &kernel_ms);
-        else if (delta > 0)
+        if (async_nf) {
+            lrc = sssp_near_far_async(g, c, dist, src, delta, &hL, &kernel_ms);
+            if (lrc == SP_OK && hL.status == 3) {  // overflow / watchdog: synchronous form
+                k_init<<<grid_for(n, kBlock, dev), kBlock, 0, c.stream>>>(dist, enq, n, src, qa);
+                c.launches++;
+                hL = SsspLoop{};
+                lrc = sssp_near_far(g, c, dist, enq, qa, qb, chunks, cap, delta, &hL, &kernel_ms);
+            }
+        } else if (delta > 0) {
             lrc = sssp_near_far(g, c, dist, enq, qa, qb, chunks, cap, delta, &hL, &kernel_ms);
+        }
         if (trace) fprintf(stderr, "sssp: loop done %.2f ms (kernel %.2f ms)\n", tms(), kernel_ms);
         if (delta <= 0 || (lrc == SP_OK && hL.status == 3)) {  // Bellman-Ford
             k_init<<<grid_for(n, kBlock, dev), kBlock, 0, c.stream>>>(dist, enq, n, src, qa);

@@ -614,7 +614,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__res
 // search), or for longer rows stages A (up to kBigMax) with a
 // kBigFilterBits filter; each warp takes 32 of A's b's at a time, loads
 // their row descriptors with one coalesced read, and walks the flattened
-// 16-byte half-sectors of their rows (owner from a window bitmap of row starts),
+// 16-byte half-sectors of their rows (owner by a 5-step shuffle search; a
+// window bitmap of row starts, as in the warp path, measured slower here:
+// 413 -> 460 ms on RMAT-24),
 // one filter probe per element and a shared-memory binary search on a hit.
 constexpr int kBigFilterBits = 1 << 17;  // 16 KB
 constexpr int kBigFilterShift = 32 - 17;
@@ -645,8 +647,6 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
     // assignment keeps the hub tail short on skewed graphs.
     __shared__ long long s_bi;
     __shared__ int s_j;
-    __shared__ uint8_t s_wl[kBigBlock / 32][32];  // per warp: non-empty row rank -> lane
-    uint8_t *WL = s_wl[threadIdx.x >> 5];
     for (;;) {
         __syncthreads();  // every warp is done with the previous vertex
         if (threadIdx.x == 0) {
@@ -727,22 +727,15 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
             }
             const int excl = incl - secs;
             const int nhalf = __shfl_sync(0xffffffffu, incl, 31);
-            // owner of a half-sector: rank among the non-empty rows from a
-            // bitmap of the row starts inside its 32-half-sector window, then
-            // rank -> lane through a per-warp table (one ballot, one OR-reduce,
-            // one shared load instead of a 5-step shuffle search)
-            const bool ne = secs > 0;
-            const unsigned nem = __ballot_sync(0xffffffffu, ne);
-            if (ne) WL[__popc(nem & ((1u << lane) - 1u))] = (uint8_t)lane;
-            __syncwarp();
-            const unsigned le = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
             for (int h0 = 0; h0 < nhalf; h0 += 32) {
                 const int h = h0 + (int)lane;
-                const int r0 = __popc(__ballot_sync(0xffffffffu, ne && excl <= h0)) - 1;
-                const int off = excl - h0;
-                const unsigned bits =
-                    __reduce_or_sync(0xffffffffu, (ne && off >= 1 && off <= 31) ? (1u << off) : 0u);
-                const int lo = WL[r0 + __popc(bits & le)];
+                int lo = 0;  // owner lane: largest with excl <= h
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = lo + step;
+                    const int ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+                    if (cand < 32 && ex <= h) lo = cand;
+                }
                 const int ex = __shfl_sync(0xffffffffu, excl, lo);
                 const uint32_t s8 = __shfl_sync(0xffffffffu, inf.x, lo);
                 if (h >= nhalf) continue;
@@ -774,7 +767,6 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
                     }
                 }
             }
-            __syncwarp();  // WL is rewritten for the next 32 rows
         }
     }
     cnt = warp_sum(cnt);

@@ -199,6 +199,10 @@ def test_sssp_async_near_far_stress(kind, p0, p1, und, delta, monkeypatch):
         for rep in range(4):
             r = sp.run(corpus.SSSP, g, {"src": s})
             np.testing.assert_array_equal(r.env.node_props["dist"], dist, err_msg=f"rep {rep}")
+    monkeypatch.setenv("SP_NF_ASYNC_RING", "64")  # rings overflow: the synchronous fallback
+    r = sp.run(corpus.SSSP, g, {"src": 0})
+    np.testing.assert_array_equal(r.env.node_props["dist"], cpu_ref.sssp(o, 0)[0])
+    monkeypatch.delenv("SP_NF_ASYNC_RING")
     monkeypatch.setenv("SP_NF_ASYNC", "0")
     r = sp.run(corpus.SSSP, g, {"src": 0})
     np.testing.assert_array_equal(r.env.node_props["dist"], cpu_ref.sssp(o, 0)[0])
