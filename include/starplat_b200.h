@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 3
+#define SP_ABI_VERSION 4
 
 enum sp_status {
     SP_OK = 0,
@@ -182,16 +182,26 @@ int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t max_iter,
                 int64_t *iter, double *diff, int64_t *iters, sp_iter_cb cb,
                 void *user, sp_stats *st);
 
-/* Vertex-range PageRank step for block-partitioned multi-GPU runs
- * (graph.py:226-249 ownership): computes rank for v in [v0, v1) from a full
- * contrib[n] array and writes contrib_out[v-v0] = rank/outdeg; returns the
- * local max |delta| in *diff.  All pointers are device pointers. */
-int sp_pagerank_block_step(sp_graph *g, int64_t v0, int64_t v1,
-                           double damping, const double *contrib_in,
-                           double *rank_local, double *contrib_out,
-                           double *diff, unsigned flags, sp_stats *st);
+/* Vertex-block PageRank shards for block-partitioned multi-GPU runs
+ * (graph.py:226-249 ownership; replaces the BSP remote-read superstep of
+ * bsp.py:182-185,287-288 for pr.sp).  sp_pagerank_block_init writes the
+ * block's initial rank[v - v0] = 1/n and contrib_out[v - v0] = rank/outdeg.
+ * A shard is planned once per run (slot/row bounds of the block, unit
+ * index, scratch, hot sources); sp_pagerank_shard_step computes rank for
+ * v in [v0, v1) from the full contrib_in[n] array, writes
+ * contrib_out[v - v0] = rank/outdeg and the block's max |delta| into the
+ * device double *diff.  stream != NULL: every step is enqueued on that
+ * cudaStream_t (the caller's, e.g. torch's current stream) and returns
+ * without synchronising; NULL: the library's stream, synchronised.  All
+ * pointers are device pointers. */
+typedef struct sp_pagerank_shard sp_pagerank_shard;
 int sp_pagerank_block_init(sp_graph *g, int64_t v0, int64_t v1,
                            double *rank_local, double *contrib_out);
+int sp_pagerank_shard_create(sp_graph *g, int64_t v0, int64_t v1, double damping,
+                             unsigned flags, void *stream, sp_pagerank_shard **out);
+int sp_pagerank_shard_step(sp_pagerank_shard *h, const double *contrib_in,
+                           double *rank_local, double *contrib_out, double *diff);
+void sp_pagerank_shard_destroy(sp_pagerank_shard *h);
 
 /* corpus/programs/bc.sp over srcs in list order (duplicates re-run).
  * bc[n] accumulated; sigma/delta[n] of the LAST source (may be NULL). */

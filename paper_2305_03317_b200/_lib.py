@@ -13,10 +13,11 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libstarplat_b200.so")
+# SP_LIB: an alternative build of the same library (diagnostic variants)
+LIB_PATH = os.environ.get("SP_LIB") or os.path.join(HERE, "libstarplat_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "starplat_b200.h")
 
-ABI_VERSION = 3  # must equal SP_ABI_VERSION in include/starplat_b200.h
+ABI_VERSION = 4  # must equal SP_ABI_VERSION in include/starplat_b200.h
 
 SP_OK = 0
 SP_ERR_ARG = -1
@@ -81,8 +82,10 @@ SIGNATURES = {
     "sp_sssp_shard_destroy": (None, [_p]),
     "sp_pagerank": (_int, [_p, _d, _d, _i64, _i64, _u, _p, _int, _p, _p, _p,
                            ITER_CB, _p, _p]),
-    "sp_pagerank_block_step": (_int, [_p, _i64, _i64, _d, _p, _p, _p, _p, _u, _p]),
     "sp_pagerank_block_init": (_int, [_p, _i64, _i64, _p, _p]),
+    "sp_pagerank_shard_create": (_int, [_p, _i64, _i64, _d, _u, _p, _p]),
+    "sp_pagerank_shard_step": (_int, [_p, _p, _p, _p, _p]),
+    "sp_pagerank_shard_destroy": (None, [_p]),
     "sp_bc": (_int, [_p, _p, _i64, _u, _p, _p, _p, _int, _p]),
     "sp_tc": (_int, [_p, _i64, _i64, _p, _p]),
     "sp_neighbor_sum": (_int, [_p, _p, _int, _int, _p, _p, _p]),

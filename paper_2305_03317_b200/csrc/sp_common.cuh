@@ -67,6 +67,10 @@ struct Call {
     void *pinned = nullptr;  // kPinnedBlock bytes of pinned host memory
     bool owned = true;       // stream/events belong to this call (else thread-cached)
     bool persisting = false; // an L2 access-policy window is set on the stream
+    bool external = false;   // runs on a caller's stream: no sync at the end
+    // as begin(), but enqueue on the caller's stream `s` (stream-ordered: the
+    // call returns without synchronising; its scratch is freed in order)
+    int begin_external(int dev, cudaStream_t s);
     // Keep [base, base+bytes) in the persisting L2 set-aside for this call's
     // kernels (random-access property arrays); best effort.
     void persist(const void *base, size_t bytes);

@@ -1521,6 +1521,24 @@ extern "C" int sp_pagerank(sp_graph *g, double damping, double epsilon, int64_t 
     return rc;
 }
 
+// ---- vertex-block shards (multi-GPU, graph.py:226-249 ownership) --------
+// A shard is planned once per run (the block's slot and row bounds, unit
+// index, scratch, hot sources): a step only launches the pull over the
+// block and writes the block's max |delta| into a caller device double, on
+// the caller's stream (`stream`, e.g. torch's current stream, so the
+// exchange collectives order after it without a host sync; NULL: the
+// library's per-thread stream, synchronised per step).
+struct sp_pagerank_shard {
+    sp_graph *g = nullptr;
+    int64_t v0 = 0, v1 = 0;
+    double damping = 0.0;
+    bool det = false;
+    cudaStream_t stream = nullptr;
+    FastPlan plan;
+    void *keep[32];
+    int nkeep = 0;
+};
+
 extern "C" int sp_pagerank_block_init(sp_graph *g, int64_t v0, int64_t v1, double *rank_local,
                                       double *contrib_out) {
     SP_CHECK(g && v0 >= 0 && v0 <= v1 && v1 <= g->n, SP_ERR_ARG, "bad vertex block");
@@ -1534,30 +1552,65 @@ extern "C" int sp_pagerank_block_init(sp_graph *g, int64_t v0, int64_t v1, doubl
     return SP_OK;
 }
 
-extern "C" int sp_pagerank_block_step(sp_graph *g, int64_t v0, int64_t v1, double damping,
-                                      const double *contrib_in, double *rank_local,
-                                      double *contrib_out, double *diff, unsigned flags,
-                                      sp_stats *st) {
-    SP_CHECK(g && v0 >= 0 && v0 <= v1 && v1 <= g->n && diff, SP_ERR_ARG, "bad vertex block");
+extern "C" int sp_pagerank_shard_create(sp_graph *g, int64_t v0, int64_t v1, double damping,
+                                        unsigned flags, void *stream, sp_pagerank_shard **out) {
+    SP_CHECK(g && out && v0 >= 0 && v0 <= v1 && v1 <= g->n, SP_ERR_ARG, "bad vertex block");
+    *out = nullptr;
     Call c;
     SP_TRY(c.begin(g->device));
-    double *slot;
-    SP_TRY(c.alloc(&slot, 1));
-    SP_CUDA(cudaMemsetAsync(slot, 0, sizeof(double), c.stream));
-    if (v1 > v0) {
-        if (flags & SP_FLAG_DETERMINISTIC) {
-            SP_TRY(launch_exact(g, c, v0, v1, damping, contrib_in, rank_local, contrib_out, slot,
-                                nullptr, nullptr));
+    sp_pagerank_shard *h = new sp_pagerank_shard;
+    h->g = g;
+    h->v0 = v0;
+    h->v1 = v1;
+    h->damping = damping;
+    h->det = (flags & SP_FLAG_DETERMINISTIC) != 0;
+    h->stream = static_cast<cudaStream_t>(stream);
+    int rc = SP_OK;
+    if (!h->det && v1 > v0) rc = plan_fast(g, c, v0, v1, damping, h->plan);
+    // the plan's scratch outlives this call: the shard owns it
+    for (int i = 0; i < c.nbufs && h->nkeep < 32; i++) h->keep[h->nkeep++] = c.bufs[i];
+    c.nbufs = 0;
+    if (rc == SP_OK) rc = c.finish(nullptr);
+    if (rc != SP_OK) {
+        cudaDeviceSynchronize();
+        for (int i = 0; i < h->nkeep; i++) scratch_free(h->keep[i], nullptr);
+        delete h;
+        return rc;
+    }
+    *out = h;
+    return SP_OK;
+}
+
+extern "C" int sp_pagerank_shard_step(sp_pagerank_shard *h, const double *contrib_in,
+                                      double *rank_local, double *contrib_out, double *diff) {
+    SP_CHECK(h && contrib_in && rank_local && contrib_out && diff, SP_ERR_ARG,
+             "sp_pagerank_shard_step: bad arguments");
+    sp_graph *g = h->g;
+    Call c;
+    if (h->stream) SP_TRY(c.begin_external(g->device, h->stream));
+    else SP_TRY(c.begin(g->device));
+    SP_CUDA(cudaMemsetAsync(diff, 0, sizeof(double), c.stream));
+    if (h->v1 > h->v0) {
+        if (h->det) {
+            SP_TRY(launch_exact(g, c, h->v0, h->v1, h->damping, contrib_in, rank_local,
+                                contrib_out, diff, nullptr, nullptr));
         } else {
-            FastPlan plan;
-            SP_TRY(plan_fast(g, c, v0, v1, damping, plan));
             // contrib_out is a single persistent buffer here: zero rows are
             // rewritten every step (cheap: one indeg pass over the block)
-            SP_TRY(launch_fast(c, plan, g, v1, contrib_in, rank_local, contrib_out, nullptr, true,
-                               slot, nullptr, nullptr));
+            SP_TRY(launch_fast(c, h->plan, g, h->v1, contrib_in, rank_local, contrib_out,
+                               nullptr, true, diff, nullptr, nullptr));
         }
     }
-    SP_CUDA(cudaMemcpyAsync(diff, slot, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    SP_TRY(c.finish(st));
+    SP_CUDA(cudaGetLastError());
+    if (!h->stream) SP_TRY(c.finish(nullptr));
     return SP_OK;
+}
+
+extern "C" void sp_pagerank_shard_destroy(sp_pagerank_shard *h) {
+    if (!h) return;
+    cudaSetDevice(h->g->device);
+    cudaDeviceSynchronize();
+    for (int i = 0; i < h->nkeep; i++) scratch_free(h->keep[i], nullptr);
+    cudaDeviceSynchronize();
+    delete h;
 }

@@ -251,7 +251,22 @@ int Call::host(void **p) {
     return SP_OK;
 }
 
+int Call::begin_external(int dev, cudaStream_t s) {
+    device = dev;
+    SP_CUDA(cudaSetDevice(dev));
+    if (dev >= 0 && dev < 64) std::call_once(g_pool_once[dev], tune_pool, dev);
+    stream = s;
+    owned = false;
+    external = true;
+    return SP_OK;
+}
+
 Call::~Call() {
+    if (stream && external) {
+        for (int i = 0; i < nbufs; i++) scratch_free(bufs[i], stream);
+        pinned_put(pinned);
+        return;
+    }
     if (stream) {
         for (int i = 0; i < nbufs; i++) scratch_free(bufs[i], stream);
         cudaStreamSynchronize(stream);

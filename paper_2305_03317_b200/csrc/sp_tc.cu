@@ -625,7 +625,14 @@ constexpr int kHashMax = 8 * 1024;      // rows up to this are hashed: 2^14 x (k
 // One CTA per SM (the shared table); 8 warps per vertex -- 32 warps
 // measured slower (744 vs 534 ms on RMAT-24): the static 32-row batches
 // leave more warps idle at each vertex's barrier.
-constexpr int kBigBlock = 256;
+#ifndef SP_TC_BIG_BLOCK
+#define SP_TC_BIG_BLOCK 256
+#endif
+constexpr int kBigBlock = SP_TC_BIG_BLOCK;
+#ifndef SP_TC_BIG_UNROLL
+#define SP_TC_BIG_UNROLL 1  // RMAT-24: 1 -> 253 ms, 4 -> 264 ms
+#endif
+constexpr int kUnrollBig = SP_TC_BIG_UNROLL;  // 16-byte loads in flight per lane in k_tc_big
 
 __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restrict__ ustart8,
                                                       const int32_t *__restrict__ ulen,
@@ -727,28 +734,38 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
             }
             const int excl = incl - secs;
             const int nhalf = __shfl_sync(0xffffffffu, incl, 31);
-            for (int h0 = 0; h0 < nhalf; h0 += 32) {
-                const int h = h0 + (int)lane;
-                int lo = 0;  // owner lane: largest with excl <= h
+            // kUnrollBig half-sectors per lane in flight (their owner searches
+            // are independent); one load per lane measured latency-bound
+            for (int h0 = 0; h0 < nhalf; h0 += 32 * kUnrollBig) {
+                int4 xs[kUnrollBig];
 #pragma unroll
-                for (int step = 16; step > 0; step >>= 1) {
-                    const int cand = lo + step;
-                    const int ex = __shfl_sync(0xffffffffu, excl, cand & 31);
-                    if (cand < 32 && ex <= h) lo = cand;
+                for (int u = 0; u < kUnrollBig; u++) {
+                    const int h = h0 + u * 32 + (int)lane;
+                    int lo = 0;  // owner lane: largest with excl <= h
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int cand = lo + step;
+                        const int ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+                        if (cand < 32 && ex <= h) lo = cand;
+                    }
+                    const int ex = __shfl_sync(0xffffffffu, excl, lo);
+                    const uint32_t s8 = __shfl_sync(0xffffffffu, inf.x, lo);
+                    xs[u] = h < nhalf ? __ldg(reinterpret_cast<const int4 *>(uadj) +
+                                              kQ * (int64_t)s8 + (h - ex))
+                                      : make_int4(-1, -1, -1, -1);
                 }
-                const int ex = __shfl_sync(0xffffffffu, excl, lo);
-                const uint32_t s8 = __shfl_sync(0xffffffffu, inf.x, lo);
-                if (h >= nhalf) continue;
-                const int4 xs = __ldg(reinterpret_cast<const int4 *>(uadj) +
-                                      kQ * (int64_t)s8 + (h - ex));
-                const int32_t xv[4] = {xs.x, xs.y, xs.z, xs.w};
+#pragma unroll
+                for (int u = 0; u < kUnrollBig; u++) {
+                const int32_t xv[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
                     const int32_t x = xv[i];
                     if (x < 0) continue;
                     if (hashed) {  // multiplicity of x in A
+#ifndef SP_TC_BIG_NOFILTER
                         const uint32_t fb = ((uint32_t)x * 0x9E3779B1u) >> (32 - fbits);
                         if (!(HF[fb >> 5] & (1u << (fb & 31)))) continue;
+#endif
                         uint32_t h = ((uint32_t)x * 2654435761u) >> (32 - tbits);
                         for (;;) {
                             const int32_t k = HK[h];
@@ -765,6 +782,7 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
                     } else {
                         cnt += mult_g(uadj, r0, r0 + na, x);
                     }
+                }
                 }
             }
         }

@@ -12,10 +12,11 @@ trident/bsp.py; its ownership rule is graph.py:226-249):
          data-path collective.
 * TC  -- vertex ranges balanced by a sum-of-squared-degree work proxy, graph
          replicated; one integer ``all_reduce(sum)`` (exact).
-* PR  -- block partition; per iteration a local pull over the owned block,
-         ``all_gather`` of the owned contrib slices (the reference's
-         remote-read snapshot, bsp.py:182-185/287-288) and ``all_reduce(max)``
-         of diff (the scalar merge, bsp.py:322-330).
+* PR  -- block partition, planned once per run; per iteration a local pull
+         over the owned block, ``all_reduce(max)`` of diff (the scalar merge,
+         bsp.py:322-330) and ``all_gather`` of the owned contrib slices (the
+         reference's remote-read snapshot, bsp.py:182-185/287-288), all
+         queued on the device; one host read per iteration (convergence).
 * SSSP -- owner-computes over the block partition: per superstep each rank
          relaxes its owned frontier (one pass, or to a local fixpoint);
          remote improvements leave as ONE aggregated (vertex, local min)
@@ -117,15 +118,8 @@ class NativeBackend:
                   "sp_pagerank_block_init")
         return rank, contrib
 
-    def pr_step(self, g, v0, v1, damping, contrib_full, rank, contrib, deterministic) -> float:
-        self._fence()
-        diff = C.c_double()
-        flags = _lib.SP_FLAG_DETERMINISTIC if deterministic else 0
-        self._chk(self.L.sp_pagerank_block_step(
-            g.handle, int(v0), int(v1), float(damping), C.c_void_p(contrib_full.data_ptr()),
-            C.c_void_p(rank.data_ptr()), C.c_void_p(contrib.data_ptr()), C.byref(diff), flags,
-            None), "sp_pagerank_block_step")
-        return float(diff.value)
+    def pr_shard(self, g, v0, v1, damping, deterministic):
+        return _NativePrShard(self, g, v0, v1, damping, deterministic)
 
     # -- SSSP (owner-computes shard, one handle per run)
     def sssp_shard(self, g, src, v0, v1, per, world):
@@ -133,6 +127,33 @@ class NativeBackend:
 
     def to_host(self, x):
         return x.cpu().numpy()
+
+
+class _NativePrShard:
+    """sp_pagerank_shard_* planned once per run; every step is enqueued on
+    torch's current stream (no host synchronisation: the exchange
+    collectives that follow are ordered after it on the device)."""
+
+    def __init__(self, be, g, v0, v1, damping, det):
+        self.be = be
+        self.h = C.c_void_p()
+        flags = _lib.SP_FLAG_DETERMINISTIC if det else 0
+        stream = be.torch.cuda.current_stream(be.device).cuda_stream
+        be._fence()
+        be._chk(be.L.sp_pagerank_shard_create(g.handle, int(v0), int(v1), float(damping), flags,
+                                              C.c_void_p(stream), C.byref(self.h)),
+                "sp_pagerank_shard_create")
+
+    def step(self, contrib_full, rank, contrib, diff):
+        self.be._chk(self.be.L.sp_pagerank_shard_step(
+            self.h, C.c_void_p(contrib_full.data_ptr()), C.c_void_p(rank.data_ptr()),
+            C.c_void_p(contrib.data_ptr()), C.c_void_p(diff.data_ptr())),
+            "sp_pagerank_shard_step")
+
+    def close(self):
+        if self.h:
+            self.be.L.sp_pagerank_shard_destroy(self.h)
+            self.h = C.c_void_p()
 
 
 class _NativeShard:
@@ -407,20 +428,27 @@ def _pr(be, g, bound, cap, world, me, group, det, E, prog, tr):
     it = 0
     iters = 0
     diff = 0.0
-    while True:
-        d = be.pr_step(g, v0, v1, bound["damping"], full, rank_l, contrib_l, det)
-        dt = torch.tensor([d], dtype=torch.float64, device=be.device)
-        dist.all_reduce(dt, op=dist.ReduceOp.MAX, group=group)
-        diff = float(dt.item())
-        gather()
-        it += 1
-        iters += 1
-        done = diff < bound["epsilon"] or it >= bound["maxIter"]  # pr.sp:10
-        tr.record("fixedPoint converged", v1 - v0, v1 - v0, finished=done)
-        if done:
-            break
-        if iters >= cap:
-            raise E.NonConvergenceError(prog.flag, cap)
+    dt = torch.zeros(1, dtype=torch.float64, device=be.device)
+    sh = be.pr_shard(g, v0, v1, bound["damping"], det)  # planned once per run
+    try:
+        while True:
+            # the step, the max-reduce of diff and the contrib exchange are
+            # all queued on the device; the convergence test is the
+            # iteration's one host read
+            sh.step(full, rank_l, contrib_l, dt)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX, group=group)
+            gather()
+            diff = float(dt.item())
+            it += 1
+            iters += 1
+            done = diff < bound["epsilon"] or it >= bound["maxIter"]  # pr.sp:10
+            tr.record("fixedPoint converged", v1 - v0, v1 - v0, finished=done)
+            if done:
+                break
+            if iters >= cap:
+                raise E.NonConvergenceError(prog.flag, cap)
+    finally:
+        sh.close()
     # ranks back to every rank (owned slices, padded to per)
     rl = torch.zeros(per, dtype=torch.float64, device=be.device)
     if v1 > v0:

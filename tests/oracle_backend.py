@@ -78,26 +78,38 @@ class OracleBackend:
                            + [0.0] * (1 if v1 == v0 else 0))
         return torch.from_numpy(rank), torch.from_numpy(contrib)
 
-    def pr_step(self, g, v0, v1, damping, contrib_full, rank, contrib, deterministic):
-        n = g.n
+    def pr_shard(self, g, v0, v1, damping, deterministic):
+        return _OraclePrShard(g, v0, v1, damping)
+
+    # SSSP owner-computes shard (sp_sssp_shard_* semantics)
+    def sssp_shard(self, g, src, v0, v1, per, world):
+        return _OracleShard(g, src, v0, v1, per, world)
+
+
+class _OraclePrShard:
+    """sp_pagerank_shard_* semantics: left folds in reverse-CSR order."""
+
+    def __init__(self, g, v0, v1, damping):
+        self.g, self.v0, self.v1, self.damping = g, v0, v1, damping
+
+    def step(self, contrib_full, rank, contrib, diff):
+        g, v0, v1, damping = self.g, self.v0, self.v1, self.damping
         cf = contrib_full.numpy()
         outdeg = np.diff(g.off)
-        base = (1.0 - damping) / n
+        base = (1.0 - damping) / g.n
         d = 0.0
         for v in range(v0, v1):
             s = 0.0
             for k in range(g.roff[v], g.roff[v + 1]):
                 s = s + float(cf[g.radj[k]])
             nr = base + damping * s
-            dd = abs(nr - float(rank[v - v0]))
-            d = max(d, dd)
+            d = max(d, abs(nr - float(rank[v - v0])))
             rank[v - v0] = nr
             contrib[v - v0] = nr / outdeg[v] if outdeg[v] > 0 else 0.0
-        return d
+        diff[0] = d
 
-    # SSSP owner-computes shard (sp_sssp_shard_* semantics)
-    def sssp_shard(self, g, src, v0, v1, per, world):
-        return _OracleShard(g, src, v0, v1, per, world)
+    def close(self):
+        pass
 
 
 class _OracleShard:

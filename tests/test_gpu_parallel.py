@@ -3,7 +3,7 @@
 One GPU is available, so two ranks share cuda:0 over gloo (NCCL refuses two
 ranks on one device); this drives the native block kernels
 (sp_sssp_shard_*: owner-computes SSSP with aggregated messages in both
-exchange forms, sp_pagerank_block_step, sp_tc ranges, sp_bc source shares) through the real sharding/exchange logic and checks the results
+exchange forms, sp_pagerank_shard_* (planned once, stream-ordered steps), sp_tc ranges, sp_bc source shares) through the real sharding/exchange logic and checks the results
 against the single-process CPU oracle."""
 
 import os

@@ -36,6 +36,11 @@ elif algo == "bc":
     deg = np.diff(np.asarray(g.offsets))
     srcs = np.random.default_rng(1).choice(np.flatnonzero(deg > 0), size=256, replace=False)
     prog, args = corpus.BC, {"sourceSet": srcs[:nsrc].tolist()}
+elif algo == "bc256":  # the bench's cfg4 line: all 256 sources
+    g = sp.generate("rmat", 20, 16, seed=1, undirected=True)
+    deg = np.diff(np.asarray(g.offsets))
+    srcs = np.random.default_rng(1).choice(np.flatnonzero(deg > 0), size=256, replace=False)
+    prog, args = corpus.BC, {"sourceSet": srcs.tolist()}
 elif algo == "sssp_grid_pr":
     g = sp.generate("grid", 4096, 4096, seed=1)
     prog, args = corpus.PR, {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
@@ -58,4 +63,5 @@ for i in range(reps):
           f"{r.stats['device_ms']:.2f} ms, launches {r.stats['kernel_launches']}, "
           f"edges {r.stats['edges_visited']}, vertices {r.stats['vertices_visited']}, "
           f"iters {r.stats['iterations']}, model bytes {r.stats['model_bytes']}, "
-          f"m {g.m}", flush=True)
+          f"m {g.m}" + (f", triangles {r.env.scalars['triangle_count']}" if prog is corpus.TC else ""),
+          flush=True)
