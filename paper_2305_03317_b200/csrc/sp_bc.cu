@@ -513,7 +513,10 @@ __device__ __forceinline__ void bb_row_sums(const BbChunks &ck, int64_t r, doubl
 
 // Level d's rows: short rows folded by one thread; long rows registered and
 // cut into chunks.  Deepest level (leaf = true): no children, coef = 1/sigma.
-__global__ void __launch_bounds__(256) k_bb_rows(BatchFold f, const int32_t *__restrict__ q,
+#ifndef SP_BBROWS_MINB
+#define SP_BBROWS_MINB 5
+#endif
+__global__ void __launch_bounds__(256, SP_BBROWS_MINB) k_bb_rows(BatchFold f, const int32_t *__restrict__ q,
                                                  int64_t nq, bool leaf, BbChunks ck) {
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nq;
          base += (int64_t)gridDim.x * blockDim.x) {
@@ -550,7 +553,12 @@ __global__ void __launch_bounds__(256) k_bb_rows(BatchFold f, const int32_t *__r
 
 // One warp per chunk: lanes take slots j*32 + lane, then a fixed-shape warp
 // reduction per source lane into the chunk's partials.
-__global__ void __launch_bounds__(256) k_bb_chunks(BatchFold f, BbChunks ck) {
+#ifndef SP_BB_MINB
+// blocks/SM the batched chunk kernels are compiled for (76 -> 64 registers)
+// -- with SP_BBROWS_MINB 5, BC cfg4 65 -> 55 ms in one measurement pair
+#define SP_BB_MINB 4
+#endif
+__global__ void __launch_bounds__(256, SP_BB_MINB) k_bb_chunks(BatchFold f, BbChunks ck) {
     constexpr int kPer = kBbSplit / 32;
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -597,7 +605,10 @@ __global__ void __launch_bounds__(256) k_bb_chunks(BatchFold f, BbChunks ck) {
 }
 
 // one warp per long row
-__global__ void __launch_bounds__(256) k_bb_finish(BatchFold f, BbChunks ck) {
+#ifndef SP_BBFIN_MINB
+#define SP_BBFIN_MINB 5  // BC cfg4: 59.7 -> 56.8 ms
+#endif
+__global__ void __launch_bounds__(256, SP_BBFIN_MINB) k_bb_finish(BatchFold f, BbChunks ck) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nreg = (int64_t)__ldcg(&ck.counts[0]);
@@ -648,7 +659,10 @@ struct BatchPull {
     }
 };
 
-__global__ void __launch_bounds__(256) k_bb_pull_rows(BatchPull f, int64_t n, BbChunks ck) {
+#ifndef SP_BBPULL_MINB
+#define SP_BBPULL_MINB 5  // BC cfg4: 59.7 -> 57.5 ms (6: 65 ms)
+#endif
+__global__ void __launch_bounds__(256, SP_BBPULL_MINB) k_bb_pull_rows(BatchPull f, int64_t n, BbChunks ck) {
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
          base += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = base + threadIdx.x;
@@ -685,7 +699,7 @@ __global__ void __launch_bounds__(256) k_bb_pull_rows(BatchPull f, int64_t n, Bb
     }
 }
 
-__global__ void __launch_bounds__(256) k_bb_pull_chunks(BatchPull f, BbChunks ck) {
+__global__ void __launch_bounds__(256, SP_BB_MINB) k_bb_pull_chunks(BatchPull f, BbChunks ck) {
     constexpr int kPer = kBbSplit / 32;
     const unsigned lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;

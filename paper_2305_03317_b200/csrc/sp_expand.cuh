@@ -354,8 +354,11 @@ __device__ __forceinline__ void expand_chunks_body(
     if (lane == 0 && scanned) atomicAdd(&cnt->scanned, scanned);  // warp-uniform
 }
 
+#ifndef SP_EXPCHUNK_MINB
+#define SP_EXPCHUNK_MINB 3  // blocks/SM k_expand_chunks is compiled for
+#endif
 template <class Op>
-__global__ void __launch_bounds__(kExpandBlock, 3) k_expand_chunks(
+__global__ void __launch_bounds__(kExpandBlock, SP_EXPCHUNK_MINB) k_expand_chunks(
     Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const ChunkItem *__restrict__ chunks, int32_t *__restrict__ qn, ExpandCounters *cnt) {
     expand_chunks_body(op, off, adj, chunks, qn, cnt);

@@ -1133,7 +1133,13 @@ __device__ __forceinline__ void sp_slab8(const int32_t *__restrict__ p, int64_t 
     }
 }
 
-__global__ void __launch_bounds__(256) k_spull_units(SPull a, int32_t *dist, DoLoop *L) {
+#ifndef SP_SPULL_MINB
+// blocks/SM the pull sweep is compiled for (a register cap: 64 -> 48, a few
+// bytes of spill): RMAT-24 SSSP 5.63 -> 5.18 ms and RMAT-26 25.1 -> 20.4 ms
+// together with SP_DOCHUNK_MINB 4 (6 blocks: slower)
+#define SP_SPULL_MINB 5
+#endif
+__global__ void __launch_bounds__(256, SP_SPULL_MINB) k_spull_units(SPull a, int32_t *dist, DoLoop *L) {
     if (L->mode != 1) return;
     __shared__ uint32_t bitmap[8][kSpCh / 32];
     uint32_t *bm = bitmap[threadIdx.x >> 5];
@@ -1277,7 +1283,10 @@ __global__ void k_spull_setup(SPull a) {
     }
 }
 
-__global__ void __launch_bounds__(kExpandBlock, 4) k_do_push(
+#ifndef SP_DOPUSH_MINB
+#define SP_DOPUSH_MINB 5  // RMAT-24: 4 -> 5.16 ms, 5 -> 5.06 ms, 6 -> 5.2 ms
+#endif
+__global__ void __launch_bounds__(kExpandBlock, SP_DOPUSH_MINB) k_do_push(
     int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
     const int64_t *__restrict__ off, const int32_t *__restrict__ adj, ChunkItem *chunks,
     DoLoop *D, int64_t warps) {
@@ -1290,7 +1299,10 @@ __global__ void __launch_bounds__(kExpandBlock, 4) k_do_push(
                 expand_vpw(nq, warps));
 }
 
-__global__ void __launch_bounds__(kExpandBlock, 3) k_do_push_chunks(
+#ifndef SP_DOCHUNK_MINB
+#define SP_DOCHUNK_MINB 4  // hub-chunk push (80 -> 64 registers; 5: slower)
+#endif
+__global__ void __launch_bounds__(kExpandBlock, SP_DOCHUNK_MINB) k_do_push_chunks(
     int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
     const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const ChunkItem *chunks,
     DoLoop *D) {

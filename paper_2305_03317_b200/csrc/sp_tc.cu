@@ -372,7 +372,13 @@ struct TcCounters {
 
 // Warp path, plain form: A sorted in shared memory, filter probe, binary
 // search on a filter hit (cheapest when hits are rare, e.g. uniform graphs).
-__global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__restrict__ ustart8,
+#ifndef SP_TCP_MINB
+#define SP_TCP_MINB 1
+#endif
+#ifndef SP_TCH_MINB
+#define SP_TCH_MINB 1
+#endif
+__global__ void __launch_bounds__(kBlock, SP_TCP_MINB) k_tc_fwd_plain(const uint32_t *__restrict__ ustart8,
                                                    const int32_t *__restrict__ ulen,
                                                    const int32_t *__restrict__ uadj,
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
@@ -480,7 +486,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_plain(const uint32_t *__re
 
 // Warp path, hashed form: on a filter hit the multiplicity comes from a
 // per-warp hash table of A (skewed graphs, where most probes are hits).
-__global__ void __launch_bounds__(kBlock, 1) k_tc_fwd_hash(const uint32_t *__restrict__ ustart8,
+__global__ void __launch_bounds__(kBlock, SP_TCH_MINB) k_tc_fwd_hash(const uint32_t *__restrict__ ustart8,
                                                    const int32_t *__restrict__ ulen,
                                                    const int32_t *__restrict__ uadj,
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
