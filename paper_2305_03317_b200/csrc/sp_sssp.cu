@@ -100,7 +100,13 @@ struct SsspLoop {
     unsigned blocks_done;  // k_relax_loop_chunks: the last block runs the advance
 };
 
-__global__ void __launch_bounds__(kExpandBlock, 4) k_relax_loop(
+#ifndef SP_RL_MINB
+#define SP_RL_MINB 5  // RMAT-22 SSSP 1.71 -> 1.57 ms (with SP_RLC_MINB 4); 6: slower
+#endif
+#ifndef SP_RLC_MINB
+#define SP_RLC_MINB 4
+#endif
+__global__ void __launch_bounds__(kExpandBlock, SP_RL_MINB) k_relax_loop(
     int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
     const int64_t *__restrict__ off, const int32_t *__restrict__ adj, ChunkItem *chunks,
     SsspLoop *L, int64_t warps) {
@@ -116,7 +122,7 @@ __device__ __forceinline__ int loop_advance(SsspLoop *L);
 // Hub chunks; the last block to finish also runs the loop advance (one
 // graph node per iteration fewer: ~4 us of node latency each, cfg1 runs
 // 9-10 iterations of ~40 us).
-__global__ void __launch_bounds__(kExpandBlock, 3) k_relax_loop_chunks(
+__global__ void __launch_bounds__(kExpandBlock, SP_RLC_MINB) k_relax_loop_chunks(
     int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
     const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const ChunkItem *chunks,
     SsspLoop *L, cudaGraphConditionalHandle h) {
