@@ -192,6 +192,7 @@ struct sp_graph {
     // rel_perm[v]
     int pr_rel = -1;  // -1: not decided, 0: not used, 1: built
     int pr_runs = 0;  // fast single-GPU PR runs started on this graph
+    int sssp_do_runs = 0;  // direction-optimising SSSP runs (the hot set is built on the second)
     int32_t *rel_perm = nullptr, *rel_radj = nullptr, *rel_outdeg = nullptr,
             *rel_indeg = nullptr, *rel_nzrow = nullptr;
     int64_t *rel_nzend = nullptr, *rel_unit_row = nullptr;
@@ -208,6 +209,9 @@ namespace sp {
 constexpr int kPrHotBit = 1 << 30;
 int pr_hot_prepare(sp_graph *g, Call &c, const int32_t *outdeg, int64_t max_outdeg,
                    int32_t **hot_idx, int *H);
+// Build the hot-source encoding of radj now if the graph qualifies (sets
+// g->pr_H: > 0 built, 0 not worth it); shared by PR and the SSSP pull sweep.
+int pr_hot_build(sp_graph *g, Call &c);
 int ensure_weff(sp_graph *g, Call &c);
 // Reverse-slot weights rweff[k] = w_eff[reid[k]] (undirected: w_eff itself).
 int ensure_rweff(sp_graph *g, Call &c);

@@ -570,9 +570,21 @@ int pr_hot_select(sp_graph *g, Call &c, const int32_t *outdeg, int64_t max_outde
     return SP_OK;
 }
 
+static int hot_build_locked(sp_graph *g, Call &c, bool now);
+
+int pr_hot_build_impl(sp_graph *g, Call &c) {
+    std::lock_guard<std::mutex> lk(g_hot_mu);
+    if (g->pr_H >= 0) return SP_OK;
+    return hot_build_locked(g, c, true);
+}
+
 int ensure_pr_hot(sp_graph *g, Call &c) {
     std::lock_guard<std::mutex> lk(g_hot_mu);
     if (g->pr_H >= 0) return SP_OK;
+    return hot_build_locked(g, c, false);
+}
+
+static int hot_build_locked(sp_graph *g, Call &c, bool now) {
     // Built on the graph's second fast PR call: the encoding (a sort of the
     // out-degrees + one pass over radj, ~0.9 ms at cfg2) costs more than it
     // saves in a single run (~0.4 ms), so a one-shot run on a fresh graph
@@ -586,7 +598,7 @@ int ensure_pr_hot(sp_graph *g, Call &c) {
         g->pr_H = 0;
         return SP_OK;
     }
-    if (g->pr_fast_calls++ == 0) return SP_OK;
+    if (!now && g->pr_fast_calls++ == 0) return SP_OK;
     int32_t *hot_idx = nullptr;
     int H = 0;
     SP_TRY(pr_hot_select(g, c, g->outdeg, g->max_outdeg, &hot_idx, &H));
@@ -1272,6 +1284,7 @@ int launch_exact(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, c
 }  // namespace
 
 namespace sp {
+int pr_hot_build(sp_graph *g, Call &c) { return pr_hot_build_impl(g, c); }
 int pr_hot_prepare(sp_graph *g, Call &c, const int32_t *outdeg, int64_t max_outdeg,
                    int32_t **hot_idx, int *H) {
     static_assert(kHotBit == kPrHotBit, "hot-slot encoding");

@@ -1145,10 +1145,15 @@ __device__ __forceinline__ void sp_slab8(const int32_t *__restrict__ p, int64_t 
 // together with SP_DOCHUNK_MINB 4 (6 blocks: slower)
 #define SP_SPULL_MINB 5
 #endif
-__global__ void __launch_bounds__(256, SP_SPULL_MINB) k_spull_units(SPull a, int32_t *dist, DoLoop *L) {
-    if (L->mode != 1) return;
-    __shared__ uint32_t bitmap[8][kSpCh / 32];
-    uint32_t *bm = bitmap[threadIdx.x >> 5];
+// kHot: slots whose source is one of the H hottest (most gathered) sources
+// carry kPrHotBit | hot index (the PageRank hot encoding of radj, shared
+// with sp_pagerank.cu), and their dist comes from a shared-memory snapshot
+// taken when the sweep starts.  A hot source lowered during the sweep is in
+// the next frontier (pull_apply marks it), so a stale snapshot value only
+// defers its relaxation to the next iteration: the same fixpoint.
+template <bool kHot>
+__device__ __forceinline__ void spull_body(const SPull &a, int32_t *dist, DoLoop *L, uint32_t *bm,
+                                           const int32_t *hot) {
     const unsigned lane = lane_id();
     if (lane < kSpCh / 32) bm[lane] = 0u;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1185,7 +1190,12 @@ __global__ void __launch_bounds__(256, SP_SPULL_MINB) k_spull_units(SPull a, int
             for (int i = 0; i < 8; i++) {
                 val[i] = kSpNone;
                 if (idx[i] >= 0) {
-                    const int du = __ldcg(dist + idx[i]);
+                    int du;
+                    if constexpr (kHot)
+                        du = (idx[i] & kPrHotBit) ? hot[idx[i] & (kPrHotBit - 1)]
+                                                  : __ldcg(dist + idx[i]);
+                    else
+                        du = __ldcg(dist + idx[i]);
                     if (du != kIntMax) val[i] = (int64_t)du + (int64_t)w[i];
                 }
             }
@@ -1254,6 +1264,36 @@ __global__ void __launch_bounds__(256, SP_SPULL_MINB) k_spull_units(SPull a, int
     if (lane == 0 && improved) atomicAdd(&L->s.cnt[L->s.cur].next_size, improved);
     // every swept in-slot is a relaxation (12 B: radj, w_eff, dist gather)
     if (lane == 0 && swept) atomicAdd(&L->s.cnt[L->s.cur].scanned, swept);
+}
+
+__global__ void __launch_bounds__(256, SP_SPULL_MINB) k_spull_units(SPull a, int32_t *dist, DoLoop *L) {
+    if (L->mode != 1) return;
+    __shared__ uint32_t bitmap[8][kSpCh / 32];
+    spull_body<false>(a, dist, L, bitmap[threadIdx.x >> 5], nullptr);
+}
+
+// the hot sources' dist at the start of a sweep, contiguous
+__global__ void k_spull_hot_gather(const DoLoop *L, const int32_t *__restrict__ hot_ids, int H,
+                                   const int32_t *dist, int32_t *hotd) {
+    if (L->mode != 1) return;
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x)
+        hotd[h] = __ldcg(dist + hot_ids[h]);
+}
+
+// Persistent hot variant: one 1024-thread block per SM copies the snapshot
+// into shared memory, then its warps sweep their units.
+constexpr int kSpHotBlock = 1024;
+__global__ void __launch_bounds__(kSpHotBlock, 1) k_spull_units_hot(SPull a, int32_t *dist,
+                                                                   DoLoop *L,
+                                                                   const int32_t *hotd, int H) {
+    if (L->mode != 1) return;
+    extern __shared__ int32_t sp_hot_smem[];
+    uint32_t *bitmaps = reinterpret_cast<uint32_t *>(sp_hot_smem + ((H + 3) & ~3));
+    const int4 *src = reinterpret_cast<const int4 *>(hotd);
+    int4 *dst = reinterpret_cast<int4 *>(sp_hot_smem);
+    for (int i = threadIdx.x; i < (H + 3) / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
+    __syncthreads();
+    spull_body<true>(a, dist, L, bitmaps + (threadIdx.x >> 5) * (kSpCh / 32), sp_hot_smem);
 }
 
 // rows that began in an earlier unit and end in unit u: min of the crossed
@@ -1447,9 +1487,24 @@ int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa,
     const bool big = g->max_outdeg > kSplit;
     // edge-balanced pull (SP_SSSP_PULL_TILES=1: the older row-tile kernels)
     const bool units = !getenv("SP_SSSP_PULL_TILES") && g->m > 0;
+    // hot-source snapshot in shared memory (the PageRank hot encoding of
+    // radj), built on the graph's second direction-optimising run like PR's
+    // (SP_SSSP_HOT=0: off, =1: from the first run)
+    const char *he = getenv("SP_SSSP_HOT");
+    int H = 0;
+    if (units && !(he && he[0] == '0')) {
+        if (g->sssp_do_runs++ > 0 || (he && he[0] == '1')) SP_TRY(pr_hot_build(g, c));
+        H = g->pr_H > 0 ? g->pr_H : 0;
+    }
+    int32_t *hotd = nullptr;
+    if (H) SP_TRY(c.alloc(&hotd, H + 4));
+    const size_t hot_smem = (size_t)((H + 3) & ~3) * 4 + (kSpHotBlock / 32) * (kSpCh / 32) * 4;
+    if (H)
+        SP_CUDA(cudaFuncSetAttribute(k_spull_units_hot, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)hot_smem));
     SPull sp{};
     if (units) {
-        sp.radj = g->radj;
+        sp.radj = H ? g->pr_radj_hot : g->radj;
         sp.rw = g->rweff;
         sp.nzend = g->nzend;
         sp.nzrow = g->nzrow;
@@ -1480,7 +1535,12 @@ int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa,
         if (big)
             k_do_push_chunks<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off,
                                                                   g->adj, chunks, D);
-        if (units) {
+        if (units && H) {
+            k_spull_hot_gather<<<std::max(1, (H + 255) / 256), 256, 0, c.stream>>>(
+                D, g->pr_hot_ids, H, dist, hotd);
+            k_spull_units_hot<<<sms, kSpHotBlock, hot_smem, c.stream>>>(sp, dist, D, hotd, H);
+            k_spull_fix<<<grid_for(sp.nunits, 256, c.device), 256, 0, c.stream>>>(sp, dist, D);
+        } else if (units) {
             k_spull_units<<<(int)std::max<int64_t>(1, (sp.nunits + 7) / 8), 256, 0, c.stream>>>(
                 sp, dist, D);
             k_spull_fix<<<grid_for(sp.nunits, 256, c.device), 256, 0, c.stream>>>(sp, dist, D);
@@ -1528,7 +1588,7 @@ int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa,
         cudaEventDestroy(e1);
         *kernel_ms = tot;
         *out = hD->s;
-        c.launches += hD->s.iters * (big ? 8 : 7);
+        c.launches += hD->s.iters * ((big ? 8 : 7) + (H ? 1 : 0));
         return SP_OK;
     }
     SP_CUDA(cudaGraphCreate(&graph, 0));
@@ -1560,7 +1620,7 @@ int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa,
     cudaEventDestroy(ka);
     cudaEventDestroy(kb);
     *out = hD->s;
-    c.launches += hD->s.iters * (big ? 8 : 7);
+    c.launches += hD->s.iters * ((big ? 8 : 7) + (H ? 1 : 0));
     return SP_OK;
 }
 

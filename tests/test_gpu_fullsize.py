@@ -191,6 +191,10 @@ def test_sssp_rmat24_full(rmat24):
                                   dist)
     np.testing.assert_array_equal(
         sp.run(corpus.SSSP_PULL, g, {"src": 0}).env.node_props["dist"], dist)
+    # from the second run on, the pull sweeps read the hot sources' dist from
+    # a shared-memory snapshot
+    np.testing.assert_array_equal(sp.run(corpus.SSSP, g, {"src": 0}).env.node_props["dist"],
+                                  dist)
 
 
 def test_tc_rmat24_sym_full():

@@ -208,6 +208,26 @@ def test_sssp_async_near_far_stress(kind, p0, p1, und, delta, monkeypatch):
     np.testing.assert_array_equal(r.env.node_props["dist"], cpu_ref.sssp(o, 0)[0])
 
 
+@pytest.mark.parametrize("pull_div", ["8", "1"])
+def test_sssp_pull_hot_snapshot(pull_div, monkeypatch):
+    """Direction-optimising SSSP whose pull sweeps read the hottest sources'
+    dist from a shared-memory snapshot (SP_SSSP_HOT=1: from the first run;
+    RMAT-20 qualifies for the hot encoding): the oracle's dist bit for bit,
+    from several sources, also with every iteration after the first a
+    sweep (pull_div 1)."""
+    monkeypatch.setenv("SP_SSSP_DO", "1")
+    monkeypatch.setenv("SP_SSSP_HOT", "1")
+    monkeypatch.setenv("SP_SSSP_PULL_DIV", pull_div)
+    g, o = _pair("rmat", 20, 16, 29, False)
+    for s in (0, 7, g.n // 2):
+        dist, _, rc = cpu_ref.sssp(o, s)
+        assert rc == 0
+        r = sp.run(corpus.SSSP, g, {"src": s})
+        np.testing.assert_array_equal(r.env.node_props["dist"], dist)
+        r = sp.run(corpus.SSSP_PULL, g, {"src": s})
+        np.testing.assert_array_equal(r.env.node_props["dist"], dist)
+
+
 @pytest.mark.parametrize("pull_div", ["8", "1000000"])
 @pytest.mark.parametrize("graph", ["rmat_dir", "rmat_sym", "hub", "multi", "neg_dag"])
 def test_sssp_direction_optimising(graph, pull_div, monkeypatch):

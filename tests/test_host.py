@@ -52,6 +52,17 @@ def test_library_exports_every_declared_symbol():
     assert L.sp_abi_version() == _lib.ABI_VERSION == 4
 
 
+def test_library_has_no_unresolved_internal_symbols():
+    """Every internal (sp::) function the library calls is defined in it --
+    a declaration whose definition landed in an anonymous namespace would
+    only fail at dlopen on the GPU box."""
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("library not built")
+    out = subprocess.run(["nm", "-D", "--undefined-only", _lib.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    assert not re.findall(r"_ZN2sp\w+", out)
+
+
 def test_no_gpu_means_loud_failure():
     if not os.path.exists(_lib.LIB_PATH):
         pytest.skip("library not built")
