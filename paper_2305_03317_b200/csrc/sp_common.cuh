@@ -193,6 +193,11 @@ struct sp_graph {
     int pr_rel = -1;  // -1: not decided, 0: not used, 1: built
     int pr_runs = 0;  // fast single-GPU PR runs started on this graph
     int sssp_do_runs = 0;  // direction-optimising SSSP runs (the hot set is built on the second)
+    // bounded-degree (road-like) graphs: row v's (adj, w_eff) slots at
+    // ell[v * ell_d ...], padded with x = -1 -- an expansion's row is found
+    // from v alone, without the dependent offsets load (asynchronous SSSP)
+    int2 *ell = nullptr;
+    int ell_d = 0;
     int32_t *rel_perm = nullptr, *rel_radj = nullptr, *rel_outdeg = nullptr,
             *rel_indeg = nullptr, *rel_nzrow = nullptr;
     int64_t *rel_nzend = nullptr, *rel_unit_row = nullptr;
@@ -215,6 +220,8 @@ int pr_hot_build(sp_graph *g, Call &c);
 int ensure_weff(sp_graph *g, Call &c);
 // Reverse-slot weights rweff[k] = w_eff[reid[k]] (undirected: w_eff itself).
 int ensure_rweff(sp_graph *g, Call &c);
+// The ELL form above (built once when max out-degree <= d_max; else no-op).
+int ensure_ell(sp_graph *g, Call &c, int d_max);
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 

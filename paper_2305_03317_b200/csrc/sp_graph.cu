@@ -356,6 +356,7 @@ void free_graph(sp_graph *g) {
     resident_free(g->w);
     resident_free(g->weff);
     if (g->directed) resident_free(g->rweff);
+    resident_free(g->ell);
     resident_free(g->outdeg);
     if (g->directed) {
         resident_free(g->roff);
@@ -842,6 +843,36 @@ __global__ void k_rweff(const int32_t *__restrict__ weff, const int64_t *__restr
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
          k += (int64_t)gridDim.x * blockDim.x)
         rw[k] = weff[reid[k]];
+}
+
+__global__ void k_ell_fill(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+                           const int32_t *__restrict__ weff, int64_t n, int d, int2 *ell) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / d, k = i - v * d;
+        const int64_t e = off[v] + k;
+        ell[i] = e < off[v + 1] ? make_int2(adj[e], weff[e]) : make_int2(-1, 0);
+    }
+}
+
+int ensure_ell(sp_graph *g, Call &c, int d_max) {
+    std::lock_guard<std::mutex> lk(g_lazy_mu);
+    if (g->ell || g->max_outdeg > d_max || g->n == 0) return SP_OK;
+    int d = 2;  // rows are read as 16-byte pairs of slots
+    while (d < g->max_outdeg) d <<= 1;
+    int2 *ell = nullptr;
+    SP_TRY(dalloc(&ell, g->n * d));
+    k_ell_fill<<<gridN(g->n * d, c.device), 256, 0, c.stream>>>(g->off, g->adj, g->weff, g->n, d,
+                                                                 ell);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+    if (e != cudaSuccess) {
+        resident_free(ell);
+        SP_CUDA(e);
+    }
+    g->ell = ell;
+    g->ell_d = d;
+    return SP_OK;
 }
 
 int ensure_rweff(sp_graph *g, Call &c) {

@@ -476,6 +476,7 @@ struct AsyncNf {
     int64_t T, delta;
     int64_t phases;
     unsigned long long relaxed, expanded, batches;
+    unsigned long long far_scanned, between_cycles;  // diagnostics (SP_SSSP_TRACE)
 };
 
 constexpr int kAsyncBlock = 1024;  // launch bound; the launch uses kAsyncThreads
@@ -483,6 +484,7 @@ constexpr int kAsyncThreads = 256;
 constexpr unsigned kAsyncBackoff = 256;
 constexpr int kTailStride = 16;    // one 128-byte line per ring tail
 constexpr int kOwnShift = 6;       // 64 consecutive vertices per ring chunk
+constexpr int kEllMaxDeg = 8;      // ELL rows for graphs with max out-degree <= 8
 constexpr long long kAsyncWatchdog = 1ll << 35;  // cycles (~17 s): a hang becomes a fallback
 
 __device__ __forceinline__ int async_owner(int32_t x, int nring) {
@@ -539,10 +541,15 @@ __device__ __forceinline__ void async_push_far(AsyncNf *A, int fc, bool far, int
     if (far && pos < A->fcap) A->far[fc][pos] = x;  // far_n still counts an overflow
 }
 
+// kD > 0: bounded-degree graphs in the ELL form (g->ell, kD slots per row):
+// a lane loads its vertex's whole row (one or two 16-byte loads) from v
+// alone, in parallel with the dequeue atomic -- no dependent offsets load
+// on the hop chain.  kD == 0: CSR rows, flattened over the warp.
+template <int kD>
 __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
     unsigned long long *dq, int32_t *last, const int32_t *__restrict__ weff,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, AsyncNf *A,
-    unsigned async_max_backoff) {
+    const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+    const int2 *__restrict__ ell, AsyncNf *A, unsigned async_max_backoff) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned long long s_head;  // this block's ring: next entry to pop
@@ -590,6 +597,68 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
             batches++;
             int32_t v = (int)lane < k ? sv : -1;
             if (v >= 0) myring[h + lane] = -1;  // the slot is reused next phase
+            if constexpr (kD > 0) {
+                // slot p of the batch (vertex p / kD, its slot p % kD) goes
+                // to lane p % 32 in round p / 32: the slot loads need only
+                // the popped ids, so they are issued before the dequeue
+                // atomics return, and a batch's relaxations share one push
+                // round per 32 slots (as the CSR path's flattening does)
+                constexpr int kLog = kD == 2 ? 1 : kD == 4 ? 2 : 3;
+                const int nslot = k * kD;
+                int2 s[kD];
+#pragma unroll
+                for (int r = 0; r < kD; r++) {
+                    const int pp = r * 32 + (int)lane;
+                    const int32_t vj = __shfl_sync(0xffffffffu, v, (pp >> kLog) & 31);
+                    s[r] = pp < nslot && vj >= 0 ? __ldg(ell + (size_t)vj * kD + (pp & (kD - 1)))
+                                                 : make_int2(-1, 0);
+                }
+                int dv = 0;
+                bool act = false;
+                if (v >= 0) {
+                    const int lst = __ldcg(last + v);
+                    dv = (int)(atomicAnd(dq + v, ~1ull) >> 1);
+                    act = dv < lst;  // not yet expanded at this distance
+                    if (act) {
+                        last[v] = dv;
+                        expanded++;
+                    }
+                }
+                const int64_t total = (int64_t)__popc(__ballot_sync(0xffffffffu, act)) * kD;
+                unsigned long long tok = 0;
+                if (lane == 0 && total)
+                    tok = atomicAdd(reinterpret_cast<unsigned long long *>(&A->work),
+                                    (unsigned long long)total);
+                long long pushed = 0;
+#pragma unroll
+                for (int r = 0; r < kD; r++) {
+                    if (r * 32 >= nslot) break;  // warp-uniform
+                    const int pp = r * 32 + (int)lane;
+                    const int du = __shfl_sync(0xffffffffu, dv, (pp >> kLog) & 31);
+                    const bool aj = __shfl_sync(0xffffffffu, act, (pp >> kLog) & 31);
+                    const bool live = pp < nslot && aj && s[r].x >= 0;
+                    const unsigned rm = __ballot_sync(0xffffffffu, live);
+                    if (lane == 0) relaxed += __popc(rm);
+                    bool near = false, far = false;
+                    const int64_t cand = (int64_t)du + (int64_t)s[r].y;
+                    if (live && cand < (int64_t)kIntMax) {
+                        const bool nb = cand < T;
+                        const unsigned long long old = atomicMin(
+                            dq + s[r].x, ((unsigned long long)cand << 1) | (nb ? 1ull : 0ull));
+                        if ((long long)(old >> 1) > cand) {
+                            if (nb) near = (old & 1ull) == 0;
+                            else far = true;
+                        }
+                    }
+                    pushed += async_push_near(A, near, s[r].x, lane, true, tok);
+                    async_push_far(A, fc, far, s[r].x, lane);
+                }
+                __syncwarp();
+                if (lane == 0)
+                    atomicAdd(reinterpret_cast<unsigned long long *>(&A->work),
+                              (unsigned long long)(-(long long)(k + total - pushed)));
+                continue;
+            }
             int dv = 0;
             int64_t beg = 0, deg = 0;
             if (v >= 0) {
@@ -662,6 +731,7 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
                 atomicAdd(reinterpret_cast<unsigned long long *>(&A->work),
                           (unsigned long long)(-(long long)(k + total - pushed)));
         }
+        const long long t_drained = clock64();
         grid.sync();
         if (threadIdx.x == 0) {  // drained: every ring restarts at slot 0
             s_head = 0;
@@ -672,6 +742,7 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
             const unsigned long long nf = A->far_n[src];
             int go = 1;
             A->phases++;
+            A->far_scanned += nf;
             if (A->abort) {
                 go = 0;
             } else if (nf > A->fcap) {
@@ -714,6 +785,8 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
             }
         }
         grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            A->between_cycles += (unsigned long long)(clock64() - t_drained);
     }
     relaxed = warp_sum(relaxed);
     expanded = warp_sum(expanded);
@@ -753,8 +826,11 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t src, int64_
     const char *thr = getenv("SP_NF_ASYNC_THREADS");  // threads per block (sweeps)
     const int threads = thr ? std::max(32, std::min(kAsyncBlock, atoi(thr) / 32 * 32))
                             : kAsyncThreads;
+    // bounded-degree graphs: the ELL row form (SP_NF_ELL=0: CSR rows)
+    const char *ee = getenv("SP_NF_ELL");
+    if (!(ee && ee[0] == '0')) SP_TRY(ensure_ell(g, c, kEllMaxDeg));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nf_async, threads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nf_async<0>, threads, 0);
     const char *bps = getenv("SP_NF_ASYNC_BPS");  // blocks per SM (sweeps)
     const int want = bps ? std::max(1, atoi(bps)) : kAsyncBlocksPerSm;
     const int nring = sms * std::max(1, std::min(per_sm, want));  // one ring per block
@@ -799,14 +875,18 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t src, int64_
     init.T = delta;
     init.delta = delta;
     SP_CUDA(cudaMemcpyAsync(A, &init, sizeof(AsyncNf), cudaMemcpyHostToDevice, c.stream));
-    void *kargs[] = {&dq, &last, (void *)&g->weff, (void *)&g->off, (void *)&g->adj, &A,
-                     &max_backoff};
+    const int2 *ell = g->ell;
+    void *kargs[] = {&dq, &last, (void *)&g->weff, (void *)&g->off, (void *)&g->adj, (void *)&ell,
+                     &A, &max_backoff};
+    const void *kfn = g->ell_d == 2   ? (const void *)k_nf_async<2>
+                      : g->ell_d == 4 ? (const void *)k_nf_async<4>
+                      : g->ell_d == 8 ? (const void *)k_nf_async<8>
+                                      : (const void *)k_nf_async<0>;
     cudaEvent_t ka, kb;
     SP_CUDA(cudaEventCreate(&ka));
     SP_CUDA(cudaEventCreate(&kb));
     cudaEventRecord(ka, c.stream);
-    SP_CUDA(cudaLaunchCooperativeKernel((const void *)k_nf_async, nring, threads, kargs, 0,
-                                        c.stream));
+    SP_CUDA(cudaLaunchCooperativeKernel(kfn, nring, threads, kargs, 0, c.stream));
     k_async_out<<<grid_for(n, kBlock, c.device), kBlock, 0, c.stream>>>(dq, dist, n);
     cudaEventRecord(kb, c.stream);
     c.launches += 2;
@@ -823,9 +903,10 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t src, int64_
     static const bool trace = getenv("SP_SSSP_TRACE") != nullptr;
     if (trace)
         fprintf(stderr, "sssp async: %d blocks x %d threads, ring %llu, %lld phases, %llu "
-                        "batches, %llu expansions, %llu relaxations, status %d, %.2f ms\n",
+                        "batches, %llu expansions, %llu relaxations, status %d, %.2f ms; far "
+                        "entries split %llu, between-phase cycles (block 0) %llu\n",
                 nring, threads, cap, (long long)hA->phases, hA->batches, hA->expanded,
-                hA->relaxed, hA->status, *kernel_ms);
+                hA->relaxed, hA->status, *kernel_ms, hA->far_scanned, hA->between_cycles);
     out->iters = hA->phases;
     out->relaxed = (int64_t)hA->relaxed;
     out->frontier_sum = (int64_t)hA->expanded;
