@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 4
+#define SP_ABI_VERSION 5
 
 enum sp_status {
     SP_OK = 0,
@@ -216,13 +216,22 @@ int sp_bc(sp_graph *g, const int32_t *srcs, int64_t nsrc, unsigned flags,
  * in [v0, v1); directed graphs -- the program's middle vertex v in [v0, v1). */
 int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_stats *st);
 
-/* Generic forall/reduction (corpus/programs/reduction.sp:5-10 and programs
- * of its shape): for every v, sum an int64 node property over N(v)
- * (reverse = 0, g.neighbors) or over nodesTo(v) (reverse = 1); exact.
- * prop == NULL: every property is 1 (attachNodeProperty(prop = 1)).
- * per_vertex[n] (may be NULL) gets the row sums, *total their sum. */
+/* Generic forall/reduction (corpus/programs/reduction.sp:5-10 and the
+ * programs of its shape the host layer recognises, paper_2305_03317_b200/
+ * forall.py): for every v, reduce a per-slot term over N(v) (reverse = 0,
+ * g.neighbors) or over nodesTo(v) (reverse = 1); exact in any order.
+ *   SP_REDUCE_SUM_I64: term = prop[u] (int64 node property) or, prop ==
+ *     NULL, the constant iterm; per_vertex / total are int64.
+ *   SP_REDUCE_MIN_F64 / SP_REDUCE_MAX_F64: term = the constant dterm;
+ *     per_vertex / total are double, +inf / -inf for no slot.
+ * per_vertex[n] (may be NULL) gets the row results, *total their reduction.
+ * sp_neighbor_sum is the SUM form with iterm = 1. */
+enum sp_reduce_op { SP_REDUCE_SUM_I64 = 0, SP_REDUCE_MIN_F64 = 1, SP_REDUCE_MAX_F64 = 2 };
 int sp_neighbor_sum(sp_graph *g, const int64_t *prop, int mem, int reverse,
                     int64_t *per_vertex, int64_t *total, sp_stats *st);
+int sp_neighbor_reduce(sp_graph *g, int op, int reverse, int64_t iterm, double dterm,
+                       const int64_t *prop, int mem, void *per_vertex, void *total,
+                       sp_stats *st);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SP_LIB") or os.path.join(HERE, "libstarplat_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "starplat_b200.h")
 
-ABI_VERSION = 4  # must equal SP_ABI_VERSION in include/starplat_b200.h
+ABI_VERSION = 5  # must equal SP_ABI_VERSION in include/starplat_b200.h
 
 SP_OK = 0
 SP_ERR_ARG = -1
@@ -35,6 +35,7 @@ SP_FLAG_DETERMINISTIC = 1
 SP_ARR_OFFSETS, SP_ARR_ADJ, SP_ARR_WEIGHTS, SP_ARR_REV_OFFSETS, \
     SP_ARR_REV_ADJ, SP_ARR_REV_EID, SP_ARR_WEFF = range(7)
 SP_GEN_RMAT, SP_GEN_UNIFORM, SP_GEN_GRID = range(3)
+SP_REDUCE_SUM_I64, SP_REDUCE_MIN_F64, SP_REDUCE_MAX_F64 = range(3)
 
 
 class Stats(C.Structure):
@@ -89,6 +90,7 @@ SIGNATURES = {
     "sp_bc": (_int, [_p, _p, _i64, _u, _p, _p, _p, _int, _p]),
     "sp_tc": (_int, [_p, _i64, _i64, _p, _p]),
     "sp_neighbor_sum": (_int, [_p, _p, _int, _int, _p, _p, _p]),
+    "sp_neighbor_reduce": (_int, [_p, _int, _int, _i64, _d, _p, _int, _p, _p, _p]),
 }
 
 _lib = None

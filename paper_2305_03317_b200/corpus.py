@@ -82,11 +82,13 @@ def identify(tp, function: str | None = None) -> Program:
             return BY_KEY[tp]
         except KeyError:
             raise UnsupportedProgramError(f"unknown corpus program {tp!r}") from None
+    if getattr(tp, "key", None) == "forall":  # an already recognised ForallProgram
+        return tp.function(function)
     fn = tp.function(function)  # KeyError for an unknown name, like interp.run
     prog = _BY_PRINT.get(fingerprint(fn))
     if prog is None:
-        raise UnsupportedProgramError(
-            f"function '{getattr(fn, 'name', '?')}' is not one of the corpus programs "
-            "(sssp, sssp_pull, pr, bc, tc, reduction) that the B200 backend executes; "
-            "there is no CPU fallback")
+        # not a corpus program: the generic forall / neighbour-reduction shape
+        # (forall.py), or UnsupportedProgramError -- there is no CPU fallback
+        from . import forall
+        return forall.match(fn)
     return prog

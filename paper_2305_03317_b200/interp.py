@@ -262,6 +262,14 @@ def run(tp, g, args: dict, function: str | None = None,
         _raise_for(rc, E, None, cap, None)
         env.node_props = {"prop": np.ones(n, dtype=np.int64)}
         env.scalars = {"accum": int(tot.value)}
+    elif prog.key == "forall":  # the generic neighbour-reduction shape (forall.py)
+        from . import forall
+        props, scalars, fst = forall.execute(prog, dg)
+        env.node_props = props
+        env.scalars = scalars
+        st.kernel_launches = fst["kernel_launches"]
+        st.device_ms = fst["device_ms"]
+        st.edges_visited = fst["edges_visited"]
     elif prog.key == "tc":
         cnt = C.c_uint64()
         rc = L.sp_tc(dg.handle, 0, n, C.byref(cnt), C.byref(st))
