@@ -427,6 +427,9 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
     out = {}
     reps = 3
 
+    def K(line):  # the committed per-line DRAM capture is of a one-GPU run
+        return line if world == 1 else None
+
     def go(prog, g, args):
         if world == 1:
             return sp.run(prog, g, args, device_outputs=True)
@@ -446,7 +449,7 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
             mb = 12 * R + 20 * F
         rel = (r.stats["edges_visited"] / (ms / reps / 1e3) / 1e9) if world == 1 else None
         out["sssp_cfg1"] = _line("sssp", "rmat16 directed", g, ms / reps, m_reached, mb,
-                                 hbm_peak, key="sssp_cfg1",
+                                 hbm_peak, key=K("sssp_cfg1"),
                                  iterations=r.fixedpoint_iterations["finished"],
                                  first_call_ms=fc[0],
                                  relaxations_g_per_s=rel,
@@ -463,7 +466,7 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         if world == 1:
             mb = 12 * r.stats["edges_visited"] + 20 * r.stats["vertices_visited"]
         out["sssp_cfg5_grid"] = _line("sssp", "grid 4096x4096 undirected, w U[1,100]", g, ms / 2,
-                                      g.m, mb, hbm_peak, key="sssp_grid",
+                                      g.m, mb, hbm_peak, key=K("sssp_grid"),
                                       iterations=r.fixedpoint_iterations["finished"],
                                       first_call_ms=fc[0],
                                       note="GTEPS = m / time (every vertex reached); "
@@ -472,7 +475,7 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         ms, _, r = timed(lambda: go(corpus.PR, g, PR_ARGS), 8, 2, world, dev)  # ~1 ms runs
         it = r.env.scalars["iter"]
         out["pr_cfg5_grid"] = _line("pr", "grid 4096x4096 undirected", g, ms / 8, it * g.m,
-                                    it * (12 * g.m + 36 * g.n), hbm_peak, key="pr_grid",
+                                    it * (12 * g.m + 36 * g.n), hbm_peak, key=K("pr_grid"),
                                     iterations=it)
         g.close()
     if "bc" in a.algos:
@@ -483,7 +486,7 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         ms, _, r = timed(lambda: go(corpus.BC, g, {"sourceSet": srcs}), 1, 2, world, dev)
         st = r.stats  # summed over ranks when sharded
         out["bc_cfg4"] = _line("bc", "rmat20 symmetrized", g, ms, st["edges_visited"],
-                               st["model_bytes"], hbm_peak, key="bc_cfg4", sources=256,
+                               st["model_bytes"], hbm_peak, key=K("bc_cfg4"), sources=256,
                                sharding=f"sources/{world}",
                                note="GTEPS = slots of the reached vertices summed over "
                                     "sources / time; frac: SURVEY 8d's per-source model (48 "
@@ -499,7 +502,7 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         ms, _, r = timed(lambda: go(corpus.TC, g, {}), reps, 1, world, dev)
         mb = r.stats.get("model_bytes")
         out["tc_cfg3"] = _line("tc", "uniform 2^24 / 2^28 undirected", g, ms / reps,
-                               g.m // 2, mb, hbm_peak, key="tc_cfg3",
+                               g.m // 2, mb, hbm_peak, key=K("tc_cfg3"),
                                first_call_ms=fc[0], upper_csr_build_ms=fc[0] - ms / reps,
                                triangles=r.env.scalars["triangle_count"],
                                sharding=f"ranges/{world}")
@@ -511,7 +514,7 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         ms, _, r = timed(lambda: go(corpus.PR, g, PR_ARGS), 3, 2, world, dev)
         it = r.env.scalars["iter"]
         out["pr_rmat24"] = _line("pr", "rmat24 directed", g, ms / 3, it * g.m,
-                                 it * (12 * g.m + 36 * g.n), hbm_peak, key="pr_rmat24",
+                                 it * (12 * g.m + 36 * g.n), hbm_peak, key=K("pr_rmat24"),
                                  iterations=it, first_calls_ms=fc)
         fc = first_calls(lambda: go(corpus.SSSP, g, {"src": 0}), 1, dev)  # + w_eff, rweff
         ms, _, r = timed(lambda: go(corpus.SSSP, g, {"src": 0}), 3, 2, world, dev)
@@ -523,7 +526,7 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         if world == 1:
             mb = 12 * r.stats["edges_visited"] + 20 * r.stats["vertices_visited"]
         out["sssp_rmat24"] = _line("sssp", "rmat24 directed", g, ms / 3, m_reached, mb, hbm_peak,
-                                   key="sssp_rmat24", first_call_ms=fc[0],
+                                   key=K("sssp_rmat24"), first_call_ms=fc[0],
                                    iterations=r.fixedpoint_iterations["finished"],
                                    note="12 B per relaxation (push) or swept in-slot (pull sweeps, "
                                         "frontier > n/8) + 20 B per frontier vertex")
@@ -532,7 +535,7 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         fc = first_calls(lambda: go(corpus.TC, g, {}), 1, dev)  # + the upper CSR build
         ms, _, r = timed(lambda: go(corpus.TC, g, {}), 2, 1, world, dev)
         out["tc_rmat24"] = _line("tc", "rmat24 symmetrized", g, ms / 2, g.m // 2,
-                                 r.stats.get("model_bytes"), hbm_peak, key="tc_rmat24",
+                                 r.stats.get("model_bytes"), hbm_peak, key=K("tc_rmat24"),
                                  first_call_ms=fc[0], upper_csr_build_ms=fc[0] - ms / 2,
                                  triangles=r.env.scalars["triangle_count"],
                                  sharding=f"ranges/{world}")

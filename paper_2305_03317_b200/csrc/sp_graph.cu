@@ -860,8 +860,18 @@ int ensure_ell(sp_graph *g, Call &c, int d_max) {
     if (g->ell || g->max_outdeg > d_max || g->n == 0) return SP_OK;
     int d = 2;  // rows are read as 16-byte pairs of slots
     while (d < g->max_outdeg) d <<= 1;
+    // an optional copy: skipped (CSR rows) when it would not fit comfortably
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return SP_OK;
+    }
+    if ((double)g->n * d * sizeof(int2) > 0.25 * (double)fr) return SP_OK;
     int2 *ell = nullptr;
-    SP_TRY(dalloc(&ell, g->n * d));
+    if (dalloc(&ell, g->n * d) != SP_OK) {
+        cudaGetLastError();
+        return SP_OK;
+    }
     k_ell_fill<<<gridN(g->n * d, c.device), 256, 0, c.stream>>>(g->off, g->adj, g->weff, g->n, d,
                                                                  ell);
     cudaError_t e = cudaGetLastError();

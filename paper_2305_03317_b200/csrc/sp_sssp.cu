@@ -1574,7 +1574,9 @@ int sssp_do_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa,
     const char *he = getenv("SP_SSSP_HOT");
     int H = 0;
     if (units && !(he && he[0] == '0')) {
-        if (g->sssp_do_runs++ > 0 || (he && he[0] == '1')) SP_TRY(pr_hot_build(g, c));
+        // an optimisation: a failed build (e.g. out of memory) keeps the plain sweep
+        if ((g->sssp_do_runs++ > 0 || (he && he[0] == '1')) && pr_hot_build(g, c) != SP_OK)
+            cudaGetLastError();
         H = g->pr_H > 0 ? g->pr_H : 0;
     }
     int32_t *hotd = nullptr;
