@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 5
+#define SP_ABI_VERSION 6
 
 enum sp_status {
     SP_OK = 0,
@@ -202,6 +202,27 @@ int sp_pagerank_shard_create(sp_graph *g, int64_t v0, int64_t v1, double damping
 int sp_pagerank_shard_step(sp_pagerank_shard *h, const double *contrib_in,
                            double *rank_local, double *contrib_out, double *diff);
 void sp_pagerank_shard_destroy(sp_pagerank_shard *h);
+/* The contrib exchange fused into the step (instead of an all-gather):
+ * sp_pagerank_shard_peers gives the shard nsets x npeers device pointers
+ * (set s, peer q: rank q's contrib array for the iterations of parity s,
+ * global indices; mapped with sp_peer_open); sp_pagerank_shard_step_peers
+ * then also stores every contrib it computes at peers[set][q][v] from the
+ * producing kernel -- over NVLink for other GPUs.  The caller orders the
+ * steps (e.g. the diff all-reduce of each iteration) and alternates sets so
+ * a store never lands in an array a slower rank still reads. */
+int sp_pagerank_shard_peers(sp_pagerank_shard *h, int nsets, int npeers,
+                            double *const *peers);
+int sp_pagerank_shard_step_peers(sp_pagerank_shard *h, const double *contrib_in,
+                                 double *rank_local, double *contrib_out, double *diff,
+                                 int set);
+
+/* Peer-mapped device buffers (CUDA IPC): sp_peer_alloc allocates `bytes` on
+ * `device` and writes its 64-byte IPC handle; another process maps it with
+ * sp_peer_open (peer access over NVLink / the same GPU); sp_peer_free
+ * unmaps (opened = 1) or frees (opened = 0). */
+int sp_peer_alloc(int device, int64_t bytes, void **ptr, void *handle);
+int sp_peer_open(int device, const void *handle, void **ptr);
+void sp_peer_free(void *ptr, int opened);
 
 /* corpus/programs/bc.sp over srcs in list order (duplicates re-run).
  * bc[n] accumulated; sigma/delta[n] of the LAST source (may be NULL). */

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SP_LIB") or os.path.join(HERE, "libstarplat_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "starplat_b200.h")
 
-ABI_VERSION = 5  # must equal SP_ABI_VERSION in include/starplat_b200.h
+ABI_VERSION = 6  # must equal SP_ABI_VERSION in include/starplat_b200.h
 
 SP_OK = 0
 SP_ERR_ARG = -1
@@ -87,6 +87,11 @@ SIGNATURES = {
     "sp_pagerank_shard_create": (_int, [_p, _i64, _i64, _d, _u, _p, _p]),
     "sp_pagerank_shard_step": (_int, [_p, _p, _p, _p, _p]),
     "sp_pagerank_shard_destroy": (None, [_p]),
+    "sp_pagerank_shard_peers": (_int, [_p, _int, _int, _p]),
+    "sp_pagerank_shard_step_peers": (_int, [_p, _p, _p, _p, _p, _int]),
+    "sp_peer_alloc": (_int, [_int, _i64, _p, _p]),
+    "sp_peer_open": (_int, [_int, _p, _p]),
+    "sp_peer_free": (None, [_p, _int]),
     "sp_bc": (_int, [_p, _p, _i64, _u, _p, _p, _p, _int, _p]),
     "sp_tc": (_int, [_p, _i64, _i64, _p, _p]),
     "sp_neighbor_sum": (_int, [_p, _p, _int, _int, _p, _p, _p]),

@@ -49,6 +49,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 #include <utility>
 
@@ -98,7 +99,17 @@ struct PrArgs {
     double base, damping;
     double *diff_slot;
     struct PrLoop *loop;  // device loop state (cin/cout/slot come from it) or null
+    // multi-GPU shards: every contrib this block computes is also stored at
+    // peers[q][v] (v global) -- the other ranks' contrib arrays, mapped over
+    // NVLink (CUDA IPC): the exchange rides on the producing kernel
+    double *const *peers;
+    int npeers;
 };
+
+__device__ __forceinline__ void pr_store_contrib(const PrArgs &a, int64_t v, double c) {
+    a.cout[v - a.v0] = c;
+    for (int q = 0; q < a.npeers; q++) a.peers[q][v] = c;
+}
 
 // Device-side fixedPoint loop state (pr.sp:10), one per call, in the
 // argument block of the thread's cached executable (ArgExec): every per-call
@@ -170,7 +181,7 @@ __device__ __forceinline__ double pr_apply(const PrArgs &a, int64_t v, double su
     if (d < 0.0) d = __dsub_rn(0.0, d);
     a.rank[lv] = nr;
     const int od = __ldg(a.outdeg + v);
-    a.cout[lv] = od > 0 ? __ddiv_rn(nr, (double)od) : 0.0;
+    pr_store_contrib(a, v, od > 0 ? __ddiv_rn(nr, (double)od) : 0.0);
     return d;
 }
 
@@ -421,7 +432,7 @@ __global__ void __launch_bounds__(256) k_pr_epi(PrArgs a) {
         if (d < 0.0) d = __dsub_rn(0.0, d);
         dmax = fmax(dmax, d);
         a.rank[v[j] - a.v0] = nr;
-        a.cout[v[j] - a.v0] = od[j] > 0 ? __ddiv_rn(nr, (double)od[j]) : 0.0;
+        pr_store_contrib(a, v[j], od[j] > 0 ? __ddiv_rn(nr, (double)od[j]) : 0.0);
     }
     block_diff(a, dmax);
 }
@@ -1550,7 +1561,20 @@ struct sp_pagerank_shard {
     FastPlan plan;
     void *keep[32];
     int nkeep = 0;
+    double **peers = nullptr;  // device: nsets x npeers contrib-array pointers
+    int npeers = 0, nsets = 0;
 };
+
+// Deterministic-mode form of the peer stores: the block's contribs to every
+// peer's array (the exact kernel writes contrib_out only).
+__global__ void k_pr_scatter_peers(const double *__restrict__ cout, int64_t v0, int64_t nb,
+                                   double *const *peers, int npeers) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double c = cout[i];
+        for (int q = 0; q < npeers; q++) peers[q][v0 + i] = c;
+    }
+}
 
 extern "C" int sp_pagerank_block_init(sp_graph *g, int64_t v0, int64_t v1, double *rank_local,
                                       double *contrib_out) {
@@ -1594,8 +1618,42 @@ extern "C" int sp_pagerank_shard_create(sp_graph *g, int64_t v0, int64_t v1, dou
     return SP_OK;
 }
 
+extern "C" int sp_pagerank_shard_peers(sp_pagerank_shard *h, int nsets, int npeers,
+                                       double *const *peers) {
+    SP_CHECK(h && nsets >= 1 && npeers >= 1 && npeers <= 1024 && peers, SP_ERR_ARG,
+             "sp_pagerank_shard_peers: bad arguments");
+    Call c;
+    SP_TRY(c.begin(h->g->device));
+    double **d = nullptr;
+    SP_TRY(resident_alloc((void **)&d, (size_t)nsets * npeers * sizeof(double *)));
+    SP_CUDA(cudaMemcpyAsync(d, peers, (size_t)nsets * npeers * sizeof(double *),
+                            cudaMemcpyHostToDevice, c.stream));
+    SP_TRY(c.finish(nullptr));
+    if (h->peers) resident_free(h->peers);
+    h->peers = d;
+    h->npeers = npeers;
+    h->nsets = nsets;
+    return SP_OK;
+}
+
+static int shard_step(sp_pagerank_shard *h, const double *contrib_in, double *rank_local,
+                      double *contrib_out, double *diff, int set);
+
+extern "C" int sp_pagerank_shard_step_peers(sp_pagerank_shard *h, const double *contrib_in,
+                                            double *rank_local, double *contrib_out,
+                                            double *diff, int set) {
+    SP_CHECK(h && h->peers && set >= 0 && set < h->nsets, SP_ERR_ARG,
+             "sp_pagerank_shard_step_peers: no peer set %d", set);
+    return shard_step(h, contrib_in, rank_local, contrib_out, diff, set);
+}
+
 extern "C" int sp_pagerank_shard_step(sp_pagerank_shard *h, const double *contrib_in,
                                       double *rank_local, double *contrib_out, double *diff) {
+    return shard_step(h, contrib_in, rank_local, contrib_out, diff, -1);
+}
+
+static int shard_step(sp_pagerank_shard *h, const double *contrib_in, double *rank_local,
+                      double *contrib_out, double *diff, int set) {
     SP_CHECK(h && contrib_in && rank_local && contrib_out && diff, SP_ERR_ARG,
              "sp_pagerank_shard_step: bad arguments");
     sp_graph *g = h->g;
@@ -1603,15 +1661,26 @@ extern "C" int sp_pagerank_shard_step(sp_pagerank_shard *h, const double *contri
     if (h->stream) SP_TRY(c.begin_external(g->device, h->stream));
     else SP_TRY(c.begin(g->device));
     SP_CUDA(cudaMemsetAsync(diff, 0, sizeof(double), c.stream));
+    double *const *peers = set >= 0 ? h->peers + (size_t)set * h->npeers : nullptr;
+    const int np = set >= 0 ? h->npeers : 0;
     if (h->v1 > h->v0) {
         if (h->det) {
             SP_TRY(launch_exact(g, c, h->v0, h->v1, h->damping, contrib_in, rank_local,
                                 contrib_out, diff, nullptr, nullptr));
+            if (np) {
+                k_pr_scatter_peers<<<grid_for(h->v1 - h->v0, 256, c.device), 256, 0, c.stream>>>(
+                    contrib_out, h->v0, h->v1 - h->v0, peers, np);
+                c.launches++;
+            }
         } else {
             // contrib_out is a single persistent buffer here: zero rows are
-            // rewritten every step (cheap: one indeg pass over the block)
-            SP_TRY(launch_fast(c, h->plan, g, h->v1, contrib_in, rank_local, contrib_out,
-                               nullptr, true, diff, nullptr, nullptr));
+            // rewritten every step (cheap: one indeg pass over the block);
+            // with peers, the epilogue also stores every contrib into them
+            FastPlan plan = h->plan;
+            plan.a.peers = peers;
+            plan.a.npeers = np;
+            SP_TRY(launch_fast(c, plan, g, h->v1, contrib_in, rank_local, contrib_out, nullptr,
+                               true, diff, nullptr, nullptr));
         }
     }
     SP_CUDA(cudaGetLastError());
@@ -1624,6 +1693,40 @@ extern "C" void sp_pagerank_shard_destroy(sp_pagerank_shard *h) {
     cudaSetDevice(h->g->device);
     cudaDeviceSynchronize();
     for (int i = 0; i < h->nkeep; i++) scratch_free(h->keep[i], nullptr);
+    if (h->peers) resident_free(h->peers);
     cudaDeviceSynchronize();
     delete h;
+}
+
+// ---- peer-mapped buffers (CUDA IPC: other processes' GPUs over NVLink) ----
+extern "C" int sp_peer_alloc(int device, int64_t bytes, void **ptr, void *handle) {
+    SP_CHECK(ptr && handle && bytes > 0, SP_ERR_ARG, "sp_peer_alloc: bad arguments");
+    SP_CUDA(cudaSetDevice(device));
+    // plain cudaMalloc: IPC handles need it (not the stream-ordered pool)
+    SP_CUDA(cudaMalloc(ptr, (size_t)bytes));
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, *ptr);
+    if (e != cudaSuccess) {
+        cudaFree(*ptr);
+        *ptr = nullptr;
+        SP_CUDA(e);
+    }
+    memcpy(handle, &h, sizeof(h));
+    return SP_OK;
+}
+
+extern "C" int sp_peer_open(int device, const void *handle, void **ptr) {
+    SP_CHECK(ptr && handle, SP_ERR_ARG, "sp_peer_open: bad arguments");
+    SP_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    SP_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return SP_OK;
+}
+
+extern "C" void sp_peer_free(void *ptr, int opened) {
+    if (!ptr) return;
+    cudaDeviceSynchronize();
+    if (opened) cudaIpcCloseMemHandle(ptr);
+    else cudaFree(ptr);
 }

@@ -13,10 +13,15 @@ trident/bsp.py; its ownership rule is graph.py:226-249):
 * TC  -- vertex ranges balanced by a sum-of-squared-degree work proxy, graph
          replicated; one integer ``all_reduce(sum)`` (exact).
 * PR  -- block partition, planned once per run; per iteration a local pull
-         over the owned block, ``all_reduce(max)`` of diff (the scalar merge,
-         bsp.py:322-330) and ``all_gather`` of the owned contrib slices (the
-         reference's remote-read snapshot, bsp.py:182-185/287-288), all
-         queued on the device; one host read per iteration (convergence).
+         over the owned block whose epilogue also stores every contrib it
+         computes straight into every rank's contrib array for the next
+         iteration (peer memory: CUDA IPC, NVLink between GPUs; two arrays
+         alternate by iteration parity) -- the reference's remote-read
+         snapshot (bsp.py:182-185/287-288) without a separate collective --
+         then ``all_reduce(max)`` of diff (the scalar merge, bsp.py:322-330),
+         which also orders every rank's stores before the next step.  With
+         SP_PR_EXCHANGE=nccl, or where peer mapping fails, an ``all_gather``
+         of the owned slices after the step.  One host read per iteration.
 * SSSP -- owner-computes over the block partition: per superstep each rank
          relaxes its owned frontier (one pass, or to a local fixpoint);
          remote improvements leave as ONE aggregated (vertex, local min)
@@ -150,10 +155,53 @@ class _NativePrShard:
             C.c_void_p(contrib.data_ptr()), C.c_void_p(diff.data_ptr())),
             "sp_pagerank_shard_step")
 
+    # -- the contrib exchange fused into the step (peer stores over NVLink)
+    def peer_setup(self, n, world, me, group):
+        """Map every rank's two contrib arrays (one per iteration parity) into
+        this process (CUDA IPC) and hand them to the shard; returns this
+        rank's own two arrays as device pointers wrapped for reading."""
+        dist = _dist()
+        L, dev = self.be.L, self.be.index
+        self.own, self.opened = [], []
+        handles = []
+        for _ in range(2):
+            ptr, hnd = C.c_void_p(), (C.c_char * 64)()
+            self.be._chk(L.sp_peer_alloc(dev, max(8, 8 * n), C.byref(ptr), hnd),
+                         "sp_peer_alloc")
+            self.own.append(ptr.value)
+            handles.append(bytes(hnd))
+        allh = [None] * world
+        dist.all_gather_object(allh, handles, group=group)
+        table = (C.c_void_p * (2 * world))()
+        for s in range(2):
+            for q in range(world):
+                if q == me:
+                    table[s * world + q] = self.own[s]
+                else:
+                    p = C.c_void_p()
+                    hb = (C.c_char * 64).from_buffer_copy(allh[q][s])
+                    self.be._chk(L.sp_peer_open(dev, hb, C.byref(p)), "sp_peer_open")
+                    self.opened.append(p.value)
+                    table[s * world + q] = p.value
+        self.be._chk(L.sp_pagerank_shard_peers(self.h, 2, world, table),
+                     "sp_pagerank_shard_peers")
+        return self.own
+
+    def step_peers(self, contrib_in_ptr, rank, contrib, diff, parity):
+        self.be._chk(self.be.L.sp_pagerank_shard_step_peers(
+            self.h, C.c_void_p(contrib_in_ptr), C.c_void_p(rank.data_ptr()),
+            C.c_void_p(contrib.data_ptr()), C.c_void_p(diff.data_ptr()), int(parity)),
+            "sp_pagerank_shard_step_peers")
+
     def close(self):
         if self.h:
             self.be.L.sp_pagerank_shard_destroy(self.h)
             self.h = C.c_void_p()
+        for p in getattr(self, "opened", []):
+            self.be.L.sp_peer_free(C.c_void_p(p), 1)
+        for p in getattr(self, "own", []):
+            self.be.L.sp_peer_free(C.c_void_p(p), 0)
+        self.opened, self.own = [], []
 
 
 class _NativeShard:
@@ -430,14 +478,40 @@ def _pr(be, g, bound, cap, world, me, group, det, E, prog, tr):
     diff = 0.0
     dt = torch.zeros(1, dtype=torch.float64, device=be.device)
     sh = be.pr_shard(g, v0, v1, bound["damping"], det)  # planned once per run
+    # the contrib exchange: fused into the step as peer stores (each rank's
+    # epilogue writes its contribs straight into every rank's array for the
+    # next iteration, NVLink on a multi-GPU box) or, SP_PR_EXCHANGE=nccl /
+    # backends without peer mapping, an all-gather after the step
+    p2p = (world > 1 and hasattr(sh, "peer_setup")
+           and os.environ.get("SP_PR_EXCHANGE", "p2p") != "nccl")
+    if p2p:  # iteration 1 reads the initial all-gather (`full`), then sets 1, 0, 1, ...
+        try:
+            arrays = sh.peer_setup(g.n, world, me, group)
+            ok = 1
+        except RuntimeError:  # e.g. no peer access / IPC between these processes
+            ok = 0
+        okt = torch.tensor([ok], dtype=torch.int32, device=be.device)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN, group=group)  # every rank or none
+        if not int(okt.item()):
+            p2p = False
+            sh.close()
+            sh = be.pr_shard(g, v0, v1, bound["damping"], det)
     try:
         while True:
             # the step, the max-reduce of diff and the contrib exchange are
             # all queued on the device; the convergence test is the
             # iteration's one host read
-            sh.step(full, rank_l, contrib_l, dt)
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX, group=group)
-            gather()
+            if p2p:
+                # reads set it % 2, stores into every rank's set (it + 1) % 2;
+                # the diff all-reduce orders every rank's stores before any
+                # rank's next step
+                sh.step_peers(arrays[it % 2] if it else full.data_ptr(), rank_l, contrib_l,
+                              dt, (it + 1) % 2)
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX, group=group)
+            else:
+                sh.step(full, rank_l, contrib_l, dt)
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX, group=group)
+                gather()
             diff = float(dt.item())
             it += 1
             iters += 1

@@ -3,7 +3,9 @@
 One GPU is available, so two ranks share cuda:0 over gloo (NCCL refuses two
 ranks on one device); this drives the native block kernels
 (sp_sssp_shard_*: owner-computes SSSP with aggregated messages in both
-exchange forms, sp_pagerank_shard_* (planned once, stream-ordered steps), sp_tc ranges, sp_bc source shares) through the real sharding/exchange logic and checks the results
+exchange forms, sp_pagerank_shard_* (planned once, stream-ordered steps, the
+contrib exchange as peer stores fused into the step -- CUDA IPC between the
+two processes -- and as an all-gather), sp_tc ranges, sp_bc source shares) through the real sharding/exchange logic and checks the results
 against the single-process CPU oracle."""
 
 import os
@@ -73,6 +75,17 @@ def _worker(rank, world, port, kind, q):
         r = parallel.run_sharded(corpus.PR, g, {"damping": 0.85, "epsilon": 1e-6,
                                                 "maxIter": 100}, backend=be)
         out["rank_fast"] = r.env.node_props["rank"]
+        # the same two runs with the all-gather exchange instead of the
+        # peer stores fused into the step (CUDA IPC between the two
+        # processes here; NVLink between GPUs): identical results
+        os.environ["SP_PR_EXCHANGE"] = "nccl"
+        r = parallel.run_sharded(corpus.PR, g, {"damping": 0.85, "epsilon": 1e-6,
+                                                "maxIter": 100}, backend=be, deterministic=True)
+        out["rank_gather"], out["iter_gather"] = r.env.node_props["rank"], r.env.scalars["iter"]
+        r = parallel.run_sharded(corpus.PR, g, {"damping": 0.85, "epsilon": 1e-6,
+                                                "maxIter": 100}, backend=be)
+        out["rank_fast_gather"] = r.env.node_props["rank"]
+        os.environ["SP_PR_EXCHANGE"] = "p2p"
         srcs = list(range(0, 40, 3))
         r = parallel.run_sharded(corpus.BC, g, {"sourceSet": srcs}, backend=be)
         out["bc"] = r.env.node_props["bc"]
@@ -122,5 +135,7 @@ def test_native_sharded_two_ranks(kind):
             sum(s[2][0] + s[2][1] for s in x["steps"]) >= reached - 1
         assert x["rank"].tobytes() == rank_ref.tobytes() and x["iter"] == it_ref
         assert np.abs(x["rank_fast"] - rank_ref).max() <= 1e-12 * np.abs(rank_ref).max()
+        assert x["rank_gather"].tobytes() == rank_ref.tobytes() and x["iter_gather"] == it_ref
+        assert x["rank_fast_gather"].tobytes() == x["rank_fast"].tobytes()
         assert np.abs(x["bc"] - bc_ref).max() <= 1e-9 * max(1.0, np.abs(bc_ref).max())
         assert x["tc"] == tc_ref
