@@ -16,7 +16,7 @@ run() {  # name algo reps [env...] -- the last of `reps` runs is measured (the
 # conditional graph); BC with one worker: NVTX ranges are per host thread
 run pr_cfg2 pr 3 SP_HOSTLOOP=1
 run sssp_cfg1 sssp 2 SP_HOSTLOOP=1
-run sssp_rmat24 sssp_rmat24 2 SP_HOSTLOOP=2
+run sssp_rmat24 sssp_rmat24 3 SP_HOSTLOOP=2
 run sssp_grid sssp_grid 2
 run pr_grid sssp_grid_pr 3 SP_HOSTLOOP=1
 run bc_cfg4 bc256 2 SP_BC_WORKERS=1
