@@ -64,7 +64,10 @@ constexpr int kFilterShift = 20;   // 32 - log2(4096)
 constexpr int kBatch = 32;
 constexpr int kUnroll = 2;         // 16-byte loads in flight per lane in k_tc_fwd_plain
 constexpr int kUnrollHash = 4;     // ... in k_tc_fwd_hash (skewed graphs; 2 is faster on cfg3)
-constexpr int kPad = 8;            // upper rows padded/aligned to 32-byte sectors
+#ifndef SP_TC_PAD
+#define SP_TC_PAD 8
+#endif
+constexpr int kPad = SP_TC_PAD;     // upper rows padded/aligned to 32-byte sectors
 constexpr int kQ = kPad / 4;       // 16-byte quarters per padded block
 
 std::mutex g_up_mu;  // guards the lazy upper-CSR build
