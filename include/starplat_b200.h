@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 6
+#define SP_ABI_VERSION 7
 
 enum sp_status {
     SP_OK = 0,
@@ -174,6 +174,19 @@ int sp_sssp_shard_relax(sp_sssp_shard *h, int64_t max_rounds, int64_t per,
 int sp_sssp_shard_apply(sp_sssp_shard *h, const int64_t *msgs, int64_t k,
                         const int32_t *block, int64_t *frontier);
 void sp_sssp_shard_destroy(sp_sssp_shard *h);
+/* The exchange fused into the relaxation (instead of messages + an
+ * all-to-all): with every rank's dist array, inbox (capacity n) and inbox
+ * tail mapped into this process (sp_peer_alloc / sp_peer_open; over NVLink
+ * between GPUs; indices = ranks, owner = v / per), sp_sssp_shard_relax
+ * lowers a remote vertex's dist in its owner's array directly and, once per
+ * superstep, appends the vertex to the owner's inbox -- counts come back 0.
+ * After every rank's relax has completed (the caller's barrier),
+ * sp_sssp_shard_collect appends this rank's inbox to its frontier, resets
+ * the tail and returns the next frontier size. */
+int sp_sssp_shard_peers(sp_sssp_shard *h, int64_t per, int32_t *const *peer_dist,
+                        int32_t *const *peer_inbox, unsigned long long *const *peer_tail,
+                        int32_t *inbox, unsigned long long *tail);
+int sp_sssp_shard_collect(sp_sssp_shard *h, int64_t *frontier);
 
 /* corpus/programs/pr.sp.  rank[n] = final ranks (== rank_nxt at exit);
  * iter / diff = the program's scalars; iters = fixedPoint iterations. */

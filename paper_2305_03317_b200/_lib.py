@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SP_LIB") or os.path.join(HERE, "libstarplat_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "starplat_b200.h")
 
-ABI_VERSION = 6  # must equal SP_ABI_VERSION in include/starplat_b200.h
+ABI_VERSION = 7  # must equal SP_ABI_VERSION in include/starplat_b200.h
 
 SP_OK = 0
 SP_ERR_ARG = -1
@@ -81,6 +81,8 @@ SIGNATURES = {
     "sp_sssp_shard_relax": (_int, [_p, _i64, _i64, _p, _p, _p]),
     "sp_sssp_shard_apply": (_int, [_p, _p, _i64, _p, _p]),
     "sp_sssp_shard_destroy": (None, [_p]),
+    "sp_sssp_shard_peers": (_int, [_p, _i64, _p, _p, _p, _p, _p]),
+    "sp_sssp_shard_collect": (_int, [_p, _p]),
     "sp_pagerank": (_int, [_p, _d, _d, _i64, _i64, _u, _p, _int, _p, _p, _p,
                            ITER_CB, _p, _p]),
     "sp_pagerank_block_init": (_int, [_p, _i64, _i64, _p, _p]),

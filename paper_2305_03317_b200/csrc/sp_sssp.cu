@@ -1982,6 +1982,17 @@ struct RelaxShardOp {
     int64_t v0, v1;
     int it;      // round stamp (owned vertices)
     int sstamp;  // superstep stamp (remote vertices)
+    // fused exchange (peers != null): a remote winner lowers the owner's
+    // dist in place (peer memory: CUDA IPC, NVLink between GPUs) and, once
+    // per superstep, appends itself to the owner's inbox -- the message
+    // exchange rides on the relaxation kernel; the local dist entry of a
+    // remote vertex stays this rank's best sent value (the pre-filter)
+    int32_t *const *peer_dist;
+    int32_t *const *peer_inbox;
+    unsigned long long *const *peer_tail;
+    int64_t per;
+    unsigned long long inbox_cap;
+    unsigned long long *msg_counts;  // fused: messages sent per owner (the trace)
     __device__ __forceinline__ int payload(int32_t v) const { return __ldcg(dist + v); }
     __device__ __forceinline__ Probe probe(int64_t e, int32_t x) const {
         return Probe{__ldcs(weff + e), __ldcg(dist + x)};
@@ -1998,9 +2009,36 @@ struct RelaxShardOp {
         const int old = atomicMin(dist + x, c);
         if (c >= old) return 0;
         if (x >= v0 && x < v1) return atomicExch(enq + x, it) != it ? 1 : 0;
+        if (peer_dist) {
+            const int64_t r = x / per;
+            if (c < atomicMin(peer_dist[r] + x, c) && atomicExch(enq + x, sstamp) != sstamp) {
+                const unsigned long long pos = atomicAdd(peer_tail[r], 1ull);
+                if (pos < inbox_cap) peer_inbox[r][pos] = x;
+                else atomicAdd(overflow, 1ull << 32);  // inbox overflow (never: capacity n)
+                atomicAdd(msg_counts + r, 1ull);
+            }
+            return 0;
+        }
         return atomicExch(enq + x, sstamp) != sstamp ? 2 : 0;
     }
 };
+
+// Fused-exchange collect: the owner's inbox (vertices other ranks lowered in
+// its dist this superstep) joins its frontier (apply-stamp deduped).
+__global__ void k_shard_collect(const int32_t *__restrict__ inbox, int64_t k, int32_t *enq,
+                                int stamp, int32_t *q, unsigned long long *nq) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < k; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = b + threadIdx.x;
+        bool win = false;
+        int32_t x = 0;
+        if (i < k) {
+            x = __ldcg(inbox + i);
+            win = atomicExch(enq + x, stamp) != stamp;
+        }
+        const int64_t at = warp_append(win, nq);
+        if (win) q[at] = x;
+    }
+}
 
 __global__ void k_shard_init(int32_t *dist, int32_t *enq, int64_t n, int32_t src) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
@@ -2092,11 +2130,18 @@ struct sp_sssp_shard {
     int64_t qcap = 0;
     int round = 0;      // round stamps 1, 2, ...
     int step = 0;       // supersteps done
+    // fused exchange: device tables of every rank's dist / inbox / inbox tail
+    int32_t **peer_dist = nullptr, **peer_inbox = nullptr;
+    unsigned long long **peer_tail = nullptr;
+    int32_t *inbox = nullptr;            // this rank's inbox (peer-mapped, caller-owned)
+    unsigned long long *tail = nullptr;  // its tail
+    int64_t per = 0;
 };
 
 static void shard_free(sp_sssp_shard *h) {
     if (!h) return;
-    void *ps[] = {h->enq, h->q[0], h->q[1], h->ob, h->chunks, h->cnt, h->aux};
+    void *ps[] = {h->enq, h->q[0], h->q[1], h->ob, h->chunks, h->cnt, h->aux, h->peer_dist,
+                  h->peer_inbox, h->peer_tail};
     for (void *p : ps)
         if (p) resident_free(p);
     delete h;
@@ -2171,7 +2216,8 @@ extern "C" int sp_sssp_shard_relax(sp_sssp_shard *h, int64_t max_rounds, int64_t
         SP_CUDA(cudaMemsetAsync(cc, 0, sizeof(ExpandCounters), c.stream));
         RelaxShardOp op{h->dist, h->enq, g->weff, &cc->flag, h->ob, &h->aux[0],
                         (unsigned long long)std::max<int64_t>(1, g->n), h->v0, h->v1,
-                        h->round, h->step};
+                        h->round, h->step, h->peer_dist, h->peer_inbox, h->peer_tail, h->per,
+                        (unsigned long long)std::max<int64_t>(1, g->n), h->aux + 2};
         launch_expand(op, g->off, g->adj, h->q[h->cur], h->nq, h->q[h->cur ^ 1], h->chunks, cc,
                       sms, big, c.stream, &c.launches);
         SP_CUDA(cudaGetLastError());
@@ -2183,9 +2229,25 @@ extern "C" int sp_sssp_shard_relax(sp_sssp_shard *h, int64_t max_rounds, int64_t
         h->cur ^= 1;
         h->nq = (int64_t)hc->next_size;
         if (hc->flag) {
+            SP_CHECK((hc->flag >> 32) == 0, SP_ERR_CUDA, "sp_sssp_shard_relax: inbox overflow");
             overflow = true;
             break;
         }
+    }
+    if (h->peer_dist) {  // fused exchange: the messages are already in the owners' inboxes
+        unsigned long long *hk = reinterpret_cast<unsigned long long *>(hc);
+        SP_CUDA(cudaMemcpyAsync(hk, h->aux + 2, h->world * 8, cudaMemcpyDeviceToHost, c.stream));
+        SP_TRY(c.finish(nullptr));
+        for (int r = 0; r < h->world; r++) counts[r] = (int64_t)hk[r];  // sent (trace only)
+        if (info) {
+            info[0] = updates;
+            info[1] = relaxed;
+            info[2] = rounds;
+            info[3] = h->nq;
+        }
+        SP_CHECK(!overflow, SP_ERR_OVERFLOW,
+                 "SSSP distance left the int32 range (negative weights)");
+        return SP_OK;
     }
     // outbox -> per-owner counts -> packed messages grouped by owner
     unsigned long long *hk = reinterpret_cast<unsigned long long *>(hc);
@@ -2250,6 +2312,62 @@ extern "C" int sp_sssp_shard_apply(sp_sssp_shard *h, const int64_t *msgs, int64_
     SP_TRY(c.finish(nullptr));
     h->nq = (int64_t)hk[0];
     SP_CHECK(h->nq <= h->qcap, SP_ERR_CUDA, "sp_sssp_shard_apply: frontier overflow");
+    if (frontier) *frontier = h->nq;
+    return SP_OK;
+}
+
+extern "C" int sp_sssp_shard_peers(sp_sssp_shard *h, int64_t per, int32_t *const *peer_dist,
+                                   int32_t *const *peer_inbox,
+                                   unsigned long long *const *peer_tail, int32_t *inbox,
+                                   unsigned long long *tail) {
+    SP_CHECK(h && per >= 1 && peer_dist && peer_inbox && peer_tail && inbox && tail, SP_ERR_ARG,
+             "sp_sssp_shard_peers: bad arguments");
+    Call c;
+    SP_TRY(c.begin(h->g->device));
+    const size_t b = (size_t)h->world * sizeof(void *);
+    void *d[3] = {nullptr, nullptr, nullptr};
+    const void *src[3] = {peer_dist, peer_inbox, peer_tail};
+    for (int i = 0; i < 3; i++) {
+        int rc = resident_alloc(&d[i], b);
+        if (rc != SP_OK) {
+            for (int j = 0; j < i; j++) resident_free(d[j]);
+            return rc;
+        }
+        SP_CUDA(cudaMemcpyAsync(d[i], src[i], b, cudaMemcpyHostToDevice, c.stream));
+    }
+    SP_CUDA(cudaMemsetAsync(tail, 0, 8, c.stream));
+    SP_TRY(c.finish(nullptr));
+    h->peer_dist = static_cast<int32_t **>(d[0]);
+    h->peer_inbox = static_cast<int32_t **>(d[1]);
+    h->peer_tail = static_cast<unsigned long long **>(d[2]);
+    h->inbox = inbox;
+    h->tail = tail;
+    h->per = per;
+    return SP_OK;
+}
+
+extern "C" int sp_sssp_shard_collect(sp_sssp_shard *h, int64_t *frontier) {
+    SP_CHECK(h && h->inbox, SP_ERR_ARG, "sp_sssp_shard_collect: no peers set");
+    Call c;
+    SP_TRY(c.begin(h->g->device));
+    unsigned long long *hk;
+    SP_TRY(c.host_as(&hk));
+    SP_CUDA(cudaMemcpyAsync(hk, h->tail, 8, cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t k = (int64_t)hk[0];
+    SP_CHECK(k <= h->g->n, SP_ERR_CUDA, "sp_sssp_shard_collect: inbox overflow");
+    const int stamp = -2 - h->step;  // as sp_sssp_shard_apply
+    SP_CUDA(cudaMemcpyAsync(h->aux + 1, &h->nq, 8, cudaMemcpyHostToDevice, c.stream));
+    if (k > 0) {
+        k_shard_collect<<<grid_for(k, kBlock, c.device), kBlock, 0, c.stream>>>(
+            h->inbox, k, h->enq, stamp, h->q[h->cur], h->aux + 1);
+        c.launches++;
+    }
+    SP_CUDA(cudaMemsetAsync(h->tail, 0, 8, c.stream));
+    SP_CUDA(cudaMemcpyAsync(hk, h->aux + 1, 8, cudaMemcpyDeviceToHost, c.stream));
+    SP_TRY(c.finish(nullptr));
+    h->nq = (int64_t)hk[0];
+    SP_CHECK(h->nq <= h->qcap, SP_ERR_CUDA, "sp_sssp_shard_collect: frontier overflow");
     if (frontier) *frontier = h->nq;
     return SP_OK;
 }

@@ -127,8 +127,11 @@ class NativeBackend:
         return _NativePrShard(self, g, v0, v1, damping, deterministic)
 
     # -- SSSP (owner-computes shard, one handle per run)
-    def sssp_shard(self, g, src, v0, v1, per, world):
-        return _NativeShard(self, g, src, v0, v1, per, world)
+    def sssp_shard(self, g, src, v0, v1, per, world, p2p=None):
+        """p2p = (group, me): the exchange fused into the relaxation over
+        peer-mapped dist arrays and inboxes (raises RuntimeError if the peer
+        mapping fails)."""
+        return _NativeShard(self, g, src, v0, v1, per, world, p2p)
 
     def to_host(self, x):
         return x.cpu().numpy()
@@ -204,20 +207,67 @@ class _NativePrShard:
         self.opened, self.own = [], []
 
 
+class _DevArray:
+    """A torch-visible view of a raw device pointer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
 class _NativeShard:
     """sp_sssp_shard_* on this rank's GPU: dist (padded to per * world for a
-    reduce-scatter) and the message send buffer are torch tensors."""
+    reduce-scatter) and the message send buffer are torch tensors.  With p2p
+    = (group, me), dist, the inbox and its tail are peer-mapped buffers
+    (sp_peer_alloc) shared with every rank, and the exchange is fused into
+    the relaxation (sp_sssp_shard_peers / _collect)."""
 
-    def __init__(self, be, g, src, v0, v1, per, world):
+    def __init__(self, be, g, src, v0, v1, per, world, p2p=None):
         t = be.torch
         self.be, self.g, self.world, self.per = be, g, world, per
-        self.dist = t.full((per * world,), 2147483647, dtype=t.int32, device=be.device)
-        self.send = t.empty(max(1, g.n), dtype=t.int64, device=be.device)
+        self.own, self.opened = [], []
+        self.fused = p2p is not None
         self.h = C.c_void_p()
+        L, dev = be.L, be.index
+        if self.fused:
+            group, me = p2p
+            handles = []
+            for nbytes in (4 * per * world, 4 * max(1, g.n), 8):  # dist, inbox, tail
+                ptr, hnd = C.c_void_p(), (C.c_char * 64)()
+                be._chk(L.sp_peer_alloc(dev, max(8, nbytes), C.byref(ptr), hnd), "sp_peer_alloc")
+                self.own.append(ptr.value)
+                handles.append(bytes(hnd))
+            self.dist = t.as_tensor(_DevArray(self.own[0], per * world, "<i4"), device=be.device)
+            self.dist.fill_(2147483647)
+        else:
+            self.dist = t.full((per * world,), 2147483647, dtype=t.int32, device=be.device)
+        self.send = t.empty(max(1, g.n), dtype=t.int64, device=be.device)
         be._fence()
         be._chk(be.L.sp_sssp_shard_create(g.handle, int(v0), int(v1), int(src), int(world),
                                           C.c_void_p(self.dist.data_ptr()), C.byref(self.h)),
                 "sp_sssp_shard_create")
+        if self.fused:
+            allh = [None] * world
+            _dist().all_gather_object(allh, handles, group=group)
+            tabs = [(C.c_void_p * world)() for _ in range(3)]
+            for q in range(world):
+                for i in range(3):
+                    if q == me:
+                        tabs[i][q] = self.own[i]
+                    else:
+                        ptr = C.c_void_p()
+                        hb = (C.c_char * 64).from_buffer_copy(allh[q][i])
+                        be._chk(L.sp_peer_open(dev, hb, C.byref(ptr)), "sp_peer_open")
+                        self.opened.append(ptr.value)
+                        tabs[i][q] = ptr.value
+            be._chk(L.sp_sssp_shard_peers(self.h, int(per), tabs[0], tabs[1], tabs[2],
+                                          C.c_void_p(self.own[1]), C.c_void_p(self.own[2])),
+                    "sp_sssp_shard_peers")
+
+    def collect(self) -> int:
+        f = C.c_int64()
+        self.be._chk(self.be.L.sp_sssp_shard_collect(self.h, C.byref(f)), "sp_sssp_shard_collect")
+        return int(f.value)
 
     def relax(self, max_rounds):
         """-> (per-owner message counts, info[4]: owned expanded, slots
@@ -250,6 +300,11 @@ class _NativeShard:
         if self.h:
             self.be.L.sp_sssp_shard_destroy(self.h)
             self.h = C.c_void_p()
+        for p in self.opened:
+            self.be.L.sp_peer_free(C.c_void_p(p), 1)
+        for p in self.own:
+            self.be.L.sp_peer_free(C.c_void_p(p), 0)
+        self.opened, self.own = [], []
 
 
 def _dist():
@@ -550,7 +605,28 @@ def _sssp(be, g, bound, cap, world, me, group, det, E, prog, tr, local_fixpoint=
     rr = parts[me].real_range()
     v0, v1 = rr.start, rr.stop
     n = g.n
-    sh = be.sssp_shard(g, bound["src"], v0, v1, per, world)
+    # the exchange fused into the relaxation over peer memory (NVLink between
+    # GPUs) unless SP_SSSP_EXCHANGE forces a message form or the mapping
+    # fails on any rank (decided collectively)
+    mode = os.environ.get("SP_SSSP_EXCHANGE", "auto")
+    sh = None
+    if world > 1 and mode in ("auto", "p2p") and hasattr(be, "sssp_shard") and \
+            isinstance(be, NativeBackend):
+        try:
+            sh = be.sssp_shard(g, bound["src"], v0, v1, per, world, p2p=(group, me))
+            ok = 1
+        except RuntimeError:
+            ok = 0
+        okt = torch.tensor([ok], dtype=torch.int32, device=be.device)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN, group=group)
+        if not int(okt.item()) and sh is not None:
+            sh.close()
+            sh = None
+        elif not int(okt.item()):
+            sh = None
+    if sh is None:
+        sh = be.sssp_shard(g, bound["src"], v0, v1, per, world)
+    fused = getattr(sh, "fused", False)
     try:
         steps = relaxed = sent_total = 0
         dense_steps = 0
@@ -561,6 +637,23 @@ def _sssp(be, g, bound, cap, world, me, group, det, E, prog, tr, local_fixpoint=
             except OverflowError:
                 counts, info, bad = np.zeros(world, dtype=np.int64), np.zeros(4, np.int64), 1
             relaxed += int(info[1])
+            if fused:  # messages already in the owners' inboxes
+                okt = torch.tensor([bad], dtype=torch.int64, device=be.device)
+                dist.all_reduce(okt, op=dist.ReduceOp.MAX, group=group)  # + every relax done
+                if int(okt.item()):
+                    raise E.ExecError("SSSP distance left the int32 range (negative weights)")
+                sent_total += int(counts.sum())
+                f = sh.collect()
+                steps += 1
+                ft = torch.tensor([f], dtype=torch.int64, device=be.device)
+                dist.all_reduce(ft, op=dist.ReduceOp.SUM, group=group)
+                done = int(ft.item()) == 0
+                tr.record("fixedPoint finished", int(info[0]), int(counts.sum()), finished=done)
+                if done:
+                    break
+                if steps >= cap:
+                    raise E.NonConvergenceError(prog.flag, cap)
+                continue
             # every rank's per-owner counts (+ overflow flag): the send and
             # receive splits of the all-to-all and the global message volume
             row = torch.tensor(list(counts) + [bad], dtype=torch.int64, device=be.device)
@@ -571,8 +664,8 @@ def _sssp(be, g, bound, cap, world, me, group, det, E, prog, tr, local_fixpoint=
                 raise E.ExecError("SSSP distance left the int32 range (negative weights)")
             total = int(M[:, :world].sum())
             sent_total += int(counts.sum())
-            mode = os.environ.get("SP_SSSP_EXCHANGE", "auto")  # tests force each form
-            dense = mode == "dense" or (mode == "auto" and 8 * total > 4 * per * world)
+            # message forms (tests force each with SP_SSSP_EXCHANGE)
+            dense = mode == "dense" or (mode in ("auto", "p2p") and 8 * total > 4 * per * world)
             if dense:  # a MIN reduce-scatter of the dist arrays moves fewer bytes
                 dense_steps += 1
                 blk = torch.empty(per, dtype=torch.int32, device=be.device)
@@ -608,4 +701,5 @@ def _sssp(be, g, bound, cap, world, me, group, det, E, prog, tr, local_fixpoint=
                                   "modified_nxt": np.zeros(n, dtype=bool)},
                       scalars={"finished": True})
     return env, {"finished": steps}, {"relaxed": relaxed, "block": (v0, v1),
-                                      "messages": sent_total, "dense_supersteps": dense_steps}
+                                      "messages": sent_total, "dense_supersteps": dense_steps,
+                                      "exchange": "peer" if fused else "messages"}

@@ -2,8 +2,10 @@
 
 One GPU is available, so two ranks share cuda:0 over gloo (NCCL refuses two
 ranks on one device); this drives the native block kernels
-(sp_sssp_shard_*: owner-computes SSSP with aggregated messages in both
-exchange forms, sp_pagerank_shard_* (planned once, stream-ordered steps, the
+(sp_sssp_shard_*: owner-computes SSSP with the exchange fused into the
+relaxation over peer memory -- remote atomicMin into the owner's dist and
+its inbox, CUDA IPC between the two processes -- and with aggregated
+messages in both exchange forms, sp_pagerank_shard_* (planned once, stream-ordered steps, the
 contrib exchange as peer stores fused into the step -- CUDA IPC between the
 two processes -- and as an all-gather), sp_tc ranges, sp_bc source shares) through the real sharding/exchange logic and checks the results
 against the single-process CPU oracle."""
@@ -54,8 +56,8 @@ def _worker(rank, world, port, kind, q):
         g = sp.from_arrays(u, v, w, directed=directed, n=n)
         be = parallel.NativeBackend(0)
         out = {}
-        out["dist"] = parallel.run_sharded(corpus.SSSP, g, {"src": 0},
-                                           backend=be).env.node_props["dist"]
+        r = parallel.run_sharded(corpus.SSSP, g, {"src": 0}, backend=be)
+        out["dist"], out["sssp_exchange"] = r.env.node_props["dist"], r.stats["exchange"]
         for ex in ("sparse", "dense"):
             os.environ["SP_SSSP_EXCHANGE"] = ex
             r = parallel.run_sharded(corpus.SSSP, g, {"src": 0}, backend=be)
@@ -117,6 +119,7 @@ def test_native_sharded_two_ranks(kind):
     for r in range(2):
         x = res[r]
         assert np.array_equal(x["dist"], d_ref)
+        assert x["sssp_exchange"] == "peer"  # fused into the relaxation (CUDA IPC here)
         for key in ("dist_sparse", "dist_dense", "dist_lf"):
             assert np.array_equal(x[key], d_ref), key
         assert x["k_sparse"] == x["k_dense"]  # same supersteps, either exchange form
