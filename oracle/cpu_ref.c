@@ -189,6 +189,81 @@ done:
 }
 
 /* ------------------------------------------------------------------------
+ * SSSP distances by Dijkstra: trident/oracles.py:23-40 (oracle_dijkstra,
+ * the reference's own independent validator) over the w_eff slot weights
+ * sssp.sp relaxes with (get_edge's first-slot weight).  For
+ * non-negative weights the shortest distances are the unique relaxation
+ * fixpoint, so this equals cr_sssp's dist without its ~10^4 sequential
+ * sweeps on a large-diameter graph (cfg5a).  Binary heap of (dist, vertex)
+ * with lazy deletion, like heapq.  Returns 0, or 3 for a negative weight.
+ * ---------------------------------------------------------------------- */
+typedef struct { int64_t d; int32_t v; } cr_hent;
+
+static void heap_push(cr_hent **h, int64_t *len, int64_t *cap, int64_t d, int32_t v)
+{
+    if (*len == *cap) {
+        *cap = *cap ? 2 * *cap : 1024;
+        *h = realloc(*h, (size_t)*cap * sizeof(cr_hent));
+    }
+    int64_t i = (*len)++;
+    while (i > 0) {
+        int64_t p = (i - 1) / 2;
+        if ((*h)[p].d < d || ((*h)[p].d == d && (*h)[p].v <= v)) break;
+        (*h)[i] = (*h)[p];
+        i = p;
+    }
+    (*h)[i].d = d;
+    (*h)[i].v = v;
+}
+
+static cr_hent heap_pop(cr_hent *h, int64_t *len)
+{
+    cr_hent top = h[0], last = h[--*len];
+    int64_t i = 0;
+    for (;;) {
+        int64_t c = 2 * i + 1;
+        if (c >= *len) break;
+        if (c + 1 < *len && (h[c + 1].d < h[c].d || (h[c + 1].d == h[c].d && h[c + 1].v < h[c].v)))
+            c++;
+        if (last.d < h[c].d || (last.d == h[c].d && last.v <= h[c].v)) break;
+        h[i] = h[c];
+        i = c;
+    }
+    if (*len) h[i] = last;
+    return top;
+}
+
+int cr_sssp_dijkstra(int64_t n, const int64_t *off, const int32_t *adj,
+                     const int32_t *weff, int32_t src, int32_t *dist)
+{
+    for (int64_t e = 0; n && e < off[n]; e++)
+        if (weff[e] < 0) return 3;
+    uint8_t *done = calloc((size_t)(n ? n : 1), 1);
+    cr_hent *h = NULL;
+    int64_t len = 0, cap = 0;
+    for (int64_t x = 0; x < n; x++)
+        dist[x] = (int32_t)CR_INT_MAX;
+    dist[src] = 0;
+    heap_push(&h, &len, &cap, 0, src);
+    while (len) {
+        cr_hent t = heap_pop(h, &len);
+        if (done[t.v]) continue;
+        done[t.v] = 1;
+        for (int64_t e = off[t.v]; e < off[t.v + 1]; e++) {
+            int32_t y = adj[e];
+            int64_t nd = t.d + (int64_t)weff[e];
+            if (nd < (int64_t)dist[y]) {  /* candidates >= INT_MAX never win (F12) */
+                dist[y] = (int32_t)nd;
+                heap_push(&h, &len, &cap, nd, y);
+            }
+        }
+    }
+    free(h);
+    free(done);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------
  * PageRank: corpus/programs/pr.sp:1-30.  Per vertex a left fold over the
  * reverse-CSR row (interp.py:395-398) of u.rank / count_outNbrs(u)
  * (interp.py:543-544), newRank = (1-d)/n + d*sum, diff = max |newRank-rank|,

@@ -48,6 +48,7 @@ def lib():
         L.cr_weff.argtypes = [_i64, _p, _p, _p, _p]
         L.cr_sssp.restype = C.c_int
         L.cr_sssp.argtypes = [_i64, _p, _p, _p, _i32, _i64, _p, _p]
+        L.cr_sssp_dijkstra.argtypes = [_i64, _p, _p, _p, _i32, _p]
         L.cr_pagerank.restype = C.c_int
         L.cr_pagerank.argtypes = [_i64, _p, _p, _p, C.c_double, C.c_double,
                                   _i64, _i64, _p, _p, _p, _p, C.c_int]
@@ -112,6 +113,14 @@ def sssp(g: Csr, src: int, cap: int | None = None):
     rc = lib().cr_sssp(g.n, _ptr(g.off), _ptr(g.adj), _ptr(g.weff), src, cap,
                        _ptr(dist), _ptr(it))
     return dist, int(it[0]), rc
+
+
+def sssp_dijkstra(g: Csr, src: int):
+    """Exact distances by Dijkstra (trident/oracles.py:23-40) over w_eff;
+    equal to sssp()'s for non-negative weights.  Returns (dist, rc)."""
+    dist = np.zeros(g.n, np.int32)
+    rc = lib().cr_sssp_dijkstra(g.n, _ptr(g.off), _ptr(g.adj), _ptr(g.weff), src, _ptr(dist))
+    return dist, rc
 
 
 def pagerank(g: Csr, damping=0.85, eps=1e-6, max_iter=100,

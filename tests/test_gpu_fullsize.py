@@ -113,10 +113,11 @@ def test_tc_cfg3_full():
 
 
 def test_sssp_grid_cfg5_bellman_certificate():
-    """BASELINE cfg5a: 4096x4096 grid, SSSP from 0.  dist[0] = 0 and, for
-    every other vertex, dist = min over in-edges of dist[u] + w_eff (all
-    vertices are reached on a connected grid): the Bellman equations, whose
-    solution is unique for positive weights."""
+    """BASELINE cfg5a: 4096x4096 grid, SSSP from 0 (the asynchronous
+    near-far kernel).  dist[0] = 0 and, for every other vertex, dist = min
+    over in-edges of dist[u] + w_eff (all vertices are reached on a
+    connected grid): the Bellman equations, whose solution is unique for
+    positive weights; and bit-exact parity with the oracle's Dijkstra."""
     g = sp.generate("grid", 4096, 4096, seed=1)
     dist = sp.run(corpus.SSSP, g, {"src": 0}).env.node_props["dist"].astype(np.int64)
     off, adj = np.asarray(g.offsets), np.asarray(g.adj)
@@ -127,6 +128,13 @@ def test_sssp_grid_cfg5_bellman_certificate():
     np.minimum.at(best, adj, dist[src] + w)
     best[0] = 0
     np.testing.assert_array_equal(dist, best)
+    # and oracle parity: the reference's own validator algorithm
+    # (trident/oracles.py:23-40, Dijkstra) restated in the C oracle
+    o = cpu_ref.Csr(g.n, g.m, False, off, adj, None, None, None, None,
+                    np.asarray(g.effective_weights))
+    want, rc = cpu_ref.sssp_dijkstra(o, 0)
+    assert rc == 0
+    np.testing.assert_array_equal(dist, want)
     g.close()
 
 

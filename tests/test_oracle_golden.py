@@ -86,3 +86,26 @@ def test_tc_matches_reference(case):
     g = _csr(z)
     assert cpu_ref.tc(g) == int(z["tc"])
     assert cpu_ref.tc(g, nthreads=4) == int(z["tc"])
+
+
+def test_dijkstra_oracle_matches_reference_sssp_goldens():
+    """cr_sssp_dijkstra (trident/oracles.py:23-40 over w_eff) gives the
+    reference interpreter's SSSP distances on every non-negative golden case
+    (it certifies the cfg5a grid, where the interpreter-order oracle would
+    need ~10^4 sweeps)."""
+    import glob
+    import os
+    checked = 0
+    for f in sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))):
+        z = np.load(f)
+        if "sssp_dist" not in z:
+            continue
+        o = cpu_ref.build_csr(z["u"], z["v"], z["w"], bool(z["directed"]), int(z["n"]))
+        if (o.weff < 0).any():
+            continue
+        for i, s in enumerate(z["sssp_srcs"]):
+            d, rc = cpu_ref.sssp_dijkstra(o, int(s))
+            assert rc == 0
+            np.testing.assert_array_equal(d, z["sssp_dist"][i])
+            checked += 1
+    assert checked >= 50
