@@ -371,6 +371,7 @@ void free_graph(sp_graph *g) {
     resident_free(g->uadj);
     resident_free(g->uinfo);
     resident_free(g->ubig);
+    resident_free(g->uorder);
     resident_free(g->pr_hot_ids);
     resident_free(g->pr_radj_hot);
     resident_free(g->pr_unit_row);

@@ -19,6 +19,14 @@
 //              on the device (count -> scan -> fill -> info) and cached;
 //   count    = sum over slots b of N+(a), over slots x of N+(b), of
 //              mult(x in N+(a))  (= m_ab * m_bc * m_ac summed per triangle).
+// Rows and elements are degree RANKS, not vertex ids (the count is
+// label-invariant): row r belongs to vertex uorder[r], rows ascend by rank,
+// each row's elements are ascending ranks -- so for a row of the top ranks
+// ("hub" rows, r >= n - H) every element of N+(a) and of every N+(b) lies
+// in [n - H, n), and k_tc_big counts them in a direct-indexed 16-bit array
+// instead of hash probes.  The build ranks the vertices by (degree, id)
+// (one radix sort), emits (row rank, element rank) keys for every upper
+// slot and sorts them (one 64-bit radix sort), then places the rows.
 // Kernel k_tc_fwd: persistent warps pull 32-vertex batches from a global
 // counter.  Per vertex a the warp stages A = N+(a), the row starts of its
 // b's (from uinfo) and a prefix of their element-holding 16-byte half-sector
@@ -183,64 +191,89 @@ __device__ __forceinline__ void walk_owners(const int32_t *S, int nr, int h0, in
 
 // ---- upper CSR build (undirected) -------------------------------------
 
+// rank = position in ascending (degree, id) order: keys for the sort
+__global__ void k_rank_keys(const int32_t *__restrict__ deg, int64_t n, uint64_t *key,
+                            int32_t *id) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        key[v] = ((uint64_t)(uint32_t)deg[v] << 32) | (uint32_t)v;
+        id[v] = (int32_t)v;
+    }
+}
+
+__global__ void k_rank_scatter(const int32_t *__restrict__ order, int64_t n, int32_t *rank) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        rank[order[r]] = (int32_t)r;
+}
+
+// Row rank[v] of the upper CSR = the ranks of v's neighbours ranked above v.
 __global__ void k_up_count(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
-                           const int32_t *__restrict__ deg, int64_t n, int32_t *ulen,
-                           int64_t *pad8) {
+                           const int32_t *__restrict__ rank, int64_t n, int32_t *ulen,
+                           int64_t *len64, int64_t *pad8) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const unsigned lane = lane_id();
     for (int64_t v = warp; v < n; v += nw) {
         const int64_t r0 = off[v], r1 = off[v + 1];
-        const int32_t dv = deg[v];
+        const int32_t rv = rank[v];
         int64_t c = 0;
-        for (int64_t e = r0 + lane; e < r1; e += 32) {
-            const int32_t x = adj[e];
-            c += (x != (int32_t)v && rank_gt(__ldg(deg + x), x, dv, (int32_t)v)) ? 1 : 0;
-        }
+        for (int64_t e = r0 + lane; e < r1; e += 32) c += __ldg(rank + adj[e]) > rv ? 1 : 0;
         c = warp_sum(c);
         if (lane == 0) {
-            ulen[v] = (int32_t)c;
-            pad8[v] = (c + kPad - 1) / kPad;  // 32-byte sectors of the padded row
+            ulen[rv] = (int32_t)c;
+            len64[rv] = c;
+            pad8[rv] = (c + kPad - 1) / kPad;  // 32-byte sectors of the padded row
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) pad8[n] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        pad8[n] = 0;
+        len64[n] = 0;
+    }
 }
 
-__global__ void k_up_fill(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
-                          const int32_t *__restrict__ deg, const int64_t *__restrict__ start8,
-                          int64_t n, int32_t *uadj) {
+// (row rank, element rank) keys of every upper slot, row-grouped by S.
+__global__ void k_up_emit(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+                          const int32_t *__restrict__ rank, const int64_t *__restrict__ S,
+                          int64_t n, uint64_t *keys) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const unsigned lane = lane_id();
     for (int64_t v = warp; v < n; v += nw) {
         const int64_t r0 = off[v], r1 = off[v + 1];
-        const int32_t dv = deg[v];
-        const int64_t base = kPad * start8[v], end = kPad * start8[v + 1];
-        int64_t pos = base;
+        const int32_t rv = rank[v];
+        int64_t pos = S[rv];
         for (int64_t e0 = r0; e0 < r1; e0 += 32) {
             const int64_t e = e0 + lane;
-            int32_t x = 0;
-            bool keep = false;
-            if (e < r1) {
-                x = adj[e];
-                keep = x != (int32_t)v && rank_gt(__ldg(deg + x), x, dv, (int32_t)v);
-            }
+            int32_t rx = -1;
+            if (e < r1) rx = __ldg(rank + adj[e]);
+            const bool keep = e < r1 && rx > rv;
             const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep) uadj[pos + __popc(m & ((1u << lane) - 1u))] = x;
+            if (keep)
+                keys[pos + __popc(m & ((1u << lane) - 1u))] =
+                    ((uint64_t)(uint32_t)rv << 32) | (uint32_t)rx;
             pos += __popc(m);
         }
-        for (int64_t p = pos + lane; p < end; p += 32) uadj[p] = -1;  // row padding
     }
 }
 
-__global__ void k_up_info(const int32_t *__restrict__ uadj, const int64_t *__restrict__ start8,
-                          const int32_t *__restrict__ ulen, int64_t mpad, uint2 *uinfo,
-                          uint32_t *ustart8, int64_t n) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < mpad;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t x = uadj[e];
-        uinfo[e] = x >= 0 ? make_uint2((uint32_t)start8[x], (uint32_t)ulen[x]) : make_uint2(0u, 0u);
+// Sorted keys -> padded rows: uadj (ascending element ranks) and uinfo
+// (start and length of the row each element points to).
+__global__ void k_up_place(const uint64_t *__restrict__ keys, int64_t mu,
+                           const int64_t *__restrict__ S, const int64_t *__restrict__ start8,
+                           const int32_t *__restrict__ ulen, int32_t *uadj, uint2 *uinfo) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < mu;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        const int64_t r = (int64_t)(k >> 32);
+        const int32_t y = (int32_t)(uint32_t)k;
+        const int64_t at = kPad * start8[r] + (i - S[r]);
+        uadj[at] = y;
+        uinfo[at] = make_uint2((uint32_t)start8[y], (uint32_t)ulen[y]);
     }
+}
+
+__global__ void k_up_start(const int64_t *__restrict__ start8, int64_t n, uint32_t *ustart8) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n;
          v += (int64_t)gridDim.x * blockDim.x)
         ustart8[v] = (uint32_t)start8[v];
@@ -268,36 +301,70 @@ __global__ void k_big_keys(const int32_t *__restrict__ big, const int32_t *__res
         key[i] = (uint32_t)ulen[big[i]];
 }
 
+template <class F>
+static int cub_call(Call &c, F f) {  // two-phase CUB call with stream-ordered scratch
+    size_t tmp = 0;
+    SP_CUDA(f(nullptr, tmp));
+    void *dt = nullptr;
+    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
+    cudaError_t e = f(dt, tmp);
+    scratch_free(dt, c.stream);
+    SP_CUDA(e);
+    return SP_OK;
+}
+
 int ensure_upper(sp_graph *g, Call &c) {
     std::lock_guard<std::mutex> lk(g_up_mu);
     if (g->m_up >= 0) return SP_OK;
     const int64_t n = g->n;
-    int64_t *pad8, *start8;
-    int32_t *ulen = nullptr;
-    SP_TRY(c.alloc(&pad8, n + 1));
-    SP_TRY(c.alloc(&start8, n + 1));
+    // ---- degree ranks (ascending (degree, id)); rows and elements are ranks
+    uint64_t *rkey, *rkey_s;
+    int32_t *rid, *rank;
+    int32_t *order = nullptr, *ulen = nullptr;
+    SP_TRY(c.alloc(&rkey, n));
+    SP_TRY(c.alloc(&rkey_s, n));
+    SP_TRY(c.alloc(&rid, n));
+    SP_TRY(c.alloc(&rank, n));
+    SP_TRY(resident_alloc((void **)&order, std::max<int64_t>(1, n) * sizeof(int32_t)));
     SP_TRY(resident_alloc((void **)&ulen, std::max<int64_t>(1, n) * sizeof(int32_t)));
     struct Guard {
-        void *p[4] = {nullptr, nullptr, nullptr, nullptr};
+        void *p[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
         bool keep = false;
         ~Guard() { if (!keep) for (void *q : p) resident_free(q); }
     } gd;
     gd.p[0] = ulen;
+    gd.p[4] = order;
+    const int gridn = grid_for(n, 256, c.device, 16);
+    k_rank_keys<<<gridn, 256, 0, c.stream>>>(g->outdeg, n, rkey, rid);
+    int nbits = 1;
+    while (nbits < 31 && ((int64_t)1 << nbits) < n) nbits++;
+    int dbits = 1;
+    while (dbits < 31 && ((int64_t)1 << dbits) <= g->max_outdeg) dbits++;
+    SP_TRY(cub_call(c, [&](void *t, size_t &s) {
+        return cub::DeviceRadixSort::SortPairs(t, s, rkey, rkey_s, rid, order, n, 0, 32 + dbits,
+                                               c.stream);
+    }));
+    k_rank_scatter<<<gridn, 256, 0, c.stream>>>(order, n, rank);
+    // ---- row lengths, unpadded (S) and padded (start8) row starts
+    int64_t *len64, *pad8, *S, *start8;
+    SP_TRY(c.alloc(&len64, n + 1));
+    SP_TRY(c.alloc(&pad8, n + 1));
+    SP_TRY(c.alloc(&S, n + 1));
+    SP_TRY(c.alloc(&start8, n + 1));
     const int grid = grid_for(n * 32, 256, c.device, 16);
-    k_up_count<<<grid, 256, 0, c.stream>>>(g->off, g->adj, g->outdeg, n, ulen, pad8);
-    size_t tmp = 0;
-    SP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, pad8, start8, n + 1, c.stream));
-    void *dt = nullptr;
-    SP_TRY(scratch_alloc(&dt, tmp, c.stream));
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(dt, tmp, pad8, start8, n + 1, c.stream);
-    scratch_free(dt, c.stream);
-    SP_CUDA(e);
-    // real upper slots = sum of ulen (= m/2 minus self-loops); padded total
+    k_up_count<<<grid, 256, 0, c.stream>>>(g->off, g->adj, rank, n, ulen, len64, pad8);
+    SP_TRY(cub_call(c, [&](void *t, size_t &s) {
+        return cub::DeviceScan::ExclusiveSum(t, s, pad8, start8, n + 1, c.stream);
+    }));
+    SP_TRY(cub_call(c, [&](void *t, size_t &s) {
+        return cub::DeviceScan::ExclusiveSum(t, s, len64, S, n + 1, c.stream);
+    }));
     int64_t *h;
     SP_TRY(c.host_as(&h));
     SP_CUDA(cudaMemcpyAsync(h, start8 + n, 8, cudaMemcpyDeviceToHost, c.stream));
+    SP_CUDA(cudaMemcpyAsync(h + 3, S + n, 8, cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
-    const int64_t mpad = kPad * h[0];
+    const int64_t mpad = kPad * h[0], mu = h[3];
     SP_CHECK(h[0] < (int64_t)0xFFFFFFFFll, SP_ERR_UNSUPPORTED,
              "triangle counting: upper CSR of %lld slots exceeds the 2^35 limit",
              (long long)mpad);
@@ -310,9 +377,24 @@ int ensure_upper(sp_graph *g, Call &c) {
     gd.p[2] = uinfo;
     SP_TRY(resident_alloc((void **)&ustart8, (n + 1) * sizeof(uint32_t)));
     gd.p[3] = ustart8;
-    k_up_fill<<<grid, 256, 0, c.stream>>>(g->off, g->adj, g->outdeg, start8, n, uadj);
-    k_up_info<<<grid_for(std::max<int64_t>(mpad, n + 1), 256, c.device, 16), 256, 0, c.stream>>>(
-        uadj, start8, ulen, mpad, uinfo, ustart8, n);
+    SP_CUDA(cudaMemsetAsync(uadj, 0xFF, std::max<int64_t>(8, mpad) * sizeof(int32_t), c.stream));
+    SP_CUDA(cudaMemsetAsync(uinfo, 0, std::max<int64_t>(8, mpad) * sizeof(uint2), c.stream));
+    // ---- (row, element) keys, sorted: every row ascending
+    if (mu > 0) {
+        uint64_t *keys, *keys_s;
+        SP_TRY(c.alloc(&keys, mu));
+        SP_TRY(c.alloc(&keys_s, mu));
+        k_up_emit<<<grid, 256, 0, c.stream>>>(g->off, g->adj, rank, S, n, keys);
+        SP_TRY(cub_call(c, [&](void *t, size_t &s) {
+            return cub::DeviceRadixSort::SortKeys(t, s, keys, keys_s, mu, 0, 32 + nbits,
+                                                  c.stream);
+        }));
+        k_up_place<<<grid_for(mu, 256, c.device, 16), 256, 0, c.stream>>>(keys_s, mu, S, start8,
+                                                                        ulen, uadj, uinfo);
+    }
+    k_up_start<<<grid_for(n + 1, 256, c.device, 16), 256, 0, c.stream>>>(start8, n, ustart8);
+    c.launches += 9;
+    SP_CUDA(cudaGetLastError());
     int32_t *big = nullptr;
     SP_TRY(resident_alloc((void **)&big, std::max<int64_t>(1, n) * sizeof(int32_t)));
     unsigned long long *bc;
@@ -349,6 +431,7 @@ int ensure_upper(sp_graph *g, Call &c) {
         SP_CUDA(cudaStreamSynchronize(c.stream));
     }
     gd.keep = true;
+    g->uorder = order;
     g->tc_warp_max = warp_max;
     g->ubig = big;
     g->nbig = (int64_t)h[1];
@@ -385,7 +468,9 @@ __global__ void __launch_bounds__(kBlock, SP_TCP_MINB) k_tc_fwd_plain(const uint
                                                    const int32_t *__restrict__ ulen,
                                                    const int32_t *__restrict__ uadj,
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
-                                                   int64_t v1, int amax, TcCounters *ctr) {
+                                                   int64_t v1, int amax, TcCounters *ctr,
+                                                   const int32_t *__restrict__ order,
+                                                   int64_t id0, int64_t id1) {
     __shared__ int32_t sA[kWarps][kA];
     __shared__ uint32_t sB[kWarps][kA];       // sector start of row b_j
     __shared__ int32_t sS[kWarps][kA + 1];    // half-sector prefix over the rows b_j (element-holding halves only)
@@ -409,6 +494,12 @@ __global__ void __launch_bounds__(kBlock, SP_TCP_MINB) k_tc_fwd_plain(const uint
         const uint32_t my_s8 = my < ve ? ustart8[my] : 0u;
         const int32_t my_len = my < ve ? ulen[my] : 0;
         for (int64_t a = vb; a < ve; a++) {
+            // rows are degree ranks; a sharded call keeps the rows of its
+            // vertex range (warp-uniform)
+            if (order) {
+                const int32_t id = __ldg(order + a);
+                if (id < id0 || id >= id1) continue;
+            }
             const int src = (int)(a - vb);
             const int na = __shfl_sync(0xffffffffu, my_len, src);
             if (na < 2) continue;  // a triangle needs b and x in N+(a)
@@ -493,7 +584,9 @@ __global__ void __launch_bounds__(kBlock, SP_TCH_MINB) k_tc_fwd_hash(const uint3
                                                    const int32_t *__restrict__ ulen,
                                                    const int32_t *__restrict__ uadj,
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
-                                                   int64_t v1, int amax, TcCounters *ctr) {
+                                                   int64_t v1, int amax, TcCounters *ctr,
+                                                   const int32_t *__restrict__ order,
+                                                   int64_t id0, int64_t id1) {
     // per warp, dynamic shared memory: hash keys[kT] + counts[kT] of A,
     // sector starts B[kA], half-sector prefix S[kA+1], filter F[kFilterWords]
     extern __shared__ uint32_t fwd_smem[];
@@ -518,6 +611,12 @@ __global__ void __launch_bounds__(kBlock, SP_TCH_MINB) k_tc_fwd_hash(const uint3
         const uint32_t my_s8 = my < ve ? ustart8[my] : 0u;
         const int32_t my_len = my < ve ? ulen[my] : 0;
         for (int64_t a = vb; a < ve; a++) {
+            // rows are degree ranks; a sharded call keeps the rows of its
+            // vertex range (warp-uniform)
+            if (order) {
+                const int32_t id = __ldg(order + a);
+                if (id < id0 || id >= id1) continue;
+            }
             const int src = (int)(a - vb);
             const int na = __shfl_sync(0xffffffffu, my_len, src);
             if (na < 2) continue;  // a triangle needs b and x in N+(a)
@@ -630,6 +729,10 @@ __global__ void __launch_bounds__(kBlock, SP_TCH_MINB) k_tc_fwd_hash(const uint3
 constexpr int kBigFilterBits = 1 << 17;  // 16 KB
 constexpr int kBigFilterShift = 32 - 17;
 constexpr int kBigMax = 48 * 1024;      // staged A entries (192 KB) -- beyond: global search
+#ifndef SP_TC_HUB_SMEM
+#define SP_TC_HUB_SMEM (32 * 1024)  // RMAT-24: off 398 ms, 32 KB 382, 64 KB 488, 128 KB 956 (occupancy)
+#endif
+constexpr int kHubSmem = SP_TC_HUB_SMEM;  // bytes of 16-bit hub counts (16 K top-ranked rows)
 constexpr int kHashMax = 8 * 1024;      // rows up to this are hashed: 2^14 x (key, count) = 128 KB
 // One CTA per SM (the shared table); 8 warps per vertex -- 32 warps
 // measured slower (744 vs 534 ms on RMAT-24): the static 32-row batches
@@ -648,8 +751,10 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
                                                       const int32_t *__restrict__ uadj,
                                                       const uint2 *__restrict__ uinfo,
                                                       const int32_t *__restrict__ big,
-                                                      int64_t nbig, int64_t v0, int64_t v1,
-                                                      int hash_max, int big_max, TcCounters *ctr) {
+                                                      int64_t nbig, const int32_t *__restrict__ order,
+                                                      int64_t id0, int64_t id1,
+                                                      int hash_max, int big_max, TcCounters *ctr,
+                                                      int64_t hub_base, int hub_words) {
     extern __shared__ uint32_t smem[];
     uint32_t *F = smem;                                        // kBigFilterBits / 32 words
     int32_t *A = reinterpret_cast<int32_t *>(smem + kBigFilterBits / 32);
@@ -673,11 +778,16 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
         const int64_t bi = s_bi;
         if (bi >= nbig) break;
         const int32_t a = big[bi];
-        if (a < v0 || a >= v1) continue;  // block-uniform
+        if (order && (__ldg(order + a) < id0 || __ldg(order + a) >= id1)) continue;  // block-uniform
         const int na = ulen[a];
         const int64_t r0 = kPad * (int64_t)ustart8[a];
-        const bool staged = na <= big_max;
-        const bool hashed = na <= hash_max;
+        // hub rows (rank >= hub_base): every element of N+(a) and of every
+        // N+(b) ranks above a, i.e. inside [hub_base, n) -- a direct-indexed
+        // array of 16-bit multiplicities replaces the hash probes (one
+        // shared load per element, no probe loop, no divergence)
+        const bool hub = a >= hub_base && na <= 65535;
+        const bool staged = !hub && na <= big_max;
+        const bool hashed = !hub && na <= hash_max;
         int tbits = 6;  // table of 2^tbits >= 2 na entries
         while ((1 << tbits) < 2 * na) tbits++;
         const int T = 1 << tbits;
@@ -688,7 +798,16 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
         uint32_t *HF = HC + T;
         const int fbits = tbits + 3;
         __syncthreads();  // previous vertex done with the shared structures
-        if (hashed) {
+        uint32_t *HUB = smem;  // hub form: 16-bit counts, two per word, index x - hub_base
+        if (hub) {
+            for (int k = threadIdx.x; k < hub_words; k += blockDim.x) HUB[k] = 0u;
+            __syncthreads();
+            for (int k = threadIdx.x; k < na; k += blockDim.x) {
+                const int64_t i = (int64_t)uadj[r0 + k] - hub_base;
+                atomicAdd(&HUB[i >> 1], 1u << ((i & 1) * 16));
+            }
+            __syncthreads();
+        } else if (hashed) {
             for (int k = threadIdx.x; k < T; k += blockDim.x) {
                 HK[k] = -1;
                 HC[k] = 0u;
@@ -770,7 +889,10 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
                 for (int i = 0; i < 4; i++) {
                     const int32_t x = xv[i];
                     if (x < 0) continue;
-                    if (hashed) {  // multiplicity of x in A
+                    if (hub) {
+                        const int64_t i = (int64_t)x - hub_base;
+                        cnt += (HUB[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+                    } else if (hashed) {  // multiplicity of x in A
 #ifndef SP_TC_BIG_NOFILTER
                         const uint32_t fb = ((uint32_t)x * 0x9E3779B1u) >> (32 - fbits);
                         if (!(HF[fb >> 5] & (1u << (fb & 31)))) continue;
@@ -886,8 +1008,13 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
     SP_CUDA(cudaEventCreate(&ka));
     SP_CUDA(cudaEventCreate(&kb));
     cudaEventRecord(ka, c.stream);
+    // undirected rows are degree ranks: a partial vertex range filters rows
+    // by their vertex id (uorder), the full range needs no filter
+    const int64_t n = g->n;
+    const int32_t *order = (!g->directed && (v0 != 0 || v1 != n)) ? g->uorder : nullptr;
     if (v1 > v0) {
-        int64_t want = (v1 - v0 + kBatch * kWarps - 1) / (kBatch * kWarps);
+        const int64_t rows = g->directed ? v1 - v0 : n;
+        int64_t want = (rows + kBatch * kWarps - 1) / (kBatch * kWarps);
         int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
         if (g->directed) {
             k_tc_mid<<<grid, kBlock, 0, c.stream>>>(g->off, g->adj, v0, v1, ctr);
@@ -898,12 +1025,12 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
                 SP_CUDA(cudaFuncSetAttribute(k_tc_fwd_hash,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
                 k_tc_fwd_hash<<<grid, kBlock, fsm, c.stream>>>(g->ustart8, g->ulen, g->uadj,
-                                                               g->uinfo, v0, v1, g->tc_warp_max,
-                                                               ctr);
+                                                               g->uinfo, 0, n, g->tc_warp_max,
+                                                               ctr, order, v0, v1);
             } else {
                 k_tc_fwd_plain<<<grid, kBlock, 0, c.stream>>>(g->ustart8, g->ulen, g->uadj,
-                                                              g->uinfo, v0, v1, g->tc_warp_max,
-                                                              ctr);
+                                                              g->uinfo, 0, n, g->tc_warp_max,
+                                                              ctr, order, v0, v1);
             }
             c.launches++;
             if (g->nbig) {
@@ -914,9 +1041,17 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
                 const int big_max = bm ? std::max(1, std::min(kBigMax, atoi(bm))) : kBigMax;
                 int tb = 6;
                 while ((1 << tb) < 2 * std::min<int64_t>(g->max_ulen, hash_max)) tb++;
-                const size_t smem = std::max<size_t>(
+                size_t smem = std::max<size_t>(
                     ((size_t)8 << tb) + ((size_t)1 << tb),  // hash keys + counts + filter
                     kBigFilterBits / 8 + 4 * (size_t)std::min<int64_t>(g->max_ulen, big_max));
+                // hub rows: the top ranks whose 16-bit count array fits kHubSmem
+                // (SP_TC_HUB=0: off; rows are ranks, so hubs are [hub_base, n))
+                const char *he = getenv("SP_TC_HUB");
+                const int64_t hub_n = (he && he[0] == '0') ? 0
+                                      : std::min<int64_t>(n, (int64_t)kHubSmem / 2);
+                const int64_t hub_base = n - hub_n;
+                const int hub_words = (int)((hub_n + 1) / 2);
+                if (hub_n) smem = std::max<size_t>(smem, (size_t)hub_words * 4);
                 SP_CUDA(cudaFuncSetAttribute(k_tc_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
                 int per_sm = 1;
@@ -924,8 +1059,9 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
                 const int gb = (int)std::min<int64_t>(g->nbig,
                                                       (int64_t)sms * std::max(1, per_sm));
                 k_tc_big<<<gb, kBigBlock, smem, c.stream>>>(g->ustart8, g->ulen, g->uadj, g->uinfo,
-                                                         g->ubig, g->nbig, v0, v1, hash_max,
-                                                         big_max, ctr);
+                                                         g->ubig, g->nbig, order, v0, v1,
+                                                         hash_max, big_max, ctr, hub_base,
+                                                         hub_words);
                 c.launches++;
             }
         }

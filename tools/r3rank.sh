@@ -1,0 +1,7 @@
+#!/bin/bash
+OUT=gpurun_out/r3rank; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { tail -30 $OUT/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parallel.py -m gpu -x -q -k "tc or TC or golden or parallel" > $OUT/pytest.log 2>&1; echo "rc=$?" >> $OUT/pytest.log; tail -2 $OUT/pytest.log; grep -m5 "Error\|assert" $OUT/pytest.log
+echo "== tc cfg3"; timeout 200 python tools/run_algo.py tc 3 2>&1 | tail -2
+echo "== tc rmat24"; timeout 300 python tools/run_algo.py tc_rmat24 2 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_fullsize.py -m gpu -x -q -k "tc" > $OUT/pf.log 2>&1; echo "rc=$?" >> $OUT/pf.log; tail -1 $OUT/pf.log
