@@ -169,6 +169,7 @@ struct sp_graph {
     int32_t *uadj = nullptr;
     uint2 *uinfo = nullptr;
     int32_t *uorder = nullptr;  // upper-CSR row r is the vertex uorder[r] (rows = degree ranks)
+    bool tc_simple = false;     // no multi-edge: every upper-slot multiplicity is 1
     int64_t m_up = -1;      // real upper slots; -1: not built
     int64_t m_up_pad = 0;   // padded slots
     int32_t *ubig = nullptr;  // vertices whose upper row exceeds the warp path

@@ -273,6 +273,15 @@ __global__ void k_up_place(const uint64_t *__restrict__ keys, int64_t mu,
     }
 }
 
+__global__ void k_up_dups(const uint64_t *__restrict__ keys, int64_t mu, unsigned long long *dup) {
+    for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < mu;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (keys[i] == keys[i - 1]) {
+            *dup = 1ull;
+            return;
+        }
+}
+
 __global__ void k_up_start(const int64_t *__restrict__ start8, int64_t n, uint32_t *ustart8) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n;
          v += (int64_t)gridDim.x * blockDim.x)
@@ -391,7 +400,17 @@ int ensure_upper(sp_graph *g, Call &c) {
         }));
         k_up_place<<<grid_for(mu, 256, c.device, 16), 256, 0, c.stream>>>(keys_s, mu, S, start8,
                                                                         ulen, uadj, uinfo);
+        // a repeated (row, element) key = a multi-edge: multiplicities > 1
+        unsigned long long *dup;
+        SP_TRY(c.alloc(&dup, 1));
+        SP_CUDA(cudaMemsetAsync(dup, 0, 8, c.stream));
+        k_up_dups<<<grid_for(mu, 256, c.device, 16), 256, 0, c.stream>>>(keys_s, mu, dup);
+        SP_CUDA(cudaMemcpyAsync(h + 4, dup, 8, cudaMemcpyDeviceToHost, c.stream));
+        SP_CUDA(cudaStreamSynchronize(c.stream));
+    } else {
+        h[4] = 0;
     }
+    const bool simple = h[4] == 0;
     k_up_start<<<grid_for(n + 1, 256, c.device, 16), 256, 0, c.stream>>>(start8, n, ustart8);
     c.launches += 9;
     SP_CUDA(cudaGetLastError());
@@ -432,6 +451,7 @@ int ensure_upper(sp_graph *g, Call &c) {
     }
     gd.keep = true;
     g->uorder = order;
+    g->tc_simple = simple;
     g->tc_warp_max = warp_max;
     g->ubig = big;
     g->nbig = (int64_t)h[1];
@@ -754,7 +774,8 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
                                                       int64_t nbig, const int32_t *__restrict__ order,
                                                       int64_t id0, int64_t id1,
                                                       int hash_max, int big_max, TcCounters *ctr,
-                                                      int64_t hub_base, int hub_words) {
+                                                      int64_t hub_base, int hub_words,
+                                                      int hub_bits) {
     extern __shared__ uint32_t smem[];
     uint32_t *F = smem;                                        // kBigFilterBits / 32 words
     int32_t *A = reinterpret_cast<int32_t *>(smem + kBigFilterBits / 32);
@@ -785,7 +806,7 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
         // N+(b) ranks above a, i.e. inside [hub_base, n) -- a direct-indexed
         // array of 16-bit multiplicities replaces the hash probes (one
         // shared load per element, no probe loop, no divergence)
-        const bool hub = a >= hub_base && na <= 65535;
+        const bool hub = a >= hub_base && (hub_bits || na <= 65535);
         const bool staged = !hub && na <= big_max;
         const bool hashed = !hub && na <= hash_max;
         int tbits = 6;  // table of 2^tbits >= 2 na entries
@@ -804,7 +825,10 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
             __syncthreads();
             for (int k = threadIdx.x; k < na; k += blockDim.x) {
                 const int64_t i = (int64_t)uadj[r0 + k] - hub_base;
-                atomicAdd(&HUB[i >> 1], 1u << ((i & 1) * 16));
+                if (hub_bits)  // simple graph: multiplicities are 0 / 1
+                    atomicOr(&HUB[i >> 5], 1u << (i & 31));
+                else
+                    atomicAdd(&HUB[i >> 1], 1u << ((i & 1) * 16));
             }
             __syncthreads();
         } else if (hashed) {
@@ -891,7 +915,8 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
                     if (x < 0) continue;
                     if (hub) {
                         const int64_t i = (int64_t)x - hub_base;
-                        cnt += (HUB[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+                        cnt += hub_bits ? (HUB[i >> 5] >> (i & 31)) & 1u
+                                        : (HUB[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
                     } else if (hashed) {  // multiplicity of x in A
 #ifndef SP_TC_BIG_NOFILTER
                         const uint32_t fb = ((uint32_t)x * 0x9E3779B1u) >> (32 - fbits);
@@ -1047,10 +1072,14 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
                 // hub rows: the top ranks whose 16-bit count array fits kHubSmem
                 // (SP_TC_HUB=0: off; rows are ranks, so hubs are [hub_base, n))
                 const char *he = getenv("SP_TC_HUB");
-                const int64_t hub_n = (he && he[0] == '0') ? 0
-                                      : std::min<int64_t>(n, (int64_t)kHubSmem / 2);
+                // simple graphs (no multi-edges): one bit per hub rank, 8x the rows
+                const int hub_bits = g->tc_simple && !(he && he[0] == '2') ? 1 : 0;
+                const int64_t hub_n =
+                    (he && he[0] == '0') ? 0
+                                         : std::min<int64_t>(n, (int64_t)kHubSmem * (hub_bits ? 8 : 1) /
+                                                                    (hub_bits ? 1 : 2));
                 const int64_t hub_base = n - hub_n;
-                const int hub_words = (int)((hub_n + 1) / 2);
+                const int hub_words = (int)(hub_bits ? (hub_n + 31) / 32 : (hub_n + 1) / 2);
                 if (hub_n) smem = std::max<size_t>(smem, (size_t)hub_words * 4);
                 SP_CUDA(cudaFuncSetAttribute(k_tc_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
@@ -1061,7 +1090,7 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
                 k_tc_big<<<gb, kBigBlock, smem, c.stream>>>(g->ustart8, g->ulen, g->uadj, g->uinfo,
                                                          g->ubig, g->nbig, order, v0, v1,
                                                          hash_max, big_max, ctr, hub_base,
-                                                         hub_words);
+                                                         hub_words, hub_bits);
                 c.launches++;
             }
         }
