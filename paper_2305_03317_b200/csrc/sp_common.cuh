@@ -170,6 +170,8 @@ struct sp_graph {
     uint2 *uinfo = nullptr;
     int32_t *uorder = nullptr;  // upper-CSR row r is the vertex uorder[r] (rows = degree ranks)
     bool tc_simple = false;     // no multi-edge: every upper-slot multiplicity is 1
+    int64_t tc_hub_base = 0;    // upper rows >= this rank are hub rows (k_tc_big's bitmap form)
+    int tc_hub_min = 0;         // hub rows longer than this are in ubig
     int64_t m_up = -1;      // real upper slots; -1: not built
     int64_t m_up_pad = 0;   // padded slots
     int32_t *ubig = nullptr;  // vertices whose upper row exceeds the warp path

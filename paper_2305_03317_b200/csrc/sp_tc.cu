@@ -75,6 +75,14 @@ constexpr int kUnrollHash = 4;     // ... in k_tc_fwd_hash (skewed graphs; 2 is 
 #ifndef SP_TC_PAD
 #define SP_TC_PAD 8
 #endif
+#ifndef SP_TC_HUB_SMEM
+#define SP_TC_HUB_SMEM (32 * 1024)  // bits, RMAT-24: 16 KB 308 ms, 32 KB 280, 48 KB 304 (16-bit: 32 KB 382, 64 KB 488)
+#endif
+constexpr int kHubSmem = SP_TC_HUB_SMEM;  // bytes of hub bits / 16-bit counts (256 K / 16 K ranks)
+#ifndef SP_TC_HUB_MIN
+#define SP_TC_HUB_MIN 128  // RMAT-22: 256 -> 63.9 ms, 128 -> 46.7; RMAT-24: 279.6 -> 282.5 (32, 64: no better)
+#endif
+constexpr int kHubMinRow = SP_TC_HUB_MIN;  // hub rows longer than this go to k_tc_big
 constexpr int kPad = SP_TC_PAD;     // upper rows padded/aligned to 32-byte sectors
 constexpr int kQ = kPad / 4;       // 16-byte quarters per padded block
 
@@ -288,14 +296,14 @@ __global__ void k_up_start(const int64_t *__restrict__ start8, int64_t n, uint32
         ustart8[v] = (uint32_t)start8[v];
 }
 
-__global__ void k_big_list(const int32_t *__restrict__ ulen, int64_t n, int thr, int32_t *list,
-                           unsigned long long *cnt) {
+__global__ void k_big_list(const int32_t *__restrict__ ulen, int64_t n, int thr, int64_t hub_base,
+                           int hub_min, int32_t *list, unsigned long long *cnt) {
     unsigned long long mx = 0;
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = b + threadIdx.x;
         const int32_t l = v < n ? ulen[v] : 0;
         mx = max(mx, (unsigned long long)l);
-        const bool big = l > thr;
+        const bool big = l > thr || (v >= hub_base && l > hub_min);
         const int64_t slot = warp_append(big, &cnt[0]);
         if (big) list[slot] = (int32_t)v;
     }
@@ -422,7 +430,17 @@ int ensure_upper(sp_graph *g, Call &c) {
     // SP_TC_WARP_MAX (tests): route shorter rows to k_tc_big too (<= kA)
     const char *wm = getenv("SP_TC_WARP_MAX");
     const int warp_max = wm ? std::max(1, std::min(kA, atoi(wm))) : kA;
-    k_big_list<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(ulen, n, warp_max, big, bc);
+    // hub rows (the top ranks, a bitmap / count array in k_tc_big): on
+    // simple graphs one bit per rank; rows of those ranks longer than
+    // hub_min also go to k_tc_big (SP_TC_HUB_MIN)
+    const char *hmn = getenv("SP_TC_HUB_MIN");
+    const int hub_min = hmn ? std::max(0, atoi(hmn)) : kHubMinRow;
+    const bool hub_bits = simple;
+    const int64_t hub_n = std::min<int64_t>(n, (int64_t)kHubSmem * (hub_bits ? 8 : 1) /
+                                                   (hub_bits ? 1 : 2));
+    const int64_t hub_base = n - hub_n;
+    k_big_list<<<grid_for(n, 256, c.device, 16), 256, 0, c.stream>>>(ulen, n, warp_max, hub_base,
+                                                                    hub_min, big, bc);
     c.launches += 4;
     SP_CUDA(cudaGetLastError());
     SP_CUDA(cudaMemcpyAsync(h + 1, bc, 16, cudaMemcpyDeviceToHost, c.stream));
@@ -452,6 +470,8 @@ int ensure_upper(sp_graph *g, Call &c) {
     gd.keep = true;
     g->uorder = order;
     g->tc_simple = simple;
+    g->tc_hub_base = hub_base;
+    g->tc_hub_min = hub_min;
     g->tc_warp_max = warp_max;
     g->ubig = big;
     g->nbig = (int64_t)h[1];
@@ -490,7 +510,7 @@ __global__ void __launch_bounds__(kBlock, SP_TCP_MINB) k_tc_fwd_plain(const uint
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
                                                    int64_t v1, int amax, TcCounters *ctr,
                                                    const int32_t *__restrict__ order,
-                                                   int64_t id0, int64_t id1) {
+                                                   int64_t id0, int64_t id1, int64_t hub_base, int hub_min) {
     __shared__ int32_t sA[kWarps][kA];
     __shared__ uint32_t sB[kWarps][kA];       // sector start of row b_j
     __shared__ int32_t sS[kWarps][kA + 1];    // half-sector prefix over the rows b_j (element-holding halves only)
@@ -524,7 +544,8 @@ __global__ void __launch_bounds__(kBlock, SP_TCP_MINB) k_tc_fwd_plain(const uint
             const int na = __shfl_sync(0xffffffffu, my_len, src);
             if (na < 2) continue;  // a triangle needs b and x in N+(a)
             const int64_t r0 = kPad * (int64_t)__shfl_sync(0xffffffffu, my_s8, src);
-            if (na > amax) continue;  // k_tc_big (one CTA per vertex) counts it
+            if (na > amax || (a >= hub_base && na > hub_min))
+                continue;  // k_tc_big (one CTA per vertex) counts it
             if (lane == 0) {
                 pairs += (unsigned long long)na;
                 abytes += (unsigned long long)na * (unsigned long long)na;
@@ -606,7 +627,7 @@ __global__ void __launch_bounds__(kBlock, SP_TCH_MINB) k_tc_fwd_hash(const uint3
                                                    const uint2 *__restrict__ uinfo, int64_t v0,
                                                    int64_t v1, int amax, TcCounters *ctr,
                                                    const int32_t *__restrict__ order,
-                                                   int64_t id0, int64_t id1) {
+                                                   int64_t id0, int64_t id1, int64_t hub_base, int hub_min) {
     // per warp, dynamic shared memory: hash keys[kT] + counts[kT] of A,
     // sector starts B[kA], half-sector prefix S[kA+1], filter F[kFilterWords]
     extern __shared__ uint32_t fwd_smem[];
@@ -641,7 +662,8 @@ __global__ void __launch_bounds__(kBlock, SP_TCH_MINB) k_tc_fwd_hash(const uint3
             const int na = __shfl_sync(0xffffffffu, my_len, src);
             if (na < 2) continue;  // a triangle needs b and x in N+(a)
             const int64_t r0 = kPad * (int64_t)__shfl_sync(0xffffffffu, my_s8, src);
-            if (na > amax) continue;  // k_tc_big (one CTA per vertex) counts it
+            if (na > amax || (a >= hub_base && na > hub_min))
+                continue;  // k_tc_big (one CTA per vertex) counts it
             if (lane == 0) {
                 pairs += (unsigned long long)na;
                 abytes += (unsigned long long)na * (unsigned long long)na;
@@ -749,10 +771,6 @@ __global__ void __launch_bounds__(kBlock, SP_TCH_MINB) k_tc_fwd_hash(const uint3
 constexpr int kBigFilterBits = 1 << 17;  // 16 KB
 constexpr int kBigFilterShift = 32 - 17;
 constexpr int kBigMax = 48 * 1024;      // staged A entries (192 KB) -- beyond: global search
-#ifndef SP_TC_HUB_SMEM
-#define SP_TC_HUB_SMEM (32 * 1024)  // RMAT-24: off 398 ms, 32 KB 382, 64 KB 488, 128 KB 956 (occupancy)
-#endif
-constexpr int kHubSmem = SP_TC_HUB_SMEM;  // bytes of 16-bit hub counts (16 K top-ranked rows)
 constexpr int kHashMax = 8 * 1024;      // rows up to this are hashed: 2^14 x (key, count) = 128 KB
 // One CTA per SM (the shared table); 8 warps per vertex -- 32 warps
 // measured slower (744 vs 534 ms on RMAT-24): the static 32-row batches
@@ -789,6 +807,9 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
     // assignment keeps the hub tail short on skewed graphs.
     __shared__ long long s_bi;
     __shared__ int s_j;
+    bool hub_clean = false;  // the hub array holds only row (prev_r0, prev_na)'s entries
+    int64_t prev_r0 = 0;
+    int prev_na = 0;
     for (;;) {
         __syncthreads();  // every warp is done with the previous vertex
         if (threadIdx.x == 0) {
@@ -819,9 +840,16 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
         uint32_t *HF = HC + T;
         const int fbits = tbits + 3;
         __syncthreads();  // previous vertex done with the shared structures
-        uint32_t *HUB = smem;  // hub form: 16-bit counts, two per word, index x - hub_base
+        uint32_t *HUB = smem;  // hub form: bits (or 16-bit counts), index x - hub_base
         if (hub) {
-            for (int k = threadIdx.x; k < hub_words; k += blockDim.x) HUB[k] = 0u;
+            if (hub_clean) {  // only the previous hub row's words are set: clear them
+                for (int k = threadIdx.x; k < prev_na; k += blockDim.x) {
+                    const int64_t i = (int64_t)uadj[prev_r0 + k] - hub_base;
+                    HUB[hub_bits ? i >> 5 : i >> 1] = 0u;
+                }
+            } else {  // after a hash / staged row (or at the start): the whole array
+                for (int k = threadIdx.x; k < hub_words; k += blockDim.x) HUB[k] = 0u;
+            }
             __syncthreads();
             for (int k = threadIdx.x; k < na; k += blockDim.x) {
                 const int64_t i = (int64_t)uadj[r0 + k] - hub_base;
@@ -868,6 +896,10 @@ __global__ void __launch_bounds__(kBigBlock, 1) k_tc_big(const uint32_t *__restr
             pairs += (unsigned long long)na;
             abytes += (unsigned long long)na * (unsigned long long)na;
         }
+        // (block-uniform) the next hub row clears only this row's words
+        hub_clean = hub;
+        prev_r0 = r0;
+        prev_na = na;
         for (;;) {
             int j0 = 0;
             if (lane == 0) j0 = atomicAdd(&s_j, 32);
@@ -1051,11 +1083,13 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
                 k_tc_fwd_hash<<<grid, kBlock, fsm, c.stream>>>(g->ustart8, g->ulen, g->uadj,
                                                                g->uinfo, 0, n, g->tc_warp_max,
-                                                               ctr, order, v0, v1);
+                                                               ctr, order, v0, v1, g->tc_hub_base,
+                                                               g->tc_hub_min);
             } else {
                 k_tc_fwd_plain<<<grid, kBlock, 0, c.stream>>>(g->ustart8, g->ulen, g->uadj,
                                                               g->uinfo, 0, n, g->tc_warp_max,
-                                                              ctr, order, v0, v1);
+                                                              ctr, order, v0, v1, g->tc_hub_base,
+                                                              g->tc_hub_min);
             }
             c.launches++;
             if (g->nbig) {
@@ -1073,12 +1107,13 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
                 // (SP_TC_HUB=0: off; rows are ranks, so hubs are [hub_base, n))
                 const char *he = getenv("SP_TC_HUB");
                 // simple graphs (no multi-edges): one bit per hub rank, 8x the rows
+                // (SP_TC_HUB=2: 16-bit counts, =0: the hash forms for every row)
                 const int hub_bits = g->tc_simple && !(he && he[0] == '2') ? 1 : 0;
-                const int64_t hub_n =
-                    (he && he[0] == '0') ? 0
-                                         : std::min<int64_t>(n, (int64_t)kHubSmem * (hub_bits ? 8 : 1) /
-                                                                    (hub_bits ? 1 : 2));
-                const int64_t hub_base = n - hub_n;
+                int64_t hub_base = g->tc_hub_base;
+                if (!hub_bits && g->tc_simple)  // 16-bit counts cover 16x fewer ranks
+                    hub_base = std::max<int64_t>(hub_base, n - (int64_t)kHubSmem / 2);
+                if (he && he[0] == '0') hub_base = n;
+                const int64_t hub_n = n - hub_base;
                 const int hub_words = (int)(hub_bits ? (hub_n + 31) / 32 : (hub_n + 1) / 2);
                 if (hub_n) smem = std::max<size_t>(smem, (size_t)hub_words * 4);
                 SP_CUDA(cudaFuncSetAttribute(k_tc_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
