@@ -1903,6 +1903,10 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
         iters++;
         frontier_sum += nq;
         relaxed += (int64_t)hc->scanned;
+        if (trace)
+            fprintf(stderr, "sssp it %lld: frontier %lld, scanned %llu, next %llu, %.1f us\n",
+                    (long long)iters, (long long)nq, (unsigned long long)hc->scanned,
+                    (unsigned long long)hc->next_size, ms * 1e3);
         if (hc->flag) {
             set_error("SSSP distance left the int32 range (negative weights)");
             rc = SP_ERR_OVERFLOW;

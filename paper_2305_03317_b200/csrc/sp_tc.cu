@@ -51,6 +51,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <chrono>
 #include <mutex>
 
 #include "sp_common.cuh"
@@ -334,6 +335,16 @@ int ensure_upper(sp_graph *g, Call &c) {
     std::lock_guard<std::mutex> lk(g_up_mu);
     if (g->m_up >= 0) return SP_OK;
     const int64_t n = g->n;
+    // SP_TC_TRACE: host time of each build phase (synchronising; diagnostics)
+    static const bool trace = getenv("SP_TC_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char *what) {
+        if (!trace) return;
+        cudaStreamSynchronize(c.stream);
+        fprintf(stderr, "tc upper build: %-12s %8.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                    .count());
+    };
     // ---- degree ranks (ascending (degree, id)); rows and elements are ranks
     uint64_t *rkey, *rkey_s;
     int32_t *rid, *rank;
@@ -362,6 +373,7 @@ int ensure_upper(sp_graph *g, Call &c) {
                                                c.stream);
     }));
     k_rank_scatter<<<gridn, 256, 0, c.stream>>>(order, n, rank);
+    mark("ranks");
     // ---- row lengths, unpadded (S) and padded (start8) row starts
     int64_t *len64, *pad8, *S, *start8;
     SP_TRY(c.alloc(&len64, n + 1));
@@ -370,6 +382,7 @@ int ensure_upper(sp_graph *g, Call &c) {
     SP_TRY(c.alloc(&start8, n + 1));
     const int grid = grid_for(n * 32, 256, c.device, 16);
     k_up_count<<<grid, 256, 0, c.stream>>>(g->off, g->adj, rank, n, ulen, len64, pad8);
+    mark("count");
     SP_TRY(cub_call(c, [&](void *t, size_t &s) {
         return cub::DeviceScan::ExclusiveSum(t, s, pad8, start8, n + 1, c.stream);
     }));
@@ -396,16 +409,20 @@ int ensure_upper(sp_graph *g, Call &c) {
     gd.p[3] = ustart8;
     SP_CUDA(cudaMemsetAsync(uadj, 0xFF, std::max<int64_t>(8, mpad) * sizeof(int32_t), c.stream));
     SP_CUDA(cudaMemsetAsync(uinfo, 0, std::max<int64_t>(8, mpad) * sizeof(uint2), c.stream));
+    mark("alloc rows");
     // ---- (row, element) keys, sorted: every row ascending
     if (mu > 0) {
         uint64_t *keys, *keys_s;
         SP_TRY(c.alloc(&keys, mu));
         SP_TRY(c.alloc(&keys_s, mu));
+        mark("alloc keys");
         k_up_emit<<<grid, 256, 0, c.stream>>>(g->off, g->adj, rank, S, n, keys);
+        mark("emit");
         SP_TRY(cub_call(c, [&](void *t, size_t &s) {
             return cub::DeviceRadixSort::SortKeys(t, s, keys, keys_s, mu, 0, 32 + nbits,
                                                   c.stream);
         }));
+        mark("sort");
         k_up_place<<<grid_for(mu, 256, c.device, 16), 256, 0, c.stream>>>(keys_s, mu, S, start8,
                                                                         ulen, uadj, uinfo);
         // a repeated (row, element) key = a multi-edge: multiplicities > 1
@@ -418,6 +435,7 @@ int ensure_upper(sp_graph *g, Call &c) {
     } else {
         h[4] = 0;
     }
+    mark("place+dups");
     const bool simple = h[4] == 0;
     k_up_start<<<grid_for(n + 1, 256, c.device, 16), 256, 0, c.stream>>>(start8, n, ustart8);
     c.launches += 9;
@@ -467,6 +485,7 @@ int ensure_upper(sp_graph *g, Call &c) {
         c.launches += 2;
         SP_CUDA(cudaStreamSynchronize(c.stream));
     }
+    mark("big list");
     gd.keep = true;
     g->uorder = order;
     g->tc_simple = simple;
