@@ -74,6 +74,50 @@ struct RelaxOp {
     }
 };
 
+// RelaxOp with dist and the enqueue stamp in one 64-bit word per vertex
+// (high half: dist, low half: the iteration that queued it): one atomicMin
+// relaxes and, through the old word, says whether x was already queued this
+// iteration -- one returning atomic per improving slot instead of two in
+// series.  Ordered by dist first (the stamp only breaks ties, which never
+// count as improvements).
+struct RelaxPackedOp {
+    using Payload = int;
+    using Probe = RelaxOp::Probe;
+    long long *__restrict__ dq;
+    const int32_t *__restrict__ weff;
+    unsigned long long *overflow;
+    int it;
+    __device__ __forceinline__ int payload(int32_t v) const { return (int)(__ldcg(dq + v) >> 32); }
+    __device__ __forceinline__ Probe probe(int64_t e, int32_t x) const {
+        return Probe{__ldcs(weff + e), (int)(__ldcg(dq + x) >> 32)};
+    }
+    __device__ __forceinline__ bool apply(int dv, int64_t, int32_t x, Probe p) const {
+        const int64_t cand = (int64_t)dv + (int64_t)p.w;
+        if (cand >= (int64_t)kIntMax) return false;  // never beats INT_MAX (F12)
+        if (cand < (int64_t)(-2147483647 - 1)) {
+            atomicAdd(overflow, 1ull);
+            return false;
+        }
+        const int c = (int)cand;
+        if (c >= p.dx) return false;  // conservative pre-filter
+        const long long w = (long long)(((unsigned long long)(unsigned)c << 32) | (unsigned)it);
+        const long long old = atomicMin(dq + x, w);
+        return (int)(old >> 32) > c && (unsigned)old != (unsigned)it;
+    }
+};
+
+__global__ void k_init_packed(long long *dq, int64_t n, int32_t src) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x)
+        dq[x] = x == src ? 0ll : (long long)(((unsigned long long)kIntMax << 32) | 0xFFFFFFFFull);
+}
+
+__global__ void k_unpack(const long long *__restrict__ dq, int64_t n, int32_t *dist) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x)
+        dist[x] = (int32_t)(dq[x] >> 32);
+}
+
 __global__ void k_init(int32_t *dist, int32_t *enq, int64_t n, int32_t src, int32_t *q) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
          x += (int64_t)gridDim.x * blockDim.x) {
@@ -106,13 +150,16 @@ struct SsspLoop {
 #ifndef SP_RLC_MINB
 #define SP_RLC_MINB 4
 #endif
+// Op: RelaxOp or RelaxPackedOp; its overflow counter and stamp are this
+// iteration's (from L)
+template <class Op>
 __global__ void __launch_bounds__(kExpandBlock, SP_RL_MINB) k_relax_loop(
-    int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, ChunkItem *chunks,
+    Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj, ChunkItem *chunks,
     SsspLoop *L, int64_t warps) {
     const int cur = L->cur;
     const int64_t nq = L->nq;
-    RelaxOp op{dist, enq, weff, &L->cnt[cur].flag, L->it};
+    op.overflow = &L->cnt[cur].flag;
+    op.it = L->it;
     expand_body(op, off, adj, L->q[cur], nq, L->q[cur ^ 1], chunks, &L->cnt[cur],
                 expand_vpw(nq, warps));
 }
@@ -122,12 +169,13 @@ __device__ __forceinline__ int loop_advance(SsspLoop *L);
 // Hub chunks; the last block to finish also runs the loop advance (one
 // graph node per iteration fewer: ~4 us of node latency each, cfg1 runs
 // 9-10 iterations of ~40 us).
+template <class Op>
 __global__ void __launch_bounds__(kExpandBlock, SP_RLC_MINB) k_relax_loop_chunks(
-    int32_t *dist, int32_t *enq, const int32_t *__restrict__ weff,
-    const int64_t *__restrict__ off, const int32_t *__restrict__ adj, const ChunkItem *chunks,
-    SsspLoop *L, cudaGraphConditionalHandle h) {
+    Op op, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+    const ChunkItem *chunks, SsspLoop *L, cudaGraphConditionalHandle h) {
     const int cur = L->cur;
-    RelaxOp op{dist, enq, weff, &L->cnt[cur].flag, L->it};
+    op.overflow = &L->cnt[cur].flag;
+    op.it = L->it;
     expand_chunks_body(op, off, adj, chunks, L->q[cur ^ 1], &L->cnt[cur]);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1721,7 +1769,8 @@ int64_t near_far_delta(const sp_graph *g, int32_t wmin, int32_t wmax) {
 }
 
 int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t *qa, int32_t *qb,
-                     ChunkItem *chunks, int64_t cap, SsspLoop *hL, float *kernel_ms) {
+                     ChunkItem *chunks, int64_t cap, SsspLoop *hL, float *kernel_ms,
+                     int32_t init_src) {
     SsspLoop *L;
     SP_TRY(c.alloc(&L, 1));
     SsspLoop init{};
@@ -1737,8 +1786,17 @@ int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t 
     // wants 8); SP_SSSP_GRID_MUL overrides
     const char *gm = getenv("SP_SSSP_GRID_MUL");
     const int grid = sms * (gm ? std::max(1, atoi(gm)) : (g->m < (int64_t(1) << 22) ? 4 : 8));
+    // (dist, stamp) words: one returning atomic per improving slot
+    // (SP_SSSP_PACKED=0: separate dist / enq arrays)
+    const char *pe = getenv("SP_SSSP_PACKED");
+    const bool packed = !(pe && pe[0] == '0');
     const int64_t warps = (int64_t)grid * (kExpandBlock / 32);
     const bool big = g->max_outdeg > kSplit;
+    long long *dq = nullptr;
+    if (packed) {
+        SP_TRY(c.alloc(&dq, std::max<int64_t>(1, g->n)));
+        k_init_packed<<<grid_for(g->n, kBlock, c.device), kBlock, 0, c.stream>>>(dq, g->n, init_src);
+    }
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     struct GraphFree {
@@ -1762,13 +1820,18 @@ int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t 
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     SP_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0,
                                           cudaStreamCaptureModeThreadLocal));
-    k_relax_loop<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off, g->adj, chunks,
-                                                      L, warps);
-    if (big)
-        k_relax_loop_chunks<<<grid, kExpandBlock, 0, c.stream>>>(dist, enq, g->weff, g->off,
-                                                                 g->adj, chunks, L, h);
+    auto body_nodes = [&](auto op) {
+        k_relax_loop<<<grid, kExpandBlock, 0, c.stream>>>(op, g->off, g->adj, chunks, L, warps);
+        if (big)
+            k_relax_loop_chunks<<<grid, kExpandBlock, 0, c.stream>>>(op, g->off, g->adj, chunks, L,
+                                                                     h);
+        else
+            k_loop_advance<<<1, 1, 0, c.stream>>>(L, h);
+    };
+    if (packed)
+        body_nodes(RelaxPackedOp{dq, g->weff, nullptr, 0});
     else
-        k_loop_advance<<<1, 1, 0, c.stream>>>(L, h);
+        body_nodes(RelaxOp{dist, enq, g->weff, nullptr, 0});
     cudaError_t ce = cudaStreamEndCapture(c.stream, &body);
     SP_CUDA(ce);
     cudaEvent_t ka, kb;
@@ -1776,13 +1839,14 @@ int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t 
     SP_CUDA(cudaEventCreate(&kb));
     cudaEventRecord(ka, c.stream);
     SP_TRY(launch_cached_graph(graph, g, kLoopSsspBf, c.stream));
+    if (packed) k_unpack<<<grid_for(g->n, kBlock, c.device), kBlock, 0, c.stream>>>(dq, g->n, dist);
     cudaEventRecord(kb, c.stream);
     SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(SsspLoop), cudaMemcpyDeviceToHost, c.stream));
     SP_CUDA(cudaStreamSynchronize(c.stream));
     cudaEventElapsedTime(kernel_ms, ka, kb);
     cudaEventDestroy(ka);
     cudaEventDestroy(kb);
-    c.launches += hL->iters * 2;
+    c.launches += hL->iters * 2 + (packed ? 2 : 0);
     return SP_OK;
 }
 
@@ -1867,7 +1931,7 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
             if (pull_form || use_do)  // sssp_pull.sp: pull steps for large frontiers
                 lrc = sssp_do_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
             else
-                lrc = sssp_device_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms);
+                lrc = sssp_device_loop(g, c, dist, enq, qa, qb, chunks, cap, &hL, &kernel_ms, src);
         }
         if (lrc == SP_OK) {
             iters = hL.iters;

@@ -136,10 +136,6 @@ __device__ __forceinline__ void stage_a(const int32_t *__restrict__ adj, int64_t
     __syncwarp();
 }
 
-__device__ __forceinline__ bool rank_gt(int32_t dx, int32_t x, int32_t dv, int32_t v) {
-    return dx > dv || (dx == dv && x > v);
-}
-
 // Append the non-empty rows of one 32-row staging chunk (lane: sector start
 // s8, `secs` element-holding half-sectors) to B/S at nr; returns the new
 // running half-sector total (nr and the total are warp-uniform).
@@ -1073,9 +1069,17 @@ __global__ void __launch_bounds__(kBlock, 1) k_tc_mid(const int64_t *__restrict_
 extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_stats *st) {
     SP_CHECK(g && count && v0 >= 0 && v0 <= v1 && v1 <= g->n, SP_ERR_ARG,
              "sp_tc: bad arguments");
+    static const bool trace = getenv("SP_TC_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     Call c;
     SP_TRY(c.begin(g->device));
     if (!g->directed && g->n) SP_TRY(ensure_upper(g, c));
+    if (trace) {
+        cudaStreamSynchronize(c.stream);
+        fprintf(stderr, "tc: begin + upper CSR %.2f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                    .count());
+    }
     TcCounters *ctr;
     SP_TRY(c.alloc(&ctr, 1));
     SP_CUDA(cudaMemsetAsync(ctr, 0, sizeof(TcCounters), c.stream));
@@ -1159,6 +1163,10 @@ extern "C" int sp_tc(sp_graph *g, int64_t v0, int64_t v1, uint64_t *count, sp_st
     cudaEventElapsedTime(&ms, ka, kb);
     cudaEventDestroy(ka);
     cudaEventDestroy(kb);
+    if (trace)
+        fprintf(stderr, "tc: counting %.2f ms (device), call %.2f ms\n", ms,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                    .count());
     SP_TRY(rc);
     *count = (uint64_t)h->total;
     if (st) {

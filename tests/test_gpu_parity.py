@@ -179,6 +179,29 @@ def test_sssp_seeded(kind, p0, p1, und):
             np.testing.assert_array_equal(r.env.node_props["dist"], dist)
 
 
+@pytest.mark.parametrize("packed", ["1", "0"])
+@pytest.mark.parametrize("kind,p0,p1,und", [("rmat", 16, 16, False), ("rmat", 12, 48, True),
+                                            ("uniform", 1 << 12, 1 << 17, False)])
+def test_sssp_packed_words(kind, p0, p1, und, packed, monkeypatch):
+    """Bellman-Ford device loop with (dist, enqueue stamp) packed in one
+    64-bit word per vertex (one atomicMin relaxes and dedupes the next
+    frontier; the default) and with separate dist / enq arrays
+    (SP_SSSP_PACKED=0): the oracle's dist bit for bit, from several sources
+    including the largest hub, repeated (the atomics' order is racy)."""
+    monkeypatch.setenv("SP_SSSP_PACKED", packed)
+    monkeypatch.setenv("SP_SSSP_DELTA", "0")  # Bellman-Ford even on thin graphs
+    g, o = _pair(kind, p0, p1, 31, und)
+    deg = np.diff(np.asarray(g.offsets))
+    hub = int(np.argmax(deg))
+    for s in (0, hub, g.n // 2):
+        dist, _, rc = cpu_ref.sssp(o, s)
+        assert rc == 0
+        for rep in range(3):
+            r = sp.run(corpus.SSSP, g, {"src": s})
+            np.testing.assert_array_equal(r.env.node_props["dist"], dist, err_msg=f"rep {rep}")
+            assert not r.env.node_props["modified"].any()
+
+
 @pytest.mark.parametrize("kind,p0,p1,und,delta", [
     ("grid", 300, 280, True, None), ("grid", 512, 512, True, "40"), ("grid", 97, 1031, True, None),
     ("uniform", 1 << 16, 1 << 18, True, None), ("uniform", 1 << 16, 1 << 18, False, "7"),
