@@ -1828,6 +1828,8 @@ int sssp_device_loop(sp_graph *g, Call &c, int32_t *dist, int32_t *enq, int32_t 
         else
             k_loop_advance<<<1, 1, 0, c.stream>>>(L, h);
     };
+    // (a variant without the dq[x] pre-read before the atomic measured the
+    // same on cfg1 and 1.5x slower on RMAT-22: more atomics)
     if (packed)
         body_nodes(RelaxPackedOp{dq, g->weff, nullptr, 0});
     else
@@ -1908,6 +1910,8 @@ static int sssp_impl(sp_graph *g, int32_t src, int64_t cap, int32_t *dist_out, i
         // no caller cap is in force (the reference default 2n+16, which no
         // near-far run approaches) and the graph is thin (SP_NF_ASYNC=0: off)
         const char *ae = getenv("SP_NF_ASYNC");
+        // (forced onto cfg1's RMAT-16, hub rows walked by one warp: 0.9 ms --
+        // 2x the relaxations of the synchronous loop, 3.4 entries per batch)
         const bool async_nf = delta > 0 && g->max_outdeg <= kSplit && cap >= 2 * n + 16 &&
                               !(ae && ae[0] == '0');
         if (async_nf) {
