@@ -503,7 +503,8 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         mb = r.stats.get("model_bytes")
         out["tc_cfg3"] = _line("tc", "uniform 2^24 / 2^28 undirected", g, ms / reps,
                                g.m // 2, mb, hbm_peak, key=K("tc_cfg3"),
-                               first_call_ms=fc[0], upper_csr_build_ms=fc[0] - ms / reps,
+                               first_call_ms=fc[0],
+                               upper_csr_build_ms=g.preprocessing_ms().get("tc_upper"),
                                triangles=r.env.scalars["triangle_count"],
                                sharding=f"ranges/{world}")
         g.close()
@@ -515,7 +516,9 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         it = r.env.scalars["iter"]
         out["pr_rmat24"] = _line("pr", "rmat24 directed", g, ms / 3, it * g.m,
                                  it * (12 * g.m + 36 * g.n), hbm_peak, key=K("pr_rmat24"),
-                                 iterations=it, first_calls_ms=fc)
+                                 iterations=it, first_calls_ms=fc,
+                                 preprocessing_ms={k: v for k, v in g.preprocessing_ms().items()
+                                                   if k.startswith("pr_")})
         fc = first_calls(lambda: go(corpus.SSSP, g, {"src": 0}), 1, dev)  # + w_eff, rweff
         ms, _, r = timed(lambda: go(corpus.SSSP, g, {"src": 0}), 3, 2, world, dev)
         offs = np.asarray(g.offsets)
@@ -527,6 +530,8 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
             mb = 12 * r.stats["edges_visited"] + 20 * r.stats["vertices_visited"]
         out["sssp_rmat24"] = _line("sssp", "rmat24 directed", g, ms / 3, m_reached, mb, hbm_peak,
                                    key=K("sssp_rmat24"), first_call_ms=fc[0],
+                                   preprocessing_ms={k: v for k, v in g.preprocessing_ms().items()
+                                                     if k in ("weff", "rweff")},
                                    iterations=r.fixedpoint_iterations["finished"],
                                    note="12 B per relaxation (push) or swept in-slot (pull sweeps, "
                                         "frontier > n/8) + 20 B per frontier vertex")
@@ -536,7 +541,8 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
         ms, _, r = timed(lambda: go(corpus.TC, g, {}), 2, 1, world, dev)
         out["tc_rmat24"] = _line("tc", "rmat24 symmetrized", g, ms / 2, g.m // 2,
                                  r.stats.get("model_bytes"), hbm_peak, key=K("tc_rmat24"),
-                                 first_call_ms=fc[0], upper_csr_build_ms=fc[0] - ms / 2,
+                                 first_call_ms=fc[0],
+                                 upper_csr_build_ms=g.preprocessing_ms().get("tc_upper"),
                                  triangles=r.env.scalars["triangle_count"],
                                  sharding=f"ranges/{world}")
         g.close()

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 7
+#define SP_ABI_VERSION 8
 
 enum sp_status {
     SP_OK = 0,
@@ -128,6 +128,18 @@ int sp_graph_info(const sp_graph *g, int64_t *n, int64_t *m, int *directed);
 int sp_graph_download(const sp_graph *g, int which, void *host_dst);
 /* min_wt / max_wt (graph.py:252-261); SP_ERR_ARG when m == 0. */
 int sp_graph_weight_range(const sp_graph *g, int32_t *wmin, int32_t *wmax);
+/* One-time per-graph preprocessing that the first call needing it builds
+ * and caches on the handle (no reference counterpart: the interpreter keeps
+ * no derived structures).  *ms = device time of that build (CUDA events on
+ * the building call's stream), -1 when it was not built (or was built
+ * during the upload, untimed).  Waits for the build to finish. */
+#define SP_PREP_TC_UPPER 0 /* degree-ordered upper CSR (sp_tc)               */
+#define SP_PREP_WEFF     1 /* first-slot weights w_eff (sp_sssp)            */
+#define SP_PREP_RWEFF    2 /* reverse-slot w_eff (pull sweeps)              */
+#define SP_PREP_PR_HOT   3 /* PR hot-source encoding of radj                */
+#define SP_PREP_PR_REL   4 /* PR relabelled (out-degree rank) layout        */
+#define SP_PREP_ELL      5 /* ELL rows of bounded-degree graphs (async SSSP) */
+int sp_graph_prep_ms(const sp_graph *g, int kind, double *ms);
 void sp_graph_destroy(sp_graph *g);
 
 /* ---- executor: replaces trident/interp.py:579-589 on the corpus -------- */

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SP_LIB") or os.path.join(HERE, "libstarplat_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "starplat_b200.h")
 
-ABI_VERSION = 7  # must equal SP_ABI_VERSION in include/starplat_b200.h
+ABI_VERSION = 8  # must equal SP_ABI_VERSION in include/starplat_b200.h
 
 SP_OK = 0
 SP_ERR_ARG = -1
@@ -36,6 +36,7 @@ SP_ARR_OFFSETS, SP_ARR_ADJ, SP_ARR_WEIGHTS, SP_ARR_REV_OFFSETS, \
     SP_ARR_REV_ADJ, SP_ARR_REV_EID, SP_ARR_WEFF = range(7)
 SP_GEN_RMAT, SP_GEN_UNIFORM, SP_GEN_GRID = range(3)
 SP_REDUCE_SUM_I64, SP_REDUCE_MIN_F64, SP_REDUCE_MAX_F64 = range(3)
+PREP_KINDS = ("tc_upper", "weff", "rweff", "pr_hot", "pr_rel", "ell")  # SP_PREP_* order
 
 
 class Stats(C.Structure):
@@ -74,6 +75,7 @@ SIGNATURES = {
     "sp_graph_info": (_int, [_p, _p, _p, _p]),
     "sp_graph_download": (_int, [_p, _int, _p]),
     "sp_graph_weight_range": (_int, [_p, _p, _p]),
+    "sp_graph_prep_ms": (_int, [_p, _int, _p]),
     "sp_graph_destroy": (None, [_p]),
     "sp_sssp": (_int, [_p, _i32, _i64, _p, _int, _p, ITER_CB, _p, _p]),
     "sp_sssp_pull": (_int, [_p, _i32, _i64, _p, _int, _p, ITER_CB, _p, _p]),

@@ -207,6 +207,9 @@ struct sp_graph {
     int64_t *rel_nzend = nullptr, *rel_unit_row = nullptr;
     int64_t rel_nnz = 0, rel_nunits = 0;
     int rel_H = 0;
+    // one-time preprocessing timers (sp_graph_prep_ms): device events at the
+    // start and end of each lazily built structure, read on demand
+    cudaEvent_t prep_ev[8][2] = {};
 };
 
 // ---- device helpers --------------------------------------------------------
@@ -222,6 +225,14 @@ int pr_hot_prepare(sp_graph *g, Call &c, const int32_t *outdeg, int64_t max_outd
 // g->pr_H: > 0 built, 0 not worth it); shared by PR and the SSSP pull sweep.
 int pr_hot_build(sp_graph *g, Call &c);
 int ensure_weff(sp_graph *g, Call &c);
+// The lazily built per-graph structures whose build time sp_graph_prep_ms
+// reports (SP_PREP_* in starplat_b200.h).
+enum PrepKind {
+    kPrepTcUpper = 0, kPrepWeff = 1, kPrepRweff = 2, kPrepPrHot = 3, kPrepPrRel = 4,
+    kPrepEll = 5, kPrepKinds = 6
+};
+// Records the start (end = 0) or the end (end = 1) of one build on stream s.
+void prep_mark(sp_graph *g, int kind, int end, cudaStream_t s);
 // Reverse-slot weights rweff[k] = w_eff[reid[k]] (undirected: w_eff itself).
 int ensure_rweff(sp_graph *g, Call &c);
 // The ELL form above (built once when max out-degree <= d_max; else no-op).

@@ -383,8 +383,12 @@ void free_graph(sp_graph *g) {
     resident_free(g->rel_nzend);
     resident_free(g->rel_unit_row);
     resident_free(g->wrange);
+    for (auto &ev : g->prep_ev)
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
     delete g;
 }
+
 
 template <class T>
 int dalloc(T **p, size_t count) {
@@ -822,13 +826,26 @@ int unique_keys(Call &c, uint64_t *key, int64_t ne, uint64_t **uniq, int64_t *nu
 
 namespace sp {
 
+void prep_mark(sp_graph *g, int kind, int end, cudaStream_t s) {
+    if (kind < 0 || kind >= kPrepKinds) return;
+    cudaEvent_t &e = g->prep_ev[kind][end ? 1 : 0];
+    if (!e && cudaEventCreate(&e) != cudaSuccess) {
+        cudaGetLastError();
+        e = nullptr;
+        return;
+    }
+    cudaEventRecord(e, s);
+}
+
 // w_eff on first use (graphs adopted from a CSR defer it; see from_csr).
 int ensure_weff(sp_graph *g, Call &c) {
     std::lock_guard<std::mutex> lk(g_lazy_mu);
     if (g->weff || g->m == 0) return SP_OK;
     int32_t *weff = nullptr;
+    prep_mark(g, kPrepWeff, 0, c.stream);
     SP_TRY(dalloc(&weff, g->m));
     k_weff_csr<<<gridN(g->n * 32, c.device), 256, 0, c.stream>>>(g->off, g->adj, g->w, g->n, weff);
+    prep_mark(g, kPrepWeff, 1, c.stream);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
     if (e != cudaSuccess) {
@@ -869,12 +886,14 @@ int ensure_ell(sp_graph *g, Call &c, int d_max) {
     }
     if ((double)g->n * d * sizeof(int2) > 0.25 * (double)fr) return SP_OK;
     int2 *ell = nullptr;
+    prep_mark(g, kPrepEll, 0, c.stream);
     if (dalloc(&ell, g->n * d) != SP_OK) {
         cudaGetLastError();
         return SP_OK;
     }
     k_ell_fill<<<gridN(g->n * d, c.device), 256, 0, c.stream>>>(g->off, g->adj, g->weff, g->n, d,
                                                                  ell);
+    prep_mark(g, kPrepEll, 1, c.stream);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
     if (e != cudaSuccess) {
@@ -894,10 +913,12 @@ int ensure_rweff(sp_graph *g, Call &c) {
         g->rweff = g->weff;
         return SP_OK;
     }
+    prep_mark(g, kPrepRweff, 0, c.stream);
     if (!g->reid) SP_TRY(build_reverse(g, c, false, true));
     int32_t *rw = nullptr;
     SP_TRY(dalloc(&rw, g->m));
     k_rweff<<<gridN(g->m, c.device), 256, 0, c.stream>>>(g->weff, g->reid, g->m, rw);
+    prep_mark(g, kPrepRweff, 1, c.stream);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
     if (e != cudaSuccess) {
@@ -911,6 +932,20 @@ int ensure_rweff(sp_graph *g, Call &c) {
 }  // namespace sp
 
 extern "C" {
+
+int sp_graph_prep_ms(const sp_graph *g, int kind, double *ms) {
+    SP_CHECK(g && ms && kind >= 0 && kind < kPrepKinds, SP_ERR_ARG,
+             "sp_graph_prep_ms: bad arguments");
+    *ms = -1.0;
+    cudaEvent_t a = g->prep_ev[kind][0], b = g->prep_ev[kind][1];
+    if (!a || !b) return SP_OK;  // not built (or built at creation, untimed)
+    SP_CUDA(cudaSetDevice(g->device));
+    SP_CUDA(cudaEventSynchronize(b));
+    float f = 0.f;
+    SP_CUDA(cudaEventElapsedTime(&f, a, b));
+    *ms = f;
+    return SP_OK;
+}
 
 int sp_graph_from_edges(const int32_t *u, const int32_t *v, const int32_t *w, int64_t nedges,
                         int64_t n, int directed, int mem, int device, sp_graph **out) {

@@ -610,6 +610,7 @@ static int hot_build_locked(sp_graph *g, Call &c, bool now) {
         return SP_OK;
     }
     if (!now && g->pr_fast_calls++ == 0) return SP_OK;
+    prep_mark(g, kPrepPrHot, 0, c.stream);
     int32_t *hot_idx = nullptr;
     int H = 0;
     SP_TRY(pr_hot_select(g, c, g->outdeg, g->max_outdeg, &hot_idx, &H));
@@ -621,6 +622,7 @@ static int hot_build_locked(sp_graph *g, Call &c, bool now) {
     SP_TRY(resident_alloc((void **)&enc, (size_t)g->m * sizeof(int32_t)));
     k_hot_encode<<<grid_for(g->m, 256, c.device, 16), 256, 0, c.stream>>>(g->radj, g->m, hot_idx,
                                                                           enc);
+    prep_mark(g, kPrepPrHot, 1, c.stream);
     c.launches++;
     SP_CUDA(cudaGetLastError());
     SP_CUDA(cudaStreamSynchronize(c.stream));
@@ -752,6 +754,7 @@ int ensure_pr_rel(sp_graph *g, Call &c) {
         return SP_OK;
     }
     const int b = bits_for_n(n);
+    prep_mark(g, kPrepPrRel, 0, c.stream);
     // out-degree ranking (stable: ties by id) and the hot coverage
     uint32_t *key, *key_s;
     int32_t *id, *id_s;
@@ -873,6 +876,7 @@ int ensure_pr_rel(sp_graph *g, Call &c) {
     g->rel_nnz = nnz;
     g->rel_nunits = nunits;
     g->rel_H = H;
+    prep_mark(g, kPrepPrRel, 1, c.stream);
     g->pr_rel = 1;
     guard.ok = true;
     return SP_OK;

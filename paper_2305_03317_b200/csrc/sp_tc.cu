@@ -330,6 +330,7 @@ static int cub_call(Call &c, F f) {  // two-phase CUB call with stream-ordered s
 int ensure_upper(sp_graph *g, Call &c) {
     std::lock_guard<std::mutex> lk(g_up_mu);
     if (g->m_up >= 0) return SP_OK;
+    prep_mark(g, kPrepTcUpper, 0, c.stream);
     const int64_t n = g->n;
     // SP_TC_TRACE: host time of each build phase (synchronising; diagnostics)
     static const bool trace = getenv("SP_TC_TRACE") != nullptr;
@@ -482,6 +483,7 @@ int ensure_upper(sp_graph *g, Call &c) {
         SP_CUDA(cudaStreamSynchronize(c.stream));
     }
     mark("big list");
+    prep_mark(g, kPrepTcUpper, 1, c.stream);
     gd.keep = true;
     g->uorder = order;
     g->tc_simple = simple;

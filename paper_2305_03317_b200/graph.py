@@ -87,6 +87,21 @@ class CsrGraph:
             self._finalizer()
             self._h = None
 
+    def preprocessing_ms(self) -> dict:
+        """Device time (ms) of each one-time per-graph structure built so far
+        by the first call that needed it (degree-ordered upper CSR for TC,
+        w_eff, PR hot-source encoding / relabelled layout, ...); structures
+        not built (or built during the upload) are omitted.  No reference
+        counterpart: a measurement aid (sp_graph_prep_ms)."""
+        out = {}
+        ms = C.c_double(-1.0)
+        for kind, name in enumerate(_lib.PREP_KINDS):
+            _check(_lib.lib().sp_graph_prep_ms(self.handle, kind, C.byref(ms)),
+                   "sp_graph_prep_ms")
+            if ms.value >= 0:
+                out[name] = ms.value
+        return out
+
     # -- lazily downloaded host views (graph.py:28-36) ----------------------
     def _array(self, which: int, dtype, count: int) -> np.ndarray:
         with self._lock:

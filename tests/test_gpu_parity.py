@@ -883,3 +883,18 @@ def test_from_csr_rejects_bad_ids_pipelined():
     bad[m // 2] = -3
     with pytest.raises(ArgError):
         sp.from_csr(off, bad, None, directed=True)
+
+
+def test_preprocessing_times_reported():
+    """sp_graph_prep_ms: each lazily built per-graph structure reports its
+    build time once built (TC upper CSR, w_eff, PR hot encoding on the
+    second fast call) and nothing before."""
+    g, _ = _pair("rmat", 14, 16, 5, True)
+    assert "tc_upper" not in g.preprocessing_ms()
+    sp.run(corpus.TC, g, {})
+    sp.run(corpus.SSSP, g, {"src": 0})
+    pre = g.preprocessing_ms()
+    assert pre["tc_upper"] > 0 and pre["weff"] > 0
+    for _ in range(2):
+        sp.run(corpus.PR, g, {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100})
+    assert all(v >= 0 for v in g.preprocessing_ms().values())

@@ -49,7 +49,7 @@ def test_library_exports_every_declared_symbol():
     missing = set(header_symbols()) - exported
     assert not missing, missing
     L = _lib.lib()  # binds every signature
-    assert L.sp_abi_version() == _lib.ABI_VERSION == 7
+    assert L.sp_abi_version() == _lib.ABI_VERSION == 8
 
 
 def test_library_has_no_unresolved_internal_symbols():
