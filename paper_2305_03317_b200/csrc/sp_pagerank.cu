@@ -389,7 +389,13 @@ __global__ void __launch_bounds__(kHotBlock, 1) k_pr_units_rel(PrArgs a, int H) 
 // A row whose first and last slots lie in different units (a "spill" row)
 // was not summed by k_pr_units: its partials are added here left to right,
 // tp of every unit it crosses, then hp of the unit holding its end.
-constexpr int kEpi = 1;  // rows per thread; cfg2: 1/2/4/8 -> 239/237/234/221 GTEPS (more blocks beat per-thread MLP)
+#ifndef SP_PR_EPI_ROWS
+#define SP_PR_EPI_ROWS 2
+#endif
+// rows per thread; round 1 cfg2: 1/2/4/8 -> 239/237/234/221 GTEPS; round 2
+// (unrolled init, same box): 1 -> 2.90 / 7.85 ms, 2 -> 2.87 / 7.80 ms,
+// 4 -> 2.90 / 7.86 ms (cfg2 / RMAT-24 per run)
+constexpr int kEpi = SP_PR_EPI_ROWS;
 __global__ void __launch_bounds__(256) k_pr_epi(PrArgs a) {
     pr_bind(a);
     const int64_t nk = a.K1 - a.K0;
@@ -886,9 +892,18 @@ int ensure_pr_rel(sp_graph *g, Call &c) {
 __global__ void k_pr_unperm(const PrLoop *L, const int32_t *__restrict__ perm, int64_t n) {
     const double *rr = L->rank;
     double *out = L->rank_out;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x)
-        out[v] = rr[__ldcs(perm + v)];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n; v0 += 4 * stride) {
+        int32_t p[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) p[j] = v0 + j * stride < n ? __ldcs(perm + v0 + j * stride) : 0;
+        double r[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) r[j] = v0 + j * stride < n ? __ldcs(rr + p[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (v0 + j * stride < n) out[v0 + j * stride] = r[j];
+    }
 }
 
 // Per-call state of the fast path for a vertex block [v0, v1).
@@ -1097,6 +1112,10 @@ int launch_fast(Call &c, FastPlan &p, sp_graph *g, int64_t v1, const double *cin
     return SP_OK;
 }
 
+#ifndef SP_PR_INIT_U
+#define SP_PR_INIT_U 4
+#endif
+constexpr int kInitU = SP_PR_INIT_U;
 // Loop-path init (pr.sp:5-8 plus iteration 1 of the zero-in-degree rows):
 // rank = 1/n and c0 = rank/outdeg for every vertex; rows with no in-edges
 // get their final rank = base now, c1 = c2 = base/outdeg, and contribute
@@ -1108,20 +1127,34 @@ __global__ void __launch_bounds__(256) k_pr_init(PrLoop *L, const int32_t *__res
     const double base = L->base;
     double *rank = L->rank, *c0 = L->c0, *c1 = L->c1, *c2 = L->c2;
     double dmax = 0.0;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
-         x += (int64_t)gridDim.x * blockDim.x) {
-        const int d = __ldcs(outdeg + x);
-        c0[x] = d > 0 ? __ddiv_rn(r0, (double)d) : 0.0;
-        if (__ldcs(indeg + x) == 0) {
-            rank[x] = base;
-            const double cz = d > 0 ? __ddiv_rn(base, (double)d) : 0.0;
-            c1[x] = cz;
-            c2[x] = cz;
-            double t = __dsub_rn(base, r0);
-            if (t < 0.0) t = __dsub_rn(0.0, t);
-            dmax = fmax(dmax, t);
-        } else {
-            rank[x] = r0;
+    // kInitU vertices per thread and step, their loads issued first: the
+    // stream needs that many bytes in flight per SM (RMAT-24: 194 -> 169 us)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x0 < n;
+         x0 += stride * kInitU) {
+        int d[kInitU], in[kInitU];
+#pragma unroll
+        for (int j = 0; j < kInitU; j++) {
+            const int64_t x = x0 + j * stride;
+            d[j] = x < n ? __ldcs(outdeg + x) : 0;
+            in[j] = x < n ? __ldcs(indeg + x) : 1;
+        }
+#pragma unroll
+        for (int j = 0; j < kInitU; j++) {
+            const int64_t x = x0 + j * stride;
+            if (x >= n) break;
+            c0[x] = d[j] > 0 ? __ddiv_rn(r0, (double)d[j]) : 0.0;
+            if (in[j] == 0) {
+                rank[x] = base;
+                const double cz = d[j] > 0 ? __ddiv_rn(base, (double)d[j]) : 0.0;
+                c1[x] = cz;
+                c2[x] = cz;
+                double t = __dsub_rn(base, r0);
+                if (t < 0.0) t = __dsub_rn(0.0, t);
+                dmax = fmax(dmax, t);
+            } else {
+                rank[x] = r0;
+            }
         }
     }
     dmax = warp_max(dmax);
