@@ -212,6 +212,8 @@ __global__ void k_rank_scatter(const int32_t *__restrict__ order, int64_t n, int
         rank[order[r]] = (int32_t)r;
 }
 
+constexpr int kUpU = 4;  // upper-CSR build: 32-element groups in flight per warp step
+
 // Row rank[v] of the upper CSR = the ranks of v's neighbours ranked above v.
 __global__ void k_up_count(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
                            const int32_t *__restrict__ rank, int64_t n, int32_t *ulen,
@@ -223,7 +225,15 @@ __global__ void k_up_count(const int64_t *__restrict__ off, const int32_t *__res
         const int64_t r0 = off[v], r1 = off[v + 1];
         const int32_t rv = rank[v];
         int64_t c = 0;
-        for (int64_t e = r0 + lane; e < r1; e += 32) c += __ldg(rank + adj[e]) > rv ? 1 : 0;
+        // kUpU x 32 elements per step, loads first: a hub row of 10^6
+        // elements is otherwise a long chain of adj -> rank round trips
+        for (int64_t e0 = r0 + lane; e0 < r1; e0 += 32 * kUpU) {
+            int32_t x[kUpU];
+#pragma unroll
+            for (int j = 0; j < kUpU; j++) x[j] = e0 + 32 * j < r1 ? __ldg(adj + e0 + 32 * j) : -1;
+#pragma unroll
+            for (int j = 0; j < kUpU; j++) c += x[j] >= 0 && __ldg(rank + x[j]) > rv ? 1 : 0;
+        }
         c = warp_sum(c);
         if (lane == 0) {
             ulen[rv] = (int32_t)c;
@@ -248,16 +258,24 @@ __global__ void k_up_emit(const int64_t *__restrict__ off, const int32_t *__rest
         const int64_t r0 = off[v], r1 = off[v + 1];
         const int32_t rv = rank[v];
         int64_t pos = S[rv];
-        for (int64_t e0 = r0; e0 < r1; e0 += 32) {
-            const int64_t e = e0 + lane;
-            int32_t rx = -1;
-            if (e < r1) rx = __ldg(rank + adj[e]);
-            const bool keep = e < r1 && rx > rv;
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep)
-                keys[pos + __popc(m & ((1u << lane) - 1u))] =
-                    ((uint64_t)(uint32_t)rv << 32) | (uint32_t)rx;
-            pos += __popc(m);
+        for (int64_t e0 = r0; e0 < r1; e0 += 32 * kUpU) {
+            int32_t x[kUpU], rx[kUpU];
+#pragma unroll
+            for (int j = 0; j < kUpU; j++) {
+                const int64_t e = e0 + 32 * j + lane;
+                x[j] = e < r1 ? __ldg(adj + e) : -1;
+            }
+#pragma unroll
+            for (int j = 0; j < kUpU; j++) rx[j] = x[j] >= 0 ? __ldg(rank + x[j]) : -1;
+#pragma unroll
+            for (int j = 0; j < kUpU; j++) {
+                const bool keep = x[j] >= 0 && rx[j] > rv;
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (keep)
+                    keys[pos + __popc(m & ((1u << lane) - 1u))] =
+                        ((uint64_t)(uint32_t)rv << 32) | (uint32_t)rx[j];
+                pos += __popc(m);
+            }
         }
     }
 }
