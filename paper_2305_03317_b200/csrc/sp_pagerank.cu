@@ -49,6 +49,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <utility>
@@ -1352,6 +1353,16 @@ int pr_fast_run(sp_graph *g, Call &c, double damping, double epsilon, int64_t ma
     const int64_t n = g->n;
     const char *hl = getenv("SP_HOSTLOOP");
     const bool hostloop = cb || (hl && hl[0] == '1');
+    // SP_PR_TRACE: host time of the call's phases (diagnostics; syncs)
+    static const bool trace = getenv("SP_PR_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char *what) {
+        if (!trace) return;
+        cudaStreamSynchronize(c.stream);
+        fprintf(stderr, "pr: %-14s %7.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                    .count());
+    };
     // the layout must be settled before the executable is chosen: the
     // relabelled one from the graph's second fast call on (its build costs
     // about two runs), else the hot-encoded or plain one
@@ -1381,12 +1392,14 @@ int pr_fast_run(sp_graph *g, Call &c, double damping, double epsilon, int64_t ma
         L = reinterpret_cast<PrLoop *>(blk);
         hotc = reinterpret_cast<double *>(blk + hot_off);
     }
+    mark("layout+exec");
     FastPlan plan;
     if (rel) {
         SP_TRY(plan_rel(g, c, damping, plan));
     } else {
         SP_TRY(plan_fast(g, c, 0, n, damping, plan, hotc, true));
     }
+    mark("plan");
     double *c0, *c1, *c2, *rank_rel = nullptr;
     if (rel) SP_TRY(c.alloc(&rank_rel, n));
     SP_TRY(c.alloc(&c0, n));
@@ -1430,18 +1443,21 @@ int pr_fast_run(sp_graph *g, Call &c, double damping, double epsilon, int64_t ma
                 fprintf(stderr, "pr exec: %s (graph %llu)\n",
                         e->exec ? "capture + update" : "capture + instantiate",
                         (unsigned long long)g->uid);
+            mark("allocs+init");
             int rc = pr_build_exec(g, c, plan, L, &e->exec);
             c.launches = l0;
             if (rc != SP_OK) {
                 e->exec = nullptr;
                 return rc;
             }
+            mark("capture+update");
         }
         SP_CUDA(cudaEventRecord(ka, c.stream));
         SP_CUDA(cudaGraphLaunch(e->exec, c.stream));
         SP_CUDA(cudaEventRecord(kb, c.stream));
         SP_CUDA(cudaMemcpyAsync(hL, L, sizeof(PrLoop), cudaMemcpyDeviceToHost, c.stream));
         SP_CUDA(cudaStreamSynchronize(c.stream));
+        mark("loop");
         c.launches += 1 + hL->iters * per_it + (rel ? 1 : 0);
     } else {
         PrArgs a = plan.a;

@@ -356,9 +356,19 @@ int ensure_upper(sp_graph *g, Call &c) {
     auto mark = [&](const char *what) {
         if (!trace) return;
         cudaStreamSynchronize(c.stream);
-        fprintf(stderr, "tc upper build: %-12s %8.2f ms\n", what,
+        cudaMemPool_t pool;
+        uint64_t used = 0, resv = 0;
+        if (cudaDeviceGetDefaultMemPool(&pool, c.device) == cudaSuccess) {
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &resv);
+        }
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        fprintf(stderr, "tc upper build: %-12s %8.2f ms (pool used %.1f / reserved %.1f GiB, free %.1f GiB)\n",
+                what,
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
-                    .count());
+                    .count(),
+                used / 1073741824.0, resv / 1073741824.0, fr / 1073741824.0);
     };
     // ---- degree ranks (ascending (degree, id)); rows and elements are ranks
     uint64_t *rkey, *rkey_s;
@@ -377,6 +387,7 @@ int ensure_upper(sp_graph *g, Call &c) {
     } gd;
     gd.p[0] = ulen;
     gd.p[4] = order;
+    mark("alloc ranks");
     const int gridn = grid_for(n, 256, c.device, 16);
     k_rank_keys<<<gridn, 256, 0, c.stream>>>(g->outdeg, n, rkey, rid);
     int nbits = 1;
