@@ -44,6 +44,7 @@
 //   through shared memory and every lane folds its own row sequentially in
 //   CSR order: bit-identical to the interpreter, slower on hub rows.
 // No FMA contraction anywhere: __dadd_rn/__dmul_rn are used explicitly.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <stdlib.h>
@@ -226,10 +227,14 @@ __device__ __forceinline__ void load_slab(const int32_t *__restrict__ radj, int6
 // kMode: kPlain (every gather from cin), kEnc (radj slots carry kHotBit |
 // hot index for the hot sources), kRel (relabelled layout: sources are
 // ranked by out-degree, the hot ones are exactly the ids below relH).
-enum { kPlain = 0, kEnc = 1, kRel = 2 };
+enum { kPlain = 0, kEnc = 1, kRel = 2, kEnc2 = 3 };
+// kEnc2: a hot set split over a CTA pair (thread-block cluster): hot index
+// h lives in CTA h / relH's shared memory -- this CTA's (rank `my`) or the
+// peer's, read through distributed shared memory (`peer`).
 template <int kMode>
 __device__ __forceinline__ void pr_units_body(const PrArgs &a, uint32_t *bm, const double *hot,
-                                              int relH = 0) {
+                                              int relH = 0, const double *peer = nullptr,
+                                              int my = 0) {
     const unsigned lane = lane_id();
     if (lane < kCh / 32) bm[lane] = 0u;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -277,6 +282,18 @@ __device__ __forceinline__ void pr_units_body(const PrArgs &a, uint32_t *bm, con
                 } else if constexpr (kMode == kRel) {
                     const int x = idx[i];
                     val[i] = x < 0 ? 0.0 : x < relH ? hot[x] : __ldg(a.cin + x);
+                } else if constexpr (kMode == kEnc2) {
+                    const int x = idx[i];
+                    if (x < 0) {
+                        val[i] = 0.0;
+                    } else if (x & kHotBit) {
+                        const int h = x & (kHotBit - 1);
+                        const int ow = h >= relH ? 1 : 0;
+                        const int off = h - ow * relH;
+                        val[i] = ow == my ? hot[off] : peer[off];
+                    } else {
+                        val[i] = __ldg(a.cin + x);
+                    }
                 } else {
                     val[i] = idx[i] >= 0 ? __ldg(a.cin + idx[i]) : 0.0;
                 }
@@ -369,6 +386,28 @@ __global__ void __launch_bounds__(kHotBlock, 1) k_pr_units_hot(PrArgs a, const d
     for (int i = threadIdx.x; i < (H + 1) / 2; i += blockDim.x) dst[i] = __ldcg(src + i);
     __syncthreads();
     pr_units_body<kEnc>(a, bitmaps + (threadIdx.x >> 5) * (kCh / 32), hot_smem);
+}
+
+// Cluster variant (hot sets beyond one CTA's shared memory, SP_PR_HOT_MAX):
+// CTA pairs, each holding half of the H hot contribs; a gather whose hot
+// index lies in the peer's half reads it through distributed shared memory.
+// The pair synchronises after the refill (the peer's half is complete) and
+// before exiting (its shared memory stays readable until the peer is done).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kHotBlock, 1)
+    k_pr_units_hot2(PrArgs a, const double *hotc, int H) {
+    pr_bind(a);
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double hot_smem[];
+    const int Hl = ((H + 1) / 2 + 1) & ~1;  // even: int4 refills
+    const int my = (int)cl.block_rank();
+    uint32_t *bitmaps = reinterpret_cast<uint32_t *>(hot_smem + Hl);
+    const int lo = my * Hl, cnt = min(Hl, H - lo);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) hot_smem[i] = __ldcg(hotc + lo + i);
+    cl.sync();
+    const double *peer = cl.map_shared_rank(hot_smem, my ^ 1);
+    pr_units_body<kEnc2>(a, bitmaps + (threadIdx.x >> 5) * (kCh / 32), hot_smem, Hl, peer, my);
+    cl.sync();
 }
 
 // Relabelled layout: the hot contribs are cin[0, H) -- one contiguous copy
@@ -522,6 +561,17 @@ __global__ void k_hot_encode(const int32_t *__restrict__ radj, int64_t m,
     }
 }
 
+// Hot-set size: kHotMax (one CTA's shared memory); SP_PR_HOT_MAX up to
+// 2 x kHotMax splits the set over a CTA pair (k_pr_units_hot2).
+static int hot_max() {
+    static const int h = [] {
+        const char *e = getenv("SP_PR_HOT_MAX");
+        const int v = e ? atoi(e) : kHotMax;
+        return std::max(2, std::min(2 * kHotMax - 4, v)) & ~1;
+    }();
+    return h;
+}
+
 // Hot-set selection: the H sources of largest out-degree, if they cover at
 // least kHotMinCover of the slots.  On success g->pr_hot_ids is set (H
 // resident ids), *hot_idx (call scratch, n entries: hot index or -1) and *H_out
@@ -536,9 +586,9 @@ int pr_hot_select(sp_graph *g, Call &c, const int32_t *outdeg, int64_t max_outde
     // free upper bound on the coverage: H sources of at most max_outdeg
     // slots each (a grid decides here, without the sort)
     if (m < kHotMinSlots || n >= kHotBit ||
-        (double)std::min<int64_t>(kHotMax, n) * (double)max_outdeg < min_cover * (double)m)
+        (double)std::min<int64_t>(hot_max(), n) * (double)max_outdeg < min_cover * (double)m)
         return SP_OK;
-    const int H = (int)std::min<int64_t>(kHotMax, n);
+    const int H = (int)std::min<int64_t>(hot_max(), n);
     uint32_t *key, *key_s;
     int32_t *id, *id_s, *hot_idx;
     SP_TRY(c.alloc(&key, n));
@@ -611,7 +661,7 @@ static int hot_build_locked(sp_graph *g, Call &c, bool now) {
     const char *ce = getenv("SP_PR_HOT_COVER");
     const double min_cover = ce ? atof(ce) : kHotMinCover;
     if (g->m < kHotMinSlots || g->n >= kHotBit ||
-        (double)std::min<int64_t>(kHotMax, g->n) * (double)g->max_outdeg <
+        (double)std::min<int64_t>(hot_max(), g->n) * (double)g->max_outdeg <
             min_cover * (double)g->m) {
         g->pr_H = 0;
         return SP_OK;
@@ -1037,10 +1087,20 @@ int plan_fast(sp_graph *g, Call &c, int64_t v0, int64_t v1, double damping, Fast
         } else {
             p.hotc = hotc_ext;
         }
-        p.hot_smem = (size_t)p.H * sizeof(double) + (kHotBlock / 32) * (kCh / 32) * 4;
-        SP_CUDA(cudaFuncSetAttribute(k_pr_units_hot, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)p.hot_smem));
-        p.grid_hot = num_sms(c.device);
+        if (p.H > kHotMax) {  // split over a CTA pair
+            const int Hl = ((p.H + 1) / 2 + 1) & ~1;
+            p.hot_smem = (size_t)Hl * sizeof(double) + (kHotBlock / 32) * (kCh / 32) * 4;
+            SP_CUDA(cudaFuncSetAttribute(k_pr_units_hot2,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)p.hot_smem));
+            p.grid_hot = num_sms(c.device) & ~1;
+        } else {
+            p.hot_smem = (size_t)p.H * sizeof(double) + (kHotBlock / 32) * (kCh / 32) * 4;
+            SP_CUDA(cudaFuncSetAttribute(k_pr_units_hot,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)p.hot_smem));
+            p.grid_hot = num_sms(c.device);
+        }
     }
     p.grid_epi = (int)std::max<int64_t>(1, (a.K1 - a.K0 + 256 * kEpi - 1) / (256 * kEpi));
     p.grid_zero = (int)std::max<int64_t>(1, (v1 - v0 + 255) / 256);
@@ -1080,8 +1140,12 @@ void launch_units(Call &c, const FastPlan &p, const PrArgs &a) {
     } else if (p.H > 0) {
         launch_pdl(k_pr_hot_gather, grid_for(p.H, 256, c.device), 256, 0, c.stream, a, p.hot_ids,
                    p.H, p.hotc);
-        launch_pdl(k_pr_units_hot, p.grid_hot, kHotBlock, p.hot_smem, c.stream, a,
-                   (const double *)p.hotc, p.H);
+        if (p.H > kHotMax)
+            launch_pdl(k_pr_units_hot2, p.grid_hot, kHotBlock, p.hot_smem, c.stream, a,
+                       (const double *)p.hotc, p.H);
+        else
+            launch_pdl(k_pr_units_hot, p.grid_hot, kHotBlock, p.hot_smem, c.stream, a,
+                       (const double *)p.hotc, p.H);
         c.launches += 2;
     } else {
         launch_pdl(k_pr_units, p.grid_units, kBlock, 0, c.stream, a);

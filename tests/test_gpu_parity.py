@@ -901,3 +901,38 @@ def test_preprocessing_times_reported():
     d, _ = _pair("rmat", 12, 16, 5, False)
     sp.run(corpus.SSSP_PULL, d, {"src": 0})
     assert d.preprocessing_ms().get("rweff", 0) > 0
+
+
+def test_pagerank_cluster_hot_set_subprocess():
+    """The 2-CTA cluster hot set (k_pr_units_hot2: half of a 40 K-source hot
+    set per CTA, the other half read through distributed shared memory;
+    SP_PR_HOT_MAX is read once per process, so this runs in a child
+    process): ranks within 1e-12 of the oracle and its iteration count on
+    RMAT-20, whose top 40 K sources qualify."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2305_03317_b200 as sp
+from paper_2305_03317_b200 import corpus, gen
+from oracle import cpu_ref
+u, v, w, n = gen.rmat(20, 16, seed=7)
+g = sp.from_arrays(u, v, w, directed=True, n=n)
+o = cpu_ref.build_csr(u, v, w, True, n)
+args = {"damping": 0.85, "epsilon": 1e-6, "maxIter": 100}
+for _ in range(3):  # the hot set is built on the graph's second fast call
+    r = sp.run(corpus.PR, g, args)
+rank, it, diff, its, rc = cpu_ref.pagerank(o, 0.85, 1e-6, 100)
+assert r.env.scalars["iter"] == it, (r.env.scalars["iter"], it)
+np.testing.assert_allclose(r.env.node_props["rank"], rank, rtol=1e-12, atol=0)
+print("ok", r.stats["kernel_launches"])
+'''
+    env = dict(os.environ, SP_PR_HOT_MAX="40960", SP_PR_REL="0", SP_PR_HOT_VERBOSE="1")
+    p = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert p.stdout.startswith("ok")
+    assert "top 4095" in p.stderr  # the split (> 20 K) hot set was built
