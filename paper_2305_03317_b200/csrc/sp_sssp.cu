@@ -531,7 +531,10 @@ constexpr int kAsyncBlock = 1024;  // launch bound; the launch uses kAsyncThread
 constexpr int kAsyncThreads = 256;
 constexpr unsigned kAsyncBackoff = 256;
 constexpr int kTailStride = 16;    // one 128-byte line per ring tail
-constexpr int kOwnShift = 6;       // 64 consecutive vertices per ring chunk
+#ifndef SP_NF_OWN_SHIFT
+#define SP_NF_OWN_SHIFT 6
+#endif
+constexpr int kOwnShift = SP_NF_OWN_SHIFT;  // 2^6 consecutive vertices per ring chunk (cfg5a: 4 / 6 / 8 / 10 / 12 -> 39.5 / 39.6 / 42.0 / 46.0 / 39.8 ms)
 constexpr int kEllMaxDeg = 8;      // ELL rows for graphs with max out-degree <= 8
 constexpr long long kAsyncWatchdog = 1ll << 35;  // cycles (~17 s): a hang becomes a fallback
 
@@ -1575,8 +1578,6 @@ __global__ void k_do_convert(DoLoop *D) {
             }
         }
     }
-    // counters of the new current iteration start clean (chunks was borrowed)
-    if (blockIdx.x == 0 && threadIdx.x == 0 && conv == 2) {}
 }
 
 __global__ void k_do_mode(DoLoop *D) {
