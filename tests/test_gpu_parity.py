@@ -573,10 +573,14 @@ TC_FORMS = [{"SP_TC_WARP_MAX": "16", "SP_TC_HUB": "0"},
             {"SP_TC_WARP_MAX": "16", "SP_TC_HASH_MAX": "32", "SP_TC_BIG_MAX": "64",
              "SP_TC_HUB": "0"},
             {"SP_TC_WARP_MAX": "16"},
-            {"SP_TC_WARP_MAX": "16", "SP_TC_HUB": "2"}]
+            {"SP_TC_WARP_MAX": "16", "SP_TC_HUB": "2"},
+            # every hub-rank row to k_tc_big / none of them
+            {"SP_TC_WARP_MAX": "16", "SP_TC_HUB_MIN": "0"},
+            {"SP_TC_HUB_MIN": "1000000"}]
 
 
-@pytest.mark.parametrize("form", TC_FORMS, ids=["hashed", "staged", "global", "hub", "hub16"])
+@pytest.mark.parametrize("form", TC_FORMS, ids=["hashed", "staged", "global", "hub", "hub16",
+                                                "hub_all", "hub_none"])
 @pytest.mark.parametrize("graph", ["dense_dup", "rmat_sym"])
 def test_tc_big_row_forms(graph, form, monkeypatch):
     """k_tc_big's three row forms -- shared hash table, staged A with a
