@@ -19,6 +19,12 @@
 //     appended to the next frontier with one atomic per warp;
 //   * the frontier size is the convergence flag (finished = size == 0):
 //     one 8-byte device->host read per iteration (K5/K6 in SURVEY 2.2).
+// The Bellman-Ford device loop (CUDA-graph WHILE node) keeps dist and the
+// enqueue stamp in one 64-bit word per vertex instead (RelaxPackedOp): one
+// atomicMin relaxes and, through the old word, dedupes the next frontier.
+// Large graphs run the direction-optimising loop (push steps + edge-
+// balanced pull sweeps), thin non-negative graphs the asynchronous
+// near-far kernel (per-block ring queues, no barrier per hop).
 // Candidates >= INT_MAX never win (interp.py:11-14).
 #include <cooperative_groups.h>
 
