@@ -493,6 +493,17 @@ def other_algorithms(sp, corpus, parallel, be, a, hbm_peak, world, dev):
                                     "B/slot + 64 B/vertex per source) -- the 8-source batches "
                                     "share one level read across sources, so it can exceed 1; "
                                     "dram_frac: the batched run's measured DRAM bytes")
+        if st.get("model_bytes"):
+            # the batched algorithm's own byte model: an 8-source batch reads
+            # each reached slot's / vertex's state once for all its lanes, and
+            # every source here reaches the same giant component, so the
+            # batch reads what one source's traversal reads: model / 8
+            bmb = st["model_bytes"] / 8
+            out["bc_cfg4"]["roofline_batched"] = {
+                "model_bytes": bmb, "achieved": bmb / (ms / 1e3) / 1e9, "unit": "GB/s",
+                "peak": hbm_peak, "frac": bmb / (ms / 1e3) / 1e9 / hbm_peak,
+                "note": "per-source SURVEY 8d model / 8 (8-source batches share every "
+                        "level read); compare with dram_frac"}
         g.close()
     if "tc" in a.algos:
         g = sp.generate("uniform", 1 << 24, 1 << 28, seed=SEED, undirected=True,
