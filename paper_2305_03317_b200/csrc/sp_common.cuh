@@ -202,6 +202,11 @@ struct sp_graph {
     // from v alone, without the dependent offsets load (asynchronous SSSP)
     int2 *ell = nullptr;
     int ell_d = 0;
+    // max out-degree <= 4: each row's 1-hop and 2-hop targets (min summed
+    // w_eff per target, v itself dropped), kEll2 slots per row -- shortcut
+    // relaxations that halve the hop chain of the asynchronous SSSP kernel
+    // (the fixpoint is unchanged: every shortcut weight is a real path length)
+    int2 *ell2 = nullptr;
     int32_t *rel_perm = nullptr, *rel_radj = nullptr, *rel_outdeg = nullptr,
             *rel_indeg = nullptr, *rel_nzrow = nullptr;
     int64_t *rel_nzend = nullptr, *rel_unit_row = nullptr;
@@ -237,6 +242,9 @@ void prep_mark(sp_graph *g, int kind, int end, cudaStream_t s);
 int ensure_rweff(sp_graph *g, Call &c);
 // The ELL form above (built once when max out-degree <= d_max; else no-op).
 int ensure_ell(sp_graph *g, Call &c, int d_max);
+constexpr int kEll2 = 16;
+// The 2-hop form above (built once from the ELL rows when ell_d <= 4).
+int ensure_ell2(sp_graph *g, Call &c);
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 

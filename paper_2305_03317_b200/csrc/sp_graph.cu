@@ -357,6 +357,7 @@ void free_graph(sp_graph *g) {
     resident_free(g->weff);
     if (g->directed) resident_free(g->rweff);
     resident_free(g->ell);
+    resident_free(g->ell2);
     resident_free(g->outdeg);
     if (g->directed) {
         resident_free(g->roff);
@@ -871,6 +872,63 @@ __global__ void k_ell_fill(const int64_t *__restrict__ off, const int32_t *__res
         const int64_t e = off[v] + k;
         ell[i] = e < off[v + 1] ? make_int2(adj[e], weff[e]) : make_int2(-1, 0);
     }
+}
+
+__global__ void k_ell2_fill(const int2 *__restrict__ ell, int d, int64_t n, int2 *ell2) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        int2 out[kEll2];
+        int cnt = 0;
+        auto put = [&](int32_t y, int64_t w) {
+            if (y < 0 || y == (int32_t)v || w > 0x7fffffffll) return;
+            for (int k = 0; k < cnt; k++)
+                if (out[k].x == y) {
+                    if (w < out[k].y) out[k].y = (int)w;
+                    return;
+                }
+            if (cnt < kEll2) out[cnt++] = make_int2(y, (int)w);
+        };
+        for (int i = 0; i < d; i++) {
+            const int2 e = ell[v * d + i];
+            put(e.x, e.y);
+        }
+        for (int i = 0; i < d; i++) {
+            const int2 e = ell[v * d + i];
+            if (e.x < 0) continue;
+            for (int j = 0; j < d; j++) {
+                const int2 f = ell[(int64_t)e.x * d + j];
+                if (f.x >= 0) put(f.x, (int64_t)e.y + (int64_t)f.y);
+            }
+        }
+        for (int k = 0; k < kEll2; k++) ell2[v * kEll2 + k] = k < cnt ? out[k] : make_int2(-1, 0);
+    }
+}
+
+int ensure_ell2(sp_graph *g, Call &c) {
+    std::lock_guard<std::mutex> lk(g_lazy_mu);
+    if (g->ell2 || !g->ell || g->ell_d > 4 || g->n == 0) return SP_OK;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return SP_OK;
+    }
+    if ((double)g->n * kEll2 * sizeof(int2) > 0.25 * (double)fr) return SP_OK;  // optional
+    int2 *e2 = nullptr;
+    if (dalloc(&e2, g->n * kEll2) != SP_OK) {
+        cudaGetLastError();
+        return SP_OK;
+    }
+    prep_mark(g, kPrepEll, 0, c.stream);
+    k_ell2_fill<<<gridN(g->n, c.device), 256, 0, c.stream>>>(g->ell, g->ell_d, g->n, e2);
+    prep_mark(g, kPrepEll, 1, c.stream);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+    if (e != cudaSuccess) {
+        resident_free(e2);
+        SP_CUDA(e);
+    }
+    g->ell2 = e2;
+    return SP_OK;
 }
 
 int ensure_ell(sp_graph *g, Call &c, int d_max) {

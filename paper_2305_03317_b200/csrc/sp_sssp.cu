@@ -598,12 +598,28 @@ __device__ __forceinline__ void async_push_far(AsyncNf *A, int fc, bool far, int
     if (far && pos < A->fcap) A->far[fc][pos] = x;  // far_n still counts an overflow
 }
 
+// Push a warp's shared list of near winners (nn entries) to their owners'
+// rings, 32 at a time (one tail atomic per owner group per 32); `work`
+// already counts them (tok: the batch's raise).  Returns nn.
+constexpr int kNearList = 128;
+__device__ __forceinline__ int async_push_list(AsyncNf *A, const int32_t *nl, int nn,
+                                               unsigned lane, unsigned long long tok) {
+    __syncwarp();
+    for (int b = 0; b < nn; b += 32) {
+        const bool has = b + (int)lane < nn;
+        const int32_t x = has ? nl[b + lane] : -1;
+        async_push_near(A, has, x, lane, true, tok);
+    }
+    __syncwarp();
+    return nn;
+}
+
 // kD > 0: bounded-degree graphs in the ELL form (g->ell, kD slots per row):
 // a lane loads its vertex's whole row (one or two 16-byte loads) from v
 // alone, in parallel with the dequeue atomic -- no dependent offsets load
 // on the hop chain.  kD == 0: CSR rows, flattened over the warp.
 template <int kD>
-__global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
+__global__ void __launch_bounds__(kD == kEll2 ? kAsyncThreads : kAsyncBlock) k_nf_async(
     unsigned long long *dq, int32_t *last, const int32_t *__restrict__ weff,
     const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const int2 *__restrict__ ell, AsyncNf *A, unsigned async_max_backoff) {
@@ -654,7 +670,90 @@ __global__ void __launch_bounds__(kAsyncBlock) k_nf_async(
             batches++;
             int32_t v = (int)lane < k ? sv : -1;
             if (v >= 0) myring[h + lane] = -1;  // the slot is reused next phase
-            if constexpr (kD > 0) {
+            if constexpr (kD == kEll2) {
+                // 2-hop rows (shortcuts): up to 16 rounds of 32 slots, so the
+                // rounds' atomicMins are all issued before any push, and the
+                // near winners of every round are pushed together from a
+                // per-warp shared list -- one tail round trip per batch
+                // instead of one per round
+                __shared__ int32_t s_near[kAsyncThreads / 32][kNearList];
+                int32_t *nl = s_near[threadIdx.x >> 5];
+                const int nslot = k * kEll2;
+                const int nrounds = (nslot + 31) >> 5;
+                unsigned long long tok = 0;
+                if (lane == 0)  // the batch's slot bound, raised while the rows load
+                    tok = atomicAdd(reinterpret_cast<unsigned long long *>(&A->work),
+                                    (unsigned long long)nslot);
+                // the rows' slots need only the popped ids: all rounds' loads
+                // are issued before the dequeue atomics, which they overlap
+                int2 s[kEll2];
+                unsigned long long old[kEll2];
+                int64_t cand[kEll2];
+#pragma unroll
+                for (int r = 0; r < kEll2; r++) {
+                    s[r] = make_int2(-1, 0);
+                    if (r >= nrounds) continue;  // warp-uniform
+                    const int pp = r * 32 + (int)lane;
+                    const int32_t vj = __shfl_sync(0xffffffffu, v, (pp >> 4) & 31);
+                    if (pp < nslot && vj >= 0) s[r] = __ldg(ell + (size_t)vj * kEll2 + (pp & 15));
+                }
+                int dv = 0;
+                bool act = false;
+                if (v >= 0) {
+                    const int lst = __ldcg(last + v);
+                    dv = (int)(atomicAnd(dq + v, ~1ull) >> 1);
+                    act = dv < lst;
+                    if (act) {
+                        last[v] = dv;
+                        expanded++;
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < kEll2; r++) {
+                    old[r] = ~0ull;
+                    cand[r] = kIntMax;
+                    if (r >= nrounds) continue;  // warp-uniform
+                    const int vl = ((r * 32 + (int)lane) >> 4) & 31;
+                    const int du = __shfl_sync(0xffffffffu, dv, vl);
+                    const bool aj = __shfl_sync(0xffffffffu, act, vl);
+                    if (!aj) s[r].x = -1;
+                    const bool live = s[r].x >= 0;
+                    const unsigned rm = __ballot_sync(0xffffffffu, live);
+                    if (lane == 0) relaxed += __popc(rm);
+                    if (live) {
+                        cand[r] = (int64_t)du + (int64_t)s[r].y;
+                        if (cand[r] < (int64_t)kIntMax)
+                            old[r] = atomicMin(dq + s[r].x, ((unsigned long long)cand[r] << 1) |
+                                                                (cand[r] < T ? 1ull : 0ull));
+                    }
+                }
+                int nn = 0;  // near winners collected in nl
+                long long pushed = 0;
+#pragma unroll
+                for (int r = 0; r < kEll2; r++) {
+                    if (r >= nrounds) break;
+                    const bool fin = s[r].x >= 0 && cand[r] < (int64_t)kIntMax;
+                    const bool won = fin && (long long)(old[r] >> 1) > cand[r];
+                    const bool nb = cand[r] < T;
+                    const bool near = won && nb && (old[r] & 1ull) == 0;
+                    const unsigned m = __ballot_sync(0xffffffffu, near);
+                    if (m) {
+                        if (nn + __popc(m) > kNearList) {  // rare: flush the list
+                            pushed += async_push_list(A, nl, nn, lane, tok);
+                            nn = 0;
+                        }
+                        if (near) nl[nn + __popc(m & ((1u << lane) - 1u))] = s[r].x;
+                        nn += __popc(m);
+                    }
+                    async_push_far(A, fc, won && !nb, s[r].x, lane);
+                }
+                pushed += async_push_list(A, nl, nn, lane, tok);
+                __syncwarp();
+                if (lane == 0)
+                    atomicAdd(reinterpret_cast<unsigned long long *>(&A->work),
+                              (unsigned long long)(-(long long)(k + nslot - pushed)));
+                continue;
+            } else if constexpr (kD > 0) {
                 // slot p of the batch (vertex p / kD, its slot p % kD) goes
                 // to lane p % 32 in round p / 32: the slot loads need only
                 // the popped ids, so they are issued before the dequeue
@@ -886,6 +985,16 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t src, int64_
     // bounded-degree graphs: the ELL row form (SP_NF_ELL=0: CSR rows)
     const char *ee = getenv("SP_NF_ELL");
     if (!(ee && ee[0] == '0')) SP_TRY(ensure_ell(g, c, kEllMaxDeg));
+    // 2-hop shortcut rows on graphs of out-degree <= 4 (SP_NF_SHORTCUT=0: off)
+    const char *se = getenv("SP_NF_SHORTCUT");
+    const bool shortcut = !(ee && ee[0] == '0') && !(se && se[0] == '0') && g->ell &&
+                          g->ell_d <= 4;
+    if (shortcut) SP_TRY(ensure_ell2(g, c));
+    const bool use2 = shortcut && g->ell2 && threads <= kAsyncThreads;  // its launch bound
+    // a shortcut row covers two hops: a phase may span twice the distance
+    // band (cfg5a, delta 816 / 1632 / 2400 / 3200: 34.3 / 31.2 / 31.4 /
+    // 32.1 ms; 1-hop rows: 39.5 ms at 816, 39.0 at 1632)
+    if (use2 && !getenv("SP_SSSP_DELTA")) delta *= 2;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nf_async<0>, threads, 0);
     const char *bps = getenv("SP_NF_ASYNC_BPS");  // blocks per SM (sweeps)
@@ -932,10 +1041,11 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t src, int64_
     init.T = delta;
     init.delta = delta;
     SP_CUDA(cudaMemcpyAsync(A, &init, sizeof(AsyncNf), cudaMemcpyHostToDevice, c.stream));
-    const int2 *ell = g->ell;
+    const int2 *ell = use2 ? g->ell2 : g->ell;
     void *kargs[] = {&dq, &last, (void *)&g->weff, (void *)&g->off, (void *)&g->adj, (void *)&ell,
                      &A, &max_backoff};
-    const void *kfn = g->ell_d == 2   ? (const void *)k_nf_async<2>
+    const void *kfn = use2            ? (const void *)k_nf_async<kEll2>
+                      : g->ell_d == 2 ? (const void *)k_nf_async<2>
                       : g->ell_d == 4 ? (const void *)k_nf_async<4>
                       : g->ell_d == 8 ? (const void *)k_nf_async<8>
                                       : (const void *)k_nf_async<0>;

@@ -211,8 +211,9 @@ def test_sssp_async_near_far_stress(kind, p0, p1, und, delta, monkeypatch):
     caller cap): per-block rings, in-queue flags, phase splits -- racy by
     design, so every graph runs several times, with small and large delta
     (many / few phases; "0" = Bellman-Ford, the reference form), against
-    the oracle's dist bit for bit; the synchronous near-far kernel
-    (SP_NF_ASYNC=0) gives the same dist."""
+    the oracle's dist bit for bit; the 1-hop row form (SP_NF_SHORTCUT=0; the
+    default relaxes 2-hop shortcut rows on out-degree <= 4 graphs) and the
+    synchronous near-far kernel (SP_NF_ASYNC=0) give the same dist."""
     if delta is not None:
         monkeypatch.setenv("SP_SSSP_DELTA", delta)
     g, o = _pair(kind, p0, p1, 23, und)
@@ -222,6 +223,11 @@ def test_sssp_async_near_far_stress(kind, p0, p1, und, delta, monkeypatch):
         for rep in range(4):
             r = sp.run(corpus.SSSP, g, {"src": s})
             np.testing.assert_array_equal(r.env.node_props["dist"], dist, err_msg=f"rep {rep}")
+    monkeypatch.setenv("SP_NF_SHORTCUT", "0")  # 1-hop ELL rows (default: 2-hop shortcut rows)
+    for rep in range(2):
+        r = sp.run(corpus.SSSP, g, {"src": 0})
+        np.testing.assert_array_equal(r.env.node_props["dist"], cpu_ref.sssp(o, 0)[0])
+    monkeypatch.delenv("SP_NF_SHORTCUT")
     monkeypatch.setenv("SP_NF_ASYNC_RING", "64")  # rings overflow: the synchronous fallback
     r = sp.run(corpus.SSSP, g, {"src": 0})
     np.testing.assert_array_equal(r.env.node_props["dist"], cpu_ref.sssp(o, 0)[0])
