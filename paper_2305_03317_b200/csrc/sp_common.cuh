@@ -207,6 +207,7 @@ struct sp_graph {
     // relaxations that halve the hop chain of the asynchronous SSSP kernel
     // (the fixpoint is unchanged: every shortcut weight is a real path length)
     int2 *ell2 = nullptr;
+    int ell2_slots = 0;  // kEll2 or kEll3
     int32_t *rel_perm = nullptr, *rel_radj = nullptr, *rel_outdeg = nullptr,
             *rel_indeg = nullptr, *rel_nzrow = nullptr;
     int64_t *rel_nzend = nullptr, *rel_unit_row = nullptr;
@@ -242,9 +243,11 @@ void prep_mark(sp_graph *g, int kind, int end, cudaStream_t s);
 int ensure_rweff(sp_graph *g, Call &c);
 // The ELL form above (built once when max out-degree <= d_max; else no-op).
 int ensure_ell(sp_graph *g, Call &c, int d_max);
-constexpr int kEll2 = 16;
-// The 2-hop form above (built once from the ELL rows when ell_d <= 4).
-int ensure_ell2(sp_graph *g, Call &c);
+constexpr int kEll2 = 16, kEll3 = 32;
+// The shortcut form above (built once from the ELL rows when ell_d <= 4):
+// hops = 2 -> kEll2 slots, hops = 3 -> kEll3 slots (1-, 2-, then 3-hop
+// targets while they fit; dropping a shortcut never changes the fixpoint).
+int ensure_ell2(sp_graph *g, Call &c, int hops);
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 

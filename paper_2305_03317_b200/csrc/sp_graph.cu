@@ -874,10 +874,11 @@ __global__ void k_ell_fill(const int64_t *__restrict__ off, const int32_t *__res
     }
 }
 
-__global__ void k_ell2_fill(const int2 *__restrict__ ell, int d, int64_t n, int2 *ell2) {
+template <int S>
+__global__ void k_ell2_fill(const int2 *__restrict__ ell, int d, int64_t n, int hops, int2 *ell2) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
-        int2 out[kEll2];
+        int2 out[S];
         int cnt = 0;
         auto put = [&](int32_t y, int64_t w) {
             if (y < 0 || y == (int32_t)v || w > 0x7fffffffll) return;
@@ -886,40 +887,51 @@ __global__ void k_ell2_fill(const int2 *__restrict__ ell, int d, int64_t n, int2
                     if (w < out[k].y) out[k].y = (int)w;
                     return;
                 }
-            if (cnt < kEll2) out[cnt++] = make_int2(y, (int)w);
+            if (cnt < S) out[cnt++] = make_int2(y, (int)w);
         };
         for (int i = 0; i < d; i++) {
             const int2 e = ell[v * d + i];
             put(e.x, e.y);
         }
-        for (int i = 0; i < d; i++) {
-            const int2 e = ell[v * d + i];
-            if (e.x < 0) continue;
-            for (int j = 0; j < d; j++) {
-                const int2 f = ell[(int64_t)e.x * d + j];
-                if (f.x >= 0) put(f.x, (int64_t)e.y + (int64_t)f.y);
+        // one more hop from every entry so far, `hops - 1` times (the 1-hop
+        // entries come first, so they are never crowded out)
+        int lo = 0;
+        for (int h = 1; h < hops; h++) {
+            const int hi = cnt;
+            for (int k = lo; k < hi; k++) {
+                const int32_t x = out[k].x;
+                const int64_t wx = out[k].y;
+                for (int j = 0; j < d; j++) {
+                    const int2 f = ell[(int64_t)x * d + j];
+                    if (f.x >= 0) put(f.x, wx + (int64_t)f.y);
+                }
             }
+            lo = hi;
         }
-        for (int k = 0; k < kEll2; k++) ell2[v * kEll2 + k] = k < cnt ? out[k] : make_int2(-1, 0);
+        for (int k = 0; k < S; k++) ell2[v * S + k] = k < cnt ? out[k] : make_int2(-1, 0);
     }
 }
 
-int ensure_ell2(sp_graph *g, Call &c) {
+int ensure_ell2(sp_graph *g, Call &c, int hops) {
     std::lock_guard<std::mutex> lk(g_lazy_mu);
     if (g->ell2 || !g->ell || g->ell_d > 4 || g->n == 0) return SP_OK;
+    const int S = hops >= 3 ? kEll3 : kEll2;
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
         cudaGetLastError();
         return SP_OK;
     }
-    if ((double)g->n * kEll2 * sizeof(int2) > 0.25 * (double)fr) return SP_OK;  // optional
+    if ((double)g->n * S * sizeof(int2) > 0.25 * (double)fr) return SP_OK;  // optional
     int2 *e2 = nullptr;
-    if (dalloc(&e2, g->n * kEll2) != SP_OK) {
+    if (dalloc(&e2, g->n * S) != SP_OK) {
         cudaGetLastError();
         return SP_OK;
     }
     prep_mark(g, kPrepEll, 0, c.stream);
-    k_ell2_fill<<<gridN(g->n, c.device), 256, 0, c.stream>>>(g->ell, g->ell_d, g->n, e2);
+    if (S == kEll3)
+        k_ell2_fill<kEll3><<<gridN(g->n, c.device), 256, 0, c.stream>>>(g->ell, g->ell_d, g->n, 3, e2);
+    else
+        k_ell2_fill<kEll2><<<gridN(g->n, c.device), 256, 0, c.stream>>>(g->ell, g->ell_d, g->n, 2, e2);
     prep_mark(g, kPrepEll, 1, c.stream);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
@@ -928,6 +940,7 @@ int ensure_ell2(sp_graph *g, Call &c) {
         SP_CUDA(e);
     }
     g->ell2 = e2;
+    g->ell2_slots = S;
     return SP_OK;
 }
 

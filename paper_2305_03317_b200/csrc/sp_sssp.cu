@@ -618,8 +618,11 @@ __device__ __forceinline__ int async_push_list(AsyncNf *A, const int32_t *nl, in
 // a lane loads its vertex's whole row (one or two 16-byte loads) from v
 // alone, in parallel with the dequeue atomic -- no dependent offsets load
 // on the hop chain.  kD == 0: CSR rows, flattened over the warp.
+// shortcut rows keep their slots and atomic results in registers: a lower
+// thread bound (2-hop: 512 -> <= 128 registers; 3-hop: 256)
+constexpr int async_bound(int kD) { return kD == kEll3 ? 256 : kD == kEll2 ? 512 : kAsyncBlock; }
 template <int kD>
-__global__ void __launch_bounds__(kD == kEll2 ? kAsyncThreads : kAsyncBlock) k_nf_async(
+__global__ void __launch_bounds__(async_bound(kD)) k_nf_async(
     unsigned long long *dq, int32_t *last, const int32_t *__restrict__ weff,
     const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
     const int2 *__restrict__ ell, AsyncNf *A, unsigned async_max_backoff) {
@@ -670,15 +673,16 @@ __global__ void __launch_bounds__(kD == kEll2 ? kAsyncThreads : kAsyncBlock) k_n
             batches++;
             int32_t v = (int)lane < k ? sv : -1;
             if (v >= 0) myring[h + lane] = -1;  // the slot is reused next phase
-            if constexpr (kD == kEll2) {
+            if constexpr (kD >= kEll2) {
                 // 2-hop rows (shortcuts): up to 16 rounds of 32 slots, so the
                 // rounds' atomicMins are all issued before any push, and the
                 // near winners of every round are pushed together from a
                 // per-warp shared list -- one tail round trip per batch
                 // instead of one per round
-                __shared__ int32_t s_near[kAsyncThreads / 32][kNearList];
+                constexpr int kLogD = kD == kEll2 ? 4 : 5;
+                __shared__ int32_t s_near[async_bound(kD) / 32][kNearList];
                 int32_t *nl = s_near[threadIdx.x >> 5];
-                const int nslot = k * kEll2;
+                const int nslot = k * kD;
                 const int nrounds = (nslot + 31) >> 5;
                 unsigned long long tok = 0;
                 if (lane == 0)  // the batch's slot bound, raised while the rows load
@@ -686,16 +690,15 @@ __global__ void __launch_bounds__(kD == kEll2 ? kAsyncThreads : kAsyncBlock) k_n
                                     (unsigned long long)nslot);
                 // the rows' slots need only the popped ids: all rounds' loads
                 // are issued before the dequeue atomics, which they overlap
-                int2 s[kEll2];
-                unsigned long long old[kEll2];
-                int64_t cand[kEll2];
+                int2 s[kD];
+                unsigned long long old[kD];
 #pragma unroll
-                for (int r = 0; r < kEll2; r++) {
+                for (int r = 0; r < kD; r++) {
                     s[r] = make_int2(-1, 0);
                     if (r >= nrounds) continue;  // warp-uniform
                     const int pp = r * 32 + (int)lane;
-                    const int32_t vj = __shfl_sync(0xffffffffu, v, (pp >> 4) & 31);
-                    if (pp < nslot && vj >= 0) s[r] = __ldg(ell + (size_t)vj * kEll2 + (pp & 15));
+                    const int32_t vj = __shfl_sync(0xffffffffu, v, (pp >> kLogD) & 31);
+                    if (pp < nslot && vj >= 0) s[r] = __ldg(ell + (size_t)vj * kD + (pp & (kD - 1)));
                 }
                 int dv = 0;
                 bool act = false;
@@ -709,11 +712,10 @@ __global__ void __launch_bounds__(kD == kEll2 ? kAsyncThreads : kAsyncBlock) k_n
                     }
                 }
 #pragma unroll
-                for (int r = 0; r < kEll2; r++) {
+                for (int r = 0; r < kD; r++) {
                     old[r] = ~0ull;
-                    cand[r] = kIntMax;
                     if (r >= nrounds) continue;  // warp-uniform
-                    const int vl = ((r * 32 + (int)lane) >> 4) & 31;
+                    const int vl = ((r * 32 + (int)lane) >> kLogD) & 31;
                     const int du = __shfl_sync(0xffffffffu, dv, vl);
                     const bool aj = __shfl_sync(0xffffffffu, act, vl);
                     if (!aj) s[r].x = -1;
@@ -721,20 +723,24 @@ __global__ void __launch_bounds__(kD == kEll2 ? kAsyncThreads : kAsyncBlock) k_n
                     const unsigned rm = __ballot_sync(0xffffffffu, live);
                     if (lane == 0) relaxed += __popc(rm);
                     if (live) {
-                        cand[r] = (int64_t)du + (int64_t)s[r].y;
-                        if (cand[r] < (int64_t)kIntMax)
-                            old[r] = atomicMin(dq + s[r].x, ((unsigned long long)cand[r] << 1) |
-                                                                (cand[r] < T ? 1ull : 0ull));
+                        const int64_t cd = (int64_t)du + (int64_t)s[r].y;
+                        if (cd < (int64_t)kIntMax)
+                            old[r] = atomicMin(dq + s[r].x, ((unsigned long long)cd << 1) |
+                                                                (cd < T ? 1ull : 0ull));
+                        else
+                            s[r].x = -1;  // never wins (F12)
                     }
                 }
                 int nn = 0;  // near winners collected in nl
                 long long pushed = 0;
 #pragma unroll
-                for (int r = 0; r < kEll2; r++) {
+                for (int r = 0; r < kD; r++) {
                     if (r >= nrounds) break;
-                    const bool fin = s[r].x >= 0 && cand[r] < (int64_t)kIntMax;
-                    const bool won = fin && (long long)(old[r] >> 1) > cand[r];
-                    const bool nb = cand[r] < T;
+                    const int vl = ((r * 32 + (int)lane) >> kLogD) & 31;
+                    const int64_t cd = (int64_t)__shfl_sync(0xffffffffu, dv, vl) + (int64_t)s[r].y;
+                    const bool fin = s[r].x >= 0;
+                    const bool won = fin && (long long)(old[r] >> 1) > cd;
+                    const bool nb = cd < T;
                     const bool near = won && nb && (old[r] & 1ull) == 0;
                     const unsigned m = __ballot_sync(0xffffffffu, near);
                     if (m) {
@@ -980,23 +986,35 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t src, int64_
     const int64_t n = g->n, m = g->m;
     const int sms = num_sms(c.device);
     const char *thr = getenv("SP_NF_ASYNC_THREADS");  // threads per block (sweeps)
-    const int threads = thr ? std::max(32, std::min(kAsyncBlock, atoi(thr) / 32 * 32))
-                            : kAsyncThreads;
+    int threads = thr ? std::max(32, std::min(kAsyncBlock, atoi(thr) / 32 * 32))
+                      : kAsyncThreads;
     // bounded-degree graphs: the ELL row form (SP_NF_ELL=0: CSR rows)
     const char *ee = getenv("SP_NF_ELL");
     if (!(ee && ee[0] == '0')) SP_TRY(ensure_ell(g, c, kEllMaxDeg));
     // 2-hop shortcut rows on graphs of out-degree <= 4 (SP_NF_SHORTCUT=0: off)
+    // (SP_NF_SHORTCUT=3: 1- to 3-hop rows of 32 slots)
     const char *se = getenv("SP_NF_SHORTCUT");
     const bool shortcut = !(ee && ee[0] == '0') && !(se && se[0] == '0') && g->ell &&
                           g->ell_d <= 4;
-    if (shortcut) SP_TRY(ensure_ell2(g, c));
-    const bool use2 = shortcut && g->ell2 && threads <= kAsyncThreads;  // its launch bound
+    const int hops = se && se[0] == '3' ? 3 : 2;
+    if (shortcut) SP_TRY(ensure_ell2(g, c, hops));
+    // 2-hop rows: 384 threads per block (cfg5a, 256 / 384 / 512: 32.0 /
+    // 30.7 / 33.2 ms; two blocks per SM 35 ms)
+    if (!thr && shortcut && g->ell2 && g->ell2_slots == kEll2) threads = 384;
+    const bool use2 = shortcut && g->ell2 &&
+                      threads <= (g->ell2_slots == kEll3 ? 256 : 512);  // its launch bound
     // a shortcut row covers two hops: a phase may span twice the distance
     // band (cfg5a, delta 816 / 1632 / 2400 / 3200: 34.3 / 31.2 / 31.4 /
     // 32.1 ms; 1-hop rows: 39.5 ms at 816, 39.0 at 1632)
-    if (use2 && !getenv("SP_SSSP_DELTA")) delta *= 2;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nf_async<0>, threads, 0);
+    if (use2 && !getenv("SP_SSSP_DELTA")) delta *= g->ell2_slots == kEll3 ? 3 : 2;
+    const void *kfn = use2 && g->ell2_slots == kEll3 ? (const void *)k_nf_async<kEll3>
+                      : use2          ? (const void *)k_nf_async<kEll2>
+                      : g->ell_d == 2 ? (const void *)k_nf_async<2>
+                      : g->ell_d == 4 ? (const void *)k_nf_async<4>
+                      : g->ell_d == 8 ? (const void *)k_nf_async<8>
+                                      : (const void *)k_nf_async<0>;
+    int per_sm = 0;  // co-residency of the cooperative launch: this kernel's own
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, 0);
     const char *bps = getenv("SP_NF_ASYNC_BPS");  // blocks per SM (sweeps)
     const int want = bps ? std::max(1, atoi(bps)) : kAsyncBlocksPerSm;
     const int nring = sms * std::max(1, std::min(per_sm, want));  // one ring per block
@@ -1044,11 +1062,6 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t src, int64_
     const int2 *ell = use2 ? g->ell2 : g->ell;
     void *kargs[] = {&dq, &last, (void *)&g->weff, (void *)&g->off, (void *)&g->adj, (void *)&ell,
                      &A, &max_backoff};
-    const void *kfn = use2            ? (const void *)k_nf_async<kEll2>
-                      : g->ell_d == 2 ? (const void *)k_nf_async<2>
-                      : g->ell_d == 4 ? (const void *)k_nf_async<4>
-                      : g->ell_d == 8 ? (const void *)k_nf_async<8>
-                                      : (const void *)k_nf_async<0>;
     cudaEvent_t ka, kb;
     SP_CUDA(cudaEventCreate(&ka));
     SP_CUDA(cudaEventCreate(&kb));
