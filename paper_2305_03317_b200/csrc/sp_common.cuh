@@ -203,7 +203,7 @@ struct sp_graph {
     int2 *ell = nullptr;
     int ell_d = 0;
     // max out-degree <= 4: each row's 1-hop and 2-hop targets (min summed
-    // w_eff per target, v itself dropped), kEll2 slots per row -- shortcut
+    // w_eff per target, v itself dropped; 1-hop first), kEll2 slots per row -- shortcut
     // relaxations that halve the hop chain of the asynchronous SSSP kernel
     // (the fixpoint is unchanged: every shortcut weight is a real path length)
     int2 *ell2 = nullptr;
@@ -243,7 +243,13 @@ void prep_mark(sp_graph *g, int kind, int end, cudaStream_t s);
 int ensure_rweff(sp_graph *g, Call &c);
 // The ELL form above (built once when max out-degree <= d_max; else no-op).
 int ensure_ell(sp_graph *g, Call &c, int d_max);
-constexpr int kEll2 = 16, kEll3 = 32;
+// 2-hop row slots: a 4-regular grid row has exactly 4 + 8 targets
+// (cfg5a: 12 slots 27.7 ms, 16 slots 30.7 ms -- fewer dead lanes and
+// rounds); rows with more distinct targets keep the first 12 (1-hop first)
+#ifndef SP_NF_ELL2_SLOTS
+#define SP_NF_ELL2_SLOTS 12
+#endif
+constexpr int kEll2 = SP_NF_ELL2_SLOTS, kEll3 = 32;
 // The shortcut form above (built once from the ELL rows when ell_d <= 4):
 // hops = 2 -> kEll2 slots, hops = 3 -> kEll3 slots (1-, 2-, then 3-hop
 // targets while they fit; dropping a shortcut never changes the fixpoint).

@@ -679,7 +679,6 @@ __global__ void __launch_bounds__(async_bound(kD)) k_nf_async(
                 // near winners of every round are pushed together from a
                 // per-warp shared list -- one tail round trip per batch
                 // instead of one per round
-                constexpr int kLogD = kD == kEll2 ? 4 : 5;
                 __shared__ int32_t s_near[async_bound(kD) / 32][kNearList];
                 int32_t *nl = s_near[threadIdx.x >> 5];
                 const int nslot = k * kD;
@@ -697,8 +696,8 @@ __global__ void __launch_bounds__(async_bound(kD)) k_nf_async(
                     s[r] = make_int2(-1, 0);
                     if (r >= nrounds) continue;  // warp-uniform
                     const int pp = r * 32 + (int)lane;
-                    const int32_t vj = __shfl_sync(0xffffffffu, v, (pp >> kLogD) & 31);
-                    if (pp < nslot && vj >= 0) s[r] = __ldg(ell + (size_t)vj * kD + (pp & (kD - 1)));
+                    const int32_t vj = __shfl_sync(0xffffffffu, v, (pp / kD) & 31);
+                    if (pp < nslot && vj >= 0) s[r] = __ldg(ell + (size_t)vj * kD + (pp % kD));
                 }
                 int dv = 0;
                 bool act = false;
@@ -715,7 +714,7 @@ __global__ void __launch_bounds__(async_bound(kD)) k_nf_async(
                 for (int r = 0; r < kD; r++) {
                     old[r] = ~0ull;
                     if (r >= nrounds) continue;  // warp-uniform
-                    const int vl = ((r * 32 + (int)lane) >> kLogD) & 31;
+                    const int vl = ((r * 32 + (int)lane) / kD) & 31;
                     const int du = __shfl_sync(0xffffffffu, dv, vl);
                     const bool aj = __shfl_sync(0xffffffffu, act, vl);
                     if (!aj) s[r].x = -1;
@@ -736,7 +735,7 @@ __global__ void __launch_bounds__(async_bound(kD)) k_nf_async(
 #pragma unroll
                 for (int r = 0; r < kD; r++) {
                     if (r >= nrounds) break;
-                    const int vl = ((r * 32 + (int)lane) >> kLogD) & 31;
+                    const int vl = ((r * 32 + (int)lane) / kD) & 31;
                     const int64_t cd = (int64_t)__shfl_sync(0xffffffffu, dv, vl) + (int64_t)s[r].y;
                     const bool fin = s[r].x >= 0;
                     const bool won = fin && (long long)(old[r] >> 1) > cd;
@@ -998,15 +997,16 @@ int sssp_near_far_async(sp_graph *g, Call &c, int32_t *dist, int32_t src, int64_
                           g->ell_d <= 4;
     const int hops = se && se[0] == '3' ? 3 : 2;
     if (shortcut) SP_TRY(ensure_ell2(g, c, hops));
-    // 2-hop rows: 384 threads per block (cfg5a, 256 / 384 / 512: 32.0 /
-    // 30.7 / 33.2 ms; two blocks per SM 35 ms)
-    if (!thr && shortcut && g->ell2 && g->ell2_slots == kEll2) threads = 384;
+    // 2-hop rows: 320 threads per block (cfg5a, 12-slot rows, 256 / 320 /
+    // 384 / 448: 27.4 / 26.9 / 27.5 / 28.9 ms; two blocks per SM: slower)
+    if (!thr && shortcut && g->ell2 && g->ell2_slots == kEll2) threads = 320;
     const bool use2 = shortcut && g->ell2 &&
                       threads <= (g->ell2_slots == kEll3 ? 256 : 512);  // its launch bound
-    // a shortcut row covers two hops: a phase may span twice the distance
-    // band (cfg5a, delta 816 / 1632 / 2400 / 3200: 34.3 / 31.2 / 31.4 /
-    // 32.1 ms; 1-hop rows: 39.5 ms at 816, 39.0 at 1632)
-    if (use2 && !getenv("SP_SSSP_DELTA")) delta *= g->ell2_slots == kEll3 ? 3 : 2;
+    // a shortcut row covers two hops: a phase may span a wider distance
+    // band (cfg5a, 16-slot rows, delta 816 / 1632 / 2400 / 3200: 34.3 / 31.2
+    // / 31.4 / 32.1 ms; 12-slot rows at 384 threads, 1632 / 2400: 27.4 /
+    // 26.7 ms; 1-hop rows: 39.5 ms at 816, 39.0 at 1632)
+    if (use2 && !getenv("SP_SSSP_DELTA")) delta *= 3;
     const void *kfn = use2 && g->ell2_slots == kEll3 ? (const void *)k_nf_async<kEll3>
                       : use2          ? (const void *)k_nf_async<kEll2>
                       : g->ell_d == 2 ? (const void *)k_nf_async<2>
