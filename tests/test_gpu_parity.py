@@ -237,6 +237,50 @@ def test_sssp_async_near_far_stress(kind, p0, p1, und, delta, monkeypatch):
     np.testing.assert_array_equal(r.env.node_props["dist"], cpu_ref.sssp(o, 0)[0])
 
 
+@pytest.mark.parametrize("directed", [True, False])
+def test_sssp_shortcut_rows_random_low_degree(directed, monkeypatch):
+    """The asynchronous kernel's 2-hop shortcut rows on a random graph of
+    out-degree <= 4 (rows with more than 12 distinct 1-2-hop targets keep
+    the 1-hop ones and the first 2-hop ones), with self-loops, parallel
+    edges and zero weights: the oracle's dist bit for bit, also against the
+    1-hop rows (SP_NF_SHORTCUT=0)."""
+    rng = np.random.default_rng(41)
+    n = 20000
+    deg = rng.integers(0, 5, n)
+    u = np.repeat(np.arange(n), deg)
+    v = rng.integers(0, n, len(u))
+    loops = rng.random(len(u)) < 0.01
+    v[loops] = u[loops]
+    w = rng.integers(0, 60, len(u))
+    dup = rng.random(len(u)) < 0.02
+    u = np.concatenate([u, u[dup]])
+    v = np.concatenate([v, v[dup]])
+    w = np.concatenate([w, w[dup] + 3])
+    # every row <= 4 slots (undirected: both mirrors count; a self-loop once, F9)
+    cnt = np.zeros(n, dtype=np.int64)
+    keep = np.zeros(len(u), dtype=bool)
+    for i in range(len(u)):
+        a, b = int(u[i]), int(v[i])
+        if cnt[a] + 1 <= 4 and (directed or a == b or cnt[b] + 1 <= 4):
+            keep[i] = True
+            cnt[a] += 1
+            if not directed and a != b:
+                cnt[b] += 1
+    u, v, w = u[keep], v[keep], w[keep]
+    g = sp.from_arrays(u, v, w, directed=directed, n=n)
+    assert np.diff(np.asarray(g.offsets)).max() <= 4  # the shortcut-row form applies
+    o = cpu_ref.build_csr(u, v, w, directed, n)
+    for s in (0, n // 2, int(np.argmax(np.bincount(u, minlength=n)))):
+        dist, _, rc = cpu_ref.sssp(o, s)
+        assert rc == 0
+        for form in ("2", "0"):
+            monkeypatch.setenv("SP_NF_SHORTCUT", form)
+            for rep in range(2):
+                r = sp.run(corpus.SSSP, g, {"src": s})
+                np.testing.assert_array_equal(r.env.node_props["dist"], dist,
+                                              err_msg=f"form {form} rep {rep}")
+
+
 @pytest.mark.parametrize("pull_div", ["8", "1"])
 def test_sssp_pull_hot_snapshot(pull_div, monkeypatch):
     """Direction-optimising SSSP whose pull sweeps read the hottest sources'
