@@ -674,11 +674,11 @@ __global__ void __launch_bounds__(async_bound(kD)) k_nf_async(
             int32_t v = (int)lane < k ? sv : -1;
             if (v >= 0) myring[h + lane] = -1;  // the slot is reused next phase
             if constexpr (kD >= kEll2) {
-                // 2-hop rows (shortcuts): up to 16 rounds of 32 slots, so the
-                // rounds' atomicMins are all issued before any push, and the
-                // near winners of every round are pushed together from a
-                // per-warp shared list -- one tail round trip per batch
-                // instead of one per round
+                // shortcut rows (kD slots each): a batch of k rows is up to
+                // kD rounds of 32 slots, so the rounds' atomicMins are all
+                // issued before any push, and the near winners of every
+                // round are pushed together from a per-warp shared list --
+                // one tail round trip per batch instead of one per round
                 __shared__ int32_t s_near[async_bound(kD) / 32][kNearList];
                 int32_t *nl = s_near[threadIdx.x >> 5];
                 const int nslot = k * kD;
