@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kExpandBlock) k_nf_persistent(
 // ---- asynchronous near-far (thin graphs, non-negative weights) ----------
 // One cooperative launch; no grid-wide barrier per hop.  Improvements below
 // the threshold T go to ring queues, the rest to a far pile.  Every block
-// owns one ring -- vertex x belongs to ring (x / 64) mod #blocks -- whose
+// owns one ring -- vertex x belongs to ring (x / 16) mod #blocks -- whose
 // head is a shared-memory counter of the block; its warps pop up to 32
 // consecutive published entries at a time, expand them and push their near
 // improvements to the owners' rings (one tail atomic per group of lanes
@@ -538,9 +538,12 @@ constexpr int kAsyncThreads = 256;
 constexpr unsigned kAsyncBackoff = 256;
 constexpr int kTailStride = 16;    // one 128-byte line per ring tail
 #ifndef SP_NF_OWN_SHIFT
-#define SP_NF_OWN_SHIFT 6
+#define SP_NF_OWN_SHIFT 4
 #endif
-constexpr int kOwnShift = SP_NF_OWN_SHIFT;  // 2^6 consecutive vertices per ring chunk (cfg5a: 4 / 6 / 8 / 10 / 12 -> 39.5 / 39.6 / 42.0 / 46.0 / 39.8 ms)
+// 2^4 consecutive vertices per ring chunk: cfg5a, 1-hop rows, shift 4 / 6 /
+// 8 / 10 / 12 -> 39.5 / 39.6 / 42.0 / 46.0 / 39.8 ms; 2-hop shortcut rows,
+// 3 / 4 / 5 / 6 / 7 / 8 -> 25.5 / 25.5 / 25.6 / 26.2 / 27.1 / 28.2 ms
+constexpr int kOwnShift = SP_NF_OWN_SHIFT;
 constexpr int kEllMaxDeg = 8;      // ELL rows for graphs with max out-degree <= 8
 constexpr long long kAsyncWatchdog = 1ll << 35;  // cycles (~17 s): a hang becomes a fallback
 
