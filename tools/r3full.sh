@@ -1,6 +1,6 @@
 #!/bin/bash
 # Full round-2 pass: GPU tests, smoke, default bench, per-line ncu traffic, launch list.
-OUT=gpurun_out/r3full8; mkdir -p $OUT
+OUT=gpurun_out/r3full9; mkdir -p $OUT
 nvidia-smi > $OUT/nvsmi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { tail -30 $OUT/build.log; exit 1; }
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
@@ -14,4 +14,4 @@ print("value",d["value"],"ms",d["ms_per_step"],"frac",d["roofline"]["frac"],"mea
 for k,v in d.get("algorithms",{}).items(): print(k, round(v["ms"],3), v.get("gteps"), v.get("roofline",{}).get("frac"), {kk:vv for kk,vv in v.items() if kk.startswith(("first","upper"))})
 PY
 tail -3 $OUT/bench.err
-bash tools/ncu_lines.sh r3lines8 > $OUT/ncu_lines.log 2>&1; cat $OUT/ncu_lines.log | tail -12
+bash tools/ncu_lines.sh r3lines9 > $OUT/ncu_lines.log 2>&1; cat $OUT/ncu_lines.log | tail -12
