@@ -71,7 +71,10 @@ constexpr int kFwdWarpWords = kT + kT / 2 + 2 * kA + 1 + 128;
 constexpr int kFilterWords = 128;  // 4096-bit filter per warp
 constexpr int kFilterShift = 20;   // 32 - log2(4096)
 constexpr int kBatch = 32;
-constexpr int kUnroll = 2;         // 16-byte loads in flight per lane in k_tc_fwd_plain
+#ifndef SP_TC_PLAIN_UNROLL
+#define SP_TC_PLAIN_UNROLL 2
+#endif
+constexpr int kUnroll = SP_TC_PLAIN_UNROLL;  // 16-byte loads in flight per lane in k_tc_fwd_plain (cfg3: 1 / 2 / 3 / 4 -> 9.00 / 8.56 / 9.35 / 9.69 ms)
 constexpr int kUnrollHash = 4;     // ... in k_tc_fwd_hash (skewed graphs; 2 is faster on cfg3)
 #ifndef SP_TC_PAD
 #define SP_TC_PAD 8
