@@ -139,6 +139,7 @@ int sp_graph_weight_range(const sp_graph *g, int32_t *wmin, int32_t *wmax);
 #define SP_PREP_PR_HOT   3 /* PR hot-source encoding of radj                */
 #define SP_PREP_PR_REL   4 /* PR relabelled (out-degree rank) layout        */
 #define SP_PREP_ELL      5 /* ELL rows of bounded-degree graphs (async SSSP) */
+#define SP_PREP_ELL2     6 /* 2-hop shortcut rows (async SSSP, out-degree <= 4) */
 int sp_graph_prep_ms(const sp_graph *g, int kind, double *ms);
 void sp_graph_destroy(sp_graph *g);
 

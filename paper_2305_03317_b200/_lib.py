@@ -36,7 +36,7 @@ SP_ARR_OFFSETS, SP_ARR_ADJ, SP_ARR_WEIGHTS, SP_ARR_REV_OFFSETS, \
     SP_ARR_REV_ADJ, SP_ARR_REV_EID, SP_ARR_WEFF = range(7)
 SP_GEN_RMAT, SP_GEN_UNIFORM, SP_GEN_GRID = range(3)
 SP_REDUCE_SUM_I64, SP_REDUCE_MIN_F64, SP_REDUCE_MAX_F64 = range(3)
-PREP_KINDS = ("tc_upper", "weff", "rweff", "pr_hot", "pr_rel", "ell")  # SP_PREP_* order
+PREP_KINDS = ("tc_upper", "weff", "rweff", "pr_hot", "pr_rel", "ell", "ell2")  # SP_PREP_* order
 
 
 class Stats(C.Structure):

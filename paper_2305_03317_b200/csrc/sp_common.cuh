@@ -235,7 +235,7 @@ int ensure_weff(sp_graph *g, Call &c);
 // reports (SP_PREP_* in starplat_b200.h).
 enum PrepKind {
     kPrepTcUpper = 0, kPrepWeff = 1, kPrepRweff = 2, kPrepPrHot = 3, kPrepPrRel = 4,
-    kPrepEll = 5, kPrepKinds = 6
+    kPrepEll = 5, kPrepEll2 = 6, kPrepKinds = 7
 };
 // Records the start (end = 0) or the end (end = 1) of one build on stream s.
 void prep_mark(sp_graph *g, int kind, int end, cudaStream_t s);

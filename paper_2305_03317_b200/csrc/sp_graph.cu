@@ -927,12 +927,12 @@ int ensure_ell2(sp_graph *g, Call &c, int hops) {
         cudaGetLastError();
         return SP_OK;
     }
-    prep_mark(g, kPrepEll, 0, c.stream);
+    prep_mark(g, kPrepEll2, 0, c.stream);
     if (S == kEll3)
         k_ell2_fill<kEll3><<<gridN(g->n, c.device), 256, 0, c.stream>>>(g->ell, g->ell_d, g->n, 3, e2);
     else
         k_ell2_fill<kEll2><<<gridN(g->n, c.device), 256, 0, c.stream>>>(g->ell, g->ell_d, g->n, 2, e2);
-    prep_mark(g, kPrepEll, 1, c.stream);
+    prep_mark(g, kPrepEll2, 1, c.stream);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
     if (e != cudaSuccess) {

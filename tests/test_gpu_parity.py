@@ -955,6 +955,10 @@ def test_preprocessing_times_reported():
     d, _ = _pair("rmat", 12, 16, 5, False)
     sp.run(corpus.SSSP_PULL, d, {"src": 0})
     assert d.preprocessing_ms().get("rweff", 0) > 0
+    gr, _ = _pair("grid", 64, 64, 5, True)  # thin: ELL rows, then 2-hop shortcut rows
+    sp.run(corpus.SSSP, gr, {"src": 0})
+    pre = gr.preprocessing_ms()
+    assert pre.get("ell", 0) > 0 and pre.get("ell2", 0) > 0
 
 
 def test_pagerank_cluster_hot_set_subprocess():
